@@ -1,0 +1,122 @@
+"""TEST INFRASTRUCTURE ONLY -- the CPU oracle for the fast Basic-SSA hot path.
+
+Plain, slow, obviously-correct definitions (explicit Hankel entries, one-sided Jacobi
+SVD, direct diagonal averaging) in ``ssa_oracle.c`` (fp64, -ffp-contract=off), loaded
+through ctypes.  Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s
+``cpu_baseline`` / ``--impl reference`` legs may import this package; the product
+package ``paper_0911_4498_b200`` never does, and the two share no code.
+
+Each wrapper names the PAPER.md passage it follows; see the C file header.
+Parity status: all functions pinned by tests/test_oracle.py (no "parity unpinned").
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "ssa_oracle.c")
+_LIB_PATH = os.path.join(_HERE, "liboracle.so")
+_lib = None
+_lock = threading.Lock()
+
+_dp = ctypes.POINTER(ctypes.c_double)
+
+
+def build(force: bool = False) -> str:
+    """Compile ssa_oracle.c with gcc (-O2, no FMA contraction) into oracle/liboracle.so."""
+    if force or not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(_SRC):
+        tmp = _LIB_PATH + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
+                               "-std=c99", "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB_PATH)
+    return _LIB_PATH
+
+
+def _load():
+    global _lib
+    with _lock:
+        if _lib is None:
+            build()
+            lib = ctypes.CDLL(_LIB_PATH)
+            i64 = ctypes.c_int64
+            lib.oracle_trajectory.argtypes = [_dp, i64, i64, _dp]
+            lib.oracle_matvec.argtypes = [_dp, i64, i64, _dp, _dp, ctypes.c_int]
+            lib.oracle_diag_average.argtypes = [_dp, i64, i64, _dp]
+            lib.oracle_hankelize_rank1.argtypes = [ctypes.c_double, _dp, i64, _dp, i64, _dp]
+            lib.oracle_svd_jacobi.argtypes = [_dp, i64, i64, i64, _dp, _dp, _dp]
+            lib.oracle_svd_jacobi.restype = ctypes.c_int
+            _lib = lib
+    return _lib
+
+
+def _c(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _p(a: np.ndarray):
+    return a.ctypes.data_as(_dp)
+
+
+def trajectory(f, L: int) -> np.ndarray:
+    """Explicit L x K trajectory matrix, x_ij = f_{i+j-1} (sec 2.1)."""
+    f = _c(f)
+    N = f.shape[0]
+    K = N - L + 1
+    X = np.empty((L, K))
+    _load().oracle_trajectory(_p(f), N, L, _p(X))
+    return X
+
+
+def matvec(f, L: int, x, transpose: bool = False) -> np.ndarray:
+    """y = X x (x len K) or X^T x (x len L) over the explicit entries (Algs. 2-3 compute this)."""
+    f = _c(f); x = _c(x)
+    N = f.shape[0]
+    K = N - L + 1
+    y = np.empty(K if transpose else L)
+    assert x.shape[0] == (L if transpose else K)
+    _load().oracle_matvec(_p(f), N, L, _p(x), _p(y), 1 if transpose else 0)
+    return y
+
+
+def diag_average(Y) -> np.ndarray:
+    """Diagonal averaging of an L x K matrix (sec 2.4)."""
+    Y = _c(Y)
+    L, K = Y.shape
+    g = np.empty(L + K - 1)
+    _load().oracle_diag_average(_p(Y), L, K, _p(g))
+    return g
+
+
+def hankelize_rank1(sigma: float, u, v) -> np.ndarray:
+    """Diagonal averaging of sigma u v^T, entries formed on the fly (Eq. hankelization1)."""
+    u = _c(u); v = _c(v)
+    g = np.empty(u.shape[0] + v.shape[0] - 1)
+    _load().oracle_hankelize_rank1(float(sigma), _p(u), u.shape[0], _p(v), v.shape[0], _p(g))
+    return g
+
+
+def svd(f, L: int, nsv: int | None = None):
+    """Leading nsv singular triples of the trajectory matrix by one-sided Jacobi
+    (sec 2.2, with X = U Sigma V^T, R3).
+    Returns (sigma[nsv], U[nsv][L], V[nsv][K], sweeps)."""
+    f = _c(f)
+    N = f.shape[0]
+    K = N - L + 1
+    n = min(L, K)
+    nsv = n if nsv is None else min(nsv, n)
+    s = np.empty(nsv); U = np.empty((nsv, L)); V = np.empty((nsv, K))
+    sweeps = _load().oracle_svd_jacobi(_p(f), N, L, nsv, _p(s), _p(U), _p(V))
+    return s, U, V, sweeps
+
+
+def reconstruct(f, L: int, nsv: int | None = None):
+    """Oracle decompose + reconstruct: triples by Jacobi, then each elementary series by
+    direct averaging.  Returns (sigma, U, V, G[nsv][N])."""
+    s, U, V, _ = svd(f, L, nsv)
+    G = np.stack([hankelize_rank1(s[i], U[i], V[i]) for i in range(s.shape[0])]) if s.shape[0] else np.zeros((0, len(f)))
+    return s, U, V, G
