@@ -1,0 +1,166 @@
+/*
+ * ssa.h -- C-ABI of libssa.so, the B200 (sm_100a) hot path of fast Basic SSA
+ * (Korobeynikov, "Computation- and Space-Efficient Implementation of SSA",
+ * arXiv:0911.4498).  Citations are PAPER.md line ranges with section / algorithm.
+ *
+ * Problem statement (sec 2): a real series F = (f_1..f_N), N > 2, window
+ * 1 < L < N, K = N - L + 1, trajectory matrix X (L x K, x_ij = f_{i+j-1},
+ * PAPER.md:84-94 sec 2.1).  The library computes the k leading singular triples
+ * (sigma_i, u_i, v_i) of X (sec 2.2, X = U Sigma V^T -- see DESIGN.md
+ * reading R3) without ever forming X, and the elementary reconstructed series
+ * g_i = diagonal averaging of sigma_i u_i v_i^T (sec 2.4, 747-828 sec 5).
+ *
+ * Conventions shared by every entry point:
+ *  - All numbers are IEEE binary64 (double).  Arrays are dense, C row-major, with
+ *    the shapes written next to each argument; no padding in caller buffers.
+ *  - Pointers named d_* are DEVICE pointers on the plan's device (e.g. torch CUDA
+ *    tensors' data_ptr()), h_* are HOST pointers (pageable or pinned).  The caller
+ *    owns every buffer passed in; inputs are read-only.  Device buffers must be
+ *    8-byte aligned (16-byte for d_spec).
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).  Every
+ *    device-pointer call is asynchronous with respect to the host: it only enqueues
+ *    kernels on `stream`.  Argument validation happens synchronously before anything
+ *    is enqueued.
+ *  - Errors are status codes; no exception crosses the ABI.  ssa_last_error() returns
+ *    a thread-local human-readable detail for the last non-OK status.
+ *  - A plan owns all its device workspace (spectra, Krylov bases, bidiagonal factors,
+ *    scratch), allocated once in ssa_plan_create, so out-of-memory is reported there.
+ *    Plans are not thread-safe; use one plan per concurrent stream.
+ */
+#ifndef SSA_H_
+#define SSA_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct ssa_plan_s* ssa_plan_t;
+
+typedef enum {
+  SSA_OK = 0,
+  SSA_ERR_INVALID_ARGUMENT = 1, /* bad sizes / null pointers; non-finite series (d_info) */
+  SSA_ERR_NOT_CONVERGED = 2,    /* some series did not meet tol within max_steps       */
+  SSA_ERR_OUT_OF_MEMORY = 3,    /* workspace allocation failed in ssa_plan_create       */
+  SSA_ERR_CUDA = 4,             /* a CUDA runtime call failed (detail in ssa_last_error)*/
+  SSA_ERR_INTERNAL = 5,
+  SSA_ERR_UNSUPPORTED = 6       /* valid request this build cannot run (e.g. FFT size) */
+} ssa_status;
+
+/* Options of the truncated SVD (sec 3.1-3.2).  Fill with ssa_options_default first. */
+typedef struct {
+  double tol;            /* stop when every one of the k leading Ritz triples has residual
+                            alpha_{m+1} |P_{m+1,i}| <= tol * omega_1 (R7; the paper
+                            gives no criterion).  Default 1e-12.        */
+  int32_t max_steps;     /* m_max, Lanczos steps cap; default max(256, 8k) clipped to
+                            min(L, K).  Fixes the Krylov basis workspace size.             */
+  int32_t check_every;   /* run the convergence test every c steps once m >= k; default 4 */
+  uint64_t seed;         /* start vector p_0 (Alg. 1 line 1): uniform(-1,1)
+                            entries from a counter-based hash of (seed, series, i); dflt 42 */
+  int32_t reorth;        /* 1 = full reorthogonalization (sec 3.2.2) by
+                            classical Gram-Schmidt with a DGKS second pass when the norm
+                            drops below 1/sqrt(2) (default); 2 = always two passes.       */
+  int32_t reserved;
+} ssa_options;
+
+/* Per-series outcome of ssa_decompose (device array, one entry per series). */
+typedef struct {
+  int32_t steps;          /* m: Lanczos steps in B_m                                       */
+  int32_t converged;      /* 1 if all k residuals met tol                                  */
+  int32_t breakdown_step; /* first step with alpha or beta < 1e-12 * running max, else 0   */
+  int32_t reorth_extra;   /* number of DGKS second passes taken                            */
+  int32_t status;         /* ssa_status for this series (INVALID_ARGUMENT if non-finite)   */
+  int32_t reserved;
+  double max_residual;    /* max_i alpha_{m+1}|P_{m+1,i}| / omega_1 over the k triples     */
+  double sigma1;          /* omega_1                                                       */
+} ssa_series_info;
+
+/* Fill *opt with the defaults above (max_steps = 0 means "derive from k, L, K"). */
+ssa_status ssa_options_default(ssa_options* opt);
+
+/* Create a plan for `batch` independent series of length N with window L and k triples.
+ * Validation: N >= 3; 2 <= L <= N-1; 1 <= k <= min(L, K);
+ * batch >= 1.  k = 0 is accepted for plans used only for ssa_spectrum / ssa_matvec /
+ * ssa_hankelize.  The FFT size M is the smallest power of two >= N (R5).
+ * `device` is the CUDA ordinal.  opt may be NULL (defaults).  On success *out owns
+ * device workspace sized for ssa_decompose (about 8 B * batch_in_flight * (m_max+1) *
+ * (L+K) for the Krylov bases plus spectra). */
+ssa_status ssa_plan_create(int64_t N, int64_t L, int32_t k, int64_t batch,
+                           const ssa_options* opt, int device, ssa_plan_t* out);
+void ssa_plan_destroy(ssa_plan_t plan);
+
+int64_t ssa_plan_fft_size(ssa_plan_t plan);     /* M, or -1 for a NULL plan */
+int32_t ssa_plan_max_steps(ssa_plan_t plan);    /* resolved m_max            */
+
+/* Spectrum of each series (Alg. 2 lines 1-2, computed once and reused,
+ * PAPER.md:699-702): d_spec[b][q] = sum_{n<N} f_{n+1} exp(-2 pi i q n / M), q = 0..M/2,
+ * stored as interleaved (re, im) pairs.  This is the paper's c-hat up to the phase
+ * exp(-2 pi i q L / M) (R1/R5; the correlation form needs no rotation).
+ *   d_series: [batch][N]     d_spec: [batch][M/2+1][2] */
+ssa_status ssa_spectrum(ssa_plan_t plan, const double* d_series, double* d_spec, void* stream);
+
+/* Hankel matrix-vector products through the stored spectra (Alg. 2 / Alg. 3,
+ * PAPER.md:680-729 sec 4.3; Alg. 3 output slice read as p'_L..p'_N, R1):
+ *   transpose = 0 : d_y[b] = X_b d_x[b]     d_x: [batch][K]   d_y: [batch][L]
+ *   transpose = 1 : d_y[b] = X_b^T d_x[b]   d_x: [batch][L]   d_y: [batch][K]
+ * computed as y = irfft(spec * conj(rfft(x, M)))[0 : len(y)]; X is never formed. */
+ssa_status ssa_matvec(ssa_plan_t plan, const double* d_spec, const double* d_x, double* d_y,
+                      int transpose, void* stream);
+
+/* Rank-1 Hankelization (diagonal averaging of sigma u v^T) of nterms terms per series via
+ * linear convolution (sec 5, Eqs. hankelization1/conv, Alg. 4 with the
+ * weights read as division by the antidiagonal counts c_t = min(t, L, K, N-t+1),
+ * DESIGN.md R2):
+ *   d_out[b][i][t-1] = sigma[b][i] * (u' * v')_t / c_t,  t = 1..N
+ *   d_sigma: [batch][nterms]  d_U: [batch][nterms][L]  d_V: [batch][nterms][K]
+ *   d_out: [batch][nterms][N] */
+ssa_status ssa_hankelize(ssa_plan_t plan, const double* d_sigma, const double* d_U, const double* d_V,
+                         int32_t nterms, double* d_out, void* stream);
+
+/* Truncated SVD of each trajectory matrix by Golub-Kahan-Lanczos bidiagonalization
+ * (Alg. 1, sec 3.1) with full reorthogonalization,
+ * every product by the FFT correlation above, then the SVD of the (m+1) x m lower
+ * bidiagonal B_m on device and Ritz assembly U_k = U_{m+1} P_k,
+ * V_k = V_m Q_k (Eq. 1):
+ *   d_series: [batch][N]   d_sigma: [batch][k] (descending)   d_U: [batch][k][L]
+ *   d_V: [batch][k][K]     d_info: [batch] or NULL
+ * Each u_i is sign-canonicalized (largest-|.| entry positive, lowest index on ties; v_i
+ * flipped with it).  Per-series failures (non-finite input -> INVALID_ARGUMENT, not
+ * converged -> NOT_CONVERGED with the best triples written) are reported in d_info after
+ * the stream synchronizes; the return value covers validation and launch only. */
+ssa_status ssa_decompose(ssa_plan_t plan, const double* d_series, double* d_sigma, double* d_U,
+                         double* d_V, ssa_series_info* d_info, void* stream);
+
+/* Elementary reconstructed series of the k triples (grouping with
+ * I_j = {j} combined with averaging; equals ssa_hankelize with nterms = k).
+ *   d_out: [batch][k][N] */
+ssa_status ssa_reconstruct(ssa_plan_t plan, const double* d_sigma, const double* d_U, const double* d_V,
+                           double* d_out, void* stream);
+
+/* End-to-end call on HOST buffers: copies h_series to the device, runs ssa_decompose and
+ * ssa_reconstruct on plan-owned device buffers, copies sigma, U, V, the reconstructions
+ * and info back, and synchronizes `stream`.  Any output pointer may be NULL to skip its
+ * copy.  Returns NOT_CONVERGED / INVALID_ARGUMENT if any series reported it.
+ *   h_series: [batch][N]  h_sigma: [batch][k]  h_U: [batch][k][L]  h_V: [batch][k][K]
+ *   h_recon: [batch][k][N]  h_info: [batch] */
+ssa_status ssa_run_host(ssa_plan_t plan, const double* h_series, double* h_sigma, double* h_U,
+                        double* h_V, double* h_recon, ssa_series_info* h_info, void* stream);
+
+const char* ssa_status_string(ssa_status s);
+const char* ssa_last_error(void);
+
+/* Number of kernels the library enqueued since the plan was created (for bench.py's
+ * gpu_launches claim). */
+int64_t ssa_plan_launch_count(ssa_plan_t plan);
+
+/* Device time (ms, CUDA events recorded on the launching stream around each kernel) of
+ * the most recent spectrum, Lanczos (decompose minus spectrum) and hankelization launches
+ * of this plan: out_ms[0] = spectrum, out_ms[1] = lanczos, out_ms[2] = hankelize.  Blocks
+ * until those events completed; entries never launched are reported as -1. */
+ssa_status ssa_plan_phase_ms(ssa_plan_t plan, double out_ms[3]);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SSA_H_ */

@@ -1,0 +1,217 @@
+// fft_smem.cuh -- fp64 FFT building blocks held entirely in shared memory (sm_100a).
+//
+// One CTA transforms one complex vector of H = M/2 points (H a power of two, H <= 8192)
+// in place:
+//   * forward: in-place decimation-in-frequency passes (radix 8, final radix 4/2),
+//     natural order in -> mixed-radix digit-reversed order out;
+//   * inverse: the exact inverse passes in reverse order with conjugate twiddles,
+//     digit-reversed in -> natural order out, unnormalized (result x H).
+// So forward -> pointwise work in digit-reversed positions -> inverse needs no
+// permutation pass.  Real transforms of length M are packed into H complex points
+// (z_n = x_2n + i x_2n+1) with the usual split post-/pre-processing (see
+// ssa_kernels.cu).  This is the DFT of PAPER.md:473-509 (sec 4.1: unnormalized forward,
+// 1/N inverse), evaluated as an FFT.
+//
+// Shared-memory layout: element i lives at slot i + (i >> 3) (one pad slot per 8) so
+// that stride-8 radix-8 butterflies of the last pass hit distinct banks.
+// Twiddles come from a global table T[t] = exp(-2 pi i t / M), t in [0, H), computed on
+// the host in extended precision (ssa_api.cu); exp(-2 pi i t / M) for t in [H, M) is
+// -T[t - H].
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace ssa {
+
+__device__ __forceinline__ int fpad(int i) { return i + (i >> 3); }
+__host__ __device__ __forceinline__ int fpad_size(int H) { return H + (H >> 3) + 1; }
+
+struct cplx { double x, y; };
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ double2 cmulc(double2 a, double2 b) {  // a * conj(b)
+  return make_double2(fma(a.x, b.x, a.y * b.y), fma(a.y, b.x, -a.x * b.y));
+}
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 conjg(double2 a) { return make_double2(a.x, -a.y); }
+
+// exp(-2 pi i t / M) for t in [0, M) from the half table (t < H direct, else negated).
+__device__ __forceinline__ double2 twiddle(const double2* __restrict__ T, int t, int H) {
+  if (t < H) return __ldg(T + t);
+  double2 w = __ldg(T + (t - H));
+  return make_double2(-w.x, -w.y);
+}
+
+// Radix sequence: passes of radix 8 while >= 8 remain, then one of radix 4 or 2.
+struct FftShape {
+  int H;        // points
+  int npass;
+  int radix[6];
+};
+
+__host__ __device__ inline FftShape make_shape(int H) {
+  FftShape s;
+  s.H = H;
+  s.npass = 0;
+  int rem = H;
+  while (rem >= 8) { s.radix[s.npass++] = 8; rem >>= 3; }
+  if (rem > 1) s.radix[s.npass++] = rem;  // 2 or 4
+  return s;
+}
+
+// Digit-reversed position of frequency k (forward output order).
+__device__ __forceinline__ int rev_index(const FftShape& s, int k) {
+  int pos = 0, size = s.H;
+  for (int p = 0; p < s.npass; ++p) {
+    int r = s.radix[p];
+    size /= r;
+    pos += (k % r) * size;
+    k /= r;
+  }
+  return pos;
+}
+
+// ---- small DFT kernels (forward sign exp(-2 pi i / R)); INV selects exp(+...) ----
+template <bool INV>
+__device__ __forceinline__ void dft2(double2& a, double2& b) {
+  double2 t = a;
+  a = cadd(t, b);
+  b = csub(t, b);
+}
+
+template <bool INV>
+__device__ __forceinline__ double2 mul_mi(double2 a) {  // multiply by -i (forward) or +i (inverse)
+  return INV ? make_double2(-a.y, a.x) : make_double2(a.y, -a.x);
+}
+
+template <bool INV>
+__device__ __forceinline__ void dft4(double2& a0, double2& a1, double2& a2, double2& a3) {
+  double2 s0 = cadd(a0, a2), d0 = csub(a0, a2);
+  double2 s1 = cadd(a1, a3), d1 = mul_mi<INV>(csub(a1, a3));
+  a0 = cadd(s0, s1);
+  a2 = csub(s0, s1);
+  a1 = cadd(d0, d1);
+  a3 = csub(d0, d1);
+}
+
+template <bool INV>
+__device__ __forceinline__ void dft8(double2* a) {
+  const double r = 0.70710678118654752440084436210485;  // 1/sqrt(2)
+  // split into even / odd DFT4s
+  double2 e0 = a[0], e1 = a[2], e2 = a[4], e3 = a[6];
+  double2 o0 = a[1], o1 = a[3], o2 = a[5], o3 = a[7];
+  dft4<INV>(e0, e1, e2, e3);
+  dft4<INV>(o0, o1, o2, o3);
+  // twiddle odds by W8^k, W8 = exp(-+ 2 pi i / 8)
+  double2 t1, t2, t3;
+  if (!INV) {
+    t1 = make_double2(r * (o1.x + o1.y), r * (o1.y - o1.x));    // * (1 - i)/sqrt2
+    t2 = make_double2(o2.y, -o2.x);                               // * -i
+    t3 = make_double2(r * (o3.y - o3.x), -r * (o3.x + o3.y));   // * (-1 - i)/sqrt2
+  } else {
+    t1 = make_double2(r * (o1.x - o1.y), r * (o1.y + o1.x));    // * (1 + i)/sqrt2
+    t2 = make_double2(-o2.y, o2.x);                               // * i
+    t3 = make_double2(-r * (o3.x + o3.y), r * (o3.x - o3.y));   // * (-1 + i)/sqrt2
+  }
+  a[0] = cadd(e0, o0); a[4] = csub(e0, o0);
+  a[1] = cadd(e1, t1); a[5] = csub(e1, t1);
+  a[2] = cadd(e2, t2); a[6] = csub(e2, t2);
+  a[3] = cadd(e3, t3); a[7] = csub(e3, t3);
+}
+
+template <int R, bool INV>
+__device__ __forceinline__ void dftR(double2* a) {
+  if constexpr (R == 8) dft8<INV>(a);
+  else if constexpr (R == 4) dft4<INV>(a[0], a[1], a[2], a[3]);
+  else dft2<INV>(a[0], a[1]);
+}
+
+// One forward DIF pass: block size S, radix R, Q = S / R.  Butterfly (b, n1):
+//   y[n1 + Q k2] = W_S^{n1 k2} * sum_{n2} x[n1 + Q n2] W_R^{n2 k2}
+template <int R>
+__device__ __forceinline__ void dif_pass(double2* buf, int H, int S, const double2* __restrict__ T,
+                                         int tid, int nthr) {
+  const int Q = S / R;
+  const int M = 2 * H;
+  const int tstep = M / S;  // exp(-2 pi i n1 k2 / S) = T[n1 k2 M / S]
+  for (int bf = tid; bf < H / R; bf += nthr) {
+    int b = bf / Q, n1 = bf - b * Q;
+    int base = b * S + n1;
+    double2 a[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) a[q] = buf[fpad(base + q * Q)];
+    dftR<R, false>(a);
+    if (Q > 1) {
+#pragma unroll
+      for (int q = 1; q < R; ++q) a[q] = cmul(a[q], twiddle(T, n1 * q * tstep, H));
+    }
+#pragma unroll
+    for (int q = 0; q < R; ++q) buf[fpad(base + q * Q)] = a[q];
+  }
+}
+
+// Inverse of dif_pass (times R): x[n1 + Q n2] = sum_{k2} W_R^{-n2 k2} W_S^{-n1 k2} y[n1 + Q k2]
+template <int R>
+__device__ __forceinline__ void dit_inv_pass(double2* buf, int H, int S, const double2* __restrict__ T,
+                                             int tid, int nthr) {
+  const int Q = S / R;
+  const int M = 2 * H;
+  const int tstep = M / S;
+  for (int bf = tid; bf < H / R; bf += nthr) {
+    int b = bf / Q, n1 = bf - b * Q;
+    int base = b * S + n1;
+    double2 a[R];
+#pragma unroll
+    for (int q = 0; q < R; ++q) a[q] = buf[fpad(base + q * Q)];
+    if (Q > 1) {
+#pragma unroll
+      for (int q = 1; q < R; ++q) a[q] = cmulc(a[q], twiddle(T, n1 * q * tstep, H));
+    }
+    dftR<R, true>(a);
+#pragma unroll
+    for (int q = 0; q < R; ++q) buf[fpad(base + q * Q)] = a[q];
+  }
+}
+
+// Barrier abstraction: all participating threads call sync().
+struct CtaSync {
+  __device__ __forceinline__ void operator()() const { __syncthreads(); }
+};
+
+// Forward FFT of H points in place (natural -> digit-reversed).  Caller must have
+// synchronized after writing buf; returns after a final barrier.
+template <class Sync>
+__device__ void fft_forward(double2* buf, const FftShape& s, const double2* __restrict__ T,
+                            int tid, int nthr, Sync sync) {
+  int S = s.H;
+  for (int p = 0; p < s.npass; ++p) {
+    int r = s.radix[p];
+    if (r == 8) dif_pass<8>(buf, s.H, S, T, tid, nthr);
+    else if (r == 4) dif_pass<4>(buf, s.H, S, T, tid, nthr);
+    else dif_pass<2>(buf, s.H, S, T, tid, nthr);
+    S /= r;
+    sync();
+  }
+}
+
+// Inverse (unnormalized, x H) FFT in place (digit-reversed -> natural).
+template <class Sync>
+__device__ void fft_inverse(double2* buf, const FftShape& s, const double2* __restrict__ T,
+                            int tid, int nthr, Sync sync) {
+  // block sizes seen by the forward passes were H, H/r0, H/(r0 r1), ...; undo last first
+  int sizes[6];
+  int S = s.H;
+  for (int p = 0; p < s.npass; ++p) { sizes[p] = S; S /= s.radix[p]; }
+  for (int p = s.npass - 1; p >= 0; --p) {
+    int r = s.radix[p];
+    if (r == 8) dit_inv_pass<8>(buf, s.H, sizes[p], T, tid, nthr);
+    else if (r == 4) dit_inv_pass<4>(buf, s.H, sizes[p], T, tid, nthr);
+    else dit_inv_pass<2>(buf, s.H, sizes[p], T, tid, nthr);
+    sync();
+  }
+}
+
+}  // namespace ssa

@@ -1,0 +1,354 @@
+// ssa_api.cu -- the extern "C" boundary of libssa.so (include/ssa.h).
+// Host-side validation, workspace sizing, twiddle tables and kernel enqueueing only;
+// every arithmetic step of the method runs in the kernels of ssa_kernels.cu.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "ssa_internal.h"
+
+using ssa::Plan;
+
+static thread_local char g_err[512] = "";
+
+static ssa_status fail(ssa_status s, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return s;
+}
+
+static ssa_status cuda_fail(cudaError_t e, const char* what) {
+  cudaGetLastError();  // clear sticky-free errors
+  return fail(SSA_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+}
+
+#define CK(call, what)                               \
+  do {                                               \
+    cudaError_t e_ = (call);                         \
+    if (e_ != cudaSuccess) return cuda_fail(e_, what); \
+  } while (0)
+
+struct ssa_plan_s {
+  Plan p;
+};
+
+static int round_up(int x, int m) { return (x + m - 1) / m * m; }
+// Golub-Kahan QR on an m x m bidiagonal takes ~2 sweeps per value (<= 2 m^2 rotations per
+// side); 6 (m+2)^2 leaves ample room.  Overflow is reported as SSA_ERR_INTERNAL per series.
+static int rot_cap(int m_max) { return 6 * (m_max + 2) * (m_max + 2) + 1024; }
+
+extern "C" ssa_status ssa_options_default(ssa_options* opt) {
+  if (!opt) return fail(SSA_ERR_INVALID_ARGUMENT, "opt is NULL");
+  memset(opt, 0, sizeof(*opt));
+  opt->tol = 1e-12;
+  opt->max_steps = 0;
+  opt->check_every = 4;
+  opt->seed = 42;
+  opt->reorth = 1;
+  return SSA_OK;
+}
+
+// exp(-2 pi i t / M) for t in [0, H), in extended precision then rounded once.
+static std::vector<double2> make_twiddles(int64_t M) {
+  int64_t H = M / 2;
+  std::vector<double2> tw((size_t)H);
+  for (int64_t t = 0; t < H; ++t) {
+    long double ang = 2.0L * 3.14159265358979323846264338327950288L * (long double)t / (long double)M;
+    tw[(size_t)t].x = (double)cosl(ang);
+    tw[(size_t)t].y = (double)(-sinl(ang));
+  }
+  return tw;
+}
+
+static void free_plan(Plan& p) {
+  void* ptrs[] = {p.d_tw, p.d_spec, p.d_U, p.d_V, p.d_rot, p.d_pq, p.d_info, p.d_counter,
+                  p.d_series, p.d_sigma, p.d_Uout, p.d_Vout, p.d_recon, p.d_hscratch};
+  for (void* q : ptrs)
+    if (q) cudaFree(q);
+  for (int i = 0; i < 6; ++i)
+    if (p.ev[i]) cudaEventDestroy(p.ev[i]);
+}
+
+static ssa_status alloc(void** ptr, size_t bytes, const char* what) {
+  if (bytes == 0) bytes = 16;
+  cudaError_t e = cudaMalloc(ptr, bytes);
+  if (e == cudaErrorMemoryAllocation) {
+    cudaGetLastError();
+    return fail(SSA_ERR_OUT_OF_MEMORY, "cudaMalloc(%zu bytes) for %s failed", bytes, what);
+  }
+  if (e != cudaSuccess) return cuda_fail(e, what);
+  return SSA_OK;
+}
+
+extern "C" ssa_status ssa_plan_create(int64_t N, int64_t L, int32_t k, int64_t batch, const ssa_options* opt,
+                                      int device, ssa_plan_t* out) {
+  if (!out) return fail(SSA_ERR_INVALID_ARGUMENT, "out is NULL");
+  *out = nullptr;
+  if (N < 3) return fail(SSA_ERR_INVALID_ARGUMENT, "N = %lld < 3 (PAPER.md:70 requires N > 2)", (long long)N);
+  if (L < 2 || L > N - 1)
+    return fail(SSA_ERR_INVALID_ARGUMENT, "L = %lld outside [2, N-1] (PAPER.md:71: 1 < L < N)", (long long)L);
+  int64_t K = N - L + 1;
+  if (k < 0 || k > std::min(L, K))
+    return fail(SSA_ERR_INVALID_ARGUMENT, "k = %d outside [1, min(L,K) = %lld]", k, (long long)std::min(L, K));
+  if (batch < 1) return fail(SSA_ERR_INVALID_ARGUMENT, "batch = %lld < 1", (long long)batch);
+  ssa_options o;
+  ssa_options_default(&o);
+  if (opt) o = *opt;
+  if (!(o.tol > 0.0) || o.reorth < 1 || o.reorth > 2 || o.check_every < 0 || o.max_steps < 0)
+    return fail(SSA_ERR_INVALID_ARGUMENT, "bad options (tol > 0, reorth in {1,2}, check_every >= 0, max_steps >= 0)");
+
+  int64_t M = 1;
+  while (M < N) M <<= 1;
+  int64_t H = M / 2;
+  if (H > ssa::kMaxSmemH)
+    return fail(SSA_ERR_UNSUPPORTED, "N = %lld needs M = %lld > %d: the multi-CTA FFT path is not built yet",
+                (long long)N, (long long)M, 2 * ssa::kMaxSmemH);
+
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice");
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+  if (prop.major < 10)
+    return fail(SSA_ERR_UNSUPPORTED, "device %d is sm_%d%d; libssa is built for sm_100a only", device, prop.major,
+                prop.minor);
+
+  ssa_plan_s* ps = new ssa_plan_s();
+  Plan& p = ps->p;
+  p.device = device;
+  p.N = N; p.L = L; p.K = K; p.M = M; p.H = H; p.k = k; p.batch = batch; p.opt = o;
+  p.sms = prop.multiProcessorCount;
+  int64_t mn = std::min(L, K);
+  int64_t mm = o.max_steps > 0 ? o.max_steps : std::max<int64_t>(256, 8 * (int64_t)k);
+  p.m_max = (int32_t)std::min(mm, mn);
+  p.ldL = round_up((int)L, 16);
+  p.ldK = round_up((int)K, 16);
+
+  ssa_status st = SSA_OK;
+  for (int i = 0; i < 6; ++i) {
+    e = cudaEventCreate(&p.ev[i]);
+    if (e != cudaSuccess) { st = cuda_fail(e, "cudaEventCreate"); goto bad; }
+  }
+  {
+  std::vector<double2> tw = make_twiddles(M);
+  if ((st = alloc((void**)&p.d_tw, tw.size() * sizeof(double2), "twiddles")) != SSA_OK) goto bad;
+  e = cudaMemcpy(p.d_tw, tw.data(), tw.size() * sizeof(double2), cudaMemcpyHostToDevice);
+  if (e != cudaSuccess) { st = cuda_fail(e, "twiddle upload"); goto bad; }
+  }
+  {
+    const char* which = "";
+    e = ssa::fft_set_attributes((int)H, &which);
+    if (e != cudaSuccess) {
+      st = fail(SSA_ERR_CUDA, "cudaFuncSetAttribute(%s, %zu B smem): %s", which, (size_t)ssa::fpad_bytes((int)H),
+                cudaGetErrorString(e));
+      cudaGetLastError();
+      goto bad;
+    }
+  }
+  if (H > ssa::kMaxHankelSmemH) {
+    p.hank_slots = p.sms;
+    if ((st = alloc((void**)&p.d_hscratch, (size_t)p.hank_slots * (H + 1) * 16, "hankelization scratch")) != SSA_OK)
+      goto bad;
+  }
+
+  if (k > 0) {
+    if (k > 32) { st = fail(SSA_ERR_UNSUPPORTED, "k = %d > 32 not supported by the batched decompose", k); goto bad; }
+    p.smem_lanczos = ssa::lanczos_smem_bytes((int)H, p.ldL, p.ldK, p.m_max, k);
+    if (p.smem_lanczos > (size_t)prop.sharedMemPerBlockOptin) {
+      st = fail(SSA_ERR_UNSUPPORTED, "decompose needs %zu B shared memory > %zu", p.smem_lanczos,
+                (size_t)prop.sharedMemPerBlockOptin);
+      goto bad;
+    }
+    e = ssa::lanczos_set_attributes(p.smem_lanczos);
+    if (e != cudaSuccess) { st = cuda_fail(e, "lanczos attributes"); goto bad; }
+    int per_sm = (int)std::max<size_t>(1, std::min<size_t>(2, (size_t)prop.sharedMemPerMultiprocessor / (p.smem_lanczos + 1024)));
+    p.slots = (int)std::min<int64_t>(batch, (int64_t)p.sms * per_sm);
+    size_t sU = (size_t)(p.m_max + 1) * p.ldL, sV = (size_t)(p.m_max + 1) * p.ldK;
+    size_t cap = (size_t)rot_cap(p.m_max);  // rotation records per side
+    p.d_U = nullptr;
+    if ((st = alloc((void**)&p.d_U, sU * p.slots * 8, "U basis")) != SSA_OK) goto bad;
+    if ((st = alloc((void**)&p.d_V, sV * p.slots * 8, "V basis")) != SSA_OK) goto bad;
+    if ((st = alloc((void**)&p.d_rot, cap * 6 * p.slots * 8, "rotation records")) != SSA_OK) goto bad;
+    if ((st = alloc((void**)&p.d_pq, (size_t)2 * (p.m_max + 2) * k * p.slots * 8, "Ritz coefficients")) != SSA_OK) goto bad;
+    if ((st = alloc((void**)&p.d_spec, (size_t)batch * (H + 1) * 16, "spectra")) != SSA_OK) goto bad;
+    if ((st = alloc((void**)&p.d_info, (size_t)batch * sizeof(ssa_series_info), "info")) != SSA_OK) goto bad;
+    if ((st = alloc((void**)&p.d_counter, 16, "counter")) != SSA_OK) goto bad;
+  }
+  *out = ps;
+  return SSA_OK;
+bad:
+  free_plan(p);
+  delete ps;
+  return st;
+}
+
+extern "C" void ssa_plan_destroy(ssa_plan_t plan) {
+  if (!plan) return;
+  cudaSetDevice(plan->p.device);
+  free_plan(plan->p);
+  delete plan;
+}
+
+extern "C" int64_t ssa_plan_fft_size(ssa_plan_t plan) { return plan ? plan->p.M : -1; }
+extern "C" int32_t ssa_plan_max_steps(ssa_plan_t plan) { return plan ? plan->p.m_max : -1; }
+extern "C" int64_t ssa_plan_launch_count(ssa_plan_t plan) { return plan ? plan->p.launches : -1; }
+
+static cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+extern "C" ssa_status ssa_spectrum(ssa_plan_t plan, const double* d_series, double* d_spec, void* stream) {
+  if (!plan || !d_series || !d_spec) return fail(SSA_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (((uintptr_t)d_spec) & 15) return fail(SSA_ERR_INVALID_ARGUMENT, "d_spec must be 16-byte aligned");
+  Plan& p = plan->p;
+  CK(cudaSetDevice(p.device), "cudaSetDevice");
+  CK(cudaEventRecord(p.ev[0], S(stream)), "event");
+  CK(ssa::launch_spectrum(p, d_series, reinterpret_cast<double2*>(d_spec), S(stream)), "spectrum launch");
+  CK(cudaEventRecord(p.ev[1], S(stream)), "event");
+  p.ev_used[0] = true;
+  p.launches += 1;
+  return SSA_OK;
+}
+
+extern "C" ssa_status ssa_matvec(ssa_plan_t plan, const double* d_spec, const double* d_x, double* d_y,
+                                 int transpose, void* stream) {
+  if (!plan || !d_spec || !d_x || !d_y) return fail(SSA_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (((uintptr_t)d_spec) & 15) return fail(SSA_ERR_INVALID_ARGUMENT, "d_spec must be 16-byte aligned");
+  if (transpose != 0 && transpose != 1) return fail(SSA_ERR_INVALID_ARGUMENT, "transpose must be 0 or 1");
+  Plan& p = plan->p;
+  CK(cudaSetDevice(p.device), "cudaSetDevice");
+  CK(ssa::launch_matvec(p, reinterpret_cast<const double2*>(d_spec), d_x, d_y, transpose, S(stream)),
+     "matvec launch");
+  p.launches += 1;
+  return SSA_OK;
+}
+
+extern "C" ssa_status ssa_hankelize(ssa_plan_t plan, const double* d_sigma, const double* d_U, const double* d_V,
+                                    int32_t nterms, double* d_out, void* stream) {
+  if (!plan || !d_sigma || !d_U || !d_V || !d_out) return fail(SSA_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (nterms < 1) return fail(SSA_ERR_INVALID_ARGUMENT, "nterms = %d < 1", nterms);
+  Plan& p = plan->p;
+  if ((int64_t)p.batch * nterms > (int64_t)0x7fffffff) return fail(SSA_ERR_INVALID_ARGUMENT, "batch*nterms too large");
+  CK(cudaSetDevice(p.device), "cudaSetDevice");
+  CK(cudaEventRecord(p.ev[4], S(stream)), "event");
+  CK(ssa::launch_hankelize(p, d_sigma, d_U, d_V, nterms, d_out, S(stream)), "hankelize launch");
+  CK(cudaEventRecord(p.ev[5], S(stream)), "event");
+  p.ev_used[2] = true;
+  p.launches += 1;
+  return SSA_OK;
+}
+
+extern "C" ssa_status ssa_decompose(ssa_plan_t plan, const double* d_series, double* d_sigma, double* d_U,
+                                    double* d_V, ssa_series_info* d_info, void* stream) {
+  if (!plan || !d_series || !d_sigma || !d_U || !d_V) return fail(SSA_ERR_INVALID_ARGUMENT, "NULL argument");
+  Plan& p = plan->p;
+  if (p.k < 1) return fail(SSA_ERR_INVALID_ARGUMENT, "plan was created with k = 0");
+  CK(cudaSetDevice(p.device), "cudaSetDevice");
+  cudaStream_t s = S(stream);
+  CK(cudaEventRecord(p.ev[0], s), "event");
+  CK(ssa::launch_spectrum(p, d_series, p.d_spec, s), "spectrum launch");
+  CK(cudaEventRecord(p.ev[1], s), "event");
+  p.ev_used[0] = true;
+  CK(cudaMemsetAsync(p.d_counter, 0, sizeof(int), s), "counter reset");
+  ssa::LanczosArgs a;
+  a.N = (int)p.N; a.L = (int)p.L; a.K = (int)p.K; a.M = (int)p.M; a.H = (int)p.H; a.k = p.k;
+  a.m_max = p.m_max; a.ldL = p.ldL; a.ldK = p.ldK;
+  a.check_every = p.opt.check_every; a.reorth_mode = p.opt.reorth; a.batch = (int)p.batch;
+  a.tol = p.opt.tol; a.seed = p.opt.seed;
+  a.series = d_series; a.spec = p.d_spec; a.tw = p.d_tw;
+  a.Ubase = p.d_U; a.Vbase = p.d_V;
+  a.slot_stride_U = (size_t)(p.m_max + 1) * p.ldL;
+  a.slot_stride_V = (size_t)(p.m_max + 1) * p.ldK;
+  a.rot_cap = rot_cap(p.m_max);
+  a.rot = p.d_rot;
+  a.slot_stride_rot = (size_t)a.rot_cap * 6;
+  a.pq = p.d_pq;
+  a.slot_stride_pq = (size_t)2 * (p.m_max + 2) * p.k;
+  a.sigma = d_sigma; a.Uout = d_U; a.Vout = d_V;
+  a.info = d_info ? d_info : p.d_info;
+  a.counter = p.d_counter;
+  CK(cudaEventRecord(p.ev[2], s), "event");
+  CK(ssa::launch_lanczos(p, a, s), "lanczos launch");
+  CK(cudaEventRecord(p.ev[3], s), "event");
+  p.ev_used[1] = true;
+  p.launches += 2;
+  return SSA_OK;
+}
+
+extern "C" ssa_status ssa_reconstruct(ssa_plan_t plan, const double* d_sigma, const double* d_U, const double* d_V,
+                                      double* d_out, void* stream) {
+  if (!plan) return fail(SSA_ERR_INVALID_ARGUMENT, "NULL plan");
+  if (plan->p.k < 1) return fail(SSA_ERR_INVALID_ARGUMENT, "plan was created with k = 0");
+  return ssa_hankelize(plan, d_sigma, d_U, d_V, plan->p.k, d_out, stream);
+}
+
+extern "C" ssa_status ssa_run_host(ssa_plan_t plan, const double* h_series, double* h_sigma, double* h_U,
+                                   double* h_V, double* h_recon, ssa_series_info* h_info, void* stream) {
+  if (!plan || !h_series) return fail(SSA_ERR_INVALID_ARGUMENT, "NULL argument");
+  Plan& p = plan->p;
+  if (p.k < 1) return fail(SSA_ERR_INVALID_ARGUMENT, "plan was created with k = 0");
+  CK(cudaSetDevice(p.device), "cudaSetDevice");
+  ssa_status st;
+  size_t B = (size_t)p.batch, k = (size_t)p.k;
+  if (!p.d_series) {
+    if ((st = alloc((void**)&p.d_series, B * p.N * 8, "series staging")) != SSA_OK) return st;
+    if ((st = alloc((void**)&p.d_sigma, B * k * 8, "sigma staging")) != SSA_OK) return st;
+    if ((st = alloc((void**)&p.d_Uout, B * k * p.L * 8, "U staging")) != SSA_OK) return st;
+    if ((st = alloc((void**)&p.d_Vout, B * k * p.K * 8, "V staging")) != SSA_OK) return st;
+    if ((st = alloc((void**)&p.d_recon, B * k * p.N * 8, "recon staging")) != SSA_OK) return st;
+  }
+  cudaStream_t s = S(stream);
+  CK(cudaMemcpyAsync(p.d_series, h_series, B * p.N * 8, cudaMemcpyHostToDevice, s), "H2D series");
+  if ((st = ssa_decompose(plan, p.d_series, p.d_sigma, p.d_Uout, p.d_Vout, p.d_info, stream)) != SSA_OK) return st;
+  if ((st = ssa_reconstruct(plan, p.d_sigma, p.d_Uout, p.d_Vout, p.d_recon, stream)) != SSA_OK) return st;
+  if (h_sigma) CK(cudaMemcpyAsync(h_sigma, p.d_sigma, B * k * 8, cudaMemcpyDeviceToHost, s), "D2H sigma");
+  if (h_U) CK(cudaMemcpyAsync(h_U, p.d_Uout, B * k * p.L * 8, cudaMemcpyDeviceToHost, s), "D2H U");
+  if (h_V) CK(cudaMemcpyAsync(h_V, p.d_Vout, B * k * p.K * 8, cudaMemcpyDeviceToHost, s), "D2H V");
+  if (h_recon) CK(cudaMemcpyAsync(h_recon, p.d_recon, B * k * p.N * 8, cudaMemcpyDeviceToHost, s), "D2H recon");
+  std::vector<ssa_series_info> info(B);
+  CK(cudaMemcpyAsync(info.data(), p.d_info, B * sizeof(ssa_series_info), cudaMemcpyDeviceToHost, s), "D2H info");
+  CK(cudaStreamSynchronize(s), "stream sync");
+  if (h_info) memcpy(h_info, info.data(), B * sizeof(ssa_series_info));
+  ssa_status worst = SSA_OK;
+  for (size_t b = 0; b < B; ++b) {
+    if (info[b].status == SSA_ERR_INVALID_ARGUMENT) return fail(SSA_ERR_INVALID_ARGUMENT, "series %zu is not finite", b);
+    if (info[b].status != SSA_OK) worst = (ssa_status)info[b].status;
+  }
+  if (worst != SSA_OK) return fail(worst, "some series did not converge");
+  return SSA_OK;
+}
+
+extern "C" ssa_status ssa_plan_phase_ms(ssa_plan_t plan, double out_ms[3]) {
+  if (!plan || !out_ms) return fail(SSA_ERR_INVALID_ARGUMENT, "NULL argument");
+  Plan& p = plan->p;
+  CK(cudaSetDevice(p.device), "cudaSetDevice");
+  for (int i = 0; i < 3; ++i) {
+    out_ms[i] = -1.0;
+    if (!p.ev_used[i]) continue;
+    CK(cudaEventSynchronize(p.ev[2 * i + 1]), "event sync");
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, p.ev[2 * i], p.ev[2 * i + 1]), "event elapsed");
+    out_ms[i] = ms;
+  }
+  return SSA_OK;
+}
+
+extern "C" const char* ssa_status_string(ssa_status s) {
+  switch (s) {
+    case SSA_OK: return "SSA_OK";
+    case SSA_ERR_INVALID_ARGUMENT: return "SSA_ERR_INVALID_ARGUMENT";
+    case SSA_ERR_NOT_CONVERGED: return "SSA_ERR_NOT_CONVERGED";
+    case SSA_ERR_OUT_OF_MEMORY: return "SSA_ERR_OUT_OF_MEMORY";
+    case SSA_ERR_CUDA: return "SSA_ERR_CUDA";
+    case SSA_ERR_INTERNAL: return "SSA_ERR_INTERNAL";
+    case SSA_ERR_UNSUPPORTED: return "SSA_ERR_UNSUPPORTED";
+  }
+  return "SSA_ERR_UNKNOWN";
+}
+
+extern "C" const char* ssa_last_error(void) { return g_err; }

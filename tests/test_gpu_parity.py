@@ -1,0 +1,226 @@
+"""GPU parity: the CUDA path through the C-ABI (paper_0911_4498_b200 -> libssa.so) against
+the CPU oracle (oracle/), on the same seeded inputs.  Tolerances (BASELINE.json north_star,
+DESIGN.md §Parity):
+  * matvec: normwise ‖y − y°‖/‖y°‖ ≤ 1e-12
+  * hankelization: normwise ≤ 1e-12 relative to ‖g°‖
+  * σ: relative ≤ 1e-10; sine angles ≤ 1e-8 (well separated / non-straddling clusters);
+    reconstructions ‖g − g°‖ ≤ 1e-9 ‖F‖ (per triple / per cluster).
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import parity
+import ssa_inputs
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_0911_4498_b200 as pkg
+    assert torch.cuda.is_available()
+    return pkg
+
+
+def cuda(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).cuda()
+
+
+def nrel(a, b):
+    nb = np.linalg.norm(b)
+    return np.linalg.norm(a - b) / (nb if nb > 0 else 1.0)
+
+
+# ----------------------------------------------------------------------------- matvec
+@pytest.mark.parametrize("case", GOLD["matvec"])
+def test_matvec_golden(P, case):
+    f = np.array(case["f"], float)
+    plan = P.Plan(len(f), case["L"], 0, 1)
+    spec = plan.spectrum(cuda(f[None]))
+    y = plan.matvec(spec, cuda(np.array(case["x"], float)[None]), transpose=case["transpose"])
+    assert np.allclose(y.cpu().numpy()[0], case["y"], rtol=0, atol=1e-13), case["cite"]
+
+
+@pytest.mark.parametrize("N", [3, 4, 5, 7, 16, 17, 33, 64, 100])
+def test_matvec_all_windows_vs_oracle(P, N):
+    rng = np.random.default_rng(1000 + N)
+    for L in range(2, N):
+        K = N - L + 1
+        B = 3
+        F = rng.standard_normal((B, N))
+        x = rng.standard_normal((B, K)); u = rng.standard_normal((B, L))
+        plan = P.Plan(N, L, 0, B)
+        spec = plan.spectrum(cuda(F))
+        y = plan.matvec(spec, cuda(x)).cpu().numpy()
+        z = plan.matvec(spec, cuda(u), transpose=True).cpu().numpy()
+        for b in range(B):
+            assert nrel(y[b], oracle.matvec(F[b], L, x[b])) <= 1e-12
+            assert nrel(z[b], oracle.matvec(F[b], L, u[b], True)) <= 1e-12
+
+
+def test_spectrum_matches_dft(P):
+    rng = np.random.default_rng(5)
+    for N in (5, 64, 1000, 4096):
+        F = rng.standard_normal((2, N))
+        plan = P.Plan(N, N // 2, 0, 2)
+        spec = plan.spectrum(cuda(F)).cpu().numpy()
+        S = spec[..., 0] + 1j * spec[..., 1]
+        ref = np.fft.rfft(F, plan.M)   # library DFT, debugging cross-check only
+        assert np.abs(S - ref).max() <= 1e-13 * np.abs(ref).max()
+
+
+def test_matvec_cfg4_sample(P):
+    """cfg4 shape (N=8192, L=4096), series 0..7 of the seeded generator."""
+    c = ssa_inputs.CONFIGS["cfg4"]
+    N, L = c["N"], c["L"]
+    F, V, U = ssa_inputs.cfg4_batch(0, 8, N, L)
+    plan = P.Plan(N, L, 0, 8)
+    spec = plan.spectrum(cuda(F))
+    y = plan.matvec(spec, cuda(V)).cpu().numpy()
+    z = plan.matvec(spec, cuda(U), transpose=True).cpu().numpy()
+    for b in range(8):
+        assert nrel(y[b], oracle.matvec(F[b], L, V[b])) <= 1e-12
+        assert nrel(z[b], oracle.matvec(F[b], L, U[b], True)) <= 1e-12
+
+
+def test_matvec_adjoint(P):
+    rng = np.random.default_rng(6)
+    N, L = 4096, 2048
+    K = N - L + 1
+    F = rng.standard_normal((4, N)); v = rng.standard_normal((4, K)); u = rng.standard_normal((4, L))
+    plan = P.Plan(N, L, 0, 4)
+    spec = plan.spectrum(cuda(F))
+    Xv = plan.matvec(spec, cuda(v)).cpu().numpy()
+    XTu = plan.matvec(spec, cuda(u), transpose=True).cpu().numpy()
+    for b in range(4):
+        lhs, rhs = np.dot(Xv[b], u[b]), np.dot(v[b], XTu[b])
+        assert abs(lhs - rhs) <= 1e-12 * np.linalg.norm(Xv[b]) * np.linalg.norm(u[b])
+
+
+# ----------------------------------------------------------------------------- hankelize
+@pytest.mark.parametrize("case", GOLD["hankelize_rank1"])
+def test_hankelize_golden(P, case):
+    u = np.array(case["u"], float); v = np.array(case["v"], float)
+    N = len(u) + len(v) - 1
+    plan = P.Plan(N, len(u), 0, 1)
+    g = plan.hankelize(cuda([[case["sigma"]]]), cuda(u[None, None]), cuda(v[None, None])).cpu().numpy()
+    assert np.allclose(g[0, 0], case["g"], rtol=0, atol=1e-14), case["cite"]
+
+
+@pytest.mark.parametrize("N,L", [(3, 2), (5, 3), (10, 3), (10, 8), (33, 17), (64, 5), (100, 90), (1000, 500),
+                                 (4096, 2048), (8192, 3000), (16384, 8192)])
+def test_hankelize_vs_oracle(P, N, L):
+    rng = np.random.default_rng(N * 7 + L)
+    K = N - L + 1
+    B, T = 2, 3
+    s = rng.uniform(0.5, 2, (B, T)); U = rng.standard_normal((B, T, L)); V = rng.standard_normal((B, T, K))
+    plan = P.Plan(N, L, 0, B)
+    g = plan.hankelize(cuda(s), cuda(U), cuda(V)).cpu().numpy()
+    for b in range(B):
+        for i in range(T):
+            ref = oracle.hankelize_rank1(s[b, i], U[b, i], V[b, i])
+            assert nrel(g[b, i], ref) <= 1e-12
+
+
+# ----------------------------------------------------------------------------- decompose
+def run_decompose(P, F, L, k, **kw):
+    B, N = F.shape
+    plan = P.Plan(N, L, k, B, **kw)
+    sigma, U, V, info = plan.decompose(cuda(F))
+    G = plan.reconstruct(sigma, U, V)
+    torch.cuda.synchronize()
+    return (sigma.cpu().numpy(), U.cpu().numpy(), V.cpu().numpy(), G.cpu().numpy(),
+            P.info_to_numpy(info))
+
+
+def check_against_oracle(f, L, k, s, U, V, G, sigma_tol=1e-10, recon_scale=None):
+    s_ref, U_ref, V_ref, _ = oracle.svd(f, L, k + 1)
+    G_ref = np.stack([oracle.hankelize_rank1(s_ref[i], U_ref[i], V_ref[i]) for i in range(k)])
+    scale = np.linalg.norm(f) if recon_scale is None else recon_scale
+    rep = parity.compare(s_ref, U_ref, V_ref, s, U, V, k, G_ref, G, recon_scale=scale, sigma_tol=sigma_tol)
+    assert rep.ok(), rep.failures
+    return rep
+
+
+def test_decompose_cfg1(P):
+    c = ssa_inputs.CONFIGS["cfg1"]
+    f = ssa_inputs.cfg1_series(c["N"])
+    s, U, V, G, info = run_decompose(P, f[None], c["L"], c["k"])
+    assert info[0]["status"] == 0 and info[0]["converged"] == 1, info
+    assert info[0]["max_residual"] <= 1e-12
+    rep = check_against_oracle(f, c["L"], c["k"], s[0], U[0], V[0], G[0])
+    print("cfg1 worst:", rep.worst(), "steps", info[0]["steps"])
+
+
+@pytest.mark.parametrize("N,L,k", [(40, 20, 3), (41, 30, 5), (64, 10, 4), (100, 50, 8), (127, 64, 6),
+                                   (300, 100, 10), (513, 256, 12), (2000, 1700, 16)])
+def test_decompose_random_shapes(P, N, L, k):
+    rng = np.random.default_rng(N + 13 * L)
+    n = np.arange(1, N + 1)
+    B = 3
+    F = np.stack([np.sin(2 * np.pi * n / 9.7) + 0.5 * np.cos(2 * np.pi * n / 31) + 0.3 * rng.standard_normal(N)
+                  for _ in range(B)])
+    s, U, V, G, info = run_decompose(P, F, L, k)
+    for b in range(B):
+        assert info[b]["status"] == 0, info[b]
+        check_against_oracle(F[b], L, k, s[b], U[b], V[b], G[b])
+
+
+def test_decompose_full_rank_small_exact(P):
+    """k = min(L, K): the Krylov space is exhausted; all triples and Σ g_i = F."""
+    rng = np.random.default_rng(21)
+    for N, L in [(12, 5), (20, 10), (25, 20)]:
+        f = rng.standard_normal(N)
+        k = min(L, N - L + 1)
+        s, U, V, G, info = run_decompose(P, f[None], L, k)
+        assert info[0]["status"] == 0, info
+        check_against_oracle(f, L, k, s[0], U[0], V[0], G[0])
+        assert np.allclose(G[0].sum(axis=0), f, atol=1e-11 * np.abs(f).max())
+
+
+def test_decompose_rank_deficient(P):
+    """Exact sinusoid: rank 2, Lanczos breaks down; σ₃.. = 0 (restart path)."""
+    N, L, k = 200, 100, 5
+    n = np.arange(1, N + 1)
+    f = 1.5 * np.sin(2 * np.pi * n / 10 + 0.3)
+    s, U, V, G, info = run_decompose(P, f[None], L, k)
+    assert info[0]["breakdown_step"] > 0 and info[0]["status"] == 0
+    s_ref = oracle.svd(f, L, 3)[0]
+    assert np.allclose(s[0, :2], s_ref[:2], rtol=1e-12)
+    assert s[0, 2] <= 1e-10 * s[0, 0]
+    assert np.allclose(G[0, 0] + G[0, 1], f, atol=1e-10)
+
+
+def test_decompose_nonfinite_reported(P):
+    f = np.random.default_rng(3).standard_normal((2, 64))
+    f[1, 10] = np.nan
+    s, U, V, G, info = run_decompose(P, f, 32, 3)
+    assert info[0]["status"] == 0
+    assert info[1]["status"] == 1  # SSA_ERR_INVALID_ARGUMENT
+
+
+def test_invalid_arguments(P):
+    with pytest.raises(P.SsaError):
+        P.Plan(2, 1, 1, 1)
+    with pytest.raises(P.SsaError):
+        P.Plan(10, 10, 1, 1)
+    with pytest.raises(P.SsaError):
+        P.Plan(10, 5, 7, 1)   # k > min(L, K) = 5 -> 6? min(5,6)=5
+    with pytest.raises(P.SsaError):
+        P.Plan(10, 5, 1, 0)
+
+
+def test_run_host_matches_device(P):
+    c = ssa_inputs.CONFIGS["cfg1"]
+    f = ssa_inputs.cfg1_series(c["N"])[None]
+    plan = P.Plan(c["N"], c["L"], c["k"], 1)
+    s, U, V, G, info = plan.run_host(f)
+    sd, Ud, Vd, Gd, infod = run_decompose(P, f, c["L"], c["k"])
+    assert np.array_equal(s, sd) and np.array_equal(G, Gd)
