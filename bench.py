@@ -1,0 +1,395 @@
+#!/usr/bin/env python
+"""bench.py -- throughput of the fast Basic-SSA hot path on B200 (driver contract).
+
+Default workload = BASELINE.json configs[1] ("cfg2"): per GPU a batch of 4096 independent
+fp64 series, N=4096, L=2048, k=16.  One step = the whole hot path over the batch
+(SURVEY.md §8(a) rows a1-a10): spectra, GKL bidiagonalization with full
+reorthogonalization (FFT Hankel products), convergence tests and the bidiagonal SVD on
+device, Ritz assembly, and rank-1 Hankelization of all 16 triples of every series
+(ssa_decompose + ssa_reconstruct through the C-ABI).
+
+Metric: eigentriples/s (fp64) for the whole job; Hankel matvecs/s and roofline of the
+dominant kernel (lanczos_kernel, HBM-bound) are reported beside it.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--batch B]
+
+Multi-GPU (torchrun, one rank per GPU): every rank runs its own batch of 4096 series
+(global series indices rank*4096 + i), no data-path collective; weak scaling.  Timing
+is per step with CUDA events, MAX over ranks; value = all triples / that time.
+
+--impl reference times the CPU oracle (oracle/: one-sided Jacobi SVD + direct averaging)
+as it stands on the host cores on a bounded sample of the same workload (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import glob
+import json
+import os
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import ssa_inputs  # noqa: E402
+
+METRIC = "SSA eigentriples/s and Hankel matvecs/s (fp64), % HBM/fp64 roofline, 1–8 B200"
+UNIT = "eigentriples/s"
+CFG = ssa_inputs.CONFIGS["cfg2"]
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--batch", type=int, default=CFG["batch"], help="series per GPU (default 4096)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--profile-once", action="store_true", help="1 decompose, no timing (for ncu)")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------------ model bytes
+def lanczos_alg_bytes(steps: np.ndarray, N: int, L: int, k: int) -> float:
+    """Algorithmic HBM bytes of lanczos_kernel for series that ran m = steps Lanczos steps
+    (DESIGN.md §Roofline): one-pass full reorthogonalization reads the basis twice per
+    half-step (dots, update), every half-step reads the spectrum once and writes one basis
+    vector; the start reads the series and writes u_1; Ritz assembly reads U_{m+1}, V_m once
+    and writes k(L+K) outputs.
+      half-step A, j = 1..m+1: 16 K (j-1) + 16 (H+1) + 8 K
+      half-step B, j = 1..m  : 16 L j     + 16 (H+1) + 8 L
+    """
+    K = N - L + 1
+    M = 1
+    while M < N:
+        M <<= 1
+    H = M // 2
+    m = steps.astype(np.float64)
+    a = 16 * K * (m * (m + 1) / 2) + (m + 1) * (16 * (H + 1) + 8 * K)
+    b = 16 * L * (m * (m + 1) / 2) + m * (16 * (H + 1) + 8 * L)
+    start = 8 * N + 8 * L
+    ritz = 8 * ((m + 1) * L + m * K) + 8 * k * (L + K)
+    return float(np.sum(a + b + start + ritz))
+
+
+def hankelize_alg_bytes(nterms: int, N: int, L: int) -> float:
+    K = N - L + 1
+    return float(nterms) * 8 * (L + K + N + 1)
+
+
+# ------------------------------------------------------------------------ clocks
+class ClockSampler:
+    """Samples SM clock and throttle reasons with NVML every 100 ms in a thread."""
+
+    def __init__(self, dev: int):
+        self.dev = dev
+        self.samples = []
+        self.reasons = set()
+        self._stop = threading.Event()
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(dev)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover
+            self.err = str(e)
+
+    def _run(self):
+        nv = self.nv
+        names = {
+            "gpu_idle": getattr(nv, "nvmlClocksEventReasonGpuIdle", 0x1),
+            "sw_power_cap": getattr(nv, "nvmlClocksEventReasonSwPowerCap", 0x4),
+            "hw_slowdown": getattr(nv, "nvmlClocksEventReasonHwSlowdown", 0x8),
+            "sw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonSwThermalSlowdown", 0x20),
+            "hw_thermal_slowdown": getattr(nv, "nvmlClocksEventReasonHwThermalSlowdown", 0x40),
+            "hw_power_brake_slowdown": getattr(nv, "nvmlClocksEventReasonHwPowerBrakeSlowdown", 0x80),
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for n, bit in names.items():
+                    if r & bit and n != "gpu_idle":
+                        self.reasons.add(n)
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": float(self.max_mhz),
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------------ peaks
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "MEASURED_PEAKS.json hbm_gbs (driver-measured copy)"
+    return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
+
+
+def ncu_traffic(name: str):
+    """dram read+write bytes per launch of `name` from the committed ncu summary."""
+    for p in sorted(glob.glob(os.path.join(ROOT, "profiles", "*ncu_summary*.json")), reverse=True):
+        try:
+            d = json.load(open(p))
+            if name in d and d[name].get("dram_bytes_per_launch"):
+                if d[name].get("batch") == CFG["batch"]:
+                    return float(d[name]["dram_bytes_per_launch"]), os.path.basename(p)
+        except Exception:
+            pass
+    return None, None
+
+
+# ------------------------------------------------------------------------ oracle arm
+def oracle_sample(cores: int, seconds_hint: float = 20.0):
+    """Time the CPU oracle on a bounded sample of cfg2: each of `cores` threads runs ONE
+    Jacobi sweep of a different cfg2 series (GIL released inside the C call) plus the k
+    direct averagings; the full per-series time is extrapolated with the sweep count the
+    oracle itself needed on cfg2 series (tests/golden/oracle_cfg2_*.npz, written by
+    oracle/make_golden.py).  Returns (triples/s on `cores` cores, description)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    import oracle
+    N, L, k = CFG["N"], CFG["L"], CFG["k"]
+    K = N - L + 1
+    sweeps = []
+    for p in glob.glob(os.path.join(ROOT, "tests", "golden", "oracle_cfg2_*.npz")):
+        sweeps.append(abs(int(np.load(p)["sweeps"])))
+    s_full = float(np.mean(sweeps)) if sweeps else 12.0
+    rng = np.random.default_rng(0)
+    u = rng.standard_normal(L); u /= np.linalg.norm(u)
+    v = rng.standard_normal(K); v /= np.linalg.norm(v)
+
+    def work(i):
+        f = ssa_inputs.cfg2_series(i, N)
+        t0 = time.perf_counter()
+        oracle.svd_sweeps(f, L, k, 1)
+        t1 = time.perf_counter()
+        for _ in range(k):
+            oracle.hankelize_rank1(1.0, u, v)
+        t2 = time.perf_counter()
+        return t1 - t0, t2 - t1
+
+    oracle.build()
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(cores) as ex:
+        res = list(ex.map(work, range(cores)))
+    wall = time.perf_counter() - t0
+    per_series = float(np.mean([a * s_full + b for a, b in res]))
+    rate = cores * k / per_series
+    desc = (f"{cores} cfg2 series (one per core, threads): 1 Jacobi sweep each timed "
+            f"({np.mean([a for a, _ in res]):.2f} s) x {s_full:.1f} sweeps the oracle needs on cfg2 "
+            f"+ {k} direct averagings ({np.mean([b for _, b in res]):.2f} s); wall {wall:.1f} s")
+    return rate, desc, wall
+
+
+def run_reference(args, rank):
+    if rank != 0:
+        return 0
+    cores = os.cpu_count() or 1
+    times = []
+    for _ in range(args.warmup if args.warmup < 1 else 1):
+        pass
+    vals = []
+    descs = []
+    for _ in range(max(1, args.steps)):
+        rate, desc, wall = oracle_sample(cores)
+        vals.append(rate)
+        times.append(wall)
+        descs.append(desc)
+    value = float(np.median(vals))
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * CFG["batch"] * CFG["k"] / value,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "cfg2: 4096 series N=4096 L=2048 k=16, decompose+reconstruct (CPU oracle)",
+                   "N": CFG["N"], "L": CFG["L"], "k": CFG["k"], "batch_per_gpu": CFG["batch"]},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": descs[0]},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------------ our arm
+def main():
+    args = parse()
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    if args.impl == "reference":
+        return run_reference(args, rank)
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_0911_4498_b200 as P
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    N, L, k = CFG["N"], CFG["L"], CFG["k"]
+    K = N - L + 1
+    B = args.batch
+    # inputs: this rank's series, global indices rank*B + i (weak scaling)
+    host = ssa_inputs.cfg2_batch(rank * B, B, N)
+    series = torch.from_numpy(host).cuda()
+    plan = P.Plan(N, L, k, B)
+    sigma = torch.empty((B, k), dtype=torch.float64, device="cuda")
+    U = torch.empty((B, k, L), dtype=torch.float64, device="cuda")
+    V = torch.empty((B, k, K), dtype=torch.float64, device="cuda")
+    G = torch.empty((B, k, N), dtype=torch.float64, device="cuda")
+    info = torch.zeros((B, P.INFO_DTYPE.itemsize), dtype=torch.uint8, device="cuda")
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def step():
+        plan.decompose(series, sigma, U, V, info)
+        plan.reconstruct(sigma, U, V, G)
+
+    if args.profile_once:
+        step()
+        torch.cuda.synchronize()
+        return 0
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+
+    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    lan_ms, hank_ms, spec_ms = [], [], []
+    launches0 = plan.launches
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.zero_()                       # L2 flush between timed steps (untimed)
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            ev0[i].record(stream)
+            step()
+            ev1[i].record(stream)
+            torch.cuda.synchronize()
+            ph = plan.phase_ms()
+            lan_ms.append(ph["lanczos"]); hank_ms.append(ph["hankelize"]); spec_ms.append(ph["spectrum"])
+    launches = (plan.launches - launches0) // args.steps
+    step_ms = np.array([a.elapsed_time(b) for a, b in zip(ev0, ev1)])
+    total = torch.tensor([step_ms.sum()], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(total, op=dist.ReduceOp.MAX)
+    ms_per_step = float(total.item()) / args.steps
+    inf = P.info_to_numpy(info)
+    steps_m = inf["steps"].astype(np.int64)
+    conv = float(np.mean(inf["converged"]))
+    triples = B * k * world
+    value = triples / (ms_per_step * 1e-3)
+    matvecs = float((2 * steps_m + 1).sum()) * world / (ms_per_step * 1e-3)
+
+    # roofline of the dominant kernel (lanczos_kernel) from live CUDA events
+    peak, peak_src = measured_peaks()
+    alg = lanczos_alg_bytes(steps_m, N, L, k)
+    lan = float(np.mean(lan_ms))
+    achieved = alg / (lan * 1e-3) / 1e9
+    traffic, traffic_src = ncu_traffic("lanczos_kernel")
+    hk = float(np.mean(hank_ms))
+    hk_bw = hankelize_alg_bytes(B * k, N, L) / (hk * 1e-3) / 1e9
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "cfg2 (BASELINE.json configs[1]): per GPU 4096 fp64 series N=4096 L=2048 k=16, "
+                               "decompose + reconstruct all 16 triples",
+                   "N": N, "L": L, "k": k, "batch_per_gpu": B, "global_batch": B * world,
+                   "parallelism": f"series-sharded x{world} (no data-path collective)",
+                   "l2": "inputs (134 MB/GPU) > L2 and a 256 MiB L2 flush before every timed step",
+                   "tol": 1e-12, "reorth": "CGS + DGKS"},
+        "hankel_matvecs_per_s": matvecs,
+        "lanczos_steps": {"min": int(steps_m.min()), "median": float(np.median(steps_m)),
+                          "max": int(steps_m.max()), "mean": float(steps_m.mean())},
+        "converged_fraction": conv,
+        "max_residual": float(inf["max_residual"].max()),
+        "phase_ms": {"spectrum": float(np.mean(spec_ms)), "lanczos": lan, "hankelize": hk},
+        "roofline": {"kernel": "lanczos_kernel", "bound": "hbm", "achieved": achieved, "peak": peak,
+                     "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                     "traffic_src": traffic_src, "peak_src": peak_src,
+                     "alg_bytes_per_launch": alg},
+        "hankelize_roofline": {"bound": "hbm (model, fp64 FFT)", "achieved": hk_bw, "peak": peak, "unit": "GB/s",
+                               "frac": hk_bw / peak},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+
+    # e2e through the public C call on host buffers (pinned), copies inside the timed region
+    if not args.no_e2e:
+        pin_series = torch.from_numpy(host).pin_memory()
+        outs = [torch.empty(s, dtype=torch.float64).pin_memory() for s in
+                [(B, k), (B, k, L), (B, k, K), (B, k, N)]]
+        h_info = np.zeros(B, dtype=P.INFO_DTYPE)
+        import ctypes
+        lib = P.load_library()
+        plan2 = P.Plan(N, L, k, B)
+
+        def e2e_step():
+            st = lib.ssa_run_host(plan2._h, pin_series.data_ptr(), outs[0].data_ptr(), outs[1].data_ptr(),
+                                  outs[2].data_ptr(), outs[3].data_ptr(), h_info.ctypes.data,
+                                  ctypes.c_void_p(stream.cuda_stream))
+            return st
+
+        e2e_step()
+        times = []
+        for _ in range(max(1, min(3, args.steps))):
+            flush.zero_()
+            if world > 1:
+                dist.barrier()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            e2e_step()
+            times.append(time.perf_counter() - t0)
+        t = torch.tensor([float(np.mean(times))], dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        line["e2e"] = {"value": triples / float(t.item()), "unit": UNIT,
+                       "h2d_bytes_per_step": int(B * N * 8),
+                       "d2h_bytes_per_step": int(B * k * (1 + L + K + N) * 8 + B * P.INFO_DTYPE.itemsize),
+                       "api": "ssa_run_host (pinned host buffers; H2D series, D2H sigma/U/V/recon/info)"}
+        plan2.close()
+
+    if rank == 0 and not args.no_cpu_baseline:
+        cores = os.cpu_count() or 1
+        rate, desc, wall = oracle_sample(cores)
+        line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc}
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -50,6 +50,8 @@ def _load():
             lib.oracle_hankelize_rank1.argtypes = [ctypes.c_double, _dp, i64, _dp, i64, _dp]
             lib.oracle_svd_jacobi.argtypes = [_dp, i64, i64, i64, _dp, _dp, _dp]
             lib.oracle_svd_jacobi.restype = ctypes.c_int
+            lib.oracle_svd_jacobi_capped.argtypes = [_dp, i64, i64, i64, _dp, _dp, _dp, ctypes.c_int]
+            lib.oracle_svd_jacobi_capped.restype = ctypes.c_int
             _lib = lib
     return _lib
 
@@ -112,6 +114,17 @@ def svd(f, L: int, nsv: int | None = None):
     s = np.empty(nsv); U = np.empty((nsv, L)); V = np.empty((nsv, K))
     sweeps = _load().oracle_svd_jacobi(_p(f), N, L, nsv, _p(s), _p(U), _p(V))
     return s, U, V, sweeps
+
+
+def svd_sweeps(f, L: int, nsv: int, max_sweeps: int):
+    """The same Jacobi computation stopped after max_sweeps sweeps (bench.py's bounded
+    CPU-baseline sample only; results are not converged triples)."""
+    f = _c(f)
+    N = f.shape[0]
+    K = N - L + 1
+    nsv = min(nsv, min(L, K))
+    s = np.empty(nsv); U = np.empty((nsv, L)); V = np.empty((nsv, K))
+    return _load().oracle_svd_jacobi_capped(_p(f), N, L, nsv, _p(s), _p(U), _p(V), int(max_sweeps))
 
 
 def reconstruct(f, L: int, nsv: int | None = None):

@@ -224,3 +224,32 @@ def test_run_host_matches_device(P):
     s, U, V, G, info = plan.run_host(f)
     sd, Ud, Vd, Gd, infod = run_decompose(P, f, c["L"], c["k"])
     assert np.array_equal(s, sd) and np.array_equal(G, Gd)
+
+
+# ----------------------------------------------------------------------------- cfg2 full size
+def test_decompose_cfg2_full_batch_sampled(P):
+    """BASELINE configs[1] at full size in bench.py's launch configuration (batch 4096,
+    N=4096, L=2048, k=16): sampled series 0, 1234, 4095 against oracle results written by
+    oracle/make_golden.py (Jacobi + direct averaging, CPU); all series: convergence,
+    ordering and the Frobenius bound Σσ² ≤ ‖X‖_F²."""
+    import glob
+    c = ssa_inputs.CONFIGS["cfg2"]
+    N, L, k, B = c["N"], c["L"], c["k"], c["batch"]
+    F = ssa_inputs.cfg2_batch(0, B, N)
+    s, U, V, G, info = run_decompose(P, F, L, k)
+    assert np.all(info["status"] == 0), np.unique(info["status"], return_counts=True)
+    assert np.all(info["max_residual"] <= 1e-12)
+    assert np.all(np.diff(s, axis=1) <= 0)
+    K = N - L + 1
+    cnt = np.minimum.reduce([np.arange(1, N + 1), np.full(N, L), np.full(N, K), N - np.arange(N)])
+    fro2 = (F * F * cnt).sum(axis=1)
+    assert np.all((s * s).sum(axis=1) <= fro2 * (1 + 1e-12))
+    files = sorted(glob.glob(os.path.join(os.path.dirname(__file__), "golden", "oracle_cfg2_*.npz")))
+    assert files, "run python -m oracle.make_golden"
+    for p in files:
+        d = np.load(p)
+        i = int(d["series_index"])
+        rep = parity.compare(d["sigma"], d["U"], d["V"], s[i], U[i], V[i], k, d["G"], G[i],
+                             recon_scale=float(d["norm_f"]))
+        assert rep.ok(), (i, rep.failures)
+        print(f"cfg2 series {i}: steps {info[i]['steps']} worst {rep.worst()}")
