@@ -155,10 +155,25 @@ const char* ssa_last_error(void);
 int64_t ssa_plan_launch_count(ssa_plan_t plan);
 
 /* Device time (ms, CUDA events recorded on the launching stream around each kernel) of
- * the most recent spectrum, Lanczos (decompose minus spectrum) and hankelization launches
- * of this plan: out_ms[0] = spectrum, out_ms[1] = lanczos, out_ms[2] = hankelize.  Blocks
- * until those events completed; entries never launched are reported as -1. */
-ssa_status ssa_plan_phase_ms(ssa_plan_t plan, double out_ms[3]);
+ * the most recent launch of each phase of this plan: out_ms[0] spectrum, [1] Lanczos
+ * bidiagonalization, [2] bidiagonal SVD, [3] Ritz assembly, [4] hankelization.  Blocks
+ * until those events completed; phases never launched are reported as -1.  (When a
+ * decompose call is split into several chunks, the times are those of the last chunk.) */
+ssa_status ssa_plan_phase_ms(ssa_plan_t plan, double out_ms[5]);
+
+/* Diagnostic: if the plan was created with (options.reserved & 1), the decompose kernel
+ * accumulates SM clock cycles per phase summed over all CTAs and launches:
+ * out[0] FFT products, [1] reorthogonalization, [2] convergence tests, [3] final
+ * bidiagonal QR, [4] forming P_k / Q_k, [5] Ritz assembly + signs, [6] number of
+ * convergence tests, [7] other.  INVALID_ARGUMENT if profiling is off. */
+ssa_status ssa_plan_profile(ssa_plan_t plan, int64_t out[8]);
+
+/* Diagnostic / test hook: after ssa_decompose (synchronizes the device), copy the
+ * Lanczos bidiagonal factors of the series of the LAST decompose chunk (all series when
+ * the batch fits one chunk): h_alpha[b][j] = alpha_j, h_beta[b][j] = beta_j for
+ * j = 0..m_max+2 (1-based as in Alg. 1; unused entries undefined) and
+ * h_steps[b] = m.  Shapes: [nb][m_max+3], [nb][m_max+3], [nb]. */
+ssa_status ssa_plan_bidiagonals(ssa_plan_t plan, double* h_alpha, double* h_beta, int32_t* h_steps);
 
 #ifdef __cplusplus
 }

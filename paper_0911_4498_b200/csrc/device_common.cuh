@@ -1,0 +1,194 @@
+// device_common.cuh -- reductions, TMA bulk-copy streaming and the FFT correlation /
+// real-FFT pair steps shared by the kernels of libssa.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "fft_smem.cuh"
+#include "ssa_internal.h"
+
+namespace ssa {
+
+// ------------------------------------------------------------------ reductions
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Deterministic CTA sum: fixed shuffle tree, then warps summed in index order.
+__device__ __forceinline__ double block_sum(double v, double* red) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  const int nw = blockDim.x >> 5;
+  for (int i = 0; i < nw; ++i) s += red[i];
+  return s;
+}
+
+__device__ __forceinline__ int block_or(int v, int* redi) {
+  __syncthreads();
+  if (threadIdx.x == 0) *redi = 0;
+  __syncthreads();
+  if (v) atomicOr(redi, 1);
+  __syncthreads();
+  return *redi;
+}
+
+// ------------------------------------------------------------------ FFT pair steps
+// Forward real post-processing for the pair (p, H-p) from digit-reversed Z:
+//   X_p = E + W^p O,  X_{H-p} = conj(E - W^p O),  E = (Z_p + conj Z_{H-p})/2,
+//   O = -i (Z_p - conj Z_{H-p})/2,  W = exp(-2 pi i / M).
+__device__ __forceinline__ void real_pair(const double2* buf, const FftShape& sh, const double2* __restrict__ T,
+                                          int p, double2& Xp, double2& Xq, int& pr, int& qr) {
+  const int H = sh.H;
+  const int q = (H - p) & (H - 1);
+  pr = rev_index(sh, p);
+  qr = rev_index(sh, q);
+  double2 Zp = buf[fpad(pr)], Zq = buf[fpad(qr)];
+  double2 W = twiddle(T, p, H);
+  double2 E = make_double2(0.5 * (Zp.x + Zq.x), 0.5 * (Zp.y - Zq.y));
+  double2 D = make_double2(0.5 * (Zp.x - Zq.x), 0.5 * (Zp.y + Zq.y));
+  double2 O = make_double2(D.y, -D.x);  // -i D
+  double2 WO = cmul(W, O);
+  Xp = cadd(E, WO);
+  Xq = conjg(csub(E, WO));
+}
+
+// Inverse pre-processing: from half-spectrum values Y_p, Y_{H-p} of a real sequence
+// produce Z'_p = E + i O, Z'_{H-p} = conj(E) + i conj(O), E = (Y_p + conj Y_{H-p})/2,
+// O = (Y_p - conj Y_{H-p}) conj(W^p) / 2, whose inverse FFT is y_2n + i y_2n+1.
+__device__ __forceinline__ void inv_pair(double2* buf, const double2* __restrict__ T, int H, int p, int pr, int qr,
+                                         double2 Yp, double2 Yq) {
+  double2 W = twiddle(T, p, H);
+  double2 E = make_double2(0.5 * (Yp.x + Yq.x), 0.5 * (Yp.y - Yq.y));
+  double2 D = make_double2(0.5 * (Yp.x - Yq.x), 0.5 * (Yp.y + Yq.y));
+  double2 O = cmulc(D, W);
+  buf[fpad(pr)] = make_double2(E.x - O.y, E.y + O.x);
+  if (qr != pr) buf[fpad(qr)] = make_double2(E.x + O.y, O.x - E.y);
+}
+
+// Correlation spectrum step: Z (digit-reversed FFT of packed x) -> Z' whose inverse is
+// the packed correlation y = irfft(F^ conj(X^)).
+__device__ __forceinline__ void corr_pairs(double2* buf, const FftShape& sh, const double2* __restrict__ T,
+                                           const double2* __restrict__ spec, int tid, int nthr) {
+  const int H = sh.H;
+  for (int p = tid; p <= (H >> 1); p += nthr) {
+    double2 Xp, Xq;
+    int pr, qr;
+    real_pair(buf, sh, T, p, Xp, Xq, pr, qr);
+    double2 Fp = __ldg(spec + p), Fq = __ldg(spec + (H - p));
+    inv_pair(buf, T, H, p, pr, qr, cmulc(Fp, Xp), cmulc(Fq, Xq));
+  }
+}
+
+// Full correlation in one CTA (all threads): y_t = sum_s f_{t+s} x_s, t < n_out
+// (the Hankel products of Alg. 2 / Alg. 3, in correlation form).
+template <class LoadX, class StoreY>
+__device__ __forceinline__ void correlate_cta(double2* buf, const FftShape& sh, const double2* __restrict__ T,
+                                              const double2* __restrict__ spec, int n_in, int n_out, LoadX loadx,
+                                              StoreY storey) {
+  const int H = sh.H, tid = threadIdx.x, nthr = blockDim.x;
+  for (int n = tid; n < H; n += nthr) {
+    int i0 = 2 * n;
+    double a = (i0 < n_in) ? loadx(i0) : 0.0;
+    double b = (i0 + 1 < n_in) ? loadx(i0 + 1) : 0.0;
+    buf[fpad(n)] = make_double2(a, b);
+  }
+  __syncthreads();
+  fft_forward(buf, sh, T, tid, nthr, CtaSync());
+  corr_pairs(buf, sh, T, spec, tid, nthr);
+  __syncthreads();
+  fft_inverse(buf, sh, T, tid, nthr, CtaSync());
+  const double invH = 1.0 / (double)H;
+  for (int t = tid; t < n_out; t += nthr) {
+    double2 z = buf[fpad(t >> 1)];
+    storey(t, ((t & 1) ? z.y : z.x) * invH);
+  }
+}
+
+// ------------------------------------------------------------------ TMA bulk streaming
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t a = smem_u32(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+
+// Per-warp ring of kStages chunks; one lane issues cp.async.bulk, all lanes consume.
+struct WarpRing {
+  double* buf;    // kStages * slab doubles
+  uint64_t* bar;  // kStages barriers
+  uint32_t cnt;   // chunks consumed so far (== issued at the end of each stream)
+};
+
+__device__ __forceinline__ void ring_init(WarpRing& rg, double* buf, uint64_t* bar) {
+  rg.buf = buf;
+  rg.bar = bar;
+  rg.cnt = 0;
+  if ((threadIdx.x & 31) == 0)
+    for (int s = 0; s < kStages; ++s) mbar_init(bar + s, 1);
+}
+
+// Streams rows (q-th job = row q, or nb-1-q if reverse) of this warp's column slab
+// [w*slab, (w+1)*slab) of a row-major basis (row stride ld doubles) through the ring;
+// calls f(row, chunk) for each in order.  All lanes of the warp must call it.
+template <class F>
+__device__ __forceinline__ void stream_rows(const double* base_w, int ld, int nb, bool reverse, int slab, WarpRing& rg,
+                                            F f) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t bytes = (uint32_t)slab * 8u;
+  const uint32_t c0 = rg.cnt;
+  if (lane == 0) {
+    int pre = nb < kStages ? nb : kStages;
+    for (int q = 0; q < pre; ++q) {
+      int st = (int)((c0 + q) % kStages);
+      int row = reverse ? nb - 1 - q : q;
+      mbar_expect_tx(rg.bar + st, bytes);
+      tma_load_1d(rg.buf + (size_t)st * slab, base_w + (size_t)row * ld, bytes, rg.bar + st);
+    }
+  }
+  for (int q = 0; q < nb; ++q) {
+    const uint32_t c = c0 + q;
+    const int st = (int)(c % kStages);
+    mbar_wait(rg.bar + st, (c / kStages) & 1u);
+    f(reverse ? nb - 1 - q : q, rg.buf + (size_t)st * slab);
+    __syncwarp();
+    if (lane == 0 && q + kStages < nb) {
+      int row = reverse ? nb - 1 - (q + kStages) : q + kStages;
+      mbar_expect_tx(rg.bar + st, bytes);
+      tma_load_1d(rg.buf + (size_t)st * slab, base_w + (size_t)row * ld, bytes, rg.bar + st);
+    }
+  }
+  rg.cnt = c0 + nb;
+}
+
+__host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
+
+}  // namespace ssa

@@ -1,16 +1,16 @@
 // fft_smem.cuh -- fp64 FFT building blocks held entirely in shared memory (sm_100a).
 //
-// One CTA transforms one complex vector of H = M/2 points (H a power of two, H <= 8192)
-// in place:
+// One CTA transforms one complex vector of H = M/2 = 2^logH points (H <= 8192) in place:
 //   * forward: in-place decimation-in-frequency passes (radix 8, final radix 4/2),
 //     natural order in -> mixed-radix digit-reversed order out;
 //   * inverse: the exact inverse passes in reverse order with conjugate twiddles,
 //     digit-reversed in -> natural order out, unnormalized (result x H).
 // So forward -> pointwise work in digit-reversed positions -> inverse needs no
 // permutation pass.  Real transforms of length M are packed into H complex points
-// (z_n = x_2n + i x_2n+1) with the usual split post-/pre-processing (see
-// ssa_kernels.cu).  This is the DFT of PAPER.md:473-509 (sec 4.1: unnormalized forward,
-// 1/N inverse), evaluated as an FFT.
+// (z_n = x_2n + i x_2n+1) with the usual split post-/pre-processing (ssa_kernels.cu).
+// This is the DFT of PAPER.md:473-509 (sec 4.1: unnormalized forward, 1/N inverse),
+// evaluated as an FFT.  All index arithmetic is shifts/masks (H and radices are powers
+// of two).
 //
 // Shared-memory layout: element i lives at slot i + (i >> 3) (one pad slot per 8) so
 // that stride-8 radix-8 butterflies of the last pass hit distinct banks.
@@ -23,10 +23,8 @@
 
 namespace ssa {
 
-__device__ __forceinline__ int fpad(int i) { return i + (i >> 3); }
+__host__ __device__ __forceinline__ int fpad(int i) { return i + (i >> 3); }
 __host__ __device__ __forceinline__ int fpad_size(int H) { return H + (H >> 3) + 1; }
-
-struct cplx { double x, y; };
 
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
   return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
@@ -45,32 +43,32 @@ __device__ __forceinline__ double2 twiddle(const double2* __restrict__ T, int t,
   return make_double2(-w.x, -w.y);
 }
 
-// Radix sequence: passes of radix 8 while >= 8 remain, then one of radix 4 or 2.
+// Shape: n8 radix-8 passes then one radix-2^lastb pass (lastb in {0,1,2}).
 struct FftShape {
-  int H;        // points
-  int npass;
-  int radix[6];
+  int H, logH, n8, lastb;
 };
 
 __host__ __device__ inline FftShape make_shape(int H) {
   FftShape s;
   s.H = H;
-  s.npass = 0;
-  int rem = H;
-  while (rem >= 8) { s.radix[s.npass++] = 8; rem >>= 3; }
-  if (rem > 1) s.radix[s.npass++] = rem;  // 2 or 4
+  int l = 0;
+  while ((1 << l) < H) ++l;
+  s.logH = l;
+  s.n8 = l / 3;
+  s.lastb = l - 3 * s.n8;
   return s;
 }
 
 // Digit-reversed position of frequency k (forward output order).
 __device__ __forceinline__ int rev_index(const FftShape& s, int k) {
-  int pos = 0, size = s.H;
-  for (int p = 0; p < s.npass; ++p) {
-    int r = s.radix[p];
-    size /= r;
-    pos += (k % r) * size;
-    k /= r;
+  int pos = 0, lsz = s.logH;
+#pragma unroll 5
+  for (int p = 0; p < s.n8; ++p) {
+    lsz -= 3;
+    pos += (k & 7) << lsz;
+    k >>= 3;
   }
+  if (s.lastb) pos += (k & ((1 << s.lastb) - 1));  // final block size is 1
   return pos;
 }
 
@@ -100,12 +98,10 @@ __device__ __forceinline__ void dft4(double2& a0, double2& a1, double2& a2, doub
 template <bool INV>
 __device__ __forceinline__ void dft8(double2* a) {
   const double r = 0.70710678118654752440084436210485;  // 1/sqrt(2)
-  // split into even / odd DFT4s
   double2 e0 = a[0], e1 = a[2], e2 = a[4], e3 = a[6];
   double2 o0 = a[1], o1 = a[3], o2 = a[5], o3 = a[7];
   dft4<INV>(e0, e1, e2, e3);
   dft4<INV>(o0, o1, o2, o3);
-  // twiddle odds by W8^k, W8 = exp(-+ 2 pi i / 8)
   double2 t1, t2, t3;
   if (!INV) {
     t1 = make_double2(r * (o1.x + o1.y), r * (o1.y - o1.x));    // * (1 - i)/sqrt2
@@ -129,54 +125,37 @@ __device__ __forceinline__ void dftR(double2* a) {
   else dft2<INV>(a[0], a[1]);
 }
 
-// One forward DIF pass: block size S, radix R, Q = S / R.  Butterfly (b, n1):
-//   y[n1 + Q k2] = W_S^{n1 k2} * sum_{n2} x[n1 + Q n2] W_R^{n2 k2}
-template <int R>
-__device__ __forceinline__ void dif_pass(double2* buf, int H, int S, const double2* __restrict__ T,
+// One DIF pass (forward) or its inverse: block size S = 2^logS, radix R = 2^LR,
+// Q = S / R.  Butterfly (b, n1):
+//   forward: y[n1 + Q k2] = W_S^{n1 k2} * sum_{n2} x[n1 + Q n2] W_R^{n2 k2}
+//   inverse: x[n1 + Q n2] = sum_{k2} W_R^{-n2 k2} W_S^{-n1 k2} y[n1 + Q k2]   (times R)
+template <int LR, bool INV>
+__device__ __forceinline__ void fft_pass(double2* buf, int H, int logH, int logS, const double2* __restrict__ T,
                                          int tid, int nthr) {
-  const int Q = S / R;
-  const int M = 2 * H;
-  const int tstep = M / S;  // exp(-2 pi i n1 k2 / S) = T[n1 k2 M / S]
-  for (int bf = tid; bf < H / R; bf += nthr) {
-    int b = bf / Q, n1 = bf - b * Q;
-    int base = b * S + n1;
+  constexpr int R = 1 << LR;
+  const int logQ = logS - LR;
+  const int Q = 1 << logQ;
+  const int tshift = logH + 1 - logS;  // exp(-2 pi i n1 k2 / S) = T[n1 k2 << (logM - logS)]
+  for (int bf = tid; bf < (H >> LR); bf += nthr) {
+    const int b = bf >> logQ, n1 = bf & (Q - 1);
+    const int base = (b << logS) + n1;
     double2 a[R];
 #pragma unroll
-    for (int q = 0; q < R; ++q) a[q] = buf[fpad(base + q * Q)];
-    dftR<R, false>(a);
-    if (Q > 1) {
+    for (int q = 0; q < R; ++q) a[q] = buf[fpad(base + (q << logQ))];
+    if (INV && Q > 1) {
 #pragma unroll
-      for (int q = 1; q < R; ++q) a[q] = cmul(a[q], twiddle(T, n1 * q * tstep, H));
+      for (int q = 1; q < R; ++q) a[q] = cmulc(a[q], twiddle(T, (n1 * q) << tshift, H));
+    }
+    dftR<R, INV>(a);
+    if (!INV && Q > 1) {
+#pragma unroll
+      for (int q = 1; q < R; ++q) a[q] = cmul(a[q], twiddle(T, (n1 * q) << tshift, H));
     }
 #pragma unroll
-    for (int q = 0; q < R; ++q) buf[fpad(base + q * Q)] = a[q];
+    for (int q = 0; q < R; ++q) buf[fpad(base + (q << logQ))] = a[q];
   }
 }
 
-// Inverse of dif_pass (times R): x[n1 + Q n2] = sum_{k2} W_R^{-n2 k2} W_S^{-n1 k2} y[n1 + Q k2]
-template <int R>
-__device__ __forceinline__ void dit_inv_pass(double2* buf, int H, int S, const double2* __restrict__ T,
-                                             int tid, int nthr) {
-  const int Q = S / R;
-  const int M = 2 * H;
-  const int tstep = M / S;
-  for (int bf = tid; bf < H / R; bf += nthr) {
-    int b = bf / Q, n1 = bf - b * Q;
-    int base = b * S + n1;
-    double2 a[R];
-#pragma unroll
-    for (int q = 0; q < R; ++q) a[q] = buf[fpad(base + q * Q)];
-    if (Q > 1) {
-#pragma unroll
-      for (int q = 1; q < R; ++q) a[q] = cmulc(a[q], twiddle(T, n1 * q * tstep, H));
-    }
-    dftR<R, true>(a);
-#pragma unroll
-    for (int q = 0; q < R; ++q) buf[fpad(base + q * Q)] = a[q];
-  }
-}
-
-// Barrier abstraction: all participating threads call sync().
 struct CtaSync {
   __device__ __forceinline__ void operator()() const { __syncthreads(); }
 };
@@ -184,32 +163,28 @@ struct CtaSync {
 // Forward FFT of H points in place (natural -> digit-reversed).  Caller must have
 // synchronized after writing buf; returns after a final barrier.
 template <class Sync>
-__device__ void fft_forward(double2* buf, const FftShape& s, const double2* __restrict__ T,
-                            int tid, int nthr, Sync sync) {
-  int S = s.H;
-  for (int p = 0; p < s.npass; ++p) {
-    int r = s.radix[p];
-    if (r == 8) dif_pass<8>(buf, s.H, S, T, tid, nthr);
-    else if (r == 4) dif_pass<4>(buf, s.H, S, T, tid, nthr);
-    else dif_pass<2>(buf, s.H, S, T, tid, nthr);
-    S /= r;
+__device__ void fft_forward(double2* buf, const FftShape& s, const double2* __restrict__ T, int tid, int nthr,
+                            Sync sync) {
+  int logS = s.logH;
+  for (int p = 0; p < s.n8; ++p) {
+    fft_pass<3, false>(buf, s.H, s.logH, logS, T, tid, nthr);
+    logS -= 3;
     sync();
   }
+  if (s.lastb == 2) { fft_pass<2, false>(buf, s.H, s.logH, logS, T, tid, nthr); sync(); }
+  else if (s.lastb == 1) { fft_pass<1, false>(buf, s.H, s.logH, logS, T, tid, nthr); sync(); }
 }
 
 // Inverse (unnormalized, x H) FFT in place (digit-reversed -> natural).
 template <class Sync>
-__device__ void fft_inverse(double2* buf, const FftShape& s, const double2* __restrict__ T,
-                            int tid, int nthr, Sync sync) {
-  // block sizes seen by the forward passes were H, H/r0, H/(r0 r1), ...; undo last first
-  int sizes[6];
-  int S = s.H;
-  for (int p = 0; p < s.npass; ++p) { sizes[p] = S; S /= s.radix[p]; }
-  for (int p = s.npass - 1; p >= 0; --p) {
-    int r = s.radix[p];
-    if (r == 8) dit_inv_pass<8>(buf, s.H, sizes[p], T, tid, nthr);
-    else if (r == 4) dit_inv_pass<4>(buf, s.H, sizes[p], T, tid, nthr);
-    else dit_inv_pass<2>(buf, s.H, sizes[p], T, tid, nthr);
+__device__ void fft_inverse(double2* buf, const FftShape& s, const double2* __restrict__ T, int tid, int nthr,
+                            Sync sync) {
+  int logS = s.logH - 3 * s.n8;  // block size seen by the last forward pass
+  if (s.lastb == 2) { fft_pass<2, true>(buf, s.H, s.logH, logS, T, tid, nthr); sync(); }
+  else if (s.lastb == 1) { fft_pass<1, true>(buf, s.H, s.logH, logS, T, tid, nthr); sync(); }
+  for (int p = 0; p < s.n8; ++p) {
+    logS += 3;
+    fft_pass<3, true>(buf, s.H, s.logH, logS, T, tid, nthr);
     sync();
   }
 }

@@ -1,6 +1,7 @@
 // ssa_api.cu -- the extern "C" boundary of libssa.so (include/ssa.h).
 // Host-side validation, workspace sizing, twiddle tables and kernel enqueueing only;
-// every arithmetic step of the method runs in the kernels of ssa_kernels.cu.
+// every arithmetic step of the method runs in the kernels (ssa_fft_kernels.cu,
+// ssa_lanczos.cu, ssa_svd.cu).
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdarg.h>
@@ -26,13 +27,13 @@ static ssa_status fail(ssa_status s, const char* fmt, ...) {
 }
 
 static ssa_status cuda_fail(cudaError_t e, const char* what) {
-  cudaGetLastError();  // clear sticky-free errors
+  cudaGetLastError();
   return fail(SSA_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
 }
 
-#define CK(call, what)                               \
-  do {                                               \
-    cudaError_t e_ = (call);                         \
+#define CK(call, what)                                 \
+  do {                                                 \
+    cudaError_t e_ = (call);                           \
     if (e_ != cudaSuccess) return cuda_fail(e_, what); \
   } while (0)
 
@@ -41,9 +42,9 @@ struct ssa_plan_s {
 };
 
 static int round_up(int x, int m) { return (x + m - 1) / m * m; }
-// Golub-Kahan QR on an m x m bidiagonal takes ~2 sweeps per value (<= 2 m^2 rotations per
-// side); 6 (m+2)^2 leaves ample room.  Overflow is reported as SSA_ERR_INTERNAL per series.
-static int rot_cap(int m_max) { return 6 * (m_max + 2) * (m_max + 2) + 1024; }
+// Golub-Kahan QR on an m x m bidiagonal takes ~2 sweeps per value, i.e. about m^2
+// rotations per side; 2 m^2 + 8 m + 1024 leaves room.  Overflow -> SSA_ERR_INTERNAL.
+static int rot_cap(int m_max) { return 2 * m_max * m_max + 8 * m_max + 1024; }
 
 extern "C" ssa_status ssa_options_default(ssa_options* opt) {
   if (!opt) return fail(SSA_ERR_INVALID_ARGUMENT, "opt is NULL");
@@ -69,11 +70,12 @@ static std::vector<double2> make_twiddles(int64_t M) {
 }
 
 static void free_plan(Plan& p) {
-  void* ptrs[] = {p.d_tw, p.d_spec, p.d_U, p.d_V, p.d_rot, p.d_pq, p.d_info, p.d_counter,
-                  p.d_series, p.d_sigma, p.d_Uout, p.d_Vout, p.d_recon, p.d_hscratch};
+  void* ptrs[] = {p.d_tw, p.d_spec, p.d_U, p.d_V, p.d_ab, p.d_state, p.d_tgk, p.d_rot, p.d_vecs, p.d_coef,
+                  p.d_info, p.d_counters, p.d_hscratch, p.d_prof, p.d_series, p.d_sigma, p.d_Uout, p.d_Vout,
+                  p.d_recon};
   for (void* q : ptrs)
     if (q) cudaFree(q);
-  for (int i = 0; i < 6; ++i)
+  for (int i = 0; i < 2 * Plan::kPhases; ++i)
     if (p.ev[i]) cudaEventDestroy(p.ev[i]);
 }
 
@@ -88,6 +90,62 @@ static ssa_status alloc(void** ptr, size_t bytes, const char* what) {
   return SSA_OK;
 }
 
+// Bytes of per-series decompose storage (bases, spectrum, B, Ritz coefficients).
+static size_t per_series_bytes(const Plan& p) {
+  size_t s = (size_t)(p.m_max + 1) * (p.ldL + p.ldK) * 8;
+  s += (size_t)(p.H + 1) * 16;
+  s += (size_t)2 * (p.m_max + 3) * 8 + 8 * 4;
+  s += (size_t)2 * (p.m_max + 2) * p.k * 8;
+  return s;
+}
+
+static ssa_status create_decompose_workspace(Plan& p, const cudaDeviceProp& prop) {
+  ssa_status st;
+  cudaError_t e;
+  const int k = p.k;
+  if (k > ssa::kMaxK) return fail(SSA_ERR_UNSUPPORTED, "k = %d > %d not supported by the batched decompose", k, ssa::kMaxK);
+  p.smem_lanczos = ssa::lanczos_smem_bytes((int)p.H, p.ldL, p.ldK, p.m_max, k);
+  p.smem_ritz = ssa::ritz_smem_bytes(p.ldL, p.ldK, k);
+  if (p.smem_lanczos > (size_t)prop.sharedMemPerBlockOptin)
+    return fail(SSA_ERR_UNSUPPORTED, "decompose needs %zu B shared memory > %zu", p.smem_lanczos,
+                (size_t)prop.sharedMemPerBlockOptin);
+  if ((e = ssa::lanczos_set_attributes(p.smem_lanczos)) != cudaSuccess) return cuda_fail(e, "lanczos attributes");
+  if ((e = ssa::svd_ritz_set_attributes(p.m_max, p.smem_ritz)) != cudaSuccess) return cuda_fail(e, "svd/ritz attributes");
+  int per_sm = (int)std::max<size_t>(1, std::min<size_t>(2, (size_t)prop.sharedMemPerMultiprocessor / (p.smem_lanczos + 1024)));
+  // chunk: as many series as fit in ~60% of free memory (env SSA_MAX_CHUNK caps it)
+  size_t fr = 0, tot = 0;
+  CK(cudaMemGetInfo(&fr, &tot), "cudaMemGetInfo");
+  size_t per = per_series_bytes(p);
+  int64_t fit = (int64_t)((double)fr * 0.6 / (double)per);
+  int64_t chunk = std::min<int64_t>(p.batch, std::max<int64_t>(1, fit));
+  if (const char* env = getenv("SSA_MAX_CHUNK")) chunk = std::max<int64_t>(1, std::min<int64_t>(chunk, atoll(env)));
+  p.chunk = (int)chunk;
+  p.lanczos_slots = (int)std::min<int64_t>(chunk, (int64_t)p.sms * per_sm);
+  if (const char* env = getenv("SSA_LANCZOS_SLOTS")) p.lanczos_slots = std::max(1, std::min(p.lanczos_slots, atoi(env)));
+  p.svd_slots = (int)std::min<int64_t>(chunk, (int64_t)p.sms * ssa::kSvdWarpsPerCta);
+  p.ritz_slots = (int)std::min<int64_t>(chunk, (int64_t)p.sms * 2);
+  p.rot_cap = rot_cap(p.m_max);
+  size_t C = (size_t)chunk;
+  if ((st = alloc((void**)&p.d_U, C * (p.m_max + 1) * p.ldL * 8, "U bases")) != SSA_OK) return st;
+  if ((st = alloc((void**)&p.d_V, C * (p.m_max + 1) * p.ldK * 8, "V bases")) != SSA_OK) return st;
+  if ((st = alloc((void**)&p.d_spec, C * (p.H + 1) * 16, "spectra")) != SSA_OK) return st;
+  if ((st = alloc((void**)&p.d_ab, C * 2 * (p.m_max + 3) * 8, "bidiagonals")) != SSA_OK) return st;
+  if ((st = alloc((void**)&p.d_state, C * 8 * sizeof(int), "series state")) != SSA_OK) return st;
+  if ((st = alloc((void**)&p.d_coef, C * 2 * (p.m_max + 2) * k * 8, "Ritz coefficients")) != SSA_OK) return st;
+  if ((st = alloc((void**)&p.d_tgk, (size_t)p.lanczos_slots * k * (2 * p.m_max + 2) * 8, "TGK scratch")) != SSA_OK)
+    return st;
+  if ((st = alloc((void**)&p.d_rot, (size_t)p.svd_slots * 6 * p.rot_cap * 8, "rotation records")) != SSA_OK) return st;
+  if ((st = alloc((void**)&p.d_vecs, (size_t)p.svd_slots * 2 * k * (p.m_max + 2) * 8, "P/Q columns")) != SSA_OK)
+    return st;
+  if ((st = alloc((void**)&p.d_info, (size_t)p.batch * sizeof(ssa_series_info), "info")) != SSA_OK) return st;
+  if ((st = alloc((void**)&p.d_counters, 16 * sizeof(int), "counters")) != SSA_OK) return st;
+  if (p.opt.reserved & 1) {
+    if ((st = alloc((void**)&p.d_prof, 8 * sizeof(unsigned long long), "profile counters")) != SSA_OK) return st;
+    CK(cudaMemset(p.d_prof, 0, 8 * sizeof(unsigned long long)), "memset");
+  }
+  return SSA_OK;
+}
+
 extern "C" ssa_status ssa_plan_create(int64_t N, int64_t L, int32_t k, int64_t batch, const ssa_options* opt,
                                       int device, ssa_plan_t* out) {
   if (!out) return fail(SSA_ERR_INVALID_ARGUMENT, "out is NULL");
@@ -99,6 +157,7 @@ extern "C" ssa_status ssa_plan_create(int64_t N, int64_t L, int32_t k, int64_t b
   if (k < 0 || k > std::min(L, K))
     return fail(SSA_ERR_INVALID_ARGUMENT, "k = %d outside [1, min(L,K) = %lld]", k, (long long)std::min(L, K));
   if (batch < 1) return fail(SSA_ERR_INVALID_ARGUMENT, "batch = %lld < 1", (long long)batch);
+  if (batch > 0x7fffffff) return fail(SSA_ERR_INVALID_ARGUMENT, "batch = %lld too large", (long long)batch);
   ssa_options o;
   ssa_options_default(&o);
   if (opt) o = *opt;
@@ -127,26 +186,24 @@ extern "C" ssa_status ssa_plan_create(int64_t N, int64_t L, int32_t k, int64_t b
   p.sms = prop.multiProcessorCount;
   int64_t mn = std::min(L, K);
   int64_t mm = o.max_steps > 0 ? o.max_steps : std::max<int64_t>(256, 8 * (int64_t)k);
-  p.m_max = (int32_t)std::min(mm, mn);
+  p.m_max = (int32_t)std::max<int64_t>(k, std::min(mm, mn));
   p.ldL = round_up((int)L, 16);
   p.ldK = round_up((int)K, 16);
 
   ssa_status st = SSA_OK;
-  for (int i = 0; i < 6; ++i) {
+  for (int i = 0; i < 2 * Plan::kPhases; ++i) {
     e = cudaEventCreate(&p.ev[i]);
     if (e != cudaSuccess) { st = cuda_fail(e, "cudaEventCreate"); goto bad; }
   }
   {
-  std::vector<double2> tw = make_twiddles(M);
-  if ((st = alloc((void**)&p.d_tw, tw.size() * sizeof(double2), "twiddles")) != SSA_OK) goto bad;
-  e = cudaMemcpy(p.d_tw, tw.data(), tw.size() * sizeof(double2), cudaMemcpyHostToDevice);
-  if (e != cudaSuccess) { st = cuda_fail(e, "twiddle upload"); goto bad; }
-  }
-  {
+    std::vector<double2> tw = make_twiddles(M);
+    if ((st = alloc((void**)&p.d_tw, tw.size() * sizeof(double2), "twiddles")) != SSA_OK) goto bad;
+    e = cudaMemcpy(p.d_tw, tw.data(), tw.size() * sizeof(double2), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) { st = cuda_fail(e, "twiddle upload"); goto bad; }
     const char* which = "";
     e = ssa::fft_set_attributes((int)H, &which);
     if (e != cudaSuccess) {
-      st = fail(SSA_ERR_CUDA, "cudaFuncSetAttribute(%s, %zu B smem): %s", which, (size_t)ssa::fpad_bytes((int)H),
+      st = fail(SSA_ERR_CUDA, "cudaFuncSetAttribute(%s, %zu B smem): %s", which, ssa::fpad_bytes((int)H),
                 cudaGetErrorString(e));
       cudaGetLastError();
       goto bad;
@@ -157,30 +214,7 @@ extern "C" ssa_status ssa_plan_create(int64_t N, int64_t L, int32_t k, int64_t b
     if ((st = alloc((void**)&p.d_hscratch, (size_t)p.hank_slots * (H + 1) * 16, "hankelization scratch")) != SSA_OK)
       goto bad;
   }
-
-  if (k > 0) {
-    if (k > 32) { st = fail(SSA_ERR_UNSUPPORTED, "k = %d > 32 not supported by the batched decompose", k); goto bad; }
-    p.smem_lanczos = ssa::lanczos_smem_bytes((int)H, p.ldL, p.ldK, p.m_max, k);
-    if (p.smem_lanczos > (size_t)prop.sharedMemPerBlockOptin) {
-      st = fail(SSA_ERR_UNSUPPORTED, "decompose needs %zu B shared memory > %zu", p.smem_lanczos,
-                (size_t)prop.sharedMemPerBlockOptin);
-      goto bad;
-    }
-    e = ssa::lanczos_set_attributes(p.smem_lanczos);
-    if (e != cudaSuccess) { st = cuda_fail(e, "lanczos attributes"); goto bad; }
-    int per_sm = (int)std::max<size_t>(1, std::min<size_t>(2, (size_t)prop.sharedMemPerMultiprocessor / (p.smem_lanczos + 1024)));
-    p.slots = (int)std::min<int64_t>(batch, (int64_t)p.sms * per_sm);
-    size_t sU = (size_t)(p.m_max + 1) * p.ldL, sV = (size_t)(p.m_max + 1) * p.ldK;
-    size_t cap = (size_t)rot_cap(p.m_max);  // rotation records per side
-    p.d_U = nullptr;
-    if ((st = alloc((void**)&p.d_U, sU * p.slots * 8, "U basis")) != SSA_OK) goto bad;
-    if ((st = alloc((void**)&p.d_V, sV * p.slots * 8, "V basis")) != SSA_OK) goto bad;
-    if ((st = alloc((void**)&p.d_rot, cap * 6 * p.slots * 8, "rotation records")) != SSA_OK) goto bad;
-    if ((st = alloc((void**)&p.d_pq, (size_t)2 * (p.m_max + 2) * k * p.slots * 8, "Ritz coefficients")) != SSA_OK) goto bad;
-    if ((st = alloc((void**)&p.d_spec, (size_t)batch * (H + 1) * 16, "spectra")) != SSA_OK) goto bad;
-    if ((st = alloc((void**)&p.d_info, (size_t)batch * sizeof(ssa_series_info), "info")) != SSA_OK) goto bad;
-    if ((st = alloc((void**)&p.d_counter, 16, "counter")) != SSA_OK) goto bad;
-  }
+  if (k > 0 && (st = create_decompose_workspace(p, prop)) != SSA_OK) goto bad;
   *out = ps;
   return SSA_OK;
 bad:
@@ -202,15 +236,26 @@ extern "C" int64_t ssa_plan_launch_count(ssa_plan_t plan) { return plan ? plan->
 
 static cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// events around one phase: ph in [0, kPhases)
+struct PhaseTimer {
+  Plan& p;
+  int ph;
+  cudaStream_t s;
+  PhaseTimer(Plan& p_, int ph_, cudaStream_t s_) : p(p_), ph(ph_), s(s_) { cudaEventRecord(p.ev[2 * ph], s); }
+  ~PhaseTimer() {
+    cudaEventRecord(p.ev[2 * ph + 1], s);
+    p.ev_used[ph] = true;
+  }
+};
+
 extern "C" ssa_status ssa_spectrum(ssa_plan_t plan, const double* d_series, double* d_spec, void* stream) {
   if (!plan || !d_series || !d_spec) return fail(SSA_ERR_INVALID_ARGUMENT, "NULL argument");
   if (((uintptr_t)d_spec) & 15) return fail(SSA_ERR_INVALID_ARGUMENT, "d_spec must be 16-byte aligned");
   Plan& p = plan->p;
   CK(cudaSetDevice(p.device), "cudaSetDevice");
-  CK(cudaEventRecord(p.ev[0], S(stream)), "event");
-  CK(ssa::launch_spectrum(p, d_series, reinterpret_cast<double2*>(d_spec), S(stream)), "spectrum launch");
-  CK(cudaEventRecord(p.ev[1], S(stream)), "event");
-  p.ev_used[0] = true;
+  PhaseTimer pt(p, 0, S(stream));
+  CK(ssa::launch_spectrum(p, d_series, reinterpret_cast<double2*>(d_spec), (int)p.batch, S(stream)),
+     "spectrum launch");
   p.launches += 1;
   return SSA_OK;
 }
@@ -235,10 +280,8 @@ extern "C" ssa_status ssa_hankelize(ssa_plan_t plan, const double* d_sigma, cons
   Plan& p = plan->p;
   if ((int64_t)p.batch * nterms > (int64_t)0x7fffffff) return fail(SSA_ERR_INVALID_ARGUMENT, "batch*nterms too large");
   CK(cudaSetDevice(p.device), "cudaSetDevice");
-  CK(cudaEventRecord(p.ev[4], S(stream)), "event");
+  PhaseTimer pt(p, 4, S(stream));
   CK(ssa::launch_hankelize(p, d_sigma, d_U, d_V, nterms, d_out, S(stream)), "hankelize launch");
-  CK(cudaEventRecord(p.ev[5], S(stream)), "event");
-  p.ev_used[2] = true;
   p.launches += 1;
   return SSA_OK;
 }
@@ -250,33 +293,41 @@ extern "C" ssa_status ssa_decompose(ssa_plan_t plan, const double* d_series, dou
   if (p.k < 1) return fail(SSA_ERR_INVALID_ARGUMENT, "plan was created with k = 0");
   CK(cudaSetDevice(p.device), "cudaSetDevice");
   cudaStream_t s = S(stream);
-  CK(cudaEventRecord(p.ev[0], s), "event");
-  CK(ssa::launch_spectrum(p, d_series, p.d_spec, s), "spectrum launch");
-  CK(cudaEventRecord(p.ev[1], s), "event");
-  p.ev_used[0] = true;
-  CK(cudaMemsetAsync(p.d_counter, 0, sizeof(int), s), "counter reset");
-  ssa::LanczosArgs a;
+  ssa::DecomposeArgs a;
   a.N = (int)p.N; a.L = (int)p.L; a.K = (int)p.K; a.M = (int)p.M; a.H = (int)p.H; a.k = p.k;
   a.m_max = p.m_max; a.ldL = p.ldL; a.ldK = p.ldK;
-  a.check_every = p.opt.check_every; a.reorth_mode = p.opt.reorth; a.batch = (int)p.batch;
+  a.check_every = p.opt.check_every; a.reorth_mode = p.opt.reorth;
   a.tol = p.opt.tol; a.seed = p.opt.seed;
   a.series = d_series; a.spec = p.d_spec; a.tw = p.d_tw;
-  a.Ubase = p.d_U; a.Vbase = p.d_V;
-  a.slot_stride_U = (size_t)(p.m_max + 1) * p.ldL;
-  a.slot_stride_V = (size_t)(p.m_max + 1) * p.ldK;
-  a.rot_cap = rot_cap(p.m_max);
-  a.rot = p.d_rot;
-  a.slot_stride_rot = (size_t)a.rot_cap * 6;
-  a.pq = p.d_pq;
-  a.slot_stride_pq = (size_t)2 * (p.m_max + 2) * p.k;
+  a.U = p.d_U; a.V = p.d_V; a.ab = p.d_ab; a.state = p.d_state;
+  a.tgk = p.d_tgk; a.tgk_stride = (size_t)p.k * (2 * p.m_max + 2);
+  a.rot = p.d_rot; a.rot_cap = p.rot_cap; a.svd_slots = p.svd_slots; a.vecs = p.d_vecs; a.coef = p.d_coef;
   a.sigma = d_sigma; a.Uout = d_U; a.Vout = d_V;
   a.info = d_info ? d_info : p.d_info;
-  a.counter = p.d_counter;
-  CK(cudaEventRecord(p.ev[2], s), "event");
-  CK(ssa::launch_lanczos(p, a, s), "lanczos launch");
-  CK(cudaEventRecord(p.ev[3], s), "event");
-  p.ev_used[1] = true;
-  p.launches += 2;
+  a.counters = p.d_counters;
+  a.prof = p.d_prof;
+  for (int64_t b0 = 0; b0 < p.batch; b0 += p.chunk) {
+    a.b0 = (int)b0;
+    a.nb = (int)std::min<int64_t>(p.chunk, p.batch - b0);
+    CK(cudaMemsetAsync(p.d_counters, 0, 4 * sizeof(int), s), "counter reset");
+    {
+      PhaseTimer pt(p, 0, s);
+      CK(ssa::launch_spectrum(p, d_series + b0 * p.N, p.d_spec, a.nb, s), "spectrum launch");
+    }
+    {
+      PhaseTimer pt(p, 1, s);
+      CK(ssa::launch_lanczos(p, a, s), "lanczos launch");
+    }
+    {
+      PhaseTimer pt(p, 2, s);
+      CK(ssa::launch_bidiag_svd(p, a, s), "bidiag svd launch");
+    }
+    {
+      PhaseTimer pt(p, 3, s);
+      CK(ssa::launch_ritz(p, a, s), "ritz launch");
+    }
+    p.launches += 4;
+  }
   return SSA_OK;
 }
 
@@ -323,17 +374,46 @@ extern "C" ssa_status ssa_run_host(ssa_plan_t plan, const double* h_series, doub
   return SSA_OK;
 }
 
-extern "C" ssa_status ssa_plan_phase_ms(ssa_plan_t plan, double out_ms[3]) {
+extern "C" ssa_status ssa_plan_phase_ms(ssa_plan_t plan, double out_ms[5]) {
   if (!plan || !out_ms) return fail(SSA_ERR_INVALID_ARGUMENT, "NULL argument");
   Plan& p = plan->p;
   CK(cudaSetDevice(p.device), "cudaSetDevice");
-  for (int i = 0; i < 3; ++i) {
+  for (int i = 0; i < Plan::kPhases; ++i) {
     out_ms[i] = -1.0;
     if (!p.ev_used[i]) continue;
     CK(cudaEventSynchronize(p.ev[2 * i + 1]), "event sync");
     float ms = 0.f;
     CK(cudaEventElapsedTime(&ms, p.ev[2 * i], p.ev[2 * i + 1]), "event elapsed");
     out_ms[i] = ms;
+  }
+  return SSA_OK;
+}
+
+extern "C" ssa_status ssa_plan_profile(ssa_plan_t plan, int64_t out[8]) {
+  if (!plan || !out) return fail(SSA_ERR_INVALID_ARGUMENT, "NULL argument");
+  Plan& p = plan->p;
+  if (!p.d_prof) return fail(SSA_ERR_INVALID_ARGUMENT, "plan was not created with profiling (options.reserved & 1)");
+  CK(cudaSetDevice(p.device), "cudaSetDevice");
+  CK(cudaMemcpy(out, p.d_prof, 8 * sizeof(int64_t), cudaMemcpyDeviceToHost), "D2H profile");
+  return SSA_OK;
+}
+
+extern "C" ssa_status ssa_plan_bidiagonals(ssa_plan_t plan, double* h_alpha, double* h_beta, int32_t* h_steps) {
+  if (!plan || !h_alpha || !h_beta || !h_steps) return fail(SSA_ERR_INVALID_ARGUMENT, "NULL argument");
+  Plan& p = plan->p;
+  if (p.k < 1) return fail(SSA_ERR_INVALID_ARGUMENT, "plan was created with k = 0");
+  CK(cudaSetDevice(p.device), "cudaSetDevice");
+  CK(cudaDeviceSynchronize(), "sync");
+  const int64_t nb = std::min<int64_t>(p.chunk, p.batch - (p.batch - 1) / p.chunk * p.chunk);
+  const size_t w = (size_t)p.m_max + 3;
+  std::vector<double> ab((size_t)nb * 2 * w);
+  std::vector<int> st((size_t)nb * 8);
+  CK(cudaMemcpy(ab.data(), p.d_ab, ab.size() * 8, cudaMemcpyDeviceToHost), "D2H ab");
+  CK(cudaMemcpy(st.data(), p.d_state, st.size() * 4, cudaMemcpyDeviceToHost), "D2H state");
+  for (int64_t b = 0; b < nb; ++b) {
+    memcpy(h_alpha + b * w, &ab[(size_t)b * 2 * w], w * 8);
+    memcpy(h_beta + b * w, &ab[(size_t)b * 2 * w + w], w * 8);
+    h_steps[b] = st[(size_t)b * 8];
   }
   return SSA_OK;
 }

@@ -1,0 +1,182 @@
+// ssa_fft_kernels.cu -- FFT-based building blocks of the fast Basic-SSA hot path.
+//
+//  spectrum_kernel   F^ = rfft(f, M)                     Alg. 2 l.1-2
+//  matvec_kernel     y = X x / X^T x by FFT correlation  Alg. 2/3
+//  hankelize_kernel  g = sigma irfft(rfft u rfft v) / c  sec 5, Alg. 4
+//
+// Correlation form (R1): with F^ = rfft(f, M) for any M >= N,
+//   (X v)_i   = sum_j f_{i+j} v_j = irfft(F^ conj(rfft(v, M)))[i],  i < L
+//   (X^T u)_j = sum_i f_{i+j} u_i = irfft(F^ conj(rfft(u, M)))[j],  j < K
+// which is Alg. 2 / Alg. 3 (circulant embedding + backward identity) with the reversal
+// folded into the conjugate and the output slice of Alg. 3 read as p'_L..p'_N.
+#include "device_common.cuh"
+
+namespace ssa {
+
+__global__ void __launch_bounds__(kThreads) spectrum_kernel(const double* __restrict__ series, int N, int H,
+                                                            const double2* __restrict__ T, double2* __restrict__ spec) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double2* buf = reinterpret_cast<double2*>(smem_raw);
+  const FftShape sh = make_shape(H);
+  const int b = blockIdx.x;
+  const double* f = series + (size_t)b * N;
+  double2* out = spec + (size_t)b * (H + 1);
+  for (int n = threadIdx.x; n < H; n += blockDim.x) {
+    int i0 = 2 * n;
+    double a = (i0 < N) ? f[i0] : 0.0;
+    double c = (i0 + 1 < N) ? f[i0 + 1] : 0.0;
+    buf[fpad(n)] = make_double2(a, c);
+  }
+  __syncthreads();
+  fft_forward(buf, sh, T, threadIdx.x, blockDim.x, CtaSync());
+  for (int p = threadIdx.x; p <= (H >> 1); p += blockDim.x) {
+    double2 Xp, Xq;
+    int pr, qr;
+    real_pair(buf, sh, T, p, Xp, Xq, pr, qr);
+    out[p] = Xp;
+    out[H - p] = Xq;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) matvec_kernel(const double2* __restrict__ spec, int H, int n_in, int n_out,
+                                                          const double2* __restrict__ T, const double* __restrict__ x,
+                                                          double* __restrict__ y) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double2* buf = reinterpret_cast<double2*>(smem_raw);
+  const FftShape sh = make_shape(H);
+  const int b = blockIdx.x;
+  const double* xb = x + (size_t)b * n_in;
+  double* yb = y + (size_t)b * n_out;
+  correlate_cta(
+      buf, sh, T, spec + (size_t)b * (H + 1), n_in, n_out, [&](int i) { return __ldg(xb + i); },
+      [&](int t, double v) { yb[t] = v; });
+}
+
+// g_t = sigma * (u' * v')_t / c_t, c_t = min(t, L, K, N-t+1), t = 1..N  (PAPER.md:751-785,
+// Alg. 4 PAPER.md:807-824 with the weights read as division, R2).
+// Two shared-memory buffers when they fit (H <= kMaxHankelSmemH); otherwise (BIG) the
+// post-processed spectrum of u goes to a per-CTA global scratch row (L2-resident) and the
+// grid is persistent over terms.
+template <bool BIG>
+__global__ void __launch_bounds__(kThreads) hankelize_kernel(const double* __restrict__ sigma,
+                                                             const double* __restrict__ U,
+                                                             const double* __restrict__ V, size_t nterm_total, int N,
+                                                             int L, int K, int H, const double2* __restrict__ T,
+                                                             double* __restrict__ out, double2* gscratch) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double2* bufB = reinterpret_cast<double2*>(smem_raw);
+  double2* bufA = BIG ? nullptr : bufB + fpad_size(H);
+  double2* Xu = BIG ? gscratch + (size_t)blockIdx.x * (H + 1) : nullptr;
+  const FftShape sh = make_shape(H);
+  const int mn = L < K ? L : K;
+  for (size_t term = blockIdx.x; term < nterm_total; term += gridDim.x) {
+    const double* u = U + term * L;
+    const double* v = V + term * K;
+    const double sg = __ldg(sigma + term);
+    if (BIG) {
+      __syncthreads();
+      for (int n = threadIdx.x; n < H; n += blockDim.x) {
+        int i0 = 2 * n;
+        bufB[fpad(n)] = make_double2(i0 < L ? __ldg(u + i0) : 0.0, i0 + 1 < L ? __ldg(u + i0 + 1) : 0.0);
+      }
+      __syncthreads();
+      fft_forward(bufB, sh, T, threadIdx.x, blockDim.x, CtaSync());
+      for (int p = threadIdx.x; p <= (H >> 1); p += blockDim.x) {
+        double2 Up, Uq;
+        int pr, qr;
+        real_pair(bufB, sh, T, p, Up, Uq, pr, qr);
+        Xu[p] = Up;
+        Xu[H - p] = Uq;
+      }
+      __syncthreads();
+      for (int n = threadIdx.x; n < H; n += blockDim.x) {
+        int i0 = 2 * n;
+        bufB[fpad(n)] = make_double2(i0 < K ? __ldg(v + i0) : 0.0, i0 + 1 < K ? __ldg(v + i0 + 1) : 0.0);
+      }
+      __syncthreads();
+      fft_forward(bufB, sh, T, threadIdx.x, blockDim.x, CtaSync());
+      for (int p = threadIdx.x; p <= (H >> 1); p += blockDim.x) {
+        double2 Vp, Vq;
+        int pr, qr;
+        real_pair(bufB, sh, T, p, Vp, Vq, pr, qr);
+        inv_pair(bufB, T, H, p, pr, qr, cmul(Xu[p], Vp), cmul(Xu[H - p], Vq));
+      }
+    } else {
+      __syncthreads();
+      for (int n = threadIdx.x; n < H; n += blockDim.x) {
+        int i0 = 2 * n;
+        bufA[fpad(n)] = make_double2(i0 < L ? __ldg(u + i0) : 0.0, i0 + 1 < L ? __ldg(u + i0 + 1) : 0.0);
+        bufB[fpad(n)] = make_double2(i0 < K ? __ldg(v + i0) : 0.0, i0 + 1 < K ? __ldg(v + i0 + 1) : 0.0);
+      }
+      __syncthreads();
+      fft_forward(bufA, sh, T, threadIdx.x, blockDim.x, CtaSync());
+      fft_forward(bufB, sh, T, threadIdx.x, blockDim.x, CtaSync());
+      for (int p = threadIdx.x; p <= (H >> 1); p += blockDim.x) {
+        double2 Up, Uq, Vp, Vq;
+        int pr, qr;
+        real_pair(bufA, sh, T, p, Up, Uq, pr, qr);
+        real_pair(bufB, sh, T, p, Vp, Vq, pr, qr);
+        inv_pair(bufB, T, H, p, pr, qr, cmul(Up, Vp), cmul(Uq, Vq));
+      }
+    }
+    __syncthreads();
+    fft_inverse(bufB, sh, T, threadIdx.x, blockDim.x, CtaSync());
+    const double scale = sg / (double)H;
+    double* g = out + term * N;
+    for (int t = threadIdx.x; t < N; t += blockDim.x) {
+      double2 z = bufB[fpad(t >> 1)];
+      int k1 = t + 1;  // 1-based
+      int c = k1;
+      if (c > mn) c = mn;
+      if (N - k1 + 1 < c) c = N - k1 + 1;
+      g[t] = ((t & 1) ? z.y : z.x) * scale / (double)c;
+    }
+  }
+}
+
+static size_t fft_smem(int H) { return (size_t)fpad_size(H) * 16; }
+
+cudaError_t fft_set_attributes(int H, const char** which) {
+  cudaError_t e;
+  size_t s1 = fft_smem(H), s2 = 2 * fft_smem(H);
+  *which = "spectrum_kernel";
+  if ((e = cudaFuncSetAttribute(spectrum_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1))) return e;
+  *which = "matvec_kernel";
+  if ((e = cudaFuncSetAttribute(matvec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1))) return e;
+  *which = "hankelize_kernel<BIG>";
+  if ((e = cudaFuncSetAttribute(hankelize_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1))) return e;
+  *which = "hankelize_kernel";
+  if (H <= kMaxHankelSmemH)
+    if ((e = cudaFuncSetAttribute(hankelize_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2)))
+      return e;
+  return cudaSuccess;
+}
+
+cudaError_t launch_spectrum(const Plan& p, const double* series, double2* spec, int nseries, cudaStream_t s) {
+  spectrum_kernel<<<(unsigned)nseries, kThreads, fft_smem((int)p.H), s>>>(series, (int)p.N, (int)p.H, p.d_tw, spec);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_matvec(const Plan& p, const double2* spec, const double* x, double* y, int transpose,
+                          cudaStream_t s) {
+  int n_in = transpose ? (int)p.L : (int)p.K;
+  int n_out = transpose ? (int)p.K : (int)p.L;
+  matvec_kernel<<<(unsigned)p.batch, kThreads, fft_smem((int)p.H), s>>>(spec, (int)p.H, n_in, n_out, p.d_tw, x, y);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_hankelize(const Plan& p, const double* sigma, const double* U, const double* V, int nterms,
+                             double* out, cudaStream_t s) {
+  size_t total = (size_t)p.batch * nterms;
+  if (p.H <= kMaxHankelSmemH) {
+    hankelize_kernel<false><<<(unsigned)total, kThreads, 2 * fft_smem((int)p.H), s>>>(
+        sigma, U, V, total, (int)p.N, (int)p.L, (int)p.K, (int)p.H, p.d_tw, out, nullptr);
+  } else {
+    size_t grid = total < (size_t)p.hank_slots ? total : (size_t)p.hank_slots;
+    hankelize_kernel<true><<<(unsigned)grid, kThreads, fft_smem((int)p.H), s>>>(
+        sigma, U, V, total, (int)p.N, (int)p.L, (int)p.K, (int)p.H, p.d_tw, out, p.d_hscratch);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace ssa

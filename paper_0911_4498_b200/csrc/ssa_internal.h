@@ -1,5 +1,5 @@
-// ssa_internal.h -- plan layout and launcher declarations shared by ssa_api.cu and
-// ssa_kernels.cu (library-internal; not part of the C-ABI).
+// ssa_internal.h -- plan layout and launcher declarations shared by ssa_api.cu and the
+// kernel translation units (library-internal; not part of the C-ABI).
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -9,34 +9,42 @@
 namespace ssa {
 
 constexpr int kThreads = 256;          // threads per CTA for every kernel
-constexpr int kWarps = kThreads / 32;  // worker warps in the Lanczos kernel
+constexpr int kWarps = kThreads / 32;  // warps per CTA
 constexpr int kStages = 3;             // TMA ring depth per warp (basis streaming)
 constexpr int kMaxSmemH = 8192;        // largest H = M/2 held in one CTA's shared memory
 constexpr int kMaxHankelSmemH = 4096;  // largest H with both hankelization buffers in SMEM
+constexpr int kMaxK = 32;              // largest k of the batched decompose
 
 inline size_t fpad_bytes(int H) { return (size_t)(H + (H >> 3) + 1) * 16; }
 
-struct LanczosArgs {
+// Arguments of the three decompose kernels (lanczos -> bidiag SVD -> Ritz).  Per-series
+// storage covers one chunk of nb series [b0, b0+nb) of the call.
+struct DecomposeArgs {
   int N, L, K, M, H, k, m_max, ldL, ldK;
-  int check_every, reorth_mode, batch;
+  int check_every, reorth_mode;
+  int b0, nb;
   double tol;
   uint64_t seed;
-  const double* series;     // [batch][N]
-  const double2* spec;      // [batch][H+1]
-  const double2* tw;        // [H]
-  double* Ubase;            // per slot: (m_max+1) x ldL
-  double* Vbase;            // per slot: (m_max+1) x ldK
-  size_t slot_stride_U, slot_stride_V;  // doubles
-  double* rot;              // per slot rotation records
-  size_t slot_stride_rot;   // doubles
-  int rot_cap;              // records per side per slot
-  double* pq;               // per slot: P_k ((m_max+1) x k) and Q_k (m_max x k)
-  size_t slot_stride_pq;
-  double* sigma;            // [batch][k]
-  double* Uout;             // [batch][k][L]
-  double* Vout;             // [batch][k][K]
-  ssa_series_info* info;    // [batch] (never NULL: plan scratch if caller passed NULL)
-  int* counter;             // work queue head
+  const double* series;  // caller [batch][N]
+  const double2* spec;   // [nb][H+1]
+  const double2* tw;     // [H]
+  double* U;             // [nb][m_max+1][ldL]  Krylov basis U_{m+1}
+  double* V;             // [nb][m_max+1][ldK]  Krylov basis V_{m+1}
+  double* ab;            // [nb][2][m_max+3]    alpha_j, beta_j (1-based)
+  int* state;            // [nb][8]: m, converged, breakdown, reorth_extra, restarts, bad, checks, -
+  double* tgk;           // per Lanczos CTA slot: k * (2 m_max + 2) doubles
+  size_t tgk_stride;
+  double* rot;           // per SVD warp slot: 2 sides x rot_cap x 3 doubles
+  int rot_cap;
+  int svd_slots;         // warps with rotation / vector scratch
+  double* vecs;          // per SVD warp slot: 2k x (m_max+2) doubles
+  double* coef;          // [nb][2][m_max+2][k]: P_k rows then Q_k rows (signs folded)
+  double* sigma;         // caller [batch][k]
+  double* Uout;          // caller [batch][k][L]
+  double* Vout;          // caller [batch][k][K]
+  ssa_series_info* info; // [batch]
+  int* counters;         // [4] work-queue heads (lanczos, svd, ritz)
+  unsigned long long* prof;  // nullable, 8 counters
 };
 
 struct Plan {
@@ -48,18 +56,27 @@ struct Plan {
   int32_t m_max = 0;
   int ldL = 0, ldK = 0;
   int sms = 0;
-  int slots = 0;           // persistent CTAs for decompose
-  size_t smem_lanczos = 0;
-  double2* d_tw = nullptr;       // twiddles exp(-2 pi i t / M), t < H
-  double2* d_spec = nullptr;     // [batch][H+1] spectra owned by the plan (decompose)
-  double* d_U = nullptr;         // bases
+  int chunk = 0;               // series per decompose chunk (per-series storage)
+  int lanczos_slots = 0;       // persistent CTAs of the Lanczos kernel
+  int svd_slots = 0;           // warps of the SVD kernel
+  int ritz_slots = 0;          // CTAs of the Ritz kernel
+  int rot_cap = 0;
+  size_t smem_lanczos = 0, smem_ritz = 0;
+  double2* d_tw = nullptr;     // twiddles exp(-2 pi i t / M), t < H
+  double2* d_spec = nullptr;   // [chunk][H+1]
+  double* d_U = nullptr;
   double* d_V = nullptr;
+  double* d_ab = nullptr;
+  int* d_state = nullptr;
+  double* d_tgk = nullptr;
   double* d_rot = nullptr;
-  double* d_pq = nullptr;
+  double* d_vecs = nullptr;
+  double* d_coef = nullptr;
   ssa_series_info* d_info = nullptr;
-  int* d_counter = nullptr;
+  int* d_counters = nullptr;
   double2* d_hscratch = nullptr;  // BIG hankelization: per-CTA rfft(u) rows
   int hank_slots = 0;
+  unsigned long long* d_prof = nullptr;  // profiling counters (options.reserved & 1)
   // host-API staging (allocated lazily by ssa_run_host)
   double* d_series = nullptr;
   double* d_sigma = nullptr;
@@ -67,19 +84,26 @@ struct Plan {
   double* d_Vout = nullptr;
   double* d_recon = nullptr;
   int64_t launches = 0;
-  cudaEvent_t ev[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};  // [start,end] x 3 phases
-  bool ev_used[3] = {false, false, false};
+  static constexpr int kPhases = 5;  // spectrum, lanczos, bidiag_svd, ritz, hankelize
+  cudaEvent_t ev[2 * kPhases] = {};
+  bool ev_used[kPhases] = {};
 };
 
-// launchers (ssa_kernels.cu); return cudaGetLastError() after enqueue
-cudaError_t launch_spectrum(const Plan& p, const double* series, double2* spec, cudaStream_t s);
+// launchers; return cudaGetLastError() after enqueue
+cudaError_t launch_spectrum(const Plan& p, const double* series, double2* spec, int nseries, cudaStream_t s);
 cudaError_t launch_matvec(const Plan& p, const double2* spec, const double* x, double* y, int transpose,
                           cudaStream_t s);
 cudaError_t launch_hankelize(const Plan& p, const double* sigma, const double* U, const double* V, int nterms,
                              double* out, cudaStream_t s);
-cudaError_t launch_lanczos(const Plan& p, const LanczosArgs& a, cudaStream_t s);
-size_t lanczos_smem_bytes(int H, int ldL, int ldK, int m_max, int k);
-cudaError_t lanczos_set_attributes(size_t smem);
 cudaError_t fft_set_attributes(int H, const char** which);
+
+size_t lanczos_smem_bytes(int H, int ldL, int ldK, int m_max, int k);
+size_t ritz_smem_bytes(int ldL, int ldK, int k);
+cudaError_t lanczos_set_attributes(size_t smem);
+cudaError_t svd_ritz_set_attributes(int m_max, size_t smem_ritz);
+constexpr int kSvdWarpsPerCta = 8;
+cudaError_t launch_lanczos(const Plan& p, const DecomposeArgs& a, cudaStream_t s);
+cudaError_t launch_bidiag_svd(const Plan& p, const DecomposeArgs& a, cudaStream_t s);
+cudaError_t launch_ritz(const Plan& p, const DecomposeArgs& a, cudaStream_t s);
 
 }  // namespace ssa

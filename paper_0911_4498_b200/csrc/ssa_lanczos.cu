@@ -1,0 +1,358 @@
+// ssa_lanczos.cu -- persistent batched Golub-Kahan-Lanczos bidiagonalization with full
+// reorthogonalization (Alg. 1; FRO PAPER.md:388-393), one CTA per
+// series taken from a work queue.
+//
+// Per step j (all on chip except the Krylov basis, which lives in HBM):
+//   A: r = X^T u_j - beta_j v_{j-1}      FFT correlation in shared memory (Alg. 3)
+//      CGS against V_{j-1} (+ DGKS pass)  basis streamed by per-warp TMA bulk rings
+//      alpha_j = |r|, v_j = r / alpha_j   written once to HBM
+//      convergence test on B_{j-1} using alpha_j (tgk_check.cuh), on schedule
+//   B: p = X v_j - alpha_j u_j           FFT correlation (Alg. 2)
+//      CGS against U_j (+ DGKS pass); beta_{j+1} = |p|; u_{j+1} = p / beta_{j+1}
+// Lucky breakdown (alpha or beta < 1e-12 running max) restarts with a seeded random
+// vector orthogonal to the basis and a zero coefficient in B (R11).
+// Output per series: the bases, alpha/beta and the step count m; the bidiagonal SVD and
+// the Ritz assembly are separate kernels (ssa_svd.cu).
+#include "device_common.cuh"
+#include "tgk_check.cuh"
+
+namespace ssa {
+
+struct LSmem {
+  unsigned char* regionA;  // union: FFT buffer | rings + partial dots | TGK arrays
+  double* bufU;            // ldL
+  double* bufV;            // ldK
+  double* h;               // m_max + 2
+  double* alpha;           // m_max + 3 (1-based)
+  double* beta;            // m_max + 3 (1-based)
+  double* red;             // 32
+  int* redi;               // 8 ints
+  double* chk;             // 4 * kMaxK: omega, res, lohi(2k)
+  uint64_t* bars;          // kWarps * kStages
+};
+
+__host__ __device__ inline size_t lanczos_regionA_bytes(int H, int ldL, int ldK, int m_max) {
+  int slab_max = (ldL > ldK ? ldL : ldK) / kWarps;
+  size_t fft = (size_t)fpad_size(H) * 16;
+  size_t rings = (size_t)kWarps * kStages * slab_max * 8 + (size_t)kWarps * (m_max + 2) * 8;
+  size_t tgk = (size_t)2 * (2 * m_max + 2) * 8;
+  size_t r = fft;
+  if (rings > r) r = rings;
+  if (tgk > r) r = tgk;
+  return align16(r);
+}
+
+size_t lanczos_smem_bytes(int H, int ldL, int ldK, int m_max, int k) {
+  (void)k;
+  size_t s = lanczos_regionA_bytes(H, ldL, ldK, m_max);
+  s += align16((size_t)ldL * 8) + align16((size_t)ldK * 8);
+  s += 3 * align16((size_t)(m_max + 3) * 8);
+  s += 32 * 8 + 8 * 4 + 4 * kMaxK * 8;
+  s += (size_t)kWarps * kStages * 8;
+  return align16(s) + 16;
+}
+
+__device__ inline LSmem carve(unsigned char* base, const DecomposeArgs& a) {
+  LSmem s;
+  size_t off = 0;
+  s.regionA = base;
+  off += lanczos_regionA_bytes(a.H, a.ldL, a.ldK, a.m_max);
+  s.bufU = reinterpret_cast<double*>(base + off); off += align16((size_t)a.ldL * 8);
+  s.bufV = reinterpret_cast<double*>(base + off); off += align16((size_t)a.ldK * 8);
+  s.h = reinterpret_cast<double*>(base + off); off += align16((size_t)(a.m_max + 3) * 8);
+  s.alpha = reinterpret_cast<double*>(base + off); off += align16((size_t)(a.m_max + 3) * 8);
+  s.beta = reinterpret_cast<double*>(base + off); off += align16((size_t)(a.m_max + 3) * 8);
+  s.red = reinterpret_cast<double*>(base + off); off += 32 * 8;
+  s.redi = reinterpret_cast<int*>(base + off); off += 8 * 4;
+  s.chk = reinterpret_cast<double*>(base + off); off += 4 * kMaxK * 8;
+  s.bars = reinterpret_cast<uint64_t*>(base + off);
+  return s;
+}
+
+// Counter-based start / restart vectors (R6): splitmix64 of (seed, series, i).
+__device__ __forceinline__ double rng_uniform_pm1(uint64_t seed, uint64_t series, uint64_t i) {
+  uint64_t x = seed ^ (series * 0xD1B54A32D192ED03ull);
+  x += (i + 1) * 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  x ^= x >> 31;
+  return 2.0 * ((double)(x >> 11) * 0x1.0p-53) - 1.0;
+}
+
+// CGS pass(es) of r (SMEM, ld doubles, zero padding) against basis rows [0, nb).
+// Returns the new norm; nrm_in is |r| before.  mode 1: DGKS (second pass iff the norm
+// fell below 1/sqrt(2) of its value), mode 2: always two passes (PAPER.md:388-393,
+// DESIGN.md R9).  Each warp owns a column slab of r and of the basis; the dot products
+// are reduced across warps in a fixed order (deterministic).
+__device__ double reorth(double* r, const double* basis, int nb, int ld, double nrm_in, int mode, const LSmem& sm,
+                         WarpRing& rg, double* part, int pstride, int& extra) {
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int slab = ld / kWarps;
+  double* rw = r + w * slab;
+  const double* bw = basis + (size_t)w * slab;
+  double nrm = nrm_in;
+  for (int pass = 0; pass < 2 && nb > 0; ++pass) {
+    fence_proxy_async_smem();
+    __syncthreads();
+    // pass 1: partial dots of this warp's slab with every basis row
+    stream_rows(bw, ld, nb, false, slab, rg, [&](int row, const double* ch) {
+      double s = 0.0;
+      for (int e = lane; e < slab; e += 32) s = fma(ch[e], rw[e], s);
+      s = warp_sum(s);
+      if (lane == 0) part[w * pstride + row] = s;
+    });
+    __syncthreads();
+    for (int c = threadIdx.x; c < nb; c += blockDim.x) {
+      double s = 0.0;
+      for (int q = 0; q < kWarps; ++q) s += part[q * pstride + c];
+      sm.h[c] = s;
+    }
+    __syncthreads();
+    // pass 2: r -= V h, rows streamed in reverse so the most recently read rows (still
+    // in L2) come first
+    stream_rows(bw, ld, nb, true, slab, rg, [&](int row, const double* ch) {
+      const double hc = sm.h[row];
+      for (int e = lane; e < slab; e += 32) rw[e] = fma(-hc, ch[e], rw[e]);
+    });
+    double ss = 0.0;
+    for (int e = lane; e < slab; e += 32) ss = fma(rw[e], rw[e], ss);
+    double nn = sqrt(block_sum(ss, sm.red));
+    bool again = (pass == 0) && (mode == 2 || nn < 0.70710678118654752 * nrm);
+    nrm = nn;
+    if (!again) break;
+    ++extra;
+  }
+  return nrm;
+}
+
+// Write r * inv into basis row dst (plain coalesced stores), scale r in place.
+__device__ __forceinline__ void normalize_store(double* r, int n, int ld, double inv, double* dst) {
+  for (int t = threadIdx.x; t < ld; t += blockDim.x) {
+    double v = (t < n) ? r[t] * inv : 0.0;
+    r[t] = v;
+    dst[t] = v;
+  }
+  fence_proxy_async_global();
+  __syncthreads();
+}
+
+// Seeded random vector orthogonalized twice against the basis (restart at breakdown).
+// Returns its norm after orthogonalization relative to before (0 if the space is full).
+__device__ double restart_vector(double* r, int n, int ld, const double* basis, int nb, uint64_t seed,
+                                 uint64_t series, uint64_t salt, const LSmem& sm, WarpRing& rg, double* part,
+                                 int pstride) {
+  double ss = 0.0;
+  for (int t = threadIdx.x; t < ld; t += blockDim.x) {
+    double v = (t < n) ? rng_uniform_pm1(seed, series, salt + t) : 0.0;
+    r[t] = v;
+    ss += v * v;
+  }
+  double nrm = sqrt(block_sum(ss, sm.red));
+  int extra = 0;
+  double nn = reorth(r, basis, nb, ld, nrm, 2, sm, rg, part, pstride, extra);
+  return nn / nrm;
+}
+
+__global__ void __launch_bounds__(kThreads, 2) lanczos_kernel(const DecomposeArgs a) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  LSmem sm = carve(smem_raw, a);
+  const int tid = threadIdx.x, w = tid >> 5;
+  const FftShape sh = make_shape(a.H);
+  const int slab_max = (a.ldL > a.ldK ? a.ldL : a.ldK) / kWarps;
+  double2* fbuf = reinterpret_cast<double2*>(sm.regionA);
+  double* rings = reinterpret_cast<double*>(sm.regionA);
+  double* part = rings + (size_t)kWarps * kStages * slab_max;
+  const int pstride = a.m_max + 2;
+  double* tc = reinterpret_cast<double*>(sm.regionA);  // TGK off-diagonals (aliases the rings)
+  double* tc2 = tc + (2 * a.m_max + 2);
+  double* tgk_scr = a.tgk + a.tgk_stride * blockIdx.x;
+
+  WarpRing rg;
+  ring_init(rg, rings + (size_t)w * kStages * slab_max, sm.bars + w * kStages);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+
+  const int L = a.L, K = a.K, k = a.k;
+  unsigned long long pc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  long long t_mark = clock64();
+  auto lap = [&](int slot) {
+    long long t = clock64();
+    pc[slot] += (unsigned long long)(t - t_mark);
+    t_mark = t;
+  };
+
+  while (true) {
+    __syncthreads();
+    if (tid == 0) sm.redi[4] = atomicAdd(a.counters + 0, 1);
+    __syncthreads();
+    const int bl = sm.redi[4];  // series index within the chunk
+    if (bl >= a.nb) break;
+    const int b = a.b0 + bl;
+    const double* f = a.series + (size_t)b * a.N;
+    const double2* spec = a.spec + (size_t)bl * (a.H + 1);
+    double* U = a.U + (size_t)bl * (a.m_max + 1) * a.ldL;
+    double* V = a.V + (size_t)bl * (a.m_max + 1) * a.ldK;
+    double* abg = a.ab + (size_t)bl * 2 * (a.m_max + 3);
+    int* st = a.state + (size_t)bl * 8;
+
+    // ---- non-finite input -> INVALID_ARGUMENT ----
+    int bad = 0;
+    for (int t = tid; t < a.N; t += blockDim.x) bad |= !isfinite(f[t]);
+    if (block_or(bad, sm.redi)) {
+      if (tid == 0) {
+        st[0] = 0; st[1] = 0; st[2] = 0; st[3] = 0; st[4] = 0; st[5] = 1; st[6] = 0;
+      }
+      continue;
+    }
+
+    // ---- Alg. 1 lines 1-2: p0 seeded, beta_1 = |p0|, u_1 = p0 / beta_1, v_0 = 0 ----
+    double ss = 0.0;
+    for (int t = tid; t < a.ldL; t += blockDim.x) {
+      double v = (t < L) ? rng_uniform_pm1(a.seed, (uint64_t)b, (uint64_t)t) : 0.0;
+      sm.bufU[t] = v;
+      ss += v * v;
+    }
+    for (int t = tid; t < a.ldK; t += blockDim.x) sm.bufV[t] = 0.0;
+    double beta1 = sqrt(block_sum(ss, sm.red));
+    if (tid == 0) { sm.beta[1] = beta1; sm.alpha[0] = 0.0; sm.beta[0] = 0.0; }
+    normalize_store(sm.bufU, L, a.ldL, 1.0 / beta1, U);
+
+    double runmax = 0.0, bcur = beta1;
+    int m = 0, converged = 0, breakdown = 0, extra = 0, restarts = 0, checks = 0;
+    int next_check = k;
+    double prev_res = -1.0;
+    int prev_m = 0;
+    const int ce = a.check_every > 0 ? a.check_every : 4;
+
+    for (int j = 1; j <= a.m_max + 1; ++j) {
+      // ---- half-step A (Alg. 1 l.4-5): r = X^T u_j - beta_j v_{j-1}; FRO vs V_{j-1} ----
+      lap(7);
+      const double bj = bcur;  // beta_j (register copy: sm.beta is written by thread 0 only)
+      correlate_cta(
+          fbuf, sh, a.tw, spec, L, K, [&](int i) { return sm.bufU[i]; },
+          [&](int t, double y) { sm.bufV[t] = y - bj * sm.bufV[t]; });
+      __syncthreads();
+      ss = 0.0;
+      for (int t = tid; t < K; t += blockDim.x) ss = fma(sm.bufV[t], sm.bufV[t], ss);
+      double nr = sqrt(block_sum(ss, sm.red));
+      lap(0);
+      double al = reorth(sm.bufV, V, j - 1, a.ldK, nr, a.reorth_mode, sm, rg, part, pstride, extra);
+      if (!(al > 1e-12 * runmax) || al == 0.0) {
+        if (!breakdown) breakdown = j;
+        double q = (j - 1 < K) ? restart_vector(sm.bufV, K, a.ldK, V, j - 1, a.seed, (uint64_t)b,
+                                                ((uint64_t)(++restarts) << 40), sm, rg, part, pstride)
+                               : 0.0;
+        if (q > 1e-8) {
+          ss = 0.0;
+          for (int t = tid; t < K; t += blockDim.x) ss = fma(sm.bufV[t], sm.bufV[t], ss);
+          double nn = sqrt(block_sum(ss, sm.red));
+          normalize_store(sm.bufV, K, a.ldK, 1.0 / nn, V + (size_t)(j - 1) * a.ldK);
+        } else {
+          normalize_store(sm.bufV, K, a.ldK, 0.0, V + (size_t)(j - 1) * a.ldK);
+        }
+        al = 0.0;
+      } else {
+        normalize_store(sm.bufV, K, a.ldK, 1.0 / al, V + (size_t)(j - 1) * a.ldK);
+      }
+      if (tid == 0) sm.alpha[j] = al;
+      runmax = fmax(runmax, al);
+      m = j - 1;
+      lap(1);
+
+      // ---- convergence test on B_m with alpha_{m+1} = al (R7) ----
+      const bool last = (m >= a.m_max);
+      if (m >= k && (m >= next_check || last)) {
+        // TGK off-diagonals (alpha_1, beta_2, ..., alpha_m, beta_{m+1}) into SMEM
+        const int n = 2 * m + 1;
+        __syncthreads();
+        for (int i = tid; i < n - 1; i += blockDim.x) {
+          double v = (i & 1) ? sm.beta[(i >> 1) + 2] : sm.alpha[(i >> 1) + 1];
+          tc[i] = v;
+          tc2[i] = v * v;
+        }
+        __syncthreads();
+        double* om = sm.chk;
+        double* res = om + kMaxK;
+        double* lohi = res + kMaxK;
+        tgk_check(tc, tc2, m, k, al, om, res, lohi, tgk_scr);
+        double mr = 0.0;
+        for (int i = 0; i < k; ++i) mr = fmax(mr, res[i]);
+        const double rel = (om[0] > 0.0) ? mr / om[0] : 0.0;
+        ++checks;
+        lap(2);
+        // the estimate must be below tol/2 (the final QR residual is what gets reported)
+        if (rel <= 0.5 * a.tol) { converged = 1; break; }
+        // schedule the next test from the observed geometric decay of the residual
+        int step = ce;
+        if (prev_res > 0.0 && rel < prev_res && rel > 0.0) {
+          double rate = log(rel / prev_res) / (double)(m - prev_m);
+          double need = log(0.5 * a.tol / rel) / rate;
+          int s2 = (int)(0.7 * need);
+          if (s2 > step) step = s2 < 4 * ce ? s2 : 4 * ce;
+        }
+        prev_res = rel;
+        prev_m = m;
+        next_check = m + step;
+      }
+      if (last) break;
+
+      // ---- half-step B (Alg. 1 l.6-7): p = X v_j - alpha_j u_j; FRO vs U_j ----
+      lap(7);
+      const double aj = al;
+      correlate_cta(
+          fbuf, sh, a.tw, spec, K, L, [&](int i) { return sm.bufV[i]; },
+          [&](int t, double y) { sm.bufU[t] = y - aj * sm.bufU[t]; });
+      __syncthreads();
+      ss = 0.0;
+      for (int t = tid; t < L; t += blockDim.x) ss = fma(sm.bufU[t], sm.bufU[t], ss);
+      nr = sqrt(block_sum(ss, sm.red));
+      lap(0);
+      double be = reorth(sm.bufU, U, j, a.ldL, nr, a.reorth_mode, sm, rg, part, pstride, extra);
+      if (!(be > 1e-12 * runmax) || be == 0.0) {
+        if (!breakdown) breakdown = j;
+        double q = (j < L) ? restart_vector(sm.bufU, L, a.ldL, U, j, a.seed, (uint64_t)b,
+                                            ((uint64_t)(++restarts) << 40), sm, rg, part, pstride)
+                           : 0.0;
+        if (q > 1e-8) {
+          ss = 0.0;
+          for (int t = tid; t < L; t += blockDim.x) ss = fma(sm.bufU[t], sm.bufU[t], ss);
+          double nn = sqrt(block_sum(ss, sm.red));
+          normalize_store(sm.bufU, L, a.ldL, 1.0 / nn, U + (size_t)j * a.ldL);
+        } else {
+          normalize_store(sm.bufU, L, a.ldL, 0.0, U + (size_t)j * a.ldL);
+        }
+        be = 0.0;
+      } else {
+        normalize_store(sm.bufU, L, a.ldL, 1.0 / be, U + (size_t)j * a.ldL);
+      }
+      if (tid == 0) sm.beta[j + 1] = be;
+      bcur = be;
+      runmax = fmax(runmax, be);
+      lap(1);
+    }
+    lap(7);
+    // ---- publish B_m and the step count for the SVD kernel ----
+    __syncthreads();
+    for (int i = tid; i <= m + 2 && i < a.m_max + 3; i += blockDim.x) {
+      abg[i] = sm.alpha[i];
+      abg[a.m_max + 3 + i] = sm.beta[i];
+    }
+    if (tid == 0) {
+      st[0] = m; st[1] = converged; st[2] = breakdown; st[3] = extra; st[4] = restarts; st[5] = 0; st[6] = checks;
+    }
+  }
+  if (a.prof && tid == 0)
+    for (int i = 0; i < 8; ++i) atomicAdd(a.prof + i, pc[i]);
+}
+
+cudaError_t lanczos_set_attributes(size_t smem) {
+  return cudaFuncSetAttribute(lanczos_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+
+cudaError_t launch_lanczos(const Plan& p, const DecomposeArgs& a, cudaStream_t s) {
+  int grid = p.lanczos_slots < a.nb ? p.lanczos_slots : a.nb;
+  lanczos_kernel<<<grid, kThreads, p.smem_lanczos, s>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace ssa

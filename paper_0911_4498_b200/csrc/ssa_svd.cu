@@ -1,0 +1,275 @@
+// ssa_svd.cu -- the small projected bidiagonal SVD (north star (b)) and the Ritz assembly.
+//
+//  bidiag_svd_kernel  one warp per series (persistent): implicit-shift QR SVD of the
+//                     (m+1) x m lower bidiagonal B_m by lane 0
+//                     with every rotation recorded; then P_k, Q_k columns of the k largest
+//                     singular values are formed by 2k lanes applying the records in
+//                     reverse to unit vectors (bidiag_qr.cuh).  Writes sigma, the Ritz
+//                     coefficients and the final residual alpha_{m+1} |P_{m+1,i}| (Eq. 2).
+//  ritz_kernel        one CTA per series (persistent): U_k = U_{m+1} P_k, V_k = V_m Q_k
+//                     (Eq. 1) streaming each basis once more through
+//                     the per-warp TMA rings, then sign canonicalization (largest-|.| entry
+//                     of u_i positive, R12).
+#include "bidiag_qr.cuh"
+#include "device_common.cuh"
+
+namespace ssa {
+
+constexpr int kSvdWarps = kSvdWarpsPerCta;
+
+__global__ void __launch_bounds__(kSvdWarps * 32) bidiag_svd_kernel(const DecomposeArgs a) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int wslot = blockIdx.x * kSvdWarps + warp;
+  if (wslot >= a.svd_slots) return;  // scratch exists for svd_slots warps only
+  const int mstride = a.m_max + 2;
+  double* d = reinterpret_cast<double*>(smem_raw) + (size_t)warp * (3 * mstride + 2 * kMaxK);
+  double* e = d + mstride;
+  double* wv = e + mstride;
+  double* om = wv + mstride;
+  int* sel = reinterpret_cast<int*>(om + kMaxK);
+  double* rbase = a.rot + (size_t)wslot * 6 * a.rot_cap;
+  int2* abL = reinterpret_cast<int2*>(rbase);
+  double2* csL = reinterpret_cast<double2*>(rbase + a.rot_cap);
+  int2* abR = reinterpret_cast<int2*>(rbase + 3 * (size_t)a.rot_cap);
+  double2* csR = reinterpret_cast<double2*>(rbase + 4 * (size_t)a.rot_cap);
+  const int k = a.k, k2 = 2 * a.k;
+  double* vec = a.vecs + (size_t)wslot * k2 * mstride;  // vec[row * 2k + t]
+  unsigned long long cq = 0, ca = 0;
+  while (true) {
+    int bl = 0;
+    if (lane == 0) bl = atomicAdd(a.counters + 1, 1);
+    bl = __shfl_sync(0xffffffffu, bl, 0);
+    if (bl >= a.nb) break;
+    const int b = a.b0 + bl;
+    const int* st = a.state + (size_t)bl * 8;
+    const int m = st[0];
+    const double* alpha = a.ab + (size_t)bl * 2 * (a.m_max + 3);
+    const double* beta = alpha + (a.m_max + 3);
+    if (st[5]) {  // non-finite series
+      if (lane < k) a.sigma[(size_t)b * k + lane] = __longlong_as_double(0x7ff8000000000000ll);
+      if (lane == 0) {
+        ssa_series_info inf = {};
+        inf.status = SSA_ERR_INVALID_ARGUMENT;
+        a.info[b] = inf;
+      }
+      continue;
+    }
+    long long t0 = clock64();
+    int nL = 0, nR = 0, it = 0;
+    double fres = 0.0;
+    if (lane == 0) {
+      RotRec rl{abL, csL, a.rot_cap, 0}, rr{abR, csR, a.rot_cap, 0};
+      it = bidiag_qr<true, true>(m, alpha, beta, d, e, wv, &rl, &rr, 30 * m + 100);
+      select_topk(m, d, k, sel, om);
+      double mr = 0.0;
+      for (int i = 0; i < k; ++i)
+        if (sel[i] >= 0) mr = fmax(mr, alpha[m + 1] * fabs(wv[sel[i]]));
+      fres = (om[0] > 0.0) ? mr / om[0] : 0.0;
+      nL = rl.n;
+      nR = rr.n;
+      if (it < 0 || nL > a.rot_cap || nR > a.rot_cap) nL = -1;
+    }
+    __syncwarp();
+    long long t1 = clock64();
+    nL = __shfl_sync(0xffffffffu, nL, 0);
+    nR = __shfl_sync(0xffffffffu, nR, 0);
+    const bool ok = nL >= 0;
+    // columns of P (length m+1) and Q (length m): one lane per column
+    for (int t = lane; t < k2; t += 32) {
+      const bool isP = t < k;
+      const int i = isP ? t : t - k;
+      const int len = isP ? m + 1 : m;
+      for (int r = 0; r < len; ++r) vec[(size_t)r * k2 + t] = 0.0;
+      const int si = sel[i];
+      if (si >= 0 && ok) {
+        vec[(size_t)si * k2 + t] = 1.0;
+        if (isP) apply_records_reverse(abL, csL, nL, vec + t, k2);
+        else apply_records_reverse(abR, csR, nR, vec + t, k2);
+        if (!isP && d[si] < 0.0)
+          for (int r = 0; r < len; ++r) vec[(size_t)r * k2 + t] = -vec[(size_t)r * k2 + t];
+      }
+    }
+    __syncwarp();
+    // Ritz coefficients [2][m_max+2][k]
+    double* cP = a.coef + (size_t)bl * 2 * mstride * k;
+    double* cQ = cP + (size_t)mstride * k;
+    for (int idx = lane; idx < (m + 1) * k; idx += 32) {
+      int r = idx / k, i = idx - r * k;
+      cP[idx] = vec[(size_t)r * k2 + i];
+      cQ[idx] = (r < m) ? vec[(size_t)r * k2 + k + i] : 0.0;
+    }
+    if (lane < k) a.sigma[(size_t)b * k + lane] = om[lane];
+    if (lane == 0) {
+      ssa_series_info inf;
+      inf.steps = m;
+      inf.converged = st[1];
+      inf.breakdown_step = st[2];
+      inf.reorth_extra = st[3];
+      inf.reserved = st[4];
+      inf.status = !ok ? SSA_ERR_INTERNAL : (fres <= a.tol ? SSA_OK : SSA_ERR_NOT_CONVERGED);
+      inf.max_residual = fres;
+      inf.sigma1 = om[0];
+      a.info[b] = inf;
+    }
+    __syncwarp();
+    long long t2 = clock64();
+    cq += (unsigned long long)(t1 - t0);
+    ca += (unsigned long long)(t2 - t1);
+  }
+  if (a.prof && lane == 0) {
+    atomicAdd(a.prof + 3, cq);
+    atomicAdd(a.prof + 4, ca);
+  }
+}
+
+size_t ritz_smem_bytes(int ldL, int ldK, int k) {
+  (void)k;
+  int slab_max = (ldL > ldK ? ldL : ldK) / kWarps;
+  size_t s = (size_t)kWarps * kStages * slab_max * 8;
+  s += (size_t)kWarps * kMaxK * (8 + 4) + kMaxK * 8;
+  s += (size_t)kWarps * kStages * 8;
+  return align16(s) + 16;
+}
+
+__global__ void __launch_bounds__(kThreads, 2) ritz_kernel(const DecomposeArgs a) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  const int slab_max = (a.ldL > a.ldK ? a.ldL : a.ldK) / kWarps;
+  double* rings = reinterpret_cast<double*>(smem_raw);
+  double* mxv = rings + (size_t)kWarps * kStages * slab_max;  // [kWarps][kMaxK]
+  double* sgn = mxv + kWarps * kMaxK;                          // [kMaxK]
+  int* mxi = reinterpret_cast<int*>(sgn + kMaxK);              // [kWarps][kMaxK]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(mxi + kWarps * kMaxK);
+  __shared__ int sb;
+  WarpRing rg;
+  ring_init(rg, rings + (size_t)w * kStages * slab_max, bars + w * kStages);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+  const int L = a.L, K = a.K, k = a.k;
+  const int mstride = a.m_max + 2;
+  unsigned long long t0 = clock64();
+  while (true) {
+    __syncthreads();
+    if (tid == 0) sb = atomicAdd(a.counters + 2, 1);
+    __syncthreads();
+    const int bl = sb;
+    if (bl >= a.nb) break;
+    const int b = a.b0 + bl;
+    const int* st = a.state + (size_t)bl * 8;
+    if (st[5]) continue;
+    const int m = st[0];
+    const double* cP = a.coef + (size_t)bl * 2 * mstride * k;
+    for (int side = 0; side < 2; ++side) {
+      const bool isU = side == 0;
+      const int n = isU ? L : K, ld = isU ? a.ldL : a.ldK, rows = isU ? m + 1 : m;
+      const double* basis = isU ? a.U + (size_t)bl * (a.m_max + 1) * a.ldL : a.V + (size_t)bl * (a.m_max + 1) * a.ldK;
+      const double* coef = cP + (isU ? 0 : (size_t)mstride * k);
+      double* out = (isU ? a.Uout : a.Vout) + (size_t)b * k * n;
+      const int slab = ld / kWarps;
+      const double* bw = basis + (size_t)w * slab;
+      double bestv[kMaxK];
+      int besti[kMaxK];
+#pragma unroll
+      for (int i = 0; i < kMaxK; ++i) { bestv[i] = -1.0; besti[i] = 0; }
+      constexpr int E = 2;
+      for (int e0 = 0; e0 < slab; e0 += 32 * E) {
+        for (int i0 = 0; i0 < k; i0 += 16) {
+          const int ki = (k - i0) < 16 ? (k - i0) : 16;
+          double acc[E][16];
+#pragma unroll
+          for (int t = 0; t < E; ++t)
+#pragma unroll
+            for (int i = 0; i < 16; ++i) acc[t][i] = 0.0;
+          fence_proxy_async_smem();
+          __syncwarp();
+          stream_rows(bw, ld, rows, false, slab, rg, [&](int row, const double* ch) {
+            const double* cr = coef + (size_t)row * k + i0;
+            double cf[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) cf[i] = (i < ki) ? __ldg(cr + i) : 0.0;
+#pragma unroll
+            for (int t = 0; t < E; ++t) {
+              int e = e0 + t * 32 + lane;
+              double x = (e < slab) ? ch[e] : 0.0;
+#pragma unroll
+              for (int i = 0; i < 16; ++i) acc[t][i] = fma(cf[i], x, acc[t][i]);
+            }
+          });
+#pragma unroll
+          for (int t = 0; t < E; ++t) {
+            int e = e0 + t * 32 + lane;
+            int g = w * slab + e;
+            if (e < slab && g < n) {
+#pragma unroll
+              for (int i = 0; i < 16; ++i)
+                if (i < ki) {
+                  out[(size_t)(i0 + i) * n + g] = acc[t][i];
+                  if (isU && fabs(acc[t][i]) > bestv[i0 + i]) { bestv[i0 + i] = fabs(acc[t][i]); besti[i0 + i] = g; }
+                }
+            }
+          }
+        }
+      }
+      if (isU) {
+        for (int i = 0; i < k; ++i) {
+          double v = bestv[i];
+          int ix = besti[i];
+          for (int o = 16; o > 0; o >>= 1) {
+            double v2 = __shfl_xor_sync(0xffffffffu, v, o);
+            int i2 = __shfl_xor_sync(0xffffffffu, ix, o);
+            if (v2 > v || (v2 == v && i2 < ix)) { v = v2; ix = i2; }
+          }
+          if (lane == 0) { mxv[w * kMaxK + i] = v; mxi[w * kMaxK + i] = ix; }
+        }
+      }
+    }
+    __syncthreads();
+    if (tid < k) {
+      double v = -1.0;
+      int ix = 0;
+      for (int q = 0; q < kWarps; ++q) {
+        double v2 = mxv[q * kMaxK + tid];
+        int i2 = mxi[q * kMaxK + tid];
+        if (v2 > v || (v2 == v && i2 < ix)) { v = v2; ix = i2; }
+      }
+      const double* uo = a.Uout + ((size_t)b * k + tid) * L;
+      sgn[tid] = (uo[ix] < 0.0) ? -1.0 : 1.0;
+    }
+    __syncthreads();
+    for (int i = 0; i < k; ++i) {
+      if (sgn[i] < 0.0) {
+        double* uo = a.Uout + ((size_t)b * k + i) * L;
+        double* vo = a.Vout + ((size_t)b * k + i) * K;
+        for (int t = tid; t < L; t += blockDim.x) uo[t] = -uo[t];
+        for (int t = tid; t < K; t += blockDim.x) vo[t] = -vo[t];
+      }
+    }
+  }
+  if (a.prof && tid == 0) atomicAdd(a.prof + 5, (unsigned long long)(clock64() - t0));
+}
+
+static size_t svd_smem_bytes(int m_max) { return (size_t)kSvdWarps * ((3 * (m_max + 2) + 2 * kMaxK) * 8); }
+
+cudaError_t svd_ritz_set_attributes(int m_max, size_t smem_ritz) {
+  cudaError_t e;
+  if ((e = cudaFuncSetAttribute(ritz_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_ritz))) return e;
+  if ((e = cudaFuncSetAttribute(bidiag_svd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)svd_smem_bytes(m_max))))
+    return e;
+  return cudaSuccess;
+}
+
+cudaError_t launch_bidiag_svd(const Plan& p, const DecomposeArgs& a, cudaStream_t s) {
+  int grid = (a.svd_slots + kSvdWarps - 1) / kSvdWarps;
+  bidiag_svd_kernel<<<grid, kSvdWarps * 32, svd_smem_bytes(a.m_max), s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ritz(const Plan& p, const DecomposeArgs& a, cudaStream_t s) {
+  int grid = p.ritz_slots < a.nb ? p.ritz_slots : a.nb;
+  ritz_kernel<<<grid, kThreads, p.smem_ritz, s>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace ssa

@@ -17,7 +17,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libssa.so")
+LIB_PATH = os.environ.get("SSA_LIB", os.path.join(_HERE, "libssa.so"))
 
 SSA_OK = 0
 STATUS = {0: "SSA_OK", 1: "SSA_ERR_INVALID_ARGUMENT", 2: "SSA_ERR_NOT_CONVERGED", 3: "SSA_ERR_OUT_OF_MEMORY",
@@ -27,7 +27,7 @@ STATUS = {0: "SSA_OK", 1: "SSA_ERR_INVALID_ARGUMENT", 2: "SSA_ERR_NOT_CONVERGED"
 EXPORTS = ["ssa_options_default", "ssa_plan_create", "ssa_plan_destroy", "ssa_plan_fft_size",
            "ssa_plan_max_steps", "ssa_spectrum", "ssa_matvec", "ssa_hankelize", "ssa_decompose",
            "ssa_reconstruct", "ssa_run_host", "ssa_status_string", "ssa_last_error",
-           "ssa_plan_launch_count", "ssa_plan_phase_ms"]
+           "ssa_plan_launch_count", "ssa_plan_phase_ms", "ssa_plan_profile", "ssa_plan_bidiagonals"]
 
 
 class SsaError(RuntimeError):
@@ -76,6 +76,10 @@ def load_library():
     lib.ssa_plan_launch_count.restype = i64
     lib.ssa_plan_phase_ms.argtypes = [vp, ctypes.POINTER(ctypes.c_double)]
     lib.ssa_plan_phase_ms.restype = ctypes.c_int
+    lib.ssa_plan_profile.argtypes = [vp, ctypes.POINTER(ctypes.c_int64)]
+    lib.ssa_plan_profile.restype = ctypes.c_int
+    lib.ssa_plan_bidiagonals.argtypes = [vp, vp, vp, vp]
+    lib.ssa_plan_bidiagonals.restype = ctypes.c_int
     lib.ssa_spectrum.argtypes = [vp, dp, dp, vp]
     lib.ssa_matvec.argtypes = [vp, dp, dp, dp, ctypes.c_int, vp]
     lib.ssa_hankelize.argtypes = [vp, dp, dp, dp, i32, dp, vp]
@@ -119,7 +123,8 @@ class Plan:
     """ssa_plan_create / ssa_plan_destroy wrapper.  One plan per (N, L, k, batch)."""
 
     def __init__(self, N: int, L: int, k: int, batch: int, *, tol: float = 1e-12, max_steps: int = 0,
-                 check_every: int = 4, seed: int = 42, reorth: int = 1, device: int | None = None):
+                 check_every: int = 4, seed: int = 42, reorth: int = 1, device: int | None = None,
+                 profile: bool = False):
         import torch
         lib = load_library()
         if not torch.cuda.is_available():
@@ -128,6 +133,7 @@ class Plan:
         opt = Options()
         _check(lib.ssa_options_default(ctypes.byref(opt)))
         opt.tol, opt.max_steps, opt.check_every, opt.seed, opt.reorth = tol, max_steps, check_every, seed, reorth
+        opt.reserved = 1 if profile else 0
         h = ctypes.c_void_p()
         _check(lib.ssa_plan_create(N, L, k, batch, ctypes.byref(opt), self.device, ctypes.byref(h)))
         self._h = h
@@ -152,9 +158,25 @@ class Plan:
 
     def phase_ms(self) -> dict:
         """Device ms of the last spectrum / lanczos / hankelize launches (CUDA events)."""
-        out = (ctypes.c_double * 3)()
+        out = (ctypes.c_double * 5)()
         _check(load_library().ssa_plan_phase_ms(self._h, out))
-        return {"spectrum": out[0], "lanczos": out[1], "hankelize": out[2]}
+        return {"spectrum": out[0], "lanczos": out[1], "bidiag_svd": out[2], "ritz": out[3], "hankelize": out[4]}
+
+    def profile(self) -> dict:
+        """Per-phase SM cycles of the decompose kernel (plan created with profile=True)."""
+        out = (ctypes.c_int64 * 8)()
+        _check(load_library().ssa_plan_profile(self._h, out))
+        keys = ["fft", "reorth", "check", "svd_qr", "svd_apply", "ritz_kernel", "unused6", "other"]
+        return dict(zip(keys, list(out)))
+
+    def bidiagonals(self):
+        """(alpha, beta, steps) of the last decompose (test hook): alpha[b][j] = alpha_j,
+        beta[b][j] = beta_j (1-based, Alg. 1), steps[b] = m."""
+        nb = min(self.batch, self.batch)  # single-chunk plans: all series
+        w = self.m_max + 3
+        al = np.zeros((nb, w)); be = np.zeros((nb, w)); st = np.zeros(nb, dtype=np.int32)
+        _check(load_library().ssa_plan_bidiagonals(self._h, al.ctypes.data, be.ctypes.data, st.ctypes.data))
+        return al, be, st
 
     def _t(self, *shape):
         import torch
