@@ -71,7 +71,7 @@ static std::vector<double2> make_twiddles(int64_t M) {
 
 static void free_plan(Plan& p) {
   void* ptrs[] = {p.d_tw, p.d_spec, p.d_U, p.d_V, p.d_ab, p.d_state, p.d_tgk, p.d_rot, p.d_vecs, p.d_coef,
-                  p.d_info, p.d_counters, p.d_hscratch, p.d_prof, p.d_series, p.d_sigma, p.d_Uout, p.d_Vout,
+                  p.d_info, p.d_counters, p.d_hscratch, p.d_prof, p.d_tgkw, p.d_series, p.d_sigma, p.d_Uout, p.d_Vout,
                   p.d_recon};
   for (void* q : ptrs)
     if (q) cudaFree(q);
@@ -98,6 +98,9 @@ static size_t per_series_bytes(const Plan& p) {
   s += (size_t)2 * (p.m_max + 2) * p.k * 8;
   return s;
 }
+
+// doubles per TGK-SVD CTA slot: Z (n k), LU factors (5 n k), pivots (n k ints)
+static size_t tgkw_stride(const Plan& p) { return (size_t)(2 * p.m_max + 1) * p.k * 7; }
 
 static ssa_status create_decompose_workspace(Plan& p, const cudaDeviceProp& prop) {
   ssa_status st;
@@ -134,9 +137,15 @@ static ssa_status create_decompose_workspace(Plan& p, const cudaDeviceProp& prop
   if ((st = alloc((void**)&p.d_coef, C * 2 * (p.m_max + 2) * k * 8, "Ritz coefficients")) != SSA_OK) return st;
   if ((st = alloc((void**)&p.d_tgk, (size_t)p.lanczos_slots * k * (2 * p.m_max + 2) * 8, "TGK scratch")) != SSA_OK)
     return st;
-  if ((st = alloc((void**)&p.d_rot, (size_t)p.svd_slots * 6 * p.rot_cap * 8, "rotation records")) != SSA_OK) return st;
-  if ((st = alloc((void**)&p.d_vecs, (size_t)p.svd_slots * 2 * k * (p.m_max + 2) * 8, "P/Q columns")) != SSA_OK)
-    return st;
+  if (p.opt.reserved & 2) {  // bidiagonal SVD by QR with rotation records
+    if ((st = alloc((void**)&p.d_rot, (size_t)p.svd_slots * 6 * p.rot_cap * 8, "rotation records")) != SSA_OK)
+      return st;
+    if ((st = alloc((void**)&p.d_vecs, (size_t)p.svd_slots * 2 * k * (p.m_max + 2) * 8, "P/Q columns")) != SSA_OK)
+      return st;
+  } else {  // TGK multisection + inverse iteration
+    p.tgk_slots = (int)std::min<int64_t>(chunk, (int64_t)p.sms * 8);
+    if ((st = alloc((void**)&p.d_tgkw, (size_t)p.tgk_slots * tgkw_stride(p) * 8, "TGK vectors")) != SSA_OK) return st;
+  }
   if ((st = alloc((void**)&p.d_info, (size_t)p.batch * sizeof(ssa_series_info), "info")) != SSA_OK) return st;
   if ((st = alloc((void**)&p.d_counters, 16 * sizeof(int), "counters")) != SSA_OK) return st;
   if (p.opt.reserved & 1) {
@@ -301,7 +310,8 @@ extern "C" ssa_status ssa_decompose(ssa_plan_t plan, const double* d_series, dou
   a.series = d_series; a.spec = p.d_spec; a.tw = p.d_tw;
   a.U = p.d_U; a.V = p.d_V; a.ab = p.d_ab; a.state = p.d_state;
   a.tgk = p.d_tgk; a.tgk_stride = (size_t)p.k * (2 * p.m_max + 2);
-  a.rot = p.d_rot; a.rot_cap = p.rot_cap; a.svd_slots = p.svd_slots; a.vecs = p.d_vecs; a.coef = p.d_coef;
+  a.rot = p.d_rot; a.rot_cap = p.rot_cap; a.svd_slots = p.svd_slots;
+  a.svd_method = (p.opt.reserved & 2) ? 1 : 0; a.tgkw = p.d_tgkw; a.tgkw_stride = tgkw_stride(p); a.vecs = p.d_vecs; a.coef = p.d_coef;
   a.sigma = d_sigma; a.Uout = d_U; a.Vout = d_V;
   a.info = d_info ? d_info : p.d_info;
   a.counters = p.d_counters;

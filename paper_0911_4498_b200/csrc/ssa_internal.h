@@ -36,7 +36,10 @@ struct DecomposeArgs {
   size_t tgk_stride;
   double* rot;           // per SVD warp slot: 2 sides x rot_cap x 3 doubles
   int rot_cap;
-  int svd_slots;         // warps with rotation / vector scratch
+  int svd_slots;         // warps with rotation / vector scratch (QR method)
+  int svd_method;        // 0: TGK multisection + inverse iteration, 1: QR with records
+  double* tgkw;          // per TGK-SVD CTA slot: Z (n k) + W (5 n k) + ipv (n k ints)
+  size_t tgkw_stride;    // doubles
   double* vecs;          // per SVD warp slot: 2k x (m_max+2) doubles
   double* coef;          // [nb][2][m_max+2][k]: P_k rows then Q_k rows (signs folded)
   double* sigma;         // caller [batch][k]
@@ -60,6 +63,8 @@ struct Plan {
   int lanczos_slots = 0;       // persistent CTAs of the Lanczos kernel
   int svd_slots = 0;           // warps of the SVD kernel
   int ritz_slots = 0;          // CTAs of the Ritz kernel
+  int tgk_slots = 0;           // CTAs of the TGK SVD kernel
+  double* d_tgkw = nullptr;
   int rot_cap = 0;
   size_t smem_lanczos = 0, smem_ritz = 0;
   double2* d_tw = nullptr;     // twiddles exp(-2 pi i t / M), t < H

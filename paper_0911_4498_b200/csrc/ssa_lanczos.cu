@@ -14,7 +14,7 @@
 // Output per series: the bases, alpha/beta and the step count m; the bidiagonal SVD and
 // the Ritz assembly are separate kernels (ssa_svd.cu).
 #include "device_common.cuh"
-#include "tgk_check.cuh"
+#include "tgk.cuh"
 
 namespace ssa {
 
@@ -35,7 +35,7 @@ __host__ __device__ inline size_t lanczos_regionA_bytes(int H, int ldL, int ldK,
   int slab_max = (ldL > ldK ? ldL : ldK) / kWarps;
   size_t fft = (size_t)fpad_size(H) * 16;
   size_t rings = (size_t)kWarps * kStages * slab_max * 8 + (size_t)kWarps * (m_max + 2) * 8;
-  size_t tgk = (size_t)2 * (2 * m_max + 2) * 8;
+  size_t tgk = (size_t)3 * (2 * m_max + 2) * 8;
   size_t r = fft;
   if (rings > r) r = rings;
   if (tgk > r) r = tgk;
@@ -84,12 +84,20 @@ __device__ __forceinline__ double rng_uniform_pm1(uint64_t seed, uint64_t series
 // fell below 1/sqrt(2) of its value), mode 2: always two passes (PAPER.md:388-393,
 // DESIGN.md R9).  Each warp owns a column slab of r and of the basis; the dot products
 // are reduced across warps in a fixed order (deterministic).
-__device__ double reorth(double* r, const double* basis, int nb, int ld, double nrm_in, int mode, const LSmem& sm,
-                         WarpRing& rg, double* part, int pstride, int& extra) {
+// EPL elements of the warp's slab per lane live in registers (element lane + 32 t).
+template <int EPL>
+__device__ double reorth_t(double* r, const double* basis, int nb, int ld, double nrm_in, int mode, const LSmem& sm,
+                           WarpRing& rg, double* part, int pstride, int& extra) {
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int slab = ld / kWarps;
   double* rw = r + w * slab;
   const double* bw = basis + (size_t)w * slab;
+  double rv[EPL];
+#pragma unroll
+  for (int t = 0; t < EPL; ++t) {
+    const int e = lane + 32 * t;
+    rv[t] = (e < slab) ? rw[e] : 0.0;
+  }
   double nrm = nrm_in;
   for (int pass = 0; pass < 2 && nb > 0; ++pass) {
     fence_proxy_async_smem();
@@ -97,7 +105,11 @@ __device__ double reorth(double* r, const double* basis, int nb, int ld, double 
     // pass 1: partial dots of this warp's slab with every basis row
     stream_rows(bw, ld, nb, false, slab, rg, [&](int row, const double* ch) {
       double s = 0.0;
-      for (int e = lane; e < slab; e += 32) s = fma(ch[e], rw[e], s);
+#pragma unroll
+      for (int t = 0; t < EPL; ++t) {
+        const int e = lane + 32 * t;
+        if (e < slab) s = fma(ch[e], rv[t], s);
+      }
       s = warp_sum(s);
       if (lane == 0) part[w * pstride + row] = s;
     });
@@ -112,17 +124,46 @@ __device__ double reorth(double* r, const double* basis, int nb, int ld, double 
     // in L2) come first
     stream_rows(bw, ld, nb, true, slab, rg, [&](int row, const double* ch) {
       const double hc = sm.h[row];
-      for (int e = lane; e < slab; e += 32) rw[e] = fma(-hc, ch[e], rw[e]);
+#pragma unroll
+      for (int t = 0; t < EPL; ++t) {
+        const int e = lane + 32 * t;
+        if (e < slab) rv[t] = fma(-hc, ch[e], rv[t]);
+      }
     });
     double ss = 0.0;
-    for (int e = lane; e < slab; e += 32) ss = fma(rw[e], rw[e], ss);
+#pragma unroll
+    for (int t = 0; t < EPL; ++t) ss = fma(rv[t], rv[t], ss);
     double nn = sqrt(block_sum(ss, sm.red));
     bool again = (pass == 0) && (mode == 2 || nn < 0.70710678118654752 * nrm);
     nrm = nn;
     if (!again) break;
     ++extra;
   }
+#pragma unroll
+  for (int t = 0; t < EPL; ++t) {
+    const int e = lane + 32 * t;
+    if (e < slab) rw[e] = rv[t];
+  }
+  __syncthreads();
   return nrm;
+}
+
+// CGS pass(es) of r (SMEM, ld doubles, zero padding) against basis rows [0, nb).
+// Returns the new norm; nrm_in is |r| before.  mode 1: DGKS (second pass iff the norm
+// fell below 1/sqrt(2) of its value), mode 2: always two passes (PAPER.md:388-393,
+// DESIGN.md R9).  Each warp owns a column slab of r (held in registers) and of the basis;
+// the dot products are reduced across warps in a fixed order (deterministic).
+__device__ double reorth(double* r, const double* basis, int nb, int ld, double nrm_in, int mode, const LSmem& sm,
+                         WarpRing& rg, double* part, int pstride, int& extra) {
+  const int epl = (ld / kWarps + 31) / 32;
+  if (epl <= 1) return reorth_t<1>(r, basis, nb, ld, nrm_in, mode, sm, rg, part, pstride, extra);
+  if (epl <= 2) return reorth_t<2>(r, basis, nb, ld, nrm_in, mode, sm, rg, part, pstride, extra);
+  if (epl <= 4) return reorth_t<4>(r, basis, nb, ld, nrm_in, mode, sm, rg, part, pstride, extra);
+  if (epl <= 8) return reorth_t<8>(r, basis, nb, ld, nrm_in, mode, sm, rg, part, pstride, extra);
+  if (epl <= 9) return reorth_t<9>(r, basis, nb, ld, nrm_in, mode, sm, rg, part, pstride, extra);
+  if (epl <= 16) return reorth_t<16>(r, basis, nb, ld, nrm_in, mode, sm, rg, part, pstride, extra);
+  if (epl <= 17) return reorth_t<17>(r, basis, nb, ld, nrm_in, mode, sm, rg, part, pstride, extra);
+  return reorth_t<32>(r, basis, nb, ld, nrm_in, mode, sm, rg, part, pstride, extra);
 }
 
 // Write r * inv into basis row dst (plain coalesced stores), scale r in place.
@@ -219,7 +260,7 @@ __global__ void __launch_bounds__(kThreads, 2) lanczos_kernel(const DecomposeArg
 
     double runmax = 0.0, bcur = beta1;
     int m = 0, converged = 0, breakdown = 0, extra = 0, restarts = 0, checks = 0;
-    int next_check = k;
+    int next_check = (2 * k < a.m_max) ? 2 * k : k;
     double prev_res = -1.0;
     int prev_m = 0;
     const int ce = a.check_every > 0 ? a.check_every : 4;
@@ -274,7 +315,11 @@ __global__ void __launch_bounds__(kThreads, 2) lanczos_kernel(const DecomposeArg
         double* om = sm.chk;
         double* res = om + kMaxK;
         double* lohi = res + kMaxK;
-        tgk_check(tc, tc2, m, k, al, om, res, lohi, tgk_scr);
+        // pivots of the twisted factorizations: shared memory when they fit in region A
+        double* tc2n = tc2 + (2 * a.m_max + 2);
+        const size_t need = (size_t)(3 * (2 * a.m_max + 2) + k * n) * 8;
+        double* dsc = (need <= lanczos_regionA_bytes(a.H, a.ldL, a.ldK, a.m_max)) ? tc2n + (2 * a.m_max + 2) : tgk_scr;
+        tgk_check(tc, tc2, tc2n, m, k, al, om, res, lohi, dsc);
         double mr = 0.0;
         for (int i = 0; i < k; ++i) mr = fmax(mr, res[i]);
         const double rel = (om[0] > 0.0) ? mr / om[0] : 0.0;
@@ -288,7 +333,7 @@ __global__ void __launch_bounds__(kThreads, 2) lanczos_kernel(const DecomposeArg
           double rate = log(rel / prev_res) / (double)(m - prev_m);
           double need = log(0.5 * a.tol / rel) / rate;
           int s2 = (int)(0.7 * need);
-          if (s2 > step) step = s2 < 4 * ce ? s2 : 4 * ce;
+          if (s2 > step) step = s2 < 2 * ce ? s2 : 2 * ce;
         }
         prev_res = rel;
         prev_m = m;

@@ -1,6 +1,8 @@
 // ssa_svd.cu -- the small projected bidiagonal SVD (north star (b)) and the Ritz assembly.
 //
-//  bidiag_svd_kernel  one warp per series (persistent): implicit-shift QR SVD of the
+//  bidiag_svd_tgk_kernel (default) one CTA per series: TGK multisection + inverse
+//                     iteration (tgk.cuh).
+//  bidiag_svd_kernel  (option) one warp per series (persistent): implicit-shift QR SVD of the
 //                     (m+1) x m lower bidiagonal B_m by lane 0
 //                     with every rotation recorded; then P_k, Q_k columns of the k largest
 //                     singular values are formed by 2k lanes applying the records in
@@ -12,6 +14,7 @@
 //                     of u_i positive, R12).
 #include "bidiag_qr.cuh"
 #include "device_common.cuh"
+#include "tgk.cuh"
 
 namespace ssa {
 
@@ -121,6 +124,114 @@ __global__ void __launch_bounds__(kSvdWarps * 32) bidiag_svd_kernel(const Decomp
     atomicAdd(a.prof + 3, cq);
     atomicAdd(a.prof + 4, ca);
   }
+}
+
+// Default final SVD: one CTA per series (persistent).  sigma = k largest eigenvalues of
+// TGK(B_m) by multisection; P_k, Q_k from TGK eigenvectors by inverse iteration
+// (tgk.cuh); residual alpha_{m+1} |P_{m+1,i}| (Eq. 2) reported in info.
+__global__ void __launch_bounds__(kThreads) bidiag_svd_tgk_kernel(const DecomposeArgs a) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int tid = threadIdx.x;
+  const int nmax = 2 * a.m_max + 1;
+  double* c = reinterpret_cast<double*>(smem_raw);
+  double* c2 = c + nmax;
+  double* lohi = c2 + nmax;
+  double* lam = lohi + 2 * kMaxK;
+  double* red = lam + kMaxK;
+  int* cl = reinterpret_cast<int*>(red + 2 * kMaxK);
+  __shared__ int sb;
+  const int k = a.k;
+  double* Z = a.tgkw + a.tgkw_stride * blockIdx.x;
+  double* W = Z + (size_t)nmax * k;
+  int* ipv = reinterpret_cast<int*>(W + (size_t)5 * nmax * k);
+  const int mstride = a.m_max + 2;
+  long long tvals = 0, tvecs = 0;
+  while (true) {
+    __syncthreads();
+    if (tid == 0) sb = atomicAdd(a.counters + 1, 1);
+    __syncthreads();
+    const int bl = sb;
+    if (bl >= a.nb) break;
+    const int b = a.b0 + bl;
+    const int* st = a.state + (size_t)bl * 8;
+    const int m = st[0];
+    const double* alpha = a.ab + (size_t)bl * 2 * (a.m_max + 3);
+    const double* beta = alpha + (a.m_max + 3);
+    if (st[5]) {  // non-finite series
+      if (tid < k) a.sigma[(size_t)b * k + tid] = __longlong_as_double(0x7ff8000000000000ll);
+      if (tid == 0) {
+        ssa_series_info inf = {};
+        inf.status = SSA_ERR_INVALID_ARGUMENT;
+        a.info[b] = inf;
+      }
+      continue;
+    }
+    const int n = 2 * m + 1;
+    for (int i = tid; i < n - 1; i += blockDim.x) {
+      double v = (i & 1) ? beta[(i >> 1) + 2] : alpha[(i >> 1) + 1];
+      c[i] = v;
+      c2[i] = v * v;
+    }
+    __syncthreads();
+    const TgkNorms nrm = tgk_norms(c, c2, n);
+    {
+      const double ig2 = (nrm.gmax > 0.0) ? 1.0 / (nrm.gmax * nrm.gmax) : 0.0;
+      __syncthreads();
+      for (int i = tid; i < n - 1; i += blockDim.x) c2[i] *= ig2;  // c2 now holds c^2 / |T|^2
+      __syncthreads();
+    }
+    long long ta = clock64();
+    tgk_topk_values(c2, n, k, nrm, lohi, lam, 40);
+    long long tb = clock64();
+    tgk_vectors(c, n, k, lam, nrm, Z, W, ipv, a.seed ^ ((unsigned long long)b << 20), cl);
+    long long tc = clock64();
+    tvals += tb - ta;
+    tvecs += tc - tb;
+    // split z = (p1, q1, p2, ..., q_m, p_{m+1}) into unit p (m+1) and q (m)
+    const double anext = alpha[m + 1];
+    double* cP = a.coef + (size_t)bl * 2 * mstride * k;
+    double* cQ = cP + (size_t)mstride * k;
+    if (tid < k) {
+      const int j = tid;
+      double sp = 0.0, sq = 0.0;
+      for (int r = 0; r <= m; ++r) { double v = Z[(size_t)(2 * r) * k + j]; sp = fma(v, v, sp); }
+      for (int r = 0; r < m; ++r) { double v = Z[(size_t)(2 * r + 1) * k + j]; sq = fma(v, v, sq); }
+      const double ip = sp > 0.0 ? 1.0 / sqrt(sp) : 0.0, iq = sq > 0.0 ? 1.0 / sqrt(sq) : 0.0;
+      red[j] = anext * fabs(Z[(size_t)(2 * m) * k + j]) * ip;
+      red[kMaxK + j] = ip;
+      lohi[j] = iq;
+    }
+    __syncthreads();
+    for (int idx = tid; idx < (m + 1) * k; idx += blockDim.x) {
+      const int r = idx / k, j = idx - r * k;
+      cP[idx] = Z[(size_t)(2 * r) * k + j] * red[kMaxK + j];
+      cQ[idx] = (r < m) ? Z[(size_t)(2 * r + 1) * k + j] * lohi[j] : 0.0;
+    }
+    if (tid < k) a.sigma[(size_t)b * k + tid] = lam[tid];
+    if (tid == 0) {
+      double mr = 0.0;
+      for (int j = 0; j < k; ++j) mr = fmax(mr, red[j]);
+      const double fres = lam[0] > 0.0 ? mr / lam[0] : 0.0;
+      ssa_series_info inf;
+      inf.steps = m;
+      inf.converged = st[1];
+      inf.breakdown_step = st[2];
+      inf.reorth_extra = st[3];
+      inf.reserved = st[4];
+      inf.status = fres <= a.tol ? SSA_OK : SSA_ERR_NOT_CONVERGED;
+      inf.max_residual = fres;
+      inf.sigma1 = lam[0];
+      a.info[b] = inf;
+    }
+  }
+  if (a.prof && tid == 0) {
+    atomicAdd(a.prof + 3, (unsigned long long)tvals);
+    atomicAdd(a.prof + 4, (unsigned long long)tvecs);
+  }
+}
+
+size_t tgk_svd_smem_bytes(int m_max) {
+  return (size_t)(2 * (2 * m_max + 1) + 2 * kMaxK + kMaxK + 2 * kMaxK) * 8 + 40 * 4 + 16;
 }
 
 size_t ritz_smem_bytes(int ldL, int ldK, int k) {
@@ -257,12 +368,20 @@ cudaError_t svd_ritz_set_attributes(int m_max, size_t smem_ritz) {
   if ((e = cudaFuncSetAttribute(bidiag_svd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)svd_smem_bytes(m_max))))
     return e;
+  if ((e = cudaFuncSetAttribute(bidiag_svd_tgk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)tgk_svd_smem_bytes(m_max))))
+    return e;
   return cudaSuccess;
 }
 
 cudaError_t launch_bidiag_svd(const Plan& p, const DecomposeArgs& a, cudaStream_t s) {
-  int grid = (a.svd_slots + kSvdWarps - 1) / kSvdWarps;
-  bidiag_svd_kernel<<<grid, kSvdWarps * 32, svd_smem_bytes(a.m_max), s>>>(a);
+  if (a.svd_method == 0) {
+    int grid = p.tgk_slots < a.nb ? p.tgk_slots : a.nb;
+    bidiag_svd_tgk_kernel<<<grid, kThreads, tgk_svd_smem_bytes(a.m_max), s>>>(a);
+  } else {
+    int grid = (a.svd_slots + kSvdWarps - 1) / kSvdWarps;
+    bidiag_svd_kernel<<<grid, kSvdWarps * 32, svd_smem_bytes(a.m_max), s>>>(a);
+  }
   return cudaGetLastError();
 }
 

@@ -1,0 +1,292 @@
+// tgk.cuh -- CTA-parallel singular triples of the (m+1) x m lower bidiagonal B_m of
+// Golub-Kahan-Lanczos bidiagonalization through its Golub-Kahan
+// tridiagonal TGK: the cyclic matrix [[0, B],[B^T, 0]] of Theorem 1
+// permuted to tridiagonal form, size n = 2m+1, zero diagonal, off-diagonal
+// c = (alpha_1, beta_2, alpha_2, beta_3, ..., alpha_m, beta_{m+1}).  Its eigenvalues are
+// +-omega_i and 0; the eigenvector of +omega_i interleaves (p_1, q_1, p_2, ..., q_m,
+// p_{m+1}) / sqrt(2) with B q = omega p, B^T p = omega q.
+//
+//  tgk_topk_values  k largest eigenvalues by multisection on Sturm counts (negcount of
+//                   the LDL^T pivots of TGK - x I), T threads per value, to full precision.
+//  tgk_check        values + last eigenvector entry by a twisted factorization: the Ritz
+//                   residual alpha_{m+1} |P_{m+1,i}| of Eq. (2) that
+//                   decides when Lanczos stops (R7).
+//  tgk_vectors      eigenvectors by inverse iteration with a partially pivoted tridiagonal
+//                   LU (LAPACK dgttrf/dgttrs style), Gram-Schmidt inside clusters of close
+//                   values (|gap| <= 1e-5 |T|), one thread per cluster.
+#pragma once
+#include <cuda_runtime.h>
+
+namespace ssa {
+
+// Number of eigenvalues of TGK that are < x.  c2[i] = (i-th off-diagonal)^2, i < n-1.
+__device__ __forceinline__ int tgk_negcount(const double* c2, int n, double x, double pivmin) {
+  double q = -x;
+  int cnt = q < 0.0;
+  for (int i = 1; i < n; ++i) {
+    if (fabs(q) < pivmin) q = -pivmin;
+    q = -x - c2[i - 1] / q;
+    cnt += q < 0.0;
+  }
+  return cnt;
+}
+
+// Division-free Sturm count: number of eigenvalues of TGK below x, from the sign changes
+// of the characteristic-polynomial sequence p_0 = 1, p_1 = -x, p_i = -x p_{i-1} -
+// c_{i-1}^2 p_{i-2} (Wilkinson), on the matrix scaled by 1/|T| (c2n = c2 / |T|^2,
+// xn = x / |T|) so |p_i| grows at most like the golden ratio per step; an exact
+// power-of-two rescale every 16 steps keeps the pair away from under/overflow.  Only
+// one FMA per step sits on the dependency chain (the ratio form q_i = p_i / p_{i-1}
+// has a division there).  A zero p_i takes the sign opposite to p_{i-1}.
+__device__ __forceinline__ int tgk_negcount_poly(const double* c2n, int n, double xn) {
+  double p2 = 1.0, p1 = -xn;
+  int cnt = p1 < 0.0;
+  for (int i = 1; i < n; ++i) {
+    double p = fma(-xn, p1, -c2n[i - 1] * p2);
+    if (p == 0.0) p = -copysign(0x1.0p-900, p1);
+    cnt += (p < 0.0) != (p1 < 0.0);
+    p2 = p1;
+    p1 = p;
+    if ((i & 15) == 0) {
+      const double mx = fmax(fabs(p1), fabs(p2));
+      if (mx < 0x1.0p-400) { p1 *= 0x1.0p+400; p2 *= 0x1.0p+400; }
+      else if (mx > 0x1.0p+400) { p1 *= 0x1.0p-400; p2 *= 0x1.0p-400; }
+    }
+  }
+  return cnt;
+}
+
+struct TgkNorms {
+  double gmax;    // Gershgorin bound >= |T|
+  double pivmin;  // smallest pivot magnitude allowed in the Sturm recurrence
+};
+
+__device__ __forceinline__ TgkNorms tgk_norms(const double* c, const double* c2, int n) {
+  double gmax = 0.0, cmax2 = 0.0;
+  for (int i = 0; i < n; ++i) {
+    double l = (i > 0) ? fabs(c[i - 1]) : 0.0, r = (i < n - 1) ? fabs(c[i]) : 0.0;
+    gmax = fmax(gmax, l + r);
+  }
+  for (int i = 0; i < n - 1; ++i) cmax2 = fmax(cmax2, c2[i]);
+  TgkNorms t;
+  t.gmax = gmax;
+  t.pivmin = 1e-290 * fmax(1.0, cmax2);
+  return t;
+}
+
+// k largest eigenvalues of TGK into lam[0..k-1] (descending).  lohi: SMEM scratch 2k.
+// max_rounds multisection rounds (each shrinks the bracket T+1 fold); stops early when
+// every bracket is below 2 eps of its upper end.  All threads call; ends with a barrier.
+// c2n: c2 / gmax^2 (shared memory).
+__device__ inline void tgk_topk_values(const double* c2n, int n, int k, const TgkNorms& nrm, double* lohi, double* lam,
+                                int max_rounds) {
+  const int tid = threadIdx.x, nthr = blockDim.x;
+  int T = 32;
+  while (T > 1 && k * T > nthr) T >>= 1;
+  const int j = tid / T, t = tid - j * T;
+  const bool act = j < k;
+  if (act && t == 0) { lohi[2 * j] = 0.0; lohi[2 * j + 1] = nrm.gmax * (1.0 + 1e-15) + 1e-300; }
+  __syncthreads();
+  for (int round = 0; round < max_rounds; ++round) {
+    double lo = act ? lohi[2 * j] : 0.0, hi = act ? lohi[2 * j + 1] : 0.0;
+    int open = act && (hi - lo > 4.440892098500626e-16 * hi) && (hi - lo > nrm.pivmin);
+    if (!__syncthreads_or(open)) break;
+    double x = lo + (hi - lo) * (double)(t + 1) / (double)(T + 1);
+    bool pred = act && (n - tgk_negcount_poly(c2n, n, x / nrm.gmax) >= j + 1);
+    unsigned bits = __ballot_sync(0xffffffffu, pred);
+    int shift = (T >= 32) ? 0 : ((tid & 31) / T) * T;
+    unsigned gb = (T >= 32) ? bits : ((bits >> shift) & ((1u << T) - 1u));
+    int ts = __popc(gb) - 1;  // monotone predicate: true for t <= ts
+    __syncthreads();
+    if (act && t == 0) {
+      double nlo = (ts >= 0) ? lo + (hi - lo) * (double)(ts + 1) / (double)(T + 1) : lo;
+      double nhi = (ts < T - 1) ? lo + (hi - lo) * (double)(ts + 2) / (double)(T + 1) : hi;
+      lohi[2 * j] = nlo;
+      lohi[2 * j + 1] = nhi;
+    }
+    __syncthreads();
+  }
+  if (tid < k) lam[tid] = 0.5 * (lohi[2 * tid] + lohi[2 * tid + 1]);
+  __syncthreads();
+}
+
+// Convergence test: omega[j], res[j] (SMEM) for j < k; scratch: >= k * n doubles (shared
+// memory when it fits, else global; layout [i][j]).
+// alpha_next = alpha_{m+1}.  All threads call; ends with a barrier.
+// c2n: scratch of n-1 doubles (shared memory) for the normalized squares.
+__device__ inline void tgk_check(const double* c, const double* c2, double* c2n, int m, int k, double alpha_next,
+                                 double* omega, double* res, double* lohi, double* scratch) {
+  const int n = 2 * m + 1;
+  const int tid = threadIdx.x;
+  const TgkNorms nrm = tgk_norms(c, c2, n);
+  const double pivmin = nrm.pivmin;
+  {
+    const double ig2 = (nrm.gmax > 0.0) ? 1.0 / (nrm.gmax * nrm.gmax) : 0.0;
+    for (int i = tid; i < n - 1; i += blockDim.x) c2n[i] = c2[i] * ig2;
+    __syncthreads();
+  }
+  tgk_topk_values(c2n, n, k, nrm, lohi, omega, 16);
+  // twisted factorization for lambda = omega_j, one thread per value: twist r at the
+  // smallest |gamma_r|, z_r = 1, z_i = -(c_i / D+_i) z_{i+1} above, -(c_{i-1} / D-_i) z_{i-1}
+  // below; last entry |z_n| / |z|
+  if (tid < k) {
+    const double lam = omega[tid];
+    double* D = scratch;  // D[i * k + tid]
+    double q = -lam;
+    D[tid] = q;
+    for (int i = 1; i < n; ++i) {
+      if (fabs(q) < pivmin) q = -pivmin;
+      q = -lam - c2[i - 1] / q;
+      D[(size_t)i * k + tid] = q;
+    }
+    double dm = -lam;
+    int r = n - 1;
+    double gbest = fabs(D[(size_t)(n - 1) * k + tid] + dm + lam);
+    for (int i = n - 2; i >= 0; --i) {
+      if (fabs(dm) < pivmin) dm = -pivmin;
+      dm = -lam - c2[i] / dm;
+      double g = fabs(D[(size_t)i * k + tid] + dm + lam);
+      if (g < gbest) { gbest = g; r = i; }
+    }
+    dm = -lam;
+    for (int i = n - 1; i > r; --i) {
+      if (i < n - 1) {
+        if (fabs(dm) < pivmin) dm = -pivmin;
+        dm = -lam - c2[i] / dm;
+      }
+      D[(size_t)i * k + tid] = dm;
+    }
+    double nrm2 = 1.0, z = 1.0;
+    for (int i = r - 1; i >= 0; --i) {
+      double d = D[(size_t)i * k + tid];
+      if (fabs(d) < pivmin) d = -pivmin;
+      z = -(c[i] / d) * z;
+      nrm2 = fma(z, z, nrm2);
+    }
+    z = 1.0;
+    for (int i = r + 1; i < n; ++i) {
+      double d = D[(size_t)i * k + tid];
+      if (fabs(d) < pivmin) d = -pivmin;
+      z = -(c[i - 1] / d) * z;
+      nrm2 = fma(z, z, nrm2);
+    }
+    const double zn = (r == n - 1) ? 1.0 : z;
+    res[tid] = alpha_next * 1.4142135623730951 * fabs(zn) / sqrt(nrm2);
+  }
+  __syncthreads();
+}
+
+// splitmix64-based uniform(-1,1) for inverse-iteration start vectors.
+__device__ __forceinline__ double tgk_rand(unsigned long long key, unsigned long long i) {
+  unsigned long long x = key + (i + 1) * 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  x ^= x >> 31;
+  return 2.0 * ((double)(x >> 11) * 0x1.0p-53) - 1.0;
+}
+
+// Eigenvectors of TGK for lam[0..k-1] (descending, from tgk_topk_values).
+// Z: global, column j at Z[i * k + j] (i < n).  W: global scratch >= 5 * n * k doubles
+// (LU factors of each shifted matrix), ipv: global scratch >= n * k ints.  Clusters:
+// maximal runs with lam[j-1] - lam[j] <= 1e-5 |T| (outside a cluster inverse iteration
+// alone keeps |z_i^T z_j| ~ eps |T| / gap <= 2e-11); one thread per cluster runs the
+// members in order, orthogonalizing each iterate against the earlier members (MGS, as
+// LAPACK dstein).  2 inverse-iteration steps (3 inside clusters) from a seeded random
+// start; the LU recurrences carry their running values in registers so the only memory
+// traffic on the dependency chain is independent loads/stores.  All threads call; ends
+// with a barrier.
+__device__ inline void tgk_vectors(const double* c, int n, int k, const double* lam, const TgkNorms& nrm, double* Z,
+                                   double* W, int* ipv, unsigned long long seed, int* cl_start) {
+  const int tid = threadIdx.x;
+  const double tnorm = nrm.gmax;
+  const double ortol = 1e-5 * tnorm;
+  if (tid == 0) {
+    int nc = 0;
+    for (int j = 0; j < k; ++j)
+      if (j == 0 || lam[j - 1] - lam[j] > ortol) cl_start[nc++] = j;
+    cl_start[nc] = k;
+    cl_start[33] = nc;
+  }
+  __syncthreads();
+  const int nclus = cl_start[33];
+  if (tid < nclus) {
+    const int j0 = cl_start[tid], j1 = cl_start[tid + 1];
+    const double eps = 2.220446049250313e-16;
+    const double pert = eps * tnorm;
+    for (int j = j0; j < j1; ++j) {
+      // perturb members of a cluster apart (LAPACK dstein: separate equal shifts)
+      double x = lam[j];
+      if (j > j0 && fabs(x - lam[j - 1]) < 10.0 * pert) x = lam[j - 1] - 10.0 * pert;
+      double* __restrict__ fl = W;                      // multipliers l_i
+      double* __restrict__ rd = W + (size_t)1 * n * k;  // 1 / u_ii
+      double* __restrict__ u1 = W + (size_t)2 * n * k;  // first superdiagonal of U
+      double* __restrict__ u2 = W + (size_t)3 * n * k;  // second superdiagonal of U
+      double* __restrict__ b = W + (size_t)4 * n * k;
+#define IX(i) ((size_t)(i) * k + j)
+      // dgttrf of T - x I (sub/super diagonal c, diagonal -x), running d_i, du_i in registers
+      double di = -x, dui = (n > 1) ? c[0] : 0.0;
+      for (int i = 0; i < n - 1; ++i) {
+        const double li = c[i];
+        const double dn = -x;
+        const double dun = (i < n - 2) ? c[i + 1] : 0.0;
+        if (fabs(di) >= fabs(li)) {
+          const double piv = (fabs(di) < pert) ? copysign(pert, di == 0.0 ? 1.0 : di) : di;
+          const double f = li / piv;
+          fl[IX(i)] = f; rd[IX(i)] = 1.0 / piv; u1[IX(i)] = dui; u2[IX(i)] = 0.0; ipv[IX(i)] = 0;
+          di = dn - f * dui;
+          dui = dun;
+        } else {
+          const double f = di / li;
+          fl[IX(i)] = f; rd[IX(i)] = 1.0 / li; u1[IX(i)] = dn; u2[IX(i)] = dun; ipv[IX(i)] = 1;
+          di = dui - f * dn;
+          dui = -f * dun;
+        }
+      }
+      {
+        const double piv = (fabs(di) < pert) ? copysign(pert, di == 0.0 ? 1.0 : di) : di;
+        rd[IX(n - 1)] = 1.0 / piv;
+      }
+      for (int i = 0; i < n; ++i) b[IX(i)] = tgk_rand(seed * 0x2545F4914F6CDD1Dull + (unsigned long long)j, i);
+      const int iters = (j1 - j0 > 1) ? 3 : 2;
+      for (int it = 0; it < iters; ++it) {
+        // forward: L (with row interchanges), running b_i in a register
+        double bi = b[IX(0)];
+        for (int i = 0; i < n - 1; ++i) {
+          const double bn = b[IX(i + 1)];
+          const double f = fl[IX(i)];
+          if (ipv[IX(i)] == 0) { b[IX(i)] = bi; bi = bn - f * bi; }
+          else { b[IX(i)] = bn; bi = bi - f * bn; }
+        }
+        b[IX(n - 1)] = bi;
+        // backward: U with two superdiagonals, running b_{i+1}, b_{i+2} in registers
+        double x1 = bi * rd[IX(n - 1)], x2 = 0.0, bmax = fabs(x1);
+        b[IX(n - 1)] = x1;
+        for (int i = n - 2; i >= 0; --i) {
+          const double xi = (b[IX(i)] - u1[IX(i)] * x1 - u2[IX(i)] * x2) * rd[IX(i)];
+          b[IX(i)] = xi;
+          bmax = fmax(bmax, fabs(xi));
+          x2 = x1;
+          x1 = xi;
+        }
+        // orthogonalize against earlier members of the cluster (their Z columns)
+        for (int p = j0; p < j; ++p) {
+          double s = 0.0;
+          for (int i = 0; i < n; ++i) s = fma(b[IX(i)], Z[(size_t)i * k + p], s);
+          for (int i = 0; i < n; ++i) b[IX(i)] = fma(-s, Z[(size_t)i * k + p], b[IX(i)]);
+          bmax = 0.0;
+          for (int i = 0; i < n; ++i) bmax = fmax(bmax, fabs(b[IX(i)]));
+        }
+        const double sc = (bmax > 0.0) ? 1.0 / bmax : 1.0;
+        double s2 = 0.0;
+        for (int i = 0; i < n; ++i) { const double v = b[IX(i)] * sc; s2 = fma(v, v, s2); }
+        const double inv = (s2 > 0.0) ? sc / sqrt(s2) : 0.0;
+        for (int i = 0; i < n; ++i) b[IX(i)] *= inv;
+      }
+      for (int i = 0; i < n; ++i) Z[(size_t)i * k + j] = b[IX(i)];
+#undef IX
+    }
+  }
+  __syncthreads();
+}
+
+}  // namespace ssa
