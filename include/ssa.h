@@ -61,7 +61,9 @@ typedef struct {
   int32_t reorth;        /* 1 = full reorthogonalization (sec 3.2.2) by
                             classical Gram-Schmidt with a DGKS second pass when the norm
                             drops below 1/sqrt(2) (default); 2 = always two passes.       */
-  int32_t reserved;
+  int32_t reserved;      /* flags: 1 = per-phase cycle counters (ssa_plan_profile); 2 = bidiagonal
+                            SVD by implicit-shift QR instead of TGK inverse iteration; 4 = use
+                            the long-series (multi-CTA FFT) path even when M <= 16384 (tests) */
 } ssa_options;
 
 /* Per-series outcome of ssa_decompose (device array, one entry per series). */

@@ -65,6 +65,16 @@ struct Plan {
   int ritz_slots = 0;          // CTAs of the Ritz kernel
   int tgk_slots = 0;           // CTAs of the TGK SVD kernel
   double* d_tgkw = nullptr;
+  // long-series (M > 2 kMaxSmemH) path: four-step FFT tables and buffers, Lanczos scratch
+  bool large = false;
+  double2* d_tw1 = nullptr;      // exp(-2 pi i t / (2 N1)), t < N1
+  double2* d_tw2 = nullptr;      // exp(-2 pi i t / (2 N2)), t < N2
+  double2* d_lbuf = nullptr;     // [lbuf_items][H] complex work buffers
+  int lbuf_items = 0;
+  double* d_lgsc = nullptr;      // device scalars (LgScalars)
+  double* d_lgpart = nullptr;    // partial sums
+  double* d_lgh = nullptr;       // reorth coefficients
+  double* d_lgr = nullptr;       // work vector
   int rot_cap = 0;
   size_t smem_lanczos = 0, smem_ritz = 0;
   double2* d_tw = nullptr;     // twiddles exp(-2 pi i t / M), t < H
@@ -110,5 +120,18 @@ constexpr int kSvdWarpsPerCta = 8;
 cudaError_t launch_lanczos(const Plan& p, const DecomposeArgs& a, cudaStream_t s);
 cudaError_t launch_bidiag_svd(const Plan& p, const DecomposeArgs& a, cudaStream_t s);
 cudaError_t launch_ritz(const Plan& p, const DecomposeArgs& a, cudaStream_t s);
+
+// long-series path (ssa_large_fft.cu, ssa_large_lanczos.cu)
+constexpr int kMaxLargeH = 1 << 20;  // N1, N2 <= 1024
+void large_geom(const Plan& p, int* N1, int* N2);
+cudaError_t large_set_attributes(int N1, int N2);
+cudaError_t large_lanczos_set_attributes(int m_max);
+cudaError_t large_spectrum(const Plan& p, const double* series, double2* spec, int items, cudaStream_t s);
+cudaError_t large_correlate(const Plan& p, const double2* spec, size_t spec_stride, const double* x, size_t xs, int n_in,
+                            double* out, size_t os, int n_out, int ld_out, const double* prev, size_t ps,
+                            const double* coef, double* part, int items, cudaStream_t s);
+cudaError_t large_hankelize(const Plan& p, const double* sigma, const double* U, const double* V, size_t nterm_total,
+                            double* out, cudaStream_t s);
+cudaError_t large_decompose_one(Plan& p, const DecomposeArgs& a, int b, cudaStream_t s);
 
 }  // namespace ssa

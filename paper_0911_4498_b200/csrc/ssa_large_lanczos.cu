@@ -1,0 +1,431 @@
+// ssa_large_lanczos.cu -- Golub-Kahan-Lanczos with full reorthogonalization for a series
+// too long for one CTA (BASELINE config 3: N = 2^20, L = 2^19, k = 32), one series at a
+// time with the whole GPU on it (Alg. 1, FRO PAPER.md:388-393).
+//
+// Each half-step is a short sequence of grid-wide kernels on the same stream:
+//   correlation  three-pass four-step FFT (ssa_large_fft.cu) with the recurrence term
+//                fused in the epilogue: r = X^T u_j - beta_j v_{j-1} (or X v_j - alpha_j u_j),
+//                plus per-CTA partial sums of squares;
+//   dots         h = B^T r: each CTA owns a 2048-element chunk of r (shared memory) and
+//                every warp streams whole basis rows of that chunk; per-CTA partials are
+//                then summed in a fixed order (deterministic);
+//   update       r -= B h with the rows in reverse order (recently read rows hit L2);
+//   finish       one thread: norms, the DGKS decision for a second pass, breakdown,
+//                alpha_j / beta_{j+1} in device memory; second-pass kernels read the flag
+//                and return at once when it is not needed;
+//   normalize    v = r / alpha into the basis row.
+// Convergence (the residual test of tgk.cuh on B_m) is evaluated by a one-CTA kernel and
+// read by the host every check interval; after it, the bidiagonal SVD reuses
+// bidiag_svd_tgk_kernel and the Ritz vectors come from lg_ritz (grid-wide, one pass over
+// each basis) with sign canonicalization.
+#include <stdio.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "device_common.cuh"
+#include "tgk.cuh"
+
+namespace ssa {
+
+cudaError_t large_correlate(const Plan& p, const double2* spec, size_t spec_stride, const double* x, size_t xs, int n_in,
+                            double* out, size_t os, int n_out, int ld_out, const double* prev, size_t ps,
+                            const double* coef, double* part, int items, cudaStream_t s);
+cudaError_t large_spectrum(const Plan& p, const double* series, double2* spec, int items, cudaStream_t s);
+cudaError_t launch_bidiag_svd(const Plan& p, const DecomposeArgs& a, cudaStream_t s);
+void large_geom(const Plan& p, int* N1, int* N2);
+
+constexpr int kLgChunk = 2048;  // elements per CTA in dots / update / normalize
+
+// device scalars of the long-series run
+struct LgScalars {
+  double nr;        // |r| before reorth (from the correlation partials)
+  double nrm;       // current |r|
+  double runmax;    // running max of alpha, beta
+  double res;       // last convergence estimate
+  int again;        // DGKS second pass needed
+  int stop;         // breakdown with an exhausted space: stop
+  int breakdown;    // first breakdown step
+  int extra;        // DGKS passes taken
+  int conv;         // converged flag
+  int pad;
+};
+
+__global__ void lg_sum(const double* __restrict__ part, int n, double* out) {
+  // one warp, fixed order: lane-strided partial sums then the shuffle tree
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += 32) s += part[i];
+  s = warp_sum(s);
+  if (threadIdx.x == 0) *out = s;
+}
+
+__global__ void __launch_bounds__(kThreads) lg_start(double* r, int n, int ld, uint64_t seed, uint64_t series,
+                                                     double* part) {
+  __shared__ double red[kWarps];
+  double ss = 0.0;
+  for (int t = blockIdx.x * kLgChunk + threadIdx.x; t < (blockIdx.x + 1) * kLgChunk && t < ld; t += blockDim.x) {
+    // the same counter-based generator as the batched kernel (R6)
+    uint64_t x = seed ^ (series * 0xD1B54A32D192ED03ull);
+    x += ((uint64_t)t + 1) * 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    x ^= x >> 31;
+    double v = (t < n) ? 2.0 * ((double)(x >> 11) * 0x1.0p-53) - 1.0 : 0.0;
+    r[t] = v;
+    ss = fma(v, v, ss);
+  }
+  ss = warp_sum(ss);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < kWarps; ++i) s += red[i];
+    part[blockIdx.x] = s;
+  }
+}
+
+// dots: part[row][cta] = <basis[row][chunk], r[chunk]>, rows split over warps
+__global__ void __launch_bounds__(kThreads) lg_dots(const double* __restrict__ basis, int ld, int nb,
+                                                    const double* __restrict__ r, double* part, int nchunk,
+                                                    const LgScalars* sc, int pass) {
+  if (pass == 1 && !sc->again) return;
+  if (sc->stop) return;
+  __shared__ double rs[kLgChunk];
+  const int c0 = blockIdx.x * kLgChunk;
+  const int len = min(kLgChunk, ld - c0);
+  for (int i = threadIdx.x; i < len; i += blockDim.x) rs[i] = r[c0 + i];
+  __syncthreads();
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int row = w; row < nb; row += kWarps) {
+    const double* br = basis + (size_t)row * ld + c0;
+    double s = 0.0;
+#pragma unroll 8
+    for (int i = lane; i < len; i += 32) s = fma(__ldcs(br + i), rs[i], s);
+    s = warp_sum(s);
+    if (lane == 0) part[(size_t)row * nchunk + blockIdx.x] = s;
+  }
+}
+
+// h[row] = sum over CTAs (fixed order)
+__global__ void lg_rows(const double* __restrict__ part, int nb, int nchunk, double* h, const LgScalars* sc, int pass) {
+  if (pass == 1 && !sc->again) return;
+  if (sc->stop) return;
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (w >= nb) return;
+  double s = 0.0;
+  for (int i = lane; i < nchunk; i += 32) s += part[(size_t)w * nchunk + i];
+  s = warp_sum(s);
+  if (lane == 0) h[w] = s;
+}
+
+// update: r -= sum_row h[row] basis[row] (rows in reverse), partial sums of squares
+__global__ void __launch_bounds__(kThreads) lg_update(const double* __restrict__ basis, int ld, int nb,
+                                                      const double* __restrict__ h, double* r, double* part,
+                                                      const LgScalars* sc, int pass) {
+  if (pass == 1 && !sc->again) return;
+  if (sc->stop) return;
+  __shared__ double red[kWarps];
+  const int c0 = blockIdx.x * kLgChunk;
+  double ss = 0.0;
+  for (int i = threadIdx.x; i < kLgChunk; i += blockDim.x) {
+    const int t = c0 + i;
+    if (t >= ld) break;
+    double v = r[t];
+    for (int row = nb - 1; row >= 0; --row) v = fma(-h[row], __ldcs(basis + (size_t)row * ld + t), v);
+    r[t] = v;
+    ss = fma(v, v, ss);
+  }
+  ss = warp_sum(ss);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < kWarps; ++i) s += red[i];
+    part[blockIdx.x] = s;
+  }
+}
+
+// after a reorth pass: new norm from partials (fixed order), DGKS decision
+__global__ void lg_after_pass(const double* __restrict__ part, int nchunk, LgScalars* sc, int pass, int mode) {
+  if (sc->stop) return;
+  if (pass == 1 && !sc->again) return;
+  double s = 0.0;
+  for (int i = threadIdx.x; i < nchunk; i += 32) s += part[i];
+  s = warp_sum(s);
+  if (threadIdx.x == 0) {
+    const double nn = sqrt(s);
+    const double before = (pass == 0) ? sc->nr : sc->nrm;
+    sc->nrm = nn;
+    if (pass == 0) {
+      sc->again = (mode == 2 || nn < 0.70710678118654752 * before) ? 1 : 0;
+      if (sc->again) sc->extra += 1;
+    } else {
+      sc->again = 0;
+    }
+  }
+}
+
+// coefficient = |r| (or 0 at breakdown); v = r / coef into the basis row
+__global__ void lg_coef(LgScalars* sc, double* coef_out, int step, int space_left) {
+  if (threadIdx.x != 0) return;
+  if (sc->stop) { *coef_out = 0.0; return; }
+  const double nn = sc->nrm;
+  if (!(nn > 1e-12 * sc->runmax) || nn == 0.0) {
+    if (!sc->breakdown) sc->breakdown = step;
+    *coef_out = 0.0;
+    sc->stop = 1;  // invariant subspace found: no restart on the long path (R11)
+    (void)space_left;
+  } else {
+    *coef_out = nn;
+    if (step > 0) sc->runmax = fmax(sc->runmax, nn);  // beta_1 (start vector norm) excluded
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) lg_normalize(const double* __restrict__ r, int n, int ld,
+                                                         const double* coef, double* dst) {
+  const double c = *coef;
+  const double inv = (c > 0.0) ? 1.0 / c : 0.0;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < ld) dst[t] = (t < n) ? r[t] * inv : 0.0;
+}
+
+// convergence test on B_m (tgk.cuh); alpha/beta 1-based in ab (alpha) and ab + w (beta)
+__global__ void __launch_bounds__(kThreads) lg_check(const double* __restrict__ ab, int w, int m, int k, double tol,
+                                                     double* scratch, LgScalars* sc) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* c = reinterpret_cast<double*>(smem_raw);
+  const int n = 2 * m + 1;
+  double* c2 = c + n;
+  double* c2n = c2 + n;
+  double* om = c2n + n;
+  double* res = om + kMaxK;
+  double* lohi = res + kMaxK;
+  for (int i = threadIdx.x; i < n - 1; i += blockDim.x) {
+    double v = (i & 1) ? ab[w + (i >> 1) + 2] : ab[(i >> 1) + 1];
+    c[i] = v;
+    c2[i] = v * v;
+  }
+  __syncthreads();
+  tgk_check(c, c2, c2n, m, k, ab[m + 1], om, res, lohi, scratch);
+  if (threadIdx.x == 0) {
+    double mr = 0.0;
+    for (int i = 0; i < k; ++i) mr = fmax(mr, res[i]);
+    const double rel = (om[0] > 0.0) ? mr / om[0] : 0.0;
+    sc->res = rel;
+    sc->conv = (rel <= 0.5 * tol) ? 1 : 0;
+  }
+}
+
+// Ritz vectors: out[i][t] = sum_row coef[row][i] basis[row][t], one element per thread
+__global__ void __launch_bounds__(kThreads) lg_ritz(const double* __restrict__ basis, int ld, int rows,
+                                                    const double* __restrict__ coef, int k, int n, double* out,
+                                                    double* amax, int* aidx) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  double acc[kMaxK];
+#pragma unroll
+  for (int i = 0; i < kMaxK; ++i) acc[i] = 0.0;
+  if (t < n) {
+    for (int row = 0; row < rows; ++row) {
+      const double x = __ldcs(basis + (size_t)row * ld + t);
+      const double* cr = coef + (size_t)row * k;
+#pragma unroll
+      for (int i = 0; i < kMaxK; ++i)
+        if (i < k) acc[i] = fma(__ldg(cr + i), x, acc[i]);
+    }
+#pragma unroll
+    for (int i = 0; i < kMaxK; ++i)
+      if (i < k) out[(size_t)i * n + t] = acc[i];
+  }
+  if (amax) {
+    // per-CTA argmax |out_i| (lowest index on ties) for sign canonicalization
+    __shared__ double sv[kWarps][kMaxK];
+    __shared__ int si[kWarps][kMaxK];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int i = 0; i < k; ++i) {
+      double v = (t < n) ? fabs(acc[i]) : -1.0;
+      int ix = t;
+      for (int o = 16; o > 0; o >>= 1) {
+        double v2 = __shfl_xor_sync(0xffffffffu, v, o);
+        int i2 = __shfl_xor_sync(0xffffffffu, ix, o);
+        if (v2 > v || (v2 == v && i2 < ix)) { v = v2; ix = i2; }
+      }
+      if (lane == 0) { sv[w][i] = v; si[w][i] = ix; }
+    }
+    __syncthreads();
+    if (threadIdx.x < k) {
+      double v = -1.0;
+      int ix = 0x7fffffff;
+      for (int q = 0; q < kWarps; ++q)
+        if (sv[q][threadIdx.x] > v || (sv[q][threadIdx.x] == v && si[q][threadIdx.x] < ix)) {
+          v = sv[q][threadIdx.x];
+          ix = si[q][threadIdx.x];
+        }
+      amax[(size_t)blockIdx.x * k + threadIdx.x] = v;
+      aidx[(size_t)blockIdx.x * k + threadIdx.x] = ix;
+    }
+  }
+}
+
+__global__ void lg_sign(const double* __restrict__ amax, const int* __restrict__ aidx, int nblk, int k,
+                        const double* __restrict__ U, int L, double* sgn) {
+  const int i = threadIdx.x;
+  if (i >= k) return;
+  double v = -1.0;
+  int ix = 0x7fffffff;
+  for (int b = 0; b < nblk; ++b) {
+    const double v2 = amax[(size_t)b * k + i];
+    const int i2 = aidx[(size_t)b * k + i];
+    if (v2 > v || (v2 == v && i2 < ix)) { v = v2; ix = i2; }
+  }
+  sgn[i] = (ix < L && U[(size_t)i * L + ix] < 0.0) ? -1.0 : 1.0;
+}
+
+__global__ void lg_flip(double* X, int n, int k, const double* __restrict__ sgn) {
+  const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (size_t)n * k) return;
+  const int i = (int)(idx / n);
+  if (sgn[i] < 0.0) X[idx] = -X[idx];
+}
+
+size_t lg_check_smem(int m_max) { return (size_t)(3 * (2 * m_max + 1) + 4 * kMaxK) * 8 + 64; }
+
+cudaError_t large_lanczos_set_attributes(int m_max) {
+  return cudaFuncSetAttribute(lg_check, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lg_check_smem(m_max));
+}
+
+__global__ void lg_set_nr(const double* __restrict__ part, int n, LgScalars* sc) {
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += 32) s += part[i];
+  s = warp_sum(s);
+  if (threadIdx.x == 0) {
+    sc->nr = sqrt(s);
+    sc->nrm = sc->nr;
+    sc->again = 0;
+  }
+}
+
+__global__ void lg_finite(const double* __restrict__ f, int N, int* state) {
+  int bad = 0;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) bad |= !isfinite(f[i]);
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(state + 5, 1);
+}
+
+__global__ void lg_state(const LgScalars* sc, int* state, int m) {
+  if (threadIdx.x != 0) return;
+  state[0] = m;
+  state[1] = sc->conv;
+  state[2] = sc->breakdown;
+  state[3] = sc->extra;
+  state[4] = 0;
+  state[6] = 0;
+}
+
+// One long series b of the call: decompose into sigma/U/V (+info).  Host-driven loop; the
+// host reads the device scalars only at convergence tests.
+cudaError_t large_decompose_one(Plan& p, const DecomposeArgs& a0, int b, cudaStream_t s) {
+  DecomposeArgs a = a0;
+  a.b0 = b;
+  a.nb = 1;
+  const int L = (int)p.L, K = (int)p.K, N = (int)p.N, k = p.k;
+  const int ldL = p.ldL, ldK = p.ldK;
+  const int nchL = (ldL + kLgChunk - 1) / kLgChunk, nchK = (ldK + kLgChunk - 1) / kLgChunk;
+  int N1, N2;
+  large_geom(p, &N1, &N2);
+  const int ncol = N2 / 8;  // partial sums written by large_col_inv
+  double* U = p.d_U;
+  double* V = p.d_V;
+  const int w = p.m_max + 3;
+  double* alpha = p.d_ab;
+  double* beta = p.d_ab + w;
+  LgScalars* sc = reinterpret_cast<LgScalars*>(p.d_lgsc);
+  double* part = p.d_lgpart;
+  double* h = p.d_lgh;
+  double* r = p.d_lgr;
+  cudaError_t e;
+  if ((e = cudaMemsetAsync(p.d_state, 0, 8 * sizeof(int), s))) return e;
+  lg_finite<<<64, kThreads, 0, s>>>(a.series + (size_t)b * N, N, p.d_state);
+  if ((e = large_spectrum(p, a.series + (size_t)b * N, p.d_spec, 1, s))) return e;
+  LgScalars z{};
+  if ((e = cudaMemcpyAsync(sc, &z, sizeof(z), cudaMemcpyHostToDevice, s))) return e;
+  if ((e = cudaMemsetAsync(p.d_ab, 0, 2 * (size_t)w * 8, s))) return e;
+  // Alg. 1 lines 1-2: u_1 = p0 / |p0|
+  lg_start<<<nchL, kThreads, 0, s>>>(r, L, ldL, a.seed, (uint64_t)b, part);
+  lg_set_nr<<<1, 32, 0, s>>>(part, nchL, sc);
+  {
+    // beta_1 = |p0| into beta[1], then normalize
+    lg_coef<<<1, 32, 0, s>>>(sc, beta + 1, 0, 1);
+    lg_normalize<<<(ldL + kThreads - 1) / kThreads, kThreads, 0, s>>>(r, L, ldL, beta + 1, U);
+  }
+  auto reorth = [&](const double* basis, int ld, int nb, int nch) {
+    for (int pass = 0; pass < 2 && nb > 0; ++pass) {
+      lg_dots<<<nch, kThreads, 0, s>>>(basis, ld, nb, r, part, nch, sc, pass);
+      lg_rows<<<(nb * 32 + kThreads - 1) / kThreads, kThreads, 0, s>>>(part, nb, nch, h, sc, pass);
+      lg_update<<<nch, kThreads, 0, s>>>(basis, ld, nb, h, r, part, sc, pass);
+      lg_after_pass<<<1, 32, 0, s>>>(part, nch, sc, pass, p.opt.reorth);
+    }
+  };
+  int m = 0;
+  int next_check = (2 * k < p.m_max) ? 2 * k : k;
+  const int ce = p.opt.check_every > 0 ? p.opt.check_every : 4;
+  double prev_res = -1.0;
+  int prev_m = 0;
+  LgScalars hs{};
+  for (int j = 1; j <= p.m_max + 1; ++j) {
+    // ---- half-step A (Alg. 1 l.4-5): r = X^T u_j - beta_j v_{j-1}; FRO vs V_{j-1} ----
+    if ((e = large_correlate(p, p.d_spec, 0, U + (size_t)(j - 1) * ldL, 0, L, r, 0, K, ldK,
+                             (j > 1) ? V + (size_t)(j - 2) * ldK : nullptr, 0, beta + j, part, 1, s)))
+      return e;
+    lg_set_nr<<<1, 32, 0, s>>>(part, ncol, sc);
+    reorth(V, ldK, j - 1, nchK);
+    lg_coef<<<1, 32, 0, s>>>(sc, alpha + j, j, j - 1 < K);
+    lg_normalize<<<(ldK + kThreads - 1) / kThreads, kThreads, 0, s>>>(r, K, ldK, alpha + j, V + (size_t)(j - 1) * ldK);
+    m = j - 1;
+    const bool last = (m >= p.m_max);
+    if (m >= k && (m >= next_check || last)) {
+      lg_check<<<1, kThreads, lg_check_smem(p.m_max), s>>>(p.d_ab, w, m, k, p.opt.tol, p.d_tgk, sc);
+      if ((e = cudaMemcpyAsync(&hs, sc, sizeof(hs), cudaMemcpyDeviceToHost, s))) return e;
+      if ((e = cudaStreamSynchronize(s))) return e;
+      if (hs.conv) break;
+      int step = ce;
+      if (prev_res > 0.0 && hs.res < prev_res && hs.res > 0.0) {
+        double rate = log(hs.res / prev_res) / (double)(m - prev_m);
+        double need = log(0.5 * p.opt.tol / hs.res) / rate;
+        int s2 = (int)(0.7 * need);
+        if (s2 > step) step = s2 < 2 * ce ? s2 : 2 * ce;
+      }
+      prev_res = hs.res;
+      prev_m = m;
+      next_check = m + step;
+    }
+    if (last) break;
+    // ---- half-step B (Alg. 1 l.6-7): p = X v_j - alpha_j u_j; FRO vs U_j ----
+    if ((e = large_correlate(p, p.d_spec, 0, V + (size_t)(j - 1) * ldK, 0, K, r, 0, L, ldL,
+                             U + (size_t)(j - 1) * ldL, 0, alpha + j, part, 1, s)))
+      return e;
+    lg_set_nr<<<1, 32, 0, s>>>(part, ncol, sc);
+    reorth(U, ldL, j, nchL);
+    lg_coef<<<1, 32, 0, s>>>(sc, beta + j + 1, j, j < L);
+    lg_normalize<<<(ldL + kThreads - 1) / kThreads, kThreads, 0, s>>>(r, L, ldL, beta + j + 1, U + (size_t)j * ldL);
+  }
+  lg_state<<<1, 32, 0, s>>>(sc, p.d_state, m);
+  // ---- bidiagonal SVD (reuses the batched kernel with one series) ----
+  if ((e = cudaMemsetAsync(p.d_counters, 0, 4 * sizeof(int), s))) return e;
+  if ((e = launch_bidiag_svd(p, a, s))) return e;
+  // ---- Ritz vectors + sign canonicalization ----
+  const int mstride = p.m_max + 2;
+  const double* cP = p.d_coef;
+  const double* cQ = p.d_coef + (size_t)mstride * k;
+  double* Uo = a.Uout + (size_t)b * k * L;
+  double* Vo = a.Vout + (size_t)b * k * K;
+  const int gU = (L + kThreads - 1) / kThreads, gV = (K + kThreads - 1) / kThreads;
+  double* amax = p.d_lgpart;
+  int* aidx = reinterpret_cast<int*>(p.d_lgpart + (size_t)gU * k);
+  lg_ritz<<<gU, kThreads, 0, s>>>(U, ldL, m + 1, cP, k, L, Uo, amax, aidx);
+  lg_ritz<<<gV, kThreads, 0, s>>>(V, ldK, m, cQ, k, K, Vo, nullptr, nullptr);
+  lg_sign<<<1, 32, 0, s>>>(amax, aidx, gU, k, Uo, L, h);
+  lg_flip<<<(int)(((size_t)L * k + kThreads - 1) / kThreads), kThreads, 0, s>>>(Uo, L, k, h);
+  lg_flip<<<(int)(((size_t)K * k + kThreads - 1) / kThreads), kThreads, 0, s>>>(Vo, K, k, h);
+  return cudaGetLastError();
+}
+
+}  // namespace ssa

@@ -124,7 +124,7 @@ class Plan:
 
     def __init__(self, N: int, L: int, k: int, batch: int, *, tol: float = 1e-12, max_steps: int = 0,
                  check_every: int = 4, seed: int = 42, reorth: int = 1, device: int | None = None,
-                 profile: bool = False, svd: str = "tgk"):
+                 profile: bool = False, svd: str = "tgk", force_long: bool = False):
         import torch
         lib = load_library()
         if not torch.cuda.is_available():
@@ -133,7 +133,7 @@ class Plan:
         opt = Options()
         _check(lib.ssa_options_default(ctypes.byref(opt)))
         opt.tol, opt.max_steps, opt.check_every, opt.seed, opt.reorth = tol, max_steps, check_every, seed, reorth
-        opt.reserved = (1 if profile else 0) | (2 if svd == "qr" else 0)
+        opt.reserved = (1 if profile else 0) | (2 if svd == "qr" else 0) | (4 if force_long else 0)
         h = ctypes.c_void_p()
         _check(lib.ssa_plan_create(N, L, k, batch, ctypes.byref(opt), self.device, ctypes.byref(h)))
         self._h = h

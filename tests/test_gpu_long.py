@@ -1,0 +1,118 @@
+"""GPU parity of the long-series path (M > 16384: four-step FFT through L2, grid-wide
+Lanczos; BASELINE configs 3 and 5).  The same kernels are forced onto small problems
+(force_long) so the full oracle (Jacobi SVD) can check them; at the real sizes the
+products and Hankelizations are compared with the oracle's direct O(LK) sums."""
+import numpy as np
+import pytest
+
+import oracle
+import parity
+import ssa_inputs
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_0911_4498_b200 as pkg
+    return pkg
+
+
+def cuda(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).cuda()
+
+
+def nrel(a, b):
+    return np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
+@pytest.mark.parametrize("N,L,force", [(200, 77, True), (1000, 500, True), (4096, 1000, True), (32768, 16384, False),
+                                       (40000, 9000, False)])
+def test_long_spectrum_and_matvec(P, N, L, force):
+    rng = np.random.default_rng(N + L)
+    K = N - L + 1
+    B = 2
+    F = rng.standard_normal((B, N)); x = rng.standard_normal((B, K)); u = rng.standard_normal((B, L))
+    plan = P.Plan(N, L, 0, B, force_long=force)
+    spec = plan.spectrum(cuda(F))
+    S = spec.cpu().numpy()
+    ref = np.fft.rfft(F, plan.M)   # library cross-check of the spectrum only
+    assert np.abs(S[..., 0] + 1j * S[..., 1] - ref).max() <= 1e-12 * np.abs(ref).max()
+    y = plan.matvec(spec, cuda(x)).cpu().numpy()
+    z = plan.matvec(spec, cuda(u), transpose=True).cpu().numpy()
+    for b in range(B):
+        assert nrel(y[b], oracle.matvec(F[b], L, x[b])) <= 1e-12
+        assert nrel(z[b], oracle.matvec(F[b], L, u[b], True)) <= 1e-12
+
+
+@pytest.mark.parametrize("N,L,force", [(300, 100, True), (4096, 2048, True), (32768, 16384, False)])
+def test_long_hankelize(P, N, L, force):
+    rng = np.random.default_rng(3 * N + L)
+    K = N - L + 1
+    B, T = 2, 3
+    s = rng.uniform(0.5, 2, (B, T)); U = rng.standard_normal((B, T, L)); V = rng.standard_normal((B, T, K))
+    plan = P.Plan(N, L, 0, B, force_long=force)
+    g = plan.hankelize(cuda(s), cuda(U), cuda(V)).cpu().numpy()
+    for b in range(B):
+        for i in range(T):
+            assert nrel(g[b, i], oracle.hankelize_rank1(s[b, i], U[b, i], V[b, i])) <= 1e-12
+
+
+def test_cfg5_shape_sampled_terms(P):
+    """BASELINE configs[4] shape (N = 262144, L = 131072), problem 0, first 4 terms."""
+    c = ssa_inputs.CONFIGS["cfg5"]
+    N, L = c["N"], c["L"]
+    sig, U, V = ssa_inputs.cfg5_problem(0, N, L, terms=4)
+    plan = P.Plan(N, L, 0, 1)
+    g = plan.hankelize(cuda(sig[None]), cuda(U[None]), cuda(V[None])).cpu().numpy()
+    for i in (0, 3):
+        ref = oracle.hankelize_rank1(sig[i], U[i], V[i])
+        assert nrel(g[0, i], ref) <= 1e-10
+
+
+@pytest.mark.parametrize("N,L,k", [(1024, 512, 10), (600, 250, 8), (4096, 2048, 16)])
+def test_long_decompose_vs_oracle(P, N, L, k):
+    """The long-series Lanczos path forced onto sizes the Jacobi oracle can do."""
+    if N == 1024:
+        f = ssa_inputs.cfg1_series(N)
+    elif N == 4096:
+        f = ssa_inputs.cfg3_like_series(N)
+    else:
+        rng = np.random.default_rng(5)
+        n = np.arange(1, N + 1)
+        f = np.sin(2 * np.pi * n / 11.3) + 0.2 * rng.standard_normal(N)
+    plan = P.Plan(N, L, k, 1, force_long=True)
+    sigma, U, V, info = plan.decompose(cuda(f[None]))
+    G = plan.reconstruct(sigma, U, V)
+    torch.cuda.synchronize()
+    inf = P.info_to_numpy(info)[0]
+    assert inf["status"] == 0, inf
+    s_ref, U_ref, V_ref, _ = oracle.svd(f, L, k + 1)
+    G_ref = np.stack([oracle.hankelize_rank1(s_ref[i], U_ref[i], V_ref[i]) for i in range(k)])
+    rep = parity.compare(s_ref, U_ref, V_ref, sigma.cpu().numpy()[0], U.cpu().numpy()[0], V.cpu().numpy()[0], k,
+                         G_ref, G.cpu().numpy()[0], recon_scale=np.linalg.norm(f))
+    assert rep.ok(), rep.failures
+
+
+def test_cfg3_like_long_series_residuals(P):
+    """N = 2^17 (cfg3 generator): the oracle cannot do the SVD, so check true residuals
+    with its direct product, orthonormality and the Frobenius bound."""
+    N, L, k = 1 << 17, 1 << 16, 16
+    f = ssa_inputs.cfg3_like_series(N)
+    plan = P.Plan(N, L, k, 1)
+    sigma, U, V, info = plan.decompose(cuda(f[None]))
+    torch.cuda.synchronize()
+    inf = P.info_to_numpy(info)[0]
+    assert inf["status"] == 0, inf
+    s = sigma.cpu().numpy()[0]; Uh = U.cpu().numpy()[0]; Vh = V.cpu().numpy()[0]
+    assert np.all(np.diff(s) <= 0)
+    assert np.abs(Uh @ Uh.T - np.eye(k)).max() <= 1e-12
+    assert np.abs(Vh @ Vh.T - np.eye(k)).max() <= 1e-12
+    K = N - L + 1
+    cnt = np.minimum.reduce([np.arange(1, N + 1), np.full(N, L), np.full(N, K), N - np.arange(N)])
+    assert (s * s).sum() <= (f * f * cnt).sum() * (1 + 1e-12)
+    for i in (0, 1, k - 1):
+        r1 = np.linalg.norm(oracle.matvec(f, L, Vh[i]) - s[i] * Uh[i])
+        r2 = np.linalg.norm(oracle.matvec(f, L, Uh[i], True) - s[i] * Vh[i])
+        assert max(r1, r2) <= 1e-10 * s[0], (i, r1, r2)
