@@ -42,14 +42,15 @@ __device__ __forceinline__ int block_or(int v, int* redi) {
 // Forward real post-processing for the pair (p, H-p) from digit-reversed Z:
 //   X_p = E + W^p O,  X_{H-p} = conj(E - W^p O),  E = (Z_p + conj Z_{H-p})/2,
 //   O = -i (Z_p - conj Z_{H-p})/2,  W = exp(-2 pi i / M).
-__device__ __forceinline__ void real_pair(const double2* buf, const FftShape& sh, const double2* __restrict__ T,
-                                          int p, double2& Xp, double2& Xq, int& pr, int& qr) {
+template <class TW>
+__device__ __forceinline__ void real_pair(const double2* buf, const FftShape& sh, const TW& tw, int p, double2& Xp,
+                                          double2& Xq, int& pr, int& qr) {
   const int H = sh.H;
   const int q = (H - p) & (H - 1);
   pr = rev_index(sh, p);
   qr = rev_index(sh, q);
   double2 Zp = buf[fpad(pr)], Zq = buf[fpad(qr)];
-  double2 W = twiddle(T, p, H);
+  double2 W = tw(p);
   double2 E = make_double2(0.5 * (Zp.x + Zq.x), 0.5 * (Zp.y - Zq.y));
   double2 D = make_double2(0.5 * (Zp.x - Zq.x), 0.5 * (Zp.y + Zq.y));
   double2 O = make_double2(D.y, -D.x);  // -i D
@@ -61,9 +62,9 @@ __device__ __forceinline__ void real_pair(const double2* buf, const FftShape& sh
 // Inverse pre-processing: from half-spectrum values Y_p, Y_{H-p} of a real sequence
 // produce Z'_p = E + i O, Z'_{H-p} = conj(E) + i conj(O), E = (Y_p + conj Y_{H-p})/2,
 // O = (Y_p - conj Y_{H-p}) conj(W^p) / 2, whose inverse FFT is y_2n + i y_2n+1.
-__device__ __forceinline__ void inv_pair(double2* buf, const double2* __restrict__ T, int H, int p, int pr, int qr,
-                                         double2 Yp, double2 Yq) {
-  double2 W = twiddle(T, p, H);
+template <class TW>
+__device__ __forceinline__ void inv_pair(double2* buf, const TW& tw, int p, int pr, int qr, double2 Yp, double2 Yq) {
+  double2 W = tw(p);
   double2 E = make_double2(0.5 * (Yp.x + Yq.x), 0.5 * (Yp.y - Yq.y));
   double2 D = make_double2(0.5 * (Yp.x - Yq.x), 0.5 * (Yp.y + Yq.y));
   double2 O = cmulc(D, W);
@@ -73,7 +74,8 @@ __device__ __forceinline__ void inv_pair(double2* buf, const double2* __restrict
 
 // Correlation spectrum step: Z (digit-reversed FFT of packed x) -> Z' whose inverse is
 // the packed correlation y = irfft(F^ conj(X^)).
-__device__ __forceinline__ void corr_pairs(double2* buf, const FftShape& sh, const double2* __restrict__ T,
+template <class TW>
+__device__ __forceinline__ void corr_pairs(double2* buf, const FftShape& sh, const TW& T,
                                            const double2* __restrict__ spec, int tid, int nthr) {
   const int H = sh.H;
   for (int p = tid; p <= (H >> 1); p += nthr) {
@@ -81,17 +83,23 @@ __device__ __forceinline__ void corr_pairs(double2* buf, const FftShape& sh, con
     int pr, qr;
     real_pair(buf, sh, T, p, Xp, Xq, pr, qr);
     double2 Fp = __ldg(spec + p), Fq = __ldg(spec + (H - p));
-    inv_pair(buf, T, H, p, pr, qr, cmulc(Fp, Xp), cmulc(Fq, Xq));
+    inv_pair(buf, T, p, pr, qr, cmulc(Fp, Xp), cmulc(Fq, Xq));
   }
 }
 
 // Full correlation in one CTA (all threads): y_t = sum_s f_{t+s} x_s, t < n_out
 // (the Hankel products of Alg. 2 / Alg. 3, in correlation form).
-template <class LoadX, class StoreY>
-__device__ __forceinline__ void correlate_cta(double2* buf, const FftShape& sh, const double2* __restrict__ T,
+template <class TW, class LoadX, class StoreY>
+__device__ __forceinline__ void correlate_cta(double2* buf, const FftShape& sh, const TW& T,
                                               const double2* __restrict__ spec, int n_in, int n_out, LoadX loadx,
                                               StoreY storey) {
   const int H = sh.H, tid = threadIdx.x, nthr = blockDim.x;
+  // pull this thread's spectrum entries of the pair step towards L2 now (they are used
+  // after the forward transform; from HBM their latency would stall that step)
+  for (int p = tid; p <= (H >> 1); p += nthr) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(spec + p));
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(spec + (H - p)));
+  }
   for (int n = tid; n < H; n += nthr) {
     int i0 = 2 * n;
     double a = (i0 < n_in) ? loadx(i0) : 0.0;
@@ -190,5 +198,13 @@ __device__ __forceinline__ void stream_rows(const double* base_w, int ld, int nb
 }
 
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
+
+// Copy the two-level twiddle table of size M (global, lo then hi) into shared memory
+// (all threads; caller synchronizes).
+__device__ __forceinline__ TwSmem load_tw2(const double2* __restrict__ g, double2* sm, int M) {
+  const int n = tw2_entries(M);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) sm[i] = __ldg(g + i);
+  return TwSmem{sm, sm + 64};
+}
 
 }  // namespace ssa

@@ -43,6 +43,25 @@ __device__ __forceinline__ double2 twiddle(const double2* __restrict__ T, int t,
   return make_double2(-w.x, -w.y);
 }
 
+// Twiddle accessors: exp(-2 pi i t / M) for t in [0, M).
+//  TwGlobal: the half table T[t] = exp(-2 pi i t / M), t < H, in global memory.
+//  TwSmem:   two-level table in shared memory, lo[j] = exp(-2 pi i j / M) (j < 64) and
+//            hi[j] = exp(-2 pi i 64 j / M) (j < max(1, M/64)); one complex product per lookup
+//            (error ~1 ulp more than a direct table), 5 KB at M = 16384 -- the direct table
+//            would not stay in L1 next to 100+ KB of shared memory per CTA.
+struct TwGlobal {
+  const double2* T;
+  int H;
+  __device__ __forceinline__ double2 operator()(int t) const { return twiddle(T, t, H); }
+};
+struct TwSmem {
+  const double2* lo;
+  const double2* hi;
+  __device__ __forceinline__ double2 operator()(int t) const { return cmul(lo[t & 63], hi[t >> 6]); }
+};
+// entries of the two-level table for size M (lo then hi)
+__host__ __device__ inline int tw2_entries(int M) { return 64 + (M / 64 > 1 ? M / 64 : 1); }
+
 // Shape: n8 radix-8 passes then one radix-2^lastb pass (lastb in {0,1,2}).
 struct FftShape {
   int H, logH, n8, lastb;
@@ -129,9 +148,8 @@ __device__ __forceinline__ void dftR(double2* a) {
 // Q = S / R.  Butterfly (b, n1):
 //   forward: y[n1 + Q k2] = W_S^{n1 k2} * sum_{n2} x[n1 + Q n2] W_R^{n2 k2}
 //   inverse: x[n1 + Q n2] = sum_{k2} W_R^{-n2 k2} W_S^{-n1 k2} y[n1 + Q k2]   (times R)
-template <int LR, bool INV>
-__device__ __forceinline__ void fft_pass(double2* buf, int H, int logH, int logS, const double2* __restrict__ T,
-                                         int tid, int nthr) {
+template <int LR, bool INV, class TW>
+__device__ __forceinline__ void fft_pass(double2* buf, int H, int logH, int logS, const TW& tw, int tid, int nthr) {
   constexpr int R = 1 << LR;
   const int logQ = logS - LR;
   const int Q = 1 << logQ;
@@ -142,14 +160,23 @@ __device__ __forceinline__ void fft_pass(double2* buf, int H, int logH, int logS
     double2 a[R];
 #pragma unroll
     for (int q = 0; q < R; ++q) a[q] = buf[fpad(base + (q << logQ))];
+    double2 w[R];
+    if (Q > 1) {
+      // w_q = W_S^{n1 q} = (W_S^{n1})^q: one table lookup, powers by products
+      w[1] = tw(n1 << tshift);
+      if constexpr (R >= 4) { w[2] = cmul(w[1], w[1]); w[3] = cmul(w[2], w[1]); }
+      if constexpr (R == 8) {
+        w[4] = cmul(w[2], w[2]); w[5] = cmul(w[4], w[1]); w[6] = cmul(w[4], w[2]); w[7] = cmul(w[4], w[3]);
+      }
+    }
     if (INV && Q > 1) {
 #pragma unroll
-      for (int q = 1; q < R; ++q) a[q] = cmulc(a[q], twiddle(T, (n1 * q) << tshift, H));
+      for (int q = 1; q < R; ++q) a[q] = cmulc(a[q], w[q]);
     }
     dftR<R, INV>(a);
     if (!INV && Q > 1) {
 #pragma unroll
-      for (int q = 1; q < R; ++q) a[q] = cmul(a[q], twiddle(T, (n1 * q) << tshift, H));
+      for (int q = 1; q < R; ++q) a[q] = cmul(a[q], w[q]);
     }
 #pragma unroll
     for (int q = 0; q < R; ++q) buf[fpad(base + (q << logQ))] = a[q];
@@ -162,31 +189,59 @@ struct CtaSync {
 
 // Forward FFT of H points in place (natural -> digit-reversed).  Caller must have
 // synchronized after writing buf; returns after a final barrier.
-template <class Sync>
-__device__ void fft_forward(double2* buf, const FftShape& s, const double2* __restrict__ T, int tid, int nthr,
-                            Sync sync) {
-  int logS = s.logH;
-  for (int p = 0; p < s.n8; ++p) {
-    fft_pass<3, false>(buf, s.H, s.logH, logS, T, tid, nthr);
-    logS -= 3;
-    sync();
+// Whole transform with a compile-time size (all index arithmetic folds to constants).
+template <int LOGH, bool INV, class TW, class Sync>
+__device__ __forceinline__ void fft_run_t(double2* buf, const TW& T, int tid, int nthr, Sync sync) {
+  constexpr int N8 = LOGH / 3, LB = LOGH - 3 * N8, H = 1 << LOGH;
+  if constexpr (!INV) {
+#pragma unroll
+    for (int p = 0; p < N8; ++p) {
+      fft_pass<3, false>(buf, H, LOGH, LOGH - 3 * p, T, tid, nthr);
+      sync();
+    }
+    if constexpr (LB == 2) { fft_pass<2, false>(buf, H, LOGH, LB, T, tid, nthr); sync(); }
+    if constexpr (LB == 1) { fft_pass<1, false>(buf, H, LOGH, LB, T, tid, nthr); sync(); }
+  } else {
+    if constexpr (LB == 2) { fft_pass<2, true>(buf, H, LOGH, LB, T, tid, nthr); sync(); }
+    if constexpr (LB == 1) { fft_pass<1, true>(buf, H, LOGH, LB, T, tid, nthr); sync(); }
+#pragma unroll
+    for (int p = N8 - 1; p >= 0; --p) {
+      fft_pass<3, true>(buf, H, LOGH, LOGH - 3 * p, T, tid, nthr);
+      sync();
+    }
   }
-  if (s.lastb == 2) { fft_pass<2, false>(buf, s.H, s.logH, logS, T, tid, nthr); sync(); }
-  else if (s.lastb == 1) { fft_pass<1, false>(buf, s.H, s.logH, logS, T, tid, nthr); sync(); }
+}
+
+template <bool INV, class TW, class Sync>
+__device__ __forceinline__ void fft_run(double2* buf, int logH, const TW& T, int tid, int nthr, Sync sync) {
+  switch (logH) {
+    case 1: fft_run_t<1, INV>(buf, T, tid, nthr, sync); break;
+    case 2: fft_run_t<2, INV>(buf, T, tid, nthr, sync); break;
+    case 3: fft_run_t<3, INV>(buf, T, tid, nthr, sync); break;
+    case 4: fft_run_t<4, INV>(buf, T, tid, nthr, sync); break;
+    case 5: fft_run_t<5, INV>(buf, T, tid, nthr, sync); break;
+    case 6: fft_run_t<6, INV>(buf, T, tid, nthr, sync); break;
+    case 7: fft_run_t<7, INV>(buf, T, tid, nthr, sync); break;
+    case 8: fft_run_t<8, INV>(buf, T, tid, nthr, sync); break;
+    case 9: fft_run_t<9, INV>(buf, T, tid, nthr, sync); break;
+    case 10: fft_run_t<10, INV>(buf, T, tid, nthr, sync); break;
+    case 11: fft_run_t<11, INV>(buf, T, tid, nthr, sync); break;
+    case 12: fft_run_t<12, INV>(buf, T, tid, nthr, sync); break;
+    default: fft_run_t<13, INV>(buf, T, tid, nthr, sync); break;
+  }
+}
+
+// Forward FFT of H points in place (natural -> digit-reversed).  Caller must have
+// synchronized after writing buf; returns after a final barrier.
+template <class TW, class Sync>
+__device__ __forceinline__ void fft_forward(double2* buf, const FftShape& s, const TW& T, int tid, int nthr, Sync sync) {
+  fft_run<false>(buf, s.logH, T, tid, nthr, sync);
 }
 
 // Inverse (unnormalized, x H) FFT in place (digit-reversed -> natural).
-template <class Sync>
-__device__ void fft_inverse(double2* buf, const FftShape& s, const double2* __restrict__ T, int tid, int nthr,
-                            Sync sync) {
-  int logS = s.logH - 3 * s.n8;  // block size seen by the last forward pass
-  if (s.lastb == 2) { fft_pass<2, true>(buf, s.H, s.logH, logS, T, tid, nthr); sync(); }
-  else if (s.lastb == 1) { fft_pass<1, true>(buf, s.H, s.logH, logS, T, tid, nthr); sync(); }
-  for (int p = 0; p < s.n8; ++p) {
-    logS += 3;
-    fft_pass<3, true>(buf, s.H, s.logH, logS, T, tid, nthr);
-    sync();
-  }
+template <class TW, class Sync>
+__device__ __forceinline__ void fft_inverse(double2* buf, const FftShape& s, const TW& T, int tid, int nthr, Sync sync) {
+  fft_run<true>(buf, s.logH, T, tid, nthr, sync);
 }
 
 }  // namespace ssa

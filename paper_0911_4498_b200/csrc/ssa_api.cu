@@ -69,8 +69,21 @@ static std::vector<double2> make_twiddles(int64_t M) {
   return tw;
 }
 
+// Two-level table for size M: lo[j] = exp(-2 pi i j / M), j < 64; hi[j] = exp(-2 pi i 64 j / M).
+static std::vector<double2> make_twiddles2(int64_t M) {
+  const int nhi = (int)std::max<int64_t>(1, M / 64);
+  std::vector<double2> tw((size_t)(64 + nhi));
+  for (int j = 0; j < 64 + nhi; ++j) {
+    const long double t = (j < 64) ? (long double)j : 64.0L * (long double)(j - 64);
+    long double ang = 2.0L * 3.14159265358979323846264338327950288L * t / (long double)M;
+    tw[(size_t)j].x = (double)cosl(ang);
+    tw[(size_t)j].y = (double)(-sinl(ang));
+  }
+  return tw;
+}
+
 static void free_plan(Plan& p) {
-  void* ptrs[] = {p.d_tw, p.d_spec, p.d_U, p.d_V, p.d_ab, p.d_state, p.d_tgk, p.d_rot, p.d_vecs, p.d_coef,
+  void* ptrs[] = {p.d_tw, p.d_twl, p.d_spec, p.d_U, p.d_V, p.d_ab, p.d_state, p.d_tgk, p.d_rot, p.d_vecs, p.d_coef,
                   p.d_info, p.d_counters, p.d_hscratch, p.d_prof, p.d_tgkw, p.d_tw1, p.d_tw2, p.d_lbuf,
                   p.d_lgsc, p.d_lgpart, p.d_lgh, p.d_lgr, p.d_series, p.d_sigma, p.d_Uout, p.d_Vout,
                   p.d_recon};
@@ -236,9 +249,11 @@ extern "C" ssa_status ssa_plan_create(int64_t N, int64_t L, int32_t k, int64_t b
     if (e != cudaSuccess) { st = cuda_fail(e, "cudaEventCreate"); goto bad; }
   }
   {
-    std::vector<double2> tw = make_twiddles(M);
+    std::vector<double2> tw = make_twiddles(M), twl = make_twiddles2(M);
     if ((st = alloc((void**)&p.d_tw, tw.size() * sizeof(double2), "twiddles")) != SSA_OK) goto bad;
+    if ((st = alloc((void**)&p.d_twl, twl.size() * sizeof(double2), "twiddles")) != SSA_OK) goto bad;
     e = cudaMemcpy(p.d_tw, tw.data(), tw.size() * sizeof(double2), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMemcpy(p.d_twl, twl.data(), twl.size() * sizeof(double2), cudaMemcpyHostToDevice);
     if (e != cudaSuccess) { st = cuda_fail(e, "twiddle upload"); goto bad; }
     const char* which = "";
     e = (H <= ssa::kMaxSmemH) ? ssa::fft_set_attributes((int)H, &which) : cudaSuccess;
@@ -253,7 +268,7 @@ extern "C" ssa_status ssa_plan_create(int64_t N, int64_t L, int32_t k, int64_t b
     p.large = true;
     int N1, N2;
     ssa::large_geom(p, &N1, &N2);
-    std::vector<double2> t1 = make_twiddles(2 * (int64_t)N1), t2 = make_twiddles(2 * (int64_t)N2);
+    std::vector<double2> t1 = make_twiddles2(2 * (int64_t)N1), t2 = make_twiddles2(2 * (int64_t)N2);
     if ((st = alloc((void**)&p.d_tw1, t1.size() * 16, "twiddles N1")) != SSA_OK) goto bad;
     if ((st = alloc((void**)&p.d_tw2, t2.size() * 16, "twiddles N2")) != SSA_OK) goto bad;
     e = cudaMemcpy(p.d_tw1, t1.data(), t1.size() * 16, cudaMemcpyHostToDevice);
@@ -368,7 +383,7 @@ extern "C" ssa_status ssa_decompose(ssa_plan_t plan, const double* d_series, dou
   a.m_max = p.m_max; a.ldL = p.ldL; a.ldK = p.ldK;
   a.check_every = p.opt.check_every; a.reorth_mode = p.opt.reorth;
   a.tol = p.opt.tol; a.seed = p.opt.seed;
-  a.series = d_series; a.spec = p.d_spec; a.tw = p.d_tw;
+  a.series = d_series; a.spec = p.d_spec; a.tw = p.d_twl;
   a.U = p.d_U; a.V = p.d_V; a.ab = p.d_ab; a.state = p.d_state;
   a.tgk = p.d_tgk; a.tgk_stride = (size_t)p.k * (2 * p.m_max + 2);
   a.rot = p.d_rot; a.rot_cap = p.rot_cap; a.svd_slots = p.svd_slots;

@@ -17,6 +17,7 @@ __global__ void __launch_bounds__(kThreads) spectrum_kernel(const double* __rest
                                                             const double2* __restrict__ T, double2* __restrict__ spec) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double2* buf = reinterpret_cast<double2*>(smem_raw);
+  const TwSmem tw = load_tw2(T, buf + fpad_size(H), 2 * H);
   const FftShape sh = make_shape(H);
   const int b = blockIdx.x;
   const double* f = series + (size_t)b * N;
@@ -28,11 +29,11 @@ __global__ void __launch_bounds__(kThreads) spectrum_kernel(const double* __rest
     buf[fpad(n)] = make_double2(a, c);
   }
   __syncthreads();
-  fft_forward(buf, sh, T, threadIdx.x, blockDim.x, CtaSync());
+  fft_forward(buf, sh, tw, threadIdx.x, blockDim.x, CtaSync());
   for (int p = threadIdx.x; p <= (H >> 1); p += blockDim.x) {
     double2 Xp, Xq;
     int pr, qr;
-    real_pair(buf, sh, T, p, Xp, Xq, pr, qr);
+    real_pair(buf, sh, tw, p, Xp, Xq, pr, qr);
     out[p] = Xp;
     out[H - p] = Xq;
   }
@@ -43,12 +44,13 @@ __global__ void __launch_bounds__(kThreads) matvec_kernel(const double2* __restr
                                                           double* __restrict__ y) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double2* buf = reinterpret_cast<double2*>(smem_raw);
+  const TwSmem tw = load_tw2(T, buf + fpad_size(H), 2 * H);  // visible after correlate's first barrier
   const FftShape sh = make_shape(H);
   const int b = blockIdx.x;
   const double* xb = x + (size_t)b * n_in;
   double* yb = y + (size_t)b * n_out;
   correlate_cta(
-      buf, sh, T, spec + (size_t)b * (H + 1), n_in, n_out, [&](int i) { return __ldg(xb + i); },
+      buf, sh, tw, spec + (size_t)b * (H + 1), n_in, n_out, [&](int i) { return __ldg(xb + i); },
       [&](int t, double v) { yb[t] = v; });
 }
 
@@ -66,6 +68,7 @@ __global__ void __launch_bounds__(kThreads) hankelize_kernel(const double* __res
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double2* bufB = reinterpret_cast<double2*>(smem_raw);
   double2* bufA = BIG ? nullptr : bufB + fpad_size(H);
+  const TwSmem tw = load_tw2(T, bufB + (BIG ? 1 : 2) * fpad_size(H), 2 * H);
   double2* Xu = BIG ? gscratch + (size_t)blockIdx.x * (H + 1) : nullptr;
   const FftShape sh = make_shape(H);
   const int mn = L < K ? L : K;
@@ -80,11 +83,11 @@ __global__ void __launch_bounds__(kThreads) hankelize_kernel(const double* __res
         bufB[fpad(n)] = make_double2(i0 < L ? __ldg(u + i0) : 0.0, i0 + 1 < L ? __ldg(u + i0 + 1) : 0.0);
       }
       __syncthreads();
-      fft_forward(bufB, sh, T, threadIdx.x, blockDim.x, CtaSync());
+      fft_forward(bufB, sh, tw, threadIdx.x, blockDim.x, CtaSync());
       for (int p = threadIdx.x; p <= (H >> 1); p += blockDim.x) {
         double2 Up, Uq;
         int pr, qr;
-        real_pair(bufB, sh, T, p, Up, Uq, pr, qr);
+        real_pair(bufB, sh, tw, p, Up, Uq, pr, qr);
         Xu[p] = Up;
         Xu[H - p] = Uq;
       }
@@ -94,12 +97,12 @@ __global__ void __launch_bounds__(kThreads) hankelize_kernel(const double* __res
         bufB[fpad(n)] = make_double2(i0 < K ? __ldg(v + i0) : 0.0, i0 + 1 < K ? __ldg(v + i0 + 1) : 0.0);
       }
       __syncthreads();
-      fft_forward(bufB, sh, T, threadIdx.x, blockDim.x, CtaSync());
+      fft_forward(bufB, sh, tw, threadIdx.x, blockDim.x, CtaSync());
       for (int p = threadIdx.x; p <= (H >> 1); p += blockDim.x) {
         double2 Vp, Vq;
         int pr, qr;
-        real_pair(bufB, sh, T, p, Vp, Vq, pr, qr);
-        inv_pair(bufB, T, H, p, pr, qr, cmul(Xu[p], Vp), cmul(Xu[H - p], Vq));
+        real_pair(bufB, sh, tw, p, Vp, Vq, pr, qr);
+        inv_pair(bufB, tw, p, pr, qr, cmul(Xu[p], Vp), cmul(Xu[H - p], Vq));
       }
     } else {
       __syncthreads();
@@ -109,18 +112,18 @@ __global__ void __launch_bounds__(kThreads) hankelize_kernel(const double* __res
         bufB[fpad(n)] = make_double2(i0 < K ? __ldg(v + i0) : 0.0, i0 + 1 < K ? __ldg(v + i0 + 1) : 0.0);
       }
       __syncthreads();
-      fft_forward(bufA, sh, T, threadIdx.x, blockDim.x, CtaSync());
-      fft_forward(bufB, sh, T, threadIdx.x, blockDim.x, CtaSync());
+      fft_forward(bufA, sh, tw, threadIdx.x, blockDim.x, CtaSync());
+      fft_forward(bufB, sh, tw, threadIdx.x, blockDim.x, CtaSync());
       for (int p = threadIdx.x; p <= (H >> 1); p += blockDim.x) {
         double2 Up, Uq, Vp, Vq;
         int pr, qr;
-        real_pair(bufA, sh, T, p, Up, Uq, pr, qr);
-        real_pair(bufB, sh, T, p, Vp, Vq, pr, qr);
-        inv_pair(bufB, T, H, p, pr, qr, cmul(Up, Vp), cmul(Uq, Vq));
+        real_pair(bufA, sh, tw, p, Up, Uq, pr, qr);
+        real_pair(bufB, sh, tw, p, Vp, Vq, pr, qr);
+        inv_pair(bufB, tw, p, pr, qr, cmul(Up, Vp), cmul(Uq, Vq));
       }
     }
     __syncthreads();
-    fft_inverse(bufB, sh, T, threadIdx.x, blockDim.x, CtaSync());
+    fft_inverse(bufB, sh, tw, threadIdx.x, blockDim.x, CtaSync());
     const double scale = sg / (double)H;
     double* g = out + term * N;
     for (int t = threadIdx.x; t < N; t += blockDim.x) {
@@ -134,11 +137,13 @@ __global__ void __launch_bounds__(kThreads) hankelize_kernel(const double* __res
   }
 }
 
-static size_t fft_smem(int H) { return (size_t)fpad_size(H) * 16; }
+static size_t tw_smem(int H) { return (size_t)tw2_entries(2 * H) * 16; }
+static size_t fft_smem(int H) { return (size_t)fpad_size(H) * 16 + tw_smem(H); }
+static size_t fft_smem2(int H) { return (size_t)2 * fpad_size(H) * 16 + tw_smem(H); }
 
 cudaError_t fft_set_attributes(int H, const char** which) {
   cudaError_t e;
-  size_t s1 = fft_smem(H), s2 = 2 * fft_smem(H);
+  size_t s1 = fft_smem(H), s2 = fft_smem2(H);
   *which = "spectrum_kernel";
   if ((e = cudaFuncSetAttribute(spectrum_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1))) return e;
   *which = "matvec_kernel";
@@ -153,7 +158,7 @@ cudaError_t fft_set_attributes(int H, const char** which) {
 }
 
 cudaError_t launch_spectrum(const Plan& p, const double* series, double2* spec, int nseries, cudaStream_t s) {
-  spectrum_kernel<<<(unsigned)nseries, kThreads, fft_smem((int)p.H), s>>>(series, (int)p.N, (int)p.H, p.d_tw, spec);
+  spectrum_kernel<<<(unsigned)nseries, kThreads, fft_smem((int)p.H), s>>>(series, (int)p.N, (int)p.H, p.d_twl, spec);
   return cudaGetLastError();
 }
 
@@ -161,7 +166,7 @@ cudaError_t launch_matvec(const Plan& p, const double2* spec, const double* x, d
                           cudaStream_t s) {
   int n_in = transpose ? (int)p.L : (int)p.K;
   int n_out = transpose ? (int)p.K : (int)p.L;
-  matvec_kernel<<<(unsigned)p.batch, kThreads, fft_smem((int)p.H), s>>>(spec, (int)p.H, n_in, n_out, p.d_tw, x, y);
+  matvec_kernel<<<(unsigned)p.batch, kThreads, fft_smem((int)p.H), s>>>(spec, (int)p.H, n_in, n_out, p.d_twl, x, y);
   return cudaGetLastError();
 }
 
@@ -169,12 +174,12 @@ cudaError_t launch_hankelize(const Plan& p, const double* sigma, const double* U
                              double* out, cudaStream_t s) {
   size_t total = (size_t)p.batch * nterms;
   if (p.H <= kMaxHankelSmemH) {
-    hankelize_kernel<false><<<(unsigned)total, kThreads, 2 * fft_smem((int)p.H), s>>>(
-        sigma, U, V, total, (int)p.N, (int)p.L, (int)p.K, (int)p.H, p.d_tw, out, nullptr);
+    hankelize_kernel<false><<<(unsigned)total, kThreads, fft_smem2((int)p.H), s>>>(
+        sigma, U, V, total, (int)p.N, (int)p.L, (int)p.K, (int)p.H, p.d_twl, out, nullptr);
   } else {
     size_t grid = total < (size_t)p.hank_slots ? total : (size_t)p.hank_slots;
     hankelize_kernel<true><<<(unsigned)grid, kThreads, fft_smem((int)p.H), s>>>(
-        sigma, U, V, total, (int)p.N, (int)p.L, (int)p.K, (int)p.H, p.d_tw, out, p.d_hscratch);
+        sigma, U, V, total, (int)p.N, (int)p.L, (int)p.K, (int)p.H, p.d_twl, out, p.d_hscratch);
   }
   return cudaGetLastError();
 }

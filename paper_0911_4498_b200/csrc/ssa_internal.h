@@ -27,7 +27,7 @@ struct DecomposeArgs {
   uint64_t seed;
   const double* series;  // caller [batch][N]
   const double2* spec;   // [nb][H+1]
-  const double2* tw;     // [H]
+  const double2* tw;     // two-level twiddle table for M
   double* U;             // [nb][m_max+1][ldL]  Krylov basis U_{m+1}
   double* V;             // [nb][m_max+1][ldK]  Krylov basis V_{m+1}
   double* ab;            // [nb][2][m_max+3]    alpha_j, beta_j (1-based)
@@ -67,8 +67,8 @@ struct Plan {
   double* d_tgkw = nullptr;
   // long-series (M > 2 kMaxSmemH) path: four-step FFT tables and buffers, Lanczos scratch
   bool large = false;
-  double2* d_tw1 = nullptr;      // exp(-2 pi i t / (2 N1)), t < N1
-  double2* d_tw2 = nullptr;      // exp(-2 pi i t / (2 N2)), t < N2
+  double2* d_tw1 = nullptr;      // two-level table for the N1-point sub-FFTs (M = 2 N1)
+  double2* d_tw2 = nullptr;      // two-level table for the N2-point sub-FFTs (M = 2 N2)
   double2* d_lbuf = nullptr;     // [lbuf_items][H] complex work buffers
   int lbuf_items = 0;
   double* d_lgsc = nullptr;      // device scalars (LgScalars)
@@ -77,7 +77,8 @@ struct Plan {
   double* d_lgr = nullptr;       // work vector
   int rot_cap = 0;
   size_t smem_lanczos = 0, smem_ritz = 0;
-  double2* d_tw = nullptr;     // twiddles exp(-2 pi i t / M), t < H
+  double2* d_tw = nullptr;     // twiddles exp(-2 pi i t / M), t < H (long-series path)
+  double2* d_twl = nullptr;    // two-level twiddle table for M (tw2_entries(M))
   double2* d_spec = nullptr;   // [chunk][H+1]
   double* d_U = nullptr;
   double* d_V = nullptr;

@@ -28,6 +28,7 @@ struct LSmem {
   double* red;             // 32
   int* redi;               // 8 ints
   double* chk;             // 4 * kMaxK: omega, res, lohi(2k)
+  double2* tw;             // two-level twiddle table for M (tw2_entries(M))
   uint64_t* bars;          // kWarps * kStages
 };
 
@@ -48,6 +49,7 @@ size_t lanczos_smem_bytes(int H, int ldL, int ldK, int m_max, int k) {
   s += align16((size_t)ldL * 8) + align16((size_t)ldK * 8);
   s += 3 * align16((size_t)(m_max + 3) * 8);
   s += 32 * 8 + 8 * 4 + 4 * kMaxK * 8;
+  s += (size_t)tw2_entries(2 * H) * 16;
   s += (size_t)kWarps * kStages * 8;
   return align16(s) + 16;
 }
@@ -65,6 +67,7 @@ __device__ inline LSmem carve(unsigned char* base, const DecomposeArgs& a) {
   s.red = reinterpret_cast<double*>(base + off); off += 32 * 8;
   s.redi = reinterpret_cast<int*>(base + off); off += 8 * 4;
   s.chk = reinterpret_cast<double*>(base + off); off += 4 * kMaxK * 8;
+  s.tw = reinterpret_cast<double2*>(base + off); off += (size_t)tw2_entries(2 * a.H) * 16;
   s.bars = reinterpret_cast<uint64_t*>(base + off);
   return s;
 }
@@ -208,6 +211,7 @@ __global__ void __launch_bounds__(kThreads, 2) lanczos_kernel(const DecomposeArg
   double* tc2 = tc + (2 * a.m_max + 2);
   double* tgk_scr = a.tgk + a.tgk_stride * blockIdx.x;
 
+  const TwSmem tw = load_tw2(a.tw, sm.tw, 2 * a.H);
   WarpRing rg;
   ring_init(rg, rings + (size_t)w * kStages * slab_max, sm.bars + w * kStages);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -270,7 +274,7 @@ __global__ void __launch_bounds__(kThreads, 2) lanczos_kernel(const DecomposeArg
       lap(7);
       const double bj = bcur;  // beta_j (register copy: sm.beta is written by thread 0 only)
       correlate_cta(
-          fbuf, sh, a.tw, spec, L, K, [&](int i) { return sm.bufU[i]; },
+          fbuf, sh, tw, spec, L, K, [&](int i) { return sm.bufU[i]; },
           [&](int t, double y) { sm.bufV[t] = y - bj * sm.bufV[t]; });
       __syncthreads();
       ss = 0.0;
@@ -345,7 +349,7 @@ __global__ void __launch_bounds__(kThreads, 2) lanczos_kernel(const DecomposeArg
       lap(7);
       const double aj = al;
       correlate_cta(
-          fbuf, sh, a.tw, spec, K, L, [&](int i) { return sm.bufV[i]; },
+          fbuf, sh, tw, spec, K, L, [&](int i) { return sm.bufV[i]; },
           [&](int t, double y) { sm.bufU[t] = y - aj * sm.bufU[t]; });
       __syncthreads();
       ss = 0.0;

@@ -45,6 +45,7 @@ __global__ void __launch_bounds__(kThreads) large_col_fwd(const double* __restri
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double2* buf = reinterpret_cast<double2*>(smem_raw);
   const int cs = fpad_size(N1);
+  const TwSmem tw1 = load_tw2(T1, buf + kColW * cs, 2 * N1);
   const FftShape s1 = make_shape(N1);
   const int n2_0 = blockIdx.x * kColW;
   const double* xi = x + (size_t)blockIdx.y * xs;
@@ -59,7 +60,7 @@ __global__ void __launch_bounds__(kThreads) large_col_fwd(const double* __restri
   }
   __syncthreads();
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  fft_forward(buf + w * cs, s1, T1, lane, 32, WarpSync());
+  fft_forward(buf + w * cs, s1, tw1, lane, 32, WarpSync());
   __syncthreads();
   for (int idx = threadIdx.x; idx < N1 * kColW; idx += blockDim.x) {
     const int c = idx & (kColW - 1), k1 = idx >> 3;
@@ -94,6 +95,7 @@ __global__ void __launch_bounds__(kThreads) large_col_inv(const double2* __restr
   __shared__ double red[kWarps];
   const int H = a.H, N1 = a.N1, N2 = a.N2;
   const int cs = fpad_size(N1);
+  const TwSmem tw1 = load_tw2(T1, buf + kColW * cs, 2 * N1);
   const FftShape s1 = make_shape(N1);
   const int n2_0 = blockIdx.x * kColW;
   const size_t item = blockIdx.y;
@@ -104,7 +106,7 @@ __global__ void __launch_bounds__(kThreads) large_col_inv(const double2* __restr
   }
   __syncthreads();
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  fft_inverse(buf + w * cs, s1, T1, lane, 32, WarpSync());
+  fft_inverse(buf + w * cs, s1, tw1, lane, 32, WarpSync());
   __syncthreads();
   const double invH = 1.0 / (double)H;
   double ss = 0.0;
@@ -177,6 +179,7 @@ __global__ void __launch_bounds__(kThreads) large_row_pair(const double2* __rest
   double2* bB = bA + rs;                                // row B of Ya
   double2* cA = bB + rs;                                // mode 2: row A of Yb
   double2* cB = cA + rs;                                // mode 2: row B of Yb
+  const TwSmem tw2 = load_tw2(T2, cB + rs, 2 * N2);
   const FftShape s2 = make_shape(N2);
   const int A = blockIdx.x, B = (N1 - A) & (N1 - 1);
   const bool two = (A != B);
@@ -192,11 +195,11 @@ __global__ void __launch_bounds__(kThreads) large_row_pair(const double2* __rest
     }
   }
   __syncthreads();
-  fft_forward(bA, s2, T2, threadIdx.x, blockDim.x, CtaSync());
-  if (two) fft_forward(bB, s2, T2, threadIdx.x, blockDim.x, CtaSync());
+  fft_forward(bA, s2, tw2, threadIdx.x, blockDim.x, CtaSync());
+  if (two) fft_forward(bB, s2, tw2, threadIdx.x, blockDim.x, CtaSync());
   if (a.mode == 2) {
-    fft_forward(cA, s2, T2, threadIdx.x, blockDim.x, CtaSync());
-    if (two) fft_forward(cB, s2, T2, threadIdx.x, blockDim.x, CtaSync());
+    fft_forward(cA, s2, tw2, threadIdx.x, blockDim.x, CtaSync());
+    if (two) fft_forward(cB, s2, tw2, threadIdx.x, blockDim.x, CtaSync());
   }
   // pairs (p, q = H - p): p = A + N1 k2 in row A, q in row B at partner_k2
   const int npairs = two ? N2 : ((A == 0) ? N2 / 2 + 1 : N2 / 2);
@@ -249,16 +252,19 @@ __global__ void __launch_bounds__(kThreads) large_row_pair(const double2* __rest
   double2* oA = (a.mode == 2) ? cA : bA;
   double2* oB = (a.mode == 2) ? cB : bB;
   double2* Yo = (a.mode == 2) ? Yb : Ya;
-  fft_inverse(oA, s2, T2, threadIdx.x, blockDim.x, CtaSync());
-  if (two) fft_inverse(oB, s2, T2, threadIdx.x, blockDim.x, CtaSync());
+  fft_inverse(oA, s2, tw2, threadIdx.x, blockDim.x, CtaSync());
+  if (two) fft_inverse(oB, s2, tw2, threadIdx.x, blockDim.x, CtaSync());
   for (int n2 = threadIdx.x; n2 < N2; n2 += blockDim.x) {
     Yo[(size_t)A * N2 + n2] = cmulc(oA[fpad(n2)], twH(T, (long long)n2 * A, H));
     if (two) Yo[(size_t)B * N2 + n2] = cmulc(oB[fpad(n2)], twH(T, (long long)n2 * B, H));
   }
 }
 
-size_t large_col_smem(int N1) { return (size_t)kColW * fpad_size(N1) * 16; }
-size_t large_row_smem(int N2, int mode) { return (size_t)(mode == 2 ? 4 : 2) * fpad_size(N2) * 16; }
+size_t large_col_smem(int N1) { return ((size_t)kColW * fpad_size(N1) + tw2_entries(2 * N1)) * 16; }
+size_t large_row_smem(int N2, int mode) {
+  (void)mode;  // the table sits after four rows in every mode
+  return ((size_t)4 * fpad_size(N2) + tw2_entries(2 * N2)) * 16;
+}
 
 cudaError_t large_set_attributes(int N1, int N2) {
   cudaError_t e;
