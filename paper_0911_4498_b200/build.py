@@ -30,15 +30,34 @@ def _stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
+    """nvcc each translation unit in parallel (-c, relocatable objects), then link the
+    shared library.  Flags: -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo."""
     if not force and not _stale():
         return LIB
+    from concurrent.futures import ThreadPoolExecutor
+    import tempfile
+    tmpdir = tempfile.mkdtemp(prefix="ssa_build_")
+    compile_flags = [f for f in NVCC_FLAGS if f != "-shared"]
+
+    def cc(src):
+        obj = os.path.join(tmpdir, os.path.basename(src) + ".o")
+        r = subprocess.run([_nvcc(), *compile_flags, "-c", "-o", obj, src], capture_output=True, text=True)
+        return src, obj, r
+
+    with ThreadPoolExecutor(len(SOURCES)) as ex:
+        results = list(ex.map(cc, SOURCES))
+    logs = []
+    for src, obj, r in results:
+        if r.returncode != 0:
+            raise RuntimeError(f"nvcc failed on {src}:\n" + r.stdout + r.stderr)
+        logs.append(r.stderr)
     tmp = LIB + f".tmp{os.getpid()}"
-    cmd = [_nvcc(), *NVCC_FLAGS, "-o", tmp, *SOURCES]
-    r = subprocess.run(cmd, capture_output=True, text=True)
+    r = subprocess.run([_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp,
+                        *[o for _, o, _ in results]], capture_output=True, text=True)
     if r.returncode != 0:
-        raise RuntimeError("nvcc failed:\n" + r.stdout + r.stderr)
+        raise RuntimeError("nvcc link failed:\n" + r.stdout + r.stderr)
     if verbose:
-        print(r.stderr)
+        print("\n".join(logs))
     os.replace(tmp, LIB)
     return LIB
 

@@ -149,7 +149,7 @@ static ssa_status create_decompose_workspace(Plan& p, const cudaDeviceProp& prop
   if ((st = alloc((void**)&p.d_ab, C * 2 * (p.m_max + 3) * 8, "bidiagonals")) != SSA_OK) return st;
   if ((st = alloc((void**)&p.d_state, C * 8 * sizeof(int), "series state")) != SSA_OK) return st;
   if ((st = alloc((void**)&p.d_coef, C * 2 * (p.m_max + 2) * k * 8, "Ritz coefficients")) != SSA_OK) return st;
-  if ((st = alloc((void**)&p.d_tgk, (size_t)p.lanczos_slots * k * (2 * p.m_max + 2) * 8, "TGK scratch")) != SSA_OK)
+  if ((st = alloc((void**)&p.d_tgk, (size_t)p.lanczos_slots * 2 * k * (2 * p.m_max + 2) * 8, "TGK scratch")) != SSA_OK)
     return st;
   if (p.opt.reserved & 2) {  // bidiagonal SVD by QR with rotation records
     if ((st = alloc((void**)&p.d_rot, (size_t)p.svd_slots * 6 * p.rot_cap * 8, "rotation records")) != SSA_OK)
@@ -186,7 +186,7 @@ static ssa_status create_large_workspace(Plan& p) {
   if ((st = alloc((void**)&p.d_ab, (size_t)2 * (p.m_max + 3) * 8, "bidiagonal")) != SSA_OK) return st;
   if ((st = alloc((void**)&p.d_state, 8 * sizeof(int), "series state")) != SSA_OK) return st;
   if ((st = alloc((void**)&p.d_coef, (size_t)2 * (p.m_max + 2) * k * 8, "Ritz coefficients")) != SSA_OK) return st;
-  if ((st = alloc((void**)&p.d_tgk, (size_t)k * (2 * p.m_max + 2) * 8, "TGK scratch")) != SSA_OK) return st;
+  if ((st = alloc((void**)&p.d_tgk, (size_t)2 * k * (2 * p.m_max + 2) * 8, "TGK scratch")) != SSA_OK) return st;
   if ((st = alloc((void**)&p.d_tgkw, tgkw_stride(p) * 8, "TGK vectors")) != SSA_OK) return st;
   if ((st = alloc((void**)&p.d_info, (size_t)p.batch * sizeof(ssa_series_info), "info")) != SSA_OK) return st;
   if ((st = alloc((void**)&p.d_counters, 16 * sizeof(int), "counters")) != SSA_OK) return st;
@@ -385,7 +385,7 @@ extern "C" ssa_status ssa_decompose(ssa_plan_t plan, const double* d_series, dou
   a.tol = p.opt.tol; a.seed = p.opt.seed;
   a.series = d_series; a.spec = p.d_spec; a.tw = p.d_twl;
   a.U = p.d_U; a.V = p.d_V; a.ab = p.d_ab; a.state = p.d_state;
-  a.tgk = p.d_tgk; a.tgk_stride = (size_t)p.k * (2 * p.m_max + 2);
+  a.tgk = p.d_tgk; a.tgk_stride = (size_t)2 * p.k * (2 * p.m_max + 2);
   a.rot = p.d_rot; a.rot_cap = p.rot_cap; a.svd_slots = p.svd_slots;
   a.svd_method = (p.opt.reserved & 2) ? 1 : 0; a.tgkw = p.d_tgkw; a.tgkw_stride = tgkw_stride(p); a.vecs = p.d_vecs; a.coef = p.d_coef;
   a.sigma = d_sigma; a.Uout = d_U; a.Vout = d_V;

@@ -154,6 +154,15 @@ cudaError_t fft_set_attributes(int H, const char** which) {
   if (H <= kMaxHankelSmemH)
     if ((e = cudaFuncSetAttribute(hankelize_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2)))
       return e;
+  // shared memory over L1: these kernels keep everything in shared memory, and e.g. three
+  // 75 KB matvec CTAs per SM only fit with the maximum carveout
+  *which = "carveout";
+  const int carve = cudaSharedmemCarveoutMaxShared;
+  if ((e = cudaFuncSetAttribute(spectrum_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, carve))) return e;
+  if ((e = cudaFuncSetAttribute(matvec_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, carve))) return e;
+  if ((e = cudaFuncSetAttribute(hankelize_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout, carve))) return e;
+  if ((e = cudaFuncSetAttribute(hankelize_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout, carve)))
+    return e;
   return cudaSuccess;
 }
 

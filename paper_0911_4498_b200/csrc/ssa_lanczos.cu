@@ -264,7 +264,7 @@ __global__ void __launch_bounds__(kThreads, 2) lanczos_kernel(const DecomposeArg
 
     double runmax = 0.0, bcur = beta1;
     int m = 0, converged = 0, breakdown = 0, extra = 0, restarts = 0, checks = 0;
-    int next_check = (2 * k < a.m_max) ? 2 * k : k;
+    int next_check = (2 * k + 8 < a.m_max) ? 2 * k + 8 : k;
     double prev_res = -1.0;
     int prev_m = 0;
     const int ce = a.check_every > 0 ? a.check_every : 4;
@@ -321,7 +321,7 @@ __global__ void __launch_bounds__(kThreads, 2) lanczos_kernel(const DecomposeArg
         double* lohi = res + kMaxK;
         // pivots of the twisted factorizations: shared memory when they fit in region A
         double* tc2n = tc2 + (2 * a.m_max + 2);
-        const size_t need = (size_t)(3 * (2 * a.m_max + 2) + k * n) * 8;
+        const size_t need = (size_t)(3 * (2 * a.m_max + 2) + 2 * k * n) * 8;
         double* dsc = (need <= lanczos_regionA_bytes(a.H, a.ldL, a.ldK, a.m_max)) ? tc2n + (2 * a.m_max + 2) : tgk_scr;
         tgk_check(tc, tc2, tc2n, m, k, al, om, res, lohi, dsc);
         double mr = 0.0;
@@ -395,7 +395,11 @@ __global__ void __launch_bounds__(kThreads, 2) lanczos_kernel(const DecomposeArg
 }
 
 cudaError_t lanczos_set_attributes(size_t smem) {
-  return cudaFuncSetAttribute(lanczos_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(lanczos_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(lanczos_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             cudaSharedmemCarveoutMaxShared);
+  return e;
 }
 
 cudaError_t launch_lanczos(const Plan& p, const DecomposeArgs& a, cudaStream_t s) {

@@ -110,8 +110,8 @@ __device__ inline void tgk_topk_values(const double* c2n, int n, int k, const Tg
   __syncthreads();
 }
 
-// Convergence test: omega[j], res[j] (SMEM) for j < k; scratch: >= k * n doubles (shared
-// memory when it fits, else global; layout [i][j]).
+// Convergence test: omega[j], res[j] (SMEM) for j < k; scratch: >= 2 k n doubles (shared
+// memory when it fits, else global; layout [i][j]).  Needs 2k <= blockDim.x.
 // alpha_next = alpha_{m+1}.  All threads call; ends with a barrier.
 // c2n: scratch of n-1 doubles (shared memory) for the normalized squares.
 __device__ inline void tgk_check(const double* c, const double* c2, double* c2n, int m, int k, double alpha_next,
@@ -126,52 +126,69 @@ __device__ inline void tgk_check(const double* c, const double* c2, double* c2n,
     __syncthreads();
   }
   tgk_topk_values(c2n, n, k, nrm, lohi, omega, 16);
-  // twisted factorization for lambda = omega_j, one thread per value: twist r at the
-  // smallest |gamma_r|, z_r = 1, z_i = -(c_i / D+_i) z_{i+1} above, -(c_{i-1} / D-_i) z_{i-1}
-  // below; last entry |z_n| / |z|
-  if (tid < k) {
-    const double lam = omega[tid];
-    double* D = scratch;  // D[i * k + tid]
-    double q = -lam;
-    D[tid] = q;
-    for (int i = 1; i < n; ++i) {
-      if (fabs(q) < pivmin) q = -pivmin;
-      q = -lam - c2[i - 1] / q;
-      D[(size_t)i * k + tid] = q;
+  // twisted factorization for lambda = omega_j, two lanes per value: the even lane runs
+  // the forward pivots D+ (and later the entries above the twist), the odd lane the
+  // backward pivots D- (and the entries below).  Twist r at the smallest
+  // |gamma_r| = |D+_r + D-_r + lambda|; z_r = 1, z_i = -(c_i / D+_i) z_{i+1} above,
+  // -(c_{i-1} / D-_i) z_{i-1} below; result |z_n| / |z|.  Pivots are divided through a
+  // correctly rounded reciprocal (one multiply more, no full division on the chain).
+  const unsigned pmask = __ballot_sync(0xffffffffu, tid < 2 * k);  // lanes taking part, per warp
+  if (tid < 2 * k) {
+    const int j = tid >> 1, role = tid & 1;
+    const double lam = omega[j];
+    double* Dp = scratch;                      // Dp[i * k + j]
+    double* Dm = scratch + (size_t)n * k;      // Dm[i * k + j]
+    if (role == 0) {
+      double q = -lam;
+      Dp[j] = q;
+      for (int i = 1; i < n; ++i) {
+        if (fabs(q) < pivmin) q = -pivmin;
+        q = fma(-c2[i - 1], __drcp_rn(q), -lam);
+        Dp[(size_t)i * k + j] = q;
+      }
+    } else {
+      double q = -lam;
+      Dm[(size_t)(n - 1) * k + j] = q;
+      for (int i = n - 2; i >= 0; --i) {
+        if (fabs(q) < pivmin) q = -pivmin;
+        q = fma(-c2[i], __drcp_rn(q), -lam);
+        Dm[(size_t)i * k + j] = q;
+      }
     }
-    double dm = -lam;
-    int r = n - 1;
-    double gbest = fabs(D[(size_t)(n - 1) * k + tid] + dm + lam);
-    for (int i = n - 2; i >= 0; --i) {
-      if (fabs(dm) < pivmin) dm = -pivmin;
-      dm = -lam - c2[i] / dm;
-      double g = fabs(D[(size_t)i * k + tid] + dm + lam);
+    __syncwarp(pmask);
+    // argmin |gamma| over the two halves, then combine (lowest index on ties)
+    const int h0 = role ? n / 2 : 0, h1 = role ? n : n / 2;
+    double gbest = 1e308;
+    int r = -1;
+    for (int i = h0; i < h1; ++i) {
+      const double g = fabs(Dp[(size_t)i * k + j] + Dm[(size_t)i * k + j] + lam);
       if (g < gbest) { gbest = g; r = i; }
     }
-    dm = -lam;
-    for (int i = n - 1; i > r; --i) {
-      if (i < n - 1) {
-        if (fabs(dm) < pivmin) dm = -pivmin;
-        dm = -lam - c2[i] / dm;
+    const double go = __shfl_xor_sync(pmask, gbest, 1);
+    const int ro = __shfl_xor_sync(pmask, r, 1);
+    if (go < gbest || (go == gbest && ro >= 0 && (r < 0 || ro < r))) { gbest = go; r = ro; }
+    double nrm2 = 0.0, zn = 0.0;
+    if (role == 0) {  // entries above the twist
+      double z = 1.0;
+      for (int i = r - 1; i >= 0; --i) {
+        double d = Dp[(size_t)i * k + j];
+        if (fabs(d) < pivmin) d = -pivmin;
+        z = -(c[i] * __drcp_rn(d)) * z;
+        nrm2 = fma(z, z, nrm2);
       }
-      D[(size_t)i * k + tid] = dm;
+    } else {  // entries below the twist (and the twist itself)
+      double z = 1.0;
+      nrm2 = 1.0;
+      for (int i = r + 1; i < n; ++i) {
+        double d = Dm[(size_t)i * k + j];
+        if (fabs(d) < pivmin) d = -pivmin;
+        z = -(c[i - 1] * __drcp_rn(d)) * z;
+        nrm2 = fma(z, z, nrm2);
+      }
+      zn = z;  // z_n (1 when r = n - 1)
     }
-    double nrm2 = 1.0, z = 1.0;
-    for (int i = r - 1; i >= 0; --i) {
-      double d = D[(size_t)i * k + tid];
-      if (fabs(d) < pivmin) d = -pivmin;
-      z = -(c[i] / d) * z;
-      nrm2 = fma(z, z, nrm2);
-    }
-    z = 1.0;
-    for (int i = r + 1; i < n; ++i) {
-      double d = D[(size_t)i * k + tid];
-      if (fabs(d) < pivmin) d = -pivmin;
-      z = -(c[i - 1] / d) * z;
-      nrm2 = fma(z, z, nrm2);
-    }
-    const double zn = (r == n - 1) ? 1.0 : z;
-    res[tid] = alpha_next * 1.4142135623730951 * fabs(zn) / sqrt(nrm2);
+    const double tot = nrm2 + __shfl_xor_sync(pmask, nrm2, 1);
+    if (role == 1) res[j] = alpha_next * 1.4142135623730951 * fabs(zn) / sqrt(tot);
   }
   __syncthreads();
 }
