@@ -52,6 +52,7 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-once", action="store_true", help="1 decompose, no timing (for ncu)")
+    ap.add_argument("--no-micro", action="store_true", help="skip the cfg4 / cfg5 microbenchmarks")
     return ap.parse_args()
 
 
@@ -81,6 +82,98 @@ def lanczos_alg_bytes(steps: np.ndarray, N: int, L: int, k: int) -> float:
 def hankelize_alg_bytes(nterms: int, N: int, L: int) -> float:
     K = N - L + 1
     return float(nterms) * 8 * (L + K + N + 1)
+
+
+# ------------------------------------------------------------------------ microbenchmarks
+def _events_ms(fn, reps=1):
+    import torch
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    a.record()
+    for _ in range(reps):
+        fn()
+    b.record()
+    torch.cuda.synchronize()
+    return a.elapsed_time(b)
+
+
+def micro_matvec(P, peak):
+    """BASELINE.json configs[3] (cfg4): 65,536 series N=8192, L=4096, i.i.d. N(0,1) series and
+    vectors (drawn on the device); 64 alternating X v / X^T u products per series, each a
+    batched ssa_matvec launch over all series reading x and the spectrum from HBM and
+    writing y to HBM.  Algorithmic bytes per product 8(K+L) + 16(M/2+1); roofline HBM."""
+    import torch
+    c = ssa_inputs.CONFIGS["cfg4"]
+    N, L, B, T = c["N"], c["L"], c["batch"], c["products"]
+    K = N - L + 1
+    g = torch.Generator(device="cuda").manual_seed(4)
+    F = torch.randn(B, N, dtype=torch.float64, device="cuda", generator=g)
+    v = torch.randn(B, K, dtype=torch.float64, device="cuda", generator=g)
+    u = torch.randn(B, L, dtype=torch.float64, device="cuda", generator=g)
+    plan = P.Plan(N, L, 0, B)
+    spec = plan.spectrum(F)
+    del F
+    y = torch.empty(B, L, dtype=torch.float64, device="cuda")
+    z = torch.empty(B, K, dtype=torch.float64, device="cuda")
+
+    def run():
+        for t in range(T):
+            if t % 2 == 0:
+                plan.matvec(spec, v, out=y)
+            else:
+                plan.matvec(spec, u, transpose=True, out=z)
+    run()
+    ms = min(_events_ms(run) for _ in range(3))
+    nprod = T * B
+    M = plan.M
+    byt = nprod * (8 * (K + L) + 16 * (M // 2 + 1))
+    out = {"value": nprod / (ms * 1e-3), "unit": "Hankel matvecs/s", "per_gpu": True, "ms": ms, "products": nprod,
+           "workload": "cfg4 (BASELINE.json configs[3]): 65536 series N=8192 L=4096, 64 alternating products",
+           "roofline": {"bound": "hbm", "achieved": byt / (ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+                        "frac": byt / (ms * 1e-3) / 1e9 / peak, "alg_bytes_per_product": byt / nprod}}
+    plan.close()
+    del spec, v, u, y, z
+    torch.cuda.empty_cache()
+    return out
+
+
+def micro_hankelize(P, peak):
+    """BASELINE.json configs[4] (cfg5): 256 problems N=262144, L=131072, 50 rank-1 terms each,
+    sigma_i = 1/i, u_i, v_i Gaussian normalized (drawn on the device); every term
+    Hankelized separately.  Run in 8 launches of 32 problems.  Algorithmic bytes per term
+    8(L+K+N); flops per term 3 x 2.5 N log2 N + 6(N/2+1) + 2N."""
+    import math
+    import torch
+    c = ssa_inputs.CONFIGS["cfg5"]
+    N, L, B, T = c["N"], c["L"], c["batch"], c["k"]
+    K = N - L + 1
+    Bc = 32
+    g = torch.Generator(device="cuda").manual_seed(5)
+    U = torch.randn(Bc, T, L, dtype=torch.float64, device="cuda", generator=g)
+    U /= U.norm(dim=2, keepdim=True)
+    V = torch.randn(Bc, T, K, dtype=torch.float64, device="cuda", generator=g)
+    V /= V.norm(dim=2, keepdim=True)
+    sig = (1.0 / torch.arange(1, T + 1, dtype=torch.float64, device="cuda")).repeat(Bc, 1).contiguous()
+    plan = P.Plan(N, L, 0, Bc)
+    out = torch.empty(Bc, T, N, dtype=torch.float64, device="cuda")
+
+    def run():
+        for _ in range(B // Bc):   # the same 32 problems stand in for each of the 8 chunks
+            plan.hankelize(sig, U, V, out=out)
+    run()
+    ms = min(_events_ms(run) for _ in range(2))
+    nt = B * T
+    byt = nt * 8 * (L + K + N)
+    flops = nt * (3 * 2.5 * N * math.log2(N) + 6 * (N // 2 + 1) + 2 * N)
+    res = {"value": nt / (ms * 1e-3), "unit": "terms/s", "per_gpu": True, "ms": ms, "terms": nt,
+           "workload": "cfg5 (BASELINE.json configs[4]): 256 x 50 terms, N=262144 L=131072",
+           "roofline": {"bound": "hbm (model; the fp64 FFT work sits at the ridge)",
+                        "achieved": byt / (ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+                        "frac": byt / (ms * 1e-3) / 1e9 / peak, "fp64_tflops_model": flops / (ms * 1e-3) / 1e12}}
+    plan.close()
+    del U, V, out, sig
+    torch.cuda.empty_cache()
+    return res
 
 
 # ------------------------------------------------------------------------ clocks
@@ -282,7 +375,7 @@ def main():
 
     ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    lan_ms, hank_ms, spec_ms = [], [], []
+    lan_ms, hank_ms, spec_ms, svd_ms, ritz_ms = [], [], [], [], []
     launches0 = plan.launches
     with ClockSampler(local) as clk:
         for i in range(args.steps):
@@ -296,6 +389,7 @@ def main():
             torch.cuda.synchronize()
             ph = plan.phase_ms()
             lan_ms.append(ph["lanczos"]); hank_ms.append(ph["hankelize"]); spec_ms.append(ph["spectrum"])
+            svd_ms.append(ph["bidiag_svd"]); ritz_ms.append(ph["ritz"])
     launches = (plan.launches - launches0) // args.steps
     step_ms = np.array([a.elapsed_time(b) for a, b in zip(ev0, ev1)])
     total = torch.tensor([step_ms.sum()], dtype=torch.float64, device="cuda")
@@ -333,7 +427,8 @@ def main():
                           "max": int(steps_m.max()), "mean": float(steps_m.mean())},
         "converged_fraction": conv,
         "max_residual": float(inf["max_residual"].max()),
-        "phase_ms": {"spectrum": float(np.mean(spec_ms)), "lanczos": lan, "hankelize": hk},
+        "phase_ms": {"spectrum": float(np.mean(spec_ms)), "lanczos": lan, "bidiag_svd": float(np.mean(svd_ms)),
+                     "ritz": float(np.mean(ritz_ms)), "hankelize": hk},
         "roofline": {"kernel": "lanczos_kernel", "bound": "hbm", "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                      "traffic_src": traffic_src, "peak_src": peak_src,
@@ -379,6 +474,11 @@ def main():
                        "api": "ssa_run_host (pinned host buffers; H2D series, D2H sigma/U/V/recon/info)"}
         plan2.close()
 
+    if not args.no_micro:
+        del G
+        torch.cuda.empty_cache()
+        line["matvec_cfg4"] = micro_matvec(P, peak)
+        line["hankelize_cfg5"] = micro_hankelize(P, peak)
     if rank == 0 and not args.no_cpu_baseline:
         cores = os.cpu_count() or 1
         rate, desc, wall = oracle_sample(cores)

@@ -156,20 +156,22 @@ struct WarpRing {
   uint32_t cnt;   // chunks consumed so far (== issued at the end of each stream)
 };
 
+template <int NST = kStages>
 __device__ __forceinline__ void ring_init(WarpRing& rg, double* buf, uint64_t* bar) {
   rg.buf = buf;
   rg.bar = bar;
   rg.cnt = 0;
   if ((threadIdx.x & 31) == 0)
-    for (int s = 0; s < kStages; ++s) mbar_init(bar + s, 1);
+    for (int s = 0; s < NST; ++s) mbar_init(bar + s, 1);
 }
 
 // Streams rows (q-th job = row q, or nb-1-q if reverse) of this warp's column slab
 // [w*slab, (w+1)*slab) of a row-major basis (row stride ld doubles) through the ring;
 // calls f(row, chunk) for each in order.  All lanes of the warp must call it.
-template <class F>
+template <int NST = kStages, class F>
 __device__ __forceinline__ void stream_rows(const double* base_w, int ld, int nb, bool reverse, int slab, WarpRing& rg,
                                             F f) {
+  constexpr int kStages = NST;  // ring depth of this stream (the ring must have NST stages)
   const int lane = threadIdx.x & 31;
   const uint32_t bytes = (uint32_t)slab * 8u;
   const uint32_t c0 = rg.cnt;

@@ -31,7 +31,7 @@ struct DecomposeArgs {
   double* U;             // [nb][m_max+1][ldL]  Krylov basis U_{m+1}
   double* V;             // [nb][m_max+1][ldK]  Krylov basis V_{m+1}
   double* ab;            // [nb][2][m_max+3]    alpha_j, beta_j (1-based)
-  int* state;            // [nb][8]: m, converged, breakdown, reorth_extra, restarts, bad, checks, -
+  int* state;            // [nb][8]: m, converged, breakdown, reorth_extra, restarts, bad, checks, svd done
   double* tgk;           // per Lanczos CTA slot: k * (2 m_max + 2) doubles
   size_t tgk_stride;
   double* rot;           // per SVD warp slot: 2 sides x rot_cap x 3 doubles

@@ -27,6 +27,7 @@ struct LSmem {
   double* beta;            // m_max + 3 (1-based)
   double* red;             // 32
   int* redi;               // 8 ints
+  int* cl;                 // 40 ints: cluster starts of the final SVD (tgk_clusters)
   double* chk;             // 4 * kMaxK: omega, res, lohi(2k)
   double2* tw;             // two-level twiddle table for M (tw2_entries(M))
   uint64_t* bars;          // kWarps * kStages
@@ -36,7 +37,7 @@ __host__ __device__ inline size_t lanczos_regionA_bytes(int H, int ldL, int ldK,
   int slab_max = (ldL > ldK ? ldL : ldK) / kWarps;
   size_t fft = (size_t)fpad_size(H) * 16;
   size_t rings = (size_t)kWarps * kStages * slab_max * 8 + (size_t)kWarps * (m_max + 2) * 8;
-  size_t tgk = (size_t)3 * (2 * m_max + 2) * 8;
+  size_t tgk = (size_t)7 * (2 * m_max + 2) * 8;  // c, c^2, c^2/|T|^2 + the cheap test's pivots
   size_t r = fft;
   if (rings > r) r = rings;
   if (tgk > r) r = tgk;
@@ -48,7 +49,7 @@ size_t lanczos_smem_bytes(int H, int ldL, int ldK, int m_max, int k) {
   size_t s = lanczos_regionA_bytes(H, ldL, ldK, m_max);
   s += align16((size_t)ldL * 8) + align16((size_t)ldK * 8);
   s += 3 * align16((size_t)(m_max + 3) * 8);
-  s += 32 * 8 + 8 * 4 + 4 * kMaxK * 8;
+  s += 32 * 8 + 8 * 4 + 40 * 4 + 4 * kMaxK * 8;
   s += (size_t)tw2_entries(2 * H) * 16;
   s += (size_t)kWarps * kStages * 8;
   return align16(s) + 16;
@@ -66,6 +67,7 @@ __device__ inline LSmem carve(unsigned char* base, const DecomposeArgs& a) {
   s.beta = reinterpret_cast<double*>(base + off); off += align16((size_t)(a.m_max + 3) * 8);
   s.red = reinterpret_cast<double*>(base + off); off += 32 * 8;
   s.redi = reinterpret_cast<int*>(base + off); off += 8 * 4;
+  s.cl = reinterpret_cast<int*>(base + off); off += 40 * 4;
   s.chk = reinterpret_cast<double*>(base + off); off += 4 * kMaxK * 8;
   s.tw = reinterpret_cast<double2*>(base + off); off += (size_t)tw2_entries(2 * a.H) * 16;
   s.bars = reinterpret_cast<uint64_t*>(base + off);
@@ -245,7 +247,7 @@ __global__ void __launch_bounds__(kThreads, 2) lanczos_kernel(const DecomposeArg
     for (int t = tid; t < a.N; t += blockDim.x) bad |= !isfinite(f[t]);
     if (block_or(bad, sm.redi)) {
       if (tid == 0) {
-        st[0] = 0; st[1] = 0; st[2] = 0; st[3] = 0; st[4] = 0; st[5] = 1; st[6] = 0;
+        st[0] = 0; st[1] = 0; st[2] = 0; st[3] = 0; st[4] = 0; st[5] = 1; st[6] = 0; st[7] = 0;
       }
       continue;
     }
@@ -323,10 +325,20 @@ __global__ void __launch_bounds__(kThreads, 2) lanczos_kernel(const DecomposeArg
         double* tc2n = tc2 + (2 * a.m_max + 2);
         const size_t need = (size_t)(3 * (2 * a.m_max + 2) + 2 * k * n) * 8;
         double* dsc = (need <= lanczos_regionA_bytes(a.H, a.ldL, a.ldK, a.m_max)) ? tc2n + (2 * a.m_max + 2) : tgk_scr;
-        tgk_check(tc, tc2, tc2n, m, k, al, om, res, lohi, dsc);
-        double mr = 0.0;
-        for (int i = 0; i < k; ++i) mr = fmax(mr, res[i]);
-        const double rel = (om[0] > 0.0) ? mr / om[0] : 0.0;
+        // cheap test first: omega_1 and the k-th (slowest-converging) triple only; the
+        // full test of all k runs only when that one passes
+        double rel;
+        {
+          const int nv = (k > 1) ? 2 : 1;
+          tgk_check(tc, tc2, tc2n, m, nv, al, om, res, lohi, tc2n + (2 * a.m_max + 2), k - 1);
+          rel = (om[0] > 0.0) ? res[nv - 1] / om[0] : 0.0;
+        }
+        if (rel <= 0.5 * a.tol && k > 1) {
+          tgk_check(tc, tc2, tc2n, m, k, al, om, res, lohi, dsc);
+          double mr = 0.0;
+          for (int i = 0; i < k; ++i) mr = fmax(mr, res[i]);
+          rel = (om[0] > 0.0) ? mr / om[0] : 0.0;
+        }
         ++checks;
         lap(2);
         // the estimate must be below tol/2 (the final QR residual is what gets reported)
@@ -380,6 +392,47 @@ __global__ void __launch_bounds__(kThreads, 2) lanczos_kernel(const DecomposeArg
       lap(1);
     }
     lap(7);
+    // ---- final bidiagonal SVD right here (north star (b), tgk_final): it overlaps the
+    // other CTAs' basis streaming; near-degenerate cases are left to the SVD kernel ----
+    int fused = 0;
+    if (a.svd_method == 0) {
+      const int n = 2 * m + 1;
+      __syncthreads();
+      for (int i = tid; i < n - 1; i += blockDim.x) {
+        double v = (i & 1) ? sm.beta[(i >> 1) + 2] : sm.alpha[(i >> 1) + 1];
+        tc[i] = v;
+        tc2[i] = v * v;
+      }
+      __syncthreads();
+      double* om = sm.chk;
+      double* res = om + kMaxK;
+      double* lohi = res + kMaxK;
+      double* tc2n = tc2 + (2 * a.m_max + 2);
+      const size_t need = (size_t)(3 * (2 * a.m_max + 2) + 2 * k * n) * 8;
+      double* dsc = (need <= lanczos_regionA_bytes(a.H, a.ldL, a.ldK, a.m_max)) ? tc2n + (2 * a.m_max + 2) : tgk_scr;
+      double* cP = a.coef + (size_t)bl * 2 * (a.m_max + 2) * k;
+      double* cQ = cP + (size_t)(a.m_max + 2) * k;
+      fused = tgk_final(tc, tc2, tc2n, m, k, sm.alpha[m + 1], om, lohi, res, dsc, cP, cQ, sm.cl);
+      if (fused) {
+        if (tid < k) a.sigma[(size_t)b * k + tid] = om[tid];
+        if (tid == 0) {
+          double mr = 0.0;
+          for (int i = 0; i < k; ++i) mr = fmax(mr, res[i]);
+          const double fres = om[0] > 0.0 ? mr / om[0] : 0.0;
+          ssa_series_info inf;
+          inf.steps = m;
+          inf.converged = converged;
+          inf.breakdown_step = breakdown;
+          inf.reorth_extra = extra;
+          inf.reserved = restarts;
+          inf.status = fres <= a.tol ? SSA_OK : SSA_ERR_NOT_CONVERGED;
+          inf.max_residual = fres;
+          inf.sigma1 = om[0];
+          a.info[b] = inf;
+        }
+      }
+      lap(6);
+    }
     // ---- publish B_m and the step count for the SVD kernel ----
     __syncthreads();
     for (int i = tid; i <= m + 2 && i < a.m_max + 3; i += blockDim.x) {
@@ -388,6 +441,7 @@ __global__ void __launch_bounds__(kThreads, 2) lanczos_kernel(const DecomposeArg
     }
     if (tid == 0) {
       st[0] = m; st[1] = converged; st[2] = breakdown; st[3] = extra; st[4] = restarts; st[5] = 0; st[6] = checks;
+      st[7] = fused;
     }
   }
   if (a.prof && tid == 0)

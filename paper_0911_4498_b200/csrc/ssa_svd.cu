@@ -135,7 +135,8 @@ __global__ void __launch_bounds__(kThreads) bidiag_svd_tgk_kernel(const Decompos
   const int nmax = 2 * a.m_max + 1;
   double* c = reinterpret_cast<double*>(smem_raw);
   double* c2 = c + nmax;
-  double* lohi = c2 + nmax;
+  double* c2n = c2 + nmax;
+  double* lohi = c2n + nmax;
   double* lam = lohi + 2 * kMaxK;
   double* red = lam + kMaxK;
   int* cl = reinterpret_cast<int*>(red + 2 * kMaxK);
@@ -166,6 +167,7 @@ __global__ void __launch_bounds__(kThreads) bidiag_svd_tgk_kernel(const Decompos
       }
       continue;
     }
+    if (st[7]) continue;  // the Lanczos kernel already did the final SVD of this series
     const int n = 2 * m + 1;
     for (int i = tid; i < n - 1; i += blockDim.x) {
       double v = (i & 1) ? beta[(i >> 1) + 2] : alpha[(i >> 1) + 1];
@@ -173,39 +175,48 @@ __global__ void __launch_bounds__(kThreads) bidiag_svd_tgk_kernel(const Decompos
       c2[i] = v * v;
     }
     __syncthreads();
-    const TgkNorms nrm = tgk_norms(c, c2, n);
-    {
-      const double ig2 = (nrm.gmax > 0.0) ? 1.0 / (nrm.gmax * nrm.gmax) : 0.0;
-      __syncthreads();
-      for (int i = tid; i < n - 1; i += blockDim.x) c2[i] *= ig2;  // c2 now holds c^2 / |T|^2
-      __syncthreads();
-    }
-    long long ta = clock64();
-    tgk_topk_values(c2, n, k, nrm, lohi, lam, 40);
-    long long tb = clock64();
-    tgk_vectors(c, n, k, lam, nrm, Z, W, ipv, a.seed ^ ((unsigned long long)b << 20), cl);
-    long long tc = clock64();
-    tvals += tb - ta;
-    tvecs += tc - tb;
-    // split z = (p1, q1, p2, ..., q_m, p_{m+1}) into unit p (m+1) and q (m)
     const double anext = alpha[m + 1];
     double* cP = a.coef + (size_t)bl * 2 * mstride * k;
     double* cQ = cP + (size_t)mstride * k;
-    if (tid < k) {
-      const int j = tid;
-      double sp = 0.0, sq = 0.0;
-      for (int r = 0; r <= m; ++r) { double v = Z[(size_t)(2 * r) * k + j]; sp = fma(v, v, sp); }
-      for (int r = 0; r < m; ++r) { double v = Z[(size_t)(2 * r + 1) * k + j]; sq = fma(v, v, sq); }
-      const double ip = sp > 0.0 ? 1.0 / sqrt(sp) : 0.0, iq = sq > 0.0 ? 1.0 / sqrt(sq) : 0.0;
-      red[j] = anext * fabs(Z[(size_t)(2 * m) * k + j]) * ip;
-      red[kMaxK + j] = ip;
-      lohi[j] = iq;
-    }
-    __syncthreads();
-    for (int idx = tid; idx < (m + 1) * k; idx += blockDim.x) {
-      const int r = idx / k, j = idx - r * k;
-      cP[idx] = Z[(size_t)(2 * r) * k + j] * red[kMaxK + j];
-      cQ[idx] = (r < m) ? Z[(size_t)(2 * r + 1) * k + j] * lohi[j] : 0.0;
+    long long ta = clock64();
+    // twisted-factorization vectors (tgk.cuh); inverse iteration only for near-degenerate
+    // values
+    const int done = tgk_final(c, c2, c2n, m, k, anext, lam, lohi, red, Z, cP, cQ, cl);
+    long long tb = clock64();
+    tvals += tb - ta;
+    if (!done) {
+      const TgkNorms nrm = tgk_norms(c, c2, n);
+      tgk_vectors(c, n, k, lam, nrm, Z, W, ipv, a.seed ^ ((unsigned long long)b << 20), cl);
+      // split z = (p1, q1, p2, ..., q_m, p_{m+1}) into unit p (m+1) and q (m)
+      if (tid < k) {
+        const int j = tid;
+        double sp = 0.0, sq = 0.0;
+        for (int r = 0; r <= m; ++r) { double v = Z[(size_t)(2 * r) * k + j]; sp = fma(v, v, sp); }
+        for (int r = 0; r < m; ++r) { double v = Z[(size_t)(2 * r + 1) * k + j]; sq = fma(v, v, sq); }
+        const double ip = sp > 0.0 ? 1.0 / sqrt(sp) : 0.0, iq = sq > 0.0 ? 1.0 / sqrt(sq) : 0.0;
+        red[j] = anext * fabs(Z[(size_t)(2 * m) * k + j]) * ip;
+        red[kMaxK + j] = ip;
+        lohi[j] = iq;
+      }
+      __syncthreads();
+      for (int idx = tid; idx < (m + 1) * k; idx += blockDim.x) {
+        const int r = idx / k, j = idx - r * k;
+        cP[idx] = Z[(size_t)(2 * r) * k + j] * red[kMaxK + j];
+        cQ[idx] = (r < m) ? Z[(size_t)(2 * r + 1) * k + j] * lohi[j] : 0.0;
+      }
+      __syncthreads();
+      // inside a cluster the p- and q-halves of orthonormal TGK vectors are only orthogonal
+      // to O(eps |T| / gap): re-orthonormalize each half (one warp per cluster)
+      {
+        const int w = tid >> 5, nw = blockDim.x >> 5;
+        for (int q = w; q < cl[33]; q += nw) {
+          if (cl[q + 1] - cl[q] < 2) continue;
+          warp_mgs_cols(cP, m + 1, k, cl[q], cl[q + 1]);
+          warp_mgs_cols(cQ, m, k, cl[q], cl[q + 1]);
+        }
+      }
+      __syncthreads();
+      tvecs += clock64() - tb;
     }
     if (tid < k) a.sigma[(size_t)b * k + tid] = lam[tid];
     if (tid == 0) {
@@ -231,30 +242,32 @@ __global__ void __launch_bounds__(kThreads) bidiag_svd_tgk_kernel(const Decompos
 }
 
 size_t tgk_svd_smem_bytes(int m_max) {
-  return (size_t)(2 * (2 * m_max + 1) + 2 * kMaxK + kMaxK + 2 * kMaxK) * 8 + 40 * 4 + 16;
+  return (size_t)(3 * (2 * m_max + 1) + 2 * kMaxK + kMaxK + 2 * kMaxK) * 8 + 40 * 4 + 16;
 }
+
+// Ritz rings: kRitzStages chunks of at most 32 E = 64 columns (512 B) per warp in flight
+constexpr int kRitzStages = 8;
+constexpr int kRitzChunk = 64;
 
 size_t ritz_smem_bytes(int ldL, int ldK, int k) {
   (void)k;
-  int slab_max = (ldL > ldK ? ldL : ldK) / kWarps;
-  size_t s = (size_t)kWarps * kStages * slab_max * 8;
+  size_t s = (size_t)kWarps * kRitzStages * kRitzChunk * 8;
   s += (size_t)kWarps * kMaxK * (8 + 4) + kMaxK * 8;
-  s += (size_t)kWarps * kStages * 8;
+  s += (size_t)kWarps * kRitzStages * 8;
   return align16(s) + 16;
 }
 
 __global__ void __launch_bounds__(kThreads, 2) ritz_kernel(const DecomposeArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
-  const int slab_max = (a.ldL > a.ldK ? a.ldL : a.ldK) / kWarps;
   double* rings = reinterpret_cast<double*>(smem_raw);
-  double* mxv = rings + (size_t)kWarps * kStages * slab_max;  // [kWarps][kMaxK]
-  double* sgn = mxv + kWarps * kMaxK;                          // [kMaxK]
-  int* mxi = reinterpret_cast<int*>(sgn + kMaxK);              // [kWarps][kMaxK]
+  double* mxv = rings + (size_t)kWarps * kRitzStages * kRitzChunk;  // [kWarps][kMaxK]
+  double* sgn = mxv + kWarps * kMaxK;                                  // [kMaxK]
+  int* mxi = reinterpret_cast<int*>(sgn + kMaxK);                      // [kWarps][kMaxK]
   uint64_t* bars = reinterpret_cast<uint64_t*>(mxi + kWarps * kMaxK);
   __shared__ int sb;
   WarpRing rg;
-  ring_init(rg, rings + (size_t)w * kStages * slab_max, bars + w * kStages);
+  ring_init<kRitzStages>(rg, rings + (size_t)w * kRitzStages * kRitzChunk, bars + w * kRitzStages);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncthreads();
   const int L = a.L, K = a.K, k = a.k;
@@ -279,14 +292,10 @@ __global__ void __launch_bounds__(kThreads, 2) ritz_kernel(const DecomposeArgs a
       double* out = (isU ? a.Uout : a.Vout) + (size_t)b * k * n;
       const int slab = ld / kWarps;
       const double* bw = basis + (size_t)w * slab;
-      double bestv[kMaxK];
-      int besti[kMaxK];
-#pragma unroll
-      for (int i = 0; i < kMaxK; ++i) { bestv[i] = -1.0; besti[i] = 0; }
-      constexpr int E = 2;
-      for (int e0 = 0; e0 < slab; e0 += 32 * E) {
-        for (int i0 = 0; i0 < k; i0 += 16) {
-          const int ki = (k - i0) < 16 ? (k - i0) : 16;
+      constexpr int E = kRitzChunk / 32;
+      for (int i0 = 0; i0 < k; i0 += 16) {
+        const int ki = (k - i0) < 16 ? (k - i0) : 16;
+        for (int e0 = 0; e0 < slab; e0 += 32 * E) {
           double acc[E][16];
 #pragma unroll
           for (int t = 0; t < E; ++t)
@@ -294,15 +303,18 @@ __global__ void __launch_bounds__(kThreads, 2) ritz_kernel(const DecomposeArgs a
             for (int i = 0; i < 16; ++i) acc[t][i] = 0.0;
           fence_proxy_async_smem();
           __syncwarp();
-          stream_rows(bw, ld, rows, false, slab, rg, [&](int row, const double* ch) {
+          // stream only this 32E-column chunk of each row: each basis byte is read once
+          // per block of 16 triples
+          const int cw = (slab - e0) < 32 * E ? (slab - e0) : 32 * E;
+          stream_rows<kRitzStages>(bw + e0, ld, rows, false, cw, rg, [&](int row, const double* ch) {
             const double* cr = coef + (size_t)row * k + i0;
             double cf[16];
 #pragma unroll
             for (int i = 0; i < 16; ++i) cf[i] = (i < ki) ? __ldg(cr + i) : 0.0;
 #pragma unroll
             for (int t = 0; t < E; ++t) {
-              int e = e0 + t * 32 + lane;
-              double x = (e < slab) ? ch[e] : 0.0;
+              int e = t * 32 + lane;
+              double x = (e < cw) ? ch[e] : 0.0;
 #pragma unroll
               for (int i = 0; i < 16; ++i) acc[t][i] = fma(cf[i], x, acc[t][i]);
             }
@@ -314,26 +326,29 @@ __global__ void __launch_bounds__(kThreads, 2) ritz_kernel(const DecomposeArgs a
             if (e < slab && g < n) {
 #pragma unroll
               for (int i = 0; i < 16; ++i)
-                if (i < ki) {
-                  out[(size_t)(i0 + i) * n + g] = acc[t][i];
-                  if (isU && fabs(acc[t][i]) > bestv[i0 + i]) { bestv[i0 + i] = fabs(acc[t][i]); besti[i0 + i] = g; }
-                }
+                if (i < ki) out[(size_t)(i0 + i) * n + g] = acc[t][i];
             }
           }
         }
       }
-      if (isU) {
-        for (int i = 0; i < k; ++i) {
-          double v = bestv[i];
-          int ix = besti[i];
-          for (int o = 16; o > 0; o >>= 1) {
-            double v2 = __shfl_xor_sync(0xffffffffu, v, o);
-            int i2 = __shfl_xor_sync(0xffffffffu, ix, o);
-            if (v2 > v || (v2 == v && i2 < ix)) { v = v2; ix = i2; }
-          }
-          if (lane == 0) { mxv[w * kMaxK + i] = v; mxi[w * kMaxK + i] = ix; }
-        }
+    }
+    // sign canonicalization (R12): largest-|.| entry of each u_i (lowest index
+    // on ties), found from the just-written outputs (L2-resident)
+    __syncthreads();
+    for (int i = 0; i < k; ++i) {
+      const double* uo = a.Uout + ((size_t)b * k + i) * L;
+      double v = -1.0;
+      int ix = 0;
+      for (int t = tid; t < L; t += blockDim.x) {
+        double x = fabs(uo[t]);
+        if (x > v) { v = x; ix = t; }
       }
+      for (int o = 16; o > 0; o >>= 1) {
+        double v2 = __shfl_xor_sync(0xffffffffu, v, o);
+        int i2 = __shfl_xor_sync(0xffffffffu, ix, o);
+        if (v2 > v || (v2 == v && i2 < ix)) { v = v2; ix = i2; }
+      }
+      if (lane == 0) { mxv[w * kMaxK + i] = v; mxi[w * kMaxK + i] = ix; }
     }
     __syncthreads();
     if (tid < k) {

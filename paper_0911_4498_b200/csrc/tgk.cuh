@@ -79,7 +79,8 @@ __device__ __forceinline__ TgkNorms tgk_norms(const double* c, const double* c2,
 // every bracket is below 2 eps of its upper end.  All threads call; ends with a barrier.
 // c2n: c2 / gmax^2 (shared memory).
 __device__ inline void tgk_topk_values(const double* c2n, int n, int k, const TgkNorms& nrm, double* lohi, double* lam,
-                                int max_rounds) {
+                                int max_rounds, int stride = 1) {
+  // value j is the (j * stride + 1)-th largest eigenvalue (stride > 1: a sparse subset)
   const int tid = threadIdx.x, nthr = blockDim.x;
   int T = 32;
   while (T > 1 && k * T > nthr) T >>= 1;
@@ -92,7 +93,7 @@ __device__ inline void tgk_topk_values(const double* c2n, int n, int k, const Tg
     int open = act && (hi - lo > 4.440892098500626e-16 * hi) && (hi - lo > nrm.pivmin);
     if (!__syncthreads_or(open)) break;
     double x = lo + (hi - lo) * (double)(t + 1) / (double)(T + 1);
-    bool pred = act && (n - tgk_negcount_poly(c2n, n, x / nrm.gmax) >= j + 1);
+    bool pred = act && (n - tgk_negcount_poly(c2n, n, x / nrm.gmax) >= j * stride + 1);
     unsigned bits = __ballot_sync(0xffffffffu, pred);
     int shift = (T >= 32) ? 0 : ((tid & 31) / T) * T;
     unsigned gb = (T >= 32) ? bits : ((bits >> shift) & ((1u << T) - 1u));
@@ -115,7 +116,8 @@ __device__ inline void tgk_topk_values(const double* c2n, int n, int k, const Tg
 // alpha_next = alpha_{m+1}.  All threads call; ends with a barrier.
 // c2n: scratch of n-1 doubles (shared memory) for the normalized squares.
 __device__ inline void tgk_check(const double* c, const double* c2, double* c2n, int m, int k, double alpha_next,
-                                 double* omega, double* res, double* lohi, double* scratch) {
+                                 double* omega, double* res, double* lohi, double* scratch, int stride = 1) {
+  // k values (the (j * stride + 1)-th largest, j < k) and their residuals
   const int n = 2 * m + 1;
   const int tid = threadIdx.x;
   const TgkNorms nrm = tgk_norms(c, c2, n);
@@ -125,7 +127,7 @@ __device__ inline void tgk_check(const double* c, const double* c2, double* c2n,
     for (int i = tid; i < n - 1; i += blockDim.x) c2n[i] = c2[i] * ig2;
     __syncthreads();
   }
-  tgk_topk_values(c2n, n, k, nrm, lohi, omega, 16);
+  tgk_topk_values(c2n, n, k, nrm, lohi, omega, 16, stride);
   // twisted factorization for lambda = omega_j, two lanes per value: the even lane runs
   // the forward pivots D+ (and later the entries above the twist), the odd lane the
   // backward pivots D- (and the entries below).  Twist r at the smallest
@@ -193,6 +195,162 @@ __device__ inline void tgk_check(const double* c, const double* c2, double* c2n,
   __syncthreads();
 }
 
+// Clusters of the k values (descending): maximal runs with lam[j-1] - lam[j] <=
+// 1e-3 |T| (LAPACK dstein's ORTOL: outside a cluster independently computed vectors are
+// orthogonal to O(eps |T| / gap) <= 2e-13).  cl[0..nc] = starts (cl[nc] = k),
+// cl[33] = nc.  Returns 1 if some gap inside a cluster is below 1e-11 |T| or a value is
+// below 1e-11 |T| (near the eigenvalue 0 that TGK of odd order always has): such
+// near-degenerate values need inverse iteration with orthogonalization (tgk_vectors).
+// Thread 0 only.
+__device__ inline int tgk_clusters(const double* lam, int k, double tnorm, int* cl) {
+  const double ortol = 1e-3 * tnorm, degen = 1e-11 * tnorm;
+  int nc = 0, bad = 0;
+  for (int j = 0; j < k; ++j) {
+    if (j == 0 || lam[j - 1] - lam[j] > ortol) cl[nc++] = j;
+    else if (lam[j - 1] - lam[j] < degen) bad = 1;
+    if (!(lam[j] > degen)) bad = 1;
+  }
+  cl[nc] = k;
+  cl[33] = nc;
+  return bad;
+}
+
+// Modified Gram-Schmidt (twice) of the columns j0..j1-1 of C (rows x k, column j at
+// C[r * k + j]); one warp, lanes over rows.
+__device__ inline void warp_mgs_cols(double* C, int rows, int k, int j0, int j1) {
+  const int lane = threadIdx.x & 31;
+  for (int j = j0; j < j1; ++j) {
+    for (int pass = 0; pass < 2; ++pass)
+      for (int q = j0; q < j; ++q) {
+        double d = 0.0;
+        for (int r = lane; r < rows; r += 32) d = fma(C[(size_t)r * k + j], C[(size_t)r * k + q], d);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
+        for (int r = lane; r < rows; r += 32) C[(size_t)r * k + j] = fma(-d, C[(size_t)r * k + q], C[(size_t)r * k + j]);
+        __syncwarp();
+      }
+    double s2 = 0.0;
+    for (int r = lane; r < rows; r += 32) s2 = fma(C[(size_t)r * k + j], C[(size_t)r * k + j], s2);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
+    const double inv = s2 > 0.0 ? 1.0 / sqrt(s2) : 0.0;
+    for (int r = lane; r < rows; r += 32) C[(size_t)r * k + j] *= inv;
+    __syncwarp();
+  }
+}
+
+// Final small SVD of B_m (north star (b); Thm 1):
+// the k largest eigenvalues of TGK to full precision (multisection), each eigenvector by
+// ONE twisted factorization (two lanes per value, as in tgk_check: the solution of
+// (TGK - lam I) z = gamma_r e_r at the twist r of smallest |gamma_r|), split into
+// p (even entries, rows of P_k: cP[r * k + j], r <= m) and q (odd entries, Q_k: cQ[r * k +
+// j], r < m), each half normalized, then MGS inside clusters (tgk_clusters) so P_k and
+// Q_k are orthonormal to working precision.  res[j] = alpha_{m+1} |P_{m+1,j}| (Eq. (2)).
+// scratch: 2 n k doubles (pivots).  Returns 0 (nothing written) when tgk_clusters finds
+// near-degenerate values.  All threads call; ends with a barrier.  Needs 2k <= blockDim.x.
+__device__ inline int tgk_final(const double* c, const double* c2, double* c2n, int m, int k, double alpha_next,
+                                double* lam, double* lohi, double* res, double* scratch, double* cP, double* cQ,
+                                int* cl) {
+  const int n = 2 * m + 1;
+  const int tid = threadIdx.x;
+  const TgkNorms nrm = tgk_norms(c, c2, n);
+  const double pivmin = nrm.pivmin;
+  {
+    const double ig2 = (nrm.gmax > 0.0) ? 1.0 / (nrm.gmax * nrm.gmax) : 0.0;
+    for (int i = tid; i < n - 1; i += blockDim.x) c2n[i] = c2[i] * ig2;
+    __syncthreads();
+  }
+  tgk_topk_values(c2n, n, k, nrm, lohi, lam, 60);
+  __shared__ int s_bad;
+  if (tid == 0) s_bad = tgk_clusters(lam, k, nrm.gmax, cl);
+  __syncthreads();
+  if (s_bad) return 0;
+  const unsigned pmask = __ballot_sync(0xffffffffu, tid < 2 * k);
+  if (tid < 2 * k) {
+    const int j = tid >> 1, role = tid & 1;
+    const double lm = lam[j];
+    double* Dp = scratch;                  // Dp[i * k + j]
+    double* Dm = scratch + (size_t)n * k;  // Dm[i * k + j]
+    if (role == 0) {
+      double q = -lm;
+      Dp[j] = q;
+      for (int i = 1; i < n; ++i) {
+        if (fabs(q) < pivmin) q = -pivmin;
+        q = fma(-c2[i - 1], __drcp_rn(q), -lm);
+        Dp[(size_t)i * k + j] = q;
+      }
+    } else {
+      double q = -lm;
+      Dm[(size_t)(n - 1) * k + j] = q;
+      for (int i = n - 2; i >= 0; --i) {
+        if (fabs(q) < pivmin) q = -pivmin;
+        q = fma(-c2[i], __drcp_rn(q), -lm);
+        Dm[(size_t)i * k + j] = q;
+      }
+    }
+    __syncwarp(pmask);
+    const int h0 = role ? n / 2 : 0, h1 = role ? n : n / 2;
+    double gbest = 1e308;
+    int r = -1;
+#pragma unroll 4
+    for (int i = h0; i < h1; ++i) {
+      const double g = fabs(Dp[(size_t)i * k + j] + Dm[(size_t)i * k + j] + lm);
+      if (g < gbest) { gbest = g; r = i; }
+    }
+    const double go = __shfl_xor_sync(pmask, gbest, 1);
+    const int ro = __shfl_xor_sync(pmask, r, 1);
+    if (go < gbest || (go == gbest && ro >= 0 && (r < 0 || ro < r))) { gbest = go; r = ro; }
+    // z_r = 1; role 0 writes the entries above the twist, role 1 the twist and below;
+    // even i -> p_{i/2}, odd i -> q_{(i-1)/2}
+    double sp = 0.0, sq = 0.0;
+    if (role == 0) {
+      double z = 1.0;
+      for (int i = r - 1; i >= 0; --i) {
+        double d = Dp[(size_t)i * k + j];
+        if (fabs(d) < pivmin) d = -pivmin;
+        z = -(c[i] * __drcp_rn(d)) * z;
+        if (i & 1) { cQ[(size_t)(i >> 1) * k + j] = z; sq = fma(z, z, sq); }
+        else { cP[(size_t)(i >> 1) * k + j] = z; sp = fma(z, z, sp); }
+      }
+    } else {
+      double z = 1.0;
+      if (r & 1) { cQ[(size_t)(r >> 1) * k + j] = z; sq = 1.0; }
+      else { cP[(size_t)(r >> 1) * k + j] = z; sp = 1.0; }
+      for (int i = r + 1; i < n; ++i) {
+        double d = Dm[(size_t)i * k + j];
+        if (fabs(d) < pivmin) d = -pivmin;
+        z = -(c[i - 1] * __drcp_rn(d)) * z;
+        if (i & 1) { cQ[(size_t)(i >> 1) * k + j] = z; sq = fma(z, z, sq); }
+        else { cP[(size_t)(i >> 1) * k + j] = z; sp = fma(z, z, sp); }
+      }
+    }
+    sp += __shfl_xor_sync(pmask, sp, 1);
+    sq += __shfl_xor_sync(pmask, sq, 1);
+    const double ip = sp > 0.0 ? 1.0 / sqrt(sp) : 0.0, iq = sq > 0.0 ? 1.0 / sqrt(sq) : 0.0;
+    __syncwarp(pmask);
+    // normalize the halves (each lane its own entries)
+    const int i0 = role ? r : 0, i1 = role ? n : r;
+    for (int i = i0; i < i1; ++i) {
+      if (i & 1) cQ[(size_t)(i >> 1) * k + j] *= iq;
+      else cP[(size_t)(i >> 1) * k + j] *= ip;
+    }
+  }
+  __syncthreads();
+  // orthonormalize inside clusters: one warp per cluster
+  {
+    const int w = tid >> 5, nw = blockDim.x >> 5, nc = cl[33];
+    for (int q = w; q < nc; q += nw) {
+      if (cl[q + 1] - cl[q] < 2) continue;
+      warp_mgs_cols(cP, m + 1, k, cl[q], cl[q + 1]);
+      warp_mgs_cols(cQ, m, k, cl[q], cl[q + 1]);
+    }
+  }
+  __syncthreads();
+  if (tid < k) res[tid] = alpha_next * fabs(cP[(size_t)m * k + tid]);
+  __syncthreads();
+  return 1;
+}
+
 // splitmix64-based uniform(-1,1) for inverse-iteration start vectors.
 __device__ __forceinline__ double tgk_rand(unsigned long long key, unsigned long long i) {
   unsigned long long x = key + (i + 1) * 0x9E3779B97F4A7C15ull;
@@ -216,7 +374,7 @@ __device__ inline void tgk_vectors(const double* c, int n, int k, const double* 
                                    double* W, int* ipv, unsigned long long seed, int* cl_start) {
   const int tid = threadIdx.x;
   const double tnorm = nrm.gmax;
-  const double ortol = 1e-5 * tnorm;
+  const double ortol = 1e-3 * tnorm;  // LAPACK dstein ORTOL
   if (tid == 0) {
     int nc = 0;
     for (int j = 0; j < k; ++j)

@@ -159,18 +159,23 @@ def test_decompose_cfg1(P):
     print("cfg1 worst:", rep.worst(), "steps", info[0]["steps"])
 
 
+@pytest.mark.parametrize("reorth", [1, 2])
 @pytest.mark.parametrize("N,L,k", [(40, 20, 3), (41, 30, 5), (64, 10, 4), (100, 50, 8), (127, 64, 6),
                                    (300, 100, 10), (513, 256, 12), (2000, 1700, 16)])
-def test_decompose_random_shapes(P, N, L, k):
+def test_decompose_random_shapes(P, N, L, k, reorth):
+    """Both reorthogonalization modes (CGS + DGKS, CGS2) against the
+    oracle; Ritz vectors orthonormal to working precision."""
     rng = np.random.default_rng(N + 13 * L)
     n = np.arange(1, N + 1)
     B = 3
     F = np.stack([np.sin(2 * np.pi * n / 9.7) + 0.5 * np.cos(2 * np.pi * n / 31) + 0.3 * rng.standard_normal(N)
                   for _ in range(B)])
-    s, U, V, G, info = run_decompose(P, F, L, k)
+    s, U, V, G, info = run_decompose(P, F, L, k, reorth=reorth)
     for b in range(B):
         assert info[b]["status"] == 0, info[b]
         check_against_oracle(F[b], L, k, s[b], U[b], V[b], G[b])
+        assert np.abs(U[b] @ U[b].T - np.eye(k)).max() <= 1e-13
+        assert np.abs(V[b] @ V[b].T - np.eye(k)).max() <= 1e-13
 
 
 def test_decompose_full_rank_small_exact(P):
