@@ -49,7 +49,7 @@ __device__ __forceinline__ void real_pair(const double2* buf, const FftShape& sh
   const int q = (H - p) & (H - 1);
   pr = rev_index(sh, p);
   qr = rev_index(sh, q);
-  double2 Zp = buf[fpad(pr)], Zq = buf[fpad(qr)];
+  double2 Zp = buf[fsw(pr)], Zq = buf[fsw(qr)];
   double2 W = tw(p);
   double2 E = make_double2(0.5 * (Zp.x + Zq.x), 0.5 * (Zp.y - Zq.y));
   double2 D = make_double2(0.5 * (Zp.x - Zq.x), 0.5 * (Zp.y + Zq.y));
@@ -68,8 +68,8 @@ __device__ __forceinline__ void inv_pair(double2* buf, const TW& tw, int p, int 
   double2 E = make_double2(0.5 * (Yp.x + Yq.x), 0.5 * (Yp.y - Yq.y));
   double2 D = make_double2(0.5 * (Yp.x - Yq.x), 0.5 * (Yp.y + Yq.y));
   double2 O = cmulc(D, W);
-  buf[fpad(pr)] = make_double2(E.x - O.y, E.y + O.x);
-  if (qr != pr) buf[fpad(qr)] = make_double2(E.x + O.y, O.x - E.y);
+  buf[fsw(pr)] = make_double2(E.x - O.y, E.y + O.x);
+  if (qr != pr) buf[fsw(qr)] = make_double2(E.x + O.y, O.x - E.y);
 }
 
 // Correlation spectrum step: Z (digit-reversed FFT of packed x) -> Z' whose inverse is
@@ -104,7 +104,7 @@ __device__ __forceinline__ void correlate_cta(double2* buf, const FftShape& sh, 
     int i0 = 2 * n;
     double a = (i0 < n_in) ? loadx(i0) : 0.0;
     double b = (i0 + 1 < n_in) ? loadx(i0 + 1) : 0.0;
-    buf[fpad(n)] = make_double2(a, b);
+    buf[fsw(n)] = make_double2(a, b);
   }
   __syncthreads();
   fft_forward(buf, sh, T, tid, nthr, CtaSync());
@@ -113,7 +113,7 @@ __device__ __forceinline__ void correlate_cta(double2* buf, const FftShape& sh, 
   fft_inverse(buf, sh, T, tid, nthr, CtaSync());
   const double invH = 1.0 / (double)H;
   for (int t = tid; t < n_out; t += nthr) {
-    double2 z = buf[fpad(t >> 1)];
+    double2 z = buf[fsw(t >> 1)];
     storey(t, ((t & 1) ? z.y : z.x) * invH);
   }
 }
@@ -146,6 +146,26 @@ __device__ __forceinline__ void tma_load_1d(void* dst, const void* src, uint32_t
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+// Same with an L2 cache-eviction policy (createpolicy.*: evict_last keeps a row that is
+// read again soon, evict_first drops one read for the last time).
+__device__ __forceinline__ void tma_load_1d_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                                 uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 __device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 
@@ -171,6 +191,12 @@ __device__ __forceinline__ void ring_init(WarpRing& rg, double* buf, uint64_t* b
 template <int NST = kStages, class F>
 __device__ __forceinline__ void stream_rows(const double* base_w, int ld, int nb, bool reverse, int slab, WarpRing& rg,
                                             F f) {
+  stream_rows<NST>(base_w, ld, nb, reverse, slab, rg, 0ull, f);
+}
+// Same with an L2 eviction policy for every load (0: none).
+template <int NST = kStages, class F>
+__device__ __forceinline__ void stream_rows(const double* base_w, int ld, int nb, bool reverse, int slab, WarpRing& rg,
+                                            uint64_t policy, F f) {
   constexpr int kStages = NST;  // ring depth of this stream (the ring must have NST stages)
   const int lane = threadIdx.x & 31;
   const uint32_t bytes = (uint32_t)slab * 8u;
@@ -181,7 +207,8 @@ __device__ __forceinline__ void stream_rows(const double* base_w, int ld, int nb
       int st = (int)((c0 + q) % kStages);
       int row = reverse ? nb - 1 - q : q;
       mbar_expect_tx(rg.bar + st, bytes);
-      tma_load_1d(rg.buf + (size_t)st * slab, base_w + (size_t)row * ld, bytes, rg.bar + st);
+      if (policy) tma_load_1d_hint(rg.buf + (size_t)st * slab, base_w + (size_t)row * ld, bytes, rg.bar + st, policy);
+      else tma_load_1d(rg.buf + (size_t)st * slab, base_w + (size_t)row * ld, bytes, rg.bar + st);
     }
   }
   for (int q = 0; q < nb; ++q) {
@@ -193,7 +220,8 @@ __device__ __forceinline__ void stream_rows(const double* base_w, int ld, int nb
     if (lane == 0 && q + kStages < nb) {
       int row = reverse ? nb - 1 - (q + kStages) : q + kStages;
       mbar_expect_tx(rg.bar + st, bytes);
-      tma_load_1d(rg.buf + (size_t)st * slab, base_w + (size_t)row * ld, bytes, rg.bar + st);
+      if (policy) tma_load_1d_hint(rg.buf + (size_t)st * slab, base_w + (size_t)row * ld, bytes, rg.bar + st, policy);
+      else tma_load_1d(rg.buf + (size_t)st * slab, base_w + (size_t)row * ld, bytes, rg.bar + st);
     }
   }
   rg.cnt = c0 + nb;
@@ -206,7 +234,7 @@ __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~(size_t
 __device__ __forceinline__ TwSmem load_tw2(const double2* __restrict__ g, double2* sm, int M) {
   const int n = tw2_entries(M);
   for (int i = threadIdx.x; i < n; i += blockDim.x) sm[i] = __ldg(g + i);
-  return TwSmem{sm, sm + 64};
+  return TwSmem{sm, sm + 64, sm + tw2_base_entries(M)};
 }
 
 }  // namespace ssa

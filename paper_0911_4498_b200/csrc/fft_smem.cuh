@@ -12,8 +12,7 @@
 // evaluated as an FFT.  All index arithmetic is shifts/masks (H and radices are powers
 // of two).
 //
-// Shared-memory layout: element i lives at slot i + (i >> 3) (one pad slot per 8) so
-// that stride-8 radix-8 butterflies of the last pass hit distinct banks.
+// Shared-memory layout: the XOR swizzle fsw below.
 // Twiddles come from a global table T[t] = exp(-2 pi i t / M), t in [0, H), computed on
 // the host in extended precision (ssa_api.cu); exp(-2 pi i t / M) for t in [H, M) is
 // -T[t - H].
@@ -23,8 +22,16 @@
 
 namespace ssa {
 
-__host__ __device__ __forceinline__ int fpad(int i) { return i + (i >> 3); }
-__host__ __device__ __forceinline__ int fpad_size(int H) { return H + (H >> 3) + 1; }
+// XOR swizzle of the 16-byte elements inside each 128-byte row (8 elements): element i
+// lives at i ^ g(i >> 3), g = XOR of the 3-bit digits of the row index.  Conflict-free
+// (one wavefront per 8 lanes) for unit-stride runs, the stride-8 accesses of the last
+// radix-8/4/2 passes and the digit-reversed pair steps (stride H/8), where plain rows
+// would be 8-way conflicted; no padding, so a buffer of H points is H * 16 bytes.
+__host__ __device__ __forceinline__ int fsw(int i) {
+  const int j = i >> 3;
+  return i ^ ((j ^ (j >> 3) ^ (j >> 6) ^ (j >> 9) ^ (j >> 12)) & 7);
+}
+__host__ __device__ __forceinline__ int fft_elems(int H) { return H; }
 
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
   return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
@@ -47,8 +54,22 @@ __device__ __forceinline__ double2 twiddle(const double2* __restrict__ T, int t,
 //  TwGlobal: the half table T[t] = exp(-2 pi i t / M), t < H, in global memory.
 //  TwSmem:   two-level table in shared memory, lo[j] = exp(-2 pi i j / M) (j < 64) and
 //            hi[j] = exp(-2 pi i 64 j / M) (j < max(1, M/64)); one complex product per lookup
-//            (error ~1 ulp more than a direct table), 5 KB at M = 16384 -- the direct table
-//            would not stay in L1 next to 100+ KB of shared memory per CTA.
+//            (error ~1 ulp more than a direct table) -- used by the real-FFT pair steps,
+//            whose lanes read consecutive entries.  Followed by per-pass tables for the
+//            radix-8 passes of the H = M/2 point FFT (tw_pass_entries): pass with block
+//            size S = 2^logS needs W_S^{n1}, n1 < Q = S/8, as lo_p[n1 & 63] (x hi_p[n1 >> 6]
+//            when Q > 64), so consecutive lanes (consecutive n1) read consecutive entries:
+//            no bank conflicts (a single table indexed by n1 << shift would be 2..8-way
+//            conflicted) and one complex product fewer for Q <= 64.
+__host__ __device__ constexpr int tw_pass_count(int logS) {  // entries of one radix-8 pass
+  return (logS - 3 > 6) ? 64 + (1 << (logS - 3 - 6)) : (1 << (logS - 3 > 0 ? logS - 3 : 0));
+}
+__host__ __device__ constexpr int tw_pass_offset(int logH, int logS) {  // passes before logS
+  return (logS >= logH) ? 0 : tw_pass_count(logH) + tw_pass_offset(logH - 3, logS);
+}
+__host__ __device__ constexpr int tw_pass_entries(int logH) {  // all radix-8 passes
+  return (logH < 3) ? 0 : tw_pass_count(logH) + tw_pass_entries(logH - 3);
+}
 struct TwGlobal {
   const double2* T;
   int H;
@@ -57,10 +78,22 @@ struct TwGlobal {
 struct TwSmem {
   const double2* lo;
   const double2* hi;
+  const double2* pass;  // per-pass tables of the H-point FFT (H = M/2)
   __device__ __forceinline__ double2 operator()(int t) const { return cmul(lo[t & 63], hi[t >> 6]); }
+  // W_S^{n1} for the radix-8 pass with block size 2^logS of an FFT of 2^logH points
+  __device__ __forceinline__ double2 pass_w(int logH, int logS, int n1) const {
+    const double2* tp = pass + tw_pass_offset(logH, logS);
+    if (logS - 3 > 6) return cmul(tp[n1 & 63], tp[64 + (n1 >> 6)]);
+    return tp[n1];
+  }
 };
-// entries of the two-level table for size M (lo then hi)
-__host__ __device__ inline int tw2_entries(int M) { return 64 + (M / 64 > 1 ? M / 64 : 1); }
+// entries of the two-level table for size M (lo then hi), then the pass tables of M/2
+__host__ __device__ inline int tw2_base_entries(int M) { return 64 + (M / 64 > 1 ? M / 64 : 1); }
+__host__ __device__ inline int tw2_entries(int M) {
+  int l = 0;
+  while ((1 << l) < M / 2) ++l;
+  return tw2_base_entries(M) + tw_pass_entries(l);
+}
 
 // Shape: n8 radix-8 passes then one radix-2^lastb pass (lastb in {0,1,2}).
 struct FftShape {
@@ -153,17 +186,16 @@ __device__ __forceinline__ void fft_pass(double2* buf, int H, int logH, int logS
   constexpr int R = 1 << LR;
   const int logQ = logS - LR;
   const int Q = 1 << logQ;
-  const int tshift = logH + 1 - logS;  // exp(-2 pi i n1 k2 / S) = T[n1 k2 << (logM - logS)]
   for (int bf = tid; bf < (H >> LR); bf += nthr) {
     const int b = bf >> logQ, n1 = bf & (Q - 1);
     const int base = (b << logS) + n1;
     double2 a[R];
 #pragma unroll
-    for (int q = 0; q < R; ++q) a[q] = buf[fpad(base + (q << logQ))];
+    for (int q = 0; q < R; ++q) a[q] = buf[fsw(base + (q << logQ))];
     double2 w[R];
     if (Q > 1) {
-      // w_q = W_S^{n1 q} = (W_S^{n1})^q: one table lookup, powers by products
-      w[1] = tw(n1 << tshift);
+      // w_q = W_S^{n1 q} = (W_S^{n1})^q: one per-pass table lookup, powers by products
+      w[1] = tw.pass_w(logH, logS, n1);
       if constexpr (R >= 4) { w[2] = cmul(w[1], w[1]); w[3] = cmul(w[2], w[1]); }
       if constexpr (R == 8) {
         w[4] = cmul(w[2], w[2]); w[5] = cmul(w[4], w[1]); w[6] = cmul(w[4], w[2]); w[7] = cmul(w[4], w[3]);
@@ -179,7 +211,7 @@ __device__ __forceinline__ void fft_pass(double2* buf, int H, int logH, int logS
       for (int q = 1; q < R; ++q) a[q] = cmul(a[q], w[q]);
     }
 #pragma unroll
-    for (int q = 0; q < R; ++q) buf[fpad(base + (q << logQ))] = a[q];
+    for (int q = 0; q < R; ++q) buf[fsw(base + (q << logQ))] = a[q];
   }
 }
 

@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <vector>
 
+#include "fft_smem.cuh"
 #include "ssa_internal.h"
 
 using ssa::Plan;
@@ -71,14 +72,26 @@ static std::vector<double2> make_twiddles(int64_t M) {
 
 // Two-level table for size M: lo[j] = exp(-2 pi i j / M), j < 64; hi[j] = exp(-2 pi i 64 j / M).
 static std::vector<double2> make_twiddles2(int64_t M) {
+  // two-level table lo[j] = W_M^j (j < 64), hi[j] = W_M^{64 j}, then the per-pass tables
+  // of the M/2-point FFT (fft_smem.cuh TwSmem): pass with block size S = 2^logS gets
+  // W_S^a (a < min(Q, 64)) and, when Q = S/8 > 64, W_S^{64 b} (b < Q/64)
+  const long double pi2 = 2.0L * 3.14159265358979323846264338327950288L;
+  auto w = [&](long double num, long double den) {
+    const long double ang = pi2 * num / den;
+    return make_double2((double)cosl(ang), (double)(-sinl(ang)));
+  };
   const int nhi = (int)std::max<int64_t>(1, M / 64);
-  std::vector<double2> tw((size_t)(64 + nhi));
-  for (int j = 0; j < 64 + nhi; ++j) {
-    const long double t = (j < 64) ? (long double)j : 64.0L * (long double)(j - 64);
-    long double ang = 2.0L * 3.14159265358979323846264338327950288L * t / (long double)M;
-    tw[(size_t)j].x = (double)cosl(ang);
-    tw[(size_t)j].y = (double)(-sinl(ang));
+  std::vector<double2> tw;
+  for (int j = 0; j < 64 + nhi; ++j) tw.push_back(w((j < 64) ? (long double)j : 64.0L * (long double)(j - 64), (long double)M));
+  int logH = 0;
+  while ((1LL << logH) < M / 2) ++logH;
+  for (int logS = logH; logS >= 3; logS -= 3) {
+    const int64_t Q = 1LL << (logS - 3), S = 1LL << logS;
+    for (int64_t a = 0; a < std::min<int64_t>(Q, 64); ++a) tw.push_back(w((long double)a, (long double)S));
+    if (Q > 64)
+      for (int64_t b = 0; b < Q / 64; ++b) tw.push_back(w(64.0L * (long double)b, (long double)S));
   }
+  if (tw.size() != (size_t)ssa::tw2_entries((int)M)) tw.clear();  // layout mismatch: caller fails
   return tw;
 }
 
@@ -250,6 +263,7 @@ extern "C" ssa_status ssa_plan_create(int64_t N, int64_t L, int32_t k, int64_t b
   }
   {
     std::vector<double2> tw = make_twiddles(M), twl = make_twiddles2(M);
+    if (twl.empty()) { st = fail(SSA_ERR_INTERNAL, "twiddle table layout mismatch"); goto bad; }
     if ((st = alloc((void**)&p.d_tw, tw.size() * sizeof(double2), "twiddles")) != SSA_OK) goto bad;
     if ((st = alloc((void**)&p.d_twl, twl.size() * sizeof(double2), "twiddles")) != SSA_OK) goto bad;
     e = cudaMemcpy(p.d_tw, tw.data(), tw.size() * sizeof(double2), cudaMemcpyHostToDevice);
@@ -258,7 +272,7 @@ extern "C" ssa_status ssa_plan_create(int64_t N, int64_t L, int32_t k, int64_t b
     const char* which = "";
     e = (H <= ssa::kMaxSmemH) ? ssa::fft_set_attributes((int)H, &which) : cudaSuccess;
     if (e != cudaSuccess) {
-      st = fail(SSA_ERR_CUDA, "cudaFuncSetAttribute(%s, %zu B smem): %s", which, ssa::fpad_bytes((int)H),
+      st = fail(SSA_ERR_CUDA, "cudaFuncSetAttribute(%s, %zu B smem): %s", which, ssa::fft_bytes((int)H),
                 cudaGetErrorString(e));
       cudaGetLastError();
       goto bad;
@@ -269,6 +283,7 @@ extern "C" ssa_status ssa_plan_create(int64_t N, int64_t L, int32_t k, int64_t b
     int N1, N2;
     ssa::large_geom(p, &N1, &N2);
     std::vector<double2> t1 = make_twiddles2(2 * (int64_t)N1), t2 = make_twiddles2(2 * (int64_t)N2);
+    if (t1.empty() || t2.empty()) { st = fail(SSA_ERR_INTERNAL, "twiddle table layout mismatch"); goto bad; }
     if ((st = alloc((void**)&p.d_tw1, t1.size() * 16, "twiddles N1")) != SSA_OK) goto bad;
     if ((st = alloc((void**)&p.d_tw2, t2.size() * 16, "twiddles N2")) != SSA_OK) goto bad;
     e = cudaMemcpy(p.d_tw1, t1.data(), t1.size() * 16, cudaMemcpyHostToDevice);

@@ -17,7 +17,7 @@ __global__ void __launch_bounds__(kThreads) spectrum_kernel(const double* __rest
                                                             const double2* __restrict__ T, double2* __restrict__ spec) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double2* buf = reinterpret_cast<double2*>(smem_raw);
-  const TwSmem tw = load_tw2(T, buf + fpad_size(H), 2 * H);
+  const TwSmem tw = load_tw2(T, buf + fft_elems(H), 2 * H);
   const FftShape sh = make_shape(H);
   const int b = blockIdx.x;
   const double* f = series + (size_t)b * N;
@@ -26,7 +26,7 @@ __global__ void __launch_bounds__(kThreads) spectrum_kernel(const double* __rest
     int i0 = 2 * n;
     double a = (i0 < N) ? f[i0] : 0.0;
     double c = (i0 + 1 < N) ? f[i0 + 1] : 0.0;
-    buf[fpad(n)] = make_double2(a, c);
+    buf[fsw(n)] = make_double2(a, c);
   }
   __syncthreads();
   fft_forward(buf, sh, tw, threadIdx.x, blockDim.x, CtaSync());
@@ -44,7 +44,7 @@ __global__ void __launch_bounds__(kThreads) matvec_kernel(const double2* __restr
                                                           double* __restrict__ y) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double2* buf = reinterpret_cast<double2*>(smem_raw);
-  const TwSmem tw = load_tw2(T, buf + fpad_size(H), 2 * H);  // visible after correlate's first barrier
+  const TwSmem tw = load_tw2(T, buf + fft_elems(H), 2 * H);  // visible after correlate's first barrier
   const FftShape sh = make_shape(H);
   const int b = blockIdx.x;
   const double* xb = x + (size_t)b * n_in;
@@ -67,8 +67,8 @@ __global__ void __launch_bounds__(kThreads) hankelize_kernel(const double* __res
                                                              double* __restrict__ out, double2* gscratch) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double2* bufB = reinterpret_cast<double2*>(smem_raw);
-  double2* bufA = BIG ? nullptr : bufB + fpad_size(H);
-  const TwSmem tw = load_tw2(T, bufB + (BIG ? 1 : 2) * fpad_size(H), 2 * H);
+  double2* bufA = BIG ? nullptr : bufB + fft_elems(H);
+  const TwSmem tw = load_tw2(T, bufB + (BIG ? 1 : 2) * fft_elems(H), 2 * H);
   double2* Xu = BIG ? gscratch + (size_t)blockIdx.x * (H + 1) : nullptr;
   const FftShape sh = make_shape(H);
   const int mn = L < K ? L : K;
@@ -80,7 +80,7 @@ __global__ void __launch_bounds__(kThreads) hankelize_kernel(const double* __res
       __syncthreads();
       for (int n = threadIdx.x; n < H; n += blockDim.x) {
         int i0 = 2 * n;
-        bufB[fpad(n)] = make_double2(i0 < L ? __ldg(u + i0) : 0.0, i0 + 1 < L ? __ldg(u + i0 + 1) : 0.0);
+        bufB[fsw(n)] = make_double2(i0 < L ? __ldg(u + i0) : 0.0, i0 + 1 < L ? __ldg(u + i0 + 1) : 0.0);
       }
       __syncthreads();
       fft_forward(bufB, sh, tw, threadIdx.x, blockDim.x, CtaSync());
@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(kThreads) hankelize_kernel(const double* __res
       __syncthreads();
       for (int n = threadIdx.x; n < H; n += blockDim.x) {
         int i0 = 2 * n;
-        bufB[fpad(n)] = make_double2(i0 < K ? __ldg(v + i0) : 0.0, i0 + 1 < K ? __ldg(v + i0 + 1) : 0.0);
+        bufB[fsw(n)] = make_double2(i0 < K ? __ldg(v + i0) : 0.0, i0 + 1 < K ? __ldg(v + i0 + 1) : 0.0);
       }
       __syncthreads();
       fft_forward(bufB, sh, tw, threadIdx.x, blockDim.x, CtaSync());
@@ -108,8 +108,8 @@ __global__ void __launch_bounds__(kThreads) hankelize_kernel(const double* __res
       __syncthreads();
       for (int n = threadIdx.x; n < H; n += blockDim.x) {
         int i0 = 2 * n;
-        bufA[fpad(n)] = make_double2(i0 < L ? __ldg(u + i0) : 0.0, i0 + 1 < L ? __ldg(u + i0 + 1) : 0.0);
-        bufB[fpad(n)] = make_double2(i0 < K ? __ldg(v + i0) : 0.0, i0 + 1 < K ? __ldg(v + i0 + 1) : 0.0);
+        bufA[fsw(n)] = make_double2(i0 < L ? __ldg(u + i0) : 0.0, i0 + 1 < L ? __ldg(u + i0 + 1) : 0.0);
+        bufB[fsw(n)] = make_double2(i0 < K ? __ldg(v + i0) : 0.0, i0 + 1 < K ? __ldg(v + i0 + 1) : 0.0);
       }
       __syncthreads();
       fft_forward(bufA, sh, tw, threadIdx.x, blockDim.x, CtaSync());
@@ -127,7 +127,7 @@ __global__ void __launch_bounds__(kThreads) hankelize_kernel(const double* __res
     const double scale = sg / (double)H;
     double* g = out + term * N;
     for (int t = threadIdx.x; t < N; t += blockDim.x) {
-      double2 z = bufB[fpad(t >> 1)];
+      double2 z = bufB[fsw(t >> 1)];
       int k1 = t + 1;  // 1-based
       int c = k1;
       if (c > mn) c = mn;
@@ -138,8 +138,8 @@ __global__ void __launch_bounds__(kThreads) hankelize_kernel(const double* __res
 }
 
 static size_t tw_smem(int H) { return (size_t)tw2_entries(2 * H) * 16; }
-static size_t fft_smem(int H) { return (size_t)fpad_size(H) * 16 + tw_smem(H); }
-static size_t fft_smem2(int H) { return (size_t)2 * fpad_size(H) * 16 + tw_smem(H); }
+static size_t fft_smem(int H) { return (size_t)fft_elems(H) * 16 + tw_smem(H); }
+static size_t fft_smem2(int H) { return (size_t)2 * fft_elems(H) * 16 + tw_smem(H); }
 
 cudaError_t fft_set_attributes(int H, const char** which) {
   cudaError_t e;

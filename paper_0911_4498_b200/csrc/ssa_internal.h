@@ -15,7 +15,7 @@ constexpr int kMaxSmemH = 8192;        // largest H = M/2 held in one CTA's shar
 constexpr int kMaxHankelSmemH = 4096;  // largest H with both hankelization buffers in SMEM
 constexpr int kMaxK = 32;              // largest k of the batched decompose
 
-inline size_t fpad_bytes(int H) { return (size_t)(H + (H >> 3) + 1) * 16; }
+inline size_t fft_bytes(int H) { return (size_t)H * 16; }
 
 // Arguments of the three decompose kernels (lanczos -> bidiag SVD -> Ritz).  Per-series
 // storage covers one chunk of nb series [b0, b0+nb) of the call.

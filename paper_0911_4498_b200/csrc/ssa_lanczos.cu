@@ -35,7 +35,7 @@ struct LSmem {
 
 __host__ __device__ inline size_t lanczos_regionA_bytes(int H, int ldL, int ldK, int m_max) {
   int slab_max = (ldL > ldK ? ldL : ldK) / kWarps;
-  size_t fft = (size_t)fpad_size(H) * 16;
+  size_t fft = (size_t)fft_elems(H) * 16;
   size_t rings = (size_t)kWarps * kStages * slab_max * 8 + (size_t)kWarps * (m_max + 2) * 8;
   size_t tgk = (size_t)7 * (2 * m_max + 2) * 8;  // c, c^2, c^2/|T|^2 + the cheap test's pivots
   size_t r = fft;
@@ -104,11 +104,13 @@ __device__ double reorth_t(double* r, const double* basis, int nb, int ld, doubl
     rv[t] = (e < slab) ? rw[e] : 0.0;
   }
   double nrm = nrm_in;
+  const uint64_t pol_last = policy_evict_last(), pol_first = policy_evict_first();
   for (int pass = 0; pass < 2 && nb > 0; ++pass) {
     fence_proxy_async_smem();
     __syncthreads();
-    // pass 1: partial dots of this warp's slab with every basis row
-    stream_rows(bw, ld, nb, false, slab, rg, [&](int row, const double* ch) {
+    // pass 1: partial dots of this warp's slab with every basis row; the lines stay in L2
+    // (evict_last) for pass 2
+    stream_rows(bw, ld, nb, false, slab, rg, pol_last, [&](int row, const double* ch) {
       double s = 0.0;
 #pragma unroll
       for (int t = 0; t < EPL; ++t) {
@@ -126,8 +128,8 @@ __device__ double reorth_t(double* r, const double* basis, int nb, int ld, doubl
     }
     __syncthreads();
     // pass 2: r -= V h, rows streamed in reverse so the most recently read rows (still
-    // in L2) come first
-    stream_rows(bw, ld, nb, true, slab, rg, [&](int row, const double* ch) {
+    // in L2) come first; read for the last time in this half-step (evict_first)
+    stream_rows(bw, ld, nb, true, slab, rg, pol_first, [&](int row, const double* ch) {
       const double hc = sm.h[row];
 #pragma unroll
       for (int t = 0; t < EPL; ++t) {

@@ -44,7 +44,7 @@ __global__ void __launch_bounds__(kThreads) large_col_fwd(const double* __restri
                                                           const double2* __restrict__ T1, double2* __restrict__ Y) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double2* buf = reinterpret_cast<double2*>(smem_raw);
-  const int cs = fpad_size(N1);
+  const int cs = N1 + 1;  // odd stride (16-byte units): interleaved column loads are conflict-free
   const TwSmem tw1 = load_tw2(T1, buf + kColW * cs, 2 * N1);
   const FftShape s1 = make_shape(N1);
   const int n2_0 = blockIdx.x * kColW;
@@ -56,7 +56,7 @@ __global__ void __launch_bounds__(kThreads) large_col_fwd(const double* __restri
     const long long i0 = 2 * n;
     double a = (i0 < n_in) ? __ldg(xi + i0) : 0.0;
     double b = (i0 + 1 < n_in) ? __ldg(xi + i0 + 1) : 0.0;
-    buf[c * cs + fpad(n1)] = make_double2(a, b);
+    buf[c * cs + fsw(n1)] = make_double2(a, b);
   }
   __syncthreads();
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(kThreads) large_col_fwd(const double* __restri
   for (int idx = threadIdx.x; idx < N1 * kColW; idx += blockDim.x) {
     const int c = idx & (kColW - 1), k1 = idx >> 3;
     const int n2 = n2_0 + c;
-    double2 v = buf[c * cs + fpad(subrev(s1, k1))];
+    double2 v = buf[c * cs + fsw(subrev(s1, k1))];
     v = cmul(v, twH(T, (long long)n2 * k1, H));
     Yi[(size_t)n2 + (size_t)N2 * k1] = v;
   }
@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(kThreads) large_col_inv(const double2* __restr
   double2* buf = reinterpret_cast<double2*>(smem_raw);
   __shared__ double red[kWarps];
   const int H = a.H, N1 = a.N1, N2 = a.N2;
-  const int cs = fpad_size(N1);
+  const int cs = N1 + 1;  // odd stride (16-byte units): interleaved column loads are conflict-free
   const TwSmem tw1 = load_tw2(T1, buf + kColW * cs, 2 * N1);
   const FftShape s1 = make_shape(N1);
   const int n2_0 = blockIdx.x * kColW;
@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(kThreads) large_col_inv(const double2* __restr
   const double2* Yi = Y + item * H;
   for (int idx = threadIdx.x; idx < N1 * kColW; idx += blockDim.x) {
     const int c = idx & (kColW - 1), k1 = idx >> 3;
-    buf[c * cs + fpad(subrev(s1, k1))] = Yi[(size_t)(n2_0 + c) + (size_t)N2 * k1];
+    buf[c * cs + fsw(subrev(s1, k1))] = Yi[(size_t)(n2_0 + c) + (size_t)N2 * k1];
   }
   __syncthreads();
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -119,7 +119,7 @@ __global__ void __launch_bounds__(kThreads) large_col_inv(const double2* __restr
     const int c = rest & (kColW - 1), n1 = rest >> 3;
     const long long n = (long long)(n2_0 + c) + (long long)N2 * n1;
     const long long t = 2 * n + h;
-    const double2 z = buf[c * cs + fpad(n1)];
+    const double2 z = buf[c * cs + fsw(n1)];
     const double y = (h ? z.y : z.x) * invH;
     if (a.mode == 0) {
       if (t < a.ld_out) {
@@ -174,7 +174,7 @@ __global__ void __launch_bounds__(kThreads) large_row_pair(const double2* __rest
                                                            RowArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int H = a.H, N1 = a.N1, N2 = a.N2;
-  const int rs = fpad_size(N2);
+  const int rs = fft_elems(N2);
   double2* bA = reinterpret_cast<double2*>(smem_raw);  // row A of Ya
   double2* bB = bA + rs;                                // row B of Ya
   double2* cA = bB + rs;                                // mode 2: row A of Yb
@@ -187,11 +187,11 @@ __global__ void __launch_bounds__(kThreads) large_row_pair(const double2* __rest
   double2* Ya = a.Ya + item * H;
   double2* Yb = (a.mode == 2) ? a.Yb + item * H : nullptr;
   for (int i = threadIdx.x; i < N2; i += blockDim.x) {
-    bA[fpad(i)] = Ya[(size_t)A * N2 + i];
-    if (two) bB[fpad(i)] = Ya[(size_t)B * N2 + i];
+    bA[fsw(i)] = Ya[(size_t)A * N2 + i];
+    if (two) bB[fsw(i)] = Ya[(size_t)B * N2 + i];
     if (a.mode == 2) {
-      cA[fpad(i)] = Yb[(size_t)A * N2 + i];
-      if (two) cB[fpad(i)] = Yb[(size_t)B * N2 + i];
+      cA[fsw(i)] = Yb[(size_t)A * N2 + i];
+      if (two) cB[fsw(i)] = Yb[(size_t)B * N2 + i];
     }
   }
   __syncthreads();
@@ -209,7 +209,7 @@ __global__ void __launch_bounds__(kThreads) large_row_pair(const double2* __rest
   double2* Fo = (a.mode == 0) ? a.spec_out + item * (size_t)(H + 1) : nullptr;
   for (int k2 = threadIdx.x; k2 < npairs; k2 += blockDim.x) {
     const int k2q = partner_k2(A, k2, N2);
-    const int pr = fpad(rev_index(s2, k2)), qr = fpad(rev_index(s2, k2q));
+    const int pr = fsw(rev_index(s2, k2)), qr = fsw(rev_index(s2, k2q));
     const long long p = (long long)A + (long long)N1 * k2;
     const long long q = (p == 0) ? H : H - p;
     const double2 W = twiddle(T, (int)p, H);  // exp(-2 pi i p / M), p < H
@@ -255,15 +255,15 @@ __global__ void __launch_bounds__(kThreads) large_row_pair(const double2* __rest
   fft_inverse(oA, s2, tw2, threadIdx.x, blockDim.x, CtaSync());
   if (two) fft_inverse(oB, s2, tw2, threadIdx.x, blockDim.x, CtaSync());
   for (int n2 = threadIdx.x; n2 < N2; n2 += blockDim.x) {
-    Yo[(size_t)A * N2 + n2] = cmulc(oA[fpad(n2)], twH(T, (long long)n2 * A, H));
-    if (two) Yo[(size_t)B * N2 + n2] = cmulc(oB[fpad(n2)], twH(T, (long long)n2 * B, H));
+    Yo[(size_t)A * N2 + n2] = cmulc(oA[fsw(n2)], twH(T, (long long)n2 * A, H));
+    if (two) Yo[(size_t)B * N2 + n2] = cmulc(oB[fsw(n2)], twH(T, (long long)n2 * B, H));
   }
 }
 
-size_t large_col_smem(int N1) { return ((size_t)kColW * fpad_size(N1) + tw2_entries(2 * N1)) * 16; }
+size_t large_col_smem(int N1) { return ((size_t)kColW * (N1 + 1) + tw2_entries(2 * N1)) * 16; }
 size_t large_row_smem(int N2, int mode) {
   (void)mode;  // the table sits after four rows in every mode
-  return ((size_t)4 * fpad_size(N2) + tw2_entries(2 * N2)) * 16;
+  return ((size_t)4 * fft_elems(N2) + tw2_entries(2 * N2)) * 16;
 }
 
 cudaError_t large_set_attributes(int N1, int N2) {

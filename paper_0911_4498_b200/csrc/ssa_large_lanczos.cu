@@ -100,7 +100,7 @@ __global__ void __launch_bounds__(kThreads) lg_dots(const double* __restrict__ b
     const double* br = basis + (size_t)row * ld + c0;
     double s = 0.0;
 #pragma unroll 8
-    for (int i = lane; i < len; i += 32) s = fma(__ldcs(br + i), rs[i], s);
+    for (int i = lane; i < len; i += 32) s = fma(__ldg(br + i), rs[i], s);  // lines stay in L2 for lg_update
     s = warp_sum(s);
     if (lane == 0) part[(size_t)row * nchunk + blockIdx.x] = s;
   }
@@ -118,30 +118,61 @@ __global__ void lg_rows(const double* __restrict__ part, int nb, int nchunk, dou
   if (lane == 0) h[w] = s;
 }
 
-// update: r -= sum_row h[row] basis[row] (rows in reverse), partial sums of squares
+// update: r -= sum_row h[row] basis[row] (rows in reverse: the rows lg_dots read last
+// are still in L2), partial sums of squares.  Each thread owns kLgChunk / kThreads
+// elements of the CTA's chunk; every step streams four rows (4 x 8 independent loads in
+// flight per thread) and applies them in the fixed reverse row order.
 __global__ void __launch_bounds__(kThreads) lg_update(const double* __restrict__ basis, int ld, int nb,
                                                       const double* __restrict__ h, double* r, double* part,
                                                       const LgScalars* sc, int pass) {
   if (pass == 1 && !sc->again) return;
   if (sc->stop) return;
+  constexpr int E = kLgChunk / kThreads;
   __shared__ double red[kWarps];
-  const int c0 = blockIdx.x * kLgChunk;
-  double ss = 0.0;
-  for (int i = threadIdx.x; i < kLgChunk; i += blockDim.x) {
-    const int t = c0 + i;
-    if (t >= ld) break;
-    double v = r[t];
-    for (int row = nb - 1; row >= 0; --row) v = fma(-h[row], __ldcs(basis + (size_t)row * ld + t), v);
-    r[t] = v;
-    ss = fma(v, v, ss);
+  extern __shared__ double hs[];  // nb coefficients
+  for (int i = threadIdx.x; i < nb; i += blockDim.x) hs[i] = h[i];
+  __syncthreads();
+  const int c0 = blockIdx.x * kLgChunk + threadIdx.x;
+  double v[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) v[e] = (c0 + e * kThreads < ld) ? r[c0 + e * kThreads] : 0.0;
+  const bool full = (blockIdx.x + 1) * kLgChunk <= ld;
+  int row = nb - 1;
+  if (full) {
+    for (; row >= 3; row -= 4) {
+      double b[4][E];
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+#pragma unroll
+        for (int e = 0; e < E; ++e) b[q][e] = __ldcs(basis + (size_t)(row - q) * ld + c0 + e * kThreads);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const double hr = hs[row - q];
+#pragma unroll
+        for (int e = 0; e < E; ++e) v[e] = fma(-hr, b[q][e], v[e]);
+      }
+    }
   }
+  for (; row >= 0; --row) {
+    const double hr = hs[row];
+#pragma unroll
+    for (int e = 0; e < E; ++e)
+      if (c0 + e * kThreads < ld) v[e] = fma(-hr, __ldcs(basis + (size_t)row * ld + c0 + e * kThreads), v[e]);
+  }
+  double ss = 0.0;
+#pragma unroll
+  for (int e = 0; e < E; ++e)
+    if (c0 + e * kThreads < ld) {
+      r[c0 + e * kThreads] = v[e];
+      ss = fma(v[e], v[e], ss);
+    }
   ss = warp_sum(ss);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
   __syncthreads();
   if (threadIdx.x == 0) {
-    double s = 0.0;
-    for (int i = 0; i < kWarps; ++i) s += red[i];
-    part[blockIdx.x] = s;
+    double t = 0.0;
+    for (int i = 0; i < kWarps; ++i) t += red[i];
+    part[blockIdx.x] = t;
   }
 }
 
@@ -360,7 +391,7 @@ cudaError_t large_decompose_one(Plan& p, const DecomposeArgs& a0, int b, cudaStr
     for (int pass = 0; pass < 2 && nb > 0; ++pass) {
       lg_dots<<<nch, kThreads, 0, s>>>(basis, ld, nb, r, part, nch, sc, pass);
       lg_rows<<<(nb * 32 + kThreads - 1) / kThreads, kThreads, 0, s>>>(part, nb, nch, h, sc, pass);
-      lg_update<<<nch, kThreads, 0, s>>>(basis, ld, nb, h, r, part, sc, pass);
+      lg_update<<<nch, kThreads, (size_t)(nb > 0 ? nb : 1) * 8, s>>>(basis, ld, nb, h, r, part, sc, pass);
       lg_after_pass<<<1, 32, 0, s>>>(part, nch, sc, pass, p.opt.reorth);
     }
   };

@@ -5,13 +5,14 @@ sys.path.insert(0, '.')
 import paper_0911_4498_b200 as P, ssa_inputs
 B = int(sys.argv[1]) if len(sys.argv) > 1 else 1024
 R = int(sys.argv[2]) if len(sys.argv) > 2 else 1
+CE = int(sys.argv[3]) if len(sys.argv) > 3 else 4
 c = ssa_inputs.CONFIGS["cfg2"]
 F = torch.from_numpy(ssa_inputs.cfg2_batch(0, B, c["N"])).cuda()
-plan = P.Plan(c["N"], c["L"], c["k"], B, profile=True, reorth=R)
+plan = P.Plan(c["N"], c["L"], c["k"], B, profile=True, reorth=R, check_every=CE)
 s, U, V, info = plan.decompose(F); torch.cuda.synchronize()
 t0 = time.time(); plan.decompose(F, s, U, V, info); torch.cuda.synchronize(); dt = time.time() - t0
 pr = plan.profile(); tot = sum(v for k, v in pr.items() if k != "n_checks")
-print("reorth=%d decompose %.1f ms for %d series; phase ms:" % (R, dt * 1e3, B), plan.phase_ms())
+print("check_every=%d reorth=%d decompose %.1f ms for %d series; phase ms:" % (CE, R, dt * 1e3, B), plan.phase_ms())
 for k, v in pr.items():
     print(f"  {k:10s} {v:16d}  {100*v/tot if k!='n_checks' else 0:5.1f}%")
 inf = P.info_to_numpy(info)
