@@ -39,17 +39,28 @@ __device__ __forceinline__ int block_or(int v, int* redi) {
 }
 
 // ------------------------------------------------------------------ FFT pair steps
+// Digit-reversed position of frequency k for a compile-time size 2^LOGH (rev_index).
+template <int LOGH>
+__device__ __forceinline__ int rev_t(int k) {
+  constexpr int N8 = LOGH / 3, LB = LOGH - 3 * N8;
+  int pos = 0;
+#pragma unroll
+  for (int p = 0; p < N8; ++p) pos += ((k >> (3 * p)) & 7) << (LOGH - 3 * (p + 1));
+  if constexpr (LB > 0) pos += (k >> (3 * N8)) & ((1 << LB) - 1);
+  return pos;
+}
+
 // Forward real post-processing for the pair (p, H-p) from digit-reversed Z:
 //   X_p = E + W^p O,  X_{H-p} = conj(E - W^p O),  E = (Z_p + conj Z_{H-p})/2,
-//   O = -i (Z_p - conj Z_{H-p})/2,  W = exp(-2 pi i / M).
-template <class TW>
-__device__ __forceinline__ void real_pair(const double2* buf, const FftShape& sh, const TW& tw, int p, double2& Xp,
-                                          double2& Xq, int& pr, int& qr) {
-  const int H = sh.H;
+//   O = -i (Z_p - conj Z_{H-p})/2,  W = exp(-2 pi i / M).  Returns W^p for inv_pair.
+template <int LOGH, class TW>
+__device__ __forceinline__ double2 real_pair(const double2* buf, const TW& tw, int p, double2& Xp, double2& Xq,
+                                             int& pr, int& qr) {
+  constexpr int H = 1 << LOGH;
   const int q = (H - p) & (H - 1);
-  pr = rev_index(sh, p);
-  qr = rev_index(sh, q);
-  double2 Zp = buf[fsw(pr)], Zq = buf[fsw(qr)];
+  pr = fsw(rev_t<LOGH>(p));
+  qr = fsw(rev_t<LOGH>(q));
+  double2 Zp = buf[pr], Zq = buf[qr];
   double2 W = tw(p);
   double2 E = make_double2(0.5 * (Zp.x + Zq.x), 0.5 * (Zp.y - Zq.y));
   double2 D = make_double2(0.5 * (Zp.x - Zq.x), 0.5 * (Zp.y + Zq.y));
@@ -57,43 +68,30 @@ __device__ __forceinline__ void real_pair(const double2* buf, const FftShape& sh
   double2 WO = cmul(W, O);
   Xp = cadd(E, WO);
   Xq = conjg(csub(E, WO));
+  return W;
 }
 
 // Inverse pre-processing: from half-spectrum values Y_p, Y_{H-p} of a real sequence
 // produce Z'_p = E + i O, Z'_{H-p} = conj(E) + i conj(O), E = (Y_p + conj Y_{H-p})/2,
 // O = (Y_p - conj Y_{H-p}) conj(W^p) / 2, whose inverse FFT is y_2n + i y_2n+1.
-template <class TW>
-__device__ __forceinline__ void inv_pair(double2* buf, const TW& tw, int p, int pr, int qr, double2 Yp, double2 Yq) {
-  double2 W = tw(p);
+// pr, qr: swizzled slots from real_pair.
+__device__ __forceinline__ void inv_pair(double2* buf, double2 W, int pr, int qr, double2 Yp, double2 Yq) {
   double2 E = make_double2(0.5 * (Yp.x + Yq.x), 0.5 * (Yp.y - Yq.y));
   double2 D = make_double2(0.5 * (Yp.x - Yq.x), 0.5 * (Yp.y + Yq.y));
   double2 O = cmulc(D, W);
-  buf[fsw(pr)] = make_double2(E.x - O.y, E.y + O.x);
-  if (qr != pr) buf[fsw(qr)] = make_double2(E.x + O.y, O.x - E.y);
-}
-
-// Correlation spectrum step: Z (digit-reversed FFT of packed x) -> Z' whose inverse is
-// the packed correlation y = irfft(F^ conj(X^)).
-template <class TW>
-__device__ __forceinline__ void corr_pairs(double2* buf, const FftShape& sh, const TW& T,
-                                           const double2* __restrict__ spec, int tid, int nthr) {
-  const int H = sh.H;
-  for (int p = tid; p <= (H >> 1); p += nthr) {
-    double2 Xp, Xq;
-    int pr, qr;
-    real_pair(buf, sh, T, p, Xp, Xq, pr, qr);
-    double2 Fp = __ldg(spec + p), Fq = __ldg(spec + (H - p));
-    inv_pair(buf, T, p, pr, qr, cmulc(Fp, Xp), cmulc(Fq, Xq));
-  }
+  buf[pr] = make_double2(E.x - O.y, E.y + O.x);
+  if (qr != pr) buf[qr] = make_double2(E.x + O.y, O.x - E.y);
 }
 
 // Full correlation in one CTA (all threads): y_t = sum_s f_{t+s} x_s, t < n_out
-// (the Hankel products of Alg. 2 / Alg. 3, in correlation form).
-template <class TW, class LoadX, class StoreY>
-__device__ __forceinline__ void correlate_cta(double2* buf, const FftShape& sh, const TW& T,
-                                              const double2* __restrict__ spec, int n_in, int n_out, LoadX loadx,
-                                              StoreY storey) {
-  const int H = sh.H, tid = threadIdx.x, nthr = blockDim.x;
+// (the Hankel products of Alg. 2 / Alg. 3, in correlation form):
+// packed forward FFT of x, pair step Z -> Z' whose inverse is the packed correlation
+// y = irfft(F^ conj(X^)), inverse FFT.
+template <int LOGH, class TW, class LoadX, class StoreY>
+__device__ __forceinline__ void correlate_t(double2* buf, const TW& T, const double2* __restrict__ spec, int n_in,
+                                            int n_out, LoadX loadx, StoreY storey) {
+  constexpr int H = 1 << LOGH;
+  const int tid = threadIdx.x, nthr = blockDim.x;
   // pull this thread's spectrum entries of the pair step towards L2 now (they are used
   // after the forward transform; from HBM their latency would stall that step)
   for (int p = tid; p <= (H >> 1); p += nthr) {
@@ -107,14 +105,36 @@ __device__ __forceinline__ void correlate_cta(double2* buf, const FftShape& sh, 
     buf[fsw(n)] = make_double2(a, b);
   }
   __syncthreads();
-  fft_forward(buf, sh, T, tid, nthr, CtaSync());
-  corr_pairs(buf, sh, T, spec, tid, nthr);
+  fft_run_t<LOGH, false>(buf, T, tid, nthr, CtaSync());
+  for (int p = tid; p <= (H >> 1); p += nthr) {
+    const double2 Fp = __ldg(spec + p), Fq = __ldg(spec + (H - p));
+    double2 Xp, Xq;
+    int pr, qr;
+    const double2 W = real_pair<LOGH>(buf, T, p, Xp, Xq, pr, qr);
+    inv_pair(buf, W, pr, qr, cmulc(Fp, Xp), cmulc(Fq, Xq));
+  }
   __syncthreads();
-  fft_inverse(buf, sh, T, tid, nthr, CtaSync());
+  fft_run_t<LOGH, true>(buf, T, tid, nthr, CtaSync());
   const double invH = 1.0 / (double)H;
   for (int t = tid; t < n_out; t += nthr) {
     double2 z = buf[fsw(t >> 1)];
     storey(t, ((t & 1) ? z.y : z.x) * invH);
+  }
+}
+
+// Runtime-size entry (H = 2^logH, 2 <= H <= 8192): one switch, then everything compiles
+// to constant shifts and offsets.
+template <class TW, class LoadX, class StoreY>
+__device__ __forceinline__ void correlate_cta(double2* buf, const FftShape& sh, const TW& T,
+                                              const double2* __restrict__ spec, int n_in, int n_out, LoadX loadx,
+                                              StoreY storey) {
+  switch (sh.logH) {
+#define SSA_CORR(L) \
+  case L: correlate_t<L>(buf, T, spec, n_in, n_out, loadx, storey); break;
+    SSA_CORR(1) SSA_CORR(2) SSA_CORR(3) SSA_CORR(4) SSA_CORR(5) SSA_CORR(6) SSA_CORR(7)
+    SSA_CORR(8) SSA_CORR(9) SSA_CORR(10) SSA_CORR(11) SSA_CORR(12)
+    default: correlate_t<13>(buf, T, spec, n_in, n_out, loadx, storey); break;
+#undef SSA_CORR
   }
 }
 

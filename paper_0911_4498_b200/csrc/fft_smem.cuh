@@ -177,41 +177,54 @@ __device__ __forceinline__ void dftR(double2* a) {
   else dft2<INV>(a[0], a[1]);
 }
 
-// One DIF pass (forward) or its inverse: block size S = 2^logS, radix R = 2^LR,
+// g(j) of the swizzle as a constant expression (for compile-time offsets)
+__host__ __device__ constexpr int gsw(int j) { return (j ^ (j >> 3) ^ (j >> 6) ^ (j >> 9) ^ (j >> 12)) & 7; }
+
+// One DIF pass (forward) or its inverse: block size S = 2^LOGS, radix R = 2^LR,
 // Q = S / R.  Butterfly (b, n1):
 //   forward: y[n1 + Q k2] = W_S^{n1 k2} * sum_{n2} x[n1 + Q n2] W_R^{n2 k2}
 //   inverse: x[n1 + Q n2] = sum_{k2} W_R^{-n2 k2} W_S^{-n1 k2} y[n1 + Q k2]   (times R)
-template <int LR, bool INV, class TW>
-__device__ __forceinline__ void fft_pass(double2* buf, int H, int logH, int logS, const TW& tw, int tid, int nthr) {
-  constexpr int R = 1 << LR;
-  const int logQ = logS - LR;
-  const int Q = 1 << logQ;
+// Addresses: for Q >= 8 the rows of the R elements differ by q Q / 8 in bits the row
+// of `base` leaves zero, so fsw(base + q Q) = (fsw(base) + q Q) ^ gsw(q Q / 8): one
+// swizzle per butterfly plus a constant XOR per element.
+template <int LOGH, int LOGS, int LR, bool INV, class TW>
+__device__ __forceinline__ void fft_pass_t(double2* buf, const TW& tw, int tid, int nthr) {
+  constexpr int R = 1 << LR, LOGQ = LOGS - LR, Q = 1 << LOGQ, H = 1 << LOGH;
   for (int bf = tid; bf < (H >> LR); bf += nthr) {
-    const int b = bf >> logQ, n1 = bf & (Q - 1);
-    const int base = (b << logS) + n1;
+    const int b = bf >> LOGQ, n1 = bf & (Q - 1);
+    const int base = (b << LOGS) + n1;
+    int idx[R];
+    if constexpr (Q >= 8) {
+      const int pb = fsw(base);
+#pragma unroll
+      for (int q = 0; q < R; ++q) idx[q] = (pb + (q << LOGQ)) ^ gsw((q << LOGQ) >> 3);
+    } else {
+#pragma unroll
+      for (int q = 0; q < R; ++q) idx[q] = fsw(base + (q << LOGQ));
+    }
     double2 a[R];
 #pragma unroll
-    for (int q = 0; q < R; ++q) a[q] = buf[fsw(base + (q << logQ))];
+    for (int q = 0; q < R; ++q) a[q] = buf[idx[q]];
     double2 w[R];
-    if (Q > 1) {
+    if constexpr (Q > 1) {
       // w_q = W_S^{n1 q} = (W_S^{n1})^q: one per-pass table lookup, powers by products
-      w[1] = tw.pass_w(logH, logS, n1);
+      w[1] = tw.pass_w(LOGH, LOGS, n1);
       if constexpr (R >= 4) { w[2] = cmul(w[1], w[1]); w[3] = cmul(w[2], w[1]); }
       if constexpr (R == 8) {
         w[4] = cmul(w[2], w[2]); w[5] = cmul(w[4], w[1]); w[6] = cmul(w[4], w[2]); w[7] = cmul(w[4], w[3]);
       }
-    }
-    if (INV && Q > 1) {
+      if constexpr (INV) {
 #pragma unroll
-      for (int q = 1; q < R; ++q) a[q] = cmulc(a[q], w[q]);
+        for (int q = 1; q < R; ++q) a[q] = cmulc(a[q], w[q]);
+      }
     }
     dftR<R, INV>(a);
-    if (!INV && Q > 1) {
+    if constexpr (!INV && Q > 1) {
 #pragma unroll
       for (int q = 1; q < R; ++q) a[q] = cmul(a[q], w[q]);
     }
 #pragma unroll
-    for (int q = 0; q < R; ++q) buf[fsw(base + (q << logQ))] = a[q];
+    for (int q = 0; q < R; ++q) buf[idx[q]] = a[q];
   }
 }
 
@@ -222,25 +235,33 @@ struct CtaSync {
 // Forward FFT of H points in place (natural -> digit-reversed).  Caller must have
 // synchronized after writing buf; returns after a final barrier.
 // Whole transform with a compile-time size (all index arithmetic folds to constants).
+template <int LOGH, int P, bool INV, class TW, class Sync>
+__device__ __forceinline__ void fft_radix8_passes(double2* buf, const TW& T, int tid, int nthr, Sync sync) {
+  // passes P..N8-1 forward (INV: N8-1..P, called with P counting down from the top)
+  if constexpr (P >= 0 && P < LOGH / 3) {
+    if constexpr (!INV) {
+      fft_pass_t<LOGH, LOGH - 3 * P, 3, false>(buf, T, tid, nthr);
+      sync();
+      fft_radix8_passes<LOGH, P + 1, false>(buf, T, tid, nthr, sync);
+    } else {
+      fft_pass_t<LOGH, LOGH - 3 * P, 3, true>(buf, T, tid, nthr);
+      sync();
+      fft_radix8_passes<LOGH, P - 1, true>(buf, T, tid, nthr, sync);
+    }
+  }
+}
+
 template <int LOGH, bool INV, class TW, class Sync>
 __device__ __forceinline__ void fft_run_t(double2* buf, const TW& T, int tid, int nthr, Sync sync) {
-  constexpr int N8 = LOGH / 3, LB = LOGH - 3 * N8, H = 1 << LOGH;
+  constexpr int N8 = LOGH / 3, LB = LOGH - 3 * N8;
   if constexpr (!INV) {
-#pragma unroll
-    for (int p = 0; p < N8; ++p) {
-      fft_pass<3, false>(buf, H, LOGH, LOGH - 3 * p, T, tid, nthr);
-      sync();
-    }
-    if constexpr (LB == 2) { fft_pass<2, false>(buf, H, LOGH, LB, T, tid, nthr); sync(); }
-    if constexpr (LB == 1) { fft_pass<1, false>(buf, H, LOGH, LB, T, tid, nthr); sync(); }
+    fft_radix8_passes<LOGH, 0, false>(buf, T, tid, nthr, sync);
+    if constexpr (LB == 2) { fft_pass_t<LOGH, 2, 2, false>(buf, T, tid, nthr); sync(); }
+    if constexpr (LB == 1) { fft_pass_t<LOGH, 1, 1, false>(buf, T, tid, nthr); sync(); }
   } else {
-    if constexpr (LB == 2) { fft_pass<2, true>(buf, H, LOGH, LB, T, tid, nthr); sync(); }
-    if constexpr (LB == 1) { fft_pass<1, true>(buf, H, LOGH, LB, T, tid, nthr); sync(); }
-#pragma unroll
-    for (int p = N8 - 1; p >= 0; --p) {
-      fft_pass<3, true>(buf, H, LOGH, LOGH - 3 * p, T, tid, nthr);
-      sync();
-    }
+    if constexpr (LB == 2) { fft_pass_t<LOGH, 2, 2, true>(buf, T, tid, nthr); sync(); }
+    if constexpr (LB == 1) { fft_pass_t<LOGH, 1, 1, true>(buf, T, tid, nthr); sync(); }
+    fft_radix8_passes<LOGH, N8 - 1, true>(buf, T, tid, nthr, sync);
   }
 }
 

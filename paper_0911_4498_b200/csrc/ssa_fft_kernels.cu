@@ -13,6 +13,35 @@
 
 namespace ssa {
 
+template <int LOGH>
+__device__ __forceinline__ void spectrum_body(double2* buf, const TwSmem& tw, const double* __restrict__ f, int N,
+                                              double2* __restrict__ out) {
+  constexpr int H = 1 << LOGH;
+  for (int n = threadIdx.x; n < H; n += blockDim.x) {
+    int i0 = 2 * n;
+    double a = (i0 < N) ? f[i0] : 0.0;
+    double c = (i0 + 1 < N) ? f[i0 + 1] : 0.0;
+    buf[fsw(n)] = make_double2(a, c);
+  }
+  __syncthreads();
+  fft_run_t<LOGH, false>(buf, tw, threadIdx.x, blockDim.x, CtaSync());
+  for (int p = threadIdx.x; p <= (H >> 1); p += blockDim.x) {
+    double2 Xp, Xq;
+    int pr, qr;
+    real_pair<LOGH>(buf, tw, p, Xp, Xq, pr, qr);
+    out[p] = Xp;
+    out[H - p] = Xq;
+  }
+}
+
+#define SSA_DISPATCH_LOGH(logH, CALL)                                                                   \
+  switch (logH) {                                                                                       \
+    case 1: CALL(1); break; case 2: CALL(2); break; case 3: CALL(3); break; case 4: CALL(4); break;     \
+    case 5: CALL(5); break; case 6: CALL(6); break; case 7: CALL(7); break; case 8: CALL(8); break;     \
+    case 9: CALL(9); break; case 10: CALL(10); break; case 11: CALL(11); break; case 12: CALL(12); break; \
+    default: CALL(13); break;                                                                           \
+  }
+
 __global__ void __launch_bounds__(kThreads) spectrum_kernel(const double* __restrict__ series, int N, int H,
                                                             const double2* __restrict__ T, double2* __restrict__ spec) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -22,21 +51,9 @@ __global__ void __launch_bounds__(kThreads) spectrum_kernel(const double* __rest
   const int b = blockIdx.x;
   const double* f = series + (size_t)b * N;
   double2* out = spec + (size_t)b * (H + 1);
-  for (int n = threadIdx.x; n < H; n += blockDim.x) {
-    int i0 = 2 * n;
-    double a = (i0 < N) ? f[i0] : 0.0;
-    double c = (i0 + 1 < N) ? f[i0 + 1] : 0.0;
-    buf[fsw(n)] = make_double2(a, c);
-  }
-  __syncthreads();
-  fft_forward(buf, sh, tw, threadIdx.x, blockDim.x, CtaSync());
-  for (int p = threadIdx.x; p <= (H >> 1); p += blockDim.x) {
-    double2 Xp, Xq;
-    int pr, qr;
-    real_pair(buf, sh, tw, p, Xp, Xq, pr, qr);
-    out[p] = Xp;
-    out[H - p] = Xq;
-  }
+#define SSA_SPEC(L) spectrum_body<L>(buf, tw, f, N, out)
+  SSA_DISPATCH_LOGH(sh.logH, SSA_SPEC)
+#undef SSA_SPEC
 }
 
 __global__ void __launch_bounds__(kThreads) matvec_kernel(const double2* __restrict__ spec, int H, int n_in, int n_out,
@@ -59,18 +76,12 @@ __global__ void __launch_bounds__(kThreads) matvec_kernel(const double2* __restr
 // Two shared-memory buffers when they fit (H <= kMaxHankelSmemH); otherwise (BIG) the
 // post-processed spectrum of u goes to a per-CTA global scratch row (L2-resident) and the
 // grid is persistent over terms.
-template <bool BIG>
-__global__ void __launch_bounds__(kThreads) hankelize_kernel(const double* __restrict__ sigma,
-                                                             const double* __restrict__ U,
-                                                             const double* __restrict__ V, size_t nterm_total, int N,
-                                                             int L, int K, int H, const double2* __restrict__ T,
-                                                             double* __restrict__ out, double2* gscratch) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  double2* bufB = reinterpret_cast<double2*>(smem_raw);
-  double2* bufA = BIG ? nullptr : bufB + fft_elems(H);
-  const TwSmem tw = load_tw2(T, bufB + (BIG ? 1 : 2) * fft_elems(H), 2 * H);
-  double2* Xu = BIG ? gscratch + (size_t)blockIdx.x * (H + 1) : nullptr;
-  const FftShape sh = make_shape(H);
+template <int LOGH, bool BIG>
+__device__ __forceinline__ void hankelize_body(double2* bufA, double2* bufB, const TwSmem& tw,
+                                               const double* __restrict__ sigma, const double* __restrict__ U,
+                                               const double* __restrict__ V, size_t nterm_total, int N, int L, int K,
+                                               double* __restrict__ out, double2* Xu) {
+  constexpr int H = 1 << LOGH;
   const int mn = L < K ? L : K;
   for (size_t term = blockIdx.x; term < nterm_total; term += gridDim.x) {
     const double* u = U + term * L;
@@ -83,11 +94,11 @@ __global__ void __launch_bounds__(kThreads) hankelize_kernel(const double* __res
         bufB[fsw(n)] = make_double2(i0 < L ? __ldg(u + i0) : 0.0, i0 + 1 < L ? __ldg(u + i0 + 1) : 0.0);
       }
       __syncthreads();
-      fft_forward(bufB, sh, tw, threadIdx.x, blockDim.x, CtaSync());
+      fft_run_t<LOGH, false>(bufB, tw, threadIdx.x, blockDim.x, CtaSync());
       for (int p = threadIdx.x; p <= (H >> 1); p += blockDim.x) {
         double2 Up, Uq;
         int pr, qr;
-        real_pair(bufB, sh, tw, p, Up, Uq, pr, qr);
+        real_pair<LOGH>(bufB, tw, p, Up, Uq, pr, qr);
         Xu[p] = Up;
         Xu[H - p] = Uq;
       }
@@ -97,12 +108,12 @@ __global__ void __launch_bounds__(kThreads) hankelize_kernel(const double* __res
         bufB[fsw(n)] = make_double2(i0 < K ? __ldg(v + i0) : 0.0, i0 + 1 < K ? __ldg(v + i0 + 1) : 0.0);
       }
       __syncthreads();
-      fft_forward(bufB, sh, tw, threadIdx.x, blockDim.x, CtaSync());
+      fft_run_t<LOGH, false>(bufB, tw, threadIdx.x, blockDim.x, CtaSync());
       for (int p = threadIdx.x; p <= (H >> 1); p += blockDim.x) {
         double2 Vp, Vq;
         int pr, qr;
-        real_pair(bufB, sh, tw, p, Vp, Vq, pr, qr);
-        inv_pair(bufB, tw, p, pr, qr, cmul(Xu[p], Vp), cmul(Xu[H - p], Vq));
+        const double2 W = real_pair<LOGH>(bufB, tw, p, Vp, Vq, pr, qr);
+        inv_pair(bufB, W, pr, qr, cmul(Xu[p], Vp), cmul(Xu[H - p], Vq));
       }
     } else {
       __syncthreads();
@@ -112,18 +123,18 @@ __global__ void __launch_bounds__(kThreads) hankelize_kernel(const double* __res
         bufB[fsw(n)] = make_double2(i0 < K ? __ldg(v + i0) : 0.0, i0 + 1 < K ? __ldg(v + i0 + 1) : 0.0);
       }
       __syncthreads();
-      fft_forward(bufA, sh, tw, threadIdx.x, blockDim.x, CtaSync());
-      fft_forward(bufB, sh, tw, threadIdx.x, blockDim.x, CtaSync());
+      fft_run_t<LOGH, false>(bufA, tw, threadIdx.x, blockDim.x, CtaSync());
+      fft_run_t<LOGH, false>(bufB, tw, threadIdx.x, blockDim.x, CtaSync());
       for (int p = threadIdx.x; p <= (H >> 1); p += blockDim.x) {
         double2 Up, Uq, Vp, Vq;
         int pr, qr;
-        real_pair(bufA, sh, tw, p, Up, Uq, pr, qr);
-        real_pair(bufB, sh, tw, p, Vp, Vq, pr, qr);
-        inv_pair(bufB, tw, p, pr, qr, cmul(Up, Vp), cmul(Uq, Vq));
+        real_pair<LOGH>(bufA, tw, p, Up, Uq, pr, qr);
+        const double2 W = real_pair<LOGH>(bufB, tw, p, Vp, Vq, pr, qr);
+        inv_pair(bufB, W, pr, qr, cmul(Up, Vp), cmul(Uq, Vq));
       }
     }
     __syncthreads();
-    fft_inverse(bufB, sh, tw, threadIdx.x, blockDim.x, CtaSync());
+    fft_run_t<LOGH, true>(bufB, tw, threadIdx.x, blockDim.x, CtaSync());
     const double scale = sg / (double)H;
     double* g = out + term * N;
     for (int t = threadIdx.x; t < N; t += blockDim.x) {
@@ -135,6 +146,23 @@ __global__ void __launch_bounds__(kThreads) hankelize_kernel(const double* __res
       g[t] = ((t & 1) ? z.y : z.x) * scale / (double)c;
     }
   }
+}
+
+template <bool BIG>
+__global__ void __launch_bounds__(kThreads) hankelize_kernel(const double* __restrict__ sigma,
+                                                             const double* __restrict__ U,
+                                                             const double* __restrict__ V, size_t nterm_total, int N,
+                                                             int L, int K, int H, const double2* __restrict__ T,
+                                                             double* __restrict__ out, double2* gscratch) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double2* bufB = reinterpret_cast<double2*>(smem_raw);
+  double2* bufA = BIG ? nullptr : bufB + fft_elems(H);
+  const TwSmem tw = load_tw2(T, bufB + (BIG ? 1 : 2) * fft_elems(H), 2 * H);
+  double2* Xu = BIG ? gscratch + (size_t)blockIdx.x * (H + 1) : nullptr;
+  const FftShape sh = make_shape(H);
+#define SSA_HANK(LG) hankelize_body<LG, BIG>(bufA, bufB, tw, sigma, U, V, nterm_total, N, L, K, out, Xu)
+  SSA_DISPATCH_LOGH(sh.logH, SSA_HANK)
+#undef SSA_HANK
 }
 
 static size_t tw_smem(int H) { return (size_t)tw2_entries(2 * H) * 16; }

@@ -16,6 +16,8 @@
 //                   epilogue (correlation output / Hankelization weights 1/c_t).
 // The work buffers are [items][H] complex in global memory; for one item they are
 // 8 MB (cfg3) or 2 MB (cfg5), so the three passes run out of L2.
+#include <stdlib.h>
+
 #include <algorithm>
 
 #include "device_common.cuh"
@@ -339,7 +341,11 @@ cudaError_t large_correlate(const Plan& p, const double2* spec, size_t spec_stri
 cudaError_t large_hankelize(const Plan& p, const double* sigma, const double* U, const double* V, size_t nterm_total,
                             double* out, cudaStream_t s) {
   const LargeGeom g = geom(p);
-  const int per = std::max(1, p.lbuf_items / 2);  // terms per batch: two buffers each
+  // terms per batch (two H-point buffers each): few enough that both buffers of every
+  // term in flight stay in L2 between the passes (8 x 2 x 2 MB at cfg5), many enough to
+  // fill the GPU (column passes: N2/8 x per CTAs)
+  int per = std::max(1, std::min(p.lbuf_items / 2, (int)std::max<int64_t>(1, (int64_t)(32 << 20) / (2 * (int64_t)g.H * 16))));
+  if (const char* e = getenv("SSA_HANK_PER")) per = std::max(1, std::min(p.lbuf_items / 2, atoi(e)));
   double2* Ya = p.d_lbuf;
   double2* Yb = p.d_lbuf + (size_t)per * g.H;
   for (size_t t0 = 0; t0 < nterm_total; t0 += per) {
