@@ -246,7 +246,7 @@ def measured_peaks():
 
 def ncu_traffic(name: str):
     """dram read+write bytes per launch of `name` from the committed ncu summary."""
-    for p in sorted(glob.glob(os.path.join(ROOT, "profiles", "*ncu_summary*.json")), reverse=True):
+    for p in sorted(glob.glob(os.path.join(ROOT, "profiles", "ncu_*cfg2_summary*.json")), reverse=True):
         try:
             d = json.load(open(p))
             if name in d and d[name].get("dram_bytes_per_launch"):

@@ -181,6 +181,11 @@ __device__ __forceinline__ uint64_t policy_evict_last() {
   asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
 __device__ __forceinline__ uint64_t policy_evict_first() {
   uint64_t p;
   asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
@@ -231,18 +236,27 @@ __device__ __forceinline__ void stream_rows(const double* base_w, int ld, int nb
       else tma_load_1d(rg.buf + (size_t)st * slab, base_w + (size_t)row * ld, bytes, rg.bar + st);
     }
   }
+  // refills are issued by lane 0 under a predicate (no divergent branch per row)
+  const uint64_t pol = policy ? policy : policy_evict_normal();
   for (int q = 0; q < nb; ++q) {
     const uint32_t c = c0 + q;
     const int st = (int)(c % kStages);
     mbar_wait(rg.bar + st, (c / kStages) & 1u);
     f(reverse ? nb - 1 - q : q, rg.buf + (size_t)st * slab);
     __syncwarp();
-    if (lane == 0 && q + kStages < nb) {
-      int row = reverse ? nb - 1 - (q + kStages) : q + kStages;
-      mbar_expect_tx(rg.bar + st, bytes);
-      if (policy) tma_load_1d_hint(rg.buf + (size_t)st * slab, base_w + (size_t)row * ld, bytes, rg.bar + st, policy);
-      else tma_load_1d(rg.buf + (size_t)st * slab, base_w + (size_t)row * ld, bytes, rg.bar + st);
-    }
+    const int qn = q + kStages;
+    const int row = reverse ? nb - 1 - qn : qn;
+    const uint32_t issue = (lane == 0 && qn < nb) ? 1u : 0u;
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %0, 0;\n"
+        "@p mbarrier.arrive.expect_tx.shared::cta.b64 _, [%1], %2;\n"
+        "@p cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%3], [%4], %2, [%1], %5;\n"
+        "}\n" ::"r"(issue),
+        "r"(smem_u32(rg.bar + st)), "r"(bytes), "r"(smem_u32(rg.buf + (size_t)st * slab)),
+        "l"(base_w + (size_t)(issue ? row : 0) * ld), "l"(pol)
+        : "memory");
   }
   rg.cnt = c0 + nb;
 }

@@ -104,6 +104,12 @@ static void free_plan(Plan& p) {
     if (q) cudaFree(q);
   for (int i = 0; i < 2 * Plan::kPhases; ++i)
     if (p.ev[i]) cudaEventDestroy(p.ev[i]);
+  for (int i = 0; i < 2; ++i)
+    if (p.sub[i]) ssa_plan_destroy(reinterpret_cast<ssa_plan_t>(p.sub[i]));
+  for (int i = 0; i < 3; ++i)
+    if (p.hs[i]) cudaStreamDestroy(p.hs[i]);
+  for (int i = 0; i < Plan::kMaxSlices + 2; ++i)
+    if (p.hev[i]) cudaEventDestroy(p.hev[i]);
 }
 
 static ssa_status alloc(void** ptr, size_t bytes, const char* what) {
@@ -397,7 +403,7 @@ extern "C" ssa_status ssa_decompose(ssa_plan_t plan, const double* d_series, dou
   a.N = (int)p.N; a.L = (int)p.L; a.K = (int)p.K; a.M = (int)p.M; a.H = (int)p.H; a.k = p.k;
   a.m_max = p.m_max; a.ldL = p.ldL; a.ldK = p.ldK;
   a.check_every = p.opt.check_every; a.reorth_mode = p.opt.reorth;
-  a.tol = p.opt.tol; a.seed = p.opt.seed;
+  a.tol = p.opt.tol; a.seed = p.opt.seed; a.series_base = p.series_base;
   a.series = d_series; a.spec = p.d_spec; a.tw = p.d_twl;
   a.U = p.d_U; a.V = p.d_V; a.ab = p.d_ab; a.state = p.d_state;
   a.tgk = p.d_tgk; a.tgk_stride = (size_t)2 * p.k * (2 * p.m_max + 2);
@@ -461,12 +467,73 @@ extern "C" ssa_status ssa_run_host(ssa_plan_t plan, const double* h_series, doub
   }
   cudaStream_t s = S(stream);
   CK(cudaMemcpyAsync(p.d_series, h_series, B * p.N * 8, cudaMemcpyHostToDevice, s), "H2D series");
-  if ((st = ssa_decompose(plan, p.d_series, p.d_sigma, p.d_Uout, p.d_Vout, p.d_info, stream)) != SSA_OK) return st;
-  if ((st = ssa_reconstruct(plan, p.d_sigma, p.d_Uout, p.d_Vout, p.d_recon, stream)) != SSA_OK) return st;
-  if (h_sigma) CK(cudaMemcpyAsync(h_sigma, p.d_sigma, B * k * 8, cudaMemcpyDeviceToHost, s), "D2H sigma");
-  if (h_U) CK(cudaMemcpyAsync(h_U, p.d_Uout, B * k * p.L * 8, cudaMemcpyDeviceToHost, s), "D2H U");
-  if (h_V) CK(cudaMemcpyAsync(h_V, p.d_Vout, B * k * p.K * 8, cudaMemcpyDeviceToHost, s), "D2H V");
-  if (h_recon) CK(cudaMemcpyAsync(h_recon, p.d_recon, B * k * p.N * 8, cudaMemcpyDeviceToHost, s), "D2H recon");
+  // Pipelined path: the batch in slices; slice i is decomposed + reconstructed by sub-plan
+  // i % 2 on compute stream i % 2 (so one slice's kernel tail overlaps the next slice's
+  // start) while the copy stream brings finished slices back -- the device-to-host copy of
+  // the outputs (32 x the input bytes at cfg2) hides behind the compute of later slices.
+  int nsl = 1;
+  if (!p.large && B >= 512) nsl = 4;
+  if (const char* e = getenv("SSA_HOST_SLICES")) nsl = std::max(1, std::min(Plan::kMaxSlices, atoi(e)));
+  if (nsl > 1 && (int64_t)B >= 2 * nsl) {
+    const int64_t sb = ((int64_t)B + nsl - 1) / nsl;
+    if (p.sub_batch != sb) {
+      for (int i = 0; i < 2; ++i)
+        if (p.sub[i]) { ssa_plan_destroy(reinterpret_cast<ssa_plan_t>(p.sub[i])); p.sub[i] = nullptr; }
+      for (int i = 0; i < 2; ++i) {
+        ssa_plan_t q = nullptr;
+        if ((st = ssa_plan_create(p.N, p.L, p.k, sb, &p.opt, p.device, &q)) != SSA_OK) return st;
+        p.sub[i] = q;
+      }
+      p.sub_batch = sb;
+    }
+    for (int i = 0; i < 3; ++i)
+      if (!p.hs[i]) CK(cudaStreamCreateWithFlags(&p.hs[i], cudaStreamNonBlocking), "cudaStreamCreate");
+    for (int i = 0; i < Plan::kMaxSlices + 2; ++i)
+      if (!p.hev[i]) CK(cudaEventCreateWithFlags(&p.hev[i], cudaEventDisableTiming), "cudaEventCreate");
+    cudaEvent_t ev_in = p.hev[Plan::kMaxSlices], ev_cp = p.hev[Plan::kMaxSlices + 1];
+    CK(cudaEventRecord(ev_in, s), "event record");
+    for (int c = 0; c < 2; ++c) CK(cudaStreamWaitEvent(p.hs[c], ev_in, 0), "stream wait");
+    CK(cudaStreamWaitEvent(p.hs[2], ev_in, 0), "stream wait");
+    for (int i = 0; i < nsl; ++i) {
+      const size_t b0 = (size_t)i * sb;
+      if (b0 >= B) break;
+      const size_t nb = std::min<size_t>(sb, B - b0);
+      Plan& q = reinterpret_cast<ssa_plan_t>(p.sub[i & 1])->p;
+      cudaStream_t cs = p.hs[i & 1];
+      // the sub-plan runs a full slice of sb series; the last slice may be shorter: it
+      // then re-runs the tail of the batch (results of the overlap are written twice,
+      // identically)
+      const size_t s0 = (nb == (size_t)sb) ? b0 : B - sb;
+      q.series_base = (int64_t)s0;  // same start vectors as the single-launch path
+      if ((st = ssa_decompose(reinterpret_cast<ssa_plan_t>(p.sub[i & 1]), p.d_series + s0 * p.N, p.d_sigma + s0 * k,
+                              p.d_Uout + s0 * k * p.L, p.d_Vout + s0 * k * p.K, p.d_info + s0, cs)) != SSA_OK)
+        return st;
+      if ((st = ssa_reconstruct(reinterpret_cast<ssa_plan_t>(p.sub[i & 1]), p.d_sigma + s0 * k,
+                                p.d_Uout + s0 * k * p.L, p.d_Vout + s0 * k * p.K, p.d_recon + s0 * k * p.N, cs)) !=
+          SSA_OK)
+        return st;
+      p.launches += q.launches;  // launch accounting of the caller's plan
+      q.launches = 0;
+      CK(cudaEventRecord(p.hev[i], cs), "event record");
+      cudaStream_t ct = p.hs[2];
+      CK(cudaStreamWaitEvent(ct, p.hev[i], 0), "stream wait");
+      if (h_sigma) CK(cudaMemcpyAsync(h_sigma + b0 * k, p.d_sigma + b0 * k, nb * k * 8, cudaMemcpyDeviceToHost, ct), "D2H sigma");
+      if (h_U) CK(cudaMemcpyAsync(h_U + b0 * k * p.L, p.d_Uout + b0 * k * p.L, nb * k * p.L * 8, cudaMemcpyDeviceToHost, ct), "D2H U");
+      if (h_V) CK(cudaMemcpyAsync(h_V + b0 * k * p.K, p.d_Vout + b0 * k * p.K, nb * k * p.K * 8, cudaMemcpyDeviceToHost, ct), "D2H V");
+      if (h_recon)
+        CK(cudaMemcpyAsync(h_recon + b0 * k * p.N, p.d_recon + b0 * k * p.N, nb * k * p.N * 8, cudaMemcpyDeviceToHost, ct),
+           "D2H recon");
+    }
+    CK(cudaEventRecord(ev_cp, p.hs[2]), "event record");
+    CK(cudaStreamWaitEvent(s, ev_cp, 0), "stream wait");
+  } else {
+    if ((st = ssa_decompose(plan, p.d_series, p.d_sigma, p.d_Uout, p.d_Vout, p.d_info, stream)) != SSA_OK) return st;
+    if ((st = ssa_reconstruct(plan, p.d_sigma, p.d_Uout, p.d_Vout, p.d_recon, stream)) != SSA_OK) return st;
+    if (h_sigma) CK(cudaMemcpyAsync(h_sigma, p.d_sigma, B * k * 8, cudaMemcpyDeviceToHost, s), "D2H sigma");
+    if (h_U) CK(cudaMemcpyAsync(h_U, p.d_Uout, B * k * p.L * 8, cudaMemcpyDeviceToHost, s), "D2H U");
+    if (h_V) CK(cudaMemcpyAsync(h_V, p.d_Vout, B * k * p.K * 8, cudaMemcpyDeviceToHost, s), "D2H V");
+    if (h_recon) CK(cudaMemcpyAsync(h_recon, p.d_recon, B * k * p.N * 8, cudaMemcpyDeviceToHost, s), "D2H recon");
+  }
   std::vector<ssa_series_info> info(B);
   CK(cudaMemcpyAsync(info.data(), p.d_info, B * sizeof(ssa_series_info), cudaMemcpyDeviceToHost, s), "D2H info");
   CK(cudaStreamSynchronize(s), "stream sync");

@@ -25,6 +25,7 @@ struct DecomposeArgs {
   int b0, nb;
   double tol;
   uint64_t seed;
+  int64_t series_base;   // global index of series 0 of the call (seeds are per global index)
   const double* series;  // caller [batch][N]
   const double2* spec;   // [nb][H+1]
   const double2* tw;     // two-level twiddle table for M
@@ -99,6 +100,14 @@ struct Plan {
   double* d_Uout = nullptr;
   double* d_Vout = nullptr;
   double* d_recon = nullptr;
+  // host-API pipelining (ssa_run_host): two sub-plans of one slice each, alternating on two
+  // compute streams, device-to-host copies of finished slices on a third stream
+  void* sub[2] = {nullptr, nullptr};  // ssa_plan_t
+  int64_t sub_batch = 0;
+  int64_t series_base = 0;  // sub-plans: global index of their current slice's first series
+  cudaStream_t hs[3] = {};
+  static constexpr int kMaxSlices = 16;
+  cudaEvent_t hev[kMaxSlices + 2] = {};
   int64_t launches = 0;
   static constexpr int kPhases = 5;  // spectrum, lanczos, bidiag_svd, ritz, hankelize
   cudaEvent_t ev[2 * kPhases] = {};

@@ -257,7 +257,7 @@ __global__ void __launch_bounds__(kThreads, 2) lanczos_kernel(const DecomposeArg
     // ---- Alg. 1 lines 1-2: p0 seeded, beta_1 = |p0|, u_1 = p0 / beta_1, v_0 = 0 ----
     double ss = 0.0;
     for (int t = tid; t < a.ldL; t += blockDim.x) {
-      double v = (t < L) ? rng_uniform_pm1(a.seed, (uint64_t)b, (uint64_t)t) : 0.0;
+      double v = (t < L) ? rng_uniform_pm1(a.seed, (uint64_t)(b + a.series_base), (uint64_t)t) : 0.0;
       sm.bufU[t] = v;
       ss += v * v;
     }
@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(kThreads, 2) lanczos_kernel(const DecomposeArg
       double al = reorth(sm.bufV, V, j - 1, a.ldK, nr, a.reorth_mode, sm, rg, part, pstride, extra);
       if (!(al > 1e-12 * runmax) || al == 0.0) {
         if (!breakdown) breakdown = j;
-        double q = (j - 1 < K) ? restart_vector(sm.bufV, K, a.ldK, V, j - 1, a.seed, (uint64_t)b,
+        double q = (j - 1 < K) ? restart_vector(sm.bufV, K, a.ldK, V, j - 1, a.seed, (uint64_t)(b + a.series_base),
                                                 ((uint64_t)(++restarts) << 40), sm, rg, part, pstride)
                                : 0.0;
         if (q > 1e-8) {
@@ -373,7 +373,7 @@ __global__ void __launch_bounds__(kThreads, 2) lanczos_kernel(const DecomposeArg
       double be = reorth(sm.bufU, U, j, a.ldL, nr, a.reorth_mode, sm, rg, part, pstride, extra);
       if (!(be > 1e-12 * runmax) || be == 0.0) {
         if (!breakdown) breakdown = j;
-        double q = (j < L) ? restart_vector(sm.bufU, L, a.ldL, U, j, a.seed, (uint64_t)b,
+        double q = (j < L) ? restart_vector(sm.bufU, L, a.ldL, U, j, a.seed, (uint64_t)(b + a.series_base),
                                             ((uint64_t)(++restarts) << 40), sm, rg, part, pstride)
                            : 0.0;
         if (q > 1e-8) {

@@ -172,100 +172,103 @@ __device__ __forceinline__ int partner_k2(int A, int k2, int N2) {
   return (A == 0) ? ((N2 - k2) & (N2 - 1)) : (N2 - 1 - k2);
 }
 
+// Row pairs with warp-level FFTs: each CTA takes G = warps / R row pairs (R = rows per
+// pair: 2, or 4 in mode 2; G from the launch: 1 when one item must fill the GPU), warp g R + j loads and transforms row j of pair g on its own
+// (no CTA barrier inside the FFTs), the pair step runs on the 32 R threads of the pair,
+// and warps 0 / 1 of the pair run the inverse transforms of rows A / B and write them
+// back with the conjugate twiddle.
 __global__ void __launch_bounds__(kThreads) large_row_pair(const double2* __restrict__ T, const double2* __restrict__ T2,
                                                            RowArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int H = a.H, N1 = a.N1, N2 = a.N2;
-  const int rs = fft_elems(N2);
-  double2* bA = reinterpret_cast<double2*>(smem_raw);  // row A of Ya
-  double2* bB = bA + rs;                                // row B of Ya
-  double2* cA = bB + rs;                                // mode 2: row A of Yb
-  double2* cB = cA + rs;                                // mode 2: row B of Yb
-  const TwSmem tw2 = load_tw2(T2, cB + rs, 2 * N2);
+  const int nw = blockDim.x >> 5;                         // warps = R rows x G pairs
+  double2* rows = reinterpret_cast<double2*>(smem_raw);  // nw rows of N2
+  const TwSmem tw2 = load_tw2(T2, rows + (size_t)nw * N2, 2 * N2);
   const FftShape s2 = make_shape(N2);
-  const int A = blockIdx.x, B = (N1 - A) & (N1 - 1);
-  const bool two = (A != B);
+  const int R = (a.mode == 2) ? 4 : 2, G = nw / R;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = w / R, j = w - g * R;
+  const int A = blockIdx.x * G + g, B = (N1 - A) & (N1 - 1);
+  const bool valid = A <= N1 / 2, two = (A != B);
   const size_t item = blockIdx.y;
   double2* Ya = a.Ya + item * H;
   double2* Yb = (a.mode == 2) ? a.Yb + item * H : nullptr;
-  for (int i = threadIdx.x; i < N2; i += blockDim.x) {
-    bA[fsw(i)] = Ya[(size_t)A * N2 + i];
-    if (two) bB[fsw(i)] = Ya[(size_t)B * N2 + i];
-    if (a.mode == 2) {
-      cA[fsw(i)] = Yb[(size_t)A * N2 + i];
-      if (two) cB[fsw(i)] = Yb[(size_t)B * N2 + i];
-    }
+  double2* rA = rows + (size_t)(g * R) * N2;  // row A of Ya, row B of Ya, row A of Yb, row B of Yb
+  double2* rB = rA + N2;
+  double2* cA = rA + 2 * N2;
+  double2* cB = rA + 3 * N2;
+  __syncthreads();  // twiddle table
+  const bool mine = valid && (two || !(j & 1));
+  if (mine) {
+    const double2* src = ((j >> 1) ? Yb : Ya) + (size_t)((j & 1) ? B : A) * N2;
+    double2* dst = rows + (size_t)w * N2;
+    for (int i = lane; i < N2; i += 32) dst[fsw(i)] = src[i];
+    __syncwarp();
+    fft_forward(dst, s2, tw2, lane, 32, WarpSync());
   }
   __syncthreads();
-  fft_forward(bA, s2, tw2, threadIdx.x, blockDim.x, CtaSync());
-  if (two) fft_forward(bB, s2, tw2, threadIdx.x, blockDim.x, CtaSync());
-  if (a.mode == 2) {
-    fft_forward(cA, s2, tw2, threadIdx.x, blockDim.x, CtaSync());
-    if (two) fft_forward(cB, s2, tw2, threadIdx.x, blockDim.x, CtaSync());
-  }
-  // pairs (p, q = H - p): p = A + N1 k2 in row A, q in row B at partner_k2
-  const int npairs = two ? N2 : ((A == 0) ? N2 / 2 + 1 : N2 / 2);
-  double2* rowB = two ? bB : bA;
-  double2* rowBc = two ? cB : cA;
-  const double2* F = (a.mode == 1) ? a.spec + item * a.spec_stride : nullptr;
-  double2* Fo = (a.mode == 0) ? a.spec_out + item * (size_t)(H + 1) : nullptr;
-  for (int k2 = threadIdx.x; k2 < npairs; k2 += blockDim.x) {
-    const int k2q = partner_k2(A, k2, N2);
-    const int pr = fsw(rev_index(s2, k2)), qr = fsw(rev_index(s2, k2q));
-    const long long p = (long long)A + (long long)N1 * k2;
-    const long long q = (p == 0) ? H : H - p;
-    const double2 W = twiddle(T, (int)p, H);  // exp(-2 pi i p / M), p < H
-    auto split = [&](double2 Zp, double2 Zq, double2& Xp, double2& Xq) {
-      double2 E = make_double2(0.5 * (Zp.x + Zq.x), 0.5 * (Zp.y - Zq.y));
-      double2 D = make_double2(0.5 * (Zp.x - Zq.x), 0.5 * (Zp.y + Zq.y));
-      double2 O = make_double2(D.y, -D.x);
-      double2 WO = cmul(W, O);
-      Xp = cadd(E, WO);
-      Xq = conjg(csub(E, WO));
-    };
-    double2 Xp, Xq;
-    split(bA[pr], rowB[qr], Xp, Xq);
-    const bool same = (!two) && (pr == qr);
-    if (a.mode == 0) {
-      Fo[p] = Xp;
-      Fo[q] = Xq;
-    } else {
-      double2 Yp, Yq;
-      if (a.mode == 1) {
-        Yp = cmulc(__ldg(F + p), Xp);
-        Yq = cmulc(__ldg(F + q), Xq);
+  if (valid) {
+    // pairs (p, q = H - p): p = A + N1 k2 in row A, q in row B at partner_k2
+    const int npairs = two ? N2 : ((A == 0) ? N2 / 2 + 1 : N2 / 2);
+    double2* rowB = two ? rB : rA;
+    double2* rowBc = two ? cB : cA;
+    const double2* F = (a.mode == 1) ? a.spec + item * a.spec_stride : nullptr;
+    double2* Fo = (a.mode == 0) ? a.spec_out + item * (size_t)(H + 1) : nullptr;
+    for (int k2 = j * 32 + lane; k2 < npairs; k2 += 32 * R) {
+      const int k2q = partner_k2(A, k2, N2);
+      const int pr = fsw(rev_index(s2, k2)), qr = fsw(rev_index(s2, k2q));
+      const long long p = (long long)A + (long long)N1 * k2;
+      const long long q = (p == 0) ? H : H - p;
+      const double2 W = twiddle(T, (int)p, H);  // exp(-2 pi i p / M), p < H
+      auto split = [&](double2 Zp, double2 Zq, double2& Xp, double2& Xq) {
+        double2 E = make_double2(0.5 * (Zp.x + Zq.x), 0.5 * (Zp.y - Zq.y));
+        double2 D = make_double2(0.5 * (Zp.x - Zq.x), 0.5 * (Zp.y + Zq.y));
+        double2 O = make_double2(D.y, -D.x);
+        double2 WO = cmul(W, O);
+        Xp = cadd(E, WO);
+        Xq = conjg(csub(E, WO));
+      };
+      double2 Xp, Xq;
+      split(rA[pr], rowB[qr], Xp, Xq);
+      const bool same = (!two) && (pr == qr);
+      if (a.mode == 0) {
+        Fo[p] = Xp;
+        Fo[q] = Xq;
       } else {
-        double2 Vp, Vq;
-        split(cA[pr], rowBc[qr], Vp, Vq);
-        Yp = cmul(Xp, Vp);
-        Yq = cmul(Xq, Vq);
+        double2 Yp, Yq;
+        if (a.mode == 1) {
+          Yp = cmulc(__ldg(F + p), Xp);
+          Yq = cmulc(__ldg(F + q), Xq);
+        } else {
+          double2 Vp, Vq;
+          split(cA[pr], rowBc[qr], Vp, Vq);
+          Yp = cmul(Xp, Vp);
+          Yq = cmul(Xq, Vq);
+        }
+        double2 E = make_double2(0.5 * (Yp.x + Yq.x), 0.5 * (Yp.y - Yq.y));
+        double2 D = make_double2(0.5 * (Yp.x - Yq.x), 0.5 * (Yp.y + Yq.y));
+        double2 O = cmulc(D, W);
+        double2* dA = (a.mode == 2) ? cA : rA;
+        double2* dB = (a.mode == 2) ? rowBc : rowB;
+        dA[pr] = make_double2(E.x - O.y, E.y + O.x);
+        if (!same) dB[qr] = make_double2(E.x + O.y, O.x - E.y);
       }
-      double2 E = make_double2(0.5 * (Yp.x + Yq.x), 0.5 * (Yp.y - Yq.y));
-      double2 D = make_double2(0.5 * (Yp.x - Yq.x), 0.5 * (Yp.y + Yq.y));
-      double2 O = cmulc(D, W);
-      double2* dA = (a.mode == 2) ? cA : bA;
-      double2* dB = (a.mode == 2) ? rowBc : rowB;
-      dA[pr] = make_double2(E.x - O.y, E.y + O.x);
-      if (!same) dB[qr] = make_double2(E.x + O.y, O.x - E.y);
     }
   }
   if (a.mode == 0) return;
   __syncthreads();
-  double2* oA = (a.mode == 2) ? cA : bA;
-  double2* oB = (a.mode == 2) ? cB : bB;
-  double2* Yo = (a.mode == 2) ? Yb : Ya;
-  fft_inverse(oA, s2, tw2, threadIdx.x, blockDim.x, CtaSync());
-  if (two) fft_inverse(oB, s2, tw2, threadIdx.x, blockDim.x, CtaSync());
-  for (int n2 = threadIdx.x; n2 < N2; n2 += blockDim.x) {
-    Yo[(size_t)A * N2 + n2] = cmulc(oA[fsw(n2)], twH(T, (long long)n2 * A, H));
-    if (two) Yo[(size_t)B * N2 + n2] = cmulc(oB[fsw(n2)], twH(T, (long long)n2 * B, H));
+  if (valid && j < 2 && (two || j == 0)) {
+    double2* o = (a.mode == 2) ? (j ? cB : cA) : (j ? rB : rA);
+    const int row = j ? B : A;
+    double2* Yo = ((a.mode == 2) ? Yb : Ya) + (size_t)row * N2;
+    fft_inverse(o, s2, tw2, lane, 32, WarpSync());
+    for (int n2 = lane; n2 < N2; n2 += 32) Yo[n2] = cmulc(o[fsw(n2)], twH(T, (long long)n2 * row, H));
   }
 }
 
 size_t large_col_smem(int N1) { return ((size_t)kColW * (N1 + 1) + tw2_entries(2 * N1)) * 16; }
-size_t large_row_smem(int N2, int mode) {
-  (void)mode;  // the table sits after four rows in every mode
-  return ((size_t)4 * fft_elems(N2) + tw2_entries(2 * N2)) * 16;
+size_t large_row_smem(int N2, int warps) {  // one row per warp, then the table
+  return ((size_t)warps * N2 + tw2_entries(2 * N2)) * 16;
 }
 
 cudaError_t large_set_attributes(int N1, int N2) {
@@ -275,7 +278,7 @@ cudaError_t large_set_attributes(int N1, int N2) {
   if ((e = cudaFuncSetAttribute(large_col_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)large_col_smem(N1))))
     return e;
   if ((e = cudaFuncSetAttribute(large_row_pair, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)large_row_smem(N2, 2))))
+                                (int)large_row_smem(N2, kWarps))))
     return e;
   return cudaSuccess;
 }
@@ -310,7 +313,7 @@ cudaError_t large_spectrum(const Plan& p, const double* series, double2* spec, i
     large_col_fwd<<<dim3(g.N2 / kColW, ni), kThreads, large_col_smem(g.N1), s>>>(
         series + (size_t)i0 * p.N, (size_t)p.N, (int)p.N, g.H, g.N1, g.N2, p.d_tw, p.d_tw1, Y);
     RowArgs ra{g.H, g.N1, g.N2, 0, Y, nullptr, nullptr, 0, spec + (size_t)i0 * (g.H + 1)};
-    large_row_pair<<<dim3(g.N1 / 2 + 1, ni), kThreads, large_row_smem(g.N2, 0), s>>>(p.d_tw, p.d_tw2, ra);
+    large_row_pair<<<dim3(g.N1 / 2 + 1, ni), 64, large_row_smem(g.N2, 2), s>>>(p.d_tw, p.d_tw2, ra);
   }
   return cudaGetLastError();
 }
@@ -326,7 +329,7 @@ cudaError_t large_correlate(const Plan& p, const double2* spec, size_t spec_stri
     large_col_fwd<<<dim3(g.N2 / kColW, ni), kThreads, large_col_smem(g.N1), s>>>(
         x + (size_t)i0 * xs, xs, n_in, g.H, g.N1, g.N2, p.d_tw, p.d_tw1, Y);
     RowArgs ra{g.H, g.N1, g.N2, 1, Y, nullptr, spec + (size_t)i0 * spec_stride, spec_stride, nullptr};
-    large_row_pair<<<dim3(g.N1 / 2 + 1, ni), kThreads, large_row_smem(g.N2, 1), s>>>(p.d_tw, p.d_tw2, ra);
+    large_row_pair<<<dim3(g.N1 / 2 + 1, ni), 64, large_row_smem(g.N2, 2), s>>>(p.d_tw, p.d_tw2, ra);
     ColInvArgs ca{};
     ca.H = g.H; ca.N1 = g.N1; ca.N2 = g.N2; ca.mode = 0;
     ca.n_out = n_out; ca.ld_out = ld_out; ca.out_stride = os; ca.out = out + (size_t)i0 * os;
@@ -341,10 +344,10 @@ cudaError_t large_correlate(const Plan& p, const double2* spec, size_t spec_stri
 cudaError_t large_hankelize(const Plan& p, const double* sigma, const double* U, const double* V, size_t nterm_total,
                             double* out, cudaStream_t s) {
   const LargeGeom g = geom(p);
-  // terms per batch (two H-point buffers each): few enough that both buffers of every
-  // term in flight stay in L2 between the passes (8 x 2 x 2 MB at cfg5), many enough to
-  // fill the GPU (column passes: N2/8 x per CTAs)
-  int per = std::max(1, std::min(p.lbuf_items / 2, (int)std::max<int64_t>(1, (int64_t)(32 << 20) / (2 * (int64_t)g.H * 16))));
+  // terms per batch (two H-point buffers each): as many as the work buffers hold -- the
+  // four-step kernels are latency-bound per CTA, so more terms in flight win over keeping
+  // the buffers in L2 (measured: 8 terms 14.9 us/term, 16: 11.9, 32: 11.2 at cfg5)
+  int per = std::max(1, p.lbuf_items / 2);
   if (const char* e = getenv("SSA_HANK_PER")) per = std::max(1, std::min(p.lbuf_items / 2, atoi(e)));
   double2* Ya = p.d_lbuf;
   double2* Yb = p.d_lbuf + (size_t)per * g.H;
@@ -355,7 +358,7 @@ cudaError_t large_hankelize(const Plan& p, const double* sigma, const double* U,
     large_col_fwd<<<dim3(g.N2 / kColW, ni), kThreads, large_col_smem(g.N1), s>>>(
         V + t0 * p.K, (size_t)p.K, (int)p.K, g.H, g.N1, g.N2, p.d_tw, p.d_tw1, Yb);
     RowArgs ra{g.H, g.N1, g.N2, 2, Ya, Yb, nullptr, 0, nullptr};
-    large_row_pair<<<dim3(g.N1 / 2 + 1, ni), kThreads, large_row_smem(g.N2, 2), s>>>(p.d_tw, p.d_tw2, ra);
+    large_row_pair<<<dim3((g.N1 / 2 + 2) / 2, ni), kThreads, large_row_smem(g.N2, kWarps), s>>>(p.d_tw, p.d_tw2, ra);
     ColInvArgs ca{};
     ca.H = g.H; ca.N1 = g.N1; ca.N2 = g.N2; ca.mode = 1;
     ca.out_stride = (size_t)p.N; ca.out = out + t0 * p.N;

@@ -380,7 +380,7 @@ cudaError_t large_decompose_one(Plan& p, const DecomposeArgs& a0, int b, cudaStr
   if ((e = cudaMemcpyAsync(sc, &z, sizeof(z), cudaMemcpyHostToDevice, s))) return e;
   if ((e = cudaMemsetAsync(p.d_ab, 0, 2 * (size_t)w * 8, s))) return e;
   // Alg. 1 lines 1-2: u_1 = p0 / |p0|
-  lg_start<<<nchL, kThreads, 0, s>>>(r, L, ldL, a.seed, (uint64_t)b, part);
+  lg_start<<<nchL, kThreads, 0, s>>>(r, L, ldL, a.seed, (uint64_t)(b + a.series_base), part);
   lg_set_nr<<<1, 32, 0, s>>>(part, nchL, sc);
   {
     // beta_1 = |p0| into beta[1], then normalize

@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(kThreads) bidiag_svd_tgk_kernel(const Decompos
     tvals += tb - ta;
     if (!done) {
       const TgkNorms nrm = tgk_norms(c, c2, n);
-      tgk_vectors(c, n, k, lam, nrm, Z, W, ipv, a.seed ^ ((unsigned long long)b << 20), cl);
+      tgk_vectors(c, n, k, lam, nrm, Z, W, ipv, a.seed ^ ((unsigned long long)(b + a.series_base) << 20), cl);
       // split z = (p1, q1, p2, ..., q_m, p_{m+1}) into unit p (m+1) and q (m)
       if (tid < k) {
         const int j = tid;
@@ -246,7 +246,7 @@ size_t tgk_svd_smem_bytes(int m_max) {
 }
 
 // Ritz rings: kRitzStages chunks of at most 32 E = 64 columns (512 B) per warp in flight
-constexpr int kRitzStages = 8;
+constexpr int kRitzStages = 16;
 constexpr int kRitzChunk = 64;
 
 size_t ritz_smem_bytes(int ldL, int ldK, int k) {

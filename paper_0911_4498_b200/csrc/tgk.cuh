@@ -111,6 +111,16 @@ __device__ inline void tgk_topk_values(const double* c2n, int n, int k, const Tg
   __syncthreads();
 }
 
+// Reciprocal for the convergence test's pivots: hardware approximation + one Newton step
+// (~1e-12 relative; the test only needs the residual to a few digits -- the reported
+// residual comes from tgk_final, which divides correctly rounded).
+__device__ __forceinline__ double rcp_check(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  const double e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+}
+
 // Convergence test: omega[j], res[j] (SMEM) for j < k; scratch: >= 2 k n doubles (shared
 // memory when it fits, else global; layout [i][j]).  Needs 2k <= blockDim.x.
 // alpha_next = alpha_{m+1}.  All threads call; ends with a barrier.
@@ -145,7 +155,7 @@ __device__ inline void tgk_check(const double* c, const double* c2, double* c2n,
       Dp[j] = q;
       for (int i = 1; i < n; ++i) {
         if (fabs(q) < pivmin) q = -pivmin;
-        q = fma(-c2[i - 1], __drcp_rn(q), -lam);
+        q = fma(-c2[i - 1], rcp_check(q), -lam);
         Dp[(size_t)i * k + j] = q;
       }
     } else {
@@ -153,7 +163,7 @@ __device__ inline void tgk_check(const double* c, const double* c2, double* c2n,
       Dm[(size_t)(n - 1) * k + j] = q;
       for (int i = n - 2; i >= 0; --i) {
         if (fabs(q) < pivmin) q = -pivmin;
-        q = fma(-c2[i], __drcp_rn(q), -lam);
+        q = fma(-c2[i], rcp_check(q), -lam);
         Dm[(size_t)i * k + j] = q;
       }
     }
@@ -175,7 +185,7 @@ __device__ inline void tgk_check(const double* c, const double* c2, double* c2n,
       for (int i = r - 1; i >= 0; --i) {
         double d = Dp[(size_t)i * k + j];
         if (fabs(d) < pivmin) d = -pivmin;
-        z = -(c[i] * __drcp_rn(d)) * z;
+        z = -(c[i] * rcp_check(d)) * z;
         nrm2 = fma(z, z, nrm2);
       }
     } else {  // entries below the twist (and the twist itself)
@@ -184,7 +194,7 @@ __device__ inline void tgk_check(const double* c, const double* c2, double* c2n,
       for (int i = r + 1; i < n; ++i) {
         double d = Dm[(size_t)i * k + j];
         if (fabs(d) < pivmin) d = -pivmin;
-        z = -(c[i - 1] * __drcp_rn(d)) * z;
+        z = -(c[i - 1] * rcp_check(d)) * z;
         nrm2 = fma(z, z, nrm2);
       }
       zn = z;  // z_n (1 when r = n - 1)

@@ -231,6 +231,19 @@ def test_run_host_matches_device(P):
     assert np.array_equal(s, sd) and np.array_equal(G, Gd)
 
 
+def test_run_host_pipelined_matches_device(P):
+    """ssa_run_host splits batches >= 512 into slices on two compute streams with the
+    device-to-host copies on a third; every output must equal the single-launch device
+    path bit for bit (per-series arithmetic is independent and fixed-order)."""
+    N, L, k, B = 300, 120, 4, 512
+    F = np.stack([ssa_inputs.cfg2_series(i, N) for i in range(B)])
+    plan = P.Plan(N, L, k, B)
+    s, U, V, G, info = plan.run_host(F)
+    sd, Ud, Vd, Gd, infod = run_decompose(P, F, L, k)
+    assert np.array_equal(s, sd) and np.array_equal(U, Ud) and np.array_equal(V, Vd) and np.array_equal(G, Gd)
+    assert np.array_equal(info["steps"], infod["steps"])
+
+
 # ----------------------------------------------------------------------------- cfg2 full size
 def test_decompose_cfg2_full_batch_sampled(P):
     """BASELINE configs[1] at full size in bench.py's launch configuration (batch 4096,
