@@ -10,6 +10,8 @@
 #include <string.h>
 
 #include <algorithm>
+#include <map>
+#include <mutex>
 #include <vector>
 
 #include "fft_smem.cuh"
@@ -43,6 +45,22 @@ struct ssa_plan_s {
 };
 
 static int round_up(int x, int m) { return (x + m - 1) / m * m; }
+
+namespace ssa {
+cudaError_t raise_smem_limit(const void* func, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> limit;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& cur = limit[std::make_pair(dev, func)];
+  if (bytes <= cur) return cudaSuccess;
+  e = cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) cur = bytes;
+  return e;
+}
+}  // namespace ssa
 // Golub-Kahan QR on an m x m bidiagonal takes ~2 sweeps per value, i.e. about m^2
 // rotations per side; 2 m^2 + 8 m + 1024 leaves room.  Overflow -> SSA_ERR_INTERNAL.
 static int rot_cap(int m_max) { return 2 * m_max * m_max + 8 * m_max + 1024; }
@@ -141,7 +159,7 @@ static ssa_status create_decompose_workspace(Plan& p, const cudaDeviceProp& prop
   const int k = p.k;
   if (k > ssa::kMaxK) return fail(SSA_ERR_UNSUPPORTED, "k = %d > %d not supported by the batched decompose", k, ssa::kMaxK);
   p.smem_lanczos = ssa::lanczos_smem_bytes((int)p.H, p.ldL, p.ldK, p.m_max, k);
-  p.smem_ritz = ssa::ritz_smem_bytes(p.ldL, p.ldK, k);
+  p.smem_ritz = ssa::ritz_smem_bytes(p.ldL, p.ldK, k, p.m_max);
   if (p.smem_lanczos > (size_t)prop.sharedMemPerBlockOptin)
     return fail(SSA_ERR_UNSUPPORTED, "decompose needs %zu B shared memory > %zu", p.smem_lanczos,
                 (size_t)prop.sharedMemPerBlockOptin);

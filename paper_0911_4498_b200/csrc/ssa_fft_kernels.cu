@@ -173,14 +173,14 @@ cudaError_t fft_set_attributes(int H, const char** which) {
   cudaError_t e;
   size_t s1 = fft_smem(H), s2 = fft_smem2(H);
   *which = "spectrum_kernel";
-  if ((e = cudaFuncSetAttribute(spectrum_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1))) return e;
+  if ((e = raise_smem_limit(spectrum_kernel, (int)s1))) return e;
   *which = "matvec_kernel";
-  if ((e = cudaFuncSetAttribute(matvec_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1))) return e;
+  if ((e = raise_smem_limit(matvec_kernel, (int)s1))) return e;
   *which = "hankelize_kernel<BIG>";
-  if ((e = cudaFuncSetAttribute(hankelize_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1))) return e;
+  if ((e = raise_smem_limit(hankelize_kernel<true>, (int)s1))) return e;
   *which = "hankelize_kernel";
   if (H <= kMaxHankelSmemH)
-    if ((e = cudaFuncSetAttribute(hankelize_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2)))
+    if ((e = raise_smem_limit(hankelize_kernel<false>, (int)s2)))
       return e;
   // shared memory over L1: these kernels keep everything in shared memory, and e.g. three
   // 75 KB matvec CTAs per SM only fit with the maximum carveout

@@ -114,6 +114,15 @@ struct Plan {
   bool ev_used[kPhases] = {};
 };
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) that never lowers the limit set by an
+// earlier plan on the same device (the attribute is per function, plans are not): the
+// limit becomes the maximum over all plans created so far.  Thread-safe (ssa_api.cu).
+cudaError_t raise_smem_limit(const void* func, size_t bytes);
+template <class F>
+inline cudaError_t raise_smem_limit(F* func, size_t bytes) {
+  return raise_smem_limit(reinterpret_cast<const void*>(func), bytes);
+}
+
 // launchers; return cudaGetLastError() after enqueue
 cudaError_t launch_spectrum(const Plan& p, const double* series, double2* spec, int nseries, cudaStream_t s);
 cudaError_t launch_matvec(const Plan& p, const double2* spec, const double* x, double* y, int transpose,
@@ -123,7 +132,7 @@ cudaError_t launch_hankelize(const Plan& p, const double* sigma, const double* U
 cudaError_t fft_set_attributes(int H, const char** which);
 
 size_t lanczos_smem_bytes(int H, int ldL, int ldK, int m_max, int k);
-size_t ritz_smem_bytes(int ldL, int ldK, int k);
+size_t ritz_smem_bytes(int ldL, int ldK, int k, int m_max);
 cudaError_t lanczos_set_attributes(size_t smem);
 cudaError_t svd_ritz_set_attributes(int m_max, size_t smem_ritz);
 constexpr int kSvdWarpsPerCta = 8;

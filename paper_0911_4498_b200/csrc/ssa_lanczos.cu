@@ -451,7 +451,7 @@ __global__ void __launch_bounds__(kThreads, 2) lanczos_kernel(const DecomposeArg
 }
 
 cudaError_t lanczos_set_attributes(size_t smem) {
-  cudaError_t e = cudaFuncSetAttribute(lanczos_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = raise_smem_limit(lanczos_kernel, (int)smem);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(lanczos_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
                              cudaSharedmemCarveoutMaxShared);

@@ -273,12 +273,11 @@ size_t large_row_smem(int N2, int warps) {  // one row per warp, then the table
 
 cudaError_t large_set_attributes(int N1, int N2) {
   cudaError_t e;
-  if ((e = cudaFuncSetAttribute(large_col_fwd, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)large_col_smem(N1))))
+  if ((e = raise_smem_limit(large_col_fwd, (int)large_col_smem(N1))))
     return e;
-  if ((e = cudaFuncSetAttribute(large_col_inv, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)large_col_smem(N1))))
+  if ((e = raise_smem_limit(large_col_inv, (int)large_col_smem(N1))))
     return e;
-  if ((e = cudaFuncSetAttribute(large_row_pair, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)large_row_smem(N2, kWarps))))
+  if ((e = raise_smem_limit(large_row_pair, (int)large_row_smem(N2, kWarps))))
     return e;
   return cudaSuccess;
 }

@@ -321,7 +321,7 @@ __global__ void lg_flip(double* X, int n, int k, const double* __restrict__ sgn)
 size_t lg_check_smem(int m_max) { return (size_t)(3 * (2 * m_max + 1) + 4 * kMaxK) * 8 + 64; }
 
 cudaError_t large_lanczos_set_attributes(int m_max) {
-  return cudaFuncSetAttribute(lg_check, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)lg_check_smem(m_max));
+  return raise_smem_limit(lg_check, (int)lg_check_smem(m_max));
 }
 
 __global__ void lg_set_nr(const double* __restrict__ part, int n, LgScalars* sc) {

@@ -246,12 +246,15 @@ size_t tgk_svd_smem_bytes(int m_max) {
 }
 
 // Ritz rings: kRitzStages chunks of at most 32 E = 64 columns (512 B) per warp in flight
-constexpr int kRitzStages = 16;
+constexpr int kRitzStages = 8;
 constexpr int kRitzChunk = 64;
 
-size_t ritz_smem_bytes(int ldL, int ldK, int k) {
+// shared memory: rings, then the 16-wide coefficient block of the current side
+// ((m_max + 1) rows x 16), then the sign scratch
+size_t ritz_smem_bytes(int ldL, int ldK, int k, int m_max) {
   (void)k;
   size_t s = (size_t)kWarps * kRitzStages * kRitzChunk * 8;
+  s += (size_t)(m_max + 2) * 16 * 8;
   s += (size_t)kWarps * kMaxK * (8 + 4) + kMaxK * 8;
   s += (size_t)kWarps * kRitzStages * 8;
   return align16(s) + 16;
@@ -261,7 +264,8 @@ __global__ void __launch_bounds__(kThreads, 2) ritz_kernel(const DecomposeArgs a
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
   double* rings = reinterpret_cast<double*>(smem_raw);
-  double* mxv = rings + (size_t)kWarps * kRitzStages * kRitzChunk;  // [kWarps][kMaxK]
+  double* scoef = rings + (size_t)kWarps * kRitzStages * kRitzChunk;  // [(m_max+2)][16]
+  double* mxv = scoef + (size_t)(a.m_max + 2) * 16;                    // [kWarps][kMaxK]
   double* sgn = mxv + kWarps * kMaxK;                                  // [kMaxK]
   int* mxi = reinterpret_cast<int*>(sgn + kMaxK);                      // [kWarps][kMaxK]
   uint64_t* bars = reinterpret_cast<uint64_t*>(mxi + kWarps * kMaxK);
@@ -295,6 +299,14 @@ __global__ void __launch_bounds__(kThreads, 2) ritz_kernel(const DecomposeArgs a
       constexpr int E = kRitzChunk / 32;
       for (int i0 = 0; i0 < k; i0 += 16) {
         const int ki = (k - i0) < 16 ? (k - i0) : 16;
+        // this block's coefficients (zero-filled to 16 columns) into shared memory: the
+        // inner loop then reads them as 8 broadcast 16-byte loads per row
+        __syncthreads();
+        for (int idx = tid; idx < rows * 16; idx += blockDim.x) {
+          const int r = idx >> 4, i = idx & 15;
+          scoef[idx] = (i < ki) ? __ldg(coef + (size_t)r * k + i0 + i) : 0.0;
+        }
+        __syncthreads();
         for (int e0 = 0; e0 < slab; e0 += 32 * E) {
           double acc[E][16];
 #pragma unroll
@@ -307,10 +319,14 @@ __global__ void __launch_bounds__(kThreads, 2) ritz_kernel(const DecomposeArgs a
           // per block of 16 triples
           const int cw = (slab - e0) < 32 * E ? (slab - e0) : 32 * E;
           stream_rows<kRitzStages>(bw + e0, ld, rows, false, cw, rg, [&](int row, const double* ch) {
-            const double* cr = coef + (size_t)row * k + i0;
+            const double2* cr = reinterpret_cast<const double2*>(scoef + (size_t)row * 16);
             double cf[16];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) cf[i] = (i < ki) ? __ldg(cr + i) : 0.0;
+            for (int i = 0; i < 8; ++i) {
+              const double2 c2 = cr[i];
+              cf[2 * i] = c2.x;
+              cf[2 * i + 1] = c2.y;
+            }
 #pragma unroll
             for (int t = 0; t < E; ++t) {
               int e = t * 32 + lane;
@@ -379,12 +395,10 @@ static size_t svd_smem_bytes(int m_max) { return (size_t)kSvdWarps * ((3 * (m_ma
 
 cudaError_t svd_ritz_set_attributes(int m_max, size_t smem_ritz) {
   cudaError_t e;
-  if ((e = cudaFuncSetAttribute(ritz_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_ritz))) return e;
-  if ((e = cudaFuncSetAttribute(bidiag_svd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)svd_smem_bytes(m_max))))
+  if ((e = raise_smem_limit(ritz_kernel, (int)smem_ritz))) return e;
+  if ((e = raise_smem_limit(bidiag_svd_kernel, (int)svd_smem_bytes(m_max))))
     return e;
-  if ((e = cudaFuncSetAttribute(bidiag_svd_tgk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)tgk_svd_smem_bytes(m_max))))
+  if ((e = raise_smem_limit(bidiag_svd_tgk_kernel, (int)tgk_svd_smem_bytes(m_max))))
     return e;
   return cudaSuccess;
 }

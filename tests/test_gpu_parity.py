@@ -231,6 +231,20 @@ def test_run_host_matches_device(P):
     assert np.array_equal(s, sd) and np.array_equal(G, Gd)
 
 
+def test_plans_of_different_sizes_interleaved(P):
+    """Kernel shared-memory limits are per function, plans are not: a small plan created
+    after a large one must not lower the limit the large plan's launches need."""
+    c = ssa_inputs.CONFIGS["cfg1"]
+    f = ssa_inputs.cfg1_series(c["N"])[None]
+    big = P.Plan(c["N"], c["L"], c["k"], 1)
+    s1 = big.decompose(cuda(f))[0].cpu().numpy()
+    small = P.Plan(40, 20, 3, 1)
+    small.decompose(cuda(np.sin(np.arange(1, 41) / 3.0)[None]))
+    s2 = big.decompose(cuda(f))[0].cpu().numpy()
+    torch.cuda.synchronize()
+    assert np.array_equal(s1, s2)
+
+
 def test_run_host_pipelined_matches_device(P):
     """ssa_run_host splits batches >= 512 into slices on two compute streams with the
     device-to-host copies on a third; every output must equal the single-launch device
