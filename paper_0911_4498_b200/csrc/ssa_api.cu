@@ -115,7 +115,7 @@ static std::vector<double2> make_twiddles2(int64_t M) {
 
 static void free_plan(Plan& p) {
   void* ptrs[] = {p.d_tw, p.d_twl, p.d_spec, p.d_U, p.d_V, p.d_ab, p.d_state, p.d_tgk, p.d_rot, p.d_vecs, p.d_coef,
-                  p.d_info, p.d_counters, p.d_hscratch, p.d_prof, p.d_tgkw, p.d_tw1, p.d_tw2, p.d_lbuf,
+                  p.d_info, p.d_counters, p.d_hscratch, p.d_prof, p.d_tgkw, p.d_tw1, p.d_tw2, p.d_tw4, p.d_twp, p.d_lbuf,
                   p.d_lgsc, p.d_lgpart, p.d_lgh, p.d_lgr, p.d_series, p.d_sigma, p.d_Uout, p.d_Vout,
                   p.d_recon};
   for (void* q : ptrs)
@@ -312,6 +312,26 @@ extern "C" ssa_status ssa_plan_create(int64_t N, int64_t L, int32_t k, int64_t b
     if ((st = alloc((void**)&p.d_tw2, t2.size() * 16, "twiddles N2")) != SSA_OK) goto bad;
     e = cudaMemcpy(p.d_tw1, t1.data(), t1.size() * 16, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(p.d_tw2, t2.data(), t2.size() * 16, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) {
+      // four-step and pair-step twiddle tables in the order the kernels read them
+      // (extended precision on the host, like every other table)
+      const long double pi2 = 2.0L * 3.14159265358979323846264338327950288L;
+      std::vector<double2> t4((size_t)H), tp((size_t)(N1 / 2 + 1) * N2);
+      for (int64_t k1 = 0; k1 < N1; ++k1)
+        for (int64_t n2 = 0; n2 < N2; ++n2) {
+          const long double ang = pi2 * (long double)((n2 * k1) % H) / (long double)H;
+          t4[(size_t)(n2 + N2 * k1)] = make_double2((double)cosl(ang), (double)(-sinl(ang)));
+        }
+      for (int64_t A = 0; A <= N1 / 2; ++A)
+        for (int64_t k2 = 0; k2 < N2; ++k2) {
+          const long double ang = pi2 * (long double)(A + N1 * k2) / (long double)M;
+          tp[(size_t)(A * N2 + k2)] = make_double2((double)cosl(ang), (double)(-sinl(ang)));
+        }
+      if ((st = alloc((void**)&p.d_tw4, t4.size() * 16, "four-step twiddles")) != SSA_OK) goto bad;
+      if ((st = alloc((void**)&p.d_twp, tp.size() * 16, "pair twiddles")) != SSA_OK) goto bad;
+      e = cudaMemcpy(p.d_tw4, t4.data(), t4.size() * 16, cudaMemcpyHostToDevice);
+      if (e == cudaSuccess) e = cudaMemcpy(p.d_twp, tp.data(), tp.size() * 16, cudaMemcpyHostToDevice);
+    }
     if (e == cudaSuccess) e = ssa::large_set_attributes(N1, N2);
     if (e != cudaSuccess) { st = cuda_fail(e, "large FFT setup"); goto bad; }
     // work buffers: ~128 MB, at least 2 items (hankelization needs a pair)

@@ -70,6 +70,8 @@ struct Plan {
   bool large = false;
   double2* d_tw1 = nullptr;      // two-level table for the N1-point sub-FFTs (M = 2 N1)
   double2* d_tw2 = nullptr;      // two-level table for the N2-point sub-FFTs (M = 2 N2)
+  double2* d_tw4 = nullptr;      // four-step twiddles W_H^{n2 k1} at [n2 + N2 k1]
+  double2* d_twp = nullptr;      // pair-step twiddles W_M^{A + N1 k2} at [A N2 + k2], A <= N1/2
   double2* d_lbuf = nullptr;     // [lbuf_items][H] complex work buffers
   int lbuf_items = 0;
   double* d_lgsc = nullptr;      // device scalars (LgScalars)

@@ -74,6 +74,15 @@ __device__ inline LSmem carve(unsigned char* base, const DecomposeArgs& a) {
   return s;
 }
 
+// Values per group of twisted factorizations whose pivots (2 n doubles each) fit in
+// region A after the three TGK arrays.
+__device__ __forceinline__ int tgk_group(const DecomposeArgs& a, int n) {
+  const long long avail = (long long)(lanczos_regionA_bytes(a.H, a.ldL, a.ldK, a.m_max) / 8) - 3LL * (2 * a.m_max + 2);
+  long long kg = avail / (2LL * n);
+  if (kg > a.k) kg = a.k;
+  return kg < 1 ? 1 : (int)kg;
+}
+
 // Counter-based start / restart vectors (R6): splitmix64 of (seed, series, i).
 __device__ __forceinline__ double rng_uniform_pm1(uint64_t seed, uint64_t series, uint64_t i) {
   uint64_t x = seed ^ (series * 0xD1B54A32D192ED03ull);
@@ -213,7 +222,6 @@ __global__ void __launch_bounds__(kThreads, 2) lanczos_kernel(const DecomposeArg
   const int pstride = a.m_max + 2;
   double* tc = reinterpret_cast<double*>(sm.regionA);  // TGK off-diagonals (aliases the rings)
   double* tc2 = tc + (2 * a.m_max + 2);
-  double* tgk_scr = a.tgk + a.tgk_stride * blockIdx.x;
 
   const TwSmem tw = load_tw2(a.tw, sm.tw, 2 * a.H);
   WarpRing rg;
@@ -325,8 +333,10 @@ __global__ void __launch_bounds__(kThreads, 2) lanczos_kernel(const DecomposeArg
         double* lohi = res + kMaxK;
         // pivots of the twisted factorizations: shared memory when they fit in region A
         double* tc2n = tc2 + (2 * a.m_max + 2);
-        const size_t need = (size_t)(3 * (2 * a.m_max + 2) + 2 * k * n) * 8;
-        double* dsc = (need <= lanczos_regionA_bytes(a.H, a.ldL, a.ldK, a.m_max)) ? tc2n + (2 * a.m_max + 2) : tgk_scr;
+        // pivots of the twisted factorizations in shared memory (region A after the
+        // three TGK arrays), in groups of kg values when all k do not fit
+        double* dsc = tc2n + (2 * a.m_max + 2);
+        const int kg = tgk_group(a, n);
         // cheap test first: omega_1 and the k-th (slowest-converging) triple only; the
         // full test of all k runs only when that one passes
         double rel;
@@ -336,7 +346,7 @@ __global__ void __launch_bounds__(kThreads, 2) lanczos_kernel(const DecomposeArg
           rel = (om[0] > 0.0) ? res[nv - 1] / om[0] : 0.0;
         }
         if (rel <= 0.5 * a.tol && k > 1) {
-          tgk_check(tc, tc2, tc2n, m, k, al, om, res, lohi, dsc);
+          tgk_check(tc, tc2, tc2n, m, k, al, om, res, lohi, dsc, 1, kg);
           double mr = 0.0;
           for (int i = 0; i < k; ++i) mr = fmax(mr, res[i]);
           rel = (om[0] > 0.0) ? mr / om[0] : 0.0;
@@ -410,11 +420,11 @@ __global__ void __launch_bounds__(kThreads, 2) lanczos_kernel(const DecomposeArg
       double* res = om + kMaxK;
       double* lohi = res + kMaxK;
       double* tc2n = tc2 + (2 * a.m_max + 2);
-      const size_t need = (size_t)(3 * (2 * a.m_max + 2) + 2 * k * n) * 8;
-      double* dsc = (need <= lanczos_regionA_bytes(a.H, a.ldL, a.ldK, a.m_max)) ? tc2n + (2 * a.m_max + 2) : tgk_scr;
+      double* dsc = tc2n + (2 * a.m_max + 2);
+      const int kg = tgk_group(a, n);
       double* cP = a.coef + (size_t)bl * 2 * (a.m_max + 2) * k;
       double* cQ = cP + (size_t)(a.m_max + 2) * k;
-      fused = tgk_final(tc, tc2, tc2n, m, k, sm.alpha[m + 1], om, lohi, res, dsc, cP, cQ, sm.cl);
+      fused = tgk_final(tc, tc2, tc2n, m, k, sm.alpha[m + 1], om, lohi, res, dsc, cP, cQ, sm.cl, kg);
       if (fused) {
         if (tid < k) a.sigma[(size_t)b * k + tid] = om[tid];
         if (tid == 0) {
@@ -444,6 +454,7 @@ __global__ void __launch_bounds__(kThreads, 2) lanczos_kernel(const DecomposeArg
     if (tid == 0) {
       st[0] = m; st[1] = converged; st[2] = breakdown; st[3] = extra; st[4] = restarts; st[5] = 0; st[6] = checks;
       st[7] = fused;
+      pc[3] += (unsigned long long)checks;  // profile slot 3: number of convergence tests
     }
   }
   if (a.prof && tid == 0)

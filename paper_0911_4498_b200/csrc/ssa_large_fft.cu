@@ -42,7 +42,7 @@ __device__ __forceinline__ double2 twH(const double2* __restrict__ T, long long 
 // ---- pass 1: forward column FFTs on packed real input x (len n_in) -------------------
 // grid (N2 / kColW, items); x item stride xs; Y item stride H.
 __global__ void __launch_bounds__(kThreads) large_col_fwd(const double* __restrict__ x, size_t xs, int n_in, int H,
-                                                          int N1, int N2, const double2* __restrict__ T,
+                                                          int N1, int N2, const double2* __restrict__ T4,
                                                           const double2* __restrict__ T1, double2* __restrict__ Y) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double2* buf = reinterpret_cast<double2*>(smem_raw);
@@ -68,7 +68,7 @@ __global__ void __launch_bounds__(kThreads) large_col_fwd(const double* __restri
     const int c = idx & (kColW - 1), k1 = idx >> 3;
     const int n2 = n2_0 + c;
     double2 v = buf[c * cs + fsw(subrev(s1, k1))];
-    v = cmul(v, twH(T, (long long)n2 * k1, H));
+    v = cmul(v, __ldg(T4 + (size_t)n2 + (size_t)N2 * k1));  // W_H^{n2 k1}, same index as Y
     Yi[(size_t)n2 + (size_t)N2 * k1] = v;
   }
 }
@@ -161,6 +161,8 @@ __global__ void __launch_bounds__(kThreads) large_col_inv(const double2* __restr
 // 2 product of the spectra of two buffers (Ya * Yb, result in Yb).
 struct RowArgs {
   int H, N1, N2, mode;
+  const double2* T4;    // W_H^{n2 k1} at [n2 + N2 k1]
+  const double2* Tp;    // W_M^{A + N1 k2} at [A N2 + k2], A <= N1/2
   double2* Ya;          // buffer of the (first) vector, [items][H]
   double2* Yb;          // mode 2: second buffer
   const double2* spec;  // mode 1: F^ [items or 1][H+1]
@@ -170,6 +172,98 @@ struct RowArgs {
 
 __device__ __forceinline__ int partner_k2(int A, int k2, int N2) {
   return (A == 0) ? ((N2 - k2) & (N2 - 1)) : (N2 - 1 - k2);
+}
+
+// Row pairs, CTA-wide FFTs (modes 0/1: one item at a time, 257..513 CTAs of 256 threads
+// keep the GPU busier than warp-level rows would).
+__global__ void __launch_bounds__(kThreads) large_row_pair_cta(const double2* __restrict__ T, const double2* __restrict__ T2,
+                                                           RowArgs a) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int H = a.H, N1 = a.N1, N2 = a.N2;
+  const int rs = fft_elems(N2);
+  double2* bA = reinterpret_cast<double2*>(smem_raw);  // row A of Ya
+  double2* bB = bA + rs;                                // row B of Ya
+  double2* cA = bB + rs;                                // mode 2: row A of Yb
+  double2* cB = cA + rs;                                // mode 2: row B of Yb
+  const TwSmem tw2 = load_tw2(T2, cB + rs, 2 * N2);
+  const FftShape s2 = make_shape(N2);
+  const int A = blockIdx.x, B = (N1 - A) & (N1 - 1);
+  const bool two = (A != B);
+  const size_t item = blockIdx.y;
+  double2* Ya = a.Ya + item * H;
+  double2* Yb = (a.mode == 2) ? a.Yb + item * H : nullptr;
+  for (int i = threadIdx.x; i < N2; i += blockDim.x) {
+    bA[fsw(i)] = Ya[(size_t)A * N2 + i];
+    if (two) bB[fsw(i)] = Ya[(size_t)B * N2 + i];
+    if (a.mode == 2) {
+      cA[fsw(i)] = Yb[(size_t)A * N2 + i];
+      if (two) cB[fsw(i)] = Yb[(size_t)B * N2 + i];
+    }
+  }
+  __syncthreads();
+  fft_forward(bA, s2, tw2, threadIdx.x, blockDim.x, CtaSync());
+  if (two) fft_forward(bB, s2, tw2, threadIdx.x, blockDim.x, CtaSync());
+  if (a.mode == 2) {
+    fft_forward(cA, s2, tw2, threadIdx.x, blockDim.x, CtaSync());
+    if (two) fft_forward(cB, s2, tw2, threadIdx.x, blockDim.x, CtaSync());
+  }
+  // pairs (p, q = H - p): p = A + N1 k2 in row A, q in row B at partner_k2
+  const int npairs = two ? N2 : ((A == 0) ? N2 / 2 + 1 : N2 / 2);
+  double2* rowB = two ? bB : bA;
+  double2* rowBc = two ? cB : cA;
+  const double2* F = (a.mode == 1) ? a.spec + item * a.spec_stride : nullptr;
+  double2* Fo = (a.mode == 0) ? a.spec_out + item * (size_t)(H + 1) : nullptr;
+  for (int k2 = threadIdx.x; k2 < npairs; k2 += blockDim.x) {
+    const int k2q = partner_k2(A, k2, N2);
+    const int pr = fsw(rev_index(s2, k2)), qr = fsw(rev_index(s2, k2q));
+    const long long p = (long long)A + (long long)N1 * k2;
+    const long long q = (p == 0) ? H : H - p;
+    const double2 W = __ldg(a.Tp + (size_t)A * N2 + k2);  // exp(-2 pi i p / M), p = A + N1 k2
+    auto split = [&](double2 Zp, double2 Zq, double2& Xp, double2& Xq) {
+      double2 E = make_double2(0.5 * (Zp.x + Zq.x), 0.5 * (Zp.y - Zq.y));
+      double2 D = make_double2(0.5 * (Zp.x - Zq.x), 0.5 * (Zp.y + Zq.y));
+      double2 O = make_double2(D.y, -D.x);
+      double2 WO = cmul(W, O);
+      Xp = cadd(E, WO);
+      Xq = conjg(csub(E, WO));
+    };
+    double2 Xp, Xq;
+    split(bA[pr], rowB[qr], Xp, Xq);
+    const bool same = (!two) && (pr == qr);
+    if (a.mode == 0) {
+      Fo[p] = Xp;
+      Fo[q] = Xq;
+    } else {
+      double2 Yp, Yq;
+      if (a.mode == 1) {
+        Yp = cmulc(__ldg(F + p), Xp);
+        Yq = cmulc(__ldg(F + q), Xq);
+      } else {
+        double2 Vp, Vq;
+        split(cA[pr], rowBc[qr], Vp, Vq);
+        Yp = cmul(Xp, Vp);
+        Yq = cmul(Xq, Vq);
+      }
+      double2 E = make_double2(0.5 * (Yp.x + Yq.x), 0.5 * (Yp.y - Yq.y));
+      double2 D = make_double2(0.5 * (Yp.x - Yq.x), 0.5 * (Yp.y + Yq.y));
+      double2 O = cmulc(D, W);
+      double2* dA = (a.mode == 2) ? cA : bA;
+      double2* dB = (a.mode == 2) ? rowBc : rowB;
+      dA[pr] = make_double2(E.x - O.y, E.y + O.x);
+      if (!same) dB[qr] = make_double2(E.x + O.y, O.x - E.y);
+    }
+  }
+  if (a.mode == 0) return;
+  __syncthreads();
+  double2* oA = (a.mode == 2) ? cA : bA;
+  double2* oB = (a.mode == 2) ? cB : bB;
+  double2* Yo = (a.mode == 2) ? Yb : Ya;
+  fft_inverse(oA, s2, tw2, threadIdx.x, blockDim.x, CtaSync());
+  if (two) fft_inverse(oB, s2, tw2, threadIdx.x, blockDim.x, CtaSync());
+  for (int n2 = threadIdx.x; n2 < N2; n2 += blockDim.x) {
+    Yo[(size_t)A * N2 + n2] = cmulc(oA[fsw(n2)], __ldg(a.T4 + (size_t)N2 * A + n2));
+    if (two) Yo[(size_t)B * N2 + n2] = cmulc(oB[fsw(n2)], __ldg(a.T4 + (size_t)N2 * B + n2));
+  }
 }
 
 // Row pairs with warp-level FFTs: each CTA takes G = warps / R row pairs (R = rows per
@@ -219,7 +313,7 @@ __global__ void __launch_bounds__(kThreads) large_row_pair(const double2* __rest
       const int pr = fsw(rev_index(s2, k2)), qr = fsw(rev_index(s2, k2q));
       const long long p = (long long)A + (long long)N1 * k2;
       const long long q = (p == 0) ? H : H - p;
-      const double2 W = twiddle(T, (int)p, H);  // exp(-2 pi i p / M), p < H
+      const double2 W = __ldg(a.Tp + (size_t)A * N2 + k2);  // exp(-2 pi i p / M), p = A + N1 k2
       auto split = [&](double2 Zp, double2 Zq, double2& Xp, double2& Xq) {
         double2 E = make_double2(0.5 * (Zp.x + Zq.x), 0.5 * (Zp.y - Zq.y));
         double2 D = make_double2(0.5 * (Zp.x - Zq.x), 0.5 * (Zp.y + Zq.y));
@@ -262,7 +356,8 @@ __global__ void __launch_bounds__(kThreads) large_row_pair(const double2* __rest
     const int row = j ? B : A;
     double2* Yo = ((a.mode == 2) ? Yb : Ya) + (size_t)row * N2;
     fft_inverse(o, s2, tw2, lane, 32, WarpSync());
-    for (int n2 = lane; n2 < N2; n2 += 32) Yo[n2] = cmulc(o[fsw(n2)], twH(T, (long long)n2 * row, H));
+    const double2* t4 = a.T4 + (size_t)N2 * row;  // W_H^{n2 row}
+    for (int n2 = lane; n2 < N2; n2 += 32) Yo[n2] = cmulc(o[fsw(n2)], __ldg(t4 + n2));
   }
 }
 
@@ -270,6 +365,7 @@ size_t large_col_smem(int N1) { return ((size_t)kColW * (N1 + 1) + tw2_entries(2
 size_t large_row_smem(int N2, int warps) {  // one row per warp, then the table
   return ((size_t)warps * N2 + tw2_entries(2 * N2)) * 16;
 }
+size_t large_row_cta_smem(int N2) { return ((size_t)4 * N2 + tw2_entries(2 * N2)) * 16; }
 
 cudaError_t large_set_attributes(int N1, int N2) {
   cudaError_t e;
@@ -277,6 +373,7 @@ cudaError_t large_set_attributes(int N1, int N2) {
     return e;
   if ((e = raise_smem_limit(large_col_inv, (int)large_col_smem(N1))))
     return e;
+  if ((e = raise_smem_limit(large_row_pair_cta, (int)large_row_cta_smem(N2)))) return e;
   if ((e = raise_smem_limit(large_row_pair, (int)large_row_smem(N2, kWarps))))
     return e;
   return cudaSuccess;
@@ -310,9 +407,9 @@ cudaError_t large_spectrum(const Plan& p, const double* series, double2* spec, i
   for (int i0 = 0; i0 < items; i0 += p.lbuf_items) {
     const int ni = std::min(items - i0, p.lbuf_items);
     large_col_fwd<<<dim3(g.N2 / kColW, ni), kThreads, large_col_smem(g.N1), s>>>(
-        series + (size_t)i0 * p.N, (size_t)p.N, (int)p.N, g.H, g.N1, g.N2, p.d_tw, p.d_tw1, Y);
-    RowArgs ra{g.H, g.N1, g.N2, 0, Y, nullptr, nullptr, 0, spec + (size_t)i0 * (g.H + 1)};
-    large_row_pair<<<dim3(g.N1 / 2 + 1, ni), 64, large_row_smem(g.N2, 2), s>>>(p.d_tw, p.d_tw2, ra);
+        series + (size_t)i0 * p.N, (size_t)p.N, (int)p.N, g.H, g.N1, g.N2, p.d_tw4, p.d_tw1, Y);
+    RowArgs ra{g.H, g.N1, g.N2, 0, p.d_tw4, p.d_twp, Y, nullptr, nullptr, 0, spec + (size_t)i0 * (g.H + 1)};
+    large_row_pair_cta<<<dim3(g.N1 / 2 + 1, ni), kThreads, large_row_cta_smem(g.N2), s>>>(p.d_tw, p.d_tw2, ra);
   }
   return cudaGetLastError();
 }
@@ -326,9 +423,9 @@ cudaError_t large_correlate(const Plan& p, const double2* spec, size_t spec_stri
   for (int i0 = 0; i0 < items; i0 += p.lbuf_items) {
     const int ni = std::min(items - i0, p.lbuf_items);
     large_col_fwd<<<dim3(g.N2 / kColW, ni), kThreads, large_col_smem(g.N1), s>>>(
-        x + (size_t)i0 * xs, xs, n_in, g.H, g.N1, g.N2, p.d_tw, p.d_tw1, Y);
-    RowArgs ra{g.H, g.N1, g.N2, 1, Y, nullptr, spec + (size_t)i0 * spec_stride, spec_stride, nullptr};
-    large_row_pair<<<dim3(g.N1 / 2 + 1, ni), 64, large_row_smem(g.N2, 2), s>>>(p.d_tw, p.d_tw2, ra);
+        x + (size_t)i0 * xs, xs, n_in, g.H, g.N1, g.N2, p.d_tw4, p.d_tw1, Y);
+    RowArgs ra{g.H, g.N1, g.N2, 1, p.d_tw4, p.d_twp, Y, nullptr, spec + (size_t)i0 * spec_stride, spec_stride, nullptr};
+    large_row_pair_cta<<<dim3(g.N1 / 2 + 1, ni), kThreads, large_row_cta_smem(g.N2), s>>>(p.d_tw, p.d_tw2, ra);
     ColInvArgs ca{};
     ca.H = g.H; ca.N1 = g.N1; ca.N2 = g.N2; ca.mode = 0;
     ca.n_out = n_out; ca.ld_out = ld_out; ca.out_stride = os; ca.out = out + (size_t)i0 * os;
@@ -353,10 +450,10 @@ cudaError_t large_hankelize(const Plan& p, const double* sigma, const double* U,
   for (size_t t0 = 0; t0 < nterm_total; t0 += per) {
     const int ni = (int)std::min<size_t>(nterm_total - t0, per);
     large_col_fwd<<<dim3(g.N2 / kColW, ni), kThreads, large_col_smem(g.N1), s>>>(
-        U + t0 * p.L, (size_t)p.L, (int)p.L, g.H, g.N1, g.N2, p.d_tw, p.d_tw1, Ya);
+        U + t0 * p.L, (size_t)p.L, (int)p.L, g.H, g.N1, g.N2, p.d_tw4, p.d_tw1, Ya);
     large_col_fwd<<<dim3(g.N2 / kColW, ni), kThreads, large_col_smem(g.N1), s>>>(
-        V + t0 * p.K, (size_t)p.K, (int)p.K, g.H, g.N1, g.N2, p.d_tw, p.d_tw1, Yb);
-    RowArgs ra{g.H, g.N1, g.N2, 2, Ya, Yb, nullptr, 0, nullptr};
+        V + t0 * p.K, (size_t)p.K, (int)p.K, g.H, g.N1, g.N2, p.d_tw4, p.d_tw1, Yb);
+    RowArgs ra{g.H, g.N1, g.N2, 2, p.d_tw4, p.d_twp, Ya, Yb, nullptr, 0, nullptr};
     large_row_pair<<<dim3((g.N1 / 2 + 2) / 2, ni), kThreads, large_row_smem(g.N2, kWarps), s>>>(p.d_tw, p.d_tw2, ra);
     ColInvArgs ca{};
     ca.H = g.H; ca.N1 = g.N1; ca.N2 = g.N2; ca.mode = 1;

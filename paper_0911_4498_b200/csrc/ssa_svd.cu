@@ -121,8 +121,7 @@ __global__ void __launch_bounds__(kSvdWarps * 32) bidiag_svd_kernel(const Decomp
     ca += (unsigned long long)(t2 - t1);
   }
   if (a.prof && lane == 0) {
-    atomicAdd(a.prof + 3, cq);
-    atomicAdd(a.prof + 4, ca);
+    atomicAdd(a.prof + 4, cq + ca);  // slot 3 counts convergence tests
   }
 }
 
@@ -236,8 +235,7 @@ __global__ void __launch_bounds__(kThreads) bidiag_svd_tgk_kernel(const Decompos
     }
   }
   if (a.prof && tid == 0) {
-    atomicAdd(a.prof + 3, (unsigned long long)tvals);
-    atomicAdd(a.prof + 4, (unsigned long long)tvecs);
+    atomicAdd(a.prof + 4, (unsigned long long)(tvals + tvecs));  // slot 3 counts convergence tests
   }
 }
 

@@ -126,8 +126,10 @@ __device__ __forceinline__ double rcp_check(double x) {
 // alpha_next = alpha_{m+1}.  All threads call; ends with a barrier.
 // c2n: scratch of n-1 doubles (shared memory) for the normalized squares.
 __device__ inline void tgk_check(const double* c, const double* c2, double* c2n, int m, int k, double alpha_next,
-                                 double* omega, double* res, double* lohi, double* scratch, int stride = 1) {
-  // k values (the (j * stride + 1)-th largest, j < k) and their residuals
+                                 double* omega, double* res, double* lohi, double* scratch, int stride = 1,
+                                 int kg = 32) {
+  // k values (the (j * stride + 1)-th largest, j < k) and their residuals; the twisted
+  // factorizations run in groups of at most kg values (scratch: 2 n kg doubles)
   const int n = 2 * m + 1;
   const int tid = threadIdx.x;
   const TgkNorms nrm = tgk_norms(c, c2, n);
@@ -144,27 +146,30 @@ __device__ inline void tgk_check(const double* c, const double* c2, double* c2n,
   // |gamma_r| = |D+_r + D-_r + lambda|; z_r = 1, z_i = -(c_i / D+_i) z_{i+1} above,
   // -(c_{i-1} / D-_i) z_{i-1} below; result |z_n| / |z|.  Pivots are divided through a
   // correctly rounded reciprocal (one multiply more, no full division on the chain).
-  const unsigned pmask = __ballot_sync(0xffffffffu, tid < 2 * k);  // lanes taking part, per warp
-  if (tid < 2 * k) {
-    const int j = tid >> 1, role = tid & 1;
+  if (kg < 1) kg = 1;
+  for (int j0 = 0; j0 < k; j0 += kg) {
+  const int nvg = (k - j0) < kg ? (k - j0) : kg;
+  const unsigned pmask = __ballot_sync(0xffffffffu, tid < 2 * nvg);  // lanes taking part, per warp
+  if (tid < 2 * nvg) {
+    const int jl = tid >> 1, j = j0 + jl, role = tid & 1;
     const double lam = omega[j];
-    double* Dp = scratch;                      // Dp[i * k + j]
-    double* Dm = scratch + (size_t)n * k;      // Dm[i * k + j]
+    double* Dp = scratch;                      // Dp[i * nvg + jl]
+    double* Dm = scratch + (size_t)n * nvg;    // Dm[i * nvg + jl]
     if (role == 0) {
       double q = -lam;
-      Dp[j] = q;
+      Dp[jl] = q;
       for (int i = 1; i < n; ++i) {
         if (fabs(q) < pivmin) q = -pivmin;
         q = fma(-c2[i - 1], rcp_check(q), -lam);
-        Dp[(size_t)i * k + j] = q;
+        Dp[(size_t)i * nvg + jl] = q;
       }
     } else {
       double q = -lam;
-      Dm[(size_t)(n - 1) * k + j] = q;
+      Dm[(size_t)(n - 1) * nvg + jl] = q;
       for (int i = n - 2; i >= 0; --i) {
         if (fabs(q) < pivmin) q = -pivmin;
         q = fma(-c2[i], rcp_check(q), -lam);
-        Dm[(size_t)i * k + j] = q;
+        Dm[(size_t)i * nvg + jl] = q;
       }
     }
     __syncwarp(pmask);
@@ -173,7 +178,7 @@ __device__ inline void tgk_check(const double* c, const double* c2, double* c2n,
     double gbest = 1e308;
     int r = -1;
     for (int i = h0; i < h1; ++i) {
-      const double g = fabs(Dp[(size_t)i * k + j] + Dm[(size_t)i * k + j] + lam);
+      const double g = fabs(Dp[(size_t)i * nvg + jl] + Dm[(size_t)i * nvg + jl] + lam);
       if (g < gbest) { gbest = g; r = i; }
     }
     const double go = __shfl_xor_sync(pmask, gbest, 1);
@@ -183,7 +188,7 @@ __device__ inline void tgk_check(const double* c, const double* c2, double* c2n,
     if (role == 0) {  // entries above the twist
       double z = 1.0;
       for (int i = r - 1; i >= 0; --i) {
-        double d = Dp[(size_t)i * k + j];
+        double d = Dp[(size_t)i * nvg + jl];
         if (fabs(d) < pivmin) d = -pivmin;
         z = -(c[i] * rcp_check(d)) * z;
         nrm2 = fma(z, z, nrm2);
@@ -192,7 +197,7 @@ __device__ inline void tgk_check(const double* c, const double* c2, double* c2n,
       double z = 1.0;
       nrm2 = 1.0;
       for (int i = r + 1; i < n; ++i) {
-        double d = Dm[(size_t)i * k + j];
+        double d = Dm[(size_t)i * nvg + jl];
         if (fabs(d) < pivmin) d = -pivmin;
         z = -(c[i - 1] * rcp_check(d)) * z;
         nrm2 = fma(z, z, nrm2);
@@ -203,6 +208,7 @@ __device__ inline void tgk_check(const double* c, const double* c2, double* c2n,
     if (role == 1) res[j] = alpha_next * 1.4142135623730951 * fabs(zn) / sqrt(tot);
   }
   __syncthreads();
+  }
 }
 
 // Clusters of the k values (descending): maximal runs with lam[j-1] - lam[j] <=
@@ -260,7 +266,7 @@ __device__ inline void warp_mgs_cols(double* C, int rows, int k, int j0, int j1)
 // near-degenerate values.  All threads call; ends with a barrier.  Needs 2k <= blockDim.x.
 __device__ inline int tgk_final(const double* c, const double* c2, double* c2n, int m, int k, double alpha_next,
                                 double* lam, double* lohi, double* res, double* scratch, double* cP, double* cQ,
-                                int* cl) {
+                                int* cl, int kg = 32) {
   const int n = 2 * m + 1;
   const int tid = threadIdx.x;
   const TgkNorms nrm = tgk_norms(c, c2, n);
@@ -275,27 +281,30 @@ __device__ inline int tgk_final(const double* c, const double* c2, double* c2n, 
   if (tid == 0) s_bad = tgk_clusters(lam, k, nrm.gmax, cl);
   __syncthreads();
   if (s_bad) return 0;
-  const unsigned pmask = __ballot_sync(0xffffffffu, tid < 2 * k);
-  if (tid < 2 * k) {
-    const int j = tid >> 1, role = tid & 1;
+  if (kg < 1) kg = 1;
+  for (int j0 = 0; j0 < k; j0 += kg) {
+  const int nvg = (k - j0) < kg ? (k - j0) : kg;
+  const unsigned pmask = __ballot_sync(0xffffffffu, tid < 2 * nvg);
+  if (tid < 2 * nvg) {
+    const int jl = tid >> 1, j = j0 + jl, role = tid & 1;
     const double lm = lam[j];
-    double* Dp = scratch;                  // Dp[i * k + j]
-    double* Dm = scratch + (size_t)n * k;  // Dm[i * k + j]
+    double* Dp = scratch;                    // Dp[i * nvg + jl]
+    double* Dm = scratch + (size_t)n * nvg;  // Dm[i * nvg + jl]
     if (role == 0) {
       double q = -lm;
-      Dp[j] = q;
+      Dp[jl] = q;
       for (int i = 1; i < n; ++i) {
         if (fabs(q) < pivmin) q = -pivmin;
         q = fma(-c2[i - 1], __drcp_rn(q), -lm);
-        Dp[(size_t)i * k + j] = q;
+        Dp[(size_t)i * nvg + jl] = q;
       }
     } else {
       double q = -lm;
-      Dm[(size_t)(n - 1) * k + j] = q;
+      Dm[(size_t)(n - 1) * nvg + jl] = q;
       for (int i = n - 2; i >= 0; --i) {
         if (fabs(q) < pivmin) q = -pivmin;
         q = fma(-c2[i], __drcp_rn(q), -lm);
-        Dm[(size_t)i * k + j] = q;
+        Dm[(size_t)i * nvg + jl] = q;
       }
     }
     __syncwarp(pmask);
@@ -304,7 +313,7 @@ __device__ inline int tgk_final(const double* c, const double* c2, double* c2n, 
     int r = -1;
 #pragma unroll 4
     for (int i = h0; i < h1; ++i) {
-      const double g = fabs(Dp[(size_t)i * k + j] + Dm[(size_t)i * k + j] + lm);
+      const double g = fabs(Dp[(size_t)i * nvg + jl] + Dm[(size_t)i * nvg + jl] + lm);
       if (g < gbest) { gbest = g; r = i; }
     }
     const double go = __shfl_xor_sync(pmask, gbest, 1);
@@ -316,7 +325,7 @@ __device__ inline int tgk_final(const double* c, const double* c2, double* c2n, 
     if (role == 0) {
       double z = 1.0;
       for (int i = r - 1; i >= 0; --i) {
-        double d = Dp[(size_t)i * k + j];
+        double d = Dp[(size_t)i * nvg + jl];
         if (fabs(d) < pivmin) d = -pivmin;
         z = -(c[i] * __drcp_rn(d)) * z;
         if (i & 1) { cQ[(size_t)(i >> 1) * k + j] = z; sq = fma(z, z, sq); }
@@ -327,7 +336,7 @@ __device__ inline int tgk_final(const double* c, const double* c2, double* c2n, 
       if (r & 1) { cQ[(size_t)(r >> 1) * k + j] = z; sq = 1.0; }
       else { cP[(size_t)(r >> 1) * k + j] = z; sp = 1.0; }
       for (int i = r + 1; i < n; ++i) {
-        double d = Dm[(size_t)i * k + j];
+        double d = Dm[(size_t)i * nvg + jl];
         if (fabs(d) < pivmin) d = -pivmin;
         z = -(c[i - 1] * __drcp_rn(d)) * z;
         if (i & 1) { cQ[(size_t)(i >> 1) * k + j] = z; sq = fma(z, z, sq); }
@@ -346,6 +355,7 @@ __device__ inline int tgk_final(const double* c, const double* c2, double* c2n, 
     }
   }
   __syncthreads();
+  }
   // orthonormalize inside clusters: one warp per cluster
   {
     const int w = tid >> 5, nw = blockDim.x >> 5, nc = cl[33];
