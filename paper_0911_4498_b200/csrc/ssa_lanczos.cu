@@ -342,11 +342,11 @@ __global__ void __launch_bounds__(kThreads, 2) lanczos_kernel(const DecomposeArg
         double rel;
         {
           const int nv = (k > 1) ? 2 : 1;
-          tgk_check(tc, tc2, tc2n, m, nv, al, om, res, lohi, tc2n + (2 * a.m_max + 2), k - 1);
+          tgk_check(tc, tc2, tc2n, m, nv, al, om, res, lohi, tc2n + (2 * a.m_max + 2), k - 1, 32, pc + 4);
           rel = (om[0] > 0.0) ? res[nv - 1] / om[0] : 0.0;
         }
         if (rel <= 0.5 * a.tol && k > 1) {
-          tgk_check(tc, tc2, tc2n, m, k, al, om, res, lohi, dsc, 1, kg);
+          tgk_check(tc, tc2, tc2n, m, k, al, om, res, lohi, dsc, 1, kg, pc + 4);
           double mr = 0.0;
           for (int i = 0; i < k; ++i) mr = fmax(mr, res[i]);
           rel = (om[0] > 0.0) ? mr / om[0] : 0.0;
@@ -424,7 +424,10 @@ __global__ void __launch_bounds__(kThreads, 2) lanczos_kernel(const DecomposeArg
       const int kg = tgk_group(a, n);
       double* cP = a.coef + (size_t)bl * 2 * (a.m_max + 2) * k;
       double* cQ = cP + (size_t)(a.m_max + 2) * k;
-      fused = tgk_final(tc, tc2, tc2n, m, k, sm.alpha[m + 1], om, lohi, res, dsc, cP, cQ, sm.cl, kg);
+      // the cluster Gram-Schmidt works on a shared-memory copy when (2m+1) k doubles fit
+      const long long avail = (long long)(lanczos_regionA_bytes(a.H, a.ldL, a.ldK, a.m_max) / 8) - 3LL * (2 * a.m_max + 2);
+      double* stage = ((long long)n * k <= avail) ? dsc : nullptr;
+      fused = tgk_final(tc, tc2, tc2n, m, k, sm.alpha[m + 1], om, lohi, res, dsc, cP, cQ, sm.cl, kg, stage);
       if (fused) {
         if (tid < k) a.sigma[(size_t)b * k + tid] = om[tid];
         if (tid == 0) {

@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(kSvdWarps * 32) bidiag_svd_kernel(const Decomp
     ca += (unsigned long long)(t2 - t1);
   }
   if (a.prof && lane == 0) {
-    atomicAdd(a.prof + 4, cq + ca);  // slot 3 counts convergence tests
+    atomicAdd(a.prof + 7, cq + ca);  // slots 3-5 belong to the Lanczos kernel
   }
 }
 
@@ -210,8 +210,8 @@ __global__ void __launch_bounds__(kThreads) bidiag_svd_tgk_kernel(const Decompos
         const int w = tid >> 5, nw = blockDim.x >> 5;
         for (int q = w; q < cl[33]; q += nw) {
           if (cl[q + 1] - cl[q] < 2) continue;
-          warp_mgs_cols(cP, m + 1, k, cl[q], cl[q + 1]);
-          warp_mgs_cols(cQ, m, k, cl[q], cl[q + 1]);
+          warp_mgs_cols(cP, m + 1, k, 1, cl[q], cl[q + 1]);
+          warp_mgs_cols(cQ, m, k, 1, cl[q], cl[q + 1]);
         }
       }
       __syncthreads();
@@ -235,7 +235,7 @@ __global__ void __launch_bounds__(kThreads) bidiag_svd_tgk_kernel(const Decompos
     }
   }
   if (a.prof && tid == 0) {
-    atomicAdd(a.prof + 4, (unsigned long long)(tvals + tvecs));  // slot 3 counts convergence tests
+    atomicAdd(a.prof + 7, (unsigned long long)(tvals + tvecs));  // slots 3-5 belong to the Lanczos kernel
   }
 }
 
@@ -386,7 +386,7 @@ __global__ void __launch_bounds__(kThreads, 2) ritz_kernel(const DecomposeArgs a
       }
     }
   }
-  if (a.prof && tid == 0) atomicAdd(a.prof + 5, (unsigned long long)(clock64() - t0));
+  if (a.prof && tid == 0) atomicAdd(a.prof + 7, (unsigned long long)(clock64() - t0));
 }
 
 static size_t svd_smem_bytes(int m_max) { return (size_t)kSvdWarps * ((3 * (m_max + 2) + 2 * kMaxK) * 8); }

@@ -41,17 +41,32 @@ __device__ __forceinline__ int tgk_negcount(const double* c2, int n, double x, d
 __device__ __forceinline__ int tgk_negcount_poly(const double* c2n, int n, double xn) {
   double p2 = 1.0, p1 = -xn;
   int cnt = p1 < 0.0;
-  for (int i = 1; i < n; ++i) {
+  int i = 1;
+  // blocks of 16 steps: the 16 squared off-diagonals are loaded first so that only the
+  // FMA chain is sequential (the loads of a step-by-step loop sat on it), then the exact
+  // power-of-two rescale at i = 16, 32, ...
+  for (; i + 16 <= n; i += 16) {
+    double cv[16];
+#pragma unroll
+    for (int t = 0; t < 16; ++t) cv[t] = c2n[i - 1 + t];
+#pragma unroll
+    for (int t = 0; t < 16; ++t) {
+      double p = fma(-xn, p1, -cv[t] * p2);
+      if (p == 0.0) p = -copysign(0x1.0p-900, p1);
+      cnt += (p < 0.0) != (p1 < 0.0);
+      p2 = p1;
+      p1 = p;
+    }
+    const double mx = fmax(fabs(p1), fabs(p2));
+    if (mx < 0x1.0p-400) { p1 *= 0x1.0p+400; p2 *= 0x1.0p+400; }
+    else if (mx > 0x1.0p+400) { p1 *= 0x1.0p-400; p2 *= 0x1.0p-400; }
+  }
+  for (; i < n; ++i) {  // fewer than 16 steps left: no rescale point among them
     double p = fma(-xn, p1, -c2n[i - 1] * p2);
     if (p == 0.0) p = -copysign(0x1.0p-900, p1);
     cnt += (p < 0.0) != (p1 < 0.0);
     p2 = p1;
     p1 = p;
-    if ((i & 15) == 0) {
-      const double mx = fmax(fabs(p1), fabs(p2));
-      if (mx < 0x1.0p-400) { p1 *= 0x1.0p+400; p2 *= 0x1.0p+400; }
-      else if (mx > 0x1.0p+400) { p1 *= 0x1.0p-400; p2 *= 0x1.0p-400; }
-    }
   }
   return cnt;
 }
@@ -81,12 +96,19 @@ __device__ __forceinline__ TgkNorms tgk_norms(const double* c, const double* c2,
 __device__ inline void tgk_topk_values(const double* c2n, int n, int k, const TgkNorms& nrm, double* lohi, double* lam,
                                 int max_rounds, int stride = 1) {
   // value j is the (j * stride + 1)-th largest eigenvalue (stride > 1: a sparse subset)
+  // T threads per value: up to 32 with warp ballots; few values (the cheap convergence
+  // test) get whole warps, up to 256 threads each, counted through shared memory, so
+  // every round shrinks the bracket up to 257-fold
   const int tid = threadIdx.x, nthr = blockDim.x;
   int T = 32;
   while (T > 1 && k * T > nthr) T >>= 1;
+  if (T == 32)
+    while (T < 256 && k * T * 2 <= nthr) T *= 2;
+  __shared__ int cnt_s[8];
   const int j = tid / T, t = tid - j * T;
   const bool act = j < k;
   if (act && t == 0) { lohi[2 * j] = 0.0; lohi[2 * j + 1] = nrm.gmax * (1.0 + 1e-15) + 1e-300; }
+  if (T > 32 && tid < 8) cnt_s[tid] = 0;
   __syncthreads();
   for (int round = 0; round < max_rounds; ++round) {
     double lo = act ? lohi[2 * j] : 0.0, hi = act ? lohi[2 * j + 1] : 0.0;
@@ -95,15 +117,23 @@ __device__ inline void tgk_topk_values(const double* c2n, int n, int k, const Tg
     double x = lo + (hi - lo) * (double)(t + 1) / (double)(T + 1);
     bool pred = act && (n - tgk_negcount_poly(c2n, n, x / nrm.gmax) >= j * stride + 1);
     unsigned bits = __ballot_sync(0xffffffffu, pred);
-    int shift = (T >= 32) ? 0 : ((tid & 31) / T) * T;
-    unsigned gb = (T >= 32) ? bits : ((bits >> shift) & ((1u << T) - 1u));
-    int ts = __popc(gb) - 1;  // monotone predicate: true for t <= ts
+    int ts;
+    if (T > 32) {  // whole warps per value: popcounts summed in shared memory
+      if ((tid & 31) == 0 && act) atomicAdd(&cnt_s[j], __popc(bits));
+      __syncthreads();
+      ts = act ? cnt_s[j] - 1 : -1;  // monotone predicate: true for t <= ts
+    } else {
+      int shift = (T >= 32) ? 0 : ((tid & 31) / T) * T;
+      unsigned gb = (T >= 32) ? bits : ((bits >> shift) & ((1u << T) - 1u));
+      ts = __popc(gb) - 1;
+    }
     __syncthreads();
     if (act && t == 0) {
       double nlo = (ts >= 0) ? lo + (hi - lo) * (double)(ts + 1) / (double)(T + 1) : lo;
       double nhi = (ts < T - 1) ? lo + (hi - lo) * (double)(ts + 2) / (double)(T + 1) : hi;
       lohi[2 * j] = nlo;
       lohi[2 * j + 1] = nhi;
+      if (T > 32) cnt_s[j] = 0;
     }
     __syncthreads();
   }
@@ -127,7 +157,8 @@ __device__ __forceinline__ double rcp_check(double x) {
 // c2n: scratch of n-1 doubles (shared memory) for the normalized squares.
 __device__ inline void tgk_check(const double* c, const double* c2, double* c2n, int m, int k, double alpha_next,
                                  double* omega, double* res, double* lohi, double* scratch, int stride = 1,
-                                 int kg = 32) {
+                                 int kg = 32, unsigned long long* tm = nullptr) {
+  const long long t_start = clock64();
   // k values (the (j * stride + 1)-th largest, j < k) and their residuals; the twisted
   // factorizations run in groups of at most kg values (scratch: 2 n kg doubles)
   const int n = 2 * m + 1;
@@ -140,6 +171,7 @@ __device__ inline void tgk_check(const double* c, const double* c2, double* c2n,
     __syncthreads();
   }
   tgk_topk_values(c2n, n, k, nrm, lohi, omega, 16, stride);
+  const long long t_vals = clock64();
   // twisted factorization for lambda = omega_j, two lanes per value: the even lane runs
   // the forward pivots D+ (and later the entries above the twist), the odd lane the
   // backward pivots D- (and the entries below).  Twist r at the smallest
@@ -209,6 +241,10 @@ __device__ inline void tgk_check(const double* c, const double* c2, double* c2n,
   }
   __syncthreads();
   }
+  if (tm && threadIdx.x == 0) {  // profiling: cycles in the values / twisted parts
+    tm[0] += (unsigned long long)(t_vals - t_start);
+    tm[1] += (unsigned long long)(clock64() - t_vals);
+  }
 }
 
 // Clusters of the k values (descending): maximal runs with lam[j-1] - lam[j] <=
@@ -231,26 +267,27 @@ __device__ inline int tgk_clusters(const double* lam, int k, double tnorm, int* 
   return bad;
 }
 
-// Modified Gram-Schmidt (twice) of the columns j0..j1-1 of C (rows x k, column j at
-// C[r * k + j]); one warp, lanes over rows.
-__device__ inline void warp_mgs_cols(double* C, int rows, int k, int j0, int j1) {
+// Modified Gram-Schmidt (twice) of the columns j0..j1-1 of C (rows x k; element (r, j) at
+// C[r * rs + j * cs]); one warp, lanes over rows.
+__device__ inline void warp_mgs_cols(double* C, int rows, int rs, int cs, int j0, int j1) {
   const int lane = threadIdx.x & 31;
   for (int j = j0; j < j1; ++j) {
     for (int pass = 0; pass < 2; ++pass)
       for (int q = j0; q < j; ++q) {
         double d = 0.0;
-        for (int r = lane; r < rows; r += 32) d = fma(C[(size_t)r * k + j], C[(size_t)r * k + q], d);
+        for (int r = lane; r < rows; r += 32) d = fma(C[(size_t)r * rs + (size_t)j * cs], C[(size_t)r * rs + (size_t)q * cs], d);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) d += __shfl_xor_sync(0xffffffffu, d, o);
-        for (int r = lane; r < rows; r += 32) C[(size_t)r * k + j] = fma(-d, C[(size_t)r * k + q], C[(size_t)r * k + j]);
+        for (int r = lane; r < rows; r += 32)
+          C[(size_t)r * rs + (size_t)j * cs] = fma(-d, C[(size_t)r * rs + (size_t)q * cs], C[(size_t)r * rs + (size_t)j * cs]);
         __syncwarp();
       }
     double s2 = 0.0;
-    for (int r = lane; r < rows; r += 32) s2 = fma(C[(size_t)r * k + j], C[(size_t)r * k + j], s2);
+    for (int r = lane; r < rows; r += 32) s2 = fma(C[(size_t)r * rs + (size_t)j * cs], C[(size_t)r * rs + (size_t)j * cs], s2);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s2 += __shfl_xor_sync(0xffffffffu, s2, o);
     const double inv = s2 > 0.0 ? 1.0 / sqrt(s2) : 0.0;
-    for (int r = lane; r < rows; r += 32) C[(size_t)r * k + j] *= inv;
+    for (int r = lane; r < rows; r += 32) C[(size_t)r * rs + (size_t)j * cs] *= inv;
     __syncwarp();
   }
 }
@@ -266,7 +303,7 @@ __device__ inline void warp_mgs_cols(double* C, int rows, int k, int j0, int j1)
 // near-degenerate values.  All threads call; ends with a barrier.  Needs 2k <= blockDim.x.
 __device__ inline int tgk_final(const double* c, const double* c2, double* c2n, int m, int k, double alpha_next,
                                 double* lam, double* lohi, double* res, double* scratch, double* cP, double* cQ,
-                                int* cl, int kg = 32) {
+                                int* cl, int kg = 32, double* stage = nullptr) {
   const int n = 2 * m + 1;
   const int tid = threadIdx.x;
   const TgkNorms nrm = tgk_norms(c, c2, n);
@@ -356,13 +393,37 @@ __device__ inline int tgk_final(const double* c, const double* c2, double* c2n, 
   }
   __syncthreads();
   }
-  // orthonormalize inside clusters: one warp per cluster
+  // orthonormalize inside clusters: one warp per cluster; with `stage` (shared memory,
+  // (2m+1) k doubles, free now that the pivots are done) the columns are copied in, worked
+  // on there and copied back
   {
-    const int w = tid >> 5, nw = blockDim.x >> 5, nc = cl[33];
-    for (int q = w; q < nc; q += nw) {
-      if (cl[q + 1] - cl[q] < 2) continue;
-      warp_mgs_cols(cP, m + 1, k, cl[q], cl[q + 1]);
-      warp_mgs_cols(cQ, m, k, cl[q], cl[q + 1]);
+    const int nc = cl[33];
+    bool any = false;
+    for (int q = 0; q < nc; ++q) any |= (cl[q + 1] - cl[q] > 1);
+    if (any) {
+      // staged copies are column-major (lanes over rows read consecutive words)
+      double* P = cP;
+      double* Q = cQ;
+      int prs = k, pcs = 1, qrs = k, qcs = 1;
+      if (stage) {
+        P = stage;
+        Q = stage + (size_t)(m + 1) * k;
+        prs = 1; pcs = m + 1; qrs = 1; qcs = m;
+        for (int i = tid; i < (m + 1) * k; i += blockDim.x) P[(i % k) * (m + 1) + i / k] = cP[i];
+        for (int i = tid; i < m * k; i += blockDim.x) Q[(i % k) * m + i / k] = cQ[i];
+        __syncthreads();
+      }
+      const int w = tid >> 5, nw = blockDim.x >> 5;
+      for (int q = w; q < nc; q += nw) {
+        if (cl[q + 1] - cl[q] < 2) continue;
+        warp_mgs_cols(P, m + 1, prs, pcs, cl[q], cl[q + 1]);
+        warp_mgs_cols(Q, m, qrs, qcs, cl[q], cl[q + 1]);
+      }
+      __syncthreads();
+      if (stage) {
+        for (int i = tid; i < (m + 1) * k; i += blockDim.x) cP[i] = P[(i % k) * (m + 1) + i / k];
+        for (int i = tid; i < m * k; i += blockDim.x) cQ[i] = Q[(i % k) * m + i / k];
+      }
     }
   }
   __syncthreads();

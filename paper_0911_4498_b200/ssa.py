@@ -166,7 +166,7 @@ class Plan:
         """Per-phase SM cycles of the decompose kernel (plan created with profile=True)."""
         out = (ctypes.c_int64 * 8)()
         _check(load_library().ssa_plan_profile(self._h, out))
-        keys = ["fft", "reorth", "check", "n_checks", "svd_vectors", "ritz_kernel", "svd_fused", "other"]
+        keys = ["fft", "reorth", "check", "n_checks", "check_values", "check_twisted", "svd_fused", "other"]
         return dict(zip(keys, list(out)))
 
     def bidiagonals(self):

@@ -11,10 +11,10 @@ F = torch.from_numpy(ssa_inputs.cfg2_batch(0, B, c["N"])).cuda()
 plan = P.Plan(c["N"], c["L"], c["k"], B, profile=True, reorth=R, check_every=CE)
 s, U, V, info = plan.decompose(F); torch.cuda.synchronize()
 t0 = time.time(); plan.decompose(F, s, U, V, info); torch.cuda.synchronize(); dt = time.time() - t0
-pr = plan.profile(); tot = sum(v for k, v in pr.items() if k != "n_checks")
+pr = plan.profile(); tot = sum(v for k, v in pr.items() if k in ("fft", "reorth", "check", "svd_fused", "other"))
 print("check_every=%d reorth=%d decompose %.1f ms for %d series; phase ms:" % (CE, R, dt * 1e3, B), plan.phase_ms())
 for k, v in pr.items():
-    print(f"  {k:10s} {v:16d}  {100*v/tot if k!='n_checks' else 0:5.1f}%")
+    print(f"  {k:14s} {v:16d}  {100*v/tot:5.1f}%" if k != "n_checks" else f"  {k:14s} {v:16d}  ({v/B:.1f} per series)")
 inf = P.info_to_numpy(info)
 print("steps mean", inf["steps"].mean(), "status", np.unique(inf["status"], return_counts=True), "maxres", inf["max_residual"].max(),
       "reorth_extra mean", inf["reorth_extra"].mean(), "max", inf["reorth_extra"].max())
