@@ -71,7 +71,7 @@ def test_cfg5_shape_sampled_terms(P):
         assert nrel(g[0, i], ref) <= 1e-10
 
 
-@pytest.mark.parametrize("N,L,k", [(1024, 512, 10), (600, 250, 8), (4096, 2048, 16)])
+@pytest.mark.parametrize("N,L,k", [(1024, 512, 10), (600, 250, 8), (4096, 2048, 16), (700, 520, 6)])
 def test_long_decompose_vs_oracle(P, N, L, k):
     """The long-series Lanczos path forced onto sizes the Jacobi oracle can do."""
     if N == 1024:

@@ -231,6 +231,33 @@ def test_run_host_matches_device(P):
     assert np.array_equal(s, sd) and np.array_equal(G, Gd)
 
 
+def test_decompose_chunked_matches_single_chunk(P, monkeypatch):
+    """A plan whose workspace holds fewer series than the batch loops over chunks; every
+    series keeps its global index (start vector), so the results equal one chunk's."""
+    N, L, k, B = 400, 150, 6, 12
+    F = np.stack([ssa_inputs.cfg2_series(i, N) for i in range(B)])
+    s1, U1, V1, G1, i1 = run_decompose(P, F, L, k)
+    monkeypatch.setenv("SSA_MAX_CHUNK", "5")
+    s2, U2, V2, G2, i2 = run_decompose(P, F, L, k)
+    assert np.array_equal(s1, s2) and np.array_equal(U1, U2) and np.array_equal(G1, G2)
+    check_against_oracle(F[7], L, k, s2[7], U2[7], V2[7], G2[7])
+
+
+@pytest.mark.parametrize("svd", ["tgk", "qr"])
+def test_decompose_k_max_and_svd_options(P, svd):
+    """k = 32 (the batched path's maximum) with both bidiagonal SVD methods (TGK twisted
+    factorization + inverse iteration fallback; implicit-shift QR)."""
+    rng = np.random.default_rng(32)
+    N, L, k = 700, 300, 32
+    n = np.arange(1, N + 1)
+    f = (np.sin(2 * np.pi * n / 17) + 0.7 * np.sin(2 * np.pi * n / 45) + 0.02 * n ** 0.5
+         + 0.4 * rng.standard_normal(N))
+    s, U, V, G, info = run_decompose(P, f[None], L, k, svd=svd)
+    assert info[0]["status"] == 0, info
+    check_against_oracle(f, L, k, s[0], U[0], V[0], G[0])
+    assert np.abs(U[0] @ U[0].T - np.eye(k)).max() <= 1e-13
+
+
 def test_plans_of_different_sizes_interleaved(P):
     """Kernel shared-memory limits are per function, plans are not: a small plan created
     after a large one must not lower the limit the large plan's launches need."""
