@@ -85,6 +85,22 @@ def hankelize_alg_bytes(nterms: int, N: int, L: int) -> float:
 
 
 # ------------------------------------------------------------------------ microbenchmarks
+def fp64_peak():
+    """Measured fp64 peak (TFLOP/s of DFMA, 2 flops each) from profiles/peaks_r01.json
+    (tools/peaks.cu on a B200 of this pool); the guide's nominal 37 TF if absent."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "peaks_r01.json")) as fh:
+            return float(json.load(fh)["dfma_tflops"]), "profiles/peaks_r01.json dfma_tflops (tools/peaks.cu, measured)"
+    except Exception:
+        return 37.0, "nominal fp64 (no measured file)"
+
+
+def fft_flops(n: int) -> float:
+    """Real FFT of length n: 2.5 n log2 n (benchFFT convention)."""
+    import math
+    return 2.5 * n * math.log2(n)
+
+
 def _events_ms(fn, reps=1):
     import torch
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -127,10 +143,15 @@ def micro_matvec(P, peak):
     nprod = T * B
     M = plan.M
     byt = nprod * (8 * (K + L) + 16 * (M // 2 + 1))
+    fl = nprod * (2 * fft_flops(M) + 6 * (M // 2 + 1))
+    fpk, fsrc = fp64_peak()
     out = {"value": nprod / (ms * 1e-3), "unit": "Hankel matvecs/s", "per_gpu": True, "ms": ms, "products": nprod,
            "workload": "cfg4 (BASELINE.json configs[3]): 65536 series N=8192 L=4096, 64 alternating products",
            "roofline": {"bound": "hbm", "achieved": byt / (ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
-                        "frac": byt / (ms * 1e-3) / 1e9 / peak, "alg_bytes_per_product": byt / nprod}}
+                        "frac": byt / (ms * 1e-3) / 1e9 / peak, "alg_bytes_per_product": byt / nprod},
+           "fp64_roofline": {"bound": "fp64 (model flops: 2 x 2.5 M log2 M + 6(M/2+1) per product)",
+                             "achieved": fl / (ms * 1e-3) / 1e12, "peak": fpk, "unit": "TFLOP/s",
+                             "frac": fl / (ms * 1e-3) / 1e12 / fpk, "peak_src": fsrc}}
     plan.close()
     del spec, v, u, y, z
     torch.cuda.empty_cache()
@@ -165,13 +186,50 @@ def micro_hankelize(P, peak):
     nt = B * T
     byt = nt * 8 * (L + K + N)
     flops = nt * (3 * 2.5 * N * math.log2(N) + 6 * (N // 2 + 1) + 2 * N)
+    fpk, fsrc = fp64_peak()
     res = {"value": nt / (ms * 1e-3), "unit": "terms/s", "per_gpu": True, "ms": ms, "terms": nt,
            "workload": "cfg5 (BASELINE.json configs[4]): 256 x 50 terms, N=262144 L=131072",
-           "roofline": {"bound": "hbm (model; the fp64 FFT work sits at the ridge)",
-                        "achieved": byt / (ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
-                        "frac": byt / (ms * 1e-3) / 1e9 / peak, "fp64_tflops_model": flops / (ms * 1e-3) / 1e12}}
+           "roofline": {"bound": "fp64 (model flops 3 x 2.5 N log2 N + 6(N/2+1) + 2N per term; "
+                                 "SURVEY.md §8(d): 1.07 us/term fp64 vs 0.64 us HBM)",
+                        "achieved": flops / (ms * 1e-3) / 1e12, "peak": fpk, "unit": "TFLOP/s",
+                        "frac": flops / (ms * 1e-3) / 1e12 / fpk, "peak_src": fsrc},
+           "hbm_roofline": {"achieved": byt / (ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+                            "frac": byt / (ms * 1e-3) / 1e9 / peak, "alg_bytes_per_term": byt / nt}}
     plan.close()
     del U, V, out, sig
+    torch.cuda.empty_cache()
+    return res
+
+
+def micro_decompose_cfg3(P, peak):
+    """BASELINE.json configs[2] (cfg3): one long series N=2^20, L=2^19, k=32 (ssa_inputs
+    cfg3_series, seed 3) on one GPU: full decompose (four-step FFT products through L2,
+    full reorthogonalization, bidiagonal SVD, Ritz vectors) + reconstruct of the 32 triples.
+    Roofline: HBM, algorithmic bytes of the half-steps (lanczos_alg_bytes) with the steps run."""
+    import torch
+    c = ssa_inputs.CONFIGS["cfg3"]
+    N, L, k = c["N"], c["L"], c["k"]
+    x = torch.from_numpy(ssa_inputs.cfg3_series()[None].copy()).cuda()
+    plan = P.Plan(N, L, k, 1)
+    s_, U, V, info = plan.decompose(x)
+    G = plan.reconstruct(s_, U, V)
+    torch.cuda.synchronize()
+
+    def run():
+        plan.decompose(x, s_, U, V, info)
+        plan.reconstruct(s_, U, V, out=G)
+    ms = min(_events_ms(run) for _ in range(3))
+    inf = P.info_to_numpy(info)[0]
+    m = int(inf["steps"])
+    byt = lanczos_alg_bytes(np.array([m]), N, L, k) + hankelize_alg_bytes(k, N, L)
+    res = {"value": k / (ms * 1e-3), "unit": "eigentriples/s", "ms": ms, "steps": m,
+           "hankel_matvecs_per_s": 2 * m / (ms * 1e-3), "status": int(inf["status"]),
+           "converged": int(inf["converged"]), "max_residual": float(inf["max_residual"]),
+           "workload": "cfg3 (BASELINE.json configs[2]): one series N=2^20 L=2^19 k=32, decompose + reconstruct",
+           "roofline": {"bound": "hbm", "achieved": byt / (ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
+                        "frac": byt / (ms * 1e-3) / 1e9 / peak, "alg_bytes": byt}}
+    plan.close()
+    del x, U, V, G
     torch.cuda.empty_cache()
     return res
 
@@ -479,6 +537,7 @@ def main():
         torch.cuda.empty_cache()
         line["matvec_cfg4"] = micro_matvec(P, peak)
         line["hankelize_cfg5"] = micro_hankelize(P, peak)
+        line["decompose_cfg3"] = micro_decompose_cfg3(P, peak)
     if rank == 0 and not args.no_cpu_baseline:
         cores = os.cpu_count() or 1
         rate, desc, wall = oracle_sample(cores)

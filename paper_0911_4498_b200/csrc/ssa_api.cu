@@ -126,6 +126,9 @@ static void free_plan(Plan& p) {
     if (p.sub[i]) ssa_plan_destroy(reinterpret_cast<ssa_plan_t>(p.sub[i]));
   for (int i = 0; i < 3; ++i)
     if (p.hs[i]) cudaStreamDestroy(p.hs[i]);
+  if (p.lg_aux) cudaStreamDestroy(p.lg_aux);
+  for (int i = 0; i < 2; ++i)
+    if (p.lg_ev[i]) cudaEventDestroy(p.lg_ev[i]);
   for (int i = 0; i < Plan::kMaxSlices + 2; ++i)
     if (p.hev[i]) cudaEventDestroy(p.hev[i]);
 }
@@ -313,20 +316,25 @@ extern "C" ssa_status ssa_plan_create(int64_t N, int64_t L, int32_t k, int64_t b
     e = cudaMemcpy(p.d_tw1, t1.data(), t1.size() * 16, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMemcpy(p.d_tw2, t2.data(), t2.size() * 16, cudaMemcpyHostToDevice);
     if (e == cudaSuccess) {
-      // four-step and pair-step twiddle tables in the order the kernels read them
+      // four-step twiddles as a two-level table W_H^e = TL[e mod 2^a] TH[e >> a]
+      // (a = ceil(log2 H / 2)) and the pair-step row factors W_M^A, A <= N1/2
       // (extended precision on the host, like every other table)
       const long double pi2 = 2.0L * 3.14159265358979323846264338327950288L;
-      std::vector<double2> t4((size_t)H), tp((size_t)(N1 / 2 + 1) * N2);
-      for (int64_t k1 = 0; k1 < N1; ++k1)
-        for (int64_t n2 = 0; n2 < N2; ++n2) {
-          const long double ang = pi2 * (long double)((n2 * k1) % H) / (long double)H;
-          t4[(size_t)(n2 + N2 * k1)] = make_double2((double)cosl(ang), (double)(-sinl(ang)));
-        }
-      for (int64_t A = 0; A <= N1 / 2; ++A)
-        for (int64_t k2 = 0; k2 < N2; ++k2) {
-          const long double ang = pi2 * (long double)(A + N1 * k2) / (long double)M;
-          tp[(size_t)(A * N2 + k2)] = make_double2((double)cosl(ang), (double)(-sinl(ang)));
-        }
+      int logH = 0;
+      while ((1LL << logH) < H) ++logH;
+      const int64_t ntl = 1LL << ((logH + 1) / 2), nth = H / ntl;
+      std::vector<double2> t4, tp;
+      for (int64_t j = 0; j < ntl + nth; ++j) {
+        const long double e = (j < ntl) ? (long double)j : (long double)((j - ntl) * ntl);
+        const long double ang = pi2 * e / (long double)H;
+        t4.push_back(make_double2((double)cosl(ang), (double)(-sinl(ang))));
+      }
+      if ((int64_t)t4.size() != ssa::large_twh_entries(logH)) t4.clear();
+      for (int64_t A = 0; A <= N1 / 2; ++A) {
+        const long double ang = pi2 * (long double)A / (long double)M;
+        tp.push_back(make_double2((double)cosl(ang), (double)(-sinl(ang))));
+      }
+      if (t4.empty()) { st = fail(SSA_ERR_INTERNAL, "four-step table layout mismatch"); goto bad; }
       if ((st = alloc((void**)&p.d_tw4, t4.size() * 16, "four-step twiddles")) != SSA_OK) goto bad;
       if ((st = alloc((void**)&p.d_twp, tp.size() * 16, "pair twiddles")) != SSA_OK) goto bad;
       e = cudaMemcpy(p.d_tw4, t4.data(), t4.size() * 16, cudaMemcpyHostToDevice);
@@ -334,8 +342,8 @@ extern "C" ssa_status ssa_plan_create(int64_t N, int64_t L, int32_t k, int64_t b
     }
     if (e == cudaSuccess) e = ssa::large_set_attributes(N1, N2);
     if (e != cudaSuccess) { st = cuda_fail(e, "large FFT setup"); goto bad; }
-    // work buffers: ~128 MB, at least 2 items (hankelization needs a pair)
-    p.lbuf_items = (int)std::max<int64_t>(2, std::min<int64_t>(64, ((int64_t)128 << 20) / (H * 16)));
+    // work buffers: ~512 MB, at least 2 items (hankelization needs a pair)
+    p.lbuf_items = (int)std::max<int64_t>(2, std::min<int64_t>(256, ((int64_t)512 << 20) / (H * 16)));
     if ((st = alloc((void**)&p.d_lbuf, (size_t)p.lbuf_items * H * 16, "large FFT buffers")) != SSA_OK) goto bad;
   } else if (H > ssa::kMaxHankelSmemH) {
     p.hank_slots = p.sms;

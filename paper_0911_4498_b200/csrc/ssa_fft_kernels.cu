@@ -10,6 +10,11 @@
 // which is Alg. 2 / Alg. 3 (circulant embedding + backward identity) with the reversal
 // folded into the conjugate and the output slice of Alg. 3 read as p'_L..p'_N.
 #include "device_common.cuh"
+#include "fft_reg.cuh"
+
+#include <stdlib.h>
+
+#include <algorithm>
 
 namespace ssa {
 
@@ -69,6 +74,43 @@ __global__ void __launch_bounds__(kThreads) matvec_kernel(const double2* __restr
   correlate_cta(
       buf, sh, tw, spec + (size_t)b * (H + 1), n_in, n_out, [&](int i) { return __ldg(xb + i); },
       [&](int t, double v) { yb[t] = v; });
+}
+
+// H = 4096 (BASELINE config 4): register-resident radix-16 correlation (fft_reg.cuh).
+// Persistent CTAs (2 per SM); the next item's x is copied into a shared-memory stage by
+// cp.async and its spectrum pulled into L2 while the current item is transformed.
+__device__ __forceinline__ void cp_async8(double* dst, const double* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__global__ void __launch_bounds__(kThreads, 2) matvec4096_kernel(const double2* __restrict__ spec, int n_in, int n_out,
+                                                                 const double2* __restrict__ T,
+                                                                 const double* __restrict__ x, double* __restrict__ y,
+                                                                 int nitems) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double2* buf = reinterpret_cast<double2*>(smem_raw);
+  double2* t2 = buf + 4096;
+  double* stage = reinterpret_cast<double*>(t2 + 256);
+  const TwSmem tw = load_tw2(T, reinterpret_cast<double2*>(stage + kReg4096StageDoubles), 8192);
+  auto fetch = [&](int item) {
+    if (item < nitems) {
+      const double* src = x + (size_t)item * n_in;
+      for (int i = threadIdx.x; i < n_in; i += kThreads) cp_async8(stage + i, src + i);
+      const double2* sp = spec + (size_t)item * 4097;
+      for (int i = threadIdx.x; i < 513; i += kThreads) asm volatile("prefetch.global.L2 [%0];" ::"l"(sp + 8 * i));
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  fetch(blockIdx.x);
+  __syncthreads();
+  reg4096_tables(t2, tw);
+  for (int item = blockIdx.x; item < nitems; item += gridDim.x) {
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncthreads();
+    double* yb = y + (size_t)item * n_out;
+    correlate_reg4096(
+        buf, t2, tw, stage, spec + (size_t)item * 4097, n_in, n_out, [&]() { fetch(item + gridDim.x); },
+        [&](int t, double v) { yb[t] = v; });
+  }
 }
 
 // g_t = sigma * (u' * v')_t / c_t, c_t = min(t, L, K, N-t+1), t = 1..N  (PAPER.md:751-785,
@@ -167,6 +209,7 @@ __global__ void __launch_bounds__(kThreads) hankelize_kernel(const double* __res
 
 static size_t tw_smem(int H) { return (size_t)tw2_entries(2 * H) * 16; }
 static size_t fft_smem(int H) { return (size_t)fft_elems(H) * 16 + tw_smem(H); }
+static size_t reg4096_smem() { return (size_t)kReg4096SmemElems * 16 + kReg4096StageDoubles * 8 + tw_smem(4096); }
 static size_t fft_smem2(int H) { return (size_t)2 * fft_elems(H) * 16 + tw_smem(H); }
 
 cudaError_t fft_set_attributes(int H, const char** which) {
@@ -176,6 +219,8 @@ cudaError_t fft_set_attributes(int H, const char** which) {
   if ((e = raise_smem_limit(spectrum_kernel, (int)s1))) return e;
   *which = "matvec_kernel";
   if ((e = raise_smem_limit(matvec_kernel, (int)s1))) return e;
+  *which = "matvec4096_kernel";
+  if (H == 4096 && (e = raise_smem_limit(matvec4096_kernel, (int)reg4096_smem()))) return e;
   *which = "hankelize_kernel<BIG>";
   if ((e = raise_smem_limit(hankelize_kernel<true>, (int)s1))) return e;
   *which = "hankelize_kernel";
@@ -188,6 +233,7 @@ cudaError_t fft_set_attributes(int H, const char** which) {
   const int carve = cudaSharedmemCarveoutMaxShared;
   if ((e = cudaFuncSetAttribute(spectrum_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, carve))) return e;
   if ((e = cudaFuncSetAttribute(matvec_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, carve))) return e;
+  if ((e = cudaFuncSetAttribute(matvec4096_kernel, cudaFuncAttributePreferredSharedMemoryCarveout, carve))) return e;
   if ((e = cudaFuncSetAttribute(hankelize_kernel<true>, cudaFuncAttributePreferredSharedMemoryCarveout, carve))) return e;
   if ((e = cudaFuncSetAttribute(hankelize_kernel<false>, cudaFuncAttributePreferredSharedMemoryCarveout, carve)))
     return e;
@@ -203,6 +249,11 @@ cudaError_t launch_matvec(const Plan& p, const double2* spec, const double* x, d
                           cudaStream_t s) {
   int n_in = transpose ? (int)p.L : (int)p.K;
   int n_out = transpose ? (int)p.K : (int)p.L;
+  if (p.H == 4096 && n_in <= 4097 && !getenv("SSA_MATVEC_SMEM")) {
+    const int grid = (int)std::min<int64_t>(p.batch, 2 * (int64_t)p.sms);
+    matvec4096_kernel<<<grid, kThreads, reg4096_smem(), s>>>(spec, n_in, n_out, p.d_twl, x, y, (int)p.batch);
+    return cudaGetLastError();
+  }
   matvec_kernel<<<(unsigned)p.batch, kThreads, fft_smem((int)p.H), s>>>(spec, (int)p.H, n_in, n_out, p.d_twl, x, y);
   return cudaGetLastError();
 }

@@ -70,8 +70,11 @@ struct Plan {
   bool large = false;
   double2* d_tw1 = nullptr;      // two-level table for the N1-point sub-FFTs (M = 2 N1)
   double2* d_tw2 = nullptr;      // two-level table for the N2-point sub-FFTs (M = 2 N2)
-  double2* d_tw4 = nullptr;      // four-step twiddles W_H^{n2 k1} at [n2 + N2 k1]
-  double2* d_twp = nullptr;      // pair-step twiddles W_M^{A + N1 k2} at [A N2 + k2], A <= N1/2
+  double2* d_tw4 = nullptr;      // four-step twiddles: two-level W_H table (large_twh_entries)
+  double2* d_twp = nullptr;      // pair-step row factors W_M^A, A <= N1/2
+  int hank_per = 64;             // terms per four-step hankelization batch
+  cudaStream_t lg_aux = nullptr; // second stream: alternate hankelization batches overlap
+  cudaEvent_t lg_ev[2] = {};     // fork / join events of lg_aux
   double2* d_lbuf = nullptr;     // [lbuf_items][H] complex work buffers
   int lbuf_items = 0;
   double* d_lgsc = nullptr;      // device scalars (LgScalars)
@@ -145,13 +148,14 @@ cudaError_t launch_ritz(const Plan& p, const DecomposeArgs& a, cudaStream_t s);
 // long-series path (ssa_large_fft.cu, ssa_large_lanczos.cu)
 constexpr int kMaxLargeH = 1 << 20;  // N1, N2 <= 1024
 void large_geom(const Plan& p, int* N1, int* N2);
+int large_twh_entries(int logH);
 cudaError_t large_set_attributes(int N1, int N2);
 cudaError_t large_lanczos_set_attributes(int m_max);
 cudaError_t large_spectrum(const Plan& p, const double* series, double2* spec, int items, cudaStream_t s);
 cudaError_t large_correlate(const Plan& p, const double2* spec, size_t spec_stride, const double* x, size_t xs, int n_in,
                             double* out, size_t os, int n_out, int ld_out, const double* prev, size_t ps,
                             const double* coef, double* part, int items, cudaStream_t s);
-cudaError_t large_hankelize(const Plan& p, const double* sigma, const double* U, const double* V, size_t nterm_total,
+cudaError_t large_hankelize(Plan& p, const double* sigma, const double* U, const double* V, size_t nterm_total,
                             double* out, cudaStream_t s);
 cudaError_t large_decompose_one(Plan& p, const DecomposeArgs& a, int b, cudaStream_t s);
 

@@ -5,17 +5,21 @@
 // n = n2 + N2 n1, frequency k = k1 + N1 k2:
 //   X_{k1+N1k2} = sum_{n2} W_N2^{n2 k2} [ W_H^{n2 k1} sum_{n1} z_{n2+N2n1} W_N1^{n1 k1} ]
 // (the DFT of PAPER.md:473-509 evaluated by the Cooley-Tukey four-step split).
-//   large_col_fwd   N1-point column FFTs (one warp per column, 8 columns per CTA, shared
-//                   memory) + twiddle W_H^{n2 k1}; writes Y[n2 + N2 k1] (global, L2).
-//   large_row_pair  rows k1 and N1-k1 together: N2-point row FFTs, the real-FFT split
-//                   step on the pairs (p, H-p) -- spectrum output, correlation with a
-//                   stored spectrum (Algs. 2/3) or the product of two
-//                   spectra (Alg. 4) -- then inverse row FFTs and the
-//                   conjugate twiddle.
-//   large_col_inv   inverse N1-point column FFTs, unpacking y_2n + i y_2n+1 with an
-//                   epilogue (correlation output / Hankelization weights 1/c_t).
-// The work buffers are [items][H] complex in global memory; for one item they are
-// 8 MB (cfg3) or 2 MB (cfg5), so the three passes run out of L2.
+//   lg_col_fwd   N1-point column FFTs (one warp per column, 8 columns per CTA, shared
+//                memory) + twiddle W_H^{n2 k1}; writes Y[n2 + N2 k1] (global, L2).  One
+//                launch can transform two inputs (blockIdx.z: the u and v of a term).
+//   lg_row_*     rows k1 and N1-k1 together: N2-point row FFTs, the real-FFT split step on
+//                the pairs (p, H-p) -- spectrum output, correlation with a stored spectrum
+//                (Algs. 2/3) or the product of two spectra (Alg. 4,
+//                PAPER.md:807-824) -- then inverse row FFTs and the conjugate twiddle.
+//   lg_col_inv   inverse N1-point column FFTs, unpacking y_2n + i y_2n+1 with an epilogue
+//                (correlation output / Hankelization weights 1/c_t).
+// Every shape is a compile-time constant (one switch on log2 H per launch), so the
+// global loads of a thread are unrolled and all in flight together.  Twiddles come from
+// small tables: W_H^e = TL[e mod 2^a] TH[e >> a] (a = ceil(log2 H / 2), global, L1-resident),
+// W_M^{A + N1 k2} = W_M^A W_{2 N2}^{k2}; all tables are computed on the host in extended
+// precision.  The work buffers are [items][H] complex in global memory; for one item they
+// are 8 MB (cfg3) or 2 MB (cfg5), so the passes run out of L2.
 #include <stdlib.h>
 
 #include <algorithm>
@@ -29,48 +33,110 @@ constexpr int kColW = 8;  // columns per CTA in the column passes (one warp each
 struct WarpSync {
   __device__ __forceinline__ void operator()() const { __syncwarp(); }
 };
+// Named barrier over 64 threads (two warps); ids 1..15 (0 is __syncthreads).
+struct NamedSync64 {
+  int id;
+  __device__ __forceinline__ void operator()() const { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
+};
 
-// rev_index for a sub-FFT shape
-__device__ __forceinline__ int subrev(const FftShape& s, int k) { return rev_index(s, k); }
+// Compile-time four-step geometry for H = 2^LOGH.
+template <int LOGH>
+struct Geo {
+  static constexpr int H = 1 << LOGH;
+  static constexpr int L1 = LOGH / 2, N1 = 1 << L1;  // column length
+  static constexpr int L2 = LOGH - L1, N2 = 1 << L2;  // row length
+  static constexpr int TA = (LOGH + 1) / 2;           // W_H two-level split
+  static constexpr int NTL = 1 << TA, NTH = H >> TA;
+  static constexpr int NTW = NTL + NTH;               // entries of the W_H table
+};
 
-// exp(-2 pi i e / H) for any integer e, from the M-table T (M = 2H): index 2e mod M.
-__device__ __forceinline__ double2 twH(const double2* __restrict__ T, long long e, int H) {
-  long long t = (2 * e) % (2LL * H);
-  return twiddle(T, (int)t, H);
+int large_twh_entries(int logH) { return (1 << ((logH + 1) / 2)) + (1 << (logH - (logH + 1) / 2)); }
+
+// W_H^e for any integer e >= 0 from the two-level table (global memory, L1-resident:
+// 12-32 KB shared by every CTA of the SM).
+template <int LOGH>
+__device__ __forceinline__ double2 twH(const double2* __restrict__ th, long long e) {
+  using G = Geo<LOGH>;
+  const int t = (int)(e & (G::H - 1));
+  return cmul(__ldg(th + (t & (G::NTL - 1))), __ldg(th + G::NTL + (t >> G::TA)));
+}
+
+// f(j, W_H^{e0 + d j}) for j = 0..n-1: one table lookup per 8 values, then products by
+// W_H^d (chains of at most 7 products: each twiddle within a few ulp).
+template <int LOGH, int NMAX, class F>
+__device__ __forceinline__ void twiddle_seq(const double2* __restrict__ th, long long e0, long long d, int n, F f) {
+  const double2 step = twH<LOGH>(th, d);
+#pragma unroll
+  for (int g = 0; g < NMAX; g += 8) {
+    double2 w = twH<LOGH>(th, e0 + d * g);
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj) {
+      if (g + jj < NMAX && g + jj < n) {
+        f(g + jj, w);
+        if (jj < 7) w = cmul(w, step);
+      }
+    }
+  }
 }
 
 // ---- pass 1: forward column FFTs on packed real input x (len n_in) -------------------
-// grid (N2 / kColW, items); x item stride xs; Y item stride H.
-__global__ void __launch_bounds__(kThreads) large_col_fwd(const double* __restrict__ x, size_t xs, int n_in, int H,
-                                                          int N1, int N2, const double2* __restrict__ T4,
-                                                          const double2* __restrict__ T1, double2* __restrict__ Y) {
+struct ColFwdIn {
+  const double* x;  // [items][xs] real
+  size_t xs;
+  int n_in;
+  double2* Y;       // [items][H]
+  int vec;          // x and xs 16-byte aligned: pairs (x_2n, x_2n+1) as one 16-byte load
+};
+struct ColFwdArgs {
+  ColFwdIn in[2];   // blockIdx.z selects
+};
+
+template <int LOGH>
+__global__ void __launch_bounds__(kThreads) lg_col_fwd(ColFwdArgs args, const double2* __restrict__ T1,
+                                                       const double2* __restrict__ TWH) {
+  using G = Geo<LOGH>;
+  constexpr int N1 = G::N1, N2 = G::N2, CS = N1 + 1;  // odd column stride (16-byte units)
+  constexpr int NE = (N1 * kColW + kThreads - 1) / kThreads;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double2* buf = reinterpret_cast<double2*>(smem_raw);
-  const int cs = N1 + 1;  // odd stride (16-byte units): interleaved column loads are conflict-free
-  const TwSmem tw1 = load_tw2(T1, buf + kColW * cs, 2 * N1);
-  const FftShape s1 = make_shape(N1);
+  const double2* th = TWH;
+  const TwSmem tw1 = load_tw2(T1, buf + kColW * CS, 2 * N1);
+  const ColFwdIn a = blockIdx.z ? args.in[1] : args.in[0];
   const int n2_0 = blockIdx.x * kColW;
-  const double* xi = x + (size_t)blockIdx.y * xs;
-  double2* Yi = Y + (size_t)blockIdx.y * H;
-  for (int idx = threadIdx.x; idx < N1 * kColW; idx += blockDim.x) {
+  const double* xi = a.x + (size_t)blockIdx.y * a.xs;
+  double2* Yi = a.Y + (size_t)blockIdx.y * G::H;
+  double2 v[NE];
+#pragma unroll
+  for (int j = 0; j < NE; ++j) {
+    const int idx = threadIdx.x + j * kThreads;
     const int c = idx & (kColW - 1), n1 = idx >> 3;
-    const long long n = (long long)(n2_0 + c) + (long long)N2 * n1;
-    const long long i0 = 2 * n;
-    double a = (i0 < n_in) ? __ldg(xi + i0) : 0.0;
-    double b = (i0 + 1 < n_in) ? __ldg(xi + i0 + 1) : 0.0;
-    buf[c * cs + fsw(n1)] = make_double2(a, b);
+    const long long i0 = 2 * ((long long)(n2_0 + c) + (long long)N2 * n1);
+    const bool ok = idx < N1 * kColW;
+    if (a.vec && ok && i0 + 1 < a.n_in) {
+      v[j] = __ldg(reinterpret_cast<const double2*>(xi + i0));
+    } else {
+      v[j].x = (ok && i0 < a.n_in) ? __ldg(xi + i0) : 0.0;
+      v[j].y = (ok && i0 + 1 < a.n_in) ? __ldg(xi + i0 + 1) : 0.0;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < NE; ++j) {
+    const int idx = threadIdx.x + j * kThreads;
+    if (idx < N1 * kColW) buf[(idx & (kColW - 1)) * CS + fsw(idx >> 3)] = v[j];
   }
   __syncthreads();
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  fft_forward(buf + w * cs, s1, tw1, lane, 32, WarpSync());
+  fft_run_t<G::L1, false>(buf + w * CS, tw1, lane, 32, WarpSync());
   __syncthreads();
-  for (int idx = threadIdx.x; idx < N1 * kColW; idx += blockDim.x) {
-    const int c = idx & (kColW - 1), k1 = idx >> 3;
-    const int n2 = n2_0 + c;
-    double2 v = buf[c * cs + fsw(subrev(s1, k1))];
-    v = cmul(v, __ldg(T4 + (size_t)n2 + (size_t)N2 * k1));  // W_H^{n2 k1}, same index as Y
-    Yi[(size_t)n2 + (size_t)N2 * k1] = v;
-  }
+  // element j: column c = t & 7, k1 = (t >> 3) + (256 / 8) j; twiddle W_H^{n2 k1}
+  const int c = threadIdx.x & (kColW - 1), k0 = threadIdx.x >> 3;
+  const int n2 = n2_0 + c;
+  const int nval = (N1 * kColW - threadIdx.x + kThreads - 1) / kThreads;
+  twiddle_seq<LOGH, NE>(th, (long long)n2 * k0, (long long)n2 * (kThreads / kColW), nval, [&](int j, double2 w) {
+    const int k1 = k0 + (kThreads / kColW) * j;
+    const double2 z = buf[c * CS + fsw(rev_t<G::L1>(k1))];
+    Yi[(size_t)n2 + (size_t)N2 * k1] = cmul(z, w);
+  });
 }
 
 // ---- pass 3: inverse column FFTs + epilogue ------------------------------------------
@@ -78,7 +144,7 @@ __global__ void __launch_bounds__(kThreads) large_col_fwd(const double* __restri
 // ld_out; partial sum of squares per CTA into part[blockIdx]) ; 1 hankelization
 // (out[t] = sigma * y_t / c_t, t < N).
 struct ColInvArgs {
-  int H, N1, N2, mode;
+  int mode;
   int n_out, ld_out;           // correlation output length and padded row length
   size_t out_stride;           // item stride of out
   double* out;
@@ -90,79 +156,105 @@ struct ColInvArgs {
   int N, L, K;                 // hankelization: weights
 };
 
-__global__ void __launch_bounds__(kThreads) large_col_inv(const double2* __restrict__ Y, const double2* __restrict__ T1,
-                                                          ColInvArgs a) {
+template <int LOGH>
+__global__ void __launch_bounds__(kThreads) lg_col_inv(const double2* __restrict__ Y, const double2* __restrict__ T1,
+                                                       ColInvArgs a) {
+  using G = Geo<LOGH>;
+  constexpr int N1 = G::N1, N2 = G::N2, CS = N1 + 1;
+  constexpr int NE = (N1 * kColW + kThreads - 1) / kThreads;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double2* buf = reinterpret_cast<double2*>(smem_raw);
   __shared__ double red[kWarps];
-  const int H = a.H, N1 = a.N1, N2 = a.N2;
-  const int cs = N1 + 1;  // odd stride (16-byte units): interleaved column loads are conflict-free
-  const TwSmem tw1 = load_tw2(T1, buf + kColW * cs, 2 * N1);
-  const FftShape s1 = make_shape(N1);
+  const TwSmem tw1 = load_tw2(T1, buf + kColW * CS, 2 * N1);
   const int n2_0 = blockIdx.x * kColW;
   const size_t item = blockIdx.y;
-  const double2* Yi = Y + item * H;
-  for (int idx = threadIdx.x; idx < N1 * kColW; idx += blockDim.x) {
-    const int c = idx & (kColW - 1), k1 = idx >> 3;
-    buf[c * cs + fsw(subrev(s1, k1))] = Yi[(size_t)(n2_0 + c) + (size_t)N2 * k1];
+  const double2* Yi = Y + item * G::H;
+  double2 v[NE];
+#pragma unroll
+  for (int j = 0; j < NE; ++j) {
+    const int idx = threadIdx.x + j * kThreads;
+    if (idx < N1 * kColW) v[j] = Yi[(size_t)(n2_0 + (idx & (kColW - 1))) + (size_t)N2 * (idx >> 3)];
+  }
+#pragma unroll
+  for (int j = 0; j < NE; ++j) {
+    const int idx = threadIdx.x + j * kThreads;
+    if (idx < N1 * kColW) buf[(idx & (kColW - 1)) * CS + fsw(rev_t<G::L1>(idx >> 3))] = v[j];
   }
   __syncthreads();
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  fft_inverse(buf + w * cs, s1, tw1, lane, 32, WarpSync());
+  fft_run_t<G::L1, true>(buf + w * CS, tw1, lane, 32, WarpSync());
   __syncthreads();
-  const double invH = 1.0 / (double)H;
+  constexpr double invH = 1.0 / (double)G::H;
   double ss = 0.0;
   const double cf = (a.mode == 0 && a.coef) ? a.coef[item] : 0.0;
   const double sg = (a.mode == 1) ? a.sigma[item] : 0.0;
   const int mn = a.L < a.K ? a.L : a.K;
-  for (int idx = threadIdx.x; idx < N1 * kColW * 2; idx += blockDim.x) {
-    // element t = 2n + h of the real output, n = n2 + N2 n1
-    const int h = idx & 1, rest = idx >> 1;
-    const int c = rest & (kColW - 1), n1 = rest >> 3;
-    const long long n = (long long)(n2_0 + c) + (long long)N2 * n1;
-    const long long t = 2 * n + h;
-    const double2 z = buf[c * cs + fsw(n1)];
-    const double y = (h ? z.y : z.x) * invH;
-    if (a.mode == 0) {
-      if (t < a.ld_out) {
-        double v = 0.0;
-        if (t < a.n_out) {
-          v = y;
-          if (a.prev) v -= cf * a.prev[item * a.prev_stride + t];
+  constexpr int NO = (2 * N1 * kColW + kThreads - 1) / kThreads;
+  if (a.mode == 0) {
+    const double* pv = a.prev ? a.prev + item * a.prev_stride : nullptr;
+    double pr[NO];
+#pragma unroll
+    for (int j = 0; j < NO; ++j) {  // previous-vector loads first, all in flight
+      const int idx = threadIdx.x + j * kThreads;
+      const int h = idx & 1, rest = idx >> 1;
+      const long long t = 2 * ((long long)(n2_0 + (rest & (kColW - 1))) + (long long)N2 * (rest >> 3)) + h;
+      pr[j] = (pv && idx < 2 * N1 * kColW && t < a.n_out) ? __ldg(pv + t) : 0.0;
+    }
+#pragma unroll
+    for (int j = 0; j < NO; ++j) {
+      const int idx = threadIdx.x + j * kThreads;
+      if (idx < 2 * N1 * kColW) {
+        // element t = 2n + h of the real output, n = n2 + N2 n1
+        const int h = idx & 1, rest = idx >> 1;
+        const int c = rest & (kColW - 1), n1 = rest >> 3;
+        const long long t = 2 * ((long long)(n2_0 + c) + (long long)N2 * n1) + h;
+        const double2 z = buf[c * CS + fsw(n1)];
+        if (t < a.ld_out) {
+          double y = 0.0;
+          if (t < a.n_out) y = fma(-cf, pr[j], (h ? z.y : z.x) * invH);
+          a.out[item * a.out_stride + t] = y;
+          ss = fma(y, y, ss);
         }
-        a.out[item * a.out_stride + t] = v;
-        ss = fma(v, v, ss);
-      }
-    } else {
-      if (t < a.N) {
-        const long long k1 = t + 1;
-        long long cnt = k1;
-        if (cnt > mn) cnt = mn;
-        if (a.N - k1 + 1 < cnt) cnt = a.N - k1 + 1;
-        a.out[item * a.out_stride + t] = sg * y / (double)cnt;
       }
     }
-  }
-  if (a.mode == 0 && a.part) {
-    ss = warp_sum(ss);
-    if (lane == 0) red[w] = ss;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double s = 0.0;
-      for (int i = 0; i < kWarps; ++i) s += red[i];
-      a.part[item * gridDim.x + blockIdx.x] = s;
+    if (a.part) {
+      ss = warp_sum(ss);
+      if (lane == 0) red[w] = ss;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int i = 0; i < kWarps; ++i) s += red[i];
+        a.part[item * gridDim.x + blockIdx.x] = s;
+      }
+    }
+  } else {
+    double* o = a.out + item * a.out_stride;
+#pragma unroll
+    for (int j = 0; j < NO; ++j) {
+      const int idx = threadIdx.x + j * kThreads;
+      if (idx < 2 * N1 * kColW) {
+        const int h = idx & 1, rest = idx >> 1;
+        const int c = rest & (kColW - 1), n1 = rest >> 3;
+        const long long t = 2 * ((long long)(n2_0 + c) + (long long)N2 * n1) + h;
+        if (t < a.N) {
+          const double2 z = buf[c * CS + fsw(n1)];
+          const long long k1 = t + 1;
+          long long cnt = k1;
+          if (cnt > mn) cnt = mn;
+          if (a.N - k1 + 1 < cnt) cnt = a.N - k1 + 1;
+          o[t] = sg * ((h ? z.y : z.x) * invH) / (double)cnt;
+        }
+      }
     }
   }
 }
 
 // ---- pass 2: row pairs ----------------------------------------------------------------
-// Row index r = blockIdx.x in [0, N1/2]: rows A = r and B = N1 - r (B == A for r = 0 and
-// r = N1/2).  Modes: 0 spectrum (write F^[0..H] natural order), 1 correlation with F^,
-// 2 product of the spectra of two buffers (Ya * Yb, result in Yb).
+// Row A in [0, N1/2] with its partner B = N1 - A (B == A for A = 0 and A = N1/2).  Modes:
+// 0 spectrum (write F^[0..H] natural order), 1 correlation with F^, 2 product of the
+// spectra of two buffers (Ya * Yb, result in Yb).
 struct RowArgs {
-  int H, N1, N2, mode;
-  const double2* T4;    // W_H^{n2 k1} at [n2 + N2 k1]
-  const double2* Tp;    // W_M^{A + N1 k2} at [A N2 + k2], A <= N1/2
+  int mode;
   double2* Ya;          // buffer of the (first) vector, [items][H]
   double2* Yb;          // mode 2: second buffer
   const double2* spec;  // mode 1: F^ [items or 1][H+1]
@@ -174,51 +266,27 @@ __device__ __forceinline__ int partner_k2(int A, int k2, int N2) {
   return (A == 0) ? ((N2 - k2) & (N2 - 1)) : (N2 - 1 - k2);
 }
 
-// Row pairs, CTA-wide FFTs (modes 0/1: one item at a time, 257..513 CTAs of 256 threads
-// keep the GPU busier than warp-level rows would).
-__global__ void __launch_bounds__(kThreads) large_row_pair_cta(const double2* __restrict__ T, const double2* __restrict__ T2,
-                                                           RowArgs a) {
-  extern __shared__ __align__(128) unsigned char smem_raw[];
-  const int H = a.H, N1 = a.N1, N2 = a.N2;
-  const int rs = fft_elems(N2);
-  double2* bA = reinterpret_cast<double2*>(smem_raw);  // row A of Ya
-  double2* bB = bA + rs;                                // row B of Ya
-  double2* cA = bB + rs;                                // mode 2: row A of Yb
-  double2* cB = cA + rs;                                // mode 2: row B of Yb
-  const TwSmem tw2 = load_tw2(T2, cB + rs, 2 * N2);
-  const FftShape s2 = make_shape(N2);
-  const int A = blockIdx.x, B = (N1 - A) & (N1 - 1);
-  const bool two = (A != B);
-  const size_t item = blockIdx.y;
-  double2* Ya = a.Ya + item * H;
-  double2* Yb = (a.mode == 2) ? a.Yb + item * H : nullptr;
-  for (int i = threadIdx.x; i < N2; i += blockDim.x) {
-    bA[fsw(i)] = Ya[(size_t)A * N2 + i];
-    if (two) bB[fsw(i)] = Ya[(size_t)B * N2 + i];
-    if (a.mode == 2) {
-      cA[fsw(i)] = Yb[(size_t)A * N2 + i];
-      if (two) cB[fsw(i)] = Yb[(size_t)B * N2 + i];
-    }
-  }
-  __syncthreads();
-  fft_forward(bA, s2, tw2, threadIdx.x, blockDim.x, CtaSync());
-  if (two) fft_forward(bB, s2, tw2, threadIdx.x, blockDim.x, CtaSync());
-  if (a.mode == 2) {
-    fft_forward(cA, s2, tw2, threadIdx.x, blockDim.x, CtaSync());
-    if (two) fft_forward(cB, s2, tw2, threadIdx.x, blockDim.x, CtaSync());
-  }
-  // pairs (p, q = H - p): p = A + N1 k2 in row A, q in row B at partner_k2
+// The pair step for pairs k2 = k0, k0 + ks, ... of rows (rA, rB[, cA, cB]) already
+// transformed (digit-reversed).  WA = W_M^A; W_M^p = WA W_{2 N2}^{k2} (tw2).
+template <int LOGH>
+__device__ __forceinline__ void row_pair_step(const RowArgs& a, size_t item, int A, bool two, double2 WA,
+                                              const TwSmem& tw2, double2* rA, double2* rB, double2* cA, double2* cB,
+                                              int k0, int ks) {
+  using G = Geo<LOGH>;
+  constexpr int N1 = G::N1, N2 = G::N2, H = G::H;
   const int npairs = two ? N2 : ((A == 0) ? N2 / 2 + 1 : N2 / 2);
-  double2* rowB = two ? bB : bA;
+  double2* rowB = two ? rB : rA;
   double2* rowBc = two ? cB : cA;
   const double2* F = (a.mode == 1) ? a.spec + item * a.spec_stride : nullptr;
   double2* Fo = (a.mode == 0) ? a.spec_out + item * (size_t)(H + 1) : nullptr;
-  for (int k2 = threadIdx.x; k2 < npairs; k2 += blockDim.x) {
+  for (int k2 = k0; k2 < npairs; k2 += ks) {
     const int k2q = partner_k2(A, k2, N2);
-    const int pr = fsw(rev_index(s2, k2)), qr = fsw(rev_index(s2, k2q));
+    const int pr = fsw(rev_t<G::L2>(k2)), qr = fsw(rev_t<G::L2>(k2q));
     const long long p = (long long)A + (long long)N1 * k2;
     const long long q = (p == 0) ? H : H - p;
-    const double2 W = __ldg(a.Tp + (size_t)A * N2 + k2);  // exp(-2 pi i p / M), p = A + N1 k2
+    double2 Fp, Fq;
+    if (a.mode == 1) { Fp = __ldg(F + p); Fq = __ldg(F + q); }
+    const double2 W = cmul(WA, tw2(k2));  // exp(-2 pi i p / M), p = A + N1 k2
     auto split = [&](double2 Zp, double2 Zq, double2& Xp, double2& Xq) {
       double2 E = make_double2(0.5 * (Zp.x + Zq.x), 0.5 * (Zp.y - Zq.y));
       double2 D = make_double2(0.5 * (Zp.x - Zq.x), 0.5 * (Zp.y + Zq.y));
@@ -228,7 +296,7 @@ __global__ void __launch_bounds__(kThreads) large_row_pair_cta(const double2* __
       Xq = conjg(csub(E, WO));
     };
     double2 Xp, Xq;
-    split(bA[pr], rowB[qr], Xp, Xq);
+    split(rA[pr], rowB[qr], Xp, Xq);
     const bool same = (!two) && (pr == qr);
     if (a.mode == 0) {
       Fo[p] = Xp;
@@ -236,8 +304,8 @@ __global__ void __launch_bounds__(kThreads) large_row_pair_cta(const double2* __
     } else {
       double2 Yp, Yq;
       if (a.mode == 1) {
-        Yp = cmulc(__ldg(F + p), Xp);
-        Yq = cmulc(__ldg(F + q), Xq);
+        Yp = cmulc(Fp, Xp);
+        Yq = cmulc(Fq, Xq);
       } else {
         double2 Vp, Vq;
         split(cA[pr], rowBc[qr], Vp, Vq);
@@ -247,169 +315,268 @@ __global__ void __launch_bounds__(kThreads) large_row_pair_cta(const double2* __
       double2 E = make_double2(0.5 * (Yp.x + Yq.x), 0.5 * (Yp.y - Yq.y));
       double2 D = make_double2(0.5 * (Yp.x - Yq.x), 0.5 * (Yp.y + Yq.y));
       double2 O = cmulc(D, W);
-      double2* dA = (a.mode == 2) ? cA : bA;
+      double2* dA = (a.mode == 2) ? cA : rA;
       double2* dB = (a.mode == 2) ? rowBc : rowB;
       dA[pr] = make_double2(E.x - O.y, E.y + O.x);
       if (!same) dB[qr] = make_double2(E.x + O.y, O.x - E.y);
     }
   }
+}
+
+// Row pairs, CTA-wide FFTs (one item at a time: 257..513 CTAs of 256 threads keep the
+// GPU busier than warp-level rows would).  Smem: 4 rows, tw2, W_H table.
+template <int LOGH>
+__global__ void __launch_bounds__(kThreads) lg_row_cta(const double2* __restrict__ T2, const double2* __restrict__ TWH,
+                                                       const double2* __restrict__ TWA, RowArgs a) {
+  using G = Geo<LOGH>;
+  constexpr int N1 = G::N1, N2 = G::N2;
+  constexpr int NE = (N2 + kThreads - 1) / kThreads;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double2* bA = reinterpret_cast<double2*>(smem_raw);  // row A of Ya
+  double2* bB = bA + N2;                                // row B of Ya
+  double2* cA = bB + N2;                                // mode 2: row A of Yb
+  double2* cB = cA + N2;                                // mode 2: row B of Yb
+  const double2* th = TWH;
+  const TwSmem tw2 = load_tw2(T2, cB + N2, 2 * N2);
+  const int A = blockIdx.x, B = (N1 - A) & (N1 - 1);
+  const bool two = (A != B);
+  const size_t item = blockIdx.y;
+  double2* Ya = a.Ya + item * G::H;
+  double2* Yb = (a.mode == 2) ? a.Yb + item * G::H : nullptr;
+  const int nrows = (a.mode == 2 ? 2 : 1) * (two ? 2 : 1);
+  // all rows' loads in flight before the shared-memory stores
+  double2 v[4][NE];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const double2* src = ((r >> 1) ? Yb : Ya) + (size_t)((r & 1) ? B : A) * N2;
+    const bool use = (r >> 1) ? (a.mode == 2) : true;
+    const bool use2 = (r & 1) ? two : true;
+#pragma unroll
+    for (int j = 0; j < NE; ++j) {
+      const int i = threadIdx.x + j * kThreads;
+      if (use && use2 && i < N2) v[r][j] = src[i];
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    double2* dst = bA + r * N2;
+    const bool use = ((r >> 1) ? (a.mode == 2) : true) && ((r & 1) ? two : true);
+#pragma unroll
+    for (int j = 0; j < NE; ++j) {
+      const int i = threadIdx.x + j * kThreads;
+      if (use && i < N2) dst[fsw(i)] = v[r][j];
+    }
+  }
+  (void)nrows;
+  __syncthreads();
+  fft_run_t<G::L2, false>(bA, tw2, threadIdx.x, blockDim.x, CtaSync());
+  if (two) fft_run_t<G::L2, false>(bB, tw2, threadIdx.x, blockDim.x, CtaSync());
+  if (a.mode == 2) {
+    fft_run_t<G::L2, false>(cA, tw2, threadIdx.x, blockDim.x, CtaSync());
+    if (two) fft_run_t<G::L2, false>(cB, tw2, threadIdx.x, blockDim.x, CtaSync());
+  }
+  const double2 WA = __ldg(TWA + A);
+  row_pair_step<LOGH>(a, item, A, two, WA, tw2, bA, bB, cA, cB, threadIdx.x, blockDim.x);
   if (a.mode == 0) return;
   __syncthreads();
   double2* oA = (a.mode == 2) ? cA : bA;
   double2* oB = (a.mode == 2) ? cB : bB;
   double2* Yo = (a.mode == 2) ? Yb : Ya;
-  fft_inverse(oA, s2, tw2, threadIdx.x, blockDim.x, CtaSync());
-  if (two) fft_inverse(oB, s2, tw2, threadIdx.x, blockDim.x, CtaSync());
-  for (int n2 = threadIdx.x; n2 < N2; n2 += blockDim.x) {
-    Yo[(size_t)A * N2 + n2] = cmulc(oA[fsw(n2)], __ldg(a.T4 + (size_t)N2 * A + n2));
-    if (two) Yo[(size_t)B * N2 + n2] = cmulc(oB[fsw(n2)], __ldg(a.T4 + (size_t)N2 * B + n2));
-  }
+  fft_run_t<G::L2, true>(oA, tw2, threadIdx.x, blockDim.x, CtaSync());
+  if (two) fft_run_t<G::L2, true>(oB, tw2, threadIdx.x, blockDim.x, CtaSync());
+  const int nval = (N2 - (int)threadIdx.x + kThreads - 1) / kThreads;
+  twiddle_seq<LOGH, NE>(th, (long long)A * threadIdx.x, (long long)A * kThreads, nval, [&](int j, double2 w) {
+    const int n2 = threadIdx.x + j * kThreads;
+    Yo[(size_t)A * N2 + n2] = cmulc(oA[fsw(n2)], w);
+  });
+  if (two)
+    twiddle_seq<LOGH, NE>(th, (long long)B * threadIdx.x, (long long)B * kThreads, nval, [&](int j, double2 w) {
+      const int n2 = threadIdx.x + j * kThreads;
+      Yo[(size_t)B * N2 + n2] = cmulc(oB[fsw(n2)], w);
+    });
 }
 
 // Row pairs with warp-level FFTs: each CTA takes G = warps / R row pairs (R = rows per
-// pair: 2, or 4 in mode 2; G from the launch: 1 when one item must fill the GPU), warp g R + j loads and transforms row j of pair g on its own
+// pair: 2, or 4 in mode 2); warp g R + j loads and transforms row j of pair g on its own
 // (no CTA barrier inside the FFTs), the pair step runs on the 32 R threads of the pair,
 // and warps 0 / 1 of the pair run the inverse transforms of rows A / B and write them
-// back with the conjugate twiddle.
-__global__ void __launch_bounds__(kThreads) large_row_pair(const double2* __restrict__ T, const double2* __restrict__ T2,
-                                                           RowArgs a) {
+// back with the conjugate twiddle.  Smem: one row per warp, tw2, W_H table.
+template <int LOGH>
+__global__ void __launch_bounds__(kThreads) lg_row_warp(const double2* __restrict__ T2,
+                                                        const double2* __restrict__ TWH,
+                                                        const double2* __restrict__ TWA, RowArgs a) {
+  using Gm = Geo<LOGH>;
+  constexpr int N1 = Gm::N1, N2 = Gm::N2;
+  constexpr int NE = (N2 + 31) / 32;
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  const int H = a.H, N1 = a.N1, N2 = a.N2;
-  const int nw = blockDim.x >> 5;                         // warps = R rows x G pairs
+  constexpr int nw = kWarps;
   double2* rows = reinterpret_cast<double2*>(smem_raw);  // nw rows of N2
+  const double2* th = TWH;
   const TwSmem tw2 = load_tw2(T2, rows + (size_t)nw * N2, 2 * N2);
-  const FftShape s2 = make_shape(N2);
   const int R = (a.mode == 2) ? 4 : 2, G = nw / R;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int g = w / R, j = w - g * R;
   const int A = blockIdx.x * G + g, B = (N1 - A) & (N1 - 1);
   const bool valid = A <= N1 / 2, two = (A != B);
   const size_t item = blockIdx.y;
-  double2* Ya = a.Ya + item * H;
-  double2* Yb = (a.mode == 2) ? a.Yb + item * H : nullptr;
+  double2* Ya = a.Ya + item * Gm::H;
+  double2* Yb = (a.mode == 2) ? a.Yb + item * Gm::H : nullptr;
   double2* rA = rows + (size_t)(g * R) * N2;  // row A of Ya, row B of Ya, row A of Yb, row B of Yb
   double2* rB = rA + N2;
   double2* cA = rA + 2 * N2;
   double2* cB = rA + 3 * N2;
-  __syncthreads();  // twiddle table
   const bool mine = valid && (two || !(j & 1));
   if (mine) {
     const double2* src = ((j >> 1) ? Yb : Ya) + (size_t)((j & 1) ? B : A) * N2;
     double2* dst = rows + (size_t)w * N2;
-    for (int i = lane; i < N2; i += 32) dst[fsw(i)] = src[i];
-    __syncwarp();
-    fft_forward(dst, s2, tw2, lane, 32, WarpSync());
+    double2 v[NE];
+#pragma unroll
+    for (int e = 0; e < NE; ++e) {
+      const int i = lane + 32 * e;
+      if (i < N2) v[e] = src[i];
+    }
+#pragma unroll
+    for (int e = 0; e < NE; ++e) {
+      const int i = lane + 32 * e;
+      if (i < N2) dst[fsw(i)] = v[e];
+    }
   }
+  __syncthreads();  // tables
+  if (mine) fft_run_t<Gm::L2, false>(rows + (size_t)w * N2, tw2, lane, 32, WarpSync());
   __syncthreads();
   if (valid) {
-    // pairs (p, q = H - p): p = A + N1 k2 in row A, q in row B at partner_k2
-    const int npairs = two ? N2 : ((A == 0) ? N2 / 2 + 1 : N2 / 2);
-    double2* rowB = two ? rB : rA;
-    double2* rowBc = two ? cB : cA;
-    const double2* F = (a.mode == 1) ? a.spec + item * a.spec_stride : nullptr;
-    double2* Fo = (a.mode == 0) ? a.spec_out + item * (size_t)(H + 1) : nullptr;
-    for (int k2 = j * 32 + lane; k2 < npairs; k2 += 32 * R) {
-      const int k2q = partner_k2(A, k2, N2);
-      const int pr = fsw(rev_index(s2, k2)), qr = fsw(rev_index(s2, k2q));
-      const long long p = (long long)A + (long long)N1 * k2;
-      const long long q = (p == 0) ? H : H - p;
-      const double2 W = __ldg(a.Tp + (size_t)A * N2 + k2);  // exp(-2 pi i p / M), p = A + N1 k2
-      auto split = [&](double2 Zp, double2 Zq, double2& Xp, double2& Xq) {
-        double2 E = make_double2(0.5 * (Zp.x + Zq.x), 0.5 * (Zp.y - Zq.y));
-        double2 D = make_double2(0.5 * (Zp.x - Zq.x), 0.5 * (Zp.y + Zq.y));
-        double2 O = make_double2(D.y, -D.x);
-        double2 WO = cmul(W, O);
-        Xp = cadd(E, WO);
-        Xq = conjg(csub(E, WO));
-      };
-      double2 Xp, Xq;
-      split(rA[pr], rowB[qr], Xp, Xq);
-      const bool same = (!two) && (pr == qr);
-      if (a.mode == 0) {
-        Fo[p] = Xp;
-        Fo[q] = Xq;
-      } else {
-        double2 Yp, Yq;
-        if (a.mode == 1) {
-          Yp = cmulc(__ldg(F + p), Xp);
-          Yq = cmulc(__ldg(F + q), Xq);
-        } else {
-          double2 Vp, Vq;
-          split(cA[pr], rowBc[qr], Vp, Vq);
-          Yp = cmul(Xp, Vp);
-          Yq = cmul(Xq, Vq);
-        }
-        double2 E = make_double2(0.5 * (Yp.x + Yq.x), 0.5 * (Yp.y - Yq.y));
-        double2 D = make_double2(0.5 * (Yp.x - Yq.x), 0.5 * (Yp.y + Yq.y));
-        double2 O = cmulc(D, W);
-        double2* dA = (a.mode == 2) ? cA : rA;
-        double2* dB = (a.mode == 2) ? rowBc : rowB;
-        dA[pr] = make_double2(E.x - O.y, E.y + O.x);
-        if (!same) dB[qr] = make_double2(E.x + O.y, O.x - E.y);
-      }
-    }
+    const double2 WA = __ldg(TWA + A);
+    row_pair_step<LOGH>(a, item, A, two, WA, tw2, rA, rB, cA, cB, j * 32 + lane, 32 * R);
   }
   if (a.mode == 0) return;
   __syncthreads();
-  if (valid && j < 2 && (two || j == 0)) {
-    double2* o = (a.mode == 2) ? (j ? cB : cA) : (j ? rB : rA);
+  if (a.mode == 2) {
+    // inverse of rows A (warps 0, 1 of the group) and B (warps 2, 3) of Yb, two warps per
+    // row (named barrier per row): all four warps of the pair busy
+    const int half = j >> 1;
+    if (valid && (two || half == 0)) {
+      double2* o = half ? cB : cA;
+      const int row = half ? B : A;
+      double2* Yo = Yb + (size_t)row * N2;
+      const int tid64 = ((j & 1) << 5) | lane;
+      const NamedSync64 sync{1 + 2 * g + half};
+      fft_run_t<Gm::L2, true>(o, tw2, tid64, 64, sync);
+      constexpr int NE2 = (N2 + 63) / 64;
+      const int nval = (N2 - tid64 + 63) / 64;
+      twiddle_seq<LOGH, NE2>(th, (long long)row * tid64, (long long)row * 64, nval, [&](int e, double2 w) {
+        const int n2 = tid64 + 64 * e;
+        Yo[n2] = cmulc(o[fsw(n2)], w);
+      });
+    }
+  } else if (valid && j < 2 && (two || j == 0)) {
+    double2* o = j ? rB : rA;
     const int row = j ? B : A;
-    double2* Yo = ((a.mode == 2) ? Yb : Ya) + (size_t)row * N2;
-    fft_inverse(o, s2, tw2, lane, 32, WarpSync());
-    const double2* t4 = a.T4 + (size_t)N2 * row;  // W_H^{n2 row}
-    for (int n2 = lane; n2 < N2; n2 += 32) Yo[n2] = cmulc(o[fsw(n2)], __ldg(t4 + n2));
+    double2* Yo = Ya + (size_t)row * N2;
+    fft_run_t<Gm::L2, true>(o, tw2, lane, 32, WarpSync());
+    const int nval = (N2 - lane + 31) / 32;
+    twiddle_seq<LOGH, NE>(th, (long long)row * lane, (long long)row * 32, nval, [&](int e, double2 w) {
+      const int n2 = lane + 32 * e;
+      Yo[n2] = cmulc(o[fsw(n2)], w);
+    });
   }
 }
 
-size_t large_col_smem(int N1) { return ((size_t)kColW * (N1 + 1) + tw2_entries(2 * N1)) * 16; }
-size_t large_row_smem(int N2, int warps) {  // one row per warp, then the table
-  return ((size_t)warps * N2 + tw2_entries(2 * N2)) * 16;
+
+// ---- shared-memory sizes, attributes, dispatch ------------------------------------------
+static int ilog2(long long v) {
+  int l = 0;
+  while ((1LL << l) < v) ++l;
+  return l;
 }
-size_t large_row_cta_smem(int N2) { return ((size_t)4 * N2 + tw2_entries(2 * N2)) * 16; }
+static size_t col_smem(int logH) {
+  const int N1 = 1 << (logH / 2);
+  return ((size_t)kColW * (N1 + 1) + tw2_entries(2 * N1)) * 16;
+}
+static size_t row_cta_smem(int logH) {
+  const int N2 = 1 << (logH - logH / 2);
+  return ((size_t)4 * N2 + tw2_entries(2 * N2)) * 16;
+}
+static size_t row_warp_smem(int logH) {
+  const int N2 = 1 << (logH - logH / 2);
+  return ((size_t)kWarps * N2 + tw2_entries(2 * N2)) * 16;
+}
+
+#define SSA_LG_DISPATCH(logH, CALL)                                                               \
+  switch (logH) {                                                                                 \
+    case 6: CALL(6); break; case 7: CALL(7); break; case 8: CALL(8); break; case 9: CALL(9); break; \
+    case 10: CALL(10); break; case 11: CALL(11); break; case 12: CALL(12); break;                 \
+    case 13: CALL(13); break; case 14: CALL(14); break; case 15: CALL(15); break;                 \
+    case 16: CALL(16); break; case 17: CALL(17); break; case 18: CALL(18); break;                 \
+    case 19: CALL(19); break; default: CALL(20); break;                                           \
+  }
 
 cudaError_t large_set_attributes(int N1, int N2) {
-  cudaError_t e;
-  if ((e = raise_smem_limit(large_col_fwd, (int)large_col_smem(N1))))
-    return e;
-  if ((e = raise_smem_limit(large_col_inv, (int)large_col_smem(N1))))
-    return e;
-  if ((e = raise_smem_limit(large_row_pair_cta, (int)large_row_cta_smem(N2)))) return e;
-  if ((e = raise_smem_limit(large_row_pair, (int)large_row_smem(N2, kWarps))))
-    return e;
-  return cudaSuccess;
+  const int logH = ilog2((long long)N1 * N2);
+  cudaError_t e = cudaSuccess;
+#define SSA_LG_ATTR(LG)                                                                            \
+  do {                                                                                             \
+    if ((e = raise_smem_limit(lg_col_fwd<LG>, col_smem(LG)))) return e;                            \
+    if ((e = raise_smem_limit(lg_col_inv<LG>, col_smem(LG)))) return e;                            \
+    if ((e = raise_smem_limit(lg_row_cta<LG>, row_cta_smem(LG)))) return e;                        \
+    if ((e = raise_smem_limit(lg_row_warp<LG>, row_warp_smem(LG)))) return e;                      \
+  } while (0)
+  SSA_LG_DISPATCH(logH, SSA_LG_ATTR)
+#undef SSA_LG_ATTR
+  return e;
 }
 
 // ---- host-side drivers ----------------------------------------------------------------
-struct LargeGeom {
-  int H, N1, N2;
-};
-
 void large_geom(const Plan& p, int* N1, int* N2) {
-  int l = 0;
-  while ((1LL << l) < p.H) ++l;
+  const int l = ilog2(p.H);
   *N1 = 1 << (l / 2);
   *N2 = (int)(p.H / *N1);
 }
 
-static LargeGeom geom(const Plan& p) {
-  LargeGeom g;
-  g.H = (int)p.H;
-  int l = 0;
-  while ((1 << l) < g.H) ++l;
-  g.N1 = 1 << (l / 2);
-  g.N2 = g.H / g.N1;
-  return g;
+// rows of x (row stride xs doubles) start 16-byte aligned
+static int vec16(const double* x, size_t xs) { return ((reinterpret_cast<uintptr_t>(x) & 15) == 0) && (xs % 2 == 0); }
+
+static void col_fwd(const Plan& p, const ColFwdArgs& ca, int nz, int items, cudaStream_t s) {
+  const int logH = ilog2(p.H);
+  const int N2 = 1 << (logH - logH / 2);
+  const dim3 grid(N2 / kColW, items, nz);
+#define SSA_LG_CF(LG) lg_col_fwd<LG><<<grid, kThreads, col_smem(LG), s>>>(ca, p.d_tw1, p.d_tw4)
+  SSA_LG_DISPATCH(logH, SSA_LG_CF)
+#undef SSA_LG_CF
+}
+static void col_inv(const Plan& p, const double2* Y, const ColInvArgs& ca, int items, cudaStream_t s) {
+  const int logH = ilog2(p.H);
+  const int N2 = 1 << (logH - logH / 2);
+  const dim3 grid(N2 / kColW, items);
+#define SSA_LG_CI(LG) lg_col_inv<LG><<<grid, kThreads, col_smem(LG), s>>>(Y, p.d_tw1, ca)
+  SSA_LG_DISPATCH(logH, SSA_LG_CI)
+#undef SSA_LG_CI
+}
+static void rows(const Plan& p, const RowArgs& ra, int items, bool warp_rows, cudaStream_t s) {
+  const int logH = ilog2(p.H);
+  const int N1 = 1 << (logH / 2);
+  if (warp_rows) {
+    const int G = kWarps / (ra.mode == 2 ? 4 : 2);
+    const dim3 grid((N1 / 2 + G) / G, items);
+#define SSA_LG_RW(LG) lg_row_warp<LG><<<grid, kThreads, row_warp_smem(LG), s>>>(p.d_tw2, p.d_tw4, p.d_twp, ra)
+    SSA_LG_DISPATCH(logH, SSA_LG_RW)
+#undef SSA_LG_RW
+  } else {
+    const dim3 grid(N1 / 2 + 1, items);
+#define SSA_LG_RC(LG) lg_row_cta<LG><<<grid, kThreads, row_cta_smem(LG), s>>>(p.d_tw2, p.d_tw4, p.d_twp, ra)
+    SSA_LG_DISPATCH(logH, SSA_LG_RC)
+#undef SSA_LG_RC
+  }
 }
 
 cudaError_t large_spectrum(const Plan& p, const double* series, double2* spec, int items, cudaStream_t s) {
-  const LargeGeom g = geom(p);
   double2* Y = p.d_lbuf;
   for (int i0 = 0; i0 < items; i0 += p.lbuf_items) {
     const int ni = std::min(items - i0, p.lbuf_items);
-    large_col_fwd<<<dim3(g.N2 / kColW, ni), kThreads, large_col_smem(g.N1), s>>>(
-        series + (size_t)i0 * p.N, (size_t)p.N, (int)p.N, g.H, g.N1, g.N2, p.d_tw4, p.d_tw1, Y);
-    RowArgs ra{g.H, g.N1, g.N2, 0, p.d_tw4, p.d_twp, Y, nullptr, nullptr, 0, spec + (size_t)i0 * (g.H + 1)};
-    large_row_pair_cta<<<dim3(g.N1 / 2 + 1, ni), kThreads, large_row_cta_smem(g.N2), s>>>(p.d_tw, p.d_tw2, ra);
+    ColFwdArgs ca{};
+    ca.in[0] = ColFwdIn{series + (size_t)i0 * p.N, (size_t)p.N, (int)p.N, Y, vec16(series, p.N)};
+    col_fwd(p, ca, 1, ni, s);
+    RowArgs ra{0, Y, nullptr, nullptr, 0, spec + (size_t)i0 * (p.H + 1)};
+    rows(p, ra, ni, false, s);
   }
   return cudaGetLastError();
 }
@@ -418,48 +585,68 @@ cudaError_t large_spectrum(const Plan& p, const double* series, double2* spec, i
 cudaError_t large_correlate(const Plan& p, const double2* spec, size_t spec_stride, const double* x, size_t xs, int n_in,
                             double* out, size_t os, int n_out, int ld_out, const double* prev, size_t ps,
                             const double* coef, double* part, int items, cudaStream_t s) {
-  const LargeGeom g = geom(p);
+  int N1, N2;
+  large_geom(p, &N1, &N2);
   double2* Y = p.d_lbuf;
   for (int i0 = 0; i0 < items; i0 += p.lbuf_items) {
     const int ni = std::min(items - i0, p.lbuf_items);
-    large_col_fwd<<<dim3(g.N2 / kColW, ni), kThreads, large_col_smem(g.N1), s>>>(
-        x + (size_t)i0 * xs, xs, n_in, g.H, g.N1, g.N2, p.d_tw4, p.d_tw1, Y);
-    RowArgs ra{g.H, g.N1, g.N2, 1, p.d_tw4, p.d_twp, Y, nullptr, spec + (size_t)i0 * spec_stride, spec_stride, nullptr};
-    large_row_pair_cta<<<dim3(g.N1 / 2 + 1, ni), kThreads, large_row_cta_smem(g.N2), s>>>(p.d_tw, p.d_tw2, ra);
+    ColFwdArgs cf{};
+    cf.in[0] = ColFwdIn{x + (size_t)i0 * xs, xs, n_in, Y, vec16(x, xs)};
+    col_fwd(p, cf, 1, ni, s);
+    RowArgs ra{1, Y, nullptr, spec + (size_t)i0 * spec_stride, spec_stride, nullptr};
+    rows(p, ra, ni, ni >= 8, s);
     ColInvArgs ca{};
-    ca.H = g.H; ca.N1 = g.N1; ca.N2 = g.N2; ca.mode = 0;
+    ca.mode = 0;
     ca.n_out = n_out; ca.ld_out = ld_out; ca.out_stride = os; ca.out = out + (size_t)i0 * os;
     ca.prev = prev ? prev + (size_t)i0 * ps : nullptr; ca.prev_stride = ps;
     ca.coef = coef ? coef + i0 : nullptr;
-    ca.part = part ? part + (size_t)i0 * (g.N2 / kColW) : nullptr;
-    large_col_inv<<<dim3(g.N2 / kColW, ni), kThreads, large_col_smem(g.N1), s>>>(Y, p.d_tw1, ca);
+    ca.part = part ? part + (size_t)i0 * (N2 / kColW) : nullptr;
+    col_inv(p, Y, ca, ni, s);
   }
   return cudaGetLastError();
 }
 
-cudaError_t large_hankelize(const Plan& p, const double* sigma, const double* U, const double* V, size_t nterm_total,
+cudaError_t large_hankelize(Plan& p, const double* sigma, const double* U, const double* V, size_t nterm_total,
                             double* out, cudaStream_t s) {
-  const LargeGeom g = geom(p);
-  // terms per batch (two H-point buffers each): as many as the work buffers hold -- the
-  // four-step kernels are latency-bound per CTA, so more terms in flight win over keeping
-  // the buffers in L2 (measured: 8 terms 14.9 us/term, 16: 11.9, 32: 11.2 at cfg5)
-  int per = std::max(1, p.lbuf_items / 2);
-  if (const char* e = getenv("SSA_HANK_PER")) per = std::max(1, std::min(p.lbuf_items / 2, atoi(e)));
-  double2* Ya = p.d_lbuf;
-  double2* Yb = p.d_lbuf + (size_t)per * g.H;
-  for (size_t t0 = 0; t0 < nterm_total; t0 += per) {
+  // Batches of `per` terms (two H-point buffers each) alternate between the caller's
+  // stream and a second one with their own buffers, so one batch's launch tails overlap
+  // the next batch's work.  SSA_HANK_PER overrides the batch size (tuning).
+  const int cap = std::max(1, p.lbuf_items / 4);
+  int per = std::max(1, std::min(cap, p.hank_per));
+  if (const char* e = getenv("SSA_HANK_PER")) per = std::max(1, std::min(cap, atoi(e)));
+  const bool two = nterm_total > (size_t)per && p.lbuf_items >= 4;
+  cudaError_t err;
+  if (two && !p.lg_aux) {
+    if ((err = cudaStreamCreateWithFlags(&p.lg_aux, cudaStreamNonBlocking))) return err;
+    for (int i = 0; i < 2; ++i)
+      if ((err = cudaEventCreateWithFlags(&p.lg_ev[i], cudaEventDisableTiming))) return err;
+  }
+  if (two) {
+    if ((err = cudaEventRecord(p.lg_ev[0], s))) return err;
+    if ((err = cudaStreamWaitEvent(p.lg_aux, p.lg_ev[0], 0))) return err;
+  }
+  size_t bi = 0;
+  for (size_t t0 = 0; t0 < nterm_total; t0 += per, ++bi) {
     const int ni = (int)std::min<size_t>(nterm_total - t0, per);
-    large_col_fwd<<<dim3(g.N2 / kColW, ni), kThreads, large_col_smem(g.N1), s>>>(
-        U + t0 * p.L, (size_t)p.L, (int)p.L, g.H, g.N1, g.N2, p.d_tw4, p.d_tw1, Ya);
-    large_col_fwd<<<dim3(g.N2 / kColW, ni), kThreads, large_col_smem(g.N1), s>>>(
-        V + t0 * p.K, (size_t)p.K, (int)p.K, g.H, g.N1, g.N2, p.d_tw4, p.d_tw1, Yb);
-    RowArgs ra{g.H, g.N1, g.N2, 2, p.d_tw4, p.d_twp, Ya, Yb, nullptr, 0, nullptr};
-    large_row_pair<<<dim3((g.N1 / 2 + 2) / 2, ni), kThreads, large_row_smem(g.N2, kWarps), s>>>(p.d_tw, p.d_tw2, ra);
+    const int set = two ? (int)(bi & 1) : 0;
+    cudaStream_t st = set ? p.lg_aux : s;
+    double2* Ya = p.d_lbuf + (size_t)(2 * set) * per * p.H;
+    double2* Yb = Ya + (size_t)per * p.H;
+    ColFwdArgs cf{};
+    cf.in[0] = ColFwdIn{U + t0 * p.L, (size_t)p.L, (int)p.L, Ya, vec16(U, p.L)};
+    cf.in[1] = ColFwdIn{V + t0 * p.K, (size_t)p.K, (int)p.K, Yb, vec16(V, p.K)};
+    col_fwd(p, cf, 2, ni, st);
+    RowArgs ra{2, Ya, Yb, nullptr, 0, nullptr};
+    rows(p, ra, ni, true, st);
     ColInvArgs ca{};
-    ca.H = g.H; ca.N1 = g.N1; ca.N2 = g.N2; ca.mode = 1;
+    ca.mode = 1;
     ca.out_stride = (size_t)p.N; ca.out = out + t0 * p.N;
     ca.sigma = sigma + t0; ca.N = (int)p.N; ca.L = (int)p.L; ca.K = (int)p.K;
-    large_col_inv<<<dim3(g.N2 / kColW, ni), kThreads, large_col_smem(g.N1), s>>>(Yb, p.d_tw1, ca);
+    col_inv(p, Yb, ca, ni, st);
+  }
+  if (two) {
+    if ((err = cudaEventRecord(p.lg_ev[1], p.lg_aux))) return err;
+    if ((err = cudaStreamWaitEvent(s, p.lg_ev[1], 0))) return err;
   }
   return cudaGetLastError();
 }

@@ -90,6 +90,25 @@ def test_matvec_cfg4_sample(P):
         assert nrel(z[b], oracle.matvec(F[b], L, U[b], True)) <= 1e-12
 
 
+@pytest.mark.parametrize("N,L", [(8192, 4096), (7000, 3000), (5000, 4000), (4097, 2), (8192, 4095), (6001, 2999)])
+def test_matvec_register_path_vs_oracle(P, N, L):
+    """M = 8192 (H = 4096): the register-resident radix-16 correlation (fft_reg.cuh) when
+    the input fits the zero-padded half (n_in <= 4097), the shared-memory path otherwise;
+    ragged N, both directions, several series per launch."""
+    rng = np.random.default_rng(N + L)
+    K = N - L + 1
+    B = 3
+    F = rng.standard_normal((B, N)); v = rng.standard_normal((B, K)); u = rng.standard_normal((B, L))
+    plan = P.Plan(N, L, 0, B)
+    assert plan.M == 8192
+    spec = plan.spectrum(cuda(F))
+    y = plan.matvec(spec, cuda(v)).cpu().numpy()
+    z = plan.matvec(spec, cuda(u), transpose=True).cpu().numpy()
+    for b in range(B):
+        assert nrel(y[b], oracle.matvec(F[b], L, v[b])) <= 1e-12
+        assert nrel(z[b], oracle.matvec(F[b], L, u[b], True)) <= 1e-12
+
+
 def test_matvec_adjoint(P):
     rng = np.random.default_rng(6)
     N, L = 4096, 2048
