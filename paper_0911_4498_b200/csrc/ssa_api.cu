@@ -230,7 +230,7 @@ static ssa_status create_large_workspace(Plan& p) {
   if ((st = alloc((void**)&p.d_tgkw, tgkw_stride(p) * 8, "TGK vectors")) != SSA_OK) return st;
   if ((st = alloc((void**)&p.d_info, (size_t)p.batch * sizeof(ssa_series_info), "info")) != SSA_OK) return st;
   if ((st = alloc((void**)&p.d_counters, 16 * sizeof(int), "counters")) != SSA_OK) return st;
-  const size_t nch = (size_t)(std::max(p.ldL, p.ldK) + 2047) / 2048;
+  const size_t nch = (size_t)(std::max(p.ldL, p.ldK) + 511) / 512;  // reorth chunks (kRoChunk)
   const size_t gU = (size_t)(p.L + 255) / 256;
   const size_t npart = std::max(nch * (p.m_max + 2), gU * k * 2) + 4096;
   if ((st = alloc((void**)&p.d_lgsc, 256, "scalars")) != SSA_OK) return st;

@@ -84,25 +84,87 @@ __global__ void __launch_bounds__(kThreads) lg_start(double* r, int n, int ld, u
   }
 }
 
-// dots: part[row][cta] = <basis[row][chunk], r[chunk]>, rows split over warps
+// Reorthogonalization kernels: each CTA owns a kRoChunk-element chunk of r, each thread
+// kRoE elements of it in registers; the basis rows stream in groups of kRoG rows with all
+// kRoG x kRoE loads of a group in flight per thread (HBM-bound: bytes in flight per SM
+// set the rate).  512-element chunks: ~7 CTAs per SM at L = 2^19 (an even load).
+constexpr int kRoChunk = 512;
+constexpr int kRoE = kRoChunk / kThreads;  // 2
+constexpr int kRoG = 8;                    // rows per group (warp_sum8)
+
+// Sum of 8 values over the warp with 9 shuffles: lane l ends with the total of value
+// (l >> 2) & 7 (fixed pairing order: deterministic).
+__device__ __forceinline__ double warp_sum8(double* v, int lane) {
+  const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const double send = b4 ? v[i] : v[i + 4];
+    const double keep = b4 ? v[i + 4] : v[i];
+    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const double send = b3 ? v[i] : v[i + 2];
+    const double keep = b3 ? v[i + 2] : v[i];
+    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+  {
+    const double send = b2 ? v[0] : v[1];
+    const double keep = b2 ? v[1] : v[0];
+    v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+  }
+  v[0] += __shfl_xor_sync(0xffffffffu, v[0], 2);
+  v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+  return v[0];
+}
+
+// dots: part[row][cta] = <basis[row][chunk], r[chunk]>; smem red[nb][warps] (dynamic).
+// Rows are read with L2 evict_last so lg_update (rows in reverse) finds the last ones.
 __global__ void __launch_bounds__(kThreads) lg_dots(const double* __restrict__ basis, int ld, int nb,
                                                     const double* __restrict__ r, double* part, int nchunk,
                                                     const LgScalars* sc, int pass) {
   if (pass == 1 && !sc->again) return;
   if (sc->stop) return;
-  __shared__ double rs[kLgChunk];
-  const int c0 = blockIdx.x * kLgChunk;
-  const int len = min(kLgChunk, ld - c0);
-  for (int i = threadIdx.x; i < len; i += blockDim.x) rs[i] = r[c0 + i];
-  __syncthreads();
+  extern __shared__ double red[];  // [nb][kWarps]
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int row = w; row < nb; row += kWarps) {
-    const double* br = basis + (size_t)row * ld + c0;
+  const int c0 = blockIdx.x * kRoChunk + threadIdx.x;
+  const bool full = (blockIdx.x + 1) * kRoChunk <= ld;
+  double v[kRoE];
+#pragma unroll
+  for (int e = 0; e < kRoE; ++e) v[e] = (c0 + e * kThreads < ld) ? r[c0 + e * kThreads] : 0.0;
+  const uint64_t pol = policy_evict_last();
+  for (int row0 = 0; row0 < nb; row0 += kRoG) {
+    double b[kRoG][kRoE];
+#pragma unroll
+    for (int q = 0; q < kRoG; ++q)
+#pragma unroll
+      for (int e = 0; e < kRoE; ++e) {
+        const int t = c0 + e * kThreads;
+        double x = 0.0;
+        if (row0 + q < nb && (full || t < ld)) {
+          const double* ad = basis + (size_t)(row0 + q) * ld + t;
+          asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(x) : "l"(ad), "l"(pol));
+        }
+        b[q][e] = x;
+      }
+    double d[kRoG];
+#pragma unroll
+    for (int q = 0; q < kRoG; ++q) {
+      double acc = 0.0;
+#pragma unroll
+      for (int e = 0; e < kRoE; ++e) acc = fma(b[q][e], v[e], acc);
+      d[q] = acc;
+    }
+    const double tot = warp_sum8(d, lane);
+    const int q = (lane >> 2) & 7;
+    if ((lane & 3) == 0 && row0 + q < nb) red[(row0 + q) * kWarps + w] = tot;
+  }
+  __syncthreads();
+  for (int row = threadIdx.x; row < nb; row += kThreads) {
     double s = 0.0;
-#pragma unroll 8
-    for (int i = lane; i < len; i += 32) s = fma(__ldg(br + i), rs[i], s);  // lines stay in L2 for lg_update
-    s = warp_sum(s);
-    if (lane == 0) part[(size_t)row * nchunk + blockIdx.x] = s;
+#pragma unroll
+    for (int i = 0; i < kWarps; ++i) s += red[row * kWarps + i];
+    part[(size_t)row * nchunk + blockIdx.x] = s;
   }
 }
 
@@ -119,49 +181,46 @@ __global__ void lg_rows(const double* __restrict__ part, int nb, int nchunk, dou
 }
 
 // update: r -= sum_row h[row] basis[row] (rows in reverse: the rows lg_dots read last
-// are still in L2), partial sums of squares.  Each thread owns kLgChunk / kThreads
-// elements of the CTA's chunk; every step streams four rows (4 x 8 independent loads in
-// flight per thread) and applies them in the fixed reverse row order.
+// are still in L2), partial sums of squares; groups of kRoG rows, all loads in flight.
 __global__ void __launch_bounds__(kThreads) lg_update(const double* __restrict__ basis, int ld, int nb,
                                                       const double* __restrict__ h, double* r, double* part,
                                                       const LgScalars* sc, int pass) {
   if (pass == 1 && !sc->again) return;
   if (sc->stop) return;
-  constexpr int E = kLgChunk / kThreads;
   __shared__ double red[kWarps];
   extern __shared__ double hs[];  // nb coefficients
   for (int i = threadIdx.x; i < nb; i += blockDim.x) hs[i] = h[i];
   __syncthreads();
-  const int c0 = blockIdx.x * kLgChunk + threadIdx.x;
-  double v[E];
+  const int c0 = blockIdx.x * kRoChunk + threadIdx.x;
+  const bool full = (blockIdx.x + 1) * kRoChunk <= ld;
+  double v[kRoE];
 #pragma unroll
-  for (int e = 0; e < E; ++e) v[e] = (c0 + e * kThreads < ld) ? r[c0 + e * kThreads] : 0.0;
-  const bool full = (blockIdx.x + 1) * kLgChunk <= ld;
-  int row = nb - 1;
+  for (int e = 0; e < kRoE; ++e) v[e] = (c0 + e * kThreads < ld) ? r[c0 + e * kThreads] : 0.0;
+  int top = nb - 1;
   if (full) {
-    for (; row >= 3; row -= 4) {
-      double b[4][E];
+    for (; top >= kRoG - 1; top -= kRoG) {  // whole groups: no guards, all loads in flight
+      double b[kRoG][kRoE];
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
+      for (int q = 0; q < kRoG; ++q)
 #pragma unroll
-        for (int e = 0; e < E; ++e) b[q][e] = __ldcs(basis + (size_t)(row - q) * ld + c0 + e * kThreads);
+        for (int e = 0; e < kRoE; ++e) b[q][e] = __ldcs(basis + (size_t)(top - q) * ld + c0 + e * kThreads);
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const double hr = hs[row - q];
+      for (int q = 0; q < kRoG; ++q) {
+        const double hr = hs[top - q];
 #pragma unroll
-        for (int e = 0; e < E; ++e) v[e] = fma(-hr, b[q][e], v[e]);
+        for (int e = 0; e < kRoE; ++e) v[e] = fma(-hr, b[q][e], v[e]);
       }
     }
   }
-  for (; row >= 0; --row) {
-    const double hr = hs[row];
+  for (; top >= 0; --top) {
+    const double hr = hs[top];
 #pragma unroll
-    for (int e = 0; e < E; ++e)
-      if (c0 + e * kThreads < ld) v[e] = fma(-hr, __ldcs(basis + (size_t)row * ld + c0 + e * kThreads), v[e]);
+    for (int e = 0; e < kRoE; ++e)
+      if (c0 + e * kThreads < ld) v[e] = fma(-hr, __ldcs(basis + (size_t)top * ld + c0 + e * kThreads), v[e]);
   }
   double ss = 0.0;
 #pragma unroll
-  for (int e = 0; e < E; ++e)
+  for (int e = 0; e < kRoE; ++e)
     if (c0 + e * kThreads < ld) {
       r[c0 + e * kThreads] = v[e];
       ss = fma(v[e], v[e], ss);
@@ -321,7 +380,10 @@ __global__ void lg_flip(double* X, int n, int k, const double* __restrict__ sgn)
 size_t lg_check_smem(int m_max) { return (size_t)(3 * (2 * m_max + 1) + 4 * kMaxK) * 8 + 64; }
 
 cudaError_t large_lanczos_set_attributes(int m_max) {
-  return raise_smem_limit(lg_check, (int)lg_check_smem(m_max));
+  cudaError_t e = raise_smem_limit(lg_check, (int)lg_check_smem(m_max));
+  if (e == cudaSuccess) e = raise_smem_limit(lg_dots, (size_t)(m_max + 2) * kWarps * 8);
+  if (e == cudaSuccess) e = raise_smem_limit(lg_update, (size_t)(m_max + 2) * 8);
+  return e;
 }
 
 __global__ void lg_set_nr(const double* __restrict__ part, int n, LgScalars* sc) {
@@ -387,9 +449,10 @@ cudaError_t large_decompose_one(Plan& p, const DecomposeArgs& a0, int b, cudaStr
     lg_coef<<<1, 32, 0, s>>>(sc, beta + 1, 0, 1);
     lg_normalize<<<(ldL + kThreads - 1) / kThreads, kThreads, 0, s>>>(r, L, ldL, beta + 1, U);
   }
-  auto reorth = [&](const double* basis, int ld, int nb, int nch) {
+  auto reorth = [&](const double* basis, int ld, int nb, int) {
+    const int nch = (ld + kRoChunk - 1) / kRoChunk;
     for (int pass = 0; pass < 2 && nb > 0; ++pass) {
-      lg_dots<<<nch, kThreads, 0, s>>>(basis, ld, nb, r, part, nch, sc, pass);
+      lg_dots<<<nch, kThreads, (size_t)nb * kWarps * 8, s>>>(basis, ld, nb, r, part, nch, sc, pass);
       lg_rows<<<(nb * 32 + kThreads - 1) / kThreads, kThreads, 0, s>>>(part, nb, nch, h, sc, pass);
       lg_update<<<nch, kThreads, (size_t)(nb > 0 ? nb : 1) * 8, s>>>(basis, ld, nb, h, r, part, sc, pass);
       lg_after_pass<<<1, 32, 0, s>>>(part, nch, sc, pass, p.opt.reorth);
