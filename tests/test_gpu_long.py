@@ -59,6 +59,40 @@ def test_long_hankelize(P, N, L, force):
             assert nrel(g[b, i], oracle.hankelize_rank1(s[b, i], U[b, i], V[b, i])) <= 1e-12
 
 
+def test_long_hankelize_many_batches(P):
+    """150 terms > the 64-term batch: three batches alternating over the caller's stream
+    and the plan's second stream (own buffers); every term against the oracle, and the
+    same terms one problem at a time (single batch) bit for bit."""
+    N, L = 1000, 400
+    K = N - L + 1
+    B, T = 30, 5
+    rng = np.random.default_rng(77)
+    s = rng.uniform(0.5, 2, (B, T)); U = rng.standard_normal((B, T, L)); V = rng.standard_normal((B, T, K))
+    plan = P.Plan(N, L, 0, B, force_long=True)
+    g = plan.hankelize(cuda(s), cuda(U), cuda(V)).cpu().numpy()
+    for b in range(B):
+        for i in range(T):
+            assert nrel(g[b, i], oracle.hankelize_rank1(s[b, i], U[b, i], V[b, i])) <= 1e-12
+    one = P.Plan(N, L, 0, 1, force_long=True)
+    for b in (0, 13, 29):
+        g1 = one.hankelize(cuda(s[b:b + 1]), cuda(U[b:b + 1]), cuda(V[b:b + 1])).cpu().numpy()
+        assert np.array_equal(g1[0], g[b])
+
+
+def test_cfg5_shape_two_batches_sampled(P):
+    """BASELINE configs[4] shape, problems 0 and 1 (100 terms: two batches on two streams);
+    the last term of each problem against the oracle's direct averaging."""
+    c = ssa_inputs.CONFIGS["cfg5"]
+    N, L = c["N"], c["L"]
+    probs = [ssa_inputs.cfg5_problem(p, N, L, terms=50) for p in (0, 1)]
+    sig = np.stack([q[0] for q in probs]); U = np.stack([q[1] for q in probs]); V = np.stack([q[2] for q in probs])
+    plan = P.Plan(N, L, 0, 2)
+    g = plan.hankelize(cuda(sig), cuda(U), cuda(V)).cpu().numpy()
+    for p in (0, 1):
+        ref = oracle.hankelize_rank1(sig[p, 49], U[p, 49], V[p, 49])
+        assert nrel(g[p, 49], ref) <= 1e-10
+
+
 def test_cfg5_shape_sampled_terms(P):
     """BASELINE configs[4] shape (N = 262144, L = 131072), problem 0, first 4 terms."""
     c = ssa_inputs.CONFIGS["cfg5"]
