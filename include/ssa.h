@@ -140,6 +140,20 @@ ssa_status ssa_decompose(ssa_plan_t plan, const double* d_series, double* d_sigm
 ssa_status ssa_reconstruct(ssa_plan_t plan, const double* d_sigma, const double* d_U, const double* d_V,
                            double* d_out, void* stream);
 
+/* Grouped reconstruction (Basic SSA steps 3-4, PAPER.md:131-146 grouping and 148-167
+ * diagonal averaging): for each group I_g = { i : groups[i] == g } the series
+ *   g~_g = hankelization( sum_{i in I_g} sigma_i u_i v_i^T ) = sum_{i in I_g} g~_i
+ * (averaging is linear), computed as one inverse FFT of the summed
+ * product spectra per group (M <= 8192 and not the long path), else as elementary series
+ * in plan scratch summed per group.
+ *   groups: HOST [k], groups[i] in [0, ngroups) or -1 (triple left out); read during the
+ *           call only.  ngroups in [1, k].  An empty group yields a zero series.
+ *   d_sigma, d_U, d_V: as ssa_reconstruct.   d_out: [batch][ngroups][N]
+ * Errors: INVALID_ARGUMENT for NULL pointers, k = 0 plans, ngroups or a group id out of
+ * range; OUT_OF_MEMORY if the scratch of the long path cannot be allocated. */
+ssa_status ssa_reconstruct_grouped(ssa_plan_t plan, const double* d_sigma, const double* d_U, const double* d_V,
+                                   const int32_t* groups, int32_t ngroups, double* d_out, void* stream);
+
 /* End-to-end call on HOST buffers: copies h_series to the device, runs ssa_decompose and
  * ssa_reconstruct on plan-owned device buffers, copies sigma, U, V, the reconstructions
  * and info back, and synchronizes `stream`.  Any output pointer may be NULL to skip its

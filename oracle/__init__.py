@@ -102,6 +102,23 @@ def hankelize_rank1(sigma: float, u, v) -> np.ndarray:
     return g
 
 
+def grouped(sigma, U, V, groups, ngroups: int) -> np.ndarray:
+    """Grouped reconstruction, Basic SSA steps 3-4 written out: for each group I the
+    resultant matrix X_I = sum_{i in I} sigma_i u_i v_i^T (sec 2.3) is
+    formed explicitly and diagonally averaged (sec 2.4).  Returns
+    [ngroups][L + K - 1]; triples with group -1 are left out."""
+    U = np.asarray(U, dtype=np.float64); V = np.asarray(V, dtype=np.float64)
+    L, K = U.shape[1], V.shape[1]
+    out = np.empty((ngroups, L + K - 1))
+    for g in range(ngroups):
+        X = np.zeros((L, K))
+        for i, gi in enumerate(groups):
+            if gi == g:
+                X += float(sigma[i]) * np.outer(U[i], V[i])
+        out[g] = diag_average(X)
+    return out
+
+
 def svd(f, L: int, nsv: int | None = None):
     """Leading nsv singular triples of the trajectory matrix by one-sided Jacobi
     (sec 2.2, with X = U Sigma V^T, R3).

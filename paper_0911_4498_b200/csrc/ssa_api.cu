@@ -117,7 +117,7 @@ static void free_plan(Plan& p) {
   void* ptrs[] = {p.d_tw, p.d_twl, p.d_spec, p.d_U, p.d_V, p.d_ab, p.d_state, p.d_tgk, p.d_rot, p.d_vecs, p.d_coef,
                   p.d_info, p.d_counters, p.d_hscratch, p.d_prof, p.d_tgkw, p.d_tw1, p.d_tw2, p.d_tw4, p.d_twp, p.d_lbuf,
                   p.d_lgsc, p.d_lgpart, p.d_lgh, p.d_lgr, p.d_series, p.d_sigma, p.d_Uout, p.d_Vout,
-                  p.d_recon};
+                  p.d_recon, p.d_elem};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   for (int i = 0; i < 2 * Plan::kPhases; ++i)
@@ -305,7 +305,11 @@ extern "C" ssa_status ssa_plan_create(int64_t N, int64_t L, int32_t k, int64_t b
       goto bad;
     }
   }
-  if (H > ssa::kMaxSmemH || ((o.reserved & 4) && H >= 64)) {  // reserved & 4: force (tests)
+  // long path: M > 16384, forced (reserved & 4, tests), or a decompose whose batched
+  // kernel would not fit one CTA's shared memory (e.g. H = 8192 with k > 0)
+  if (H > ssa::kMaxSmemH || ((o.reserved & 4) && H >= 64) ||
+      (k > 0 && H >= 64 &&
+       ssa::lanczos_smem_bytes((int)H, p.ldL, p.ldK, p.m_max, k) > (size_t)prop.sharedMemPerBlockOptin)) {
     p.large = true;
     int N1, N2;
     ssa::large_geom(p, &N1, &N2);
@@ -494,6 +498,45 @@ extern "C" ssa_status ssa_reconstruct(ssa_plan_t plan, const double* d_sigma, co
   if (!plan) return fail(SSA_ERR_INVALID_ARGUMENT, "NULL plan");
   if (plan->p.k < 1) return fail(SSA_ERR_INVALID_ARGUMENT, "plan was created with k = 0");
   return ssa_hankelize(plan, d_sigma, d_U, d_V, plan->p.k, d_out, stream);
+}
+
+extern "C" ssa_status ssa_reconstruct_grouped(ssa_plan_t plan, const double* d_sigma, const double* d_U,
+                                              const double* d_V, const int32_t* groups, int32_t ngroups, double* d_out,
+                                              void* stream) {
+  if (!plan || !d_sigma || !d_U || !d_V || !d_out || !groups) return fail(SSA_ERR_INVALID_ARGUMENT, "NULL argument");
+  Plan& p = plan->p;
+  const int k = p.k;
+  if (k < 1) return fail(SSA_ERR_INVALID_ARGUMENT, "plan was created with k = 0");
+  if (ngroups < 1 || ngroups > k) return fail(SSA_ERR_INVALID_ARGUMENT, "ngroups = %d not in [1, k = %d]", ngroups, k);
+  if ((int64_t)p.batch * ngroups > (int64_t)0x7fffffff) return fail(SSA_ERR_INVALID_ARGUMENT, "batch*ngroups too large");
+  ssa::GroupList gl{};
+  gl.k = k;
+  gl.ngroups = ngroups;
+  int cnt[ssa::kMaxK + 1] = {0};
+  for (int i = 0; i < k; ++i) {
+    if (groups[i] < -1 || groups[i] >= ngroups)
+      return fail(SSA_ERR_INVALID_ARGUMENT, "groups[%d] = %d not in [-1, %d)", i, groups[i], ngroups);
+    if (groups[i] >= 0) cnt[groups[i] + 1]++;
+  }
+  for (int g = 0; g < ngroups; ++g) gl.ptr[g + 1] = gl.ptr[g] + cnt[g + 1];
+  int fill[ssa::kMaxK] = {0};
+  for (int i = 0; i < k; ++i)  // triples in increasing index order inside each group
+    if (groups[i] >= 0) gl.idx[gl.ptr[groups[i]] + fill[groups[i]]++] = i;
+  CK(cudaSetDevice(p.device), "cudaSetDevice");
+  PhaseTimer pt(p, 4, S(stream));
+  if (!p.large && p.H <= ssa::kMaxHankelSmemH) {
+    CK(ssa::launch_group_hankelize(p, d_sigma, d_U, d_V, gl, d_out, S(stream)), "grouped hankelize launch");
+    p.launches += 1;
+    return SSA_OK;
+  }
+  // long path / H = 8192: elementary series into plan scratch, then the group sums
+  ssa_status st;
+  if (!p.d_elem && (st = alloc((void**)&p.d_elem, (size_t)p.batch * k * p.N * 8, "elementary series")) != SSA_OK)
+    return st;
+  if ((st = ssa_hankelize(plan, d_sigma, d_U, d_V, k, p.d_elem, stream)) != SSA_OK) return st;
+  CK(ssa::launch_group_sum(p, p.d_elem, gl, d_out, S(stream)), "group sum launch");
+  p.launches += 1;
+  return SSA_OK;
 }
 
 extern "C" ssa_status ssa_run_host(ssa_plan_t plan, const double* h_series, double* h_sigma, double* h_U,

@@ -207,6 +207,93 @@ __global__ void __launch_bounds__(kThreads) hankelize_kernel(const double* __res
 #undef SSA_HANK
 }
 
+// Grouped reconstruction (PAPER.md:131-146 grouping, 148-167 averaging): for group I_g,
+// g = sum_{i in I_g} hankelization(sigma_i u_i v_i^T) = irfft(sum_i sigma_i rfft(u_i) rfft(v_i)) / c
+// (diagonal averaging is linear), so the packed product spectra of the group's triples
+// are accumulated in shared memory and one inverse FFT per group is run.  One CTA per
+// (series, group); three H-point buffers (H <= kMaxHankelSmemH).
+template <int LOGH>
+__device__ __forceinline__ void group_body(double2* bufA, double2* bufB, double2* acc, const TwSmem& tw,
+                                           const double* __restrict__ sigma, const double* __restrict__ U,
+                                           const double* __restrict__ V, const GroupList& gl, int b, int g, int N,
+                                           int L, int K, double* __restrict__ out) {
+  constexpr int H = 1 << LOGH;
+  const int k = gl.k;
+  const int mn = L < K ? L : K;
+  const int i0 = gl.ptr[g], i1 = gl.ptr[g + 1];
+  for (int n = threadIdx.x; n < H; n += blockDim.x) acc[fsw(n)] = make_double2(0.0, 0.0);
+  for (int ii = i0; ii < i1; ++ii) {
+    const int i = gl.idx[ii];
+    const double* u = U + ((size_t)b * k + i) * L;
+    const double* v = V + ((size_t)b * k + i) * K;
+    const double sg = __ldg(sigma + (size_t)b * k + i);
+    __syncthreads();
+    for (int n = threadIdx.x; n < H; n += blockDim.x) {
+      const int j0 = 2 * n;
+      bufA[fsw(n)] = make_double2(j0 < L ? __ldg(u + j0) : 0.0, j0 + 1 < L ? __ldg(u + j0 + 1) : 0.0);
+      bufB[fsw(n)] = make_double2(j0 < K ? __ldg(v + j0) : 0.0, j0 + 1 < K ? __ldg(v + j0 + 1) : 0.0);
+    }
+    __syncthreads();
+    fft_run_t<LOGH, false>(bufA, tw, threadIdx.x, blockDim.x, CtaSync());
+    fft_run_t<LOGH, false>(bufB, tw, threadIdx.x, blockDim.x, CtaSync());
+    for (int p = threadIdx.x; p <= (H >> 1); p += blockDim.x) {
+      double2 Up, Uq, Vp, Vq;
+      int pr, qr;
+      real_pair<LOGH>(bufA, tw, p, Up, Uq, pr, qr);
+      const double2 W = real_pair<LOGH>(bufB, tw, p, Vp, Vq, pr, qr);
+      // inv_pair of sigma * (U V) added into acc (inv_pair is linear in its inputs)
+      const double2 Yp = cmul(Up, Vp), Yq = cmul(Uq, Vq);
+      const double2 E = make_double2(0.5 * sg * (Yp.x + Yq.x), 0.5 * sg * (Yp.y - Yq.y));
+      const double2 D = make_double2(0.5 * sg * (Yp.x - Yq.x), 0.5 * sg * (Yp.y + Yq.y));
+      const double2 O = cmulc(D, W);
+      acc[pr] = cadd(acc[pr], make_double2(E.x - O.y, E.y + O.x));
+      if (qr != pr) acc[qr] = cadd(acc[qr], make_double2(E.x + O.y, O.x - E.y));
+    }
+  }
+  __syncthreads();
+  fft_run_t<LOGH, true>(acc, tw, threadIdx.x, blockDim.x, CtaSync());
+  constexpr double invH = 1.0 / (double)H;
+  double* o = out + ((size_t)b * gl.ngroups + g) * N;
+  for (int t = threadIdx.x; t < N; t += blockDim.x) {
+    const double2 z = acc[fsw(t >> 1)];
+    const int k1 = t + 1;
+    int c = k1;
+    if (c > mn) c = mn;
+    if (N - k1 + 1 < c) c = N - k1 + 1;
+    o[t] = ((t & 1) ? z.y : z.x) * invH / (double)c;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) group_hankelize_kernel(const double* __restrict__ sigma,
+                                                                   const double* __restrict__ U,
+                                                                   const double* __restrict__ V, GroupList gl, int N,
+                                                                   int L, int K, int H, const double2* __restrict__ T,
+                                                                   double* __restrict__ out) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double2* bufA = reinterpret_cast<double2*>(smem_raw);
+  double2* bufB = bufA + H;
+  double2* acc = bufB + H;
+  const TwSmem tw = load_tw2(T, acc + H, 2 * H);
+  const FftShape sh = make_shape(H);
+  const int b = blockIdx.x / gl.ngroups, g = blockIdx.x % gl.ngroups;
+#define SSA_GRP(LG) group_body<LG>(bufA, bufB, acc, tw, sigma, U, V, gl, b, g, N, L, K, out)
+  SSA_DISPATCH_LOGH(sh.logH, SSA_GRP)
+#undef SSA_GRP
+}
+
+// out[b][g][t] = sum_{i in I_g} elem[b][i][t] (large path: elementary series first).
+__global__ void group_sum_kernel(const double* __restrict__ elem, GroupList gl, int N, size_t total,
+                                 double* __restrict__ out) {
+  for (size_t x = (size_t)blockIdx.x * blockDim.x + threadIdx.x; x < total; x += (size_t)gridDim.x * blockDim.x) {
+    const size_t t = x % N, bg = x / N;
+    const int g = (int)(bg % gl.ngroups);
+    const size_t b = bg / gl.ngroups;
+    double s = 0.0;
+    for (int ii = gl.ptr[g]; ii < gl.ptr[g + 1]; ++ii) s += elem[((size_t)b * gl.k + gl.idx[ii]) * N + t];
+    out[x] = s;
+  }
+}
+
 static size_t tw_smem(int H) { return (size_t)tw2_entries(2 * H) * 16; }
 static size_t fft_smem(int H) { return (size_t)fft_elems(H) * 16 + tw_smem(H); }
 static size_t reg4096_smem() { return (size_t)kReg4096SmemElems * 16 + kReg4096StageDoubles * 8 + tw_smem(4096); }
@@ -223,6 +310,10 @@ cudaError_t fft_set_attributes(int H, const char** which) {
   if (H == 4096 && (e = raise_smem_limit(matvec4096_kernel, (int)reg4096_smem()))) return e;
   *which = "hankelize_kernel<BIG>";
   if ((e = raise_smem_limit(hankelize_kernel<true>, (int)s1))) return e;
+  *which = "group_hankelize_kernel";
+  if (H <= kMaxHankelSmemH &&
+      (e = raise_smem_limit(group_hankelize_kernel, (size_t)3 * fft_elems(H) * 16 + tw_smem(H))))
+    return e;
   *which = "hankelize_kernel";
   if (H <= kMaxHankelSmemH)
     if ((e = raise_smem_limit(hankelize_kernel<false>, (int)s2)))
@@ -255,6 +346,21 @@ cudaError_t launch_matvec(const Plan& p, const double2* spec, const double* x, d
     return cudaGetLastError();
   }
   matvec_kernel<<<(unsigned)p.batch, kThreads, fft_smem((int)p.H), s>>>(spec, (int)p.H, n_in, n_out, p.d_twl, x, y);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_group_hankelize(const Plan& p, const double* sigma, const double* U, const double* V,
+                                   const GroupList& gl, double* out, cudaStream_t s) {
+  const size_t grid = (size_t)p.batch * gl.ngroups;
+  group_hankelize_kernel<<<(unsigned)grid, kThreads, (size_t)3 * fft_elems((int)p.H) * 16 + tw_smem((int)p.H), s>>>(
+      sigma, U, V, gl, (int)p.N, (int)p.L, (int)p.K, (int)p.H, p.d_twl, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_group_sum(const Plan& p, const double* elem, const GroupList& gl, double* out, cudaStream_t s) {
+  const size_t total = (size_t)p.batch * gl.ngroups * p.N;
+  const size_t grid = std::min<size_t>((total + kThreads - 1) / kThreads, (size_t)p.sms * 16);
+  group_sum_kernel<<<(unsigned)grid, kThreads, 0, s>>>(elem, gl, (int)p.N, total, out);
   return cudaGetLastError();
 }
 

@@ -105,6 +105,7 @@ struct Plan {
   double* d_Uout = nullptr;
   double* d_Vout = nullptr;
   double* d_recon = nullptr;
+  double* d_elem = nullptr;  // grouped reconstruction on the long path: elementary series
   // host-API pipelining (ssa_run_host): two sub-plans of one slice each, alternating on two
   // compute streams, device-to-host copies of finished slices on a third stream
   void* sub[2] = {nullptr, nullptr};  // ssa_plan_t
@@ -135,6 +136,15 @@ cudaError_t launch_matvec(const Plan& p, const double2* spec, const double* x, d
 cudaError_t launch_hankelize(const Plan& p, const double* sigma, const double* U, const double* V, int nterms,
                              double* out, cudaStream_t s);
 cudaError_t fft_set_attributes(int H, const char** which);
+// Grouping of the k triples (CSR by group, passed by value): triples idx[ptr[g] .. ptr[g+1])
+struct GroupList {
+  int k, ngroups;
+  int ptr[kMaxK + 1];
+  int idx[kMaxK];
+};
+cudaError_t launch_group_hankelize(const Plan& p, const double* sigma, const double* U, const double* V,
+                                   const GroupList& gl, double* out, cudaStream_t s);
+cudaError_t launch_group_sum(const Plan& p, const double* elem, const GroupList& gl, double* out, cudaStream_t s);
 
 size_t lanczos_smem_bytes(int H, int ldL, int ldK, int m_max, int k);
 size_t ritz_smem_bytes(int ldL, int ldK, int k, int m_max);

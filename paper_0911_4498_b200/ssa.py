@@ -26,7 +26,7 @@ STATUS = {0: "SSA_OK", 1: "SSA_ERR_INVALID_ARGUMENT", 2: "SSA_ERR_NOT_CONVERGED"
 # every symbol include/ssa.h declares
 EXPORTS = ["ssa_options_default", "ssa_plan_create", "ssa_plan_destroy", "ssa_plan_fft_size",
            "ssa_plan_max_steps", "ssa_spectrum", "ssa_matvec", "ssa_hankelize", "ssa_decompose",
-           "ssa_reconstruct", "ssa_run_host", "ssa_status_string", "ssa_last_error",
+           "ssa_reconstruct", "ssa_reconstruct_grouped", "ssa_run_host", "ssa_status_string", "ssa_last_error",
            "ssa_plan_launch_count", "ssa_plan_phase_ms", "ssa_plan_profile", "ssa_plan_bidiagonals"]
 
 
@@ -85,6 +85,7 @@ def load_library():
     lib.ssa_hankelize.argtypes = [vp, dp, dp, dp, i32, dp, vp]
     lib.ssa_decompose.argtypes = [vp, dp, dp, dp, dp, dp, vp]
     lib.ssa_reconstruct.argtypes = [vp, dp, dp, dp, dp, vp]
+    lib.ssa_reconstruct_grouped.argtypes = [vp, dp, dp, dp, vp, i32, dp, vp]
     lib.ssa_run_host.argtypes = [vp, dp, dp, dp, dp, dp, dp, vp]
     lib.ssa_status_string.argtypes = [ctypes.c_int]
     lib.ssa_status_string.restype = ctypes.c_char_p
@@ -238,6 +239,23 @@ class Plan:
         _dev_f64(out, (self.batch, self.k, self.N), "out")
         _check(load_library().ssa_reconstruct(self._h, sigma.data_ptr(), U.data_ptr(), V.data_ptr(),
                                               out.data_ptr(), _stream(stream)))
+        return out
+
+    def reconstruct_grouped(self, sigma, U, V, groups, ngroups=None, out=None, stream=None):
+        """Grouped reconstruction [batch][ngroups][N]: groups[i] is the
+        group of triple i (0 .. ngroups-1, or -1 to leave it out); ngroups defaults to
+        max(groups) + 1."""
+        g = np.ascontiguousarray(groups, dtype=np.int32)
+        if g.shape != (self.k,):
+            raise ValueError(f"groups must have k = {self.k} entries")
+        ng = int(ngroups) if ngroups is not None else (int(g.max()) + 1 if g.size else 0)
+        _dev_f64(sigma, (self.batch, self.k), "sigma")
+        _dev_f64(U, (self.batch, self.k, self.L), "U")
+        _dev_f64(V, (self.batch, self.k, self.K), "V")
+        out = self._t(self.batch, max(ng, 1), self.N) if out is None else out
+        _dev_f64(out, (self.batch, max(ng, 1), self.N), "out")
+        _check(load_library().ssa_reconstruct_grouped(self._h, sigma.data_ptr(), U.data_ptr(), V.data_ptr(),
+                                                      g.ctypes.data, ng, out.data_ptr(), _stream(stream)))
         return out
 
     def run_host(self, series: np.ndarray, want_vectors: bool = True, stream=None, raise_on_status=True):

@@ -129,6 +129,26 @@ def test_long_decompose_vs_oracle(P, N, L, k):
     assert rep.ok(), rep.failures
 
 
+def test_decompose_h8192_routes_to_long_path(P):
+    """N in (8192, 16384] (M = 16384): the batched decompose kernel would exceed one CTA's
+    shared memory, so the plan takes the long path on its own; two series vs the oracle."""
+    N, L, k = 9000, 300, 6
+    F = np.stack([ssa_inputs.cfg3_like_series(N, seed) for seed in (11, 12)])
+    plan = P.Plan(N, L, k, 2)
+    assert plan.M == 16384
+    sigma, U, V, info = plan.decompose(cuda(F))
+    G = plan.reconstruct(sigma, U, V)
+    torch.cuda.synchronize()
+    for b in range(2):
+        inf = P.info_to_numpy(info)[b]
+        assert inf["status"] == 0, inf
+        s_ref, U_ref, V_ref, _ = oracle.svd(F[b], L, k + 1)
+        G_ref = np.stack([oracle.hankelize_rank1(s_ref[i], U_ref[i], V_ref[i]) for i in range(k)])
+        rep = parity.compare(s_ref, U_ref, V_ref, sigma.cpu().numpy()[b], U.cpu().numpy()[b], V.cpu().numpy()[b], k,
+                             G_ref, G.cpu().numpy()[b], recon_scale=np.linalg.norm(F[b]))
+        assert rep.ok(), rep.failures
+
+
 def test_cfg3_like_long_series_residuals(P):
     """N = 2^17 (cfg3 generator): the oracle cannot do the SVD, so check true residuals
     with its direct product, orthonormality and the Frobenius bound."""

@@ -331,3 +331,50 @@ def test_decompose_cfg2_full_batch_sampled(P):
                              recon_scale=float(d["norm_f"]))
         assert rep.ok(), (i, rep.failures)
         print(f"cfg2 series {i}: steps {info[i]['steps']} worst {rep.worst()}")
+
+
+# ----------------------------------------------------------------------------- grouping
+@pytest.mark.parametrize("N,L,k,force", [(1024, 512, 10, False), (700, 520, 6, False), (4096, 2048, 16, False),
+                                         (10000, 3000, 8, False), (1000, 400, 6, True)])
+def test_reconstruct_grouped_vs_oracle(P, N, L, k, force):
+    """Grouped reconstruction of seeded random triples against the
+    oracle's explicit X_I + averaging: shared-memory accumulation of the group's product
+    spectra (M <= 8192), the elementary-then-sum route (M = 16384, forced long path);
+    groups with several triples, a singleton, an empty group and dropped triples."""
+    rng = np.random.default_rng(N + 7 * k)
+    K = N - L + 1
+    B = 3
+    s = np.sort(rng.uniform(0.1, 3, (B, k)))[:, ::-1].copy()
+    U = rng.standard_normal((B, k, L)); V = rng.standard_normal((B, k, K))
+    groups = np.array([(i % 3) if i < k - 1 else -1 for i in range(k)], dtype=np.int32)
+    groups[0] = 3                     # singleton group 3
+    ng = 5                            # group 4 empty
+    plan = P.Plan(N, L, k, B, force_long=force)
+    G = plan.reconstruct_grouped(cuda(s), cuda(U), cuda(V), groups, ngroups=ng).cpu().numpy()
+    assert not G[:, 4].any()          # the empty group
+    for b in range(B):
+        ref = oracle.grouped(s[b], U[b], V[b], groups, 4)
+        for g in range(4):
+            assert nrel(G[b, g], ref[g]) <= 1e-12
+    E = plan.reconstruct(cuda(s), cuda(U), cuda(V)).cpu().numpy()
+    for b in range(B):
+        for g in range(4):
+            assert nrel(G[b, g], E[b][groups == g].sum(axis=0)) <= 1e-13
+
+
+def test_reconstruct_grouped_signal_of_cfg1(P):
+    """cfg1 series: the two sinusoid pairs and the trend grouped from the decomposition
+    (triples 0 | 1,2 | 3,4) equal the oracle's grouping of its own Jacobi triples (the
+    groups span whole clusters, so the result is unique); together with the residual
+    group they sum to the series."""
+    c = ssa_inputs.CONFIGS["cfg1"]
+    N, L, k = c["N"], c["L"], c["k"]
+    f = ssa_inputs.cfg1_series(N)
+    plan = P.Plan(N, L, k, 1)
+    sg, U, V, info = plan.decompose(cuda(f[None]))
+    groups = np.array([0, 1, 1, 2, 2] + [3] * (k - 5), dtype=np.int32)
+    G = plan.reconstruct_grouped(sg, U, V, groups).cpu().numpy()[0]
+    s_o, U_o, V_o, _ = oracle.svd(f, L, k)
+    ref = oracle.grouped(s_o, U_o, V_o, groups, 4)
+    for g in range(3):
+        assert np.linalg.norm(G[g] - ref[g]) <= 1e-9 * np.linalg.norm(f)

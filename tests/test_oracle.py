@@ -269,6 +269,33 @@ def test_full_reconstruction_identity_and_finite_rank():
     assert np.allclose(G.sum(axis=0), f, rtol=0, atol=1e-12)
 
 
+def test_grouped_reconstruction_pins():
+    """oracle.grouped (explicit X_I) against what the paper fixes:
+    one group of all min(L,K) triples returns F (X = sum X_i, and the
+    averaging of a Hankel matrix is the identity); a one-triple group equals the rank-1
+    on-the-fly averaging (a different code path); the groups of a partition sum to the
+    all-in-one group (linearity of the averaging); the two leading
+    triples of a pure sinusoid (rank 2) reconstruct it exactly; a dropped triple (-1)
+    contributes nothing."""
+    rng = np.random.default_rng(31)
+    N, L = 29, 12
+    f = rng.standard_normal(N)
+    s, U, V, _ = oracle.svd(f, L)
+    r = len(s)
+    allg = oracle.grouped(s, U, V, [0] * r, 1)
+    assert np.allclose(allg[0], f, rtol=0, atol=1e-12 * np.abs(f).max())
+    groups = [i % 3 for i in range(r)]
+    G3 = oracle.grouped(s, U, V, groups, 3)
+    assert np.allclose(G3.sum(axis=0), allg[0], rtol=0, atol=1e-12 * np.abs(f).max())
+    g1 = oracle.grouped(s, U, V, [-1, 0] + [-1] * (r - 2), 1)
+    assert np.allclose(g1[0], oracle.hankelize_rank1(s[1], U[1], V[1]), rtol=0, atol=1e-14 * np.abs(g1).max())
+    n = np.arange(1, 61, dtype=float)
+    sin = 1.3 * np.sin(2 * np.pi * n / 8.5 + 0.2)
+    s, U, V, _ = oracle.svd(sin + 0.0, 25, 4)
+    g = oracle.grouped(s, U, V, [0, 0, -1, -1], 1)
+    assert np.allclose(g[0], sin, rtol=0, atol=1e-12)
+
+
 def test_cfg1_oracle_spectrum_structure():
     """cfg1 (BASELINE configs[0]): σ₁ dominated by the exponential trend, then the two
     sinusoid pairs, then noise (SURVEY Appendix A 'Spectrum structure')."""
