@@ -4,10 +4,39 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 #include "fft_smem.cuh"
 #include "ssa_internal.h"
 
 namespace ssa {
+
+// ------------------------------------------------------------------ programmatic dependent launch
+// Kernels of the host-driven sequences (long-series path) are launched with programmatic
+// stream serialization: the next kernel is scheduled while the previous one drains, and
+// waits at pdl_wait() (griddepcontrol.wait: the previous grid completed and its memory is
+// visible) before touching anything the previous kernels wrote.  Every kernel launched
+// with launch_pdl calls pdl_wait() first; without a programmatic dependency it returns
+// at once.  (No early griddepcontrol.launch_dependents: dependents parked on the SMs
+// during a grid's run slowed the long-series step down, 66.5 -> 70.4 ms at cfg3; the
+// implicit trigger at completion still removes the launch gap.)
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 // ------------------------------------------------------------------ reductions
 __device__ __forceinline__ double warp_sum(double v) {

@@ -94,6 +94,7 @@ struct ColFwdArgs {
 template <int LOGH>
 __global__ void __launch_bounds__(kThreads) lg_col_fwd(ColFwdArgs args, const double2* __restrict__ T1,
                                                        const double2* __restrict__ TWH) {
+  pdl_wait();
   using G = Geo<LOGH>;
   constexpr int N1 = G::N1, N2 = G::N2, CS = N1 + 1;  // odd column stride (16-byte units)
   constexpr int NE = (N1 * kColW + kThreads - 1) / kThreads;
@@ -159,6 +160,7 @@ struct ColInvArgs {
 template <int LOGH>
 __global__ void __launch_bounds__(kThreads) lg_col_inv(const double2* __restrict__ Y, const double2* __restrict__ T1,
                                                        ColInvArgs a) {
+  pdl_wait();
   using G = Geo<LOGH>;
   constexpr int N1 = G::N1, N2 = G::N2, CS = N1 + 1;
   constexpr int NE = (N1 * kColW + kThreads - 1) / kThreads;
@@ -328,6 +330,7 @@ __device__ __forceinline__ void row_pair_step(const RowArgs& a, size_t item, int
 template <int LOGH>
 __global__ void __launch_bounds__(kThreads) lg_row_cta(const double2* __restrict__ T2, const double2* __restrict__ TWH,
                                                        const double2* __restrict__ TWA, RowArgs a) {
+  pdl_wait();
   using G = Geo<LOGH>;
   constexpr int N1 = G::N1, N2 = G::N2;
   constexpr int NE = (N2 + kThreads - 1) / kThreads;
@@ -405,6 +408,7 @@ template <int LOGH>
 __global__ void __launch_bounds__(kThreads) lg_row_warp(const double2* __restrict__ T2,
                                                         const double2* __restrict__ TWH,
                                                         const double2* __restrict__ TWA, RowArgs a) {
+  pdl_wait();
   using Gm = Geo<LOGH>;
   constexpr int N1 = Gm::N1, N2 = Gm::N2;
   constexpr int NE = (N2 + 31) / 32;
@@ -539,7 +543,7 @@ static void col_fwd(const Plan& p, const ColFwdArgs& ca, int nz, int items, cuda
   const int logH = ilog2(p.H);
   const int N2 = 1 << (logH - logH / 2);
   const dim3 grid(N2 / kColW, items, nz);
-#define SSA_LG_CF(LG) lg_col_fwd<LG><<<grid, kThreads, col_smem(LG), s>>>(ca, p.d_tw1, p.d_tw4)
+#define SSA_LG_CF(LG) launch_pdl(lg_col_fwd<LG>, dim3(grid), dim3(kThreads), col_smem(LG), s, ca, p.d_tw1, p.d_tw4)
   SSA_LG_DISPATCH(logH, SSA_LG_CF)
 #undef SSA_LG_CF
 }
@@ -547,7 +551,7 @@ static void col_inv(const Plan& p, const double2* Y, const ColInvArgs& ca, int i
   const int logH = ilog2(p.H);
   const int N2 = 1 << (logH - logH / 2);
   const dim3 grid(N2 / kColW, items);
-#define SSA_LG_CI(LG) lg_col_inv<LG><<<grid, kThreads, col_smem(LG), s>>>(Y, p.d_tw1, ca)
+#define SSA_LG_CI(LG) launch_pdl(lg_col_inv<LG>, dim3(grid), dim3(kThreads), col_smem(LG), s, Y, p.d_tw1, ca)
   SSA_LG_DISPATCH(logH, SSA_LG_CI)
 #undef SSA_LG_CI
 }
@@ -557,12 +561,12 @@ static void rows(const Plan& p, const RowArgs& ra, int items, bool warp_rows, cu
   if (warp_rows) {
     const int G = kWarps / (ra.mode == 2 ? 4 : 2);
     const dim3 grid((N1 / 2 + G) / G, items);
-#define SSA_LG_RW(LG) lg_row_warp<LG><<<grid, kThreads, row_warp_smem(LG), s>>>(p.d_tw2, p.d_tw4, p.d_twp, ra)
+#define SSA_LG_RW(LG) launch_pdl(lg_row_warp<LG>, dim3(grid), dim3(kThreads), row_warp_smem(LG), s, p.d_tw2, p.d_tw4, p.d_twp, ra)
     SSA_LG_DISPATCH(logH, SSA_LG_RW)
 #undef SSA_LG_RW
   } else {
     const dim3 grid(N1 / 2 + 1, items);
-#define SSA_LG_RC(LG) lg_row_cta<LG><<<grid, kThreads, row_cta_smem(LG), s>>>(p.d_tw2, p.d_tw4, p.d_twp, ra)
+#define SSA_LG_RC(LG) launch_pdl(lg_row_cta<LG>, dim3(grid), dim3(kThreads), row_cta_smem(LG), s, p.d_tw2, p.d_tw4, p.d_twp, ra)
     SSA_LG_DISPATCH(logH, SSA_LG_RC)
 #undef SSA_LG_RC
   }

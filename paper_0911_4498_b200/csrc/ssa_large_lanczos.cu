@@ -52,6 +52,7 @@ struct LgScalars {
 };
 
 __global__ void lg_sum(const double* __restrict__ part, int n, double* out) {
+  pdl_wait();
   // one warp, fixed order: lane-strided partial sums then the shuffle tree
   double s = 0.0;
   for (int i = threadIdx.x; i < n; i += 32) s += part[i];
@@ -61,6 +62,7 @@ __global__ void lg_sum(const double* __restrict__ part, int n, double* out) {
 
 __global__ void __launch_bounds__(kThreads) lg_start(double* r, int n, int ld, uint64_t seed, uint64_t series,
                                                      double* part) {
+  pdl_wait();
   __shared__ double red[kWarps];
   double ss = 0.0;
   for (int t = blockIdx.x * kLgChunk + threadIdx.x; t < (blockIdx.x + 1) * kLgChunk && t < ld; t += blockDim.x) {
@@ -123,6 +125,7 @@ __device__ __forceinline__ double warp_sum8(double* v, int lane) {
 __global__ void __launch_bounds__(kThreads) lg_dots(const double* __restrict__ basis, int ld, int nb,
                                                     const double* __restrict__ r, double* part, int nchunk,
                                                     const LgScalars* sc, int pass) {
+  pdl_wait();
   if (pass == 1 && !sc->again) return;
   if (sc->stop) return;
   extern __shared__ double red[];  // [nb][kWarps]
@@ -170,6 +173,7 @@ __global__ void __launch_bounds__(kThreads) lg_dots(const double* __restrict__ b
 
 // h[row] = sum over CTAs (fixed order)
 __global__ void lg_rows(const double* __restrict__ part, int nb, int nchunk, double* h, const LgScalars* sc, int pass) {
+  pdl_wait();
   if (pass == 1 && !sc->again) return;
   if (sc->stop) return;
   const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
@@ -185,6 +189,7 @@ __global__ void lg_rows(const double* __restrict__ part, int nb, int nchunk, dou
 __global__ void __launch_bounds__(kThreads) lg_update(const double* __restrict__ basis, int ld, int nb,
                                                       const double* __restrict__ h, double* r, double* part,
                                                       const LgScalars* sc, int pass) {
+  pdl_wait();
   if (pass == 1 && !sc->again) return;
   if (sc->stop) return;
   __shared__ double red[kWarps];
@@ -237,6 +242,7 @@ __global__ void __launch_bounds__(kThreads) lg_update(const double* __restrict__
 
 // after a reorth pass: new norm from partials (fixed order), DGKS decision
 __global__ void lg_after_pass(const double* __restrict__ part, int nchunk, LgScalars* sc, int pass, int mode) {
+  pdl_wait();
   if (sc->stop) return;
   if (pass == 1 && !sc->again) return;
   double s = 0.0;
@@ -257,6 +263,7 @@ __global__ void lg_after_pass(const double* __restrict__ part, int nchunk, LgSca
 
 // coefficient = |r| (or 0 at breakdown); v = r / coef into the basis row
 __global__ void lg_coef(LgScalars* sc, double* coef_out, int step, int space_left) {
+  pdl_wait();
   if (threadIdx.x != 0) return;
   if (sc->stop) { *coef_out = 0.0; return; }
   const double nn = sc->nrm;
@@ -273,6 +280,7 @@ __global__ void lg_coef(LgScalars* sc, double* coef_out, int step, int space_lef
 
 __global__ void __launch_bounds__(kThreads) lg_normalize(const double* __restrict__ r, int n, int ld,
                                                          const double* coef, double* dst) {
+  pdl_wait();
   const double c = *coef;
   const double inv = (c > 0.0) ? 1.0 / c : 0.0;
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
@@ -282,6 +290,7 @@ __global__ void __launch_bounds__(kThreads) lg_normalize(const double* __restric
 // convergence test on B_m (tgk.cuh); alpha/beta 1-based in ab (alpha) and ab + w (beta)
 __global__ void __launch_bounds__(kThreads) lg_check(const double* __restrict__ ab, int w, int m, int k, double tol,
                                                      double* scratch, LgScalars* sc) {
+  pdl_wait();
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* c = reinterpret_cast<double*>(smem_raw);
   const int n = 2 * m + 1;
@@ -310,6 +319,7 @@ __global__ void __launch_bounds__(kThreads) lg_check(const double* __restrict__ 
 __global__ void __launch_bounds__(kThreads) lg_ritz(const double* __restrict__ basis, int ld, int rows,
                                                     const double* __restrict__ coef, int k, int n, double* out,
                                                     double* amax, int* aidx) {
+  pdl_wait();
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   double acc[kMaxK];
 #pragma unroll
@@ -358,6 +368,7 @@ __global__ void __launch_bounds__(kThreads) lg_ritz(const double* __restrict__ b
 
 __global__ void lg_sign(const double* __restrict__ amax, const int* __restrict__ aidx, int nblk, int k,
                         const double* __restrict__ U, int L, double* sgn) {
+  pdl_wait();
   const int i = threadIdx.x;
   if (i >= k) return;
   double v = -1.0;
@@ -371,6 +382,7 @@ __global__ void lg_sign(const double* __restrict__ amax, const int* __restrict__
 }
 
 __global__ void lg_flip(double* X, int n, int k, const double* __restrict__ sgn) {
+  pdl_wait();
   const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (size_t)n * k) return;
   const int i = (int)(idx / n);
@@ -387,6 +399,7 @@ cudaError_t large_lanczos_set_attributes(int m_max) {
 }
 
 __global__ void lg_set_nr(const double* __restrict__ part, int n, LgScalars* sc) {
+  pdl_wait();
   double s = 0.0;
   for (int i = threadIdx.x; i < n; i += 32) s += part[i];
   s = warp_sum(s);
@@ -398,12 +411,14 @@ __global__ void lg_set_nr(const double* __restrict__ part, int n, LgScalars* sc)
 }
 
 __global__ void lg_finite(const double* __restrict__ f, int N, int* state) {
+  pdl_wait();
   int bad = 0;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) bad |= !isfinite(f[i]);
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(state + 5, 1);
 }
 
 __global__ void lg_state(const LgScalars* sc, int* state, int m) {
+  pdl_wait();
   if (threadIdx.x != 0) return;
   state[0] = m;
   state[1] = sc->conv;
@@ -436,26 +451,26 @@ cudaError_t large_decompose_one(Plan& p, const DecomposeArgs& a0, int b, cudaStr
   double* r = p.d_lgr;
   cudaError_t e;
   if ((e = cudaMemsetAsync(p.d_state, 0, 8 * sizeof(int), s))) return e;
-  lg_finite<<<64, kThreads, 0, s>>>(a.series + (size_t)b * N, N, p.d_state);
+  launch_pdl(lg_finite, dim3(64), dim3(kThreads), 0, s, a.series + (size_t)b * N, N, p.d_state);
   if ((e = large_spectrum(p, a.series + (size_t)b * N, p.d_spec, 1, s))) return e;
   LgScalars z{};
   if ((e = cudaMemcpyAsync(sc, &z, sizeof(z), cudaMemcpyHostToDevice, s))) return e;
   if ((e = cudaMemsetAsync(p.d_ab, 0, 2 * (size_t)w * 8, s))) return e;
   // Alg. 1 lines 1-2: u_1 = p0 / |p0|
-  lg_start<<<nchL, kThreads, 0, s>>>(r, L, ldL, a.seed, (uint64_t)(b + a.series_base), part);
-  lg_set_nr<<<1, 32, 0, s>>>(part, nchL, sc);
+  launch_pdl(lg_start, dim3(nchL), dim3(kThreads), 0, s, r, L, ldL, a.seed, (uint64_t)(b + a.series_base), part);
+  launch_pdl(lg_set_nr, dim3(1), dim3(32), 0, s, part, nchL, sc);
   {
     // beta_1 = |p0| into beta[1], then normalize
-    lg_coef<<<1, 32, 0, s>>>(sc, beta + 1, 0, 1);
-    lg_normalize<<<(ldL + kThreads - 1) / kThreads, kThreads, 0, s>>>(r, L, ldL, beta + 1, U);
+    launch_pdl(lg_coef, dim3(1), dim3(32), 0, s, sc, beta + 1, 0, 1);
+    launch_pdl(lg_normalize, dim3((ldL + kThreads - 1) / kThreads), dim3(kThreads), 0, s, r, L, ldL, beta + 1, U);
   }
   auto reorth = [&](const double* basis, int ld, int nb, int) {
     const int nch = (ld + kRoChunk - 1) / kRoChunk;
     for (int pass = 0; pass < 2 && nb > 0; ++pass) {
-      lg_dots<<<nch, kThreads, (size_t)nb * kWarps * 8, s>>>(basis, ld, nb, r, part, nch, sc, pass);
-      lg_rows<<<(nb * 32 + kThreads - 1) / kThreads, kThreads, 0, s>>>(part, nb, nch, h, sc, pass);
-      lg_update<<<nch, kThreads, (size_t)(nb > 0 ? nb : 1) * 8, s>>>(basis, ld, nb, h, r, part, sc, pass);
-      lg_after_pass<<<1, 32, 0, s>>>(part, nch, sc, pass, p.opt.reorth);
+      launch_pdl(lg_dots, dim3(nch), dim3(kThreads), (size_t)nb * kWarps * 8, s, basis, ld, nb, r, part, nch, sc, pass);
+      launch_pdl(lg_rows, dim3((nb * 32 + kThreads - 1) / kThreads), dim3(kThreads), 0, s, part, nb, nch, h, sc, pass);
+      launch_pdl(lg_update, dim3(nch), dim3(kThreads), (size_t)(nb > 0 ? nb : 1) * 8, s, basis, ld, nb, h, r, part, sc, pass);
+      launch_pdl(lg_after_pass, dim3(1), dim3(32), 0, s, part, nch, sc, pass, p.opt.reorth);
     }
   };
   int m = 0;
@@ -469,14 +484,14 @@ cudaError_t large_decompose_one(Plan& p, const DecomposeArgs& a0, int b, cudaStr
     if ((e = large_correlate(p, p.d_spec, 0, U + (size_t)(j - 1) * ldL, 0, L, r, 0, K, ldK,
                              (j > 1) ? V + (size_t)(j - 2) * ldK : nullptr, 0, beta + j, part, 1, s)))
       return e;
-    lg_set_nr<<<1, 32, 0, s>>>(part, ncol, sc);
+    launch_pdl(lg_set_nr, dim3(1), dim3(32), 0, s, part, ncol, sc);
     reorth(V, ldK, j - 1, nchK);
-    lg_coef<<<1, 32, 0, s>>>(sc, alpha + j, j, j - 1 < K);
-    lg_normalize<<<(ldK + kThreads - 1) / kThreads, kThreads, 0, s>>>(r, K, ldK, alpha + j, V + (size_t)(j - 1) * ldK);
+    launch_pdl(lg_coef, dim3(1), dim3(32), 0, s, sc, alpha + j, j, j - 1 < K);
+    launch_pdl(lg_normalize, dim3((ldK + kThreads - 1) / kThreads), dim3(kThreads), 0, s, r, K, ldK, alpha + j, V + (size_t)(j - 1) * ldK);
     m = j - 1;
     const bool last = (m >= p.m_max);
     if (m >= k && (m >= next_check || last)) {
-      lg_check<<<1, kThreads, lg_check_smem(p.m_max), s>>>(p.d_ab, w, m, k, p.opt.tol, p.d_tgk, sc);
+      launch_pdl(lg_check, dim3(1), dim3(kThreads), lg_check_smem(p.m_max), s, p.d_ab, w, m, k, p.opt.tol, p.d_tgk, sc);
       if ((e = cudaMemcpyAsync(&hs, sc, sizeof(hs), cudaMemcpyDeviceToHost, s))) return e;
       if ((e = cudaStreamSynchronize(s))) return e;
       if (hs.conv) break;
@@ -496,12 +511,12 @@ cudaError_t large_decompose_one(Plan& p, const DecomposeArgs& a0, int b, cudaStr
     if ((e = large_correlate(p, p.d_spec, 0, V + (size_t)(j - 1) * ldK, 0, K, r, 0, L, ldL,
                              U + (size_t)(j - 1) * ldL, 0, alpha + j, part, 1, s)))
       return e;
-    lg_set_nr<<<1, 32, 0, s>>>(part, ncol, sc);
+    launch_pdl(lg_set_nr, dim3(1), dim3(32), 0, s, part, ncol, sc);
     reorth(U, ldL, j, nchL);
-    lg_coef<<<1, 32, 0, s>>>(sc, beta + j + 1, j, j < L);
-    lg_normalize<<<(ldL + kThreads - 1) / kThreads, kThreads, 0, s>>>(r, L, ldL, beta + j + 1, U + (size_t)j * ldL);
+    launch_pdl(lg_coef, dim3(1), dim3(32), 0, s, sc, beta + j + 1, j, j < L);
+    launch_pdl(lg_normalize, dim3((ldL + kThreads - 1) / kThreads), dim3(kThreads), 0, s, r, L, ldL, beta + j + 1, U + (size_t)j * ldL);
   }
-  lg_state<<<1, 32, 0, s>>>(sc, p.d_state, m);
+  launch_pdl(lg_state, dim3(1), dim3(32), 0, s, sc, p.d_state, m);
   // ---- bidiagonal SVD (reuses the batched kernel with one series) ----
   if ((e = cudaMemsetAsync(p.d_counters, 0, 4 * sizeof(int), s))) return e;
   if ((e = launch_bidiag_svd(p, a, s))) return e;
@@ -514,11 +529,11 @@ cudaError_t large_decompose_one(Plan& p, const DecomposeArgs& a0, int b, cudaStr
   const int gU = (L + kThreads - 1) / kThreads, gV = (K + kThreads - 1) / kThreads;
   double* amax = p.d_lgpart;
   int* aidx = reinterpret_cast<int*>(p.d_lgpart + (size_t)gU * k);
-  lg_ritz<<<gU, kThreads, 0, s>>>(U, ldL, m + 1, cP, k, L, Uo, amax, aidx);
-  lg_ritz<<<gV, kThreads, 0, s>>>(V, ldK, m, cQ, k, K, Vo, nullptr, nullptr);
-  lg_sign<<<1, 32, 0, s>>>(amax, aidx, gU, k, Uo, L, h);
-  lg_flip<<<(int)(((size_t)L * k + kThreads - 1) / kThreads), kThreads, 0, s>>>(Uo, L, k, h);
-  lg_flip<<<(int)(((size_t)K * k + kThreads - 1) / kThreads), kThreads, 0, s>>>(Vo, K, k, h);
+  launch_pdl(lg_ritz, dim3(gU), dim3(kThreads), 0, s, U, ldL, m + 1, cP, k, L, Uo, amax, aidx);
+  launch_pdl(lg_ritz, dim3(gV), dim3(kThreads), 0, s, V, ldK, m, cQ, k, K, Vo, nullptr, nullptr);
+  launch_pdl(lg_sign, dim3(1), dim3(32), 0, s, amax, aidx, gU, k, Uo, L, h);
+  launch_pdl(lg_flip, dim3((int)(((size_t)L * k + kThreads - 1) / kThreads)), dim3(kThreads), 0, s, Uo, L, k, h);
+  launch_pdl(lg_flip, dim3((int)(((size_t)K * k + kThreads - 1) / kThreads)), dim3(kThreads), 0, s, Vo, K, k, h);
   return cudaGetLastError();
 }
 
