@@ -10,7 +10,7 @@
 //                every warp streams whole basis rows of that chunk; per-CTA partials are
 //                then summed in a fixed order (deterministic);
 //   update       r -= B h with the rows in reverse order (recently read rows hit L2);
-//   finish       one thread: norms, the DGKS decision for a second pass, breakdown,
+//   finish       one warp (lg_finish): norms, the DGKS decision for a second pass, breakdown,
 //                alpha_j / beta_{j+1} in device memory; second-pass kernels read the flag
 //                and return at once when it is not needed;
 //   normalize    v = r / alpha into the basis row.
@@ -240,43 +240,56 @@ __global__ void __launch_bounds__(kThreads) lg_update(const double* __restrict__
   }
 }
 
-// after a reorth pass: new norm from partials (fixed order), DGKS decision
-__global__ void lg_after_pass(const double* __restrict__ part, int nchunk, LgScalars* sc, int pass, int mode) {
+// Norm bookkeeping at the end of a reorthogonalization pass, one warp (replaces the
+// separate |r| / DGKS / coefficient kernels):
+//   pass 0: nr = |r| before reorth from the correlation partials (cpart[ncol]); with a
+//           reorth pass (nb > 0) |r| from the update partials (part[nch]) and the DGKS
+//           decision (second pass if |r| < nr / sqrt 2, or always for mode 2);
+//   pass 1: runs only after a second pass: |r| from its update partials;
+// then, unless a second pass follows, the Lanczos coefficient |r| (or 0 at breakdown,
+// DESIGN.md R11) into coef_out.  Partial sums in a fixed order (deterministic).
+__global__ void lg_finish(const double* __restrict__ cpart, int ncol, const double* __restrict__ part, int nch, int nb,
+                          LgScalars* sc, int pass, int mode, double* coef_out, int step) {
   pdl_wait();
-  if (sc->stop) return;
   if (pass == 1 && !sc->again) return;
-  double s = 0.0;
-  for (int i = threadIdx.x; i < nchunk; i += 32) s += part[i];
-  s = warp_sum(s);
-  if (threadIdx.x == 0) {
-    const double nn = sqrt(s);
-    const double before = (pass == 0) ? sc->nr : sc->nrm;
-    sc->nrm = nn;
-    if (pass == 0) {
-      sc->again = (mode == 2 || nn < 0.70710678118654752 * before) ? 1 : 0;
-      if (sc->again) sc->extra += 1;
-    } else {
-      sc->again = 0;
-    }
+  if (sc->stop) {
+    if (pass == 0 && threadIdx.x == 0) *coef_out = 0.0;
+    return;
   }
-}
-
-// coefficient = |r| (or 0 at breakdown); v = r / coef into the basis row
-__global__ void lg_coef(LgScalars* sc, double* coef_out, int step, int space_left) {
-  pdl_wait();
+  double s1 = 0.0, s2 = 0.0;
+  if (pass == 0)
+    for (int i = threadIdx.x; i < ncol; i += 32) s1 += cpart[i];
+  if (nb > 0)
+    for (int i = threadIdx.x; i < nch; i += 32) s2 += part[i];
+  s1 = warp_sum(s1);
+  s2 = warp_sum(s2);
   if (threadIdx.x != 0) return;
-  if (sc->stop) { *coef_out = 0.0; return; }
-  const double nn = sc->nrm;
+  int again = 0;
+  double nn;
+  if (pass == 0) {
+    const double nr = sqrt(s1);
+    sc->nr = nr;
+    nn = (nb > 0) ? sqrt(s2) : nr;
+    if (nb > 0) {
+      again = (mode == 2 || nn < 0.70710678118654752 * nr) ? 1 : 0;
+      if (again) sc->extra += 1;
+    }
+  } else {
+    nn = sqrt(s2);
+  }
+  sc->nrm = nn;
+  sc->again = again;
+  if (again) return;
   if (!(nn > 1e-12 * sc->runmax) || nn == 0.0) {
     if (!sc->breakdown) sc->breakdown = step;
     *coef_out = 0.0;
     sc->stop = 1;  // invariant subspace found: no restart on the long path (R11)
-    (void)space_left;
   } else {
     *coef_out = nn;
     if (step > 0) sc->runmax = fmax(sc->runmax, nn);  // beta_1 (start vector norm) excluded
   }
 }
+
 
 __global__ void __launch_bounds__(kThreads) lg_normalize(const double* __restrict__ r, int n, int ld,
                                                          const double* coef, double* dst) {
@@ -398,17 +411,6 @@ cudaError_t large_lanczos_set_attributes(int m_max) {
   return e;
 }
 
-__global__ void lg_set_nr(const double* __restrict__ part, int n, LgScalars* sc) {
-  pdl_wait();
-  double s = 0.0;
-  for (int i = threadIdx.x; i < n; i += 32) s += part[i];
-  s = warp_sum(s);
-  if (threadIdx.x == 0) {
-    sc->nr = sqrt(s);
-    sc->nrm = sc->nr;
-    sc->again = 0;
-  }
-}
 
 __global__ void lg_finite(const double* __restrict__ f, int N, int* state) {
   pdl_wait();
@@ -436,7 +438,7 @@ cudaError_t large_decompose_one(Plan& p, const DecomposeArgs& a0, int b, cudaStr
   a.nb = 1;
   const int L = (int)p.L, K = (int)p.K, N = (int)p.N, k = p.k;
   const int ldL = p.ldL, ldK = p.ldK;
-  const int nchL = (ldL + kLgChunk - 1) / kLgChunk, nchK = (ldK + kLgChunk - 1) / kLgChunk;
+  const int nchL = (ldL + kLgChunk - 1) / kLgChunk;
   int N1, N2;
   large_geom(p, &N1, &N2);
   const int ncol = N2 / 8;  // partial sums written by large_col_inv
@@ -457,20 +459,24 @@ cudaError_t large_decompose_one(Plan& p, const DecomposeArgs& a0, int b, cudaStr
   if ((e = cudaMemcpyAsync(sc, &z, sizeof(z), cudaMemcpyHostToDevice, s))) return e;
   if ((e = cudaMemsetAsync(p.d_ab, 0, 2 * (size_t)w * 8, s))) return e;
   // Alg. 1 lines 1-2: u_1 = p0 / |p0|
-  launch_pdl(lg_start, dim3(nchL), dim3(kThreads), 0, s, r, L, ldL, a.seed, (uint64_t)(b + a.series_base), part);
-  launch_pdl(lg_set_nr, dim3(1), dim3(32), 0, s, part, nchL, sc);
-  {
-    // beta_1 = |p0| into beta[1], then normalize
-    launch_pdl(lg_coef, dim3(1), dim3(32), 0, s, sc, beta + 1, 0, 1);
-    launch_pdl(lg_normalize, dim3((ldL + kThreads - 1) / kThreads), dim3(kThreads), 0, s, r, L, ldL, beta + 1, U);
-  }
-  auto reorth = [&](const double* basis, int ld, int nb, int) {
+  // partial sums of the correlation / start vector go after the dots partials (the
+  // reorth kernels overwrite `part`)
+  double* cpart = part + (size_t)((std::max(ldL, ldK) + kRoChunk - 1) / kRoChunk) * (p.m_max + 2);
+  launch_pdl(lg_start, dim3(nchL), dim3(kThreads), 0, s, r, L, ldL, a.seed, (uint64_t)(b + a.series_base), cpart);
+  // beta_1 = |p0| into beta[1], then u_1 = p0 / beta_1
+  launch_pdl(lg_finish, dim3(1), dim3(32), 0, s, cpart, nchL, part, 0, 0, sc, 0, p.opt.reorth, beta + 1, 0);
+  launch_pdl(lg_normalize, dim3((ldL + kThreads - 1) / kThreads), dim3(kThreads), 0, s, r, L, ldL, beta + 1, U);
+  // reorth against nb basis rows (CGS + DGKS), then the coefficient into coef
+  auto reorth = [&](const double* basis, int ld, int nb, double* coef, int step) {
     const int nch = (ld + kRoChunk - 1) / kRoChunk;
-    for (int pass = 0; pass < 2 && nb > 0; ++pass) {
-      launch_pdl(lg_dots, dim3(nch), dim3(kThreads), (size_t)nb * kWarps * 8, s, basis, ld, nb, r, part, nch, sc, pass);
-      launch_pdl(lg_rows, dim3((nb * 32 + kThreads - 1) / kThreads), dim3(kThreads), 0, s, part, nb, nch, h, sc, pass);
-      launch_pdl(lg_update, dim3(nch), dim3(kThreads), (size_t)(nb > 0 ? nb : 1) * 8, s, basis, ld, nb, h, r, part, sc, pass);
-      launch_pdl(lg_after_pass, dim3(1), dim3(32), 0, s, part, nch, sc, pass, p.opt.reorth);
+    for (int pass = 0; pass < 2; ++pass) {
+      if (nb > 0) {
+        launch_pdl(lg_dots, dim3(nch), dim3(kThreads), (size_t)nb * kWarps * 8, s, basis, ld, nb, r, part, nch, sc, pass);
+        launch_pdl(lg_rows, dim3((nb * 32 + kThreads - 1) / kThreads), dim3(kThreads), 0, s, part, nb, nch, h, sc, pass);
+        launch_pdl(lg_update, dim3(nch), dim3(kThreads), (size_t)nb * 8, s, basis, ld, nb, h, r, part, sc, pass);
+      }
+      launch_pdl(lg_finish, dim3(1), dim3(32), 0, s, cpart, ncol, part, nch, nb, sc, pass, p.opt.reorth, coef, step);
+      if (nb == 0) break;
     }
   };
   int m = 0;
@@ -482,11 +488,9 @@ cudaError_t large_decompose_one(Plan& p, const DecomposeArgs& a0, int b, cudaStr
   for (int j = 1; j <= p.m_max + 1; ++j) {
     // ---- half-step A (Alg. 1 l.4-5): r = X^T u_j - beta_j v_{j-1}; FRO vs V_{j-1} ----
     if ((e = large_correlate(p, p.d_spec, 0, U + (size_t)(j - 1) * ldL, 0, L, r, 0, K, ldK,
-                             (j > 1) ? V + (size_t)(j - 2) * ldK : nullptr, 0, beta + j, part, 1, s)))
+                             (j > 1) ? V + (size_t)(j - 2) * ldK : nullptr, 0, beta + j, cpart, 1, s)))
       return e;
-    launch_pdl(lg_set_nr, dim3(1), dim3(32), 0, s, part, ncol, sc);
-    reorth(V, ldK, j - 1, nchK);
-    launch_pdl(lg_coef, dim3(1), dim3(32), 0, s, sc, alpha + j, j, j - 1 < K);
+    reorth(V, ldK, j - 1, alpha + j, j);
     launch_pdl(lg_normalize, dim3((ldK + kThreads - 1) / kThreads), dim3(kThreads), 0, s, r, K, ldK, alpha + j, V + (size_t)(j - 1) * ldK);
     m = j - 1;
     const bool last = (m >= p.m_max);
@@ -509,11 +513,9 @@ cudaError_t large_decompose_one(Plan& p, const DecomposeArgs& a0, int b, cudaStr
     if (last) break;
     // ---- half-step B (Alg. 1 l.6-7): p = X v_j - alpha_j u_j; FRO vs U_j ----
     if ((e = large_correlate(p, p.d_spec, 0, V + (size_t)(j - 1) * ldK, 0, K, r, 0, L, ldL,
-                             U + (size_t)(j - 1) * ldL, 0, alpha + j, part, 1, s)))
+                             U + (size_t)(j - 1) * ldL, 0, alpha + j, cpart, 1, s)))
       return e;
-    launch_pdl(lg_set_nr, dim3(1), dim3(32), 0, s, part, ncol, sc);
-    reorth(U, ldL, j, nchL);
-    launch_pdl(lg_coef, dim3(1), dim3(32), 0, s, sc, beta + j + 1, j, j < L);
+    reorth(U, ldL, j, beta + j + 1, j);
     launch_pdl(lg_normalize, dim3((ldL + kThreads - 1) / kThreads), dim3(kThreads), 0, s, r, L, ldL, beta + j + 1, U + (size_t)j * ldL);
   }
   launch_pdl(lg_state, dim3(1), dim3(32), 0, s, sc, p.d_state, m);
