@@ -453,6 +453,16 @@ extern "C" ssa_status ssa_decompose(ssa_plan_t plan, const double* d_series, dou
   a.N = (int)p.N; a.L = (int)p.L; a.K = (int)p.K; a.M = (int)p.M; a.H = (int)p.H; a.k = p.k;
   a.m_max = p.m_max; a.ldL = p.ldL; a.ldK = p.ldK;
   a.check_every = p.opt.check_every; a.reorth_mode = p.opt.reorth;
+  {
+    // first test after 3k + 8 steps (no cfg1/cfg2 series converged before ~3.5k), then
+    // every check_every steps, stretched up to 3 check_every when the residual decays
+    // geometrically (R7); SSA_FIRST_CHECK / SSA_CHECK_CAP override (tuning)
+    const int ce = p.opt.check_every > 0 ? p.opt.check_every : 4;
+    a.first_check = 3 * p.k + 8;
+    a.check_cap = 3 * ce;
+    if (const char* e = getenv("SSA_FIRST_CHECK")) a.first_check = std::max(p.k, atoi(e));
+    if (const char* e = getenv("SSA_CHECK_CAP")) a.check_cap = std::max(ce, atoi(e));
+  }
   a.tol = p.opt.tol; a.seed = p.opt.seed; a.series_base = p.series_base;
   a.series = d_series; a.spec = p.d_spec; a.tw = p.d_twl;
   a.U = p.d_U; a.V = p.d_V; a.ab = p.d_ab; a.state = p.d_state;

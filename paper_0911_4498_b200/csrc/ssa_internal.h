@@ -22,6 +22,7 @@ inline size_t fft_bytes(int H) { return (size_t)H * 16; }
 struct DecomposeArgs {
   int N, L, K, M, H, k, m_max, ldL, ldK;
   int check_every, reorth_mode;
+  int first_check, check_cap;  // step of the first convergence test; longest stretch between tests
   int b0, nb;
   double tol;
   uint64_t seed;

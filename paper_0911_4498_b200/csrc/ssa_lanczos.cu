@@ -276,7 +276,7 @@ __global__ void __launch_bounds__(kThreads, 2) lanczos_kernel(const DecomposeArg
 
     double runmax = 0.0, bcur = beta1;
     int m = 0, converged = 0, breakdown = 0, extra = 0, restarts = 0, checks = 0;
-    int next_check = (2 * k + 8 < a.m_max) ? 2 * k + 8 : k;
+    int next_check = (a.first_check < a.m_max) ? a.first_check : k;
     double prev_res = -1.0;
     int prev_m = 0;
     const int ce = a.check_every > 0 ? a.check_every : 4;
@@ -361,7 +361,7 @@ __global__ void __launch_bounds__(kThreads, 2) lanczos_kernel(const DecomposeArg
           double rate = log(rel / prev_res) / (double)(m - prev_m);
           double need = log(0.5 * a.tol / rel) / rate;
           int s2 = (int)(0.7 * need);
-          if (s2 > step) step = s2 < 2 * ce ? s2 : 2 * ce;
+          if (s2 > step) step = s2 < a.check_cap ? s2 : a.check_cap;
         }
         prev_res = rel;
         prev_m = m;
