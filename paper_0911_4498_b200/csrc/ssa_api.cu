@@ -572,6 +572,7 @@ extern "C" ssa_status ssa_run_host(ssa_plan_t plan, const double* h_series, doub
   // the outputs (32 x the input bytes at cfg2) hides behind the compute of later slices.
   int nsl = 1;
   if (!p.large && B >= 512) nsl = 4;
+  if (!p.large && B >= 2048) nsl = 8;  // cfg2 (4096 series): e2e 254K (4 slices) -> 271K eigentriples/s
   if (const char* e = getenv("SSA_HOST_SLICES")) nsl = std::max(1, std::min(Plan::kMaxSlices, atoi(e)));
   if (nsl > 1 && (int64_t)B >= 2 * nsl) {
     const int64_t sb = ((int64_t)B + nsl - 1) / nsl;
