@@ -79,6 +79,16 @@ __device__ __forceinline__ void twiddle_seq(const double2* __restrict__ th, long
   }
 }
 
+// 1/c for an integer count c >= 1, to within an ulp: float reciprocal, two Newton steps
+// in fp64 (no fp64 division and its slow-path branch in the hot epilogue).
+__device__ __forceinline__ double rcp_count(int c) {
+  const double cd = (double)c;
+  double r = (double)__frcp_rn((float)c);
+  r = fma(r, fma(-cd, r, 1.0), r);
+  r = fma(r, fma(-cd, r, 1.0), r);
+  return r;
+}
+
 // ---- pass 1: forward column FFTs on packed real input x (len n_in) -------------------
 struct ColFwdIn {
   const double* x;  // [items][xs] real
@@ -106,13 +116,14 @@ __global__ void __launch_bounds__(kThreads) lg_col_fwd(ColFwdArgs args, const do
   const int n2_0 = blockIdx.x * kColW;
   const double* xi = a.x + (size_t)blockIdx.y * a.xs;
   double2* Yi = a.Y + (size_t)blockIdx.y * G::H;
+  // thread t: column c = t & 7 of the CTA, rows n1 = (t >> 3) + 32 j (idx = t + 256 j)
+  const int cc = threadIdx.x & (kColW - 1), r0 = threadIdx.x >> 3;
+  const int i00 = 2 * (n2_0 + cc + N2 * r0);  // packed point n = n2 + N2 n1 -> x_2n, x_2n+1
   double2 v[NE];
 #pragma unroll
   for (int j = 0; j < NE; ++j) {
-    const int idx = threadIdx.x + j * kThreads;
-    const int c = idx & (kColW - 1), n1 = idx >> 3;
-    const long long i0 = 2 * ((long long)(n2_0 + c) + (long long)N2 * n1);
-    const bool ok = idx < N1 * kColW;
+    const bool ok = threadIdx.x + j * kThreads < N1 * kColW;
+    const int i0 = i00 + j * (2 * N2 * (kThreads / kColW));
     if (a.vec && ok && i0 + 1 < a.n_in) {
       v[j] = __ldg(reinterpret_cast<const double2*>(xi + i0));
     } else {
@@ -121,10 +132,8 @@ __global__ void __launch_bounds__(kThreads) lg_col_fwd(ColFwdArgs args, const do
     }
   }
 #pragma unroll
-  for (int j = 0; j < NE; ++j) {
-    const int idx = threadIdx.x + j * kThreads;
-    if (idx < N1 * kColW) buf[(idx & (kColW - 1)) * CS + fsw(idx >> 3)] = v[j];
-  }
+  for (int j = 0; j < NE; ++j)
+    if (threadIdx.x + j * kThreads < N1 * kColW) buf[cc * CS + fsw(r0 + (kThreads / kColW) * j)] = v[j];
   __syncthreads();
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   fft_run_t<G::L1, false>(buf + w * CS, tw1, lane, 32, WarpSync());
@@ -171,17 +180,16 @@ __global__ void __launch_bounds__(kThreads) lg_col_inv(const double2* __restrict
   const int n2_0 = blockIdx.x * kColW;
   const size_t item = blockIdx.y;
   const double2* Yi = Y + item * G::H;
+  // thread t: column c = t & 7, rows n1 = (t >> 3) + 32 j (as in lg_col_fwd)
+  const int cc = threadIdx.x & (kColW - 1), r0 = threadIdx.x >> 3;
+  constexpr int RS = kThreads / kColW;  // row step between a thread's elements
   double2 v[NE];
 #pragma unroll
-  for (int j = 0; j < NE; ++j) {
-    const int idx = threadIdx.x + j * kThreads;
-    if (idx < N1 * kColW) v[j] = Yi[(size_t)(n2_0 + (idx & (kColW - 1))) + (size_t)N2 * (idx >> 3)];
-  }
+  for (int j = 0; j < NE; ++j)
+    if (threadIdx.x + j * kThreads < N1 * kColW) v[j] = Yi[n2_0 + cc + N2 * (r0 + RS * j)];
 #pragma unroll
-  for (int j = 0; j < NE; ++j) {
-    const int idx = threadIdx.x + j * kThreads;
-    if (idx < N1 * kColW) buf[(idx & (kColW - 1)) * CS + fsw(rev_t<G::L1>(idx >> 3))] = v[j];
-  }
+  for (int j = 0; j < NE; ++j)
+    if (threadIdx.x + j * kThreads < N1 * kColW) buf[cc * CS + fsw(rev_t<G::L1>(r0 + RS * j))] = v[j];
   __syncthreads();
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   fft_run_t<G::L1, true>(buf + w * CS, tw1, lane, 32, WarpSync());
@@ -191,30 +199,34 @@ __global__ void __launch_bounds__(kThreads) lg_col_inv(const double2* __restrict
   const double cf = (a.mode == 0 && a.coef) ? a.coef[item] : 0.0;
   const double sg = (a.mode == 1) ? a.sigma[item] : 0.0;
   const int mn = a.L < a.K ? a.L : a.K;
-  constexpr int NO = (2 * N1 * kColW + kThreads - 1) / kThreads;
+  // thread t handles the packed points n = n2 + N2 n1 of its column c, rows n1 = r0 + 32 j:
+  // real outputs t = 2n (z.x) and 2n + 1 (z.y)
+  const int n2 = n2_0 + cc;
   if (a.mode == 0) {
     const double* pv = a.prev ? a.prev + item * a.prev_stride : nullptr;
-    double pr[NO];
+    double* o = a.out + item * a.out_stride;
+    double2 pr[NE];
 #pragma unroll
-    for (int j = 0; j < NO; ++j) {  // previous-vector loads first, all in flight
-      const int idx = threadIdx.x + j * kThreads;
-      const int h = idx & 1, rest = idx >> 1;
-      const long long t = 2 * ((long long)(n2_0 + (rest & (kColW - 1))) + (long long)N2 * (rest >> 3)) + h;
-      pr[j] = (pv && idx < 2 * N1 * kColW && t < a.n_out) ? __ldg(pv + t) : 0.0;
+    for (int j = 0; j < NE; ++j) {  // previous-vector loads first, all in flight
+      const int t = 2 * (n2 + N2 * (r0 + RS * j));
+      const bool ok = threadIdx.x + j * kThreads < N1 * kColW;
+      pr[j].x = (pv && ok && t < a.n_out) ? __ldg(pv + t) : 0.0;
+      pr[j].y = (pv && ok && t + 1 < a.n_out) ? __ldg(pv + t + 1) : 0.0;
     }
 #pragma unroll
-    for (int j = 0; j < NO; ++j) {
-      const int idx = threadIdx.x + j * kThreads;
-      if (idx < 2 * N1 * kColW) {
-        // element t = 2n + h of the real output, n = n2 + N2 n1
-        const int h = idx & 1, rest = idx >> 1;
-        const int c = rest & (kColW - 1), n1 = rest >> 3;
-        const long long t = 2 * ((long long)(n2_0 + c) + (long long)N2 * n1) + h;
-        const double2 z = buf[c * CS + fsw(n1)];
+    for (int j = 0; j < NE; ++j) {
+      if (threadIdx.x + j * kThreads < N1 * kColW) {
+        const int n1 = r0 + RS * j;
+        const int t = 2 * (n2 + N2 * n1);
+        const double2 z = buf[cc * CS + fsw(n1)];
         if (t < a.ld_out) {
-          double y = 0.0;
-          if (t < a.n_out) y = fma(-cf, pr[j], (h ? z.y : z.x) * invH);
-          a.out[item * a.out_stride + t] = y;
+          const double y = (t < a.n_out) ? fma(-cf, pr[j].x, z.x * invH) : 0.0;
+          o[t] = y;
+          ss = fma(y, y, ss);
+        }
+        if (t + 1 < a.ld_out) {
+          const double y = (t + 1 < a.n_out) ? fma(-cf, pr[j].y, z.y * invH) : 0.0;
+          o[t + 1] = y;
           ss = fma(y, y, ss);
         }
       }
@@ -230,21 +242,22 @@ __global__ void __launch_bounds__(kThreads) lg_col_inv(const double2* __restrict
       }
     }
   } else {
+    // g_t = sigma y_t / c_t, c_t = min(t + 1, min(L, K), N - t) (R2)
     double* o = a.out + item * a.out_stride;
+    const double scale = sg * invH;
 #pragma unroll
-    for (int j = 0; j < NO; ++j) {
-      const int idx = threadIdx.x + j * kThreads;
-      if (idx < 2 * N1 * kColW) {
-        const int h = idx & 1, rest = idx >> 1;
-        const int c = rest & (kColW - 1), n1 = rest >> 3;
-        const long long t = 2 * ((long long)(n2_0 + c) + (long long)N2 * n1) + h;
+    for (int j = 0; j < NE; ++j) {
+      if (threadIdx.x + j * kThreads < N1 * kColW) {
+        const int n1 = r0 + RS * j;
+        const int t = 2 * (n2 + N2 * n1);
         if (t < a.N) {
-          const double2 z = buf[c * CS + fsw(n1)];
-          const long long k1 = t + 1;
-          long long cnt = k1;
-          if (cnt > mn) cnt = mn;
-          if (a.N - k1 + 1 < cnt) cnt = a.N - k1 + 1;
-          o[t] = sg * ((h ? z.y : z.x) * invH) / (double)cnt;
+          const double2 z = buf[cc * CS + fsw(n1)];
+          const int c0 = min(min(t + 1, mn), a.N - t);
+          o[t] = z.x * scale * rcp_count(c0);
+          if (t + 1 < a.N) {
+            const int c1 = min(min(t + 2, mn), a.N - t - 1);
+            o[t + 1] = z.y * scale * rcp_count(c1);
+          }
         }
       }
     }
