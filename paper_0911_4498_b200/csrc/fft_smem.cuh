@@ -235,18 +235,18 @@ struct CtaSync {
 // Forward FFT of H points in place (natural -> digit-reversed).  Caller must have
 // synchronized after writing buf; returns after a final barrier.
 // Whole transform with a compile-time size (all index arithmetic folds to constants).
-template <int LOGH, int P, bool INV, class TW, class Sync>
+template <int LOGH, int P, bool INV, int PMIN = 0, class TW, class Sync>
 __device__ __forceinline__ void fft_radix8_passes(double2* buf, const TW& T, int tid, int nthr, Sync sync) {
-  // passes P..N8-1 forward (INV: N8-1..P, called with P counting down from the top)
-  if constexpr (P >= 0 && P < LOGH / 3) {
+  // passes P..N8-1 forward (INV: N8-1..PMIN, called with P counting down from the top)
+  if constexpr (P >= PMIN && P < LOGH / 3) {
     if constexpr (!INV) {
       fft_pass_t<LOGH, LOGH - 3 * P, 3, false>(buf, T, tid, nthr);
       sync();
-      fft_radix8_passes<LOGH, P + 1, false>(buf, T, tid, nthr, sync);
+      fft_radix8_passes<LOGH, P + 1, false, PMIN>(buf, T, tid, nthr, sync);
     } else {
       fft_pass_t<LOGH, LOGH - 3 * P, 3, true>(buf, T, tid, nthr);
       sync();
-      fft_radix8_passes<LOGH, P - 1, true>(buf, T, tid, nthr, sync);
+      fft_radix8_passes<LOGH, P - 1, true, PMIN>(buf, T, tid, nthr, sync);
     }
   }
 }
@@ -262,6 +262,72 @@ __device__ __forceinline__ void fft_run_t(double2* buf, const TW& T, int tid, in
     if constexpr (LB == 2) { fft_pass_t<LOGH, 2, 2, true>(buf, T, tid, nthr); sync(); }
     if constexpr (LB == 1) { fft_pass_t<LOGH, 1, 1, true>(buf, T, tid, nthr); sync(); }
     fft_radix8_passes<LOGH, N8 - 1, true>(buf, T, tid, nthr, sync);
+  }
+}
+
+// The same transform without its outermost radix-8 pass (block 2^LOGH): forward runs
+// passes 1.. (the caller did pass 0 in registers, dif_pass0_store), inverse stops before
+// pass 0 (the caller finishes it in registers, dif_pass0_inverse_load).  LOGH >= 3.
+template <int LOGH, bool INV, class TW, class Sync>
+__device__ __forceinline__ void fft_run_inner_t(double2* buf, const TW& T, int tid, int nthr, Sync sync) {
+  constexpr int N8 = LOGH / 3, LB = LOGH - 3 * N8;
+  if constexpr (!INV) {
+    fft_radix8_passes<LOGH, 1, false>(buf, T, tid, nthr, sync);
+    if constexpr (LB == 2) { fft_pass_t<LOGH, 2, 2, false>(buf, T, tid, nthr); sync(); }
+    if constexpr (LB == 1) { fft_pass_t<LOGH, 1, 1, false>(buf, T, tid, nthr); sync(); }
+  } else {
+    if constexpr (LB == 2) { fft_pass_t<LOGH, 2, 2, true>(buf, T, tid, nthr); sync(); }
+    if constexpr (LB == 1) { fft_pass_t<LOGH, 1, 1, true>(buf, T, tid, nthr); sync(); }
+    fft_radix8_passes<LOGH, N8 - 1, true, 1>(buf, T, tid, nthr, sync);
+  }
+}
+
+// Pass 0 (block 2^LOGH, radix 8, stride Q = 2^LOGH / 8) on values a thread already holds:
+// v[e] = x[base + STRIDE e], e < 2^LOGH / STRIDE; the thread owns the butterflies
+// n1 = base + STRIDE b (b < NB = Q / STRIDE) with inputs e = b + NB q.  Forward: the pass
+// outputs y[n1 + Q k] are stored to buf (swizzled); the rest of the transform is
+// fft_run_inner_t.
+template <int LOGH, int STRIDE, class TW>
+__device__ __forceinline__ void dif_pass0_store(const double2* v, int base, double2* buf, const TW& tw) {
+  constexpr int Q = 1 << (LOGH - 3), NB = Q / STRIDE;
+  static_assert(NB >= 1, "pass 0 needs 8 values per butterfly");
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    const int n1 = base + STRIDE * b;
+    double2 a[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) a[q] = v[b + NB * q];
+    dftR<8, false>(a);
+    double2 w[8];
+    w[1] = tw.pass_w(LOGH, LOGH, n1);
+    w[2] = cmul(w[1], w[1]); w[3] = cmul(w[2], w[1]);
+    w[4] = cmul(w[2], w[2]); w[5] = cmul(w[4], w[1]); w[6] = cmul(w[4], w[2]); w[7] = cmul(w[4], w[3]);
+    buf[fsw(n1)] = a[0];
+#pragma unroll
+    for (int q = 1; q < 8; ++q) buf[fsw(n1 + Q * q)] = cmul(a[q], w[q]);
+  }
+}
+
+// Inverse of pass 0 after fft_run_inner_t<LOGH, true>: loads y[n1 + Q k] from buf and
+// returns v[e] = H-scaled x[base + STRIDE e] (same ownership as dif_pass0_store).
+template <int LOGH, int STRIDE, class TW>
+__device__ __forceinline__ void dif_pass0_inverse_load(double2* v, int base, const double2* buf, const TW& tw) {
+  constexpr int Q = 1 << (LOGH - 3), NB = Q / STRIDE;
+#pragma unroll
+  for (int b = 0; b < NB; ++b) {
+    const int n1 = base + STRIDE * b;
+    double2 a[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) a[q] = buf[fsw(n1 + Q * q)];
+    double2 w[8];
+    w[1] = tw.pass_w(LOGH, LOGH, n1);
+    w[2] = cmul(w[1], w[1]); w[3] = cmul(w[2], w[1]);
+    w[4] = cmul(w[2], w[2]); w[5] = cmul(w[4], w[1]); w[6] = cmul(w[4], w[2]); w[7] = cmul(w[4], w[3]);
+#pragma unroll
+    for (int q = 1; q < 8; ++q) a[q] = cmulc(a[q], w[q]);
+    dftR<8, true>(a);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) v[b + NB * q] = a[q];
   }
 }
 

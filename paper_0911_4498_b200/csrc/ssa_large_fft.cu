@@ -131,12 +131,21 @@ __global__ void __launch_bounds__(kThreads) lg_col_fwd(ColFwdArgs args, const do
       v[j].y = (ok && i0 + 1 < a.n_in) ? __ldg(xi + i0 + 1) : 0.0;
     }
   }
-#pragma unroll
-  for (int j = 0; j < NE; ++j)
-    if (threadIdx.x + j * kThreads < N1 * kColW) buf[cc * CS + fsw(r0 + (kThreads / kColW) * j)] = v[j];
-  __syncthreads();
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  fft_run_t<G::L1, false>(buf + w * CS, tw1, lane, 32, WarpSync());
+  if constexpr (G::L1 >= 8) {
+    // the thread holds rows r0 + 32 j of its column: the butterflies of the outermost
+    // radix-8 pass, done in registers before the first shared-memory store
+    __syncthreads();  // twiddle tables
+    dif_pass0_store<G::L1, kThreads / kColW>(v, r0, buf + cc * CS, tw1);
+    __syncthreads();
+    fft_run_inner_t<G::L1, false>(buf + w * CS, tw1, lane, 32, WarpSync());
+  } else {
+#pragma unroll
+    for (int j = 0; j < NE; ++j)
+      if (threadIdx.x + j * kThreads < N1 * kColW) buf[cc * CS + fsw(r0 + (kThreads / kColW) * j)] = v[j];
+    __syncthreads();
+    fft_run_t<G::L1, false>(buf + w * CS, tw1, lane, 32, WarpSync());
+  }
   __syncthreads();
   // element j: column c = t & 7, k1 = (t >> 3) + (256 / 8) j; twiddle W_H^{n2 k1}
   const int c = threadIdx.x & (kColW - 1), k0 = threadIdx.x >> 3;
@@ -167,7 +176,7 @@ struct ColInvArgs {
 };
 
 template <int LOGH>
-__global__ void __launch_bounds__(kThreads) lg_col_inv(const double2* __restrict__ Y, const double2* __restrict__ T1,
+__global__ void __launch_bounds__(kThreads, (LOGH >= 19) ? 1 : 3) lg_col_inv(const double2* __restrict__ Y, const double2* __restrict__ T1,
                                                        ColInvArgs a) {
   pdl_wait();
   using G = Geo<LOGH>;
@@ -192,8 +201,20 @@ __global__ void __launch_bounds__(kThreads) lg_col_inv(const double2* __restrict
     if (threadIdx.x + j * kThreads < N1 * kColW) buf[cc * CS + fsw(rev_t<G::L1>(r0 + RS * j))] = v[j];
   __syncthreads();
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  fft_run_t<G::L1, true>(buf + w * CS, tw1, lane, 32, WarpSync());
-  __syncthreads();
+  // z[j] = H x packed point at row r0 + 32 j of this thread's column
+  double2 z[NE];
+  if constexpr (G::L1 >= 8) {
+    // outermost inverse pass in registers: its outputs are exactly this thread's rows
+    fft_run_inner_t<G::L1, true>(buf + w * CS, tw1, lane, 32, WarpSync());
+    __syncthreads();
+    dif_pass0_inverse_load<G::L1, kThreads / kColW>(z, r0, buf + cc * CS, tw1);
+  } else {
+    fft_run_t<G::L1, true>(buf + w * CS, tw1, lane, 32, WarpSync());
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < NE; ++j)
+      if (threadIdx.x + j * kThreads < N1 * kColW) z[j] = buf[cc * CS + fsw(r0 + RS * j)];
+  }
   constexpr double invH = 1.0 / (double)G::H;
   double ss = 0.0;
   const double cf = (a.mode == 0 && a.coef) ? a.coef[item] : 0.0;
@@ -218,14 +239,13 @@ __global__ void __launch_bounds__(kThreads) lg_col_inv(const double2* __restrict
       if (threadIdx.x + j * kThreads < N1 * kColW) {
         const int n1 = r0 + RS * j;
         const int t = 2 * (n2 + N2 * n1);
-        const double2 z = buf[cc * CS + fsw(n1)];
         if (t < a.ld_out) {
-          const double y = (t < a.n_out) ? fma(-cf, pr[j].x, z.x * invH) : 0.0;
+          const double y = (t < a.n_out) ? fma(-cf, pr[j].x, z[j].x * invH) : 0.0;
           o[t] = y;
           ss = fma(y, y, ss);
         }
         if (t + 1 < a.ld_out) {
-          const double y = (t + 1 < a.n_out) ? fma(-cf, pr[j].y, z.y * invH) : 0.0;
+          const double y = (t + 1 < a.n_out) ? fma(-cf, pr[j].y, z[j].y * invH) : 0.0;
           o[t + 1] = y;
           ss = fma(y, y, ss);
         }
@@ -251,12 +271,11 @@ __global__ void __launch_bounds__(kThreads) lg_col_inv(const double2* __restrict
         const int n1 = r0 + RS * j;
         const int t = 2 * (n2 + N2 * n1);
         if (t < a.N) {
-          const double2 z = buf[cc * CS + fsw(n1)];
           const int c0 = min(min(t + 1, mn), a.N - t);
-          o[t] = z.x * scale * rcp_count(c0);
+          o[t] = z[j].x * scale * rcp_count(c0);
           if (t + 1 < a.N) {
             const int c1 = min(min(t + 2, mn), a.N - t - 1);
-            o[t + 1] = z.y * scale * rcp_count(c1);
+            o[t + 1] = z[j].y * scale * rcp_count(c1);
           }
         }
       }
@@ -443,23 +462,32 @@ __global__ void __launch_bounds__(kThreads) lg_row_warp(const double2* __restric
   double2* cA = rA + 2 * N2;
   double2* cB = rA + 3 * N2;
   const bool mine = valid && (two || !(j & 1));
+  double2 v[NE];
   if (mine) {
     const double2* src = ((j >> 1) ? Yb : Ya) + (size_t)((j & 1) ? B : A) * N2;
-    double2* dst = rows + (size_t)w * N2;
-    double2 v[NE];
 #pragma unroll
     for (int e = 0; e < NE; ++e) {
       const int i = lane + 32 * e;
       if (i < N2) v[e] = src[i];
     }
-#pragma unroll
-    for (int e = 0; e < NE; ++e) {
-      const int i = lane + 32 * e;
-      if (i < N2) dst[fsw(i)] = v[e];
-    }
   }
   __syncthreads();  // tables
-  if (mine) fft_run_t<Gm::L2, false>(rows + (size_t)w * N2, tw2, lane, 32, WarpSync());
+  if (mine) {
+    double2* dst = rows + (size_t)w * N2;
+    if constexpr (Gm::L2 >= 8) {  // outermost radix-8 pass in registers (lane holds lane + 32 e)
+      dif_pass0_store<Gm::L2, 32>(v, lane, dst, tw2);
+      __syncwarp();
+      fft_run_inner_t<Gm::L2, false>(dst, tw2, lane, 32, WarpSync());
+    } else {
+#pragma unroll
+      for (int e = 0; e < NE; ++e) {
+        const int i = lane + 32 * e;
+        if (i < N2) dst[fsw(i)] = v[e];
+      }
+      __syncwarp();
+      fft_run_t<Gm::L2, false>(dst, tw2, lane, 32, WarpSync());
+    }
+  }
   __syncthreads();
   if (valid) {
     const double2 WA = __ldg(TWA + A);
@@ -477,13 +505,22 @@ __global__ void __launch_bounds__(kThreads) lg_row_warp(const double2* __restric
       double2* Yo = Yb + (size_t)row * N2;
       const int tid64 = ((j & 1) << 5) | lane;
       const NamedSync64 sync{1 + 2 * g + half};
-      fft_run_t<Gm::L2, true>(o, tw2, tid64, 64, sync);
       constexpr int NE2 = (N2 + 63) / 64;
       const int nval = (N2 - tid64 + 63) / 64;
-      twiddle_seq<LOGH, NE2>(th, (long long)row * tid64, (long long)row * 64, nval, [&](int e, double2 w) {
-        const int n2 = tid64 + 64 * e;
-        Yo[n2] = cmulc(o[fsw(n2)], w);
-      });
+      if constexpr (Gm::L2 >= 9) {  // outermost inverse pass in registers: thread's n2 = tid64 + 64 e
+        fft_run_inner_t<Gm::L2, true>(o, tw2, tid64, 64, sync);
+        double2 x[NE2];
+        dif_pass0_inverse_load<Gm::L2, 64>(x, tid64, o, tw2);
+        twiddle_seq<LOGH, NE2>(th, (long long)row * tid64, (long long)row * 64, nval, [&](int e, double2 w) {
+          Yo[tid64 + 64 * e] = cmulc(x[e], w);
+        });
+      } else {
+        fft_run_t<Gm::L2, true>(o, tw2, tid64, 64, sync);
+        twiddle_seq<LOGH, NE2>(th, (long long)row * tid64, (long long)row * 64, nval, [&](int e, double2 w) {
+          const int n2 = tid64 + 64 * e;
+          Yo[n2] = cmulc(o[fsw(n2)], w);
+        });
+      }
     }
   } else if (valid && j < 2 && (two || j == 0)) {
     double2* o = j ? rB : rA;
