@@ -201,6 +201,34 @@ def micro_hankelize(P, peak):
     return res
 
 
+def micro_decompose_cfg1(P):
+    """BASELINE.json configs[0] (cfg1): one fp64 series N=1024, L=512, k=10 (ssa_inputs
+    cfg1_series, seed 0), decompose + reconstruct of all 10 components on one GPU.  A
+    latency regime (~60 dependent Lanczos steps in one CTA): time, us per Lanczos step and
+    triples/s are reported, no roofline."""
+    import torch
+    c = ssa_inputs.CONFIGS["cfg1"]
+    N, L, k = c["N"], c["L"], c["k"]
+    x = torch.from_numpy(ssa_inputs.cfg1_series(N)[None].copy()).cuda()
+    plan = P.Plan(N, L, k, 1)
+    s_, U, V, info = plan.decompose(x)
+    G = plan.reconstruct(s_, U, V)
+    torch.cuda.synchronize()
+
+    def run():
+        plan.decompose(x, s_, U, V, info)
+        plan.reconstruct(s_, U, V, out=G)
+    ms = min(_events_ms(run) for _ in range(5))
+    inf = P.info_to_numpy(info)[0]
+    m = int(inf["steps"])
+    res = {"value": k / (ms * 1e-3), "unit": "eigentriples/s", "ms": ms, "steps": m, "us_per_step": 1e3 * ms / m,
+           "hankel_matvecs_per_s": 2 * m / (ms * 1e-3), "status": int(inf["status"]),
+           "workload": "cfg1 (BASELINE.json configs[0]): one series N=1024 L=512 k=10, decompose + reconstruct",
+           "regime": "latency (one CTA, dependent steps): no roofline"}
+    plan.close()
+    return res
+
+
 def micro_decompose_cfg3(P, peak):
     """BASELINE.json configs[2] (cfg3): one long series N=2^20, L=2^19, k=32 (ssa_inputs
     cfg3_series, seed 3) on one GPU: full decompose (four-step FFT products through L2,
@@ -538,6 +566,7 @@ def main():
         line["matvec_cfg4"] = micro_matvec(P, peak)
         line["hankelize_cfg5"] = micro_hankelize(P, peak)
         line["decompose_cfg3"] = micro_decompose_cfg3(P, peak)
+        line["decompose_cfg1"] = micro_decompose_cfg1(P)
     if rank == 0 and not args.no_cpu_baseline:
         cores = os.cpu_count() or 1
         rate, desc, wall = oracle_sample(cores)
