@@ -201,6 +201,30 @@ def micro_hankelize(P, peak):
     return res
 
 
+def micro_hmatrix(P, N: int = 4000):
+    """Heterogeneity matrix (ssa_hmatrix) in the paper's comparison
+    setting (PAPER.md:1068-1076): Eq. (hseries) series with Q = N/2, B = T = N/4, L = B/2,
+    I = {1, 2}; N = 4000 here (3001 base-window decompositions, 6002 Hankel products of the
+    whole series, a 3001 x 3001 matrix).  Whole call timed (workspace allocation included)."""
+    import torch
+    Q, B = N // 2, N // 4
+    T, L = B, B // 2
+    f = torch.from_numpy(ssa_inputs.change_point_series(N, Q, 7)).cuda()
+    G, info = P.hmatrix(f, B, T, L, [1, 2])
+    torch.cuda.synchronize()
+    ms = min(_events_ms(lambda: P.hmatrix(f, B, T, L, [1, 2], out=G, info=info)) for _ in range(3))
+    nb, nt = N - B + 1, N - T + 1
+    inf = P.info_to_numpy(info)
+    res = {"value": nb * nt / (ms * 1e-3), "unit": "H-matrix entries/s", "ms": ms,
+           "windows_decomposed_per_s": nb / (ms * 1e-3), "mean_steps": float(inf["steps"].mean()),
+           "workload": f"H-matrix of Eq. (hseries), N={N} Q={Q} B=T={B} L={L} I={{1,2}} ({nb}x{nt})",
+           "g_inside_mean": float(G[: Q - B + 1, : Q - T + 1].mean().item()),
+           "g_across_mean": float(G[: Q - B + 1, Q:].mean().item())}
+    del f, G
+    torch.cuda.empty_cache()
+    return res
+
+
 def micro_decompose_cfg1(P):
     """BASELINE.json configs[0] (cfg1): one fp64 series N=1024, L=512, k=10 (ssa_inputs
     cfg1_series, seed 0), decompose + reconstruct of all 10 components on one GPU.  A
@@ -567,6 +591,7 @@ def main():
         line["hankelize_cfg5"] = micro_hankelize(P, peak)
         line["decompose_cfg3"] = micro_decompose_cfg3(P, peak)
         line["decompose_cfg1"] = micro_decompose_cfg1(P)
+        line["hmatrix"] = micro_hmatrix(P)
     if rank == 0 and not args.no_cpu_baseline:
         cores = os.cpu_count() or 1
         rate, desc, wall = oracle_sample(cores)

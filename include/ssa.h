@@ -154,6 +154,23 @@ ssa_status ssa_reconstruct(ssa_plan_t plan, const double* d_sigma, const double*
 ssa_status ssa_reconstruct_grouped(ssa_plan_t plan, const double* d_sigma, const double* d_U, const double* d_V,
                                    const int32_t* groups, int32_t ngroups, double* d_out, void* stream);
 
+/* Heterogeneity matrix for structural-change detection (sec 6.2):
+ *   G[i][j] = 1 - sum_{m=1}^{K2} sum_{r in I} (U_r^(i)T X_m^(j))^2 / sum_{m=1}^{K2} |X_m^(j)|^2
+ * where U_r^(i) (r in I) are left singular vectors of the base window
+ * (f_i .. f_{i+B-1}), i = 1..N-B+1, and X_m^(j), m = 1..K2 = T-L+1, the L-lagged vectors of
+ * the test window (f_j .. f_{j+T-1}), j = 1..N-T+1 (R21: windows of length B
+ * and T).  The base windows are decomposed by the batched ssa_decompose (its options and
+ * tolerances), the projections of every test window come from one FFT Hankel product
+ * X_F^T U_r^(i) of the whole series per (i, r).
+ *   d_series: [N] device;  I: HOST [nI] distinct 1-based triple indices, each <= min(L, B-L+1)
+ *   d_G: [N-B+1][N-T+1] device;  d_info: [N-B+1] per-window decompose info, or NULL
+ * Needs N >= 3, 2 <= L < B <= N, L <= T <= N.  Allocates and frees its own workspace and
+ * synchronizes `stream` before returning.  Returns NOT_CONVERGED (G still written) if a
+ * base window did not converge. */
+ssa_status ssa_hmatrix(const double* d_series, int64_t N, int64_t B, int64_t T, int64_t L, const int32_t* I,
+                       int32_t nI, const ssa_options* opt, int device, double* d_G, ssa_series_info* d_info,
+                       void* stream);
+
 /* End-to-end call on HOST buffers: copies h_series to the device, runs ssa_decompose and
  * ssa_reconstruct on plan-owned device buffers, copies sigma, U, V, the reconstructions
  * and info back, and synchronizes `stream`.  Any output pointer may be NULL to skip its

@@ -119,6 +119,30 @@ def grouped(sigma, U, V, groups, ngroups: int) -> np.ndarray:
     return out
 
 
+def hmatrix(f, B: int, T: int, L: int, I) -> np.ndarray:
+    """Heterogeneity matrix written out from PAPER.md:962-1040 (sec 6.2): base windows
+    F_i = (f_i..f_{i+B-1}), i = 1..N-B+1, test windows F_j = (f_j..f_{j+T-1}),
+    j = 1..N-T+1 (R21); for each base window the Jacobi SVD of its trajectory
+    matrix gives the orthonormal U_r, r in I (1-based); for each test window its L-lagged
+    vectors X_m are the columns of its explicit trajectory matrix, and
+        g_ij = sum_m dist^2(X_m, span U_I) / sum_m |X_m|^2            (Eq. (g))
+    with dist(X, span) = |X - U_I U_I^T X| (orthogonal projection)."""
+    f = np.asarray(f, dtype=np.float64)
+    N = f.shape[0]
+    I = [int(r) for r in I]
+    nb, nt = N - B + 1, N - T + 1
+    Xs = [trajectory(f[j:j + T], L) for j in range(nt)]
+    den = np.array([np.sum(X * X) for X in Xs])
+    G = np.empty((nb, nt))
+    for i in range(nb):
+        _, U, _, _ = svd(f[i:i + B], L, max(I))
+        P = U[[r - 1 for r in I]].T          # L x |I|, orthonormal columns
+        for j in range(nt):
+            R = Xs[j] - P @ (P.T @ Xs[j])     # residuals of the lagged vectors
+            G[i, j] = np.sum(R * R) / den[j]
+    return G
+
+
 def svd(f, L: int, nsv: int | None = None):
     """Leading nsv singular triples of the trajectory matrix by one-sided Jacobi
     (sec 2.2, with X = U Sigma V^T, R3).

@@ -9,7 +9,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libssa.so")
 SOURCES = [os.path.join(HERE, "csrc", f) for f in ("ssa_api.cu", "ssa_fft_kernels.cu", "ssa_lanczos.cu", "ssa_svd.cu", "ssa_large_fft.cu",
-                                                   "ssa_large_lanczos.cu")]
+                                                   "ssa_large_lanczos.cu", "ssa_hmatrix.cu")]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v", "-diag-suppress", "1886,550"]
 

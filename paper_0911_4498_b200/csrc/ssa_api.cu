@@ -549,6 +549,89 @@ extern "C" ssa_status ssa_reconstruct_grouped(ssa_plan_t plan, const double* d_s
   return SSA_OK;
 }
 
+extern "C" ssa_status ssa_hmatrix(const double* d_series, int64_t N, int64_t B, int64_t T, int64_t L,
+                                  const int32_t* I, int32_t nI, const ssa_options* opt, int device, double* d_G,
+                                  ssa_series_info* d_info, void* stream) {
+  if (!d_series || !d_G || !I) return fail(SSA_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (N < 3 || L < 2 || B <= L || B > N || T < L || T > N)
+    return fail(SSA_ERR_INVALID_ARGUMENT, "need N >= 3, 2 <= L < B <= N, L <= T <= N (N=%lld B=%lld T=%lld L=%lld)",
+                (long long)N, (long long)B, (long long)T, (long long)L);
+  const int64_t KB = B - L + 1, kmax = std::min(L, KB);
+  if (nI < 1 || nI > ssa::kMaxK) return fail(SSA_ERR_INVALID_ARGUMENT, "nI = %d not in [1, %d]", nI, ssa::kMaxK);
+  int kI = 0;
+  std::vector<int32_t> idx((size_t)nI);
+  for (int r = 0; r < nI; ++r) {
+    if (I[r] < 1 || I[r] > kmax) return fail(SSA_ERR_INVALID_ARGUMENT, "I[%d] = %d not in [1, %lld]", r, I[r], (long long)kmax);
+    for (int q = 0; q < r; ++q)
+      if (I[q] == I[r]) return fail(SSA_ERR_INVALID_ARGUMENT, "I[%d] = %d repeated", r, I[r]);
+    idx[(size_t)r] = I[r] - 1;
+    kI = std::max(kI, (int)I[r]);
+  }
+  if (kI > ssa::kMaxK) return fail(SSA_ERR_INVALID_ARGUMENT, "max(I) = %d > %d", kI, ssa::kMaxK);
+  CK(cudaSetDevice(device), "cudaSetDevice");
+  cudaStream_t s = S(stream);
+  const int64_t nwin = N - B + 1, KF = N - L + 1;
+  ssa_plan_t pa = nullptr, pc = nullptr, p1 = nullptr;
+  double *win = nullptr, *sig = nullptr, *U = nullptr, *V = nullptr, *x = nullptr, *y = nullptr, *spec = nullptr,
+         *den = nullptr;
+  int32_t* d_idx = nullptr;
+  ssa_series_info* info = d_info;
+  bool own_info = false;
+  ssa_status st = SSA_OK;
+  auto A = [&](void** ptr, size_t bytes, const char* what) { return alloc(ptr, bytes, what); };
+  do {
+    // 1. leading left singular vectors of every base window (batched decompose)
+    if ((st = ssa_plan_create(B, L, kI, nwin, opt, device, &pa)) != SSA_OK) break;
+    if ((st = A((void**)&win, (size_t)nwin * B * 8, "H-matrix windows")) != SSA_OK) break;
+    if ((st = A((void**)&sig, (size_t)nwin * kI * 8, "H-matrix sigma")) != SSA_OK) break;
+    if ((st = A((void**)&U, (size_t)nwin * kI * L * 8, "H-matrix U")) != SSA_OK) break;
+    if ((st = A((void**)&V, (size_t)nwin * kI * KB * 8, "H-matrix V")) != SSA_OK) break;
+    if (!info) {
+      if ((st = A((void**)&info, (size_t)nwin * sizeof(ssa_series_info), "H-matrix info")) != SSA_OK) break;
+      own_info = true;
+    }
+    if (ssa::launch_hm_windows(d_series, nwin, B, win, s) != cudaSuccess) { st = cuda_fail(cudaGetLastError(), "hm windows"); break; }
+    if ((st = ssa_decompose(pa, win, sig, U, V, info, stream)) != SSA_OK) break;
+    // 2. spectrum of the whole series once; X_F^T U_r for every (window, r) through it
+    if ((st = ssa_plan_create(N, L, 0, 1, opt, device, &p1)) != SSA_OK) break;
+    if ((st = ssa_plan_create(N, L, 0, nwin * nI, opt, device, &pc)) != SSA_OK) break;
+    const Plan& qc = pc->p;
+    if ((st = A((void**)&spec, (size_t)(qc.H + 1) * 16, "H-matrix spectrum")) != SSA_OK) break;
+    if ((st = ssa_spectrum(p1, d_series, spec, stream)) != SSA_OK) break;
+    if ((st = A((void**)&d_idx, (size_t)nI * 4, "H-matrix index")) != SSA_OK) break;
+    if ((st = A((void**)&x, (size_t)nwin * nI * L * 8, "H-matrix vectors")) != SSA_OK) break;
+    if ((st = A((void**)&y, (size_t)nwin * nI * KF * 8, "H-matrix projections")) != SSA_OK) break;
+    CK(cudaMemcpyAsync(d_idx, idx.data(), (size_t)nI * 4, cudaMemcpyHostToDevice, s), "H2D index");
+    if (ssa::launch_hm_gather(U, nwin, kI, L, d_idx, nI, x, s) != cudaSuccess) { st = cuda_fail(cudaGetLastError(), "hm gather"); break; }
+    cudaError_t e;
+    if (qc.large)
+      e = ssa::large_correlate(qc, reinterpret_cast<const double2*>(spec), 0, x, (size_t)L, (int)L, y, (size_t)KF, (int)KF,
+                               (int)KF, nullptr, 0, nullptr, nullptr, (int)(nwin * nI), s);
+    else
+      e = ssa::launch_matvec_strided(qc, reinterpret_cast<const double2*>(spec), 0, x, y, 1, s);
+    if (e != cudaSuccess) { st = cuda_fail(e, "H-matrix projections"); break; }
+    // 3. the matrix: windowed sums of the squared projections over the norms of the lags
+    if ((st = A((void**)&den, (size_t)(N - T + 1) * 8, "H-matrix norms")) != SSA_OK) break;
+    if ((e = ssa::launch_hm_matrix(d_series, N, T, L, y, nwin, nI, KF, den, d_G, s)) != cudaSuccess) {
+      st = cuda_fail(e, "H-matrix kernel");
+      break;
+    }
+    CK(cudaStreamSynchronize(s), "stream sync");
+    std::vector<ssa_series_info> hi((size_t)nwin);
+    CK(cudaMemcpy(hi.data(), info, (size_t)nwin * sizeof(ssa_series_info), cudaMemcpyDeviceToHost), "D2H info");
+    for (const auto& q : hi)
+      if (q.status != SSA_OK) { st = (ssa_status)q.status; break; }
+  } while (0);
+  cudaStreamSynchronize(s);
+  for (void* q : {(void*)win, (void*)sig, (void*)U, (void*)V, (void*)x, (void*)y, (void*)spec, (void*)d_idx, (void*)den})
+    if (q) cudaFree(q);
+  if (own_info && info) cudaFree(info);
+  if (pa) ssa_plan_destroy(pa);
+  if (pc) ssa_plan_destroy(pc);
+  if (p1) ssa_plan_destroy(p1);
+  return st;
+}
+
 extern "C" ssa_status ssa_run_host(ssa_plan_t plan, const double* h_series, double* h_sigma, double* h_U,
                                    double* h_V, double* h_recon, ssa_series_info* h_info, void* stream) {
   if (!plan || !h_series) return fail(SSA_ERR_INVALID_ARGUMENT, "NULL argument");

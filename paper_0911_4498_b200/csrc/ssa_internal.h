@@ -134,6 +134,15 @@ inline cudaError_t raise_smem_limit(F* func, size_t bytes) {
 cudaError_t launch_spectrum(const Plan& p, const double* series, double2* spec, int nseries, cudaStream_t s);
 cudaError_t launch_matvec(const Plan& p, const double2* spec, const double* x, double* y, int transpose,
                           cudaStream_t s);
+// spec_stride (double2 elements) between the items' spectra; 0: one spectrum for all
+cudaError_t launch_matvec_strided(const Plan& p, const double2* spec, size_t spec_stride, const double* x, double* y,
+                                  int transpose, cudaStream_t s);
+// heterogeneity matrix helpers (ssa_hmatrix.cu)
+cudaError_t launch_hm_windows(const double* f, int64_t nwin, int64_t B, double* win, cudaStream_t s);
+cudaError_t launch_hm_gather(const double* U, int64_t nwin, int k, int64_t L, const int32_t* d_idx, int nI, double* x,
+                             cudaStream_t s);
+cudaError_t launch_hm_matrix(const double* f, int64_t N, int64_t T, int64_t L, const double* y, int64_t nwin, int nI,
+                             int64_t KF, double* den, double* G, cudaStream_t s);
 cudaError_t launch_hankelize(const Plan& p, const double* sigma, const double* U, const double* V, int nterms,
                              double* out, cudaStream_t s);
 cudaError_t fft_set_attributes(int H, const char** which);

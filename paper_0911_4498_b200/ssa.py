@@ -26,7 +26,7 @@ STATUS = {0: "SSA_OK", 1: "SSA_ERR_INVALID_ARGUMENT", 2: "SSA_ERR_NOT_CONVERGED"
 # every symbol include/ssa.h declares
 EXPORTS = ["ssa_options_default", "ssa_plan_create", "ssa_plan_destroy", "ssa_plan_fft_size",
            "ssa_plan_max_steps", "ssa_spectrum", "ssa_matvec", "ssa_hankelize", "ssa_decompose",
-           "ssa_reconstruct", "ssa_reconstruct_grouped", "ssa_run_host", "ssa_status_string", "ssa_last_error",
+           "ssa_reconstruct", "ssa_reconstruct_grouped", "ssa_hmatrix", "ssa_run_host", "ssa_status_string", "ssa_last_error",
            "ssa_plan_launch_count", "ssa_plan_phase_ms", "ssa_plan_profile", "ssa_plan_bidiagonals"]
 
 
@@ -86,6 +86,7 @@ def load_library():
     lib.ssa_decompose.argtypes = [vp, dp, dp, dp, dp, dp, vp]
     lib.ssa_reconstruct.argtypes = [vp, dp, dp, dp, dp, vp]
     lib.ssa_reconstruct_grouped.argtypes = [vp, dp, dp, dp, vp, i32, dp, vp]
+    lib.ssa_hmatrix.argtypes = [dp, i64, i64, i64, i64, vp, i32, ctypes.POINTER(Options), ctypes.c_int, dp, dp, vp]
     lib.ssa_run_host.argtypes = [vp, dp, dp, dp, dp, dp, dp, vp]
     lib.ssa_status_string.argtypes = [ctypes.c_int]
     lib.ssa_status_string.restype = ctypes.c_char_p
@@ -274,6 +275,35 @@ class Plan:
         if raise_on_status:
             _check(st)
         return sigma, U, V, recon, info
+
+
+def hmatrix(series, B: int, T: int, L: int, I, *, tol: float = 1e-12, seed: int = 42, out=None, info=None,
+            stream=None):
+    """Heterogeneity matrix G[(N-B+1)][(N-T+1)] of a device series [N] (ssa_hmatrix,
+    PAPER.md:962-1040): base windows of length B decomposed with window L, the subspace of
+    the triples I (1-based), test windows of length T.  Returns (G, info)."""
+    import torch
+    lib = load_library()
+    if not torch.cuda.is_available():
+        raise RuntimeError("no CUDA device: libssa has no CPU fallback")
+    N = int(series.shape[-1])
+    _dev_f64(series, (N,), "series")
+    idx = np.ascontiguousarray(I, dtype=np.int32)
+    opt = Options()
+    _check(lib.ssa_options_default(ctypes.byref(opt)))
+    opt.tol, opt.seed = tol, seed
+    dev = series.device.index
+    nb, nt = N - B + 1, N - T + 1
+    if nb < 1 or nt < 1:  # let the C call report the invalid sizes (it validates first)
+        _check(lib.ssa_hmatrix(series.data_ptr(), N, B, T, L, idx.ctypes.data, len(idx), ctypes.byref(opt), dev,
+                               None, None, _stream(stream)))
+    G = torch.empty((nb, nt), dtype=torch.float64, device=series.device) if out is None else out
+    _dev_f64(G, (nb, nt), "out")
+    if info is None:
+        info = torch.zeros((nb, INFO_DTYPE.itemsize), dtype=torch.uint8, device=series.device)
+    _check(lib.ssa_hmatrix(series.data_ptr(), N, B, T, L, idx.ctypes.data, len(idx), ctypes.byref(opt), dev,
+                           G.data_ptr(), info.data_ptr(), _stream(stream)))
+    return G, info
 
 
 def info_to_numpy(info_tensor) -> np.ndarray:

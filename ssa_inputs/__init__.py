@@ -122,9 +122,10 @@ def cfg5_problem(p: int, N: int = 262144, L: int = 131072, terms: int = 50):
 
 
 def change_point_series(N: int = 400, Q: int = 200, seed: int = 7) -> np.ndarray:
-    """Paper §6.4 Eq. (hseries)-shaped series: a sinusoid whose period
-    changes at n = Q, plus small noise.  Used only for extra decomposition parity cases."""
+    """Eq. (hseries) of PAPER.md:1049-1056 (sec 6.2, H-matrix example): f_n = sin(2πn/10)
+    + 0.01 ε_n for n < Q, sin(2πn/10.5) + 0.01 ε_n for n >= Q, n = 1..N, ε_n ~ N(0,1)
+    white noise from default_rng(seed).  The paper's example: N = 400, Q = 200."""
     n = _n(N)
     rng = np.random.default_rng(seed)
-    f = np.where(n < Q, np.sin(2 * np.pi * n / 10), np.sin(2 * np.pi * n / 17))
-    return f + rng.normal(0.0, 0.01, N)
+    f = np.where(n < Q, np.sin(2 * np.pi * n / 10), np.sin(2 * np.pi * n / 10.5))
+    return f + 0.01 * rng.standard_normal(N)

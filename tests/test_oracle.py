@@ -296,6 +296,35 @@ def test_grouped_reconstruction_pins():
     assert np.allclose(g[0], sin, rtol=0, atol=1e-12)
 
 
+def test_hmatrix_oracle_pins():
+    """oracle.hmatrix (Eq. (g), PAPER.md:980-1000) against what the paper fixes: 0 <= g <= 1;
+    the rewritten form 1 - sum (U^T X)^2 / sum |X|^2 (a different formula)
+    agrees; a pure sinusoid (rank 2) with I = {1,2} gives g = 0 everywhere (every window's
+    lagged vectors lie in the same 2-D space); I = all L triples gives g = 0; the paper's
+    change-point series (Eq. (hseries)) shows the block structure of its H-matrix figure
+    (PAPER.md:1049-1066): small inside the homogeneous parts, large across the change."""
+    f = ssa_inputs.change_point_series(160, 80, 3)
+    B, T, L = 40, 40, 20
+    G = oracle.hmatrix(f, B, T, L, [1, 2])
+    assert G.min() >= 0.0 and G.max() <= 1.0
+    # rewritten formula at a few entries
+    for i, j in [(0, 0), (5, 100), (120, 7), (60, 60)]:
+        _, U, _, _ = oracle.svd(f[i:i + B], L, 2)
+        X = oracle.trajectory(f[j:j + T], L)
+        g2 = 1.0 - np.sum((U[:2] @ X) ** 2) / np.sum(X * X)
+        assert abs(g2 - G[i, j]) <= 1e-12
+    n = np.arange(1, 161, dtype=float)
+    sin = np.sin(2 * np.pi * n / 10 + 0.3)
+    assert np.abs(oracle.hmatrix(sin, B, T, L, [1, 2])).max() <= 1e-12
+    rng = np.random.default_rng(4)
+    g = rng.standard_normal(60)
+    assert np.abs(oracle.hmatrix(g, 30, 25, 10, list(range(1, 11)))).max() <= 1e-12
+    nb = 80 - B + 1  # base windows inside the first regime: i + B <= Q
+    inside = G[:nb, :nb].mean()
+    across = G[:nb, 80:].mean()
+    assert inside < 1e-3 and across > 20 * inside
+
+
 def test_cfg1_oracle_spectrum_structure():
     """cfg1 (BASELINE configs[0]): σ₁ dominated by the exponential trend, then the two
     sinusoid pairs, then noise (SURVEY Appendix A 'Spectrum structure')."""
