@@ -225,6 +225,31 @@ def micro_hmatrix(P, N: int = 4000):
     return res
 
 
+def micro_bootstrap(P, R: int = 1024):
+    """Bootstrap study of the paper (sec 6.3): the
+    rank-5 series (periods in n, R17), N = 1000, L = 500, noise sigma = 5, R
+    replicates (seeded N(0,1) noise, drawn on the host and copied once): replicates,
+    batched decompose (k = 5), grouped reconstruction, per-point mean/var/MSE."""
+    import torch
+    N, L, d, noise = 1000, 500, 5, 5.0
+    f = torch.from_numpy(ssa_inputs.bootstrap_series(N)).cuda()
+    eps = torch.from_numpy(ssa_inputs.bootstrap_noise(R, N)).cuda()
+    plan = P.Plan(N, L, d, R)
+    info = torch.zeros((R, P.INFO_DTYPE.itemsize), dtype=torch.uint8, device="cuda")
+    plan.bootstrap(f, eps, noise, info=info)
+    torch.cuda.synchronize()
+    ms = min(_events_ms(lambda: plan.bootstrap(f, eps, noise, info=info)) for _ in range(3))
+    inf = P.info_to_numpy(info)
+    res = {"value": R / (ms * 1e-3), "unit": "replicates/s", "ms": ms, "replicates": R,
+           "eigentriples_per_s": R * d / (ms * 1e-3), "mean_steps": float(inf["steps"].mean()),
+           "converged_fraction": float((inf["converged"] == 1).mean()),
+           "workload": f"bootstrap of the rank-5 series, N={N} L={L} sigma={noise}, {R} replicates"}
+    plan.close()
+    del f, eps
+    torch.cuda.empty_cache()
+    return res
+
+
 def micro_decompose_cfg1(P):
     """BASELINE.json configs[0] (cfg1): one fp64 series N=1024, L=512, k=10 (ssa_inputs
     cfg1_series, seed 0), decompose + reconstruct of all 10 components on one GPU.  A
@@ -592,6 +617,7 @@ def main():
         line["decompose_cfg3"] = micro_decompose_cfg3(P, peak)
         line["decompose_cfg1"] = micro_decompose_cfg1(P)
         line["hmatrix"] = micro_hmatrix(P)
+        line["bootstrap"] = micro_bootstrap(P)
     if rank == 0 and not args.no_cpu_baseline:
         cores = os.cpu_count() or 1
         rate, desc, wall = oracle_sample(cores)

@@ -171,6 +171,20 @@ ssa_status ssa_hmatrix(const double* d_series, int64_t N, int64_t B, int64_t T, 
                        int32_t nI, const ssa_options* opt, int device, double* d_G, ssa_series_info* d_info,
                        void* stream);
 
+/* Bootstrap study of the rank-d reconstruction (sec 6.3): for the plan's
+ * batch = R replicates F'_r = F + noise_sigma * eps_r of the clean series F, the k = d
+ * leading triples of each (ssa_decompose) are grouped into one component and averaged
+ * (ssa_reconstruct_grouped) into G_r, then per point t:
+ *   mean[t] = (1/R) sum_r G_r[t],  var[t] = 1/(R-1) sum_r (G_r[t] - mean[t])^2,
+ *   mse[t]  = (1/R) sum_r (G_r[t] - F[t])^2      (bias = mean - F;  mse = bias^2 + (R-1)/R var)
+ *   d_series: [N] the clean F;  d_eps: [R][N] the noise (caller-drawn, seeded: the library
+ *   draws no random numbers for this);  d_mean, d_var, d_mse: [N] (var, mse nullable);
+ *   d_G: [R][N] reconstructions or NULL (plan scratch);  d_info: [R] or NULL.
+ * The plan's workspace grows by 2 R N doubles on first use. */
+ssa_status ssa_bootstrap(ssa_plan_t plan, const double* d_series, const double* d_eps, double noise_sigma,
+                         double* d_mean, double* d_var, double* d_mse, double* d_G, ssa_series_info* d_info,
+                         void* stream);
+
 /* End-to-end call on HOST buffers: copies h_series to the device, runs ssa_decompose and
  * ssa_reconstruct on plan-owned device buffers, copies sigma, U, V, the reconstructions
  * and info back, and synchronizes `stream`.  Any output pointer may be NULL to skip its

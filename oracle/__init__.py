@@ -143,6 +143,32 @@ def hmatrix(f, B: int, T: int, L: int, I) -> np.ndarray:
     return G
 
 
+def bootstrap(f, eps, noise_sigma: float, L: int, d: int):
+    """Bootstrap study of the rank-d reconstruction (sec 6.3) written out:
+    for each replicate F' = F + noise_sigma eps_r, the Jacobi SVD of its trajectory matrix,
+    the first d triples grouped and averaged (Basic SSA steps 3-4) into G_r; then per point
+    the sample mean, the unbiased variance and the mean square error against F (plain
+    loops over the replicates).  Returns (mean, var, mse, G)."""
+    f = np.asarray(f, dtype=np.float64)
+    R, N = eps.shape
+    G = np.empty((R, N))
+    for r in range(R):
+        fp = f + noise_sigma * eps[r]
+        s, U, V, _ = svd(fp, L, d)
+        G[r] = grouped(s, U, V, [0] * d, 1)[0]
+    mean = np.zeros(N)
+    for r in range(R):
+        mean += G[r]
+    mean /= R
+    var = np.zeros(N)
+    mse = np.zeros(N)
+    for r in range(R):
+        var += (G[r] - mean) ** 2
+        mse += (G[r] - f) ** 2
+    var = var / (R - 1) if R > 1 else var
+    return mean, var, mse / R, G
+
+
 def svd(f, L: int, nsv: int | None = None):
     """Leading nsv singular triples of the trajectory matrix by one-sided Jacobi
     (sec 2.2, with X = U Sigma V^T, R3).

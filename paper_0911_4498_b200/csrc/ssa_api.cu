@@ -117,7 +117,7 @@ static void free_plan(Plan& p) {
   void* ptrs[] = {p.d_tw, p.d_twl, p.d_spec, p.d_U, p.d_V, p.d_ab, p.d_state, p.d_tgk, p.d_rot, p.d_vecs, p.d_coef,
                   p.d_info, p.d_counters, p.d_hscratch, p.d_prof, p.d_tgkw, p.d_tw1, p.d_tw2, p.d_tw4, p.d_twp, p.d_lbuf,
                   p.d_lgsc, p.d_lgpart, p.d_lgh, p.d_lgr, p.d_series, p.d_sigma, p.d_Uout, p.d_Vout,
-                  p.d_recon, p.d_elem};
+                  p.d_recon, p.d_elem, p.d_bs};
   for (void* q : ptrs)
     if (q) cudaFree(q);
   for (int i = 0; i < 2 * Plan::kPhases; ++i)
@@ -630,6 +630,36 @@ extern "C" ssa_status ssa_hmatrix(const double* d_series, int64_t N, int64_t B, 
   if (pc) ssa_plan_destroy(pc);
   if (p1) ssa_plan_destroy(p1);
   return st;
+}
+
+extern "C" ssa_status ssa_bootstrap(ssa_plan_t plan, const double* d_series, const double* d_eps, double noise_sigma,
+                                    double* d_mean, double* d_var, double* d_mse, double* d_G,
+                                    ssa_series_info* d_info, void* stream) {
+  if (!plan || !d_series || !d_eps || !d_mean) return fail(SSA_ERR_INVALID_ARGUMENT, "NULL argument");
+  Plan& p = plan->p;
+  if (p.k < 1) return fail(SSA_ERR_INVALID_ARGUMENT, "plan was created with k = 0");
+  if (!(noise_sigma >= 0.0)) return fail(SSA_ERR_INVALID_ARGUMENT, "noise_sigma must be >= 0");
+  CK(cudaSetDevice(p.device), "cudaSetDevice");
+  cudaStream_t s = S(stream);
+  const size_t R = (size_t)p.batch, N = (size_t)p.N, k = (size_t)p.k;
+  ssa_status st;
+  // plan scratch: replicates, reconstructions, sigma, U, V (one allocation)
+  const size_t nbs = 2 * R * N + R * k * (1 + (size_t)p.L + (size_t)p.K);
+  if (!p.d_bs && (st = alloc((void**)&p.d_bs, nbs * 8, "bootstrap workspace")) != SSA_OK) return st;
+  double* reps = p.d_bs;
+  double* G = d_G ? d_G : p.d_bs + R * N;
+  double* sg = p.d_bs + 2 * R * N;
+  double* Ub = sg + R * k;
+  double* Vb = Ub + R * k * p.L;
+  CK(ssa::launch_bs_replicates(d_series, d_eps, noise_sigma, (int64_t)R, (int64_t)N, reps, s), "bootstrap replicates");
+  p.launches += 1;
+  if ((st = ssa_decompose(plan, reps, sg, Ub, Vb, d_info, stream)) != SSA_OK) return st;
+  std::vector<int32_t> groups(k, 0);  // the first k = d triples in one group: the rank-d signal
+  if ((st = ssa_reconstruct_grouped(plan, sg, Ub, Vb, groups.data(), 1, G, stream)) != SSA_OK)
+    return st;
+  CK(ssa::launch_bs_stats(G, d_series, (int64_t)R, (int64_t)N, d_mean, d_var, d_mse, s), "bootstrap statistics");
+  p.launches += 1;
+  return SSA_OK;
 }
 
 extern "C" ssa_status ssa_run_host(ssa_plan_t plan, const double* h_series, double* h_sigma, double* h_U,

@@ -118,3 +118,52 @@ cudaError_t launch_hm_matrix(const double* f, int64_t N, int64_t T, int64_t L, c
 }
 
 }  // namespace ssa
+
+namespace ssa {
+
+// ---- bootstrap study (sec 6.3) -------------------
+// replicates F'_r = F + noise_sigma * eps_r  (eps: [R][N], the caller's seeded noise)
+__global__ void bs_replicates_kernel(const double* __restrict__ f, const double* __restrict__ eps, double noise_sigma,
+                                     int64_t R, int64_t N, double* __restrict__ out) {
+  const size_t total = (size_t)R * N;
+  for (size_t x = (size_t)blockIdx.x * blockDim.x + threadIdx.x; x < total; x += (size_t)gridDim.x * blockDim.x)
+    out[x] = fma(noise_sigma, eps[x], f[x % N]);
+}
+
+// per point t over the R reconstructions G_r: mean, unbiased variance (two passes, fixed
+// order) and the mean square error against the clean series F
+__global__ void bs_stats_kernel(const double* __restrict__ G, const double* __restrict__ f, int64_t R, int64_t N,
+                                double* __restrict__ mean, double* __restrict__ var, double* __restrict__ mse) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < N; t += (int64_t)gridDim.x * blockDim.x) {
+    double s = 0.0, e2 = 0.0;
+    const double ft = f[t];
+    for (int64_t r = 0; r < R; ++r) {
+      const double g = G[(size_t)r * N + t];
+      s += g;
+      e2 = fma(g - ft, g - ft, e2);
+    }
+    const double m = s / (double)R;
+    double v = 0.0;
+    for (int64_t r = 0; r < R; ++r) {
+      const double d = G[(size_t)r * N + t] - m;
+      v = fma(d, d, v);
+    }
+    mean[t] = m;
+    if (var) var[t] = (R > 1) ? v / (double)(R - 1) : 0.0;
+    if (mse) mse[t] = e2 / (double)R;
+  }
+}
+
+cudaError_t launch_bs_replicates(const double* f, const double* eps, double noise_sigma, int64_t R, int64_t N,
+                                 double* out, cudaStream_t s) {
+  bs_replicates_kernel<<<grid_for((size_t)R * N), kThreads, 0, s>>>(f, eps, noise_sigma, R, N, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_bs_stats(const double* G, const double* f, int64_t R, int64_t N, double* mean, double* var,
+                            double* mse, cudaStream_t s) {
+  bs_stats_kernel<<<grid_for((size_t)N), kThreads, 0, s>>>(G, f, R, N, mean, var, mse);
+  return cudaGetLastError();
+}
+
+}  // namespace ssa

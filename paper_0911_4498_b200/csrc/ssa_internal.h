@@ -107,6 +107,7 @@ struct Plan {
   double* d_Vout = nullptr;
   double* d_recon = nullptr;
   double* d_elem = nullptr;  // grouped reconstruction on the long path: elementary series
+  double* d_bs = nullptr;    // bootstrap: replicates [batch][N] then reconstructions [batch][N]
   // host-API pipelining (ssa_run_host): two sub-plans of one slice each, alternating on two
   // compute streams, device-to-host copies of finished slices on a third stream
   void* sub[2] = {nullptr, nullptr};  // ssa_plan_t
@@ -143,6 +144,10 @@ cudaError_t launch_hm_gather(const double* U, int64_t nwin, int k, int64_t L, co
                              cudaStream_t s);
 cudaError_t launch_hm_matrix(const double* f, int64_t N, int64_t T, int64_t L, const double* y, int64_t nwin, int nI,
                              int64_t KF, double* den, double* G, cudaStream_t s);
+cudaError_t launch_bs_replicates(const double* f, const double* eps, double noise_sigma, int64_t R, int64_t N,
+                                 double* out, cudaStream_t s);
+cudaError_t launch_bs_stats(const double* G, const double* f, int64_t R, int64_t N, double* mean, double* var,
+                            double* mse, cudaStream_t s);
 cudaError_t launch_hankelize(const Plan& p, const double* sigma, const double* U, const double* V, int nterms,
                              double* out, cudaStream_t s);
 cudaError_t fft_set_attributes(int H, const char** which);

@@ -26,7 +26,7 @@ STATUS = {0: "SSA_OK", 1: "SSA_ERR_INVALID_ARGUMENT", 2: "SSA_ERR_NOT_CONVERGED"
 # every symbol include/ssa.h declares
 EXPORTS = ["ssa_options_default", "ssa_plan_create", "ssa_plan_destroy", "ssa_plan_fft_size",
            "ssa_plan_max_steps", "ssa_spectrum", "ssa_matvec", "ssa_hankelize", "ssa_decompose",
-           "ssa_reconstruct", "ssa_reconstruct_grouped", "ssa_hmatrix", "ssa_run_host", "ssa_status_string", "ssa_last_error",
+           "ssa_reconstruct", "ssa_reconstruct_grouped", "ssa_hmatrix", "ssa_bootstrap", "ssa_run_host", "ssa_status_string", "ssa_last_error",
            "ssa_plan_launch_count", "ssa_plan_phase_ms", "ssa_plan_profile", "ssa_plan_bidiagonals"]
 
 
@@ -86,6 +86,7 @@ def load_library():
     lib.ssa_decompose.argtypes = [vp, dp, dp, dp, dp, dp, vp]
     lib.ssa_reconstruct.argtypes = [vp, dp, dp, dp, dp, vp]
     lib.ssa_reconstruct_grouped.argtypes = [vp, dp, dp, dp, vp, i32, dp, vp]
+    lib.ssa_bootstrap.argtypes = [vp, dp, dp, ctypes.c_double, dp, dp, dp, dp, dp, vp]
     lib.ssa_hmatrix.argtypes = [dp, i64, i64, i64, i64, vp, i32, ctypes.POINTER(Options), ctypes.c_int, dp, dp, vp]
     lib.ssa_run_host.argtypes = [vp, dp, dp, dp, dp, dp, dp, vp]
     lib.ssa_status_string.argtypes = [ctypes.c_int]
@@ -258,6 +259,20 @@ class Plan:
         _check(load_library().ssa_reconstruct_grouped(self._h, sigma.data_ptr(), U.data_ptr(), V.data_ptr(),
                                                       g.ctypes.data, ng, out.data_ptr(), _stream(stream)))
         return out
+
+    def bootstrap(self, series, eps, noise_sigma: float, G=None, info=None, stream=None):
+        """Bootstrap study of the rank-k reconstruction (ssa_bootstrap):
+        series [N] clean F, eps [batch][N] noise.  Returns (mean, var, mse) [N] each."""
+        _dev_f64(series, (self.N,), "series")
+        _dev_f64(eps, (self.batch, self.N), "eps")
+        mean, var, mse = (self._t(self.N) for _ in range(3))
+        if G is not None:
+            _dev_f64(G, (self.batch, self.N), "G")
+        _check(load_library().ssa_bootstrap(self._h, series.data_ptr(), eps.data_ptr(), float(noise_sigma),
+                                            mean.data_ptr(), var.data_ptr(), mse.data_ptr(),
+                                            G.data_ptr() if G is not None else None,
+                                            info.data_ptr() if info is not None else None, _stream(stream)))
+        return mean, var, mse
 
     def run_host(self, series: np.ndarray, want_vectors: bool = True, stream=None, raise_on_status=True):
         """End-to-end on host arrays (copies inside the C call).  Returns numpy

@@ -20,6 +20,7 @@ import numpy as np
 __all__ = [
     "CONFIGS", "cfg1_series", "cfg2_series", "cfg2_batch", "cfg3_series",
     "cfg3_like_series", "cfg4_item", "cfg4_batch", "cfg5_problem", "change_point_series",
+    "bootstrap_series", "bootstrap_noise",
 ]
 
 # name -> (N, L, k, batch); K = N - L + 1.  BASELINE.json "configs" [0..4].
@@ -129,3 +130,16 @@ def change_point_series(N: int = 400, Q: int = 200, seed: int = 7) -> np.ndarray
     rng = np.random.default_rng(seed)
     f = np.where(n < Q, np.sin(2 * np.pi * n / 10), np.sin(2 * np.pi * n / 10.5))
     return f + 0.01 * rng.standard_normal(N)
+
+
+def bootstrap_series(N: int = 1000) -> np.ndarray:
+    """The rank-5 series of the bootstrap study (sec 6.3) with the
+    periods read in n (R17 / SURVEY.md §8(c) #17: as printed, (2π/13)(n/N) makes
+    the series numerically rank 3): f_n = 10 e^{-5n/N} + sin(2πn/13) + 2.5 sin(2πn/37)."""
+    n = _n(N)
+    return 10.0 * np.exp(-5.0 * n / N) + np.sin(2 * np.pi * n / 13) + 2.5 * np.sin(2 * np.pi * n / 37)
+
+
+def bootstrap_noise(R: int, N: int, seed: int = 6) -> np.ndarray:
+    """White noise eps_r ~ N(0,1)^N of replicate r from default_rng([seed, r]) ([R][N])."""
+    return np.stack([np.random.default_rng([seed, r]).standard_normal(N) for r in range(R)])

@@ -325,6 +325,26 @@ def test_hmatrix_oracle_pins():
     assert inside < 1e-3 and across > 20 * inside
 
 
+def test_bootstrap_oracle_pins():
+    """oracle.bootstrap: with no noise every replicate is the rank-5
+    series itself (a finite-rank series is reconstructed exactly from its d triples,
+    PAPER.md:117-121), so mean = F, var = 0, mse = 0; with noise, var >= 0 and the
+    identity mse = bias^2 + (R-1)/R var holds (definitions of the three estimates)."""
+    N, L, d, R = 120, 60, 5, 6
+    f = ssa_inputs.bootstrap_series(N)
+    eps = ssa_inputs.bootstrap_noise(R, N)
+    mean, var, mse, G = oracle.bootstrap(f, eps, 0.0, L, d)
+    scale = np.abs(f).max()
+    assert np.abs(mean - f).max() <= 1e-11 * scale
+    assert var.max() <= 1e-20 * scale ** 2 and mse.max() <= 1e-20 * scale ** 2
+    mean, var, mse, G = oracle.bootstrap(f, eps, 0.3, L, d)
+    assert var.min() >= 0.0
+    assert np.abs(mse - ((mean - f) ** 2 + (R - 1) / R * var)).max() <= 1e-12 * mse.max()
+    # more noise, larger error of the estimate
+    _, _, mse2, _ = oracle.bootstrap(f, eps, 0.6, L, d)
+    assert mse2.mean() > mse.mean()
+
+
 def test_cfg1_oracle_spectrum_structure():
     """cfg1 (BASELINE configs[0]): σ₁ dominated by the exponential trend, then the two
     sinusoid pairs, then noise (SURVEY Appendix A 'Spectrum structure')."""
