@@ -185,13 +185,15 @@ __device__ __forceinline__ void correlate_reg4096(double2* buf, const double2* t
       const double2 Zp = zp;
       const double2 Zq = buf[swz4096(16 * bp + kp)];
       const double2 W = tw(p);  // exp(-2 pi i p / M)
-      const double2 E = make_double2(0.5 * (Zp.x + Zq.x), 0.5 * (Zp.y - Zq.y));
-      const double2 D = make_double2(0.5 * (Zp.x - Zq.x), 0.5 * (Zp.y + Zq.y));
+      // the two 1/2 factors of the split / merge are exact powers of two: folded into the
+      // final 1/H scale (invH / 4), bit-identical results, 8 multiplications fewer per pair
+      const double2 E = make_double2(Zp.x + Zq.x, Zp.y - Zq.y);
+      const double2 D = make_double2(Zp.x - Zq.x, Zp.y + Zq.y);
       const double2 WO = cmul(W, make_double2(D.y, -D.x));
       const double2 Xp = cadd(E, WO), Xq = conjg(csub(E, WO));
       const double2 Yp = cmulc(Fp, Xp), Yq = cmulc(Fq, Xq);
-      const double2 E2 = make_double2(0.5 * (Yp.x + Yq.x), 0.5 * (Yp.y - Yq.y));
-      const double2 D2 = make_double2(0.5 * (Yp.x - Yq.x), 0.5 * (Yp.y + Yq.y));
+      const double2 E2 = make_double2(Yp.x + Yq.x, Yp.y - Yq.y);
+      const double2 D2 = make_double2(Yp.x - Yq.x, Yp.y + Yq.y);
       const double2 O2 = cmulc(D2, W);
       zp = make_double2(E2.x - O2.y, E2.y + O2.x);
       buf[swz4096(16 * bp + kp)] = make_double2(E2.x + O2.y, O2.x - E2.y);
@@ -231,8 +233,8 @@ __device__ __forceinline__ void correlate_reg4096(double2* buf, const double2* t
   for (int q = 0; q < 16; ++q) a[q] = buf[swz4096(t + 256 * q)];
   twiddle16<true>(a, tw(2 * t));
   dft16<true, false>(a);
-  // a[n2] = H * y packed at n = t + 256 n2: real outputs 2n, 2n + 1
-  constexpr double invH = 1.0 / (double)H;
+  // a[n2] = 4 H * y packed at n = t + 256 n2 (the pair step's 1/4 deferred): real outputs 2n, 2n + 1
+  constexpr double invH = 0.25 / (double)H;
 #pragma unroll
   for (int n2 = 0; n2 < 16; ++n2) {
     const int i0 = 2 * (t + 256 * n2);
