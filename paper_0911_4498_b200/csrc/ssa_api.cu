@@ -124,12 +124,12 @@ static void free_plan(Plan& p) {
     if (p.ev[i]) cudaEventDestroy(p.ev[i]);
   for (int i = 0; i < 2; ++i)
     if (p.sub[i]) ssa_plan_destroy(reinterpret_cast<ssa_plan_t>(p.sub[i]));
-  for (int i = 0; i < 3; ++i)
+  for (int i = 0; i < 4; ++i)
     if (p.hs[i]) cudaStreamDestroy(p.hs[i]);
   if (p.lg_aux) cudaStreamDestroy(p.lg_aux);
   for (int i = 0; i < 2; ++i)
     if (p.lg_ev[i]) cudaEventDestroy(p.lg_ev[i]);
-  for (int i = 0; i < Plan::kMaxSlices + 2; ++i)
+  for (int i = 0; i < 2 * Plan::kMaxSlices + 2; ++i)
     if (p.hev[i]) cudaEventDestroy(p.hev[i]);
 }
 
@@ -678,7 +678,6 @@ extern "C" ssa_status ssa_run_host(ssa_plan_t plan, const double* h_series, doub
     if ((st = alloc((void**)&p.d_recon, B * k * p.N * 8, "recon staging")) != SSA_OK) return st;
   }
   cudaStream_t s = S(stream);
-  CK(cudaMemcpyAsync(p.d_series, h_series, B * p.N * 8, cudaMemcpyHostToDevice, s), "H2D series");
   // Pipelined path: the batch in slices; slice i is decomposed + reconstructed by sub-plan
   // i % 2 on compute stream i % 2 (so one slice's kernel tail overlaps the next slice's
   // start) while the copy stream brings finished slices back -- the device-to-host copy of
@@ -699,14 +698,25 @@ extern "C" ssa_status ssa_run_host(ssa_plan_t plan, const double* h_series, doub
       }
       p.sub_batch = sb;
     }
-    for (int i = 0; i < 3; ++i)
+    for (int i = 0; i < 4; ++i)
       if (!p.hs[i]) CK(cudaStreamCreateWithFlags(&p.hs[i], cudaStreamNonBlocking), "cudaStreamCreate");
-    for (int i = 0; i < Plan::kMaxSlices + 2; ++i)
+    for (int i = 0; i < 2 * Plan::kMaxSlices + 2; ++i)
       if (!p.hev[i]) CK(cudaEventCreateWithFlags(&p.hev[i], cudaEventDisableTiming), "cudaEventCreate");
-    cudaEvent_t ev_in = p.hev[Plan::kMaxSlices], ev_cp = p.hev[Plan::kMaxSlices + 1];
+    cudaEvent_t ev_in = p.hev[2 * Plan::kMaxSlices], ev_cp = p.hev[2 * Plan::kMaxSlices + 1];
     CK(cudaEventRecord(ev_in, s), "event record");
-    for (int c = 0; c < 2; ++c) CK(cudaStreamWaitEvent(p.hs[c], ev_in, 0), "stream wait");
-    CK(cudaStreamWaitEvent(p.hs[2], ev_in, 0), "stream wait");
+    for (int c = 0; c < 4; ++c) CK(cudaStreamWaitEvent(p.hs[c], ev_in, 0), "stream wait");
+    // inputs slice by slice on their own copy stream (host-to-device engine): slice i's
+    // compute waits only for its own series
+    for (int i = 0; i < nsl; ++i) {
+      const size_t b0 = (size_t)i * sb;
+      if (b0 >= B) break;
+      const size_t nb = std::min<size_t>(sb, B - b0);
+      const size_t s0 = (nb == (size_t)sb) ? b0 : B - sb;
+      CK(cudaMemcpyAsync(p.d_series + s0 * p.N, h_series + s0 * p.N, (size_t)sb * p.N * 8, cudaMemcpyHostToDevice,
+                         p.hs[3]),
+         "H2D series");
+      CK(cudaEventRecord(p.hev[Plan::kMaxSlices + i], p.hs[3]), "event record");
+    }
     for (int i = 0; i < nsl; ++i) {
       const size_t b0 = (size_t)i * sb;
       if (b0 >= B) break;
@@ -717,6 +727,7 @@ extern "C" ssa_status ssa_run_host(ssa_plan_t plan, const double* h_series, doub
       // then re-runs the tail of the batch (results of the overlap are written twice,
       // identically)
       const size_t s0 = (nb == (size_t)sb) ? b0 : B - sb;
+      CK(cudaStreamWaitEvent(cs, p.hev[Plan::kMaxSlices + i], 0), "stream wait");
       q.series_base = (int64_t)s0;  // same start vectors as the single-launch path
       if ((st = ssa_decompose(reinterpret_cast<ssa_plan_t>(p.sub[i & 1]), p.d_series + s0 * p.N, p.d_sigma + s0 * k,
                               p.d_Uout + s0 * k * p.L, p.d_Vout + s0 * k * p.K, p.d_info + s0, cs)) != SSA_OK)
@@ -740,6 +751,7 @@ extern "C" ssa_status ssa_run_host(ssa_plan_t plan, const double* h_series, doub
     CK(cudaEventRecord(ev_cp, p.hs[2]), "event record");
     CK(cudaStreamWaitEvent(s, ev_cp, 0), "stream wait");
   } else {
+    CK(cudaMemcpyAsync(p.d_series, h_series, B * p.N * 8, cudaMemcpyHostToDevice, s), "H2D series");
     if ((st = ssa_decompose(plan, p.d_series, p.d_sigma, p.d_Uout, p.d_Vout, p.d_info, stream)) != SSA_OK) return st;
     if ((st = ssa_reconstruct(plan, p.d_sigma, p.d_Uout, p.d_Vout, p.d_recon, stream)) != SSA_OK) return st;
     if (h_sigma) CK(cudaMemcpyAsync(h_sigma, p.d_sigma, B * k * 8, cudaMemcpyDeviceToHost, s), "D2H sigma");

@@ -113,9 +113,9 @@ struct Plan {
   void* sub[2] = {nullptr, nullptr};  // ssa_plan_t
   int64_t sub_batch = 0;
   int64_t series_base = 0;  // sub-plans: global index of their current slice's first series
-  cudaStream_t hs[3] = {};
+  cudaStream_t hs[4] = {};  // compute x2, device-to-host, host-to-device
   static constexpr int kMaxSlices = 16;
-  cudaEvent_t hev[kMaxSlices + 2] = {};
+  cudaEvent_t hev[2 * kMaxSlices + 2] = {};  // per slice: computed, inputs copied; + 2
   int64_t launches = 0;
   static constexpr int kPhases = 5;  // spectrum, lanczos, bidiag_svd, ritz, hankelize
   cudaEvent_t ev[2 * kPhases] = {};
