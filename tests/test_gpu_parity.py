@@ -291,11 +291,13 @@ def test_plans_of_different_sizes_interleaved(P):
     assert np.array_equal(s1, s2)
 
 
-def test_run_host_pipelined_matches_device(P):
-    """ssa_run_host splits batches >= 512 into slices on two compute streams with the
-    device-to-host copies on a third; every output must equal the single-launch device
-    path bit for bit (per-series arithmetic is independent and fixed-order)."""
-    N, L, k, B = 300, 120, 4, 512
+@pytest.mark.parametrize("B", [512, 2100])
+def test_run_host_pipelined_matches_device(P, B):
+    """ssa_run_host splits batches >= 512 into slices (a partial last slice re-runs an
+    overlap) on two compute streams, inputs on a copy stream, outputs on another; every
+    output must equal the single-launch device path bit for bit (per-series arithmetic is
+    independent and fixed-order)."""
+    N, L, k = 300, 120, 4
     F = np.stack([ssa_inputs.cfg2_series(i, N) for i in range(B)])
     plan = P.Plan(N, L, k, B)
     s, U, V, G, info = plan.run_host(F)
