@@ -531,6 +531,20 @@ def main():
     if world > 1:
         dist.all_reduce(total, op=dist.ReduceOp.MAX)
     ms_per_step = float(total.item()) / args.steps
+    gather = None
+    if world > 1:
+        # the only collective: after compute, all ranks gather sigma and
+        # the per-series info over NCCL (timed apart from the compute steps)
+        from paper_0911_4498_b200.parallel import gather_rows
+        dist.barrier()
+        torch.cuda.synchronize()
+        g0 = time.perf_counter()
+        all_sigma = gather_rows(sigma, world)
+        all_info = gather_rows(info, world)
+        torch.cuda.synchronize()
+        gather = {"ms": 1e3 * (time.perf_counter() - g0), "rows": int(all_sigma.shape[0]),
+                  "bytes": int(all_sigma.numel() * 8 + all_info.numel()), "backend": "nccl all_gather"}
+        assert all_sigma.shape[0] == B * world
     inf = P.info_to_numpy(info)
     steps_m = inf["steps"].astype(np.int64)
     conv = float(np.mean(inf["converged"]))
@@ -558,6 +572,7 @@ def main():
                    "l2": "inputs (134 MB/GPU) > L2 and a 256 MiB L2 flush before every timed step",
                    "tol": 1e-12, "reorth": "CGS + DGKS"},
         "hankel_matvecs_per_s": matvecs,
+        **({"gather": gather} if gather else {}),
         "lanczos_steps": {"min": int(steps_m.min()), "median": float(np.median(steps_m)),
                           "max": int(steps_m.max()), "mean": float(steps_m.mean())},
         "converged_fraction": conv,
