@@ -2,13 +2,14 @@
 // too long for one CTA (BASELINE config 3: N = 2^20, L = 2^19, k = 32), one series at a
 // time with the whole GPU on it (Alg. 1, FRO PAPER.md:388-393).
 //
-// Each half-step is a short sequence of grid-wide kernels on the same stream:
+// Each half-step is a short sequence of grid-wide kernels on the same stream, each launched
+// with programmatic dependent launch (launch_pdl / pdl_wait, device_common.cuh):
 //   correlation  three-pass four-step FFT (ssa_large_fft.cu) with the recurrence term
 //                fused in the epilogue: r = X^T u_j - beta_j v_{j-1} (or X v_j - alpha_j u_j),
 //                plus per-CTA partial sums of squares;
-//   dots         h = B^T r: each CTA owns a 2048-element chunk of r (shared memory) and
-//                every warp streams whole basis rows of that chunk; per-CTA partials are
-//                then summed in a fixed order (deterministic);
+//   dots         h = B^T r: each CTA owns a 512-element chunk of r (registers), streams the
+//                basis rows of that chunk in groups of 8 with all loads in flight; per-CTA
+//                partials are then summed in a fixed order (deterministic);
 //   update       r -= B h with the rows in reverse order (recently read rows hit L2);
 //   finish       one warp (lg_finish): norms, the DGKS decision for a second pass, breakdown,
 //                alpha_j / beta_{j+1} in device memory; second-pass kernels read the flag
@@ -35,7 +36,7 @@ cudaError_t large_spectrum(const Plan& p, const double* series, double2* spec, i
 cudaError_t launch_bidiag_svd(const Plan& p, const DecomposeArgs& a, cudaStream_t s);
 void large_geom(const Plan& p, int* N1, int* N2);
 
-constexpr int kLgChunk = 2048;  // elements per CTA in dots / update / normalize
+constexpr int kLgChunk = 2048;  // elements per CTA of the start vector (lg_start)
 
 // device scalars of the long-series run
 struct LgScalars {
@@ -50,15 +51,6 @@ struct LgScalars {
   int conv;         // converged flag
   int pad;
 };
-
-__global__ void lg_sum(const double* __restrict__ part, int n, double* out) {
-  pdl_wait();
-  // one warp, fixed order: lane-strided partial sums then the shuffle tree
-  double s = 0.0;
-  for (int i = threadIdx.x; i < n; i += 32) s += part[i];
-  s = warp_sum(s);
-  if (threadIdx.x == 0) *out = s;
-}
 
 __global__ void __launch_bounds__(kThreads) lg_start(double* r, int n, int ld, uint64_t seed, uint64_t series,
                                                      double* part) {
@@ -441,7 +433,7 @@ cudaError_t large_decompose_one(Plan& p, const DecomposeArgs& a0, int b, cudaStr
   const int nchL = (ldL + kLgChunk - 1) / kLgChunk;
   int N1, N2;
   large_geom(p, &N1, &N2);
-  const int ncol = N2 / 8;  // partial sums written by large_col_inv
+  const int ncol = N2 / 8;  // partial sums written by lg_col_inv (one per 8-column CTA)
   double* U = p.d_U;
   double* V = p.d_V;
   const int w = p.m_max + 3;
