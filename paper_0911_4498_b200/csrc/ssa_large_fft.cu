@@ -95,7 +95,7 @@ struct ColFwdIn {
   size_t xs;
   int n_in;
   double2* Y;       // [items][H]
-  int vec;          // x and xs 16-byte aligned: pairs (x_2n, x_2n+1) as one 16-byte load
+  int vec;          // x 16-byte aligned: pairs (x_2n, x_2n+1) of aligned rows as one 16-byte load
 };
 struct ColFwdArgs {
   ColFwdIn in[2];   // blockIdx.z selects
@@ -116,6 +116,9 @@ __global__ void __launch_bounds__(kThreads) lg_col_fwd(ColFwdArgs args, const do
   const int n2_0 = blockIdx.x * kColW;
   const double* xi = a.x + (size_t)blockIdx.y * a.xs;
   double2* Yi = a.Y + (size_t)blockIdx.y * G::H;
+  // 16-byte pair loads when this row starts 16-byte aligned (every row when the stride is
+  // even; every other row of an odd stride, e.g. the v_i of length K = L + 1)
+  const bool rvec = a.vec && ((reinterpret_cast<uintptr_t>(xi) & 15) == 0);
   // thread t: column c = t & 7 of the CTA, rows n1 = (t >> 3) + 32 j (idx = t + 256 j)
   const int cc = threadIdx.x & (kColW - 1), r0 = threadIdx.x >> 3;
   const int i00 = 2 * (n2_0 + cc + N2 * r0);  // packed point n = n2 + N2 n1 -> x_2n, x_2n+1
@@ -124,7 +127,7 @@ __global__ void __launch_bounds__(kThreads) lg_col_fwd(ColFwdArgs args, const do
   for (int j = 0; j < NE; ++j) {
     const bool ok = threadIdx.x + j * kThreads < N1 * kColW;
     const int i0 = i00 + j * (2 * N2 * (kThreads / kColW));
-    if (a.vec && ok && i0 + 1 < a.n_in) {
+    if (rvec && ok && i0 + 1 < a.n_in) {
       v[j] = __ldg(reinterpret_cast<const double2*>(xi + i0));
     } else {
       v[j].x = (ok && i0 < a.n_in) ? __ldg(xi + i0) : 0.0;
@@ -586,8 +589,8 @@ void large_geom(const Plan& p, int* N1, int* N2) {
   *N2 = (int)(p.H / *N1);
 }
 
-// rows of x (row stride xs doubles) start 16-byte aligned
-static int vec16(const double* x, size_t xs) { return ((reinterpret_cast<uintptr_t>(x) & 15) == 0) && (xs % 2 == 0); }
+// x is 16-byte aligned (the kernel checks each row's start)
+static int vec16(const double* x, size_t) { return (reinterpret_cast<uintptr_t>(x) & 15) == 0; }
 
 static void col_fwd(const Plan& p, const ColFwdArgs& ca, int nz, int items, cudaStream_t s) {
   const int logH = ilog2(p.H);
