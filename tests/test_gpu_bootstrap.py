@@ -45,3 +45,17 @@ def test_bootstrap_noise_free_is_exact(P):
     mean, var, mse = plan.bootstrap(torch.from_numpy(f).cuda(), torch.from_numpy(eps).cuda(), 0.0)
     assert np.abs(mean.cpu().numpy() - f).max() <= 1e-10 * np.abs(f).max()
     assert var.cpu().numpy().max() <= 1e-18 * np.abs(f).max() ** 2
+
+
+def test_bootstrap_single_replicate(P):
+    """R = 1: the variance is defined as 0, the MSE is the squared error of the one replicate."""
+    N, L = 150, 60
+    f = ssa_inputs.bootstrap_series(N)
+    eps = ssa_inputs.bootstrap_noise(1, N)
+    plan = P.Plan(N, L, 5, 1)
+    G = torch.empty(1, N, dtype=torch.float64, device="cuda")
+    mean, var, mse = plan.bootstrap(torch.from_numpy(f).cuda(), torch.from_numpy(eps).cuda(), 0.3, G=G)
+    g = G.cpu().numpy()[0]
+    assert np.array_equal(mean.cpu().numpy(), g)
+    assert not var.cpu().numpy().any()
+    assert np.allclose(mse.cpu().numpy(), (g - f) ** 2, rtol=1e-15, atol=0)

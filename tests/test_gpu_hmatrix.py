@@ -47,3 +47,18 @@ def test_hmatrix_invalid_arguments(P):
                        (120, 20, 10, [1])]:
         with pytest.raises(P.SsaError):
             P.hmatrix(f, B, T, L, I)
+
+
+@pytest.mark.parametrize("B,T,L", [(120, 120, 30), (60, 25, 25), (41, 120, 40)])
+def test_hmatrix_edge_shapes(P, B, T, L):
+    """Edge shapes: one base and one test window (B = T = N), single-lag test windows
+    (T = L: K2 = 1), the smallest base window (B = L + 1: K_B = 2)."""
+    N = 120
+    rng = np.random.default_rng(B + T + L)
+    n = np.arange(1, N + 1, dtype=float)
+    f = np.sin(2 * np.pi * n / 9.0) + 0.5 * np.cos(2 * np.pi * n / 23.0) + 0.05 * rng.standard_normal(N)
+    I = [1] if B - L + 1 < 3 else [1, 2]
+    G, info = P.hmatrix(torch.from_numpy(f).cuda(), B, T, L, I)
+    ref = oracle.hmatrix(f, B, T, L, I)
+    assert G.shape == ref.shape
+    assert np.abs(G.cpu().numpy() - ref).max() <= 1e-9
