@@ -205,14 +205,16 @@ def micro_hmatrix(P, N: int = 4000):
     """Heterogeneity matrix (ssa_hmatrix) in the paper's comparison
     setting (PAPER.md:1068-1076): Eq. (hseries) series with Q = N/2, B = T = N/4, L = B/2,
     I = {1, 2}; N = 4000 here (3001 base-window decompositions, 6002 Hankel products of the
-    whole series, a 3001 x 3001 matrix).  Whole call timed (workspace allocation included)."""
+    whole series, a 3001 x 3001 matrix).  ssa_hmatrix_exec timed (plan and workspace
+    created once, outside; the exec ends with the per-window status read-back)."""
     import torch
     Q, B = N // 2, N // 4
     T, L = B, B // 2
     f = torch.from_numpy(ssa_inputs.change_point_series(N, Q, 7)).cuda()
-    G, info = P.hmatrix(f, B, T, L, [1, 2])
+    hm = P.HMatrix(N, B, T, L, [1, 2])
+    G, info = hm(f)
     torch.cuda.synchronize()
-    ms = min(_events_ms(lambda: P.hmatrix(f, B, T, L, [1, 2], out=G, info=info)) for _ in range(3))
+    ms = min(_events_ms(lambda: hm(f, out=G, info=info)) for _ in range(3))
     nb, nt = N - B + 1, N - T + 1
     inf = P.info_to_numpy(info)
     res = {"value": nb * nt / (ms * 1e-3), "unit": "H-matrix entries/s", "ms": ms,

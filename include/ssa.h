@@ -164,12 +164,22 @@ ssa_status ssa_reconstruct_grouped(ssa_plan_t plan, const double* d_sigma, const
  * X_F^T U_r^(i) of the whole series per (i, r).
  *   d_series: [N] device;  I: HOST [nI] distinct 1-based triple indices, each <= min(L, B-L+1)
  *   d_G: [N-B+1][N-T+1] device;  d_info: [N-B+1] per-window decompose info, or NULL
- * Needs N >= 3, 2 <= L < B <= N, L <= T <= N.  Allocates and frees its own workspace and
- * synchronizes `stream` before returning.  Returns NOT_CONVERGED (G still written) if a
- * base window did not converge. */
+ * Needs N >= 3, 2 <= L < B <= N, L <= T <= N.  The one-shot call creates the plan below,
+ * executes it and destroys it.  Returns NOT_CONVERGED (G still written) if a base window
+ * did not converge. */
 ssa_status ssa_hmatrix(const double* d_series, int64_t N, int64_t B, int64_t T, int64_t L, const int32_t* I,
                        int32_t nI, const ssa_options* opt, int device, double* d_G, ssa_series_info* d_info,
                        void* stream);
+
+/* The same as a plan (sub-plans and workspace allocated once, OUT_OF_MEMORY reported at
+ * creation) and an execution that can be repeated on new series of length N; exec
+ * synchronizes `stream` to read the per-window info.  Not thread-safe per plan. */
+typedef struct ssa_hplan_s* ssa_hplan_t;
+ssa_status ssa_hmatrix_plan_create(int64_t N, int64_t B, int64_t T, int64_t L, const int32_t* I, int32_t nI,
+                                   const ssa_options* opt, int device, ssa_hplan_t* out);
+ssa_status ssa_hmatrix_exec(ssa_hplan_t hplan, const double* d_series, double* d_G, ssa_series_info* d_info,
+                            void* stream);
+void ssa_hmatrix_plan_destroy(ssa_hplan_t hplan);
 
 /* Bootstrap study of the rank-d reconstruction (sec 6.3): for the plan's
  * batch = R replicates F'_r = F + noise_sigma * eps_r of the clean series F, the k = d

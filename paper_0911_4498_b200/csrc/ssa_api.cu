@@ -549,10 +549,32 @@ extern "C" ssa_status ssa_reconstruct_grouped(ssa_plan_t plan, const double* d_s
   return SSA_OK;
 }
 
-extern "C" ssa_status ssa_hmatrix(const double* d_series, int64_t N, int64_t B, int64_t T, int64_t L,
-                                  const int32_t* I, int32_t nI, const ssa_options* opt, int device, double* d_G,
-                                  ssa_series_info* d_info, void* stream) {
-  if (!d_series || !d_G || !I) return fail(SSA_ERR_INVALID_ARGUMENT, "NULL argument");
+// ---- heterogeneity matrix: plan (sub-plans + workspace, allocated once) and exec --------
+struct ssa_hplan_s {
+  int64_t N = 0, B = 0, T = 0, L = 0, KB = 0, KF = 0, nwin = 0;
+  int nI = 0, kI = 0, device = 0;
+  ssa_plan_t pa = nullptr, p1 = nullptr, pc = nullptr;  // window decompose, spectrum, products
+  double *win = nullptr, *sig = nullptr, *U = nullptr, *V = nullptr, *x = nullptr, *y = nullptr, *spec = nullptr,
+         *den = nullptr;
+  int32_t* d_idx = nullptr;
+  ssa_series_info* info = nullptr;
+};
+
+extern "C" void ssa_hmatrix_plan_destroy(ssa_hplan_t h) {
+  if (!h) return;
+  for (void* q : {(void*)h->win, (void*)h->sig, (void*)h->U, (void*)h->V, (void*)h->x, (void*)h->y, (void*)h->spec,
+                  (void*)h->d_idx, (void*)h->den, (void*)h->info})
+    if (q) cudaFree(q);
+  if (h->pa) ssa_plan_destroy(h->pa);
+  if (h->pc) ssa_plan_destroy(h->pc);
+  if (h->p1) ssa_plan_destroy(h->p1);
+  delete h;
+}
+
+extern "C" ssa_status ssa_hmatrix_plan_create(int64_t N, int64_t B, int64_t T, int64_t L, const int32_t* I, int32_t nI,
+                                              const ssa_options* opt, int device, ssa_hplan_t* out) {
+  if (!out || !I) return fail(SSA_ERR_INVALID_ARGUMENT, "NULL argument");
+  *out = nullptr;
   if (N < 3 || L < 2 || B <= L || B > N || T < L || T > N)
     return fail(SSA_ERR_INVALID_ARGUMENT, "need N >= 3, 2 <= L < B <= N, L <= T <= N (N=%lld B=%lld T=%lld L=%lld)",
                 (long long)N, (long long)B, (long long)T, (long long)L);
@@ -569,66 +591,77 @@ extern "C" ssa_status ssa_hmatrix(const double* d_series, int64_t N, int64_t B, 
   }
   if (kI > ssa::kMaxK) return fail(SSA_ERR_INVALID_ARGUMENT, "max(I) = %d > %d", kI, ssa::kMaxK);
   CK(cudaSetDevice(device), "cudaSetDevice");
-  cudaStream_t s = S(stream);
-  const int64_t nwin = N - B + 1, KF = N - L + 1;
-  ssa_plan_t pa = nullptr, pc = nullptr, p1 = nullptr;
-  double *win = nullptr, *sig = nullptr, *U = nullptr, *V = nullptr, *x = nullptr, *y = nullptr, *spec = nullptr,
-         *den = nullptr;
-  int32_t* d_idx = nullptr;
-  ssa_series_info* info = d_info;
-  bool own_info = false;
+  ssa_hplan_s* h = new ssa_hplan_s();
+  h->N = N; h->B = B; h->T = T; h->L = L; h->KB = KB; h->KF = N - L + 1; h->nwin = N - B + 1;
+  h->nI = nI; h->kI = kI; h->device = device;
+  const int64_t nwin = h->nwin;
   ssa_status st = SSA_OK;
-  auto A = [&](void** ptr, size_t bytes, const char* what) { return alloc(ptr, bytes, what); };
   do {
-    // 1. leading left singular vectors of every base window (batched decompose)
-    if ((st = ssa_plan_create(B, L, kI, nwin, opt, device, &pa)) != SSA_OK) break;
-    if ((st = A((void**)&win, (size_t)nwin * B * 8, "H-matrix windows")) != SSA_OK) break;
-    if ((st = A((void**)&sig, (size_t)nwin * kI * 8, "H-matrix sigma")) != SSA_OK) break;
-    if ((st = A((void**)&U, (size_t)nwin * kI * L * 8, "H-matrix U")) != SSA_OK) break;
-    if ((st = A((void**)&V, (size_t)nwin * kI * KB * 8, "H-matrix V")) != SSA_OK) break;
-    if (!info) {
-      if ((st = A((void**)&info, (size_t)nwin * sizeof(ssa_series_info), "H-matrix info")) != SSA_OK) break;
-      own_info = true;
-    }
-    if (ssa::launch_hm_windows(d_series, nwin, B, win, s) != cudaSuccess) { st = cuda_fail(cudaGetLastError(), "hm windows"); break; }
-    if ((st = ssa_decompose(pa, win, sig, U, V, info, stream)) != SSA_OK) break;
-    // 2. spectrum of the whole series once; X_F^T U_r for every (window, r) through it
-    if ((st = ssa_plan_create(N, L, 0, 1, opt, device, &p1)) != SSA_OK) break;
-    if ((st = ssa_plan_create(N, L, 0, nwin * nI, opt, device, &pc)) != SSA_OK) break;
-    const Plan& qc = pc->p;
-    if ((st = A((void**)&spec, (size_t)(qc.H + 1) * 16, "H-matrix spectrum")) != SSA_OK) break;
-    if ((st = ssa_spectrum(p1, d_series, spec, stream)) != SSA_OK) break;
-    if ((st = A((void**)&d_idx, (size_t)nI * 4, "H-matrix index")) != SSA_OK) break;
-    if ((st = A((void**)&x, (size_t)nwin * nI * L * 8, "H-matrix vectors")) != SSA_OK) break;
-    if ((st = A((void**)&y, (size_t)nwin * nI * KF * 8, "H-matrix projections")) != SSA_OK) break;
-    CK(cudaMemcpyAsync(d_idx, idx.data(), (size_t)nI * 4, cudaMemcpyHostToDevice, s), "H2D index");
-    if (ssa::launch_hm_gather(U, nwin, kI, L, d_idx, nI, x, s) != cudaSuccess) { st = cuda_fail(cudaGetLastError(), "hm gather"); break; }
-    cudaError_t e;
-    if (qc.large)
-      e = ssa::large_correlate(qc, reinterpret_cast<const double2*>(spec), 0, x, (size_t)L, (int)L, y, (size_t)KF, (int)KF,
-                               (int)KF, nullptr, 0, nullptr, nullptr, (int)(nwin * nI), s);
-    else
-      e = ssa::launch_matvec_strided(qc, reinterpret_cast<const double2*>(spec), 0, x, y, 1, s);
-    if (e != cudaSuccess) { st = cuda_fail(e, "H-matrix projections"); break; }
-    // 3. the matrix: windowed sums of the squared projections over the norms of the lags
-    if ((st = A((void**)&den, (size_t)(N - T + 1) * 8, "H-matrix norms")) != SSA_OK) break;
-    if ((e = ssa::launch_hm_matrix(d_series, N, T, L, y, nwin, nI, KF, den, d_G, s)) != cudaSuccess) {
-      st = cuda_fail(e, "H-matrix kernel");
-      break;
-    }
-    CK(cudaStreamSynchronize(s), "stream sync");
-    std::vector<ssa_series_info> hi((size_t)nwin);
-    CK(cudaMemcpy(hi.data(), info, (size_t)nwin * sizeof(ssa_series_info), cudaMemcpyDeviceToHost), "D2H info");
-    for (const auto& q : hi)
-      if (q.status != SSA_OK) { st = (ssa_status)q.status; break; }
+    if ((st = ssa_plan_create(B, L, kI, nwin, opt, device, &h->pa)) != SSA_OK) break;
+    if ((st = ssa_plan_create(N, L, 0, 1, opt, device, &h->p1)) != SSA_OK) break;
+    if ((st = ssa_plan_create(N, L, 0, nwin * nI, opt, device, &h->pc)) != SSA_OK) break;
+    if ((st = alloc((void**)&h->win, (size_t)nwin * B * 8, "H-matrix windows")) != SSA_OK) break;
+    if ((st = alloc((void**)&h->sig, (size_t)nwin * kI * 8, "H-matrix sigma")) != SSA_OK) break;
+    if ((st = alloc((void**)&h->U, (size_t)nwin * kI * L * 8, "H-matrix U")) != SSA_OK) break;
+    if ((st = alloc((void**)&h->V, (size_t)nwin * kI * KB * 8, "H-matrix V")) != SSA_OK) break;
+    if ((st = alloc((void**)&h->info, (size_t)nwin * sizeof(ssa_series_info), "H-matrix info")) != SSA_OK) break;
+    if ((st = alloc((void**)&h->spec, (size_t)(h->pc->p.H + 1) * 16, "H-matrix spectrum")) != SSA_OK) break;
+    if ((st = alloc((void**)&h->d_idx, (size_t)nI * 4, "H-matrix index")) != SSA_OK) break;
+    if ((st = alloc((void**)&h->x, (size_t)nwin * nI * L * 8, "H-matrix vectors")) != SSA_OK) break;
+    if ((st = alloc((void**)&h->y, (size_t)nwin * nI * h->KF * 8, "H-matrix projections")) != SSA_OK) break;
+    if ((st = alloc((void**)&h->den, (size_t)(N - T + 1) * 8, "H-matrix norms")) != SSA_OK) break;
+    cudaError_t e = cudaMemcpy(h->d_idx, idx.data(), (size_t)nI * 4, cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) { st = cuda_fail(e, "H2D index"); break; }
   } while (0);
-  cudaStreamSynchronize(s);
-  for (void* q : {(void*)win, (void*)sig, (void*)U, (void*)V, (void*)x, (void*)y, (void*)spec, (void*)d_idx, (void*)den})
-    if (q) cudaFree(q);
-  if (own_info && info) cudaFree(info);
-  if (pa) ssa_plan_destroy(pa);
-  if (pc) ssa_plan_destroy(pc);
-  if (p1) ssa_plan_destroy(p1);
+  if (st != SSA_OK) { ssa_hmatrix_plan_destroy(h); return st; }
+  *out = h;
+  return SSA_OK;
+}
+
+extern "C" ssa_status ssa_hmatrix_exec(ssa_hplan_t h, const double* d_series, double* d_G, ssa_series_info* d_info,
+                                       void* stream) {
+  if (!h || !d_series || !d_G) return fail(SSA_ERR_INVALID_ARGUMENT, "NULL argument");
+  CK(cudaSetDevice(h->device), "cudaSetDevice");
+  cudaStream_t s = S(stream);
+  const int64_t nwin = h->nwin;
+  ssa_series_info* info = d_info ? d_info : h->info;
+  ssa_status st;
+  cudaError_t e;
+  // 1. leading left singular vectors of every base window (batched decompose)
+  if ((e = ssa::launch_hm_windows(d_series, nwin, h->B, h->win, s)) != cudaSuccess) return cuda_fail(e, "hm windows");
+  if ((st = ssa_decompose(h->pa, h->win, h->sig, h->U, h->V, info, stream)) != SSA_OK) return st;
+  // 2. spectrum of the whole series once; X_F^T U_r for every (window, r) through it
+  if ((st = ssa_spectrum(h->p1, d_series, h->spec, stream)) != SSA_OK) return st;
+  if ((e = ssa::launch_hm_gather(h->U, nwin, h->kI, h->L, h->d_idx, h->nI, h->x, s)) != cudaSuccess)
+    return cuda_fail(e, "hm gather");
+  const Plan& qc = h->pc->p;
+  if (qc.large)
+    e = ssa::large_correlate(qc, reinterpret_cast<const double2*>(h->spec), 0, h->x, (size_t)h->L, (int)h->L, h->y,
+                             (size_t)h->KF, (int)h->KF, (int)h->KF, nullptr, 0, nullptr, nullptr, (int)(nwin * h->nI), s);
+  else
+    e = ssa::launch_matvec_strided(qc, reinterpret_cast<const double2*>(h->spec), 0, h->x, h->y, 1, s);
+  if (e != cudaSuccess) return cuda_fail(e, "H-matrix projections");
+  // 3. the matrix: windowed sums of the squared projections over the norms of the lags
+  if ((e = ssa::launch_hm_matrix(d_series, h->N, h->T, h->L, h->y, nwin, h->nI, h->KF, h->den, d_G, s)) != cudaSuccess)
+    return cuda_fail(e, "H-matrix kernel");
+  // per-window outcome (the host reads it after the stream synchronizes)
+  std::vector<ssa_series_info> hi((size_t)nwin);
+  CK(cudaMemcpyAsync(hi.data(), info, (size_t)nwin * sizeof(ssa_series_info), cudaMemcpyDeviceToHost, s), "D2H info");
+  CK(cudaStreamSynchronize(s), "stream sync");
+  for (const auto& q : hi)
+    if (q.status != SSA_OK) return fail((ssa_status)q.status, "a base window did not converge");
+  return SSA_OK;
+}
+
+extern "C" ssa_status ssa_hmatrix(const double* d_series, int64_t N, int64_t B, int64_t T, int64_t L,
+                                  const int32_t* I, int32_t nI, const ssa_options* opt, int device, double* d_G,
+                                  ssa_series_info* d_info, void* stream) {
+  if (!d_series || !d_G || !I) return fail(SSA_ERR_INVALID_ARGUMENT, "NULL argument");
+  ssa_hplan_t h = nullptr;
+  ssa_status st = ssa_hmatrix_plan_create(N, B, T, L, I, nI, opt, device, &h);
+  if (st != SSA_OK) return st;
+  st = ssa_hmatrix_exec(h, d_series, d_G, d_info, stream);
+  ssa_hmatrix_plan_destroy(h);
   return st;
 }
 

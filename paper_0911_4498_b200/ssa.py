@@ -26,7 +26,8 @@ STATUS = {0: "SSA_OK", 1: "SSA_ERR_INVALID_ARGUMENT", 2: "SSA_ERR_NOT_CONVERGED"
 # every symbol include/ssa.h declares
 EXPORTS = ["ssa_options_default", "ssa_plan_create", "ssa_plan_destroy", "ssa_plan_fft_size",
            "ssa_plan_max_steps", "ssa_spectrum", "ssa_matvec", "ssa_hankelize", "ssa_decompose",
-           "ssa_reconstruct", "ssa_reconstruct_grouped", "ssa_hmatrix", "ssa_bootstrap", "ssa_run_host", "ssa_status_string", "ssa_last_error",
+           "ssa_reconstruct", "ssa_reconstruct_grouped", "ssa_hmatrix", "ssa_hmatrix_plan_create", "ssa_hmatrix_exec",
+           "ssa_hmatrix_plan_destroy", "ssa_bootstrap", "ssa_run_host", "ssa_status_string", "ssa_last_error",
            "ssa_plan_launch_count", "ssa_plan_phase_ms", "ssa_plan_profile", "ssa_plan_bidiagonals"]
 
 
@@ -87,6 +88,11 @@ def load_library():
     lib.ssa_reconstruct.argtypes = [vp, dp, dp, dp, dp, vp]
     lib.ssa_reconstruct_grouped.argtypes = [vp, dp, dp, dp, vp, i32, dp, vp]
     lib.ssa_bootstrap.argtypes = [vp, dp, dp, ctypes.c_double, dp, dp, dp, dp, dp, vp]
+    lib.ssa_hmatrix_plan_create.argtypes = [i64, i64, i64, i64, vp, i32, ctypes.POINTER(Options), ctypes.c_int,
+                                            ctypes.POINTER(vp)]
+    lib.ssa_hmatrix_exec.argtypes = [vp, dp, dp, dp, vp]
+    lib.ssa_hmatrix_plan_destroy.argtypes = [vp]
+    lib.ssa_hmatrix_plan_destroy.restype = None
     lib.ssa_hmatrix.argtypes = [dp, i64, i64, i64, i64, vp, i32, ctypes.POINTER(Options), ctypes.c_int, dp, dp, vp]
     lib.ssa_run_host.argtypes = [vp, dp, dp, dp, dp, dp, dp, vp]
     lib.ssa_status_string.argtypes = [ctypes.c_int]
@@ -319,6 +325,52 @@ def hmatrix(series, B: int, T: int, L: int, I, *, tol: float = 1e-12, seed: int 
     _check(lib.ssa_hmatrix(series.data_ptr(), N, B, T, L, idx.ctypes.data, len(idx), ctypes.byref(opt), dev,
                            G.data_ptr(), info.data_ptr(), _stream(stream)))
     return G, info
+
+
+class HMatrix:
+    """ssa_hmatrix_plan_create / exec / destroy: the heterogeneity matrix of series of
+    length N with base windows B, test windows T, window L and triples I (1-based), the
+    sub-plans and workspace allocated once."""
+
+    def __init__(self, N: int, B: int, T: int, L: int, I, *, tol: float = 1e-12, seed: int = 42,
+                 device: int | None = None):
+        import torch
+        lib = load_library()
+        if not torch.cuda.is_available():
+            raise RuntimeError("no CUDA device: libssa has no CPU fallback")
+        self.device = torch.cuda.current_device() if device is None else int(device)
+        self.N, self.B, self.T, self.L = N, B, T, L
+        idx = np.ascontiguousarray(I, dtype=np.int32)
+        opt = Options()
+        _check(lib.ssa_options_default(ctypes.byref(opt)))
+        opt.tol, opt.seed = tol, seed
+        h = ctypes.c_void_p()
+        _check(lib.ssa_hmatrix_plan_create(N, B, T, L, idx.ctypes.data, len(idx), ctypes.byref(opt), self.device,
+                                           ctypes.byref(h)))
+        self._h = h
+
+    def __call__(self, series, out=None, info=None, stream=None):
+        import torch
+        _dev_f64(series, (self.N,), "series")
+        nb, nt = self.N - self.B + 1, self.N - self.T + 1
+        G = torch.empty((nb, nt), dtype=torch.float64, device=series.device) if out is None else out
+        _dev_f64(G, (nb, nt), "out")
+        if info is None:
+            info = torch.zeros((nb, INFO_DTYPE.itemsize), dtype=torch.uint8, device=series.device)
+        _check(load_library().ssa_hmatrix_exec(self._h, series.data_ptr(), G.data_ptr(), info.data_ptr(),
+                                               _stream(stream)))
+        return G, info
+
+    def close(self):
+        if getattr(self, "_h", None):
+            load_library().ssa_hmatrix_plan_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def info_to_numpy(info_tensor) -> np.ndarray:

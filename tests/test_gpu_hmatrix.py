@@ -62,3 +62,16 @@ def test_hmatrix_edge_shapes(P, B, T, L):
     ref = oracle.hmatrix(f, B, T, L, I)
     assert G.shape == ref.shape
     assert np.abs(G.cpu().numpy() - ref).max() <= 1e-9
+
+
+def test_hmatrix_plan_reuse_matches_one_shot(P):
+    """A plan executed on two different series gives exactly the one-shot results."""
+    f1 = ssa_inputs.change_point_series(300, 150, 1)
+    f2 = ssa_inputs.change_point_series(300, 100, 2)
+    hm = P.HMatrix(300, 70, 60, 30, [1, 2])
+    for f in (f1, f2):
+        x = torch.from_numpy(f).cuda()
+        G, _ = hm(x)
+        G1, _ = P.hmatrix(x, 70, 60, 30, [1, 2])
+        assert torch.equal(G, G1)
+    hm.close()
