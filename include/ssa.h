@@ -19,13 +19,17 @@
  *    8-byte aligned (16-byte for d_spec).
  *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).  Every
  *    device-pointer call is asynchronous with respect to the host: it only enqueues
- *    kernels on `stream`.  Argument validation happens synchronously before anything
- *    is enqueued.
+ *    kernels on `stream` -- except ssa_run_host and the H-matrix calls, which
+ *    synchronize `stream` (documented there).  Argument validation happens synchronously
+ *    before anything is enqueued.
  *  - Errors are status codes; no exception crosses the ABI.  ssa_last_error() returns
  *    a thread-local human-readable detail for the last non-OK status.
  *  - A plan owns all its device workspace (spectra, Krylov bases, bidiagonal factors,
- *    scratch), allocated once in ssa_plan_create, so out-of-memory is reported there.
- *    Plans are not thread-safe; use one plan per concurrent stream.
+ *    scratch), allocated once in ssa_plan_create, so out-of-memory is reported there;
+ *    the only exceptions are scratch buffers grown on first use by ssa_run_host,
+ *    ssa_reconstruct_grouped (long path) and ssa_bootstrap, which then report
+ *    OUT_OF_MEMORY themselves.  Plans are not thread-safe; use one plan per concurrent
+ *    stream.
  */
 #ifndef SSA_H_
 #define SSA_H_
