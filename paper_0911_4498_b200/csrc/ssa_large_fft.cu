@@ -33,10 +33,14 @@ constexpr int kColW = 8;  // columns per CTA in the column passes (one warp each
 struct WarpSync {
   __device__ __forceinline__ void operator()() const { __syncwarp(); }
 };
-// Named barrier over 64 threads (two warps); ids 1..15 (0 is __syncthreads).
+// Named barriers over 64 / 128 threads (two / four warps); ids 1..15 (0 is __syncthreads).
 struct NamedSync64 {
   int id;
   __device__ __forceinline__ void operator()() const { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
+};
+struct NamedSync128 {
+  int id;
+  __device__ __forceinline__ void operator()() const { asm volatile("bar.sync %0, 128;" ::"r"(id) : "memory"); }
 };
 
 // Compile-time four-step geometry for H = 2^LOGH.
@@ -381,7 +385,45 @@ __global__ void __launch_bounds__(kThreads) lg_row_cta(const double2* __restrict
   const size_t item = blockIdx.y;
   double2* Ya = a.Ya + item * G::H;
   double2* Yb = (a.mode == 2) ? a.Yb + item * G::H : nullptr;
-  const int nrows = (a.mode == 2 ? 2 : 1) * (two ? 2 : 1);
+  if constexpr (G::L2 >= 10) {
+    if (a.mode != 2) {
+      // rows A and B concurrently, 128 threads each (named barriers): every thread holds
+      // the 8 points t + 128 e of its row, i.e. one butterfly of the outermost radix-8 pass,
+      // done in registers straight from the load; the inverse ends the same way into the
+      // twiddled store
+      constexpr int NEH = N2 / 128;
+      const int half = threadIdx.x >> 7, t = threadIdx.x & 127;
+      const bool active = (half == 0) || two;
+      double2* row = half ? bB : bA;
+      const int rid = half ? B : A;
+      double2 v[NEH];
+      if (active) {
+        const double2* src = Ya + (size_t)rid * N2;
+#pragma unroll
+        for (int e = 0; e < NEH; ++e) v[e] = src[t + 128 * e];
+      }
+      __syncthreads();  // twiddle tables
+      const NamedSync128 sync{1 + half};
+      if (active) {
+        dif_pass0_store<G::L2, 128>(v, t, row, tw2);
+        sync();
+        fft_run_inner_t<G::L2, false>(row, tw2, t, 128, sync);
+      }
+      __syncthreads();
+      row_pair_step<LOGH>(a, item, A, two, __ldg(TWA + A), tw2, bA, bB, cA, cB, threadIdx.x, blockDim.x);
+      if (a.mode == 0) return;
+      __syncthreads();
+      if (active) {
+        fft_run_inner_t<G::L2, true>(row, tw2, t, 128, sync);
+        dif_pass0_inverse_load<G::L2, 128>(v, t, row, tw2);
+        double2* Yo = Ya + (size_t)rid * N2;
+        twiddle_seq<LOGH, NEH>(th, (long long)rid * t, (long long)rid * 128, NEH, [&](int e, double2 w) {
+          Yo[t + 128 * e] = cmulc(v[e], w);
+        });
+      }
+      return;
+    }
+  }
   // all rows' loads in flight before the shared-memory stores
   double2 v[4][NE];
 #pragma unroll
@@ -405,7 +447,6 @@ __global__ void __launch_bounds__(kThreads) lg_row_cta(const double2* __restrict
       if (use && i < N2) dst[fsw(i)] = v[r][j];
     }
   }
-  (void)nrows;
   __syncthreads();
   fft_run_t<G::L2, false>(bA, tw2, threadIdx.x, blockDim.x, CtaSync());
   if (two) fft_run_t<G::L2, false>(bB, tw2, threadIdx.x, blockDim.x, CtaSync());

@@ -28,7 +28,7 @@ def nrel(a, b):
 
 
 @pytest.mark.parametrize("N,L,force", [(200, 77, True), (1000, 500, True), (4096, 1000, True), (32768, 16384, False),
-                                       (40000, 9000, False)])
+                                       (40000, 9000, False), (600000, 100, False)])
 def test_long_spectrum_and_matvec(P, N, L, force):
     rng = np.random.default_rng(N + L)
     K = N - L + 1
