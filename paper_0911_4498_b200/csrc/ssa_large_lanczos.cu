@@ -11,7 +11,7 @@
 //                basis rows of that chunk in groups of 8 with all loads in flight; per-CTA
 //                partials are then summed in a fixed order (deterministic);
 //   update       r -= B h with the rows in reverse order (recently read rows hit L2);
-//   finish       one warp (lg_finish): norms, the DGKS decision for a second pass, breakdown,
+//   finish       one CTA (lg_finish): norms, the DGKS decision for a second pass, breakdown,
 //                alpha_j / beta_{j+1} in device memory; second-pass kernels read the flag
 //                and return at once when it is not needed;
 //   normalize    v = r / alpha into the basis row.
@@ -232,7 +232,7 @@ __global__ void __launch_bounds__(kThreads) lg_update(const double* __restrict__
   }
 }
 
-// Norm bookkeeping at the end of a reorthogonalization pass, one warp (replaces the
+// Norm bookkeeping at the end of a reorthogonalization pass, one CTA (replaces the
 // separate |r| / DGKS / coefficient kernels):
 //   pass 0: nr = |r| before reorth from the correlation partials (cpart[ncol]); with a
 //           reorth pass (nb > 0) |r| from the update partials (part[nch]) and the DGKS
@@ -248,14 +248,22 @@ __global__ void lg_finish(const double* __restrict__ cpart, int ncol, const doub
     if (pass == 0 && threadIdx.x == 0) *coef_out = 0.0;
     return;
   }
+  // one CTA: thread-strided partial sums, shuffle trees, warps added in index order
+  __shared__ double r1[kWarps], r2[kWarps];
   double s1 = 0.0, s2 = 0.0;
   if (pass == 0)
-    for (int i = threadIdx.x; i < ncol; i += 32) s1 += cpart[i];
+    for (int i = threadIdx.x; i < ncol; i += blockDim.x) s1 += cpart[i];
   if (nb > 0)
-    for (int i = threadIdx.x; i < nch; i += 32) s2 += part[i];
+    for (int i = threadIdx.x; i < nch; i += blockDim.x) s2 += part[i];
   s1 = warp_sum(s1);
   s2 = warp_sum(s2);
+  const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if ((threadIdx.x & 31) == 0) { r1[w] = s1; r2[w] = s2; }
+  __syncthreads();
   if (threadIdx.x != 0) return;
+  s1 = 0.0;
+  s2 = 0.0;
+  for (int i = 0; i < nw; ++i) { s1 += r1[i]; s2 += r2[i]; }
   int again = 0;
   double nn;
   if (pass == 0) {
@@ -456,7 +464,7 @@ cudaError_t large_decompose_one(Plan& p, const DecomposeArgs& a0, int b, cudaStr
   double* cpart = part + (size_t)((std::max(ldL, ldK) + kRoChunk - 1) / kRoChunk) * (p.m_max + 2);
   launch_pdl(lg_start, dim3(nchL), dim3(kThreads), 0, s, r, L, ldL, a.seed, (uint64_t)(b + a.series_base), cpart);
   // beta_1 = |p0| into beta[1], then u_1 = p0 / beta_1
-  launch_pdl(lg_finish, dim3(1), dim3(32), 0, s, cpart, nchL, part, 0, 0, sc, 0, p.opt.reorth, beta + 1, 0);
+  launch_pdl(lg_finish, dim3(1), dim3(kThreads), 0, s, cpart, nchL, part, 0, 0, sc, 0, p.opt.reorth, beta + 1, 0);
   launch_pdl(lg_normalize, dim3((ldL + kThreads - 1) / kThreads), dim3(kThreads), 0, s, r, L, ldL, beta + 1, U);
   // reorth against nb basis rows (CGS + DGKS), then the coefficient into coef
   auto reorth = [&](const double* basis, int ld, int nb, double* coef, int step) {
@@ -467,7 +475,7 @@ cudaError_t large_decompose_one(Plan& p, const DecomposeArgs& a0, int b, cudaStr
         launch_pdl(lg_rows, dim3((nb * 32 + kThreads - 1) / kThreads), dim3(kThreads), 0, s, part, nb, nch, h, sc, pass);
         launch_pdl(lg_update, dim3(nch), dim3(kThreads), (size_t)nb * 8, s, basis, ld, nb, h, r, part, sc, pass);
       }
-      launch_pdl(lg_finish, dim3(1), dim3(32), 0, s, cpart, ncol, part, nch, nb, sc, pass, p.opt.reorth, coef, step);
+      launch_pdl(lg_finish, dim3(1), dim3(kThreads), 0, s, cpart, ncol, part, nch, nb, sc, pass, p.opt.reorth, coef, step);
       if (nb == 0) break;
     }
   };
