@@ -6,15 +6,17 @@
 // DESIGN.md R1), but each thread keeps 16 points in registers through three radix-16
 // decimation-in-frequency passes (4096 = 16^3), so per product there are five shared-
 // memory exchanges instead of ten radix-8 passes:
-//   pass 1 (block 4096, stride 256)  loads straight from global memory (thread t: points
-//                                    t + 256 q), half the inputs are the zero padding
+//   pass 1 (block 4096, stride 256)  from the x stage in shared memory (filled by cp.async
+//                                    during the previous item; thread t: points t + 256 q),
+//                                    half the inputs are the zero padding
 //   pass 2 (block 256, stride 16)    via shared memory
 //   pass 3 (block 16, stride 1)      via shared memory; thread t takes block swap(t) so it
 //                                    ends holding the frequencies r + 256 k, r = t
-//   pair step                        thread t <= 128 and its partner 256 - t hold the
-//                                    pairs (p, H - p) of the real-FFT split: the owner reads
-//                                    the partner's 16 values, forms both outputs, writes the
-//                                    partner's back (warps 0-3 work, 4-7 wait: warp-uniform)
+//   pair step                        thread t and its partner 256 - t hold the pairs
+//                                    (p, H - p) of the real-FFT split; each thread owns the
+//                                    pairs of its slots k < 8: reads the partner's value,
+//                                    keeps Z'_p, writes Z'_q into the partner's slot (every
+//                                    warp does the same work)
 //   inverse passes 3, 2, 1           in reverse; pass 3 starts from registers, pass 1
 //                                    writes the real outputs straight to global memory.
 // Shared-memory layout: swz(i) = i ^ ((i >> 8) & 7) (16-byte elements) makes every access
