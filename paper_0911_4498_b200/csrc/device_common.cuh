@@ -45,6 +45,32 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
+// Sum of 8 values over the warp with 9 shuffles: lane l ends with the total of value
+// (l >> 2) & 7 (fixed pairing order: deterministic).
+__device__ __forceinline__ double warp_sum8(double* v, int lane) {
+  const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const double send = b4 ? v[i] : v[i + 4];
+    const double keep = b4 ? v[i + 4] : v[i];
+    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+#pragma unroll
+  for (int i = 0; i < 2; ++i) {
+    const double send = b3 ? v[i] : v[i + 2];
+    const double keep = b3 ? v[i + 2] : v[i];
+    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+  {
+    const double send = b2 ? v[0] : v[1];
+    const double keep = b2 ? v[1] : v[0];
+    v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+  }
+  v[0] += __shfl_xor_sync(0xffffffffu, v[0], 2);
+  v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+  return v[0];
+}
+
 // Deterministic CTA sum: fixed shuffle tree, then warps summed in index order.
 __device__ __forceinline__ double block_sum(double v, double* red) {
   v = warp_sum(v);

@@ -119,16 +119,43 @@ __device__ double reorth_t(double* r, const double* basis, int nb, int ld, doubl
     __syncthreads();
     // pass 1: partial dots of this warp's slab with every basis row; the lines stay in L2
     // (evict_last) for pass 2
-    stream_rows(bw, ld, nb, false, slab, rg, pol_last, [&](int row, const double* ch) {
-      double s = 0.0;
+    if constexpr (EPL <= 4) {
+      // small slabs (N <~ 2K): the rows are a few hundred bytes and L2-resident, and the
+      // TMA ring is latency-bound on them; read groups of 8 rows with plain L2 loads (all
+      // in flight) and reduce their 8 partial dots together (warp_sum8: 9 shuffles)
+      for (int row0 = 0; row0 < nb; row0 += 8) {
+        double x[8][EPL];
 #pragma unroll
-      for (int t = 0; t < EPL; ++t) {
-        const int e = lane + 32 * t;
-        if (e < slab) s = fma(ch[e], rv[t], s);
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+          for (int t = 0; t < EPL; ++t) {
+            const int e = lane + 32 * t;
+            x[i][t] = (row0 + i < nb && e < slab) ? __ldcg(bw + (size_t)(row0 + i) * ld + e) : 0.0;
+          }
+        double d[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          double acc = 0.0;
+#pragma unroll
+          for (int t = 0; t < EPL; ++t) acc = fma(x[i][t], rv[t], acc);
+          d[i] = acc;
+        }
+        const double tot = warp_sum8(d, lane);
+        const int q = (lane >> 2) & 7;
+        if ((lane & 3) == 0 && row0 + q < nb) part[w * pstride + row0 + q] = tot;
       }
-      s = warp_sum(s);
-      if (lane == 0) part[w * pstride + row] = s;
-    });
+    } else {
+      stream_rows(bw, ld, nb, false, slab, rg, pol_last, [&](int row, const double* ch) {
+        double s = 0.0;
+#pragma unroll
+        for (int t = 0; t < EPL; ++t) {
+          const int e = lane + 32 * t;
+          if (e < slab) s = fma(ch[e], rv[t], s);
+        }
+        s = warp_sum(s);
+        if (lane == 0) part[w * pstride + row] = s;
+      });
+    }
     __syncthreads();
     for (int c = threadIdx.x; c < nb; c += blockDim.x) {
       double s = 0.0;
@@ -138,14 +165,34 @@ __device__ double reorth_t(double* r, const double* basis, int nb, int ld, doubl
     __syncthreads();
     // pass 2: r -= V h, rows streamed in reverse so the most recently read rows (still
     // in L2) come first; read for the last time in this half-step (evict_first)
-    stream_rows(bw, ld, nb, true, slab, rg, pol_first, [&](int row, const double* ch) {
-      const double hc = sm.h[row];
+    if constexpr (EPL <= 4) {
+      // rows in reverse, groups of 8 plain L2 loads in flight (as the dots pass)
+      for (int top = nb - 1; top >= 0; top -= 8) {
+        double x[8][EPL];
 #pragma unroll
-      for (int t = 0; t < EPL; ++t) {
-        const int e = lane + 32 * t;
-        if (e < slab) rv[t] = fma(-hc, ch[e], rv[t]);
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+          for (int t = 0; t < EPL; ++t) {
+            const int e = lane + 32 * t;
+            x[i][t] = (top - i >= 0 && e < slab) ? __ldcg(bw + (size_t)(top - i) * ld + e) : 0.0;
+          }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const double hc = (top - i >= 0) ? sm.h[top - i] : 0.0;
+#pragma unroll
+          for (int t = 0; t < EPL; ++t) rv[t] = fma(-hc, x[i][t], rv[t]);
+        }
       }
-    });
+    } else {
+      stream_rows(bw, ld, nb, true, slab, rg, pol_first, [&](int row, const double* ch) {
+        const double hc = sm.h[row];
+#pragma unroll
+        for (int t = 0; t < EPL; ++t) {
+          const int e = lane + 32 * t;
+          if (e < slab) rv[t] = fma(-hc, ch[e], rv[t]);
+        }
+      });
+    }
     double ss = 0.0;
 #pragma unroll
     for (int t = 0; t < EPL; ++t) ss = fma(rv[t], rv[t], ss);

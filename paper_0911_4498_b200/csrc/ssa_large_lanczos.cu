@@ -86,32 +86,6 @@ constexpr int kRoChunk = 512;
 constexpr int kRoE = kRoChunk / kThreads;  // 2
 constexpr int kRoG = 8;                    // rows per group (warp_sum8)
 
-// Sum of 8 values over the warp with 9 shuffles: lane l ends with the total of value
-// (l >> 2) & 7 (fixed pairing order: deterministic).
-__device__ __forceinline__ double warp_sum8(double* v, int lane) {
-  const bool b4 = lane & 16, b3 = lane & 8, b2 = lane & 4;
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const double send = b4 ? v[i] : v[i + 4];
-    const double keep = b4 ? v[i + 4] : v[i];
-    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-  }
-#pragma unroll
-  for (int i = 0; i < 2; ++i) {
-    const double send = b3 ? v[i] : v[i + 2];
-    const double keep = b3 ? v[i + 2] : v[i];
-    v[i] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-  }
-  {
-    const double send = b2 ? v[0] : v[1];
-    const double keep = b2 ? v[1] : v[0];
-    v[0] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
-  }
-  v[0] += __shfl_xor_sync(0xffffffffu, v[0], 2);
-  v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
-  return v[0];
-}
-
 // dots: part[row][cta] = <basis[row][chunk], r[chunk]>; smem red[nb][warps] (dynamic).
 // Rows are read with L2 evict_last so lg_update (rows in reverse) finds the last ones.
 __global__ void __launch_bounds__(kThreads) lg_dots(const double* __restrict__ basis, int ld, int nb,
