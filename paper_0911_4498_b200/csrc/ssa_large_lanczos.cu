@@ -308,16 +308,27 @@ __global__ void __launch_bounds__(kThreads) lg_ritz(const double* __restrict__ b
                                                     double* amax, int* aidx) {
   pdl_wait();
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  // the rows x k coefficients in shared memory, zero-padded to kMaxK per row: every
+  // thread then reads them as broadcast 16-byte loads (not k L1 loads per row)
+  extern __shared__ __align__(16) double cs[];  // [rows][kMaxK]
+  for (int e = threadIdx.x; e < rows * kMaxK; e += blockDim.x) {
+    const int r = e / kMaxK, i = e - r * kMaxK;
+    cs[e] = (i < k) ? __ldg(coef + (size_t)r * k + i) : 0.0;
+  }
+  __syncthreads();
   double acc[kMaxK];
 #pragma unroll
   for (int i = 0; i < kMaxK; ++i) acc[i] = 0.0;
   if (t < n) {
     for (int row = 0; row < rows; ++row) {
       const double x = __ldcs(basis + (size_t)row * ld + t);
-      const double* cr = coef + (size_t)row * k;
+      const double2* cr = reinterpret_cast<const double2*>(cs + (size_t)row * kMaxK);
 #pragma unroll
-      for (int i = 0; i < kMaxK; ++i)
-        if (i < k) acc[i] = fma(__ldg(cr + i), x, acc[i]);
+      for (int i = 0; i < kMaxK / 2; ++i) {
+        const double2 c = cr[i];
+        acc[2 * i] = fma(c.x, x, acc[2 * i]);
+        acc[2 * i + 1] = fma(c.y, x, acc[2 * i + 1]);
+      }
     }
 #pragma unroll
     for (int i = 0; i < kMaxK; ++i)
@@ -505,8 +516,10 @@ cudaError_t large_decompose_one(Plan& p, const DecomposeArgs& a0, int b, cudaStr
   const int gU = (L + kThreads - 1) / kThreads, gV = (K + kThreads - 1) / kThreads;
   double* amax = p.d_lgpart;
   int* aidx = reinterpret_cast<int*>(p.d_lgpart + (size_t)gU * k);
-  launch_pdl(lg_ritz, dim3(gU), dim3(kThreads), 0, s, U, ldL, m + 1, cP, k, L, Uo, amax, aidx);
-  launch_pdl(lg_ritz, dim3(gV), dim3(kThreads), 0, s, V, ldK, m, cQ, k, K, Vo, nullptr, nullptr);
+  const size_t rsm = (size_t)(m + 1) * kMaxK * 8;  // coefficient rows in shared memory
+  if ((e = raise_smem_limit(lg_ritz, rsm))) return e;
+  launch_pdl(lg_ritz, dim3(gU), dim3(kThreads), rsm, s, U, ldL, m + 1, cP, k, L, Uo, amax, aidx);
+  launch_pdl(lg_ritz, dim3(gV), dim3(kThreads), rsm, s, V, ldK, m, cQ, k, K, Vo, nullptr, nullptr);
   launch_pdl(lg_sign, dim3(1), dim3(32), 0, s, amax, aidx, gU, k, Uo, L, h);
   launch_pdl(lg_flip, dim3((int)(((size_t)L * k + kThreads - 1) / kThreads)), dim3(kThreads), 0, s, Uo, L, k, h);
   launch_pdl(lg_flip, dim3((int)(((size_t)K * k + kThreads - 1) / kThreads)), dim3(kThreads), 0, s, Vo, K, k, h);
