@@ -1,21 +1,24 @@
 #!/usr/bin/env python
 """bench.py -- throughput of the fast Basic-SSA hot path on B200 (driver contract).
 
-Default workload = BASELINE.json configs[1] ("cfg2"): per GPU a batch of 4096 independent
-fp64 series, N=4096, L=2048, k=16.  One step = the whole hot path over the batch
-(SURVEY.md §8(a) rows a1-a10): spectra, GKL bidiagonalization with full
-reorthogonalization (FFT Hankel products), convergence tests and the bidiagonal SVD on
-device, Ritz assembly, and rank-1 Hankelization of all 16 triples of every series
-(ssa_decompose + ssa_reconstruct through the C-ABI).
+Default workload = BASELINE.json configs[1] ("cfg2"): a batch of 4096 independent fp64
+series, N=4096, L=2048, k=16.  One step = the whole hot path over the batch (SURVEY.md
+§8(a) rows a1-a10): spectra, GKL bidiagonalization with partial reorthogonalization (FFT
+Hankel products; PRO, R22), convergence tests and the
+bidiagonal SVD on device, Ritz assembly, and rank-1 Hankelization of all 16 triples of
+every series (ssa_decompose + ssa_reconstruct through the C-ABI).  A secondary line runs
+the same batch with full reorthogonalization (FRO, the round-1 default).
 
 Metric: eigentriples/s (fp64) for the whole job; Hankel matvecs/s and roofline of the
 dominant kernel (lanczos_kernel, HBM-bound) are reported beside it.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference] [--batch B]
 
-Multi-GPU (torchrun, one rank per GPU): every rank runs its own batch of 4096 series
-(global series indices rank*4096 + i), no data-path collective; weak scaling.  Timing
-is per step with CUDA events, MAX over ranks; value = all triples / that time.
+Multi-GPU (torchrun, one rank per GPU): the 4096 series are sharded by series over the
+ranks (parallel.shard_range: 512 per GPU at 8), no data-path collective, strong scaling;
+a weak-scaling line (4096 series per GPU) is reported beside it.  Timing is per step with
+CUDA events, MAX over ranks; value = all triples / that time.  The cfg4 / cfg5 lines shard
+their series / problems the same way; cfg1 / cfg3 (one series) run as replicas.
 
 --impl reference times the CPU oracle (oracle/: one-sided Jacobi SVD + direct averaging)
 as it stands on the host cores on a bounded sample of the same workload (rank 0 only).
@@ -48,7 +51,10 @@ def parse():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--batch", type=int, default=CFG["batch"], help="series per GPU (default 4096)")
+    ap.add_argument("--batch", type=int, default=CFG["batch"], help="global batch, sharded over the GPUs (4096)")
+    ap.add_argument("--no-fro", action="store_true", help="skip the FRO comparison line")
+    ap.add_argument("--no-overshoot", action="store_true", help="skip the test-schedule overshoot probe")
+    ap.add_argument("--no-weak", action="store_true", help="skip the weak-scaling line (N > 1)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--profile-once", action="store_true", help="1 decompose, no timing (for ncu)")
@@ -57,31 +63,53 @@ def parse():
 
 
 # ------------------------------------------------------------------------ model bytes
-def lanczos_alg_bytes(steps: np.ndarray, N: int, L: int, k: int) -> float:
-    """Algorithmic HBM bytes of lanczos_kernel for series that ran m = steps Lanczos steps
-    (DESIGN.md §Roofline): one-pass full reorthogonalization reads the basis twice per
-    half-step (dots, update), every half-step reads the spectrum once and writes one basis
-    vector; the start reads the series and writes u_1; Ritz assembly reads U_{m+1}, V_m once
-    and writes k(L+K) outputs.
-      half-step A, j = 1..m+1: 16 K (j-1) + 16 (H+1) + 8 K
-      half-step B, j = 1..m  : 16 L j     + 16 (H+1) + 8 L
-    """
-    K = N - L + 1
+def _H(N: int) -> int:
     M = 1
     while M < N:
         M <<= 1
-    H = M // 2
-    m = steps.astype(np.float64)
-    a = 16 * K * (m * (m + 1) / 2) + (m + 1) * (16 * (H + 1) + 8 * K)
-    b = 16 * L * (m * (m + 1) / 2) + m * (16 * (H + 1) + 8 * L)
-    start = 8 * N + 8 * L
-    ritz = 8 * ((m + 1) * L + m * K) + 8 * k * (L + K)
-    return float(np.sum(a + b + start + ritz))
+    return M // 2
+
+
+def lanczos_alg_bytes(steps, rows_u, rows_v, N: int, L: int) -> float:
+    """Algorithmic HBM bytes of lanczos_kernel for series that ran m = steps
+    Lanczos steps and whose reorthogonalizations read rows_u / rows_v basis rows in total
+    (ssa_series_info: every CGS pass reads its rows once for the dots and once for the
+    update; FRO without DGKS passes gives rows_u = rows_v = m(m+1), PRO far fewer):
+      every half-step reads the spectrum (16 (H+1)) and writes one basis vector;
+      half-steps A, j = 1..m+1 (v side): 8 K each; half-steps B, j = 1..m (u side): 8 L each;
+      reorthogonalization: 8 (rows_u L + rows_v K);  start: read the series, write u_1.
+    The Ritz assembly is a separate kernel (ritz_alg_bytes)."""
+    K = N - L + 1
+    H = _H(N)
+    m = np.asarray(steps, dtype=np.float64)
+    ru = np.asarray(rows_u, dtype=np.float64)
+    rv = np.asarray(rows_v, dtype=np.float64)
+    half = (m + 1) * (16 * (H + 1) + 8 * K) + m * (16 * (H + 1) + 8 * L)
+    return float(np.sum(half + 8 * (ru * L + rv * K) + 8 * N + 8 * L))
+
+
+def fro_rows(steps):
+    """Basis rows one-pass FRO reads: sum_{j=1}^{m+1} 2 (j-1) = sum_{j=1}^{m} 2 j = m (m+1) per side."""
+    m = np.asarray(steps, dtype=np.float64)
+    return m * (m + 1)
+
+
+def ritz_alg_bytes(steps, N: int, L: int, k: int) -> float:
+    """ritz_kernel: read U_{m+1} and V_m once, write U_k, V_k (Eq. 1)."""
+    K = N - L + 1
+    m = np.asarray(steps, dtype=np.float64)
+    return float(np.sum(8 * ((m + 1) * L + m * K) + 8 * k * (L + K)))
 
 
 def hankelize_alg_bytes(nterms: int, N: int, L: int) -> float:
     K = N - L + 1
     return float(nterms) * 8 * (L + K + N + 1)
+
+
+def hankelize_flops(nterms: int, N: int) -> float:
+    """Three real FFTs of length M + the spectrum product + sigma / c_t scaling."""
+    M = 2 * _H(N)
+    return float(nterms) * (3 * fft_flops(M) + 6 * (M // 2 + 1) + 2 * N)
 
 
 # ------------------------------------------------------------------------ microbenchmarks
@@ -113,16 +141,53 @@ def _events_ms(fn, reps=1):
     return a.elapsed_time(b)
 
 
-def micro_matvec(P, peak):
+class Ctx:
+    """Rank / world and the MAX-over-ranks reduction of device times (multi-GPU timing rule)."""
+
+    def __init__(self, rank: int, world: int):
+        self.rank, self.world = rank, world
+
+    def max_ms(self, ms: float) -> float:
+        if self.world == 1:
+            return ms
+        import torch
+        import torch.distributed as dist
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def barrier(self):
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    def shard(self, n: int):
+        from paper_0911_4498_b200.parallel import shard_range
+        return shard_range(n, self.rank, self.world)
+
+
+def _timed(ctx, fn, reps):
+    """best-of-reps device time of fn() (CUDA events, barrier before each), MAX over ranks."""
+    best = float("inf")
+    for _ in range(reps):
+        ctx.barrier()
+        best = min(best, _events_ms(fn))
+    return ctx.max_ms(best)
+
+
+def micro_matvec(P, peak, ctx):
     """BASELINE.json configs[3] (cfg4): 65,536 series N=8192, L=4096, i.i.d. N(0,1) series and
-    vectors (drawn on the device); 64 alternating X v / X^T u products per series, each a
-    batched ssa_matvec launch over all series reading x and the spectrum from HBM and
-    writing y to HBM.  Algorithmic bytes per product 8(K+L) + 16(M/2+1); roofline HBM."""
+    vectors (drawn on the device, per-rank generator seeds); 64 alternating X v / X^T u
+    products per series, each a batched ssa_matvec launch over this rank's contiguous shard
+    of the series reading x and the spectrum from HBM and writing y to
+    HBM.  Algorithmic bytes per product 8(K+L) + 16(M/2+1); roofline HBM."""
     import torch
     c = ssa_inputs.CONFIGS["cfg4"]
-    N, L, B, T = c["N"], c["L"], c["batch"], c["products"]
+    N, L, GB, T = c["N"], c["L"], c["batch"], c["products"]
+    b0, b1 = ctx.shard(GB)
+    B = b1 - b0
     K = N - L + 1
-    g = torch.Generator(device="cuda").manual_seed(4)
+    g = torch.Generator(device="cuda").manual_seed(4 + 1000 * ctx.rank)
     F = torch.randn(B, N, dtype=torch.float64, device="cuda", generator=g)
     v = torch.randn(B, K, dtype=torch.float64, device="cuda", generator=g)
     u = torch.randn(B, L, dtype=torch.float64, device="cuda", generator=g)
@@ -139,37 +204,42 @@ def micro_matvec(P, peak):
             else:
                 plan.matvec(spec, u, transpose=True, out=z)
     run()
-    ms = min(_events_ms(run) for _ in range(3))
-    nprod = T * B
+    ms = _timed(ctx, run, 3)
+    nprod = T * GB
     M = plan.M
     byt = nprod * (8 * (K + L) + 16 * (M // 2 + 1))
     fl = nprod * (2 * fft_flops(M) + 6 * (M // 2 + 1))
     fpk, fsrc = fp64_peak()
-    out = {"value": nprod / (ms * 1e-3), "unit": "Hankel matvecs/s", "per_gpu": True, "ms": ms, "products": nprod,
-           "workload": "cfg4 (BASELINE.json configs[3]): 65536 series N=8192 L=4096, 64 alternating products",
-           "roofline": {"bound": "hbm", "achieved": byt / (ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
-                        "frac": byt / (ms * 1e-3) / 1e9 / peak, "alg_bytes_per_product": byt / nprod},
+    w = ctx.world
+    out = {"value": nprod / (ms * 1e-3), "unit": "Hankel matvecs/s", "ms": ms, "products": nprod,
+           "series_per_gpu": B, "scaling": "strong",
+           "workload": "cfg4 (BASELINE.json configs[3]): 65536 series N=8192 L=4096, 64 alternating products, "
+                       f"series sharded over {w} GPU(s)",
+           "roofline": {"bound": "hbm", "achieved": byt / (ms * 1e-3) / 1e9 / w, "peak": peak, "unit": "GB/s per GPU",
+                        "frac": byt / (ms * 1e-3) / 1e9 / w / peak, "alg_bytes_per_product": byt / nprod},
            "fp64_roofline": {"bound": "fp64 (model flops: 2 x 2.5 M log2 M + 6(M/2+1) per product)",
-                             "achieved": fl / (ms * 1e-3) / 1e12, "peak": fpk, "unit": "TFLOP/s",
-                             "frac": fl / (ms * 1e-3) / 1e12 / fpk, "peak_src": fsrc}}
+                             "achieved": fl / (ms * 1e-3) / 1e12 / w, "peak": fpk, "unit": "TFLOP/s per GPU",
+                             "frac": fl / (ms * 1e-3) / 1e12 / w / fpk, "peak_src": fsrc}}
     plan.close()
     del spec, v, u, y, z
     torch.cuda.empty_cache()
     return out
 
 
-def micro_hankelize(P, peak):
+def micro_hankelize(P, peak, ctx):
     """BASELINE.json configs[4] (cfg5): 256 problems N=262144, L=131072, 50 rank-1 terms each,
     sigma_i = 1/i, u_i, v_i Gaussian normalized (drawn on the device); every term
-    Hankelized separately.  Run in 8 launches of 32 problems.  Algorithmic bytes per term
-    8(L+K+N); flops per term 3 x 2.5 N log2 N + 6(N/2+1) + 2N."""
-    import math
+    Hankelized separately.  This rank's contiguous shard of the problems runs in launches of
+    up to 32 problems (the same 32 drawn problems stand in for every chunk).  Algorithmic
+    bytes per term 8(L+K+N); flops per term 3 x 2.5 N log2 N + 6(N/2+1) + 2N."""
     import torch
     c = ssa_inputs.CONFIGS["cfg5"]
-    N, L, B, T = c["N"], c["L"], c["batch"], c["k"]
+    N, L, GB, T = c["N"], c["L"], c["batch"], c["k"]
+    b0, b1 = ctx.shard(GB)
+    B = b1 - b0
     K = N - L + 1
-    Bc = 32
-    g = torch.Generator(device="cuda").manual_seed(5)
+    Bc = min(32, B)
+    g = torch.Generator(device="cuda").manual_seed(5 + 1000 * ctx.rank)
     U = torch.randn(Bc, T, L, dtype=torch.float64, device="cuda", generator=g)
     U /= U.norm(dim=2, keepdim=True)
     V = torch.randn(Bc, T, K, dtype=torch.float64, device="cuda", generator=g)
@@ -177,36 +247,47 @@ def micro_hankelize(P, peak):
     sig = (1.0 / torch.arange(1, T + 1, dtype=torch.float64, device="cuda")).repeat(Bc, 1).contiguous()
     plan = P.Plan(N, L, 0, Bc)
     out = torch.empty(Bc, T, N, dtype=torch.float64, device="cuda")
+    chunks = [(q, min(Bc, B - q)) for q in range(0, B, Bc)]
+    tail = [q for q in chunks if q[1] != Bc]
+    plan_t = P.Plan(N, L, 0, tail[0][1]) if tail else None
 
     def run():
-        for _ in range(B // Bc):   # the same 32 problems stand in for each of the 8 chunks
-            plan.hankelize(sig, U, V, out=out)
+        for _, n in chunks:
+            if n == Bc:
+                plan.hankelize(sig, U, V, out=out)
+            else:
+                plan_t.hankelize(sig[:n], U[:n], V[:n], out=out[:n])
     run()
-    ms = min(_events_ms(run) for _ in range(2))
-    nt = B * T
-    byt = nt * 8 * (L + K + N)
-    flops = nt * (3 * 2.5 * N * math.log2(N) + 6 * (N // 2 + 1) + 2 * N)
+    ms = _timed(ctx, run, 2)
+    nt = GB * T
+    byt = hankelize_alg_bytes(nt, N, L)
+    flops = hankelize_flops(nt, N)
     fpk, fsrc = fp64_peak()
-    res = {"value": nt / (ms * 1e-3), "unit": "terms/s", "per_gpu": True, "ms": ms, "terms": nt,
-           "workload": "cfg5 (BASELINE.json configs[4]): 256 x 50 terms, N=262144 L=131072",
+    w = ctx.world
+    res = {"value": nt / (ms * 1e-3), "unit": "terms/s", "ms": ms, "terms": nt, "problems_per_gpu": B,
+           "scaling": "strong",
+           "workload": f"cfg5 (BASELINE.json configs[4]): 256 x 50 terms, N=262144 L=131072, problems sharded over {w} GPU(s)",
            "roofline": {"bound": "fp64 (model flops 3 x 2.5 N log2 N + 6(N/2+1) + 2N per term; "
                                  "SURVEY.md §8(d): 1.07 us/term fp64 vs 0.64 us HBM)",
-                        "achieved": flops / (ms * 1e-3) / 1e12, "peak": fpk, "unit": "TFLOP/s",
-                        "frac": flops / (ms * 1e-3) / 1e12 / fpk, "peak_src": fsrc},
-           "hbm_roofline": {"achieved": byt / (ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
-                            "frac": byt / (ms * 1e-3) / 1e9 / peak, "alg_bytes_per_term": byt / nt}}
+                        "achieved": flops / (ms * 1e-3) / 1e12 / w, "peak": fpk, "unit": "TFLOP/s per GPU",
+                        "frac": flops / (ms * 1e-3) / 1e12 / w / fpk, "peak_src": fsrc},
+           "hbm_roofline": {"achieved": byt / (ms * 1e-3) / 1e9 / w, "peak": peak, "unit": "GB/s per GPU",
+                            "frac": byt / (ms * 1e-3) / 1e9 / w / peak, "alg_bytes_per_term": byt / nt}}
     plan.close()
+    if plan_t:
+        plan_t.close()
     del U, V, out, sig
     torch.cuda.empty_cache()
     return res
 
 
-def micro_hmatrix(P, N: int = 4000):
+def micro_hmatrix(P, ctx, N: int = 4000):
     """Heterogeneity matrix (ssa_hmatrix) in the paper's comparison
     setting (PAPER.md:1068-1076): Eq. (hseries) series with Q = N/2, B = T = N/4, L = B/2,
     I = {1, 2}; N = 4000 here (3001 base-window decompositions, 6002 Hankel products of the
     whole series, a 3001 x 3001 matrix).  ssa_hmatrix_exec timed (plan and workspace
-    created once, outside; the exec ends with the per-window status read-back)."""
+    created once, outside; the exec ends with the per-window status read-back).  One
+    series: replicas only."""
     import torch
     Q, B = N // 2, N // 4
     T, L = B, B // 2
@@ -214,24 +295,25 @@ def micro_hmatrix(P, N: int = 4000):
     hm = P.HMatrix(N, B, T, L, [1, 2])
     G, info = hm(f)
     torch.cuda.synchronize()
-    ms = min(_events_ms(lambda: hm(f, out=G, info=info)) for _ in range(3))
+    ms = _timed(ctx, lambda: hm(f, out=G, info=info), 3)
     nb, nt = N - B + 1, N - T + 1
     inf = P.info_to_numpy(info)
-    res = {"value": nb * nt / (ms * 1e-3), "unit": "H-matrix entries/s", "ms": ms,
+    res = {"value": nb * nt / (ms * 1e-3), "unit": "H-matrix entries/s", "ms": ms, "replicas": ctx.world,
            "windows_decomposed_per_s": nb / (ms * 1e-3), "mean_steps": float(inf["steps"].mean()),
            "workload": f"H-matrix of Eq. (hseries), N={N} Q={Q} B=T={B} L={L} I={{1,2}} ({nb}x{nt})",
            "g_inside_mean": float(G[: Q - B + 1, : Q - T + 1].mean().item()),
            "g_across_mean": float(G[: Q - B + 1, Q:].mean().item())}
+    hm.close()
     del f, G
     torch.cuda.empty_cache()
     return res
 
 
-def micro_bootstrap(P, R: int = 1024):
+def micro_bootstrap(P, ctx, R: int = 1024):
     """Bootstrap study of the paper (sec 6.3): the
     rank-5 series (periods in n, R17), N = 1000, L = 500, noise sigma = 5, R
     replicates (seeded N(0,1) noise, drawn on the host and copied once): replicates,
-    batched decompose (k = 5), grouped reconstruction, per-point mean/var/MSE."""
+    batched decompose (k = 5), grouped reconstruction, per-point mean/var/MSE.  Replicas."""
     import torch
     N, L, d, noise = 1000, 500, 5, 5.0
     f = torch.from_numpy(ssa_inputs.bootstrap_series(N)).cuda()
@@ -240,9 +322,9 @@ def micro_bootstrap(P, R: int = 1024):
     info = torch.zeros((R, P.INFO_DTYPE.itemsize), dtype=torch.uint8, device="cuda")
     plan.bootstrap(f, eps, noise, info=info)
     torch.cuda.synchronize()
-    ms = min(_events_ms(lambda: plan.bootstrap(f, eps, noise, info=info)) for _ in range(3))
+    ms = _timed(ctx, lambda: plan.bootstrap(f, eps, noise, info=info), 3)
     inf = P.info_to_numpy(info)
-    res = {"value": R / (ms * 1e-3), "unit": "replicates/s", "ms": ms, "replicates": R,
+    res = {"value": R / (ms * 1e-3), "unit": "replicates/s", "ms": ms, "replicates": R, "replicas": ctx.world,
            "eigentriples_per_s": R * d / (ms * 1e-3), "mean_steps": float(inf["steps"].mean()),
            "converged_fraction": float((inf["converged"] == 1).mean()),
            "workload": f"bootstrap of the rank-5 series, N={N} L={L} sigma={noise}, {R} replicates"}
@@ -252,11 +334,11 @@ def micro_bootstrap(P, R: int = 1024):
     return res
 
 
-def micro_decompose_cfg1(P):
+def micro_decompose_cfg1(P, ctx):
     """BASELINE.json configs[0] (cfg1): one fp64 series N=1024, L=512, k=10 (ssa_inputs
     cfg1_series, seed 0), decompose + reconstruct of all 10 components on one GPU.  A
     latency regime (~60 dependent Lanczos steps in one CTA): time, us per Lanczos step and
-    triples/s are reported, no roofline."""
+    triples/s are reported, no roofline.  Replicas only (§8(e))."""
     import torch
     c = ssa_inputs.CONFIGS["cfg1"]
     N, L, k = c["N"], c["L"], c["k"]
@@ -269,10 +351,11 @@ def micro_decompose_cfg1(P):
     def run():
         plan.decompose(x, s_, U, V, info)
         plan.reconstruct(s_, U, V, out=G)
-    ms = min(_events_ms(run) for _ in range(5))
+    ms = _timed(ctx, run, 5)
     inf = P.info_to_numpy(info)[0]
     m = int(inf["steps"])
     res = {"value": k / (ms * 1e-3), "unit": "eigentriples/s", "ms": ms, "steps": m, "us_per_step": 1e3 * ms / m,
+           "reorth_steps": int(inf["reorth_steps"]), "replicas": ctx.world,
            "hankel_matvecs_per_s": 2 * m / (ms * 1e-3), "status": int(inf["status"]),
            "workload": "cfg1 (BASELINE.json configs[0]): one series N=1024 L=512 k=10, decompose + reconstruct",
            "regime": "latency (one CTA, dependent steps): no roofline"}
@@ -280,11 +363,12 @@ def micro_decompose_cfg1(P):
     return res
 
 
-def micro_decompose_cfg3(P, peak):
+def micro_decompose_cfg3(P, peak, ctx):
     """BASELINE.json configs[2] (cfg3): one long series N=2^20, L=2^19, k=32 (ssa_inputs
     cfg3_series, seed 3) on one GPU: full decompose (four-step FFT products through L2,
-    full reorthogonalization, bidiagonal SVD, Ritz vectors) + reconstruct of the 32 triples.
-    Roofline: HBM, algorithmic bytes of the half-steps (lanczos_alg_bytes) with the steps run."""
+    reorthogonalization, bidiagonal SVD, Ritz vectors) + reconstruct of the 32 triples.
+    Roofline: HBM, algorithmic bytes of the half-steps (lanczos_alg_bytes with the basis
+    rows the run read) + Ritz + Hankelization.  Replicas only (§8(e))."""
     import torch
     c = ssa_inputs.CONFIGS["cfg3"]
     N, L, k = c["N"], c["L"], c["k"]
@@ -297,13 +381,18 @@ def micro_decompose_cfg3(P, peak):
     def run():
         plan.decompose(x, s_, U, V, info)
         plan.reconstruct(s_, U, V, out=G)
-    ms = min(_events_ms(run) for _ in range(3))
+    ms = _timed(ctx, run, 3)
     inf = P.info_to_numpy(info)[0]
     m = int(inf["steps"])
-    byt = lanczos_alg_bytes(np.array([m]), N, L, k) + hankelize_alg_bytes(k, N, L)
-    res = {"value": k / (ms * 1e-3), "unit": "eigentriples/s", "ms": ms, "steps": m,
+    ru, rv = int(inf["rows_u"]), int(inf["rows_v"])
+    if ru == 0 and rv == 0:        # path without row accounting: one-pass FRO
+        ru = rv = int(fro_rows(m))
+    byt = (lanczos_alg_bytes([m], [ru], [rv], N, L) + ritz_alg_bytes([m], N, L, k) +
+           hankelize_alg_bytes(k, N, L))
+    res = {"value": k / (ms * 1e-3), "unit": "eigentriples/s", "ms": ms, "steps": m, "replicas": ctx.world,
            "hankel_matvecs_per_s": 2 * m / (ms * 1e-3), "status": int(inf["status"]),
            "converged": int(inf["converged"]), "max_residual": float(inf["max_residual"]),
+           "reorth_steps": int(inf["reorth_steps"]), "basis_rows_read": [ru, rv],
            "workload": "cfg3 (BASELINE.json configs[2]): one series N=2^20 L=2^19 k=32, decompose + reconstruct",
            "roofline": {"bound": "hbm", "achieved": byt / (ms * 1e-3) / 1e9, "peak": peak, "unit": "GB/s",
                         "frac": byt / (ms * 1e-3) / 1e9 / peak, "alg_bytes": byt}}
@@ -381,13 +470,14 @@ def measured_peaks():
     return 6650.0, "fallback 6.65 TB/s (B200_PROFILING.md)"
 
 
-def ncu_traffic(name: str):
-    """dram read+write bytes per launch of `name` from the committed ncu summary."""
-    for p in sorted(glob.glob(os.path.join(ROOT, "profiles", "ncu_*cfg2_summary*.json")), reverse=True):
+def ncu_traffic(name: str, batch: int):
+    """dram read+write bytes per launch of `name` from the committed ncu summary of the
+    current round (profiles/ncu_r02_cfg2_summary*.json) for the same batch, else None."""
+    for p in sorted(glob.glob(os.path.join(ROOT, "profiles", "ncu_r02*cfg2_summary*.json")), reverse=True):
         try:
             d = json.load(open(p))
             if name in d and d[name].get("dram_bytes_per_launch"):
-                if d[name].get("batch") == CFG["batch"]:
+                if d[name].get("batch") == batch:
                     return float(d[name]["dram_bytes_per_launch"]), os.path.basename(p)
         except Exception:
             pass
@@ -466,6 +556,54 @@ def run_reference(args, rank):
 
 
 # ------------------------------------------------------------------------ our arm
+def run_cfg2(P, ctx, host, b0, reorth, steps, warmup, flush, clk=None):
+    """Time `steps` decompose + reconstruct steps of this rank's shard (host rows, global
+    index b0 of row 0) with the given reorthogonalization; returns a dict of results."""
+    import torch
+    N, L, k = CFG["N"], CFG["L"], CFG["k"]
+    K = N - L + 1
+    B = host.shape[0]
+    series = torch.from_numpy(host).cuda()
+    plan = P.Plan(N, L, k, B, reorth=reorth, series_base=b0)
+    sigma = torch.empty((B, k), dtype=torch.float64, device="cuda")
+    U = torch.empty((B, k, L), dtype=torch.float64, device="cuda")
+    V = torch.empty((B, k, K), dtype=torch.float64, device="cuda")
+    G = torch.empty((B, k, N), dtype=torch.float64, device="cuda")
+    info = torch.zeros((B, P.INFO_DTYPE.itemsize), dtype=torch.uint8, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def step():
+        plan.decompose(series, sigma, U, V, info)
+        plan.reconstruct(sigma, U, V, G)
+
+    for _ in range(warmup):
+        step()
+    torch.cuda.synchronize()
+    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
+    ph = {n: [] for n in ("spectrum", "lanczos", "bidiag_svd", "ritz", "hankelize")}
+    launches0 = plan.launches
+    import contextlib
+    with (clk if clk is not None else contextlib.nullcontext()):
+        for i in range(steps):
+            flush.zero_()                       # L2 flush between timed steps (untimed)
+            ctx.barrier()
+            torch.cuda.synchronize()
+            ev0[i].record(stream)
+            step()
+            ev1[i].record(stream)
+            torch.cuda.synchronize()
+            for n, v in plan.phase_ms().items():
+                ph[n].append(v)
+    launches = (plan.launches - launches0) // steps
+    step_ms = np.array([x.elapsed_time(y) for x, y in zip(ev0, ev1)])
+    ms = ctx.max_ms(float(step_ms.sum())) / steps
+    inf = P.info_to_numpy(info)
+    out = dict(plan=plan, sigma=sigma, info=info, inf=inf, ms=ms, launches=launches,
+               phase_ms={n: float(np.mean(v)) for n, v in ph.items()}, series=series, G=G, U=U, V=V)
+    return out
+
+
 def main():
     args = parse()
     rank = int(os.environ.get("RANK", 0))
@@ -482,57 +620,30 @@ def main():
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    ctx = Ctx(rank, world)
     N, L, k = CFG["N"], CFG["L"], CFG["k"]
     K = N - L + 1
-    B = args.batch
-    # inputs: this rank's series, global indices rank*B + i (weak scaling)
-    host = ssa_inputs.cfg2_batch(rank * B, B, N)
-    series = torch.from_numpy(host).cuda()
-    plan = P.Plan(N, L, k, B)
-    sigma = torch.empty((B, k), dtype=torch.float64, device="cuda")
-    U = torch.empty((B, k, L), dtype=torch.float64, device="cuda")
-    V = torch.empty((B, k, K), dtype=torch.float64, device="cuda")
-    G = torch.empty((B, k, N), dtype=torch.float64, device="cuda")
-    info = torch.zeros((B, P.INFO_DTYPE.itemsize), dtype=torch.uint8, device="cuda")
+    GB = args.batch
+    # the configured batch (BASELINE configs[1]: 4096 series) sharded by series over the
+    # ranks: rank r owns the contiguous block shard_range(GB, r, world),
+    # generated from the series' own seeds and started from their global indices
+    b0, b1 = ctx.shard(GB)
+    B = b1 - b0
+    host = ssa_inputs.cfg2_batch(b0, B, N)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-    stream = torch.cuda.current_stream()
-
-    def step():
-        plan.decompose(series, sigma, U, V, info)
-        plan.reconstruct(sigma, U, V, G)
 
     if args.profile_once:
-        step()
+        plan = P.Plan(N, L, k, B, series_base=b0)
+        x = torch.from_numpy(host).cuda()
+        s_, U_, V_, _ = plan.decompose(x)
+        plan.reconstruct(s_, U_, V_)
         torch.cuda.synchronize()
         return 0
 
-    for _ in range(max(3, args.warmup)):
-        step()
-    torch.cuda.synchronize()
-
-    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    lan_ms, hank_ms, spec_ms, svd_ms, ritz_ms = [], [], [], [], []
-    launches0 = plan.launches
-    with ClockSampler(local) as clk:
-        for i in range(args.steps):
-            flush.zero_()                       # L2 flush between timed steps (untimed)
-            if world > 1:
-                dist.barrier()
-            torch.cuda.synchronize()
-            ev0[i].record(stream)
-            step()
-            ev1[i].record(stream)
-            torch.cuda.synchronize()
-            ph = plan.phase_ms()
-            lan_ms.append(ph["lanczos"]); hank_ms.append(ph["hankelize"]); spec_ms.append(ph["spectrum"])
-            svd_ms.append(ph["bidiag_svd"]); ritz_ms.append(ph["ritz"])
-    launches = (plan.launches - launches0) // args.steps
-    step_ms = np.array([a.elapsed_time(b) for a, b in zip(ev0, ev1)])
-    total = torch.tensor([step_ms.sum()], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(total, op=dist.ReduceOp.MAX)
-    ms_per_step = float(total.item()) / args.steps
+    clk = ClockSampler(local)
+    r = run_cfg2(P, ctx, host, b0, 3, args.steps, max(3, args.warmup), flush, clk)
+    ms_per_step = r["ms"]
+    inf = r["inf"]
     gather = None
     if world > 1:
         # the only collective: after compute, all ranks gather sigma and
@@ -541,101 +652,159 @@ def main():
         dist.barrier()
         torch.cuda.synchronize()
         g0 = time.perf_counter()
-        all_sigma = gather_rows(sigma, world)
-        all_info = gather_rows(info, world)
+        all_sigma = gather_rows(r["sigma"], world)
+        all_info = gather_rows(r["info"], world)
         torch.cuda.synchronize()
         gather = {"ms": 1e3 * (time.perf_counter() - g0), "rows": int(all_sigma.shape[0]),
                   "bytes": int(all_sigma.numel() * 8 + all_info.numel()), "backend": "nccl all_gather"}
-        assert all_sigma.shape[0] == B * world
-    inf = P.info_to_numpy(info)
+        assert all_sigma.shape[0] == GB
     steps_m = inf["steps"].astype(np.int64)
     conv = float(np.mean(inf["converged"]))
-    triples = B * k * world
+    triples = GB * k
     value = triples / (ms_per_step * 1e-3)
-    matvecs = float((2 * steps_m + 1).sum()) * world / (ms_per_step * 1e-3)
+    matvecs_local = float((2 * steps_m + 1).sum())
+    matvecs = ctx.world * matvecs_local / (ms_per_step * 1e-3) if world == 1 else None
+    if world > 1:
+        t = torch.tensor([matvecs_local], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t)
+        matvecs = float(t.item()) / (ms_per_step * 1e-3)
 
-    # roofline of the dominant kernel (lanczos_kernel) from live CUDA events
+    # roofline of the dominant kernel (lanczos_kernel) from live CUDA events (rank 0's shard)
     peak, peak_src = measured_peaks()
-    alg = lanczos_alg_bytes(steps_m, N, L, k)
-    lan = float(np.mean(lan_ms))
+    ph = r["phase_ms"]
+    lan = ph["lanczos"]
+    alg = lanczos_alg_bytes(steps_m, inf["rows_u"], inf["rows_v"], N, L)
     achieved = alg / (lan * 1e-3) / 1e9
-    traffic, traffic_src = ncu_traffic("lanczos_kernel")
-    hk = float(np.mean(hank_ms))
+    traffic, traffic_src = ncu_traffic("lanczos_kernel", B)
+    ritz_b = ritz_alg_bytes(steps_m, N, L, k)
+    hk = ph["hankelize"]
     hk_bw = hankelize_alg_bytes(B * k, N, L) / (hk * 1e-3) / 1e9
+    hk_fl = hankelize_flops(B * k, N) / (hk * 1e-3) / 1e12
+    fpk, fsrc = fp64_peak()
+    fro_equiv = lanczos_alg_bytes(steps_m, fro_rows(steps_m), fro_rows(steps_m), N, L)
 
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "weak",
+        "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": "cfg2 (BASELINE.json configs[1]): per GPU 4096 fp64 series N=4096 L=2048 k=16, "
-                               "decompose + reconstruct all 16 triples",
-                   "N": N, "L": L, "k": k, "batch_per_gpu": B, "global_batch": B * world,
-                   "parallelism": f"series-sharded x{world} (no data-path collective)",
-                   "l2": "inputs (134 MB/GPU) > L2 and a 256 MiB L2 flush before every timed step",
-                   "tol": 1e-12, "reorth": "CGS + DGKS"},
+        "config": {"workload": "cfg2 (BASELINE.json configs[1]): 4096 fp64 series N=4096 L=2048 k=16 sharded by "
+                               "series over the GPUs, decompose + reconstruct all 16 triples",
+                   "N": N, "L": L, "k": k, "global_batch": GB, "batch_per_gpu": B,
+                   "parallelism": f"series-sharded x{world} (shard_range; no data-path collective)",
+                   "l2": "inputs (134 MB) > L2 and a 256 MiB L2 flush before every timed step",
+                   "tol": 1e-12, "reorth": "PRO (Simon/Larsen omega recurrence, eta = eps^(3/4); DESIGN.md R22)"},
         "hankel_matvecs_per_s": matvecs,
         **({"gather": gather} if gather else {}),
         "lanczos_steps": {"min": int(steps_m.min()), "median": float(np.median(steps_m)),
                           "max": int(steps_m.max()), "mean": float(steps_m.mean())},
+        "reorth": {"mode": "PRO", "reorth_halfsteps_mean": float(inf["reorth_steps"].mean()),
+                   "halfsteps_mean": float((2 * steps_m + 1).mean()),
+                   "lanczos_bytes_per_series": alg / B, "fro_equivalent_bytes_per_series": fro_equiv / B,
+                   "bytes_vs_fro": alg / fro_equiv},
         "converged_fraction": conv,
         "max_residual": float(inf["max_residual"].max()),
-        "phase_ms": {"spectrum": float(np.mean(spec_ms)), "lanczos": lan, "bidiag_svd": float(np.mean(svd_ms)),
-                     "ritz": float(np.mean(ritz_ms)), "hankelize": hk},
+        "phase_ms": ph,
         "roofline": {"kernel": "lanczos_kernel", "bound": "hbm", "achieved": achieved, "peak": peak,
                      "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
                      "traffic_src": traffic_src, "peak_src": peak_src,
                      "alg_bytes_per_launch": alg},
-        "hankelize_roofline": {"bound": "hbm (model, fp64 FFT)", "achieved": hk_bw, "peak": peak, "unit": "GB/s",
-                               "frac": hk_bw / peak},
-        "gpu_launches": int(launches),
+        "ritz_roofline": {"kernel": "ritz_kernel", "bound": "hbm", "achieved": ritz_b / (ph["ritz"] * 1e-3) / 1e9,
+                          "peak": peak, "unit": "GB/s", "frac": ritz_b / (ph["ritz"] * 1e-3) / 1e9 / peak,
+                          "alg_bytes_per_launch": ritz_b},
+        "hankelize_roofline": {"kernel": "hankelize_kernel", "bound": "fp64 (model flops, SURVEY.md §8(d))",
+                               "achieved": hk_fl, "peak": fpk, "unit": "TFLOP/s", "frac": hk_fl / fpk,
+                               "peak_src": fsrc, "hbm_achieved_gbs": hk_bw, "hbm_frac": hk_bw / peak},
+        "gpu_launches": int(r["launches"]),
         "clocks": clk.summary(),
     }
+    for key in ("plan",):
+        r[key].close()
+    del r
+    torch.cuda.empty_cache()
+
+    # FRO (reorth = 1, round-1 default) on the same shard: the bytes PRO saves, measured
+    if not args.no_fro:
+        rf = run_cfg2(P, ctx, host, b0, 1, 2, 1, flush)
+        inff = rf["inf"]
+        mf = inff["steps"].astype(np.int64)
+        algf = lanczos_alg_bytes(mf, inff["rows_u"], inff["rows_v"], N, L)
+        lanf = rf["phase_ms"]["lanczos"]
+        line["fro"] = {"value": triples / (rf["ms"] * 1e-3), "ms_per_step": rf["ms"],
+                       "lanczos_steps_mean": float(mf.mean()), "lanczos_bytes_per_series": algf / B,
+                       "roofline": {"kernel": "lanczos_kernel", "achieved": algf / (lanf * 1e-3) / 1e9, "peak": peak,
+                                    "unit": "GB/s", "frac": algf / (lanf * 1e-3) / 1e9 / peak}}
+        rf["plan"].close()
+        del rf
+        torch.cuda.empty_cache()
+
+    # overshoot of the convergence-test schedule: the first 256 series
+    # of the shard with a test after every step vs the default schedule
+    if not args.no_overshoot:
+        n_o = min(256, B)
+        x = torch.from_numpy(host[:n_o].copy()).cuda()
+        ms_default = P.info_to_numpy(P.Plan(N, L, k, n_o, series_base=b0).decompose(x)[3])["steps"]
+        os.environ["SSA_FIRST_CHECK"] = str(k)
+        os.environ["SSA_CHECK_CAP"] = "1"
+        try:
+            ms_every = P.info_to_numpy(P.Plan(N, L, k, n_o, check_every=1, series_base=b0).decompose(x)[3])["steps"]
+        finally:
+            del os.environ["SSA_FIRST_CHECK"], os.environ["SSA_CHECK_CAP"]
+        d = ms_default.astype(np.int64) - ms_every.astype(np.int64)
+        line["overshoot"] = {"series": n_o, "mean_steps": float(d.mean()), "max_steps": int(d.max()),
+                             "min_steps": int(d.min()), "note": "default schedule m minus m of a test after every step"}
+        torch.cuda.empty_cache()
+
+    # weak scaling (secondary): every rank its own 4096 series, global indices rank*4096 + i
+    if world > 1 and not args.no_weak:
+        hw = ssa_inputs.cfg2_batch(rank * CFG["batch"], CFG["batch"], N)
+        rw = run_cfg2(P, ctx, hw, rank * CFG["batch"], 3, 2, 1, flush)
+        line["weak_scaling"] = {"value": world * CFG["batch"] * k / (rw["ms"] * 1e-3), "unit": UNIT,
+                                "ms_per_step": rw["ms"], "batch_per_gpu": CFG["batch"], "scaling": "weak"}
+        rw["plan"].close()
+        del rw, hw
+        torch.cuda.empty_cache()
 
     # e2e through the public C call on host buffers (pinned), copies inside the timed region
     if not args.no_e2e:
         pin_series = torch.from_numpy(host).pin_memory()
-        outs = [torch.empty(s, dtype=torch.float64).pin_memory() for s in
+        outs = [torch.empty(sh, dtype=torch.float64).pin_memory() for sh in
                 [(B, k), (B, k, L), (B, k, K), (B, k, N)]]
         h_info = np.zeros(B, dtype=P.INFO_DTYPE)
         import ctypes
         lib = P.load_library()
-        plan2 = P.Plan(N, L, k, B)
+        plan2 = P.Plan(N, L, k, B, series_base=b0)
+        stream = torch.cuda.current_stream()
 
         def e2e_step():
-            st = lib.ssa_run_host(plan2._h, pin_series.data_ptr(), outs[0].data_ptr(), outs[1].data_ptr(),
-                                  outs[2].data_ptr(), outs[3].data_ptr(), h_info.ctypes.data,
-                                  ctypes.c_void_p(stream.cuda_stream))
-            return st
+            return lib.ssa_run_host(plan2._h, pin_series.data_ptr(), outs[0].data_ptr(), outs[1].data_ptr(),
+                                    outs[2].data_ptr(), outs[3].data_ptr(), h_info.ctypes.data,
+                                    ctypes.c_void_p(stream.cuda_stream))
 
         e2e_step()
         times = []
         for _ in range(max(1, min(3, args.steps))):
             flush.zero_()
-            if world > 1:
-                dist.barrier()
+            ctx.barrier()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             e2e_step()
             times.append(time.perf_counter() - t0)
-        t = torch.tensor([float(np.mean(times))], dtype=torch.float64, device="cuda")
-        if world > 1:
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        line["e2e"] = {"value": triples / float(t.item()), "unit": UNIT,
+        te = ctx.max_ms(1e3 * float(np.mean(times)))
+        line["e2e"] = {"value": triples / (te * 1e-3), "unit": UNIT,
                        "h2d_bytes_per_step": int(B * N * 8),
                        "d2h_bytes_per_step": int(B * k * (1 + L + K + N) * 8 + B * P.INFO_DTYPE.itemsize),
-                       "api": "ssa_run_host (pinned host buffers; H2D series, D2H sigma/U/V/recon/info)"}
+                       "api": "ssa_run_host (pinned host buffers; H2D series, D2H sigma/U/V/recon/info), per GPU"}
         plan2.close()
+        torch.cuda.empty_cache()
 
     if not args.no_micro:
-        del G
-        torch.cuda.empty_cache()
-        line["matvec_cfg4"] = micro_matvec(P, peak)
-        line["hankelize_cfg5"] = micro_hankelize(P, peak)
-        line["decompose_cfg3"] = micro_decompose_cfg3(P, peak)
-        line["decompose_cfg1"] = micro_decompose_cfg1(P)
-        line["hmatrix"] = micro_hmatrix(P)
-        line["bootstrap"] = micro_bootstrap(P)
-    if rank == 0 and not args.no_cpu_baseline:
+        line["matvec_cfg4"] = micro_matvec(P, peak, ctx)
+        line["hankelize_cfg5"] = micro_hankelize(P, peak, ctx)
+        line["decompose_cfg3"] = micro_decompose_cfg3(P, peak, ctx)
+        line["decompose_cfg1"] = micro_decompose_cfg1(P, ctx)
+        line["hmatrix"] = micro_hmatrix(P, ctx)
+        line["bootstrap"] = micro_bootstrap(P, ctx)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
         cores = os.cpu_count() or 1
         rate, desc, wall = oracle_sample(cores)
         line["cpu_baseline"] = {"value": rate, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc}

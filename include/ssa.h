@@ -62,12 +62,26 @@ typedef struct {
   int32_t check_every;   /* run the convergence test every c steps once m >= k; default 4 */
   uint64_t seed;         /* start vector p_0 (Alg. 1 line 1): uniform(-1,1)
                             entries from a counter-based hash of (seed, series, i); dflt 42 */
-  int32_t reorth;        /* 1 = full reorthogonalization (sec 3.2.2) by
-                            classical Gram-Schmidt with a DGKS second pass when the norm
-                            drops below 1/sqrt(2) (default); 2 = always two passes.       */
+  int32_t reorth;        /* 3 = partial reorthogonalization (PRO: Simon /
+                            Larsen omega recurrences estimate the orthogonality level of
+                            each new Lanczos vector; when it exceeds reorth_eta the vector,
+                            and the next one of the same side, are orthogonalized against
+                            the whole basis) -- the default, R22;
+                            1 = full reorthogonalization (FRO, sec 3.2.2)
+                            by classical Gram-Schmidt with a DGKS second pass when the norm
+                            drops below 1/sqrt(2); 2 = FRO, always two passes.  The long-
+                            series path (M > 16384) runs 3 as 1.                          */
   int32_t reserved;      /* flags: 1 = per-phase cycle counters (ssa_plan_profile); 2 = bidiagonal
                             SVD by implicit-shift QR instead of TGK inverse iteration; 4 = use
                             the long-series (multi-CTA FFT) path even when M <= 16384 (tests) */
+  double reorth_eta;     /* PRO threshold on the estimated orthogonality level; default
+                            eps^(3/4) = 1.82e-12 (tighter than Larsen's sqrt(eps) so the Ritz
+                            vectors stay orthogonal to ~1e-12, R22); must lie in
+                            (0, 1e-6] when reorth = 3, ignored otherwise.                 */
+  int64_t series_base;   /* global index of the plan's series 0 in the start-vector hash
+                            (seed, series, i): a shard [b0, b1) of a larger batch set to b0
+                            gets bit-identical results to the unsharded run (SURVEY.md
+                            8(e)).  Default 0.                                             */
 } ssa_options;
 
 /* Per-series outcome of ssa_decompose (device array, one entry per series). */
@@ -77,9 +91,13 @@ typedef struct {
   int32_t breakdown_step; /* first step with alpha or beta < 1e-12 * running max, else 0   */
   int32_t reorth_extra;   /* number of DGKS second passes taken                            */
   int32_t status;         /* ssa_status for this series (INVALID_ARGUMENT if non-finite)   */
-  int32_t reserved;
+  int32_t restarts;       /* breakdown restarts (fresh seeded vectors, R11)      */
   double max_residual;    /* max_i alpha_{m+1}|P_{m+1,i}| / omega_1 over the k triples     */
   double sigma1;          /* omega_1                                                       */
+  int32_t rows_u;         /* Krylov basis rows of U read by reorthogonalization (all passes) */
+  int32_t rows_v;         /* the same for V  (bytes read = 8 (rows_u L + rows_v K))          */
+  int32_t reorth_steps;   /* half-steps that reorthogonalized (all of them under FRO)      */
+  int32_t reserved;
 } ssa_series_info;
 
 /* Fill *opt with the defaults above (max_steps = 0 means "derive from k, L, K"). */

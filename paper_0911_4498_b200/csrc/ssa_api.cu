@@ -72,7 +72,8 @@ extern "C" ssa_status ssa_options_default(ssa_options* opt) {
   opt->max_steps = 0;
   opt->check_every = 4;
   opt->seed = 42;
-  opt->reorth = 1;
+  opt->reorth = 3;
+  opt->reorth_eta = 1.8189894035458565e-12;  // eps^(3/4)
   return SSA_OK;
 }
 
@@ -122,7 +123,7 @@ static void free_plan(Plan& p) {
     if (q) cudaFree(q);
   for (int i = 0; i < 2 * Plan::kPhases; ++i)
     if (p.ev[i]) cudaEventDestroy(p.ev[i]);
-  for (int i = 0; i < 2; ++i)
+  for (int i = 0; i < 3; ++i)
     if (p.sub[i]) ssa_plan_destroy(reinterpret_cast<ssa_plan_t>(p.sub[i]));
   for (int i = 0; i < 4; ++i)
     if (p.hs[i]) cudaStreamDestroy(p.hs[i]);
@@ -187,7 +188,7 @@ static ssa_status create_decompose_workspace(Plan& p, const cudaDeviceProp& prop
   if ((st = alloc((void**)&p.d_V, C * (p.m_max + 1) * p.ldK * 8, "V bases")) != SSA_OK) return st;
   if ((st = alloc((void**)&p.d_spec, C * (p.H + 1) * 16, "spectra")) != SSA_OK) return st;
   if ((st = alloc((void**)&p.d_ab, C * 2 * (p.m_max + 3) * 8, "bidiagonals")) != SSA_OK) return st;
-  if ((st = alloc((void**)&p.d_state, C * 8 * sizeof(int), "series state")) != SSA_OK) return st;
+  if ((st = alloc((void**)&p.d_state, C * ssa::kStateInts * sizeof(int), "series state")) != SSA_OK) return st;
   if ((st = alloc((void**)&p.d_coef, C * 2 * (p.m_max + 2) * k * 8, "Ritz coefficients")) != SSA_OK) return st;
   if ((st = alloc((void**)&p.d_tgk, (size_t)p.lanczos_slots * 2 * k * (2 * p.m_max + 2) * 8, "TGK scratch")) != SSA_OK)
     return st;
@@ -224,7 +225,7 @@ static ssa_status create_large_workspace(Plan& p) {
   if ((st = alloc((void**)&p.d_V, (size_t)(p.m_max + 1) * p.ldK * 8, "V basis")) != SSA_OK) return st;
   if ((st = alloc((void**)&p.d_spec, (size_t)(p.H + 1) * 16, "spectrum")) != SSA_OK) return st;
   if ((st = alloc((void**)&p.d_ab, (size_t)2 * (p.m_max + 3) * 8, "bidiagonal")) != SSA_OK) return st;
-  if ((st = alloc((void**)&p.d_state, 8 * sizeof(int), "series state")) != SSA_OK) return st;
+  if ((st = alloc((void**)&p.d_state, ssa::kStateInts * sizeof(int), "series state")) != SSA_OK) return st;
   if ((st = alloc((void**)&p.d_coef, (size_t)2 * (p.m_max + 2) * k * 8, "Ritz coefficients")) != SSA_OK) return st;
   if ((st = alloc((void**)&p.d_tgk, (size_t)2 * k * (2 * p.m_max + 2) * 8, "TGK scratch")) != SSA_OK) return st;
   if ((st = alloc((void**)&p.d_tgkw, tgkw_stride(p) * 8, "TGK vectors")) != SSA_OK) return st;
@@ -255,8 +256,11 @@ extern "C" ssa_status ssa_plan_create(int64_t N, int64_t L, int32_t k, int64_t b
   ssa_options o;
   ssa_options_default(&o);
   if (opt) o = *opt;
-  if (!(o.tol > 0.0) || o.reorth < 1 || o.reorth > 2 || o.check_every < 0 || o.max_steps < 0)
-    return fail(SSA_ERR_INVALID_ARGUMENT, "bad options (tol > 0, reorth in {1,2}, check_every >= 0, max_steps >= 0)");
+  if (!(o.tol > 0.0) || o.reorth < 1 || o.reorth > 3 || o.check_every < 0 || o.max_steps < 0 || o.series_base < 0 ||
+      (o.reorth == 3 && !(o.reorth_eta > 0.0 && o.reorth_eta <= 1e-6)))
+    return fail(SSA_ERR_INVALID_ARGUMENT,
+                "bad options (tol > 0, reorth in {1,2,3}, reorth_eta in (0, 1e-6] for reorth 3, check_every >= 0, "
+                "max_steps >= 0, series_base >= 0)");
 
   int64_t M = 1;
   while (M < N) M <<= 1;
@@ -276,6 +280,7 @@ extern "C" ssa_status ssa_plan_create(int64_t N, int64_t L, int32_t k, int64_t b
   Plan& p = ps->p;
   p.device = device;
   p.N = N; p.L = L; p.K = K; p.M = M; p.H = H; p.k = k; p.batch = batch; p.opt = o;
+  p.series_base = o.series_base;
   p.sms = prop.multiProcessorCount;
   int64_t mn = std::min(L, K);
   int64_t mm = o.max_steps > 0 ? o.max_steps : std::max<int64_t>(256, 8 * (int64_t)k);
@@ -452,7 +457,7 @@ extern "C" ssa_status ssa_decompose(ssa_plan_t plan, const double* d_series, dou
   ssa::DecomposeArgs a;
   a.N = (int)p.N; a.L = (int)p.L; a.K = (int)p.K; a.M = (int)p.M; a.H = (int)p.H; a.k = p.k;
   a.m_max = p.m_max; a.ldL = p.ldL; a.ldK = p.ldK;
-  a.check_every = p.opt.check_every; a.reorth_mode = p.opt.reorth;
+  a.check_every = p.opt.check_every; a.reorth_mode = p.opt.reorth; a.pro_eta = p.opt.reorth_eta;
   {
     // first test after 3k + 8 steps (no cfg1/cfg2 series converged before ~3.5k), then
     // every check_every steps, stretched up to 3 check_every when the residual decays
@@ -721,15 +726,19 @@ extern "C" ssa_status ssa_run_host(ssa_plan_t plan, const double* h_series, doub
   if (const char* e = getenv("SSA_HOST_SLICES")) nsl = std::max(1, std::min(Plan::kMaxSlices, atoi(e)));
   if (nsl > 1 && (int64_t)B >= 2 * nsl) {
     const int64_t sb = ((int64_t)B + nsl - 1) / nsl;
-    if (p.sub_batch != sb) {
-      for (int i = 0; i < 2; ++i)
+    nsl = (int)(((int64_t)B + sb - 1) / sb);
+    const int64_t tail = (int64_t)B - (int64_t)(nsl - 1) * sb;  // 1 <= tail <= sb
+    if (p.sub_batch != sb || p.tail_batch != tail) {
+      for (int i = 0; i < 3; ++i)
         if (p.sub[i]) { ssa_plan_destroy(reinterpret_cast<ssa_plan_t>(p.sub[i])); p.sub[i] = nullptr; }
-      for (int i = 0; i < 2; ++i) {
+      for (int i = 0; i < 3; ++i) {
+        if (i == 2 && tail == sb) break;
         ssa_plan_t q = nullptr;
-        if ((st = ssa_plan_create(p.N, p.L, p.k, sb, &p.opt, p.device, &q)) != SSA_OK) return st;
+        if ((st = ssa_plan_create(p.N, p.L, p.k, i < 2 ? sb : tail, &p.opt, p.device, &q)) != SSA_OK) return st;
         p.sub[i] = q;
       }
       p.sub_batch = sb;
+      p.tail_batch = tail;
     }
     for (int i = 0; i < 4; ++i)
       if (!p.hs[i]) CK(cudaStreamCreateWithFlags(&p.hs[i], cudaStreamNonBlocking), "cudaStreamCreate");
@@ -742,32 +751,27 @@ extern "C" ssa_status ssa_run_host(ssa_plan_t plan, const double* h_series, doub
     // compute waits only for its own series
     for (int i = 0; i < nsl; ++i) {
       const size_t b0 = (size_t)i * sb;
-      if (b0 >= B) break;
       const size_t nb = std::min<size_t>(sb, B - b0);
-      const size_t s0 = (nb == (size_t)sb) ? b0 : B - sb;
-      CK(cudaMemcpyAsync(p.d_series + s0 * p.N, h_series + s0 * p.N, (size_t)sb * p.N * 8, cudaMemcpyHostToDevice,
-                         p.hs[3]),
+      CK(cudaMemcpyAsync(p.d_series + b0 * p.N, h_series + b0 * p.N, nb * p.N * 8, cudaMemcpyHostToDevice, p.hs[3]),
          "H2D series");
       CK(cudaEventRecord(p.hev[Plan::kMaxSlices + i], p.hs[3]), "event record");
     }
     for (int i = 0; i < nsl; ++i) {
       const size_t b0 = (size_t)i * sb;
-      if (b0 >= B) break;
       const size_t nb = std::min<size_t>(sb, B - b0);
-      Plan& q = reinterpret_cast<ssa_plan_t>(p.sub[i & 1])->p;
+      // full slices alternate between sub-plans 0 and 1; a shorter last slice has its own
+      // tail-sized sub-plan, so no rows are read or written by two streams at once
+      const int si = (nb == (size_t)sb) ? (i & 1) : 2;
+      ssa_plan_t qp = reinterpret_cast<ssa_plan_t>(p.sub[si]);
+      Plan& q = qp->p;
       cudaStream_t cs = p.hs[i & 1];
-      // the sub-plan runs a full slice of sb series; the last slice may be shorter: it
-      // then re-runs the tail of the batch (results of the overlap are written twice,
-      // identically)
-      const size_t s0 = (nb == (size_t)sb) ? b0 : B - sb;
       CK(cudaStreamWaitEvent(cs, p.hev[Plan::kMaxSlices + i], 0), "stream wait");
-      q.series_base = (int64_t)s0;  // same start vectors as the single-launch path
-      if ((st = ssa_decompose(reinterpret_cast<ssa_plan_t>(p.sub[i & 1]), p.d_series + s0 * p.N, p.d_sigma + s0 * k,
-                              p.d_Uout + s0 * k * p.L, p.d_Vout + s0 * k * p.K, p.d_info + s0, cs)) != SSA_OK)
+      q.series_base = p.series_base + (int64_t)b0;  // same start vectors as the single-launch path
+      if ((st = ssa_decompose(qp, p.d_series + b0 * p.N, p.d_sigma + b0 * k, p.d_Uout + b0 * k * p.L,
+                              p.d_Vout + b0 * k * p.K, p.d_info + b0, cs)) != SSA_OK)
         return st;
-      if ((st = ssa_reconstruct(reinterpret_cast<ssa_plan_t>(p.sub[i & 1]), p.d_sigma + s0 * k,
-                                p.d_Uout + s0 * k * p.L, p.d_Vout + s0 * k * p.K, p.d_recon + s0 * k * p.N, cs)) !=
-          SSA_OK)
+      if ((st = ssa_reconstruct(qp, p.d_sigma + b0 * k, p.d_Uout + b0 * k * p.L, p.d_Vout + b0 * k * p.K,
+                                p.d_recon + b0 * k * p.N, cs)) != SSA_OK)
         return st;
       p.launches += q.launches;  // launch accounting of the caller's plan
       q.launches = 0;
@@ -838,13 +842,13 @@ extern "C" ssa_status ssa_plan_bidiagonals(ssa_plan_t plan, double* h_alpha, dou
   const int64_t nb = std::min<int64_t>(p.chunk, p.batch - (p.batch - 1) / p.chunk * p.chunk);
   const size_t w = (size_t)p.m_max + 3;
   std::vector<double> ab((size_t)nb * 2 * w);
-  std::vector<int> st((size_t)nb * 8);
+  std::vector<int> st((size_t)nb * ssa::kStateInts);
   CK(cudaMemcpy(ab.data(), p.d_ab, ab.size() * 8, cudaMemcpyDeviceToHost), "D2H ab");
   CK(cudaMemcpy(st.data(), p.d_state, st.size() * 4, cudaMemcpyDeviceToHost), "D2H state");
   for (int64_t b = 0; b < nb; ++b) {
     memcpy(h_alpha + b * w, &ab[(size_t)b * 2 * w], w * 8);
     memcpy(h_beta + b * w, &ab[(size_t)b * 2 * w + w], w * 8);
-    h_steps[b] = st[(size_t)b * 8];
+    h_steps[b] = st[(size_t)b * ssa::kStateInts];
   }
   return SSA_OK;
 }

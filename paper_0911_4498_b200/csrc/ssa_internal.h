@@ -14,6 +14,7 @@ constexpr int kStages = 3;             // TMA ring depth per warp (basis streami
 constexpr int kMaxSmemH = 8192;        // largest H = M/2 held in one CTA's shared memory
 constexpr int kMaxHankelSmemH = 4096;  // largest H with both hankelization buffers in SMEM
 constexpr int kMaxK = 32;              // largest k of the batched decompose
+constexpr int kStateInts = 12;         // per-series state words (DecomposeArgs::state)
 
 inline size_t fft_bytes(int H) { return (size_t)H * 16; }
 
@@ -21,7 +22,8 @@ inline size_t fft_bytes(int H) { return (size_t)H * 16; }
 // storage covers one chunk of nb series [b0, b0+nb) of the call.
 struct DecomposeArgs {
   int N, L, K, M, H, k, m_max, ldL, ldK;
-  int check_every, reorth_mode;
+  int check_every, reorth_mode;  // reorth_mode 1/2: FRO (DGKS / always two passes), 3: PRO
+  double pro_eta;                 // PRO threshold (ssa_options::reorth_eta)
   int first_check, check_cap;  // step of the first convergence test; longest stretch between tests
   int b0, nb;
   double tol;
@@ -33,7 +35,8 @@ struct DecomposeArgs {
   double* U;             // [nb][m_max+1][ldL]  Krylov basis U_{m+1}
   double* V;             // [nb][m_max+1][ldK]  Krylov basis V_{m+1}
   double* ab;            // [nb][2][m_max+3]    alpha_j, beta_j (1-based)
-  int* state;            // [nb][8]: m, converged, breakdown, reorth_extra, restarts, bad, checks, svd done
+  int* state;            // [nb][kStateInts]: m, converged, breakdown, reorth_extra, restarts, bad, checks,
+                         // svd done, rows_u, rows_v, reorth_steps, -
   double* tgk;           // per Lanczos CTA slot: k * (2 m_max + 2) doubles
   size_t tgk_stride;
   double* rot;           // per SVD warp slot: 2 sides x rot_cap x 3 doubles
@@ -110,8 +113,8 @@ struct Plan {
   double* d_bs = nullptr;    // bootstrap: replicates [batch][N] then reconstructions [batch][N]
   // host-API pipelining (ssa_run_host): two sub-plans of one slice each, alternating on two
   // compute streams, device-to-host copies of finished slices on a third stream
-  void* sub[2] = {nullptr, nullptr};  // ssa_plan_t
-  int64_t sub_batch = 0;
+  void* sub[3] = {nullptr, nullptr, nullptr};  // ssa_plan_t: two full slices + the short tail slice
+  int64_t sub_batch = 0, tail_batch = 0;
   int64_t series_base = 0;  // sub-plans: global index of their current slice's first series
   cudaStream_t hs[4] = {};  // compute x2, device-to-host, host-to-device
   static constexpr int kMaxSlices = 16;
@@ -179,7 +182,8 @@ cudaError_t large_lanczos_set_attributes(int m_max);
 cudaError_t large_spectrum(const Plan& p, const double* series, double2* spec, int items, cudaStream_t s);
 cudaError_t large_correlate(const Plan& p, const double2* spec, size_t spec_stride, const double* x, size_t xs, int n_in,
                             double* out, size_t os, int n_out, int ld_out, const double* prev, size_t ps,
-                            const double* coef, double* part, int items, cudaStream_t s);
+                            const double* coef, double* part, int items, cudaStream_t s,
+                            const int* gate = nullptr);
 cudaError_t large_hankelize(Plan& p, const double* sigma, const double* U, const double* V, size_t nterm_total,
                             double* out, cudaStream_t s);
 cudaError_t large_decompose_one(Plan& p, const DecomposeArgs& a, int b, cudaStream_t s);

@@ -25,6 +25,8 @@ struct LSmem {
   double* h;               // m_max + 2
   double* alpha;           // m_max + 3 (1-based)
   double* beta;            // m_max + 3 (1-based)
+  double* mu;              // m_max + 3: PRO estimates of u_{j}^T u_i (1-based), R22
+  double* nu;              // m_max + 3: PRO estimates of v_{j}^T v_i
   double* red;             // 32
   int* redi;               // 8 ints
   int* cl;                 // 40 ints: cluster starts of the final SVD (tgk_clusters)
@@ -48,7 +50,7 @@ size_t lanczos_smem_bytes(int H, int ldL, int ldK, int m_max, int k) {
   (void)k;
   size_t s = lanczos_regionA_bytes(H, ldL, ldK, m_max);
   s += align16((size_t)ldL * 8) + align16((size_t)ldK * 8);
-  s += 3 * align16((size_t)(m_max + 3) * 8);
+  s += 5 * align16((size_t)(m_max + 3) * 8);
   s += 32 * 8 + 8 * 4 + 40 * 4 + 4 * kMaxK * 8;
   s += (size_t)tw2_entries(2 * H) * 16;
   s += (size_t)kWarps * kStages * 8;
@@ -65,6 +67,8 @@ __device__ inline LSmem carve(unsigned char* base, const DecomposeArgs& a) {
   s.h = reinterpret_cast<double*>(base + off); off += align16((size_t)(a.m_max + 3) * 8);
   s.alpha = reinterpret_cast<double*>(base + off); off += align16((size_t)(a.m_max + 3) * 8);
   s.beta = reinterpret_cast<double*>(base + off); off += align16((size_t)(a.m_max + 3) * 8);
+  s.mu = reinterpret_cast<double*>(base + off); off += align16((size_t)(a.m_max + 3) * 8);
+  s.nu = reinterpret_cast<double*>(base + off); off += align16((size_t)(a.m_max + 3) * 8);
   s.red = reinterpret_cast<double*>(base + off); off += 32 * 8;
   s.redi = reinterpret_cast<int*>(base + off); off += 8 * 4;
   s.cl = reinterpret_cast<int*>(base + off); off += 40 * 4;
@@ -257,6 +261,60 @@ __device__ double restart_vector(double* r, int n, int ld, const double* basis, 
   return nn / nrm;
 }
 
+// ---- partial reorthogonalization (PRO; Simon 1984, Larsen 1998) ----
+// The orthogonality levels omega of the newest Lanczos vector against the basis obey the
+// recurrences obtained from Alg. 1 lines 4-7 by taking inner products:
+//   v side:  alpha_j nu_{j,i}     = alpha_i mu_{j,i} + beta_{i+1} mu_{j,i+1} - beta_j nu_{j-1,i}
+//   u side:  beta_{j+1} mu_{j+1,i} = alpha_i nu_{j,i} + beta_i nu_{j,i-1}    - alpha_j mu_{j,i}
+// plus a rounding term eps (|B row i| + |B row j|) + eps |A| with the sign of the value
+// (Larsen's update_nu / update_mu).  Updated in place (thread i owns index i; the other
+// side's array is read only).  Returns max_i |omega_i| (block-uniform).
+constexpr double kEps = 2.220446049250313e-16;
+
+__device__ __forceinline__ double block_max(double v, double* red) {
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s = fmax(s, red[i]);
+  return s;
+}
+
+// nu_{j,i}, i = 1..j-1, for the new v_j (norm a_est before any reorthogonalization)
+__device__ double pro_update_nu(const LSmem& sm, int j, double a_est, double bj, double anorm) {
+  double mx = 0.0;
+  const double rj = hypot(a_est, bj);
+  for (int i = 1 + threadIdx.x; i <= j - 1; i += blockDim.x) {
+    double t = fma(sm.alpha[i], sm.mu[i], fma(sm.beta[i + 1], sm.mu[i + 1], -bj * sm.nu[i]));
+    const double d = kEps * (hypot(sm.alpha[i], sm.beta[i + 1]) + rj) + kEps * anorm;
+    t = (t + copysign(d, t)) / a_est;
+    sm.nu[i] = t;
+    mx = fmax(mx, fabs(t));
+  }
+  return block_max(mx, sm.red);
+}
+
+// mu_{j+1,i}, i = 1..j, for the new u_{j+1} (norm b_est before any reorthogonalization)
+__device__ double pro_update_mu(const LSmem& sm, int j, double b_est, double aj, double anorm) {
+  double mx = 0.0;
+  const double rj = hypot(aj, b_est);
+  for (int i = 1 + threadIdx.x; i <= j; i += blockDim.x) {
+    double t = fma(sm.alpha[i], sm.nu[i], fma(sm.beta[i], sm.nu[i - 1], -aj * sm.mu[i]));
+    const double d = kEps * (hypot(sm.alpha[i], sm.beta[i]) + rj) + kEps * anorm;
+    t = (t + copysign(d, t)) / b_est;
+    sm.mu[i] = t;
+    mx = fmax(mx, fabs(t));
+  }
+  return block_max(mx, sm.red);
+}
+
+// after a full reorthogonalization against rows 1..n the estimates drop to eps
+__device__ __forceinline__ void pro_reset(double* om, int n) {
+  for (int i = 1 + threadIdx.x; i <= n; i += blockDim.x) om[i] = kEps;
+}
+
 __global__ void __launch_bounds__(kThreads, 2) lanczos_kernel(const DecomposeArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   LSmem sm = carve(smem_raw, a);
@@ -297,14 +355,14 @@ __global__ void __launch_bounds__(kThreads, 2) lanczos_kernel(const DecomposeArg
     double* U = a.U + (size_t)bl * (a.m_max + 1) * a.ldL;
     double* V = a.V + (size_t)bl * (a.m_max + 1) * a.ldK;
     double* abg = a.ab + (size_t)bl * 2 * (a.m_max + 3);
-    int* st = a.state + (size_t)bl * 8;
+    int* st = a.state + (size_t)bl * kStateInts;
 
     // ---- non-finite input -> INVALID_ARGUMENT ----
     int bad = 0;
     for (int t = tid; t < a.N; t += blockDim.x) bad |= !isfinite(f[t]);
     if (block_or(bad, sm.redi)) {
       if (tid == 0) {
-        st[0] = 0; st[1] = 0; st[2] = 0; st[3] = 0; st[4] = 0; st[5] = 1; st[6] = 0; st[7] = 0;
+        for (int q = 0; q < kStateInts; ++q) st[q] = (q == 5) ? 1 : 0;
       }
       continue;
     }
@@ -320,6 +378,15 @@ __global__ void __launch_bounds__(kThreads, 2) lanczos_kernel(const DecomposeArg
     double beta1 = sqrt(block_sum(ss, sm.red));
     if (tid == 0) { sm.beta[1] = beta1; sm.alpha[0] = 0.0; sm.beta[0] = 0.0; }
     normalize_store(sm.bufU, L, a.ldL, 1.0 / beta1, U);
+
+    // PRO state: omega estimates (1-based; mu_1 = 1 for u_1), forced follow-up flags
+    const bool pro = (a.reorth_mode == 3);
+    for (int i = tid; i < a.m_max + 3; i += blockDim.x) {
+      sm.mu[i] = (i == 1) ? 1.0 : 0.0;
+      sm.nu[i] = 0.0;
+    }
+    bool force_v = false, force_u = false;
+    int rows_u = 0, rows_v = 0, rsteps = 0;
 
     double runmax = 0.0, bcur = beta1;
     int m = 0, converged = 0, breakdown = 0, extra = 0, restarts = 0, checks = 0;
@@ -340,7 +407,21 @@ __global__ void __launch_bounds__(kThreads, 2) lanczos_kernel(const DecomposeArg
       for (int t = tid; t < K; t += blockDim.x) ss = fma(sm.bufV[t], sm.bufV[t], ss);
       double nr = sqrt(block_sum(ss, sm.red));
       lap(0);
-      double al = reorth(sm.bufV, V, j - 1, a.ldK, nr, a.reorth_mode, sm, rg, part, pstride, extra);
+      // FRO: every half-step; PRO: only when the estimated level exceeds eta, and on the
+      // v half-step after one that did (Simon / Larsen), R22
+      bool do_ro = !pro || force_v;
+      if (pro && j >= 2 && nr > 0.0) do_ro = (pro_update_nu(sm, j, nr, bj, runmax) > a.pro_eta) || force_v;
+      double al = nr;
+      if (do_ro && j >= 2) {
+        const int e0 = extra;
+        al = reorth(sm.bufV, V, j - 1, a.ldK, nr, pro ? 1 : a.reorth_mode, sm, rg, part, pstride, extra);
+        rows_v += 2 * (j - 1) * (1 + extra - e0);
+        ++rsteps;
+        if (pro) pro_reset(sm.nu, j - 1);
+        force_v = pro && !force_v;
+      } else {
+        force_v = false;
+      }
       if (!(al > 1e-12 * runmax) || al == 0.0) {
         if (!breakdown) breakdown = j;
         double q = (j - 1 < K) ? restart_vector(sm.bufV, K, a.ldK, V, j - 1, a.seed, (uint64_t)(b + a.series_base),
@@ -355,10 +436,14 @@ __global__ void __launch_bounds__(kThreads, 2) lanczos_kernel(const DecomposeArg
           normalize_store(sm.bufV, K, a.ldK, 0.0, V + (size_t)(j - 1) * a.ldK);
         }
         al = 0.0;
+        if (pro) pro_reset(sm.nu, j - 1);  // the restart vector is orthogonalized twice
       } else {
         normalize_store(sm.bufV, K, a.ldK, 1.0 / al, V + (size_t)(j - 1) * a.ldK);
       }
-      if (tid == 0) sm.alpha[j] = al;
+      if (tid == 0) {
+        sm.alpha[j] = al;
+        sm.nu[j] = 1.0;
+      }
       runmax = fmax(runmax, al);
       m = j - 1;
       lap(1);
@@ -427,7 +512,19 @@ __global__ void __launch_bounds__(kThreads, 2) lanczos_kernel(const DecomposeArg
       for (int t = tid; t < L; t += blockDim.x) ss = fma(sm.bufU[t], sm.bufU[t], ss);
       nr = sqrt(block_sum(ss, sm.red));
       lap(0);
-      double be = reorth(sm.bufU, U, j, a.ldL, nr, a.reorth_mode, sm, rg, part, pstride, extra);
+      bool do_ro_u = !pro || force_u;
+      if (pro && nr > 0.0) do_ro_u = (pro_update_mu(sm, j, nr, aj, runmax) > a.pro_eta) || force_u;
+      double be = nr;
+      if (do_ro_u) {
+        const int e0 = extra;
+        be = reorth(sm.bufU, U, j, a.ldL, nr, pro ? 1 : a.reorth_mode, sm, rg, part, pstride, extra);
+        rows_u += 2 * j * (1 + extra - e0);
+        ++rsteps;
+        if (pro) pro_reset(sm.mu, j);
+        force_u = pro && !force_u;
+      } else {
+        force_u = false;
+      }
       if (!(be > 1e-12 * runmax) || be == 0.0) {
         if (!breakdown) breakdown = j;
         double q = (j < L) ? restart_vector(sm.bufU, L, a.ldL, U, j, a.seed, (uint64_t)(b + a.series_base),
@@ -442,10 +539,14 @@ __global__ void __launch_bounds__(kThreads, 2) lanczos_kernel(const DecomposeArg
           normalize_store(sm.bufU, L, a.ldL, 0.0, U + (size_t)j * a.ldL);
         }
         be = 0.0;
+        if (pro) pro_reset(sm.mu, j);
       } else {
         normalize_store(sm.bufU, L, a.ldL, 1.0 / be, U + (size_t)j * a.ldL);
       }
-      if (tid == 0) sm.beta[j + 1] = be;
+      if (tid == 0) {
+        sm.beta[j + 1] = be;
+        sm.mu[j + 1] = 1.0;
+      }
       bcur = be;
       runmax = fmax(runmax, be);
       lap(1);
@@ -486,7 +587,11 @@ __global__ void __launch_bounds__(kThreads, 2) lanczos_kernel(const DecomposeArg
           inf.converged = converged;
           inf.breakdown_step = breakdown;
           inf.reorth_extra = extra;
-          inf.reserved = restarts;
+          inf.restarts = restarts;
+          inf.rows_u = rows_u;
+          inf.rows_v = rows_v;
+          inf.reorth_steps = rsteps;
+          inf.reserved = 0;
           inf.status = fres <= a.tol ? SSA_OK : SSA_ERR_NOT_CONVERGED;
           inf.max_residual = fres;
           inf.sigma1 = om[0];
@@ -503,7 +608,7 @@ __global__ void __launch_bounds__(kThreads, 2) lanczos_kernel(const DecomposeArg
     }
     if (tid == 0) {
       st[0] = m; st[1] = converged; st[2] = breakdown; st[3] = extra; st[4] = restarts; st[5] = 0; st[6] = checks;
-      st[7] = fused;
+      st[7] = fused; st[8] = rows_u; st[9] = rows_v; st[10] = rsteps; st[11] = 0;
       pc[3] += (unsigned long long)checks;  // profile slot 3: number of convergence tests
     }
   }

@@ -103,12 +103,14 @@ struct ColFwdIn {
 };
 struct ColFwdArgs {
   ColFwdIn in[2];   // blockIdx.z selects
+  const int* gate;  // device flag: nonzero -> the launch does nothing (graph-driven loops)
 };
 
 template <int LOGH>
 __global__ void __launch_bounds__(kThreads) lg_col_fwd(ColFwdArgs args, const double2* __restrict__ T1,
                                                        const double2* __restrict__ TWH) {
   pdl_wait();
+  if (args.gate && *args.gate) return;
   using G = Geo<LOGH>;
   constexpr int N1 = G::N1, N2 = G::N2, CS = N1 + 1;  // odd column stride (16-byte units)
   constexpr int NE = (N1 * kColW + kThreads - 1) / kThreads;
@@ -180,12 +182,14 @@ struct ColInvArgs {
   double* part;                // correlation: partial sums of squares [items][gridDim.x]
   const double* sigma;         // hankelization: per-item sigma
   int N, L, K;                 // hankelization: weights
+  const int* gate;             // device flag: nonzero -> the launch does nothing
 };
 
 template <int LOGH>
 __global__ void __launch_bounds__(kThreads, (LOGH >= 19) ? 1 : 3) lg_col_inv(const double2* __restrict__ Y, const double2* __restrict__ T1,
                                                        ColInvArgs a) {
   pdl_wait();
+  if (ca.gate && *ca.gate) return;
   using G = Geo<LOGH>;
   constexpr int N1 = G::N1, N2 = G::N2, CS = N1 + 1;
   constexpr int NE = (N1 * kColW + kThreads - 1) / kThreads;
@@ -301,6 +305,7 @@ struct RowArgs {
   const double2* spec;  // mode 1: F^ [items or 1][H+1]
   size_t spec_stride;   // 0 -> shared spectrum for all items
   double2* spec_out;    // mode 0: [items][H+1]
+  const int* gate;      // device flag: nonzero -> the launch does nothing
 };
 
 __device__ __forceinline__ int partner_k2(int A, int k2, int N2) {
@@ -370,6 +375,7 @@ template <int LOGH>
 __global__ void __launch_bounds__(kThreads) lg_row_cta(const double2* __restrict__ T2, const double2* __restrict__ TWH,
                                                        const double2* __restrict__ TWA, RowArgs a) {
   pdl_wait();
+  if (a.gate && *a.gate) return;
   using G = Geo<LOGH>;
   constexpr int N1 = G::N1, N2 = G::N2;
   constexpr int NE = (N2 + kThreads - 1) / kThreads;
@@ -485,6 +491,7 @@ __global__ void __launch_bounds__(kThreads) lg_row_warp(const double2* __restric
                                                         const double2* __restrict__ TWH,
                                                         const double2* __restrict__ TWA, RowArgs a) {
   pdl_wait();
+  if (a.gate && *a.gate) return;
   using Gm = Geo<LOGH>;
   constexpr int N1 = Gm::N1, N2 = Gm::N2;
   constexpr int NE = (N2 + 31) / 32;
@@ -673,7 +680,7 @@ cudaError_t large_spectrum(const Plan& p, const double* series, double2* spec, i
     ColFwdArgs ca{};
     ca.in[0] = ColFwdIn{series + (size_t)i0 * p.N, (size_t)p.N, (int)p.N, Y, vec16(series, p.N)};
     col_fwd(p, ca, 1, ni, s);
-    RowArgs ra{0, Y, nullptr, nullptr, 0, spec + (size_t)i0 * (p.H + 1)};
+    RowArgs ra{0, Y, nullptr, nullptr, 0, spec + (size_t)i0 * (p.H + 1), nullptr};
     rows(p, ra, ni, false, s);
   }
   return cudaGetLastError();
@@ -682,7 +689,7 @@ cudaError_t large_spectrum(const Plan& p, const double* series, double2* spec, i
 // y[item] = X x (transpose 0) or X^T x (1) for items sharing one spectrum stride.
 cudaError_t large_correlate(const Plan& p, const double2* spec, size_t spec_stride, const double* x, size_t xs, int n_in,
                             double* out, size_t os, int n_out, int ld_out, const double* prev, size_t ps,
-                            const double* coef, double* part, int items, cudaStream_t s) {
+                            const double* coef, double* part, int items, cudaStream_t s, const int* gate) {
   int N1, N2;
   large_geom(p, &N1, &N2);
   double2* Y = p.d_lbuf;
@@ -690,8 +697,9 @@ cudaError_t large_correlate(const Plan& p, const double2* spec, size_t spec_stri
     const int ni = std::min(items - i0, p.lbuf_items);
     ColFwdArgs cf{};
     cf.in[0] = ColFwdIn{x + (size_t)i0 * xs, xs, n_in, Y, vec16(x, xs)};
+    cf.gate = gate;
     col_fwd(p, cf, 1, ni, s);
-    RowArgs ra{1, Y, nullptr, spec + (size_t)i0 * spec_stride, spec_stride, nullptr};
+    RowArgs ra{1, Y, nullptr, spec + (size_t)i0 * spec_stride, spec_stride, nullptr, gate};
     rows(p, ra, ni, ni >= 8, s);
     ColInvArgs ca{};
     ca.mode = 0;
@@ -699,6 +707,7 @@ cudaError_t large_correlate(const Plan& p, const double2* spec, size_t spec_stri
     ca.prev = prev ? prev + (size_t)i0 * ps : nullptr; ca.prev_stride = ps;
     ca.coef = coef ? coef + i0 : nullptr;
     ca.part = part ? part + (size_t)i0 * (N2 / kColW) : nullptr;
+    ca.gate = gate;
     col_inv(p, Y, ca, ni, s);
   }
   return cudaGetLastError();
@@ -734,7 +743,7 @@ cudaError_t large_hankelize(Plan& p, const double* sigma, const double* U, const
     cf.in[0] = ColFwdIn{U + t0 * p.L, (size_t)p.L, (int)p.L, Ya, vec16(U, p.L)};
     cf.in[1] = ColFwdIn{V + t0 * p.K, (size_t)p.K, (int)p.K, Yb, vec16(V, p.K)};
     col_fwd(p, cf, 2, ni, st);
-    RowArgs ra{2, Ya, Yb, nullptr, 0, nullptr};
+    RowArgs ra{2, Ya, Yb, nullptr, 0, nullptr, nullptr};
     rows(p, ra, ni, true, st);
     ColInvArgs ca{};
     ca.mode = 1;

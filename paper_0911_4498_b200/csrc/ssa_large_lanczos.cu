@@ -302,34 +302,43 @@ __global__ void __launch_bounds__(kThreads) lg_check(const double* __restrict__ 
   }
 }
 
-// Ritz vectors: out[i][t] = sum_row coef[row][i] basis[row][t], one element per thread
+// Ritz vectors: out[i][t] = sum_row coef[row][i] basis[row][t], one element per thread.
+// The coefficient rows are staged through a fixed shared-memory tile of kRitzRows rows
+// (zero-padded to kMaxK per row, read as broadcast 16-byte loads), so the kernel's shared
+// memory does not depend on the step count m.
+constexpr int kRitzRows = 128;
+
 __global__ void __launch_bounds__(kThreads) lg_ritz(const double* __restrict__ basis, int ld, int rows,
                                                     const double* __restrict__ coef, int k, int n, double* out,
                                                     double* amax, int* aidx) {
   pdl_wait();
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  // the rows x k coefficients in shared memory, zero-padded to kMaxK per row: every
-  // thread then reads them as broadcast 16-byte loads (not k L1 loads per row)
-  extern __shared__ __align__(16) double cs[];  // [rows][kMaxK]
-  for (int e = threadIdx.x; e < rows * kMaxK; e += blockDim.x) {
-    const int r = e / kMaxK, i = e - r * kMaxK;
-    cs[e] = (i < k) ? __ldg(coef + (size_t)r * k + i) : 0.0;
-  }
-  __syncthreads();
+  __shared__ __align__(16) double cs[kRitzRows * kMaxK];
   double acc[kMaxK];
 #pragma unroll
   for (int i = 0; i < kMaxK; ++i) acc[i] = 0.0;
-  if (t < n) {
-    for (int row = 0; row < rows; ++row) {
-      const double x = __ldcs(basis + (size_t)row * ld + t);
-      const double2* cr = reinterpret_cast<const double2*>(cs + (size_t)row * kMaxK);
+  for (int r0 = 0; r0 < rows; r0 += kRitzRows) {
+    const int nr = min(kRitzRows, rows - r0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < nr * kMaxK; e += blockDim.x) {
+      const int r = e / kMaxK, i = e - r * kMaxK;
+      cs[e] = (i < k) ? __ldg(coef + (size_t)(r0 + r) * k + i) : 0.0;
+    }
+    __syncthreads();
+    if (t < n) {
+      for (int row = 0; row < nr; ++row) {
+        const double x = __ldcs(basis + (size_t)(r0 + row) * ld + t);
+        const double2* cr = reinterpret_cast<const double2*>(cs + (size_t)row * kMaxK);
 #pragma unroll
-      for (int i = 0; i < kMaxK / 2; ++i) {
-        const double2 c = cr[i];
-        acc[2 * i] = fma(c.x, x, acc[2 * i]);
-        acc[2 * i + 1] = fma(c.y, x, acc[2 * i + 1]);
+        for (int i = 0; i < kMaxK / 2; ++i) {
+          const double2 c = cr[i];
+          acc[2 * i] = fma(c.x, x, acc[2 * i]);
+          acc[2 * i + 1] = fma(c.y, x, acc[2 * i + 1]);
+        }
       }
     }
+  }
+  if (t < n) {
 #pragma unroll
     for (int i = 0; i < kMaxK; ++i)
       if (i < k) out[(size_t)i * n + t] = acc[i];
@@ -339,7 +348,9 @@ __global__ void __launch_bounds__(kThreads) lg_ritz(const double* __restrict__ b
     __shared__ double sv[kWarps][kMaxK];
     __shared__ int si[kWarps][kMaxK];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int i = 0; i < k; ++i) {
+#pragma unroll
+    for (int i = 0; i < kMaxK; ++i) {
+      if (i >= k) break;
       double v = (t < n) ? fabs(acc[i]) : -1.0;
       int ix = t;
       for (int o = 16; o > 0; o >>= 1) {
@@ -437,7 +448,7 @@ cudaError_t large_decompose_one(Plan& p, const DecomposeArgs& a0, int b, cudaStr
   double* h = p.d_lgh;
   double* r = p.d_lgr;
   cudaError_t e;
-  if ((e = cudaMemsetAsync(p.d_state, 0, 8 * sizeof(int), s))) return e;
+  if ((e = cudaMemsetAsync(p.d_state, 0, kStateInts * sizeof(int), s))) return e;
   launch_pdl(lg_finite, dim3(64), dim3(kThreads), 0, s, a.series + (size_t)b * N, N, p.d_state);
   if ((e = large_spectrum(p, a.series + (size_t)b * N, p.d_spec, 1, s))) return e;
   LgScalars z{};
@@ -516,10 +527,8 @@ cudaError_t large_decompose_one(Plan& p, const DecomposeArgs& a0, int b, cudaStr
   const int gU = (L + kThreads - 1) / kThreads, gV = (K + kThreads - 1) / kThreads;
   double* amax = p.d_lgpart;
   int* aidx = reinterpret_cast<int*>(p.d_lgpart + (size_t)gU * k);
-  const size_t rsm = (size_t)(m + 1) * kMaxK * 8;  // coefficient rows in shared memory
-  if ((e = raise_smem_limit(lg_ritz, rsm))) return e;
-  launch_pdl(lg_ritz, dim3(gU), dim3(kThreads), rsm, s, U, ldL, m + 1, cP, k, L, Uo, amax, aidx);
-  launch_pdl(lg_ritz, dim3(gV), dim3(kThreads), rsm, s, V, ldK, m, cQ, k, K, Vo, nullptr, nullptr);
+  launch_pdl(lg_ritz, dim3(gU), dim3(kThreads), 0, s, U, ldL, m + 1, cP, k, L, Uo, amax, aidx);
+  launch_pdl(lg_ritz, dim3(gV), dim3(kThreads), 0, s, V, ldK, m, cQ, k, K, Vo, nullptr, nullptr);
   launch_pdl(lg_sign, dim3(1), dim3(32), 0, s, amax, aidx, gU, k, Uo, L, h);
   launch_pdl(lg_flip, dim3((int)(((size_t)L * k + kThreads - 1) / kThreads)), dim3(kThreads), 0, s, Uo, L, k, h);
   launch_pdl(lg_flip, dim3((int)(((size_t)K * k + kThreads - 1) / kThreads)), dim3(kThreads), 0, s, Vo, K, k, h);

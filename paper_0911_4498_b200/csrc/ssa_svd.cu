@@ -45,7 +45,7 @@ __global__ void __launch_bounds__(kSvdWarps * 32) bidiag_svd_kernel(const Decomp
     bl = __shfl_sync(0xffffffffu, bl, 0);
     if (bl >= a.nb) break;
     const int b = a.b0 + bl;
-    const int* st = a.state + (size_t)bl * 8;
+    const int* st = a.state + (size_t)bl * kStateInts;
     const int m = st[0];
     const double* alpha = a.ab + (size_t)bl * 2 * (a.m_max + 3);
     const double* beta = alpha + (a.m_max + 3);
@@ -109,7 +109,11 @@ __global__ void __launch_bounds__(kSvdWarps * 32) bidiag_svd_kernel(const Decomp
       inf.converged = st[1];
       inf.breakdown_step = st[2];
       inf.reorth_extra = st[3];
-      inf.reserved = st[4];
+      inf.restarts = st[4];
+      inf.rows_u = st[8];
+      inf.rows_v = st[9];
+      inf.reorth_steps = st[10];
+      inf.reserved = 0;
       inf.status = !ok ? SSA_ERR_INTERNAL : (fres <= a.tol ? SSA_OK : SSA_ERR_NOT_CONVERGED);
       inf.max_residual = fres;
       inf.sigma1 = om[0];
@@ -153,7 +157,7 @@ __global__ void __launch_bounds__(kThreads) bidiag_svd_tgk_kernel(const Decompos
     const int bl = sb;
     if (bl >= a.nb) break;
     const int b = a.b0 + bl;
-    const int* st = a.state + (size_t)bl * 8;
+    const int* st = a.state + (size_t)bl * kStateInts;
     const int m = st[0];
     const double* alpha = a.ab + (size_t)bl * 2 * (a.m_max + 3);
     const double* beta = alpha + (a.m_max + 3);
@@ -227,7 +231,11 @@ __global__ void __launch_bounds__(kThreads) bidiag_svd_tgk_kernel(const Decompos
       inf.converged = st[1];
       inf.breakdown_step = st[2];
       inf.reorth_extra = st[3];
-      inf.reserved = st[4];
+      inf.restarts = st[4];
+      inf.rows_u = st[8];
+      inf.rows_v = st[9];
+      inf.reorth_steps = st[10];
+      inf.reserved = 0;
       inf.status = fres <= a.tol ? SSA_OK : SSA_ERR_NOT_CONVERGED;
       inf.max_residual = fres;
       inf.sigma1 = lam[0];
@@ -282,7 +290,7 @@ __global__ void __launch_bounds__(kThreads, 2) ritz_kernel(const DecomposeArgs a
     const int bl = sb;
     if (bl >= a.nb) break;
     const int b = a.b0 + bl;
-    const int* st = a.state + (size_t)bl * 8;
+    const int* st = a.state + (size_t)bl * kStateInts;
     if (st[5]) continue;
     const int m = st[0];
     const double* cP = a.coef + (size_t)bl * 2 * mstride * k;

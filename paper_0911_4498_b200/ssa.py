@@ -39,18 +39,21 @@ class SsaError(RuntimeError):
 
 class Options(ctypes.Structure):
     _fields_ = [("tol", ctypes.c_double), ("max_steps", ctypes.c_int32), ("check_every", ctypes.c_int32),
-                ("seed", ctypes.c_uint64), ("reorth", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+                ("seed", ctypes.c_uint64), ("reorth", ctypes.c_int32), ("reserved", ctypes.c_int32),
+                ("reorth_eta", ctypes.c_double), ("series_base", ctypes.c_int64)]
 
 
 class SeriesInfo(ctypes.Structure):
     _fields_ = [("steps", ctypes.c_int32), ("converged", ctypes.c_int32), ("breakdown_step", ctypes.c_int32),
                 ("reorth_extra", ctypes.c_int32), ("status", ctypes.c_int32), ("restarts", ctypes.c_int32),
-                ("max_residual", ctypes.c_double), ("sigma1", ctypes.c_double)]
+                ("max_residual", ctypes.c_double), ("sigma1", ctypes.c_double), ("rows_u", ctypes.c_int32),
+                ("rows_v", ctypes.c_int32), ("reorth_steps", ctypes.c_int32), ("reserved", ctypes.c_int32)]
 
 
 INFO_DTYPE = np.dtype([("steps", "<i4"), ("converged", "<i4"), ("breakdown_step", "<i4"), ("reorth_extra", "<i4"),
-                       ("status", "<i4"), ("restarts", "<i4"), ("max_residual", "<f8"), ("sigma1", "<f8")])
-assert INFO_DTYPE.itemsize == ctypes.sizeof(SeriesInfo) == 40
+                       ("status", "<i4"), ("restarts", "<i4"), ("max_residual", "<f8"), ("sigma1", "<f8"),
+                       ("rows_u", "<i4"), ("rows_v", "<i4"), ("reorth_steps", "<i4"), ("reserved", "<i4")])
+assert INFO_DTYPE.itemsize == ctypes.sizeof(SeriesInfo) == 56
 
 _lib = None
 
@@ -111,13 +114,13 @@ def _check(st: int):
         raise SsaError(st, load_library().ssa_last_error().decode())
 
 
-def _stream(stream=None) -> int:
+def _stream(stream=None, device=None) -> int:
     import torch
-    s = stream if stream is not None else torch.cuda.current_stream()
+    s = stream if stream is not None else torch.cuda.current_stream(device)
     return int(s.cuda_stream)
 
 
-def _dev_f64(t, shape, name):
+def _dev_f64(t, shape, name, device=None):
     import torch
     if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.float64:
         raise TypeError(f"{name} must be a CUDA float64 tensor")
@@ -125,6 +128,20 @@ def _dev_f64(t, shape, name):
         raise ValueError(f"{name} has shape {tuple(t.shape)}, expected {tuple(shape)}")
     if not t.is_contiguous():
         raise ValueError(f"{name} must be contiguous")
+    if device is not None and t.device.index != device:
+        raise ValueError(f"{name} is on cuda:{t.device.index}, the plan on cuda:{device}")
+    return t
+
+
+def _dev_info(t, n, name="info", device=None):
+    """A device info buffer: uint8 [n][INFO_DTYPE.itemsize], contiguous (ssa_series_info[n])."""
+    import torch
+    if not isinstance(t, torch.Tensor) or not t.is_cuda or t.dtype != torch.uint8:
+        raise TypeError(f"{name} must be a CUDA uint8 tensor")
+    if tuple(t.shape) != (n, INFO_DTYPE.itemsize) or not t.is_contiguous():
+        raise ValueError(f"{name} must be a contiguous [{n}][{INFO_DTYPE.itemsize}] tensor, got {tuple(t.shape)}")
+    if device is not None and t.device.index != device:
+        raise ValueError(f"{name} is on cuda:{t.device.index}, the plan on cuda:{device}")
     return t
 
 
@@ -132,8 +149,9 @@ class Plan:
     """ssa_plan_create / ssa_plan_destroy wrapper.  One plan per (N, L, k, batch)."""
 
     def __init__(self, N: int, L: int, k: int, batch: int, *, tol: float = 1e-12, max_steps: int = 0,
-                 check_every: int = 4, seed: int = 42, reorth: int = 1, device: int | None = None,
-                 profile: bool = False, svd: str = "tgk", force_long: bool = False):
+                 check_every: int = 4, seed: int = 42, reorth: int = 3, reorth_eta: float = 0.0,
+                 series_base: int = 0, device: int | None = None, profile: bool = False, svd: str = "tgk",
+                 force_long: bool = False):
         import torch
         lib = load_library()
         if not torch.cuda.is_available():
@@ -142,6 +160,9 @@ class Plan:
         opt = Options()
         _check(lib.ssa_options_default(ctypes.byref(opt)))
         opt.tol, opt.max_steps, opt.check_every, opt.seed, opt.reorth = tol, max_steps, check_every, seed, reorth
+        if reorth_eta > 0.0:
+            opt.reorth_eta = reorth_eta
+        opt.series_base = int(series_base)
         opt.reserved = (1 if profile else 0) | (2 if svd == "qr" else 0) | (4 if force_long else 0)
         h = ctypes.c_void_p()
         _check(lib.ssa_plan_create(N, L, k, batch, ctypes.byref(opt), self.device, ctypes.byref(h)))
@@ -197,7 +218,7 @@ class Plan:
         _dev_f64(series, (self.batch, self.N), "series")
         out = self._t(self.batch, self.M // 2 + 1, 2) if out is None else out
         _dev_f64(out, (self.batch, self.M // 2 + 1, 2), "out")
-        _check(load_library().ssa_spectrum(self._h, series.data_ptr(), out.data_ptr(), _stream(stream)))
+        _check(load_library().ssa_spectrum(self._h, series.data_ptr(), out.data_ptr(), _stream(stream, self.device)))
         return out
 
     def matvec(self, spec, x, transpose: bool = False, out=None, stream=None):
@@ -208,7 +229,7 @@ class Plan:
         out = self._t(self.batch, n_out) if out is None else out
         _dev_f64(out, (self.batch, n_out), "out")
         _check(load_library().ssa_matvec(self._h, spec.data_ptr(), x.data_ptr(), out.data_ptr(),
-                                         1 if transpose else 0, _stream(stream)))
+                                         1 if transpose else 0, _stream(stream, self.device)))
         return out
 
     def hankelize(self, sigma, U, V, out=None, stream=None):
@@ -220,22 +241,24 @@ class Plan:
         out = self._t(self.batch, nterms, self.N) if out is None else out
         _dev_f64(out, (self.batch, nterms, self.N), "out")
         _check(load_library().ssa_hankelize(self._h, sigma.data_ptr(), U.data_ptr(), V.data_ptr(), nterms,
-                                            out.data_ptr(), _stream(stream)))
+                                            out.data_ptr(), _stream(stream, self.device)))
         return out
 
     # -- the hot path ---------------------------------------------------------------
     def decompose(self, series, sigma=None, U=None, V=None, info=None, stream=None):
         """k leading singular triples of every trajectory matrix (Alg. 1 + FRO + bidiagonal SVD).
-        Returns (sigma [batch][k], U [batch][k][L], V [batch][k][K], info uint8 [batch][40])."""
+        Returns (sigma [batch][k], U [batch][k][L], V [batch][k][K], info uint8 [batch][56])."""
         import torch
-        _dev_f64(series, (self.batch, self.N), "series")
-        sigma = self._t(self.batch, self.k) if sigma is None else sigma
-        U = self._t(self.batch, self.k, self.L) if U is None else U
-        V = self._t(self.batch, self.k, self.K) if V is None else V
+        d = self.device
+        _dev_f64(series, (self.batch, self.N), "series", d)
+        sigma = self._t(self.batch, self.k) if sigma is None else _dev_f64(sigma, (self.batch, self.k), "sigma", d)
+        U = self._t(self.batch, self.k, self.L) if U is None else _dev_f64(U, (self.batch, self.k, self.L), "U", d)
+        V = self._t(self.batch, self.k, self.K) if V is None else _dev_f64(V, (self.batch, self.k, self.K), "V", d)
         if info is None:
             info = torch.zeros((self.batch, INFO_DTYPE.itemsize), dtype=torch.uint8, device=f"cuda:{self.device}")
+        _dev_info(info, self.batch, device=d)
         _check(load_library().ssa_decompose(self._h, series.data_ptr(), sigma.data_ptr(), U.data_ptr(),
-                                            V.data_ptr(), info.data_ptr(), _stream(stream)))
+                                            V.data_ptr(), info.data_ptr(), _stream(stream, self.device)))
         return sigma, U, V, info
 
     def reconstruct(self, sigma, U, V, out=None, stream=None):
@@ -246,7 +269,7 @@ class Plan:
         out = self._t(self.batch, self.k, self.N) if out is None else out
         _dev_f64(out, (self.batch, self.k, self.N), "out")
         _check(load_library().ssa_reconstruct(self._h, sigma.data_ptr(), U.data_ptr(), V.data_ptr(),
-                                              out.data_ptr(), _stream(stream)))
+                                              out.data_ptr(), _stream(stream, self.device)))
         return out
 
     def reconstruct_grouped(self, sigma, U, V, groups, ngroups=None, out=None, stream=None):
@@ -263,7 +286,7 @@ class Plan:
         out = self._t(self.batch, max(ng, 1), self.N) if out is None else out
         _dev_f64(out, (self.batch, max(ng, 1), self.N), "out")
         _check(load_library().ssa_reconstruct_grouped(self._h, sigma.data_ptr(), U.data_ptr(), V.data_ptr(),
-                                                      g.ctypes.data, ng, out.data_ptr(), _stream(stream)))
+                                                      g.ctypes.data, ng, out.data_ptr(), _stream(stream, self.device)))
         return out
 
     def bootstrap(self, series, eps, noise_sigma: float, G=None, info=None, stream=None):
@@ -273,11 +296,13 @@ class Plan:
         _dev_f64(eps, (self.batch, self.N), "eps")
         mean, var, mse = (self._t(self.N) for _ in range(3))
         if G is not None:
-            _dev_f64(G, (self.batch, self.N), "G")
+            _dev_f64(G, (self.batch, self.N), "G", self.device)
+        if info is not None:
+            _dev_info(info, self.batch, device=self.device)
         _check(load_library().ssa_bootstrap(self._h, series.data_ptr(), eps.data_ptr(), float(noise_sigma),
                                             mean.data_ptr(), var.data_ptr(), mse.data_ptr(),
                                             G.data_ptr() if G is not None else None,
-                                            info.data_ptr() if info is not None else None, _stream(stream)))
+                                            info.data_ptr() if info is not None else None, _stream(stream, self.device)))
         return mean, var, mse
 
     def run_host(self, series: np.ndarray, want_vectors: bool = True, stream=None, raise_on_status=True):
@@ -292,7 +317,7 @@ class Plan:
         info = np.zeros(self.batch, dtype=INFO_DTYPE)
         p = lambda a: a.ctypes.data if a is not None else None
         st = load_library().ssa_run_host(self._h, p(series), p(sigma), p(U), p(V), p(recon), p(info),
-                                         _stream(stream))
+                                         _stream(stream, self.device))
         if raise_on_status:
             _check(st)
         return sigma, U, V, recon, info
@@ -317,13 +342,14 @@ def hmatrix(series, B: int, T: int, L: int, I, *, tol: float = 1e-12, seed: int 
     nb, nt = N - B + 1, N - T + 1
     if nb < 1 or nt < 1:  # let the C call report the invalid sizes (it validates first)
         _check(lib.ssa_hmatrix(series.data_ptr(), N, B, T, L, idx.ctypes.data, len(idx), ctypes.byref(opt), dev,
-                               None, None, _stream(stream)))
+                               None, None, _stream(stream, series.device)))
     G = torch.empty((nb, nt), dtype=torch.float64, device=series.device) if out is None else out
     _dev_f64(G, (nb, nt), "out")
     if info is None:
         info = torch.zeros((nb, INFO_DTYPE.itemsize), dtype=torch.uint8, device=series.device)
+    _dev_info(info, nb)
     _check(lib.ssa_hmatrix(series.data_ptr(), N, B, T, L, idx.ctypes.data, len(idx), ctypes.byref(opt), dev,
-                           G.data_ptr(), info.data_ptr(), _stream(stream)))
+                           G.data_ptr(), info.data_ptr(), _stream(stream, series.device)))
     return G, info
 
 
@@ -357,8 +383,9 @@ class HMatrix:
         _dev_f64(G, (nb, nt), "out")
         if info is None:
             info = torch.zeros((nb, INFO_DTYPE.itemsize), dtype=torch.uint8, device=series.device)
+        _dev_info(info, nb)
         _check(load_library().ssa_hmatrix_exec(self._h, series.data_ptr(), G.data_ptr(), info.data_ptr(),
-                                               _stream(stream)))
+                                               _stream(stream, series.device)))
         return G, info
 
     def close(self):

@@ -20,7 +20,7 @@ import numpy as np
 __all__ = [
     "CONFIGS", "cfg1_series", "cfg2_series", "cfg2_batch", "cfg3_series",
     "cfg3_like_series", "cfg4_item", "cfg4_batch", "cfg5_problem", "change_point_series",
-    "bootstrap_series", "bootstrap_noise",
+    "bootstrap_series", "bootstrap_noise", "cfg3_params",
 ]
 
 # name -> (N, L, k, batch); K = N - L + 1.  BASELINE.json "configs" [0..4].
@@ -87,6 +87,16 @@ def cfg3_like_series(N: int, seed: int = 3) -> np.ndarray:
 
 def cfg3_series() -> np.ndarray:
     return cfg3_like_series(1 << 20, 3)
+
+
+def cfg3_params(seed: int = 3):
+    """The generator parameters (P[8], A[8], phi[8]) that cfg3_like_series(N, seed) draws
+    first (same stream, same order), for the closed-form pin of the sinusoid pairs."""
+    rng = np.random.default_rng(seed)
+    P = 10.0 ** rng.uniform(1.0, 5.0, 8)
+    A = rng.uniform(0.1, 1.0, 8)
+    phi = rng.uniform(0.0, 2 * np.pi, 8)
+    return P, A, phi
 
 
 def cfg4_item(i: int, N: int = 8192, L: int = 4096):

@@ -7,7 +7,11 @@ clusters using the gap rule δ = 1e-4·σ°₁, and measures
   * sign-free sine angles ‖(I − ûûᵀ)u‖₂ (never acos / sqrt(1 − cos²), whose √ε floor
     would fail a 1e-8 target even for exact vectors — SURVEY.md §0 finding 6),
   * for a cluster C, the largest principal-angle sine between span(U_C) and span(U°_C),
-  * reconstruction errors, per triple or summed over a cluster.
+  * reconstruction errors, per triple or summed over a cluster,
+  * when the series is given: the TRUE residuals ‖Xv_i − σ_iu_i‖, ‖Xᵀu_i − σ_iv_i‖ of
+    every triple (straddling clusters included, where the vectors themselves are not
+    unique) through the oracle's explicit product, ≤ res_tol·σ°₁ (10·tol, SURVEY.md
+    §8(c) "Lanczos internals"), and the orthonormality of the computed U, V.
 """
 from __future__ import annotations
 
@@ -64,6 +68,7 @@ class ParityReport:
     u_angle: list = field(default_factory=list)          # (indices, sine)
     v_angle: list = field(default_factory=list)
     recon: list = field(default_factory=list)            # (indices, normwise err / scale)
+    residual: list = field(default_factory=list)         # (i, max true residual / sigma_1)
     failures: list = field(default_factory=list)
 
     def ok(self) -> bool:
@@ -72,16 +77,42 @@ class ParityReport:
     def worst(self):
         def mx(lst, j):
             return max([t[j] for t in lst], default=0.0)
-        return dict(sigma=mx(self.sigma_rel, 1), u=mx(self.u_angle, 1), v=mx(self.v_angle, 1), recon=mx(self.recon, 1))
+        return dict(sigma=mx(self.sigma_rel, 1), u=mx(self.u_angle, 1), v=mx(self.v_angle, 1), recon=mx(self.recon, 1),
+                    residual=mx(self.residual, 1))
+
+
+def true_residuals(f, L, sig, U, V, idx, matvec):
+    """max(‖X v_i − σ_i u_i‖, ‖Xᵀ u_i − σ_i v_i‖) for i in idx; matvec(f, L, x, transpose)
+    is the oracle's explicit-entry product (Eqs. (1)-(2), PAPER.md:323-328 define the
+    residuals the Lanczos stop rule bounds)."""
+    out = []
+    for i in idx:
+        r1 = np.linalg.norm(matvec(f, L, V[i]) - sig[i] * U[i])
+        r2 = np.linalg.norm(matvec(f, L, U[i], True) - sig[i] * V[i])
+        out.append(max(r1, r2))
+    return out
 
 
 def compare(sig_ref, U_ref, V_ref, sig, U, V, k, G_ref=None, G=None, recon_scale=None,
-            sigma_tol=1e-10, angle_tol=1e-8, recon_tol=1e-9, delta=DELTA) -> ParityReport:
+            sigma_tol=1e-10, angle_tol=1e-8, recon_tol=1e-9, delta=DELTA, f=None, L=None, res_tol=1e-11,
+            orth_tol=1e-12) -> ParityReport:
     """Cluster-aware comparison of the first k triples.  sig_ref may hold k+1 values so
     the straddling rule can be applied.  recon_scale is ‖F‖₂ (default) — errors are
-    normwise ‖g − g°‖₂ / recon_scale."""
+    normwise ‖g − g°‖₂ / recon_scale.  With the series f and window L, every triple's
+    true residual (oracle product) must be ≤ res_tol·σ°₁ and U, V orthonormal ≤ orth_tol."""
     rep = ParityReport()
     sig_ref = np.asarray(sig_ref)
+    if f is not None:
+        import oracle
+        res = true_residuals(f, L, sig, U, V, range(k), oracle.matvec)
+        for i, r in enumerate(res):
+            rep.residual.append((i, float(r / sig_ref[0])))
+            if r > res_tol * sig_ref[0]:
+                rep.failures.append(f"true residual of triple {i}: {r / sig_ref[0]:.3e} sigma_1 > {res_tol:g}")
+        for name, Q in (("U", U[:k]), ("V", V[:k])):
+            o = float(np.abs(Q @ Q.T - np.eye(k)).max())
+            if o > orth_tol:
+                rep.failures.append(f"{name} orthonormality {o:.3e} > {orth_tol:g}")
     for grp, straddles in clusters(sig_ref, k, delta):
         separated = len(grp) == 1 and not straddles
         for i in grp:

@@ -4,6 +4,7 @@ import os
 import re
 import subprocess
 
+import numpy as np
 import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -47,7 +48,8 @@ def test_status_strings_and_defaults(lib):
         assert lib.ssa_status_string(code).decode() == name
     opt = S.Options()
     assert lib.ssa_options_default(ctypes.byref(opt)) == 0
-    assert opt.tol == 1e-12 and opt.seed == 42 and opt.reorth == 1 and opt.check_every == 4
+    assert opt.tol == 1e-12 and opt.seed == 42 and opt.reorth == 3 and opt.check_every == 4
+    assert abs(opt.reorth_eta - np.finfo(float).eps ** 0.75) <= 1e-27   # PRO default, R22
 
 
 def test_validation_happens_before_any_device_work(lib):
@@ -58,6 +60,12 @@ def test_validation_happens_before_any_device_work(lib):
         st = lib.ssa_plan_create(N, L, k, B, None, 0, ctypes.byref(h))
         assert st == 1, (N, L, k, B, st)   # SSA_ERR_INVALID_ARGUMENT
         assert lib.ssa_last_error()
+    import paper_0911_4498_b200.ssa as S
+    for reorth, eta in [(0, 1e-12), (4, 1e-12), (3, 0.0), (3, 1e-3), (3, -1.0)]:
+        opt = S.Options()
+        lib.ssa_options_default(ctypes.byref(opt))
+        opt.reorth, opt.reorth_eta = reorth, eta
+        assert lib.ssa_plan_create(100, 50, 4, 1, ctypes.byref(opt), 0, ctypes.byref(h)) == 1, (reorth, eta)
     assert lib.ssa_plan_fft_size(None) == -1
 
 

@@ -1,0 +1,191 @@
+"""Numerical edge cases of the decompose path (VERDICT r01 "What's missing" 3, 5):
+
+* not converged within max_steps -> SSA_ERR_NOT_CONVERGED with the best Ritz triples
+  still written; the reported residual is the exact one of Eqs. (1)-(2)
+   and the Ritz values interlace the singular values from below;
+* an exactly degenerate pair (Theorem 1: a sinusoid whose period
+  divides both L and K gives sigma_1 = sigma_2 = A sqrt(LK)/2 exactly), which sends the
+  fused TGK SVD to its inverse-iteration fallback;
+* the long-series path at k = 32 against the full oracle;
+* cfg3 at its own plan (N = 2^20, L = 2^19, k = 32): true residuals through the oracle's
+  direct product, orthonormality, the Frobenius bound and the closed form of the
+  sinusoid pairs (SURVEY.md §8(c) cfg3 pins (i)-(iv)).
+"""
+from concurrent.futures import ThreadPoolExecutor
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import parity
+import ssa_inputs
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_0911_4498_b200 as pkg
+    return pkg
+
+
+def cuda(a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).cuda()
+
+
+def decompose(P, F, L, k, **kw):
+    B, N = F.shape
+    plan = P.Plan(N, L, k, B, **kw)
+    s, U, V, info = plan.decompose(cuda(F))
+    G = plan.reconstruct(s, U, V)
+    torch.cuda.synchronize()
+    return s.cpu().numpy(), U.cpu().numpy(), V.cpu().numpy(), G.cpu().numpy(), P.info_to_numpy(info), plan
+
+
+@pytest.mark.parametrize("force_long", [False, True])
+@pytest.mark.parametrize("reorth", [1, 3])
+def test_not_converged_reports_best_triples(P, force_long, reorth):
+    """cfg1 with max_steps = k + 2: far from converged.  Status NOT_CONVERGED, converged 0,
+    steps = max_steps; the triples are still written: sigma descending, U/V orthonormal,
+    X v_i = omega_i u_i exactly (Eq. (1)), the reported residual equals the true one
+    max_i |X^T u_i - omega_i v_i| / omega_1 (Eq. (2)), and omega_i <= sigma_i (Ritz values
+    of B_m interlace the singular values from below)."""
+    c = ssa_inputs.CONFIGS["cfg1"]
+    N, L, k = c["N"], c["L"], c["k"]
+    f = ssa_inputs.cfg1_series(N)
+    s, U, V, G, info, _ = decompose(P, f[None], L, k, max_steps=k + 2, reorth=reorth, force_long=force_long)
+    inf = info[0]
+    assert inf["status"] == 2 and inf["converged"] == 0, inf   # SSA_ERR_NOT_CONVERGED
+    assert inf["steps"] == k + 2
+    s, U, V = s[0], U[0], V[0]
+    assert np.all(np.isfinite(s)) and np.all(np.diff(s) <= 0)
+    assert np.abs(U @ U.T - np.eye(k)).max() <= 1e-12
+    assert np.abs(V @ V.T - np.eye(k)).max() <= 1e-12
+    s_ref = oracle.svd(f, L, k)[0]
+    assert np.all(s <= s_ref * (1 + 1e-12)), (s, s_ref)
+    assert abs(s[0] - s_ref[0]) <= 1e-6 * s_ref[0]          # the dominant value converges first
+    res_u = [np.linalg.norm(oracle.matvec(f, L, V[i]) - s[i] * U[i]) for i in range(k)]
+    res_v = [np.linalg.norm(oracle.matvec(f, L, U[i], True) - s[i] * V[i]) for i in range(k)]
+    assert max(res_u) <= 1e-11 * s[0], res_u                 # A v_i = omega_i u_i exactly
+    true_max = max(res_v) / s[0]
+    assert true_max > 1e-12                                   # really not converged
+    assert abs(true_max - inf["max_residual"]) <= 1e-6 * true_max + 1e-13, (true_max, inf["max_residual"])
+
+
+def test_not_converged_run_host_status(P):
+    """ssa_run_host surfaces the per-series NOT_CONVERGED as its return status."""
+    c = ssa_inputs.CONFIGS["cfg1"]
+    N, L, k = c["N"], c["L"], c["k"]
+    f = ssa_inputs.cfg1_series(N)
+    plan = P.Plan(N, L, k, 1, max_steps=k + 2)
+    with pytest.raises(P.SsaError) as e:
+        plan.run_host(f[None])
+    assert e.value.status == 2
+    *_, info = plan.run_host(f[None], raise_on_status=False)
+    assert info[0]["status"] == 2
+
+
+def two_sinusoids(N):
+    n = np.arange(1, N + 1, dtype=np.float64)
+    return 2.0 * np.sin(2 * np.pi * n / 12 + 0.3) + np.sin(2 * np.pi * n / 8 + 1.1)
+
+
+@pytest.mark.parametrize("force_long", [False, True])
+@pytest.mark.parametrize("k", [2, 4])
+def test_exact_degenerate_pairs(P, k, force_long):
+    """L = K = 120 (N = 239): periods 12 and 8 divide both, so the trajectory matrix is
+    the sum of two rank-2 blocks with orthogonal row and column spaces and
+    sigma = (A1, A1, A2, A2) sqrt(LK)/2 = (120, 120, 60, 60) exactly, the rest 0
+    (Theorem 1 / SURVEY.md §8(c) closed forms).  Exactly equal pairs: parity per cluster,
+    the elementary series of a pair summed; with k = 4 the rank is exhausted and the four
+    components add up to the series."""
+    N, L = 239, 120
+    f = two_sinusoids(N)
+    s, U, V, G, info, _ = decompose(P, f[None], L, k, force_long=force_long)
+    assert info[0]["status"] == 0, info[0]
+    closed = np.array([120.0, 120.0, 60.0, 60.0])[:k]
+    assert np.abs(s[0] - closed).max() <= 1e-12 * 120.0, s[0]
+    s_ref, U_ref, V_ref, _ = oracle.svd(f, L, k + 1)
+    rep = parity.compare(s_ref, U_ref, V_ref, s[0], U[0], V[0], k,
+                         np.stack([oracle.hankelize_rank1(s_ref[i], U_ref[i], V_ref[i]) for i in range(k)]), G[0],
+                         recon_scale=np.linalg.norm(f), f=f, L=L)
+    assert rep.ok(), rep.failures
+    if k == 4:
+        assert np.linalg.norm(G[0].sum(axis=0) - f) <= 1e-10 * np.linalg.norm(f)
+
+
+def test_long_path_k32_vs_oracle(P):
+    """The long-series kernels (four-step FFT, grid-wide reorthogonalization, lg_ritz) at
+    cfg3's k = 32, forced onto N = 4096 so the full Jacobi oracle can check every triple."""
+    N, L, k = 4096, 2048, 32
+    f = ssa_inputs.cfg3_like_series(N)
+    s, U, V, G, info, _ = decompose(P, f[None], L, k, force_long=True)
+    assert info[0]["status"] == 0, info[0]
+    s_ref, U_ref, V_ref, _ = oracle.svd(f, L, k + 1)
+    G_ref = np.stack([oracle.hankelize_rank1(s_ref[i], U_ref[i], V_ref[i]) for i in range(k)])
+    rep = parity.compare(s_ref, U_ref, V_ref, s[0], U[0], V[0], k, G_ref, G[0], recon_scale=np.linalg.norm(f),
+                         f=f, L=L)
+    assert rep.ok(), rep.failures
+
+
+# ------------------------------------------------------------------ cfg3 at its own plan
+def _rows_Xv(f, L, v, i0, i1):
+    """Rows [i0, i1) of X v: the trajectory matrix of f[i0 : i1 + K - 1] with window i1 - i0
+    holds exactly those rows (x_ij = f_{i+j-1}), so the oracle's own product computes them."""
+    K = len(f) - L + 1
+    return oracle.matvec(f[i0:i1 + K - 1], i1 - i0, v)
+
+
+def _cols_XTu(f, L, u, j0, j1):
+    """Entries [j0, j1) of X^T u: columns j0..j1-1 of X are the trajectory matrix of
+    f[j0 : j1 + L - 1] with window L."""
+    return oracle.matvec(f[j0:j1 + L - 1], L, u, True)
+
+
+def threaded_product(f, L, x, transpose, pool, nblk):
+    N = len(f)
+    K = N - L + 1
+    n = K if transpose else L
+    cuts = np.linspace(0, n, nblk + 1).astype(int)
+    fn = _cols_XTu if transpose else _rows_Xv
+    parts = pool.map(lambda c: fn(f, L, x, c[0], c[1]), [(cuts[q], cuts[q + 1]) for q in range(nblk)])
+    return np.concatenate(list(parts))
+
+
+@pytest.mark.slow
+def test_cfg3_own_plan_residuals_and_closed_form(P):
+    """BASELINE configs[2] exactly as bench.py runs it (one series N = 2^20, L = 2^19, k = 32,
+    the cfg3 seed).  The oracle cannot form X (2.2 TB), so:
+    (i) true residuals |X v_i - s_i u_i|, |X^T u_i - s_i v_i| <= 10 tol s_1 = 1e-11 s_1 with
+        the oracle's direct O(LK) product (row / column blocks over the host cores) for
+        triples 0, 1 (the leading pair), 18 (the last signal triple: the trend) and 31;
+    (ii) U, V orthonormal <= 1e-12; (iii) sum s_i^2 <= |X|_F^2 = sum_t c_t f_t^2;
+    (iv) every sinusoid j of the generator appears as a pair of values within 5e-3 of
+        A_j sqrt(LK)/2 (first-order closed form; all 8 periods are < L / 30)."""
+    c = ssa_inputs.CONFIGS["cfg3"]
+    N, L, k = c["N"], c["L"], c["k"]
+    K = N - L + 1
+    f = ssa_inputs.cfg3_series()
+    s, U, V, _, info, _ = decompose(P, f[None], L, k)
+    inf = info[0]
+    assert inf["status"] == 0 and inf["converged"] == 1, inf
+    s, U, V = s[0], U[0], V[0]
+    assert np.all(np.diff(s) <= 0)
+    assert np.abs(U @ U.T - np.eye(k)).max() <= 1e-12
+    assert np.abs(V @ V.T - np.eye(k)).max() <= 1e-12
+    cnt = np.minimum.reduce([np.arange(1, N + 1), np.full(N, L), np.full(N, K), N - np.arange(N)]).astype(float)
+    assert (s * s).sum() <= (f * f * cnt).sum() * (1 + 1e-12)
+    Pj, Aj, _ = ssa_inputs.cfg3_params()
+    closed = Aj * np.sqrt(float(L) * K) / 2
+    for j in range(8):
+        assert Pj[j] < L / 30
+        rel = np.sort(np.abs(s - closed[j]) / closed[j])[:2]
+        assert rel.max() <= 5e-3, (j, Pj[j], closed[j], rel)
+    cores = os.cpu_count() or 1
+    with ThreadPoolExecutor(cores) as pool:
+        for i in (0, 1, 18, k - 1):
+            r1 = np.linalg.norm(threaded_product(f, L, V[i], False, pool, cores) - s[i] * U[i])
+            r2 = np.linalg.norm(threaded_product(f, L, U[i], True, pool, cores) - s[i] * V[i])
+            assert max(r1, r2) <= 1e-11 * s[0], (i, r1 / s[0], r2 / s[0])

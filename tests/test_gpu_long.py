@@ -125,7 +125,7 @@ def test_long_decompose_vs_oracle(P, N, L, k):
     s_ref, U_ref, V_ref, _ = oracle.svd(f, L, k + 1)
     G_ref = np.stack([oracle.hankelize_rank1(s_ref[i], U_ref[i], V_ref[i]) for i in range(k)])
     rep = parity.compare(s_ref, U_ref, V_ref, sigma.cpu().numpy()[0], U.cpu().numpy()[0], V.cpu().numpy()[0], k,
-                         G_ref, G.cpu().numpy()[0], recon_scale=np.linalg.norm(f))
+                         G_ref, G.cpu().numpy()[0], recon_scale=np.linalg.norm(f), f=f, L=L)
     assert rep.ok(), rep.failures
 
 
@@ -169,4 +169,4 @@ def test_cfg3_like_long_series_residuals(P):
     for i in (0, 1, k - 1):
         r1 = np.linalg.norm(oracle.matvec(f, L, Vh[i]) - s[i] * Uh[i])
         r2 = np.linalg.norm(oracle.matvec(f, L, Uh[i], True) - s[i] * Vh[i])
-        assert max(r1, r2) <= 1e-10 * s[0], (i, r1, r2)
+        assert max(r1, r2) <= 1e-11 * s[0], (i, r1, r2)   # 10 tol sigma_1
