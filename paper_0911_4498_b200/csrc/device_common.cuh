@@ -22,6 +22,13 @@ namespace ssa {
 // implicit trigger at completion still removes the launch gap.)
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
+// PDL attribute switch (a graph build falls back to plain launches if the driver rejects
+// programmatic edges inside conditional-node bodies)
+inline bool& pdl_enabled() {
+  static thread_local bool on = true;
+  return on;
+}
+
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                               Args&&... args) {
@@ -34,7 +41,7 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
@@ -317,6 +324,17 @@ __device__ __forceinline__ void stream_rows(const double* base_w, int ld, int nb
 }
 
 __host__ __device__ inline size_t align16(size_t x) { return (x + 15) & ~(size_t)15; }
+
+// 1/c for an integer count c >= 1 (the antidiagonal counts of Alg. 4, R2) to
+// within an ulp: float reciprocal, two Newton steps in fp64 -- no fp64 division (a long
+// instruction sequence with a slow path) in the Hankelization epilogues.
+__device__ __forceinline__ double rcp_count_f64(int c) {
+  const double cd = (double)c;
+  double r = (double)__frcp_rn((float)c);
+  r = fma(r, fma(-cd, r, 1.0), r);
+  r = fma(r, fma(-cd, r, 1.0), r);
+  return r;
+}
 
 // Copy the two-level twiddle table of size M (global, lo then hi) into shared memory
 // (all threads; caller synchronizes).

@@ -118,7 +118,9 @@ static void free_plan(Plan& p) {
   void* ptrs[] = {p.d_tw, p.d_twl, p.d_spec, p.d_U, p.d_V, p.d_ab, p.d_state, p.d_tgk, p.d_rot, p.d_vecs, p.d_coef,
                   p.d_info, p.d_counters, p.d_hscratch, p.d_prof, p.d_tgkw, p.d_tw1, p.d_tw2, p.d_tw4, p.d_twp, p.d_lbuf,
                   p.d_lgsc, p.d_lgpart, p.d_lgh, p.d_lgr, p.d_series, p.d_sigma, p.d_Uout, p.d_Vout,
-                  p.d_recon, p.d_elem, p.d_bs};
+                  p.d_recon, p.d_elem, p.d_bs, p.d_lgom, p.d_ucur, p.d_vcur};
+  if (p.lg_exec) cudaGraphExecDestroy(p.lg_exec);
+  if (p.lg_graph) cudaGraphDestroy(p.lg_graph);
   for (void* q : ptrs)
     if (q) cudaFree(q);
   for (int i = 0; i < 2 * Plan::kPhases; ++i)
@@ -238,6 +240,9 @@ static ssa_status create_large_workspace(Plan& p) {
   if ((st = alloc((void**)&p.d_lgpart, npart * 8, "partials")) != SSA_OK) return st;
   if ((st = alloc((void**)&p.d_lgh, (size_t)(p.m_max + 2 + 64) * 8, "reorth coefficients")) != SSA_OK) return st;
   if ((st = alloc((void**)&p.d_lgr, (size_t)std::max(p.ldL, p.ldK) * 8, "work vector")) != SSA_OK) return st;
+  if ((st = alloc((void**)&p.d_lgom, (size_t)2 * (p.m_max + 4) * 8, "PRO estimates")) != SSA_OK) return st;
+  if ((st = alloc((void**)&p.d_ucur, (size_t)p.ldL * 8, "current u")) != SSA_OK) return st;
+  if ((st = alloc((void**)&p.d_vcur, (size_t)p.ldK * 8, "current v")) != SSA_OK) return st;
   return SSA_OK;
 }
 

@@ -186,7 +186,7 @@ __device__ __forceinline__ void hankelize_body(double2* bufA, double2* bufB, con
       int c = k1;
       if (c > mn) c = mn;
       if (N - k1 + 1 < c) c = N - k1 + 1;
-      g[t] = ((t & 1) ? z.y : z.x) * scale / (double)c;
+      g[t] = ((t & 1) ? z.y : z.x) * (scale * rcp_count_f64(c));
     }
   }
 }
@@ -261,7 +261,7 @@ __device__ __forceinline__ void group_body(double2* bufA, double2* bufB, double2
     int c = k1;
     if (c > mn) c = mn;
     if (N - k1 + 1 < c) c = N - k1 + 1;
-    o[t] = ((t & 1) ? z.y : z.x) * invH / (double)c;
+    o[t] = ((t & 1) ? z.y : z.x) * (invH * rcp_count_f64(c));
   }
 }
 

@@ -13,7 +13,9 @@ constexpr int kWarps = kThreads / 32;  // warps per CTA
 constexpr int kStages = 3;             // TMA ring depth per warp (basis streaming)
 constexpr int kMaxSmemH = 8192;        // largest H = M/2 held in one CTA's shared memory
 constexpr int kMaxHankelSmemH = 4096;  // largest H with both hankelization buffers in SMEM
-constexpr int kMaxK = 32;              // largest k of the batched decompose
+constexpr int kMaxK = 128;             // largest k (2k <= kThreads: two lanes per value in tgk.cuh)
+constexpr int kClCount = kMaxK + 1;    // tgk_clusters: index of the cluster count in cl[]
+constexpr int kClInts = kMaxK + 2;     // ints of a cl[] array
 constexpr int kStateInts = 12;         // per-series state words (DecomposeArgs::state)
 
 inline size_t fft_bytes(int H) { return (size_t)H * 16; }
@@ -85,6 +87,12 @@ struct Plan {
   double* d_lgpart = nullptr;    // partial sums
   double* d_lgh = nullptr;       // reorth coefficients
   double* d_lgr = nullptr;       // work vector
+  double* d_lgom = nullptr;      // PRO omega estimates [2][m_max+4] (mu, nu)
+  double* d_ucur = nullptr;      // current u_j / v_j of the long-series loop (fixed graph arguments)
+  double* d_vcur = nullptr;
+  cudaGraph_t lg_graph = nullptr;       // the long-series Lanczos loop (WHILE / IF graph)
+  cudaGraphExec_t lg_exec = nullptr;
+  bool lg_pdl = false;                  // the graph's kernels use programmatic dependent launch
   int rot_cap = 0;
   size_t smem_lanczos = 0, smem_ritz = 0;
   double2* d_tw = nullptr;     // twiddles exp(-2 pi i t / M), t < H (long-series path)

@@ -29,8 +29,8 @@ struct LSmem {
   double* nu;              // m_max + 3: PRO estimates of v_{j}^T v_i
   double* red;             // 32
   int* redi;               // 8 ints
-  int* cl;                 // 40 ints: cluster starts of the final SVD (tgk_clusters)
-  double* chk;             // 4 * kMaxK: omega, res, lohi(2k)
+  int* cl;                 // kClInts ints: cluster starts of the final SVD (tgk_clusters)
+  double* chk;             // 4 k: omega, res, lohi(2k)
   double2* tw;             // two-level twiddle table for M (tw2_entries(M))
   uint64_t* bars;          // kWarps * kStages
 };
@@ -47,11 +47,10 @@ __host__ __device__ inline size_t lanczos_regionA_bytes(int H, int ldL, int ldK,
 }
 
 size_t lanczos_smem_bytes(int H, int ldL, int ldK, int m_max, int k) {
-  (void)k;
   size_t s = lanczos_regionA_bytes(H, ldL, ldK, m_max);
   s += align16((size_t)ldL * 8) + align16((size_t)ldK * 8);
   s += 5 * align16((size_t)(m_max + 3) * 8);
-  s += 32 * 8 + 8 * 4 + 40 * 4 + 4 * kMaxK * 8;
+  s += 32 * 8 + 8 * 4 + align16((size_t)kClInts * 4) + (size_t)4 * k * 8;
   s += (size_t)tw2_entries(2 * H) * 16;
   s += (size_t)kWarps * kStages * 8;
   return align16(s) + 16;
@@ -71,8 +70,8 @@ __device__ inline LSmem carve(unsigned char* base, const DecomposeArgs& a) {
   s.nu = reinterpret_cast<double*>(base + off); off += align16((size_t)(a.m_max + 3) * 8);
   s.red = reinterpret_cast<double*>(base + off); off += 32 * 8;
   s.redi = reinterpret_cast<int*>(base + off); off += 8 * 4;
-  s.cl = reinterpret_cast<int*>(base + off); off += 40 * 4;
-  s.chk = reinterpret_cast<double*>(base + off); off += 4 * kMaxK * 8;
+  s.cl = reinterpret_cast<int*>(base + off); off += align16((size_t)kClInts * 4);
+  s.chk = reinterpret_cast<double*>(base + off); off += (size_t)4 * a.k * 8;
   s.tw = reinterpret_cast<double2*>(base + off); off += (size_t)tw2_entries(2 * a.H) * 16;
   s.bars = reinterpret_cast<uint64_t*>(base + off);
   return s;
@@ -461,8 +460,8 @@ __global__ void __launch_bounds__(kThreads, 2) lanczos_kernel(const DecomposeArg
         }
         __syncthreads();
         double* om = sm.chk;
-        double* res = om + kMaxK;
-        double* lohi = res + kMaxK;
+        double* res = om + k;
+        double* lohi = res + k;
         // pivots of the twisted factorizations: shared memory when they fit in region A
         double* tc2n = tc2 + (2 * a.m_max + 2);
         // pivots of the twisted factorizations in shared memory (region A after the
@@ -565,8 +564,8 @@ __global__ void __launch_bounds__(kThreads, 2) lanczos_kernel(const DecomposeArg
       }
       __syncthreads();
       double* om = sm.chk;
-      double* res = om + kMaxK;
-      double* lohi = res + kMaxK;
+      double* res = om + k;
+      double* lohi = res + k;
       double* tc2n = tc2 + (2 * a.m_max + 2);
       double* dsc = tc2n + (2 * a.m_max + 2);
       const int kg = tgk_group(a, n);

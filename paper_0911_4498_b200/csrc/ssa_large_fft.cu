@@ -189,7 +189,7 @@ template <int LOGH>
 __global__ void __launch_bounds__(kThreads, (LOGH >= 19) ? 1 : 3) lg_col_inv(const double2* __restrict__ Y, const double2* __restrict__ T1,
                                                        ColInvArgs a) {
   pdl_wait();
-  if (ca.gate && *ca.gate) return;
+  if (a.gate && *a.gate) return;
   using G = Geo<LOGH>;
   constexpr int N1 = G::N1, N2 = G::N2, CS = N1 + 1;
   constexpr int NE = (N1 * kColW + kThreads - 1) / kThreads;

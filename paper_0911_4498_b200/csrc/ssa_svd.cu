@@ -212,7 +212,7 @@ __global__ void __launch_bounds__(kThreads) bidiag_svd_tgk_kernel(const Decompos
       // to O(eps |T| / gap): re-orthonormalize each half (one warp per cluster)
       {
         const int w = tid >> 5, nw = blockDim.x >> 5;
-        for (int q = w; q < cl[33]; q += nw) {
+        for (int q = w; q < cl[kClCount]; q += nw) {
           if (cl[q + 1] - cl[q] < 2) continue;
           warp_mgs_cols(cP, m + 1, k, 1, cl[q], cl[q + 1]);
           warp_mgs_cols(cQ, m, k, 1, cl[q], cl[q + 1]);
@@ -248,7 +248,7 @@ __global__ void __launch_bounds__(kThreads) bidiag_svd_tgk_kernel(const Decompos
 }
 
 size_t tgk_svd_smem_bytes(int m_max) {
-  return (size_t)(3 * (2 * m_max + 1) + 2 * kMaxK + kMaxK + 2 * kMaxK) * 8 + 40 * 4 + 16;
+  return (size_t)(3 * (2 * m_max + 1) + 2 * kMaxK + kMaxK + 2 * kMaxK) * 8 + kClInts * 4 + 16;
 }
 
 // Ritz rings: kRitzStages chunks of at most 32 E = 64 columns (512 B) per warp in flight

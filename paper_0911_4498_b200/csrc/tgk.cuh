@@ -250,7 +250,7 @@ __device__ inline void tgk_check(const double* c, const double* c2, double* c2n,
 // Clusters of the k values (descending): maximal runs with lam[j-1] - lam[j] <=
 // 1e-3 |T| (LAPACK dstein's ORTOL: outside a cluster independently computed vectors are
 // orthogonal to O(eps |T| / gap) <= 2e-13).  cl[0..nc] = starts (cl[nc] = k),
-// cl[33] = nc.  Returns 1 if some gap inside a cluster is below 1e-11 |T| or a value is
+// cl[kClCount] = nc.  Returns 1 if some gap inside a cluster is below 1e-11 |T| or a value is
 // below 1e-11 |T| (near the eigenvalue 0 that TGK of odd order always has): such
 // near-degenerate values need inverse iteration with orthogonalization (tgk_vectors).
 // Thread 0 only.
@@ -263,7 +263,7 @@ __device__ inline int tgk_clusters(const double* lam, int k, double tnorm, int* 
     if (!(lam[j] > degen)) bad = 1;
   }
   cl[nc] = k;
-  cl[33] = nc;
+  cl[kClCount] = nc;
   return bad;
 }
 
@@ -397,7 +397,7 @@ __device__ inline int tgk_final(const double* c, const double* c2, double* c2n, 
   // (2m+1) k doubles, free now that the pivots are done) the columns are copied in, worked
   // on there and copied back
   {
-    const int nc = cl[33];
+    const int nc = cl[kClCount];
     bool any = false;
     for (int q = 0; q < nc; ++q) any |= (cl[q + 1] - cl[q] > 1);
     if (any) {

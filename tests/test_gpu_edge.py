@@ -189,3 +189,21 @@ def test_cfg3_own_plan_residuals_and_closed_form(P):
             r1 = np.linalg.norm(threaded_product(f, L, V[i], False, pool, cores) - s[i] * U[i])
             r2 = np.linalg.norm(threaded_product(f, L, U[i], True, pool, cores) - s[i] * V[i])
             assert max(r1, r2) <= 1e-11 * s[0], (i, r1 / s[0], r2 / s[0])
+
+
+@pytest.mark.parametrize("force_long", [False, True])
+@pytest.mark.parametrize("N,L,k", [(1200, 600, 50), (1000, 500, 100)])
+def test_decompose_k_beyond_32(P, N, L, k, force_long):
+    """k up to 128 (the paper decomposes 50 and 100 leading triples, PAPER.md:1101-1105,
+    1127-1128): the batched kernel (k-sized shared-memory arrays, two TGK lanes per value
+    for 2k <= 256 threads) and the long path (lg_ritz in blocks of 32 triples) against the
+    full oracle, cluster-aware, with every triple's true residual."""
+    f = ssa_inputs.cfg3_like_series(N, 11)
+    s, U, V, G, info, plan = decompose(P, f[None], L, k, force_long=force_long)
+    assert plan.m_max == min(max(256, 8 * k), min(L, N - L + 1))
+    assert info[0]["status"] == 0 and info[0]["converged"] == 1, info[0]
+    s_ref, U_ref, V_ref, _ = oracle.svd(f, L, k + 1)
+    G_ref = np.stack([oracle.hankelize_rank1(s_ref[i], U_ref[i], V_ref[i]) for i in range(k)])
+    rep = parity.compare(s_ref, U_ref, V_ref, s[0], U[0], V[0], k, G_ref, G[0], recon_scale=np.linalg.norm(f),
+                         f=f, L=L)
+    assert rep.ok(), rep.failures

@@ -170,3 +170,27 @@ def test_cfg3_like_long_series_residuals(P):
         r1 = np.linalg.norm(oracle.matvec(f, L, Vh[i]) - s[i] * Uh[i])
         r2 = np.linalg.norm(oracle.matvec(f, L, Uh[i], True) - s[i] * Vh[i])
         assert max(r1, r2) <= 1e-11 * s[0], (i, r1, r2)   # 10 tol sigma_1
+
+
+@pytest.mark.parametrize("N,L,k", [(32768, 16384, 8), (1024, 512, 10)])
+def test_decompose_only_enqueues(P, N, L, k):
+    """include/ssa.h: ssa_decompose on device buffers only enqueues -- on the long path too
+    (the Lanczos loop is one graph launch with device-side decisions, no host sync).  The
+    stream is kept busy by a spin kernel first; the call must return while it still is."""
+    import time
+    f = ssa_inputs.cfg3_like_series(N, 7)
+    plan = P.Plan(N, L, k, 1)
+    x = cuda(f[None])
+    s, U, V, info = plan.decompose(x)          # first call builds the graph (long path)
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    torch.cuda._sleep(int(2e9))                # ~1 s of device time ahead of the decompose
+    t0 = time.perf_counter()
+    plan.decompose(x, s, U, V, info)
+    t1 = time.perf_counter()
+    busy = not stream.query()
+    torch.cuda.synchronize()
+    assert busy, "decompose waited for the device"
+    assert t1 - t0 < 0.5
+    inf = P.info_to_numpy(info)[0]
+    assert inf["status"] == 0 and inf["converged"] == 1, inf
