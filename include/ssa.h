@@ -82,6 +82,17 @@ typedef struct {
                             (seed, series, i): a shard [b0, b1) of a larger batch set to b0
                             gets bit-identical results to the unsharded run (SURVEY.md
                             8(e)).  Default 0.                                             */
+  int32_t restart_dim;   /* thick-restarted Lanczos bidiagonalization (sec 3.3,
+                            "restarting schemes"): the Krylov dimension d, i.e. at most d+1
+                            basis vectors per side are stored (O(d(L+K)) memory); when the
+                            basis is full the restart keeps restart_keep Ritz triples and the
+                            residual direction (R23).  0 (default) = no restart.
+                            Requires k + 2 <= d <= min(L, K) - 1 and the batched path
+                            (M <= 16384); reorthogonalization inside a cycle is FRO (reorth
+                            3 runs as 1).  max_steps then caps the TOTAL steps (default
+                            max(512, 16 k)) and no longer sizes the bases.                  */
+  int32_t restart_keep;  /* Ritz triples kept at a thick restart, k <= p <= min(d - 2, 64); 0 = d / 2
+                            (at least k).                                                  */
 } ssa_options;
 
 /* Per-series outcome of ssa_decompose (device array, one entry per series). */
@@ -97,7 +108,7 @@ typedef struct {
   int32_t rows_u;         /* Krylov basis rows of U read by reorthogonalization (all passes) */
   int32_t rows_v;         /* the same for V  (bytes read = 8 (rows_u L + rows_v K))          */
   int32_t reorth_steps;   /* half-steps that reorthogonalized (all of them under FRO)      */
-  int32_t reserved;
+  int32_t reserved;       /* thick restarts taken (restart_dim > 0), else 0                  */
 } ssa_series_info;
 
 /* Fill *opt with the defaults above (max_steps = 0 means "derive from k, L, K"). */

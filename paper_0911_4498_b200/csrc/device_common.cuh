@@ -22,6 +22,32 @@ namespace ssa {
 // implicit trigger at completion still removes the launch gap.)
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
+// Diagnostics (env SSA_TRACE, long-series path): thread 0 of CTA (0,0,0) of a traced kernel
+// records (%globaltimer, kernel id) after its dependency wait, so start-to-start times per
+// kernel id show where a graph's time goes (including conditional-node gaps).  One
+// pointer per translation unit (no -rdc); null = off (one predicated load per CTA).
+constexpr int kTraceMax = 1 << 18;
+static __device__ unsigned long long* g_trace;
+__device__ __forceinline__ void trace_point(int id) {
+  if (threadIdx.x == 0 && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) {
+    unsigned long long* tr = g_trace;
+    if (tr != nullptr) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      const unsigned long long i = atomicAdd(tr, 1ull);
+      if (i < (unsigned long long)kTraceMax) {
+        tr[1 + 2 * i] = t;
+        tr[2 + 2 * i] = (unsigned long long)id;
+      }
+    }
+  }
+}
+__device__ __forceinline__ void pdl_wait(int id) {
+  pdl_wait();
+  trace_point(id);
+}
+static inline cudaError_t trace_attach(unsigned long long* p) { return cudaMemcpyToSymbol(g_trace, &p, sizeof(p)); }
+
 // PDL attribute switch (a graph build falls back to plain launches if the driver rejects
 // programmatic edges inside conditional-node bodies)
 inline bool& pdl_enabled() {

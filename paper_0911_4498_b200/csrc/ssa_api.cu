@@ -164,7 +164,7 @@ static ssa_status create_decompose_workspace(Plan& p, const cudaDeviceProp& prop
   cudaError_t e;
   const int k = p.k;
   if (k > ssa::kMaxK) return fail(SSA_ERR_UNSUPPORTED, "k = %d > %d not supported by the batched decompose", k, ssa::kMaxK);
-  p.smem_lanczos = ssa::lanczos_smem_bytes((int)p.H, p.ldL, p.ldK, p.m_max, k);
+  p.smem_lanczos = ssa::lanczos_smem_bytes((int)p.H, p.ldL, p.ldK, p.m_max, k, p.opt.restart_dim > 0);
   p.smem_ritz = ssa::ritz_smem_bytes(p.ldL, p.ldK, k, p.m_max);
   if (p.smem_lanczos > (size_t)prop.sharedMemPerBlockOptin)
     return fail(SSA_ERR_UNSUPPORTED, "decompose needs %zu B shared memory > %zu", p.smem_lanczos,
@@ -235,8 +235,11 @@ static ssa_status create_large_workspace(Plan& p) {
   if ((st = alloc((void**)&p.d_counters, 16 * sizeof(int), "counters")) != SSA_OK) return st;
   const size_t nch = (size_t)(std::max(p.ldL, p.ldK) + 511) / 512;  // reorth chunks (kRoChunk)
   const size_t gU = (size_t)(p.L + 255) / 256;
-  const size_t npart = std::max(nch * (p.m_max + 2), gU * k * 2) + 4096;
-  if ((st = alloc((void**)&p.d_lgsc, 256, "scalars")) != SSA_OK) return st;
+  // dots partials [row][chunk], then 1024 correlation partials, 1024 start-vector partials
+  // and the dots group sums [row][kLgMaxGroups] (ssa_large_lanczos.cu)
+  const size_t npart = std::max(nch * (p.m_max + 2), gU * k * 2) + 2048 + (size_t)(p.m_max + 2) * 64 + 64;
+  if (nch > 64 * 32) return fail(SSA_ERR_UNSUPPORTED, "long-series reorthogonalization supports ld <= %d", 64 * 32 * 512);
+  if ((st = alloc((void**)&p.d_lgsc, 2048, "scalars")) != SSA_OK) return st;
   if ((st = alloc((void**)&p.d_lgpart, npart * 8, "partials")) != SSA_OK) return st;
   if ((st = alloc((void**)&p.d_lgh, (size_t)(p.m_max + 2 + 64) * 8, "reorth coefficients")) != SSA_OK) return st;
   if ((st = alloc((void**)&p.d_lgr, (size_t)std::max(p.ldL, p.ldK) * 8, "work vector")) != SSA_OK) return st;
@@ -262,10 +265,22 @@ extern "C" ssa_status ssa_plan_create(int64_t N, int64_t L, int32_t k, int64_t b
   ssa_options_default(&o);
   if (opt) o = *opt;
   if (!(o.tol > 0.0) || o.reorth < 1 || o.reorth > 3 || o.check_every < 0 || o.max_steps < 0 || o.series_base < 0 ||
-      (o.reorth == 3 && !(o.reorth_eta > 0.0 && o.reorth_eta <= 1e-6)))
+      (o.reorth == 3 && !(o.reorth_eta > 0.0 && o.reorth_eta <= 1e-6)) || o.restart_dim < 0 || o.restart_keep < 0)
     return fail(SSA_ERR_INVALID_ARGUMENT,
                 "bad options (tol > 0, reorth in {1,2,3}, reorth_eta in (0, 1e-6] for reorth 3, check_every >= 0, "
-                "max_steps >= 0, series_base >= 0)");
+                "max_steps >= 0, series_base >= 0, restart_dim >= 0, restart_keep >= 0)");
+
+  if (o.restart_dim > 0) {
+    // thick restart (R23): validated here, before any allocation
+    const int64_t d = o.restart_dim, mn = std::min(L, K);
+    if (k < 1 || d < (int64_t)k + 2 || d > mn - 1)
+      return fail(SSA_ERR_INVALID_ARGUMENT, "restart_dim = %lld must lie in [k + 2, min(L, K) - 1] = [%d, %lld]",
+                  (long long)d, k + 2, (long long)(mn - 1));
+    if (o.restart_keep == 0) o.restart_keep = (int32_t)std::max<int64_t>(k, d / 2);
+    if (o.restart_keep < k || o.restart_keep > d - 2 || o.restart_keep > 64)
+      return fail(SSA_ERR_INVALID_ARGUMENT, "restart_keep = %d must lie in [k, min(restart_dim - 2, 64)] = [%d, %lld]",
+                  o.restart_keep, k, (long long)std::min<int64_t>(d - 2, 64));
+  }
 
   int64_t M = 1;
   while (M < N) M <<= 1;
@@ -290,6 +305,10 @@ extern "C" ssa_status ssa_plan_create(int64_t N, int64_t L, int32_t k, int64_t b
   int64_t mn = std::min(L, K);
   int64_t mm = o.max_steps > 0 ? o.max_steps : std::max<int64_t>(256, 8 * (int64_t)k);
   p.m_max = (int32_t)std::max<int64_t>(k, std::min(mm, mn));
+  if (o.restart_dim > 0) {
+    p.m_max = o.restart_dim;  // thick restart: the bases hold d + 1 vectors
+    p.m_cap = o.max_steps > 0 ? o.max_steps : std::max(512, 16 * k);
+  }
   p.ldL = round_up((int)L, 16);
   p.ldK = round_up((int)K, 16);
 
@@ -319,8 +338,13 @@ extern "C" ssa_status ssa_plan_create(int64_t N, int64_t L, int32_t k, int64_t b
   // kernel would not fit one CTA's shared memory (e.g. H = 8192 with k > 0)
   if (H > ssa::kMaxSmemH || ((o.reserved & 4) && H >= 64) ||
       (k > 0 && H >= 64 &&
-       ssa::lanczos_smem_bytes((int)H, p.ldL, p.ldK, p.m_max, k) > (size_t)prop.sharedMemPerBlockOptin)) {
+       ssa::lanczos_smem_bytes((int)H, p.ldL, p.ldK, p.m_max, k, o.restart_dim > 0) >
+           (size_t)prop.sharedMemPerBlockOptin)) {
     p.large = true;
+    if (o.restart_dim > 0) {
+      st = fail(SSA_ERR_UNSUPPORTED, "thick restart (restart_dim > 0) runs on the batched path only (M <= 16384)");
+      goto bad;
+    }
     int N1, N2;
     ssa::large_geom(p, &N1, &N2);
     std::vector<double2> t1 = make_twiddles2(2 * (int64_t)N1), t2 = make_twiddles2(2 * (int64_t)N2);
@@ -473,6 +497,9 @@ extern "C" ssa_status ssa_decompose(ssa_plan_t plan, const double* d_series, dou
     if (const char* e = getenv("SSA_FIRST_CHECK")) a.first_check = std::max(p.k, atoi(e));
     if (const char* e = getenv("SSA_CHECK_CAP")) a.check_cap = std::max(ce, atoi(e));
   }
+  a.trl_d = p.opt.restart_dim > 0 ? p.m_max : 0;
+  a.trl_p = p.opt.restart_keep;
+  a.m_cap = p.m_cap;
   a.tol = p.opt.tol; a.seed = p.opt.seed; a.series_base = p.series_base;
   a.series = d_series; a.spec = p.d_spec; a.tw = p.d_twl;
   a.U = p.d_U; a.V = p.d_V; a.ab = p.d_ab; a.state = p.d_state;

@@ -27,6 +27,8 @@ struct DecomposeArgs {
   int check_every, reorth_mode;  // reorth_mode 1/2: FRO (DGKS / always two passes), 3: PRO
   double pro_eta;                 // PRO threshold (ssa_options::reorth_eta)
   int first_check, check_cap;  // step of the first convergence test; longest stretch between tests
+  int trl_d, trl_p;            // thick restart (ssa_options::restart_dim / restart_keep; 0: off)
+  int m_cap;                   // thick restart: cap on the total Lanczos steps (m_max = trl_d)
   int b0, nb;
   double tol;
   uint64_t seed;
@@ -63,7 +65,8 @@ struct Plan {
   int32_t k = 0;
   int64_t batch = 0;
   ssa_options opt{};
-  int32_t m_max = 0;
+  int32_t m_max = 0;           // Krylov basis rows - 1 (thick restart: the Krylov dimension d)
+  int32_t m_cap = 0;           // thick restart: cap on the total Lanczos steps
   int ldL = 0, ldK = 0;
   int sms = 0;
   int chunk = 0;               // series per decompose chunk (per-series storage)
@@ -172,7 +175,7 @@ cudaError_t launch_group_hankelize(const Plan& p, const double* sigma, const dou
                                    const GroupList& gl, double* out, cudaStream_t s);
 cudaError_t launch_group_sum(const Plan& p, const double* elem, const GroupList& gl, double* out, cudaStream_t s);
 
-size_t lanczos_smem_bytes(int H, int ldL, int ldK, int m_max, int k);
+size_t lanczos_smem_bytes(int H, int ldL, int ldK, int m_max, int k, bool trl = false);
 size_t ritz_smem_bytes(int ldL, int ldK, int k, int m_max);
 cudaError_t lanczos_set_attributes(size_t smem);
 cudaError_t svd_ritz_set_attributes(int m_max, size_t smem_ritz);

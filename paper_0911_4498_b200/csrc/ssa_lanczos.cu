@@ -33,9 +33,13 @@ struct LSmem {
   double* chk;             // 4 k: omega, res, lohi(2k)
   double2* tw;             // two-level twiddle table for M (tw2_entries(M))
   uint64_t* bars;          // kWarps * kStages
+  double* T;               // thick restart: the projected matrix, (m_max+1) x (m_max+1) row-major
 };
 
-__host__ __device__ inline size_t lanczos_regionA_bytes(int H, int ldL, int ldK, int m_max) {
+// thick restart: doubles of the one-sided Jacobi scratch in region A (W, Q, sigma, order)
+__host__ __device__ inline size_t trl_jacobi_doubles(int d) { return (size_t)2 * (d + 1) * (d + 1) + 2 * (d + 1); }
+
+__host__ __device__ inline size_t lanczos_regionA_bytes(int H, int ldL, int ldK, int m_max, bool trl = false) {
   int slab_max = (ldL > ldK ? ldL : ldK) / kWarps;
   size_t fft = (size_t)fft_elems(H) * 16;
   size_t rings = (size_t)kWarps * kStages * slab_max * 8 + (size_t)kWarps * (m_max + 2) * 8;
@@ -43,16 +47,18 @@ __host__ __device__ inline size_t lanczos_regionA_bytes(int H, int ldL, int ldK,
   size_t r = fft;
   if (rings > r) r = rings;
   if (tgk > r) r = tgk;
+  if (trl && trl_jacobi_doubles(m_max) * 8 > r) r = trl_jacobi_doubles(m_max) * 8;
   return align16(r);
 }
 
-size_t lanczos_smem_bytes(int H, int ldL, int ldK, int m_max, int k) {
-  size_t s = lanczos_regionA_bytes(H, ldL, ldK, m_max);
+size_t lanczos_smem_bytes(int H, int ldL, int ldK, int m_max, int k, bool trl) {
+  size_t s = lanczos_regionA_bytes(H, ldL, ldK, m_max, trl);
   s += align16((size_t)ldL * 8) + align16((size_t)ldK * 8);
   s += 5 * align16((size_t)(m_max + 3) * 8);
   s += 32 * 8 + 8 * 4 + align16((size_t)kClInts * 4) + (size_t)4 * k * 8;
   s += (size_t)tw2_entries(2 * H) * 16;
   s += (size_t)kWarps * kStages * 8;
+  if (trl) s += (size_t)(m_max + 1) * (m_max + 1) * 8;
   return align16(s) + 16;
 }
 
@@ -60,7 +66,7 @@ __device__ inline LSmem carve(unsigned char* base, const DecomposeArgs& a) {
   LSmem s;
   size_t off = 0;
   s.regionA = base;
-  off += lanczos_regionA_bytes(a.H, a.ldL, a.ldK, a.m_max);
+  off += lanczos_regionA_bytes(a.H, a.ldL, a.ldK, a.m_max, a.trl_d > 0);
   s.bufU = reinterpret_cast<double*>(base + off); off += align16((size_t)a.ldL * 8);
   s.bufV = reinterpret_cast<double*>(base + off); off += align16((size_t)a.ldK * 8);
   s.h = reinterpret_cast<double*>(base + off); off += align16((size_t)(a.m_max + 3) * 8);
@@ -73,7 +79,8 @@ __device__ inline LSmem carve(unsigned char* base, const DecomposeArgs& a) {
   s.cl = reinterpret_cast<int*>(base + off); off += align16((size_t)kClInts * 4);
   s.chk = reinterpret_cast<double*>(base + off); off += (size_t)4 * a.k * 8;
   s.tw = reinterpret_cast<double2*>(base + off); off += (size_t)tw2_entries(2 * a.H) * 16;
-  s.bars = reinterpret_cast<uint64_t*>(base + off);
+  s.bars = reinterpret_cast<uint64_t*>(base + off); off += (size_t)kWarps * kStages * 8;
+  s.T = (a.trl_d > 0) ? reinterpret_cast<double*>(base + off) : nullptr;
   return s;
 }
 
@@ -104,7 +111,7 @@ __device__ __forceinline__ double rng_uniform_pm1(uint64_t seed, uint64_t series
 // EPL elements of the warp's slab per lane live in registers (element lane + 32 t).
 template <int EPL>
 __device__ double reorth_t(double* r, const double* basis, int nb, int ld, double nrm_in, int mode, const LSmem& sm,
-                           WarpRing& rg, double* part, int pstride, int& extra) {
+                           WarpRing& rg, double* part, int pstride, int& extra, double* hacc) {
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int slab = ld / kWarps;
   double* rw = r + w * slab;
@@ -164,6 +171,7 @@ __device__ double reorth_t(double* r, const double* basis, int nb, int ld, doubl
       double s = 0.0;
       for (int q = 0; q < kWarps; ++q) s += part[q * pstride + c];
       sm.h[c] = s;
+      if (hacc) hacc[c] += s;  // thick restart: the coefficients are entries of T
     }
     __syncthreads();
     // pass 2: r -= V h, rows streamed in reverse so the most recently read rows (still
@@ -220,16 +228,16 @@ __device__ double reorth_t(double* r, const double* basis, int nb, int ld, doubl
 // DESIGN.md R9).  Each warp owns a column slab of r (held in registers) and of the basis;
 // the dot products are reduced across warps in a fixed order (deterministic).
 __device__ double reorth(double* r, const double* basis, int nb, int ld, double nrm_in, int mode, const LSmem& sm,
-                         WarpRing& rg, double* part, int pstride, int& extra) {
+                         WarpRing& rg, double* part, int pstride, int& extra, double* hacc = nullptr) {
   const int epl = (ld / kWarps + 31) / 32;
-  if (epl <= 1) return reorth_t<1>(r, basis, nb, ld, nrm_in, mode, sm, rg, part, pstride, extra);
-  if (epl <= 2) return reorth_t<2>(r, basis, nb, ld, nrm_in, mode, sm, rg, part, pstride, extra);
-  if (epl <= 4) return reorth_t<4>(r, basis, nb, ld, nrm_in, mode, sm, rg, part, pstride, extra);
-  if (epl <= 8) return reorth_t<8>(r, basis, nb, ld, nrm_in, mode, sm, rg, part, pstride, extra);
-  if (epl <= 9) return reorth_t<9>(r, basis, nb, ld, nrm_in, mode, sm, rg, part, pstride, extra);
-  if (epl <= 16) return reorth_t<16>(r, basis, nb, ld, nrm_in, mode, sm, rg, part, pstride, extra);
-  if (epl <= 17) return reorth_t<17>(r, basis, nb, ld, nrm_in, mode, sm, rg, part, pstride, extra);
-  return reorth_t<32>(r, basis, nb, ld, nrm_in, mode, sm, rg, part, pstride, extra);
+  if (epl <= 1) return reorth_t<1>(r, basis, nb, ld, nrm_in, mode, sm, rg, part, pstride, extra, hacc);
+  if (epl <= 2) return reorth_t<2>(r, basis, nb, ld, nrm_in, mode, sm, rg, part, pstride, extra, hacc);
+  if (epl <= 4) return reorth_t<4>(r, basis, nb, ld, nrm_in, mode, sm, rg, part, pstride, extra, hacc);
+  if (epl <= 8) return reorth_t<8>(r, basis, nb, ld, nrm_in, mode, sm, rg, part, pstride, extra, hacc);
+  if (epl <= 9) return reorth_t<9>(r, basis, nb, ld, nrm_in, mode, sm, rg, part, pstride, extra, hacc);
+  if (epl <= 16) return reorth_t<16>(r, basis, nb, ld, nrm_in, mode, sm, rg, part, pstride, extra, hacc);
+  if (epl <= 17) return reorth_t<17>(r, basis, nb, ld, nrm_in, mode, sm, rg, part, pstride, extra, hacc);
+  return reorth_t<32>(r, basis, nb, ld, nrm_in, mode, sm, rg, part, pstride, extra, hacc);
 }
 
 // Write r * inv into basis row dst (plain coalesced stores), scale r in place.
@@ -615,17 +623,30 @@ __global__ void __launch_bounds__(kThreads, 2) lanczos_kernel(const DecomposeArg
     for (int i = 0; i < 8; ++i) atomicAdd(a.prof + i, pc[i]);
 }
 
+}  // namespace ssa
+
+#include "lanczos_trl.cuh"
+
+namespace ssa {
+
 cudaError_t lanczos_set_attributes(size_t smem) {
   cudaError_t e = raise_smem_limit(lanczos_kernel, (int)smem);
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(lanczos_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             cudaSharedmemCarveoutMaxShared);
+  if (e == cudaSuccess) e = raise_smem_limit(lanczos_trl_kernel, (int)smem);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(lanczos_trl_kernel, cudaFuncAttributePreferredSharedMemoryCarveout,
                              cudaSharedmemCarveoutMaxShared);
   return e;
 }
 
 cudaError_t launch_lanczos(const Plan& p, const DecomposeArgs& a, cudaStream_t s) {
   int grid = p.lanczos_slots < a.nb ? p.lanczos_slots : a.nb;
-  lanczos_kernel<<<grid, kThreads, p.smem_lanczos, s>>>(a);
+  if (a.trl_d > 0)
+    lanczos_trl_kernel<<<grid, kThreads, p.smem_lanczos, s>>>(a);
+  else
+    lanczos_kernel<<<grid, kThreads, p.smem_lanczos, s>>>(a);
   return cudaGetLastError();
 }
 

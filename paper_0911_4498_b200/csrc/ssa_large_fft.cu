@@ -25,8 +25,11 @@
 #include <algorithm>
 
 #include "device_common.cuh"
+#include "lg_scalars.cuh"
 
 namespace ssa {
+
+cudaError_t trace_attach_fft(unsigned long long* p) { return trace_attach(p); }
 
 constexpr int kColW = 8;  // columns per CTA in the column passes (one warp each)
 
@@ -100,6 +103,8 @@ struct ColFwdIn {
   int n_in;
   double2* Y;       // [items][H]
   int vec;          // x 16-byte aligned: pairs (x_2n, x_2n+1) of aligned rows as one 16-byte load
+  LgNorm nrm;       // long-series Lanczos: x is r, scaled by *nrm.inv on the fly and written to
+                    // the basis row and the current vector (nrm.inv null: plain input)
 };
 struct ColFwdArgs {
   ColFwdIn in[2];   // blockIdx.z selects
@@ -109,7 +114,7 @@ struct ColFwdArgs {
 template <int LOGH>
 __global__ void __launch_bounds__(kThreads) lg_col_fwd(ColFwdArgs args, const double2* __restrict__ T1,
                                                        const double2* __restrict__ TWH) {
-  pdl_wait();
+  pdl_wait(1);
   if (args.gate && *args.gate) return;
   using G = Geo<LOGH>;
   constexpr int N1 = G::N1, N2 = G::N2, CS = N1 + 1;  // odd column stride (16-byte units)
@@ -139,6 +144,28 @@ __global__ void __launch_bounds__(kThreads) lg_col_fwd(ColFwdArgs args, const do
       v[j].x = (ok && i0 < a.n_in) ? __ldg(xi + i0) : 0.0;
       v[j].y = (ok && i0 + 1 < a.n_in) ? __ldg(xi + i0 + 1) : 0.0;
     }
+  }
+  if (a.nrm.inv) {
+    // Lanczos normalization of the previous half-step's vector (one item): every element of
+    // x is read by exactly one thread of the grid, which scales it and stores it to the
+    // basis row and the current vector (the padding of the basis row stays zero)
+    const double inv = *a.nrm.inv;
+    double* brow = a.nrm.basis + (size_t)(*a.nrm.jrow - 1) * a.nrm.ld;
+#pragma unroll
+    for (int j = 0; j < NE; ++j) {
+      const bool ok = threadIdx.x + j * kThreads < N1 * kColW;
+      const int i0 = i00 + j * (2 * N2 * (kThreads / kColW));
+      v[j].x *= inv;
+      v[j].y *= inv;
+      if (rvec && ok && i0 + 1 < a.n_in) {
+        *reinterpret_cast<double2*>(brow + i0) = v[j];
+        *reinterpret_cast<double2*>(a.nrm.cur + i0) = v[j];
+      } else {
+        if (ok && i0 < a.n_in) { brow[i0] = v[j].x; a.nrm.cur[i0] = v[j].x; }
+        if (ok && i0 + 1 < a.n_in) { brow[i0 + 1] = v[j].y; a.nrm.cur[i0 + 1] = v[j].y; }
+      }
+    }
+    if (blockIdx.x == 0 && threadIdx.x < a.nrm.ld - a.n_in) brow[a.n_in + threadIdx.x] = 0.0;
   }
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if constexpr (G::L1 >= 8) {
@@ -183,12 +210,14 @@ struct ColInvArgs {
   const double* sigma;         // hankelization: per-item sigma
   int N, L, K;                 // hankelization: weights
   const int* gate;             // device flag: nonzero -> the launch does nothing
+  int has_tail;                // long-series Lanczos (one item): the last CTA runs lg_pro_tail
+  LgProTail tail;
 };
 
 template <int LOGH>
 __global__ void __launch_bounds__(kThreads, (LOGH >= 19) ? 1 : 3) lg_col_inv(const double2* __restrict__ Y, const double2* __restrict__ T1,
                                                        ColInvArgs a) {
-  pdl_wait();
+  pdl_wait(4);
   if (a.gate && *a.gate) return;
   using G = Geo<LOGH>;
   constexpr int N1 = G::N1, N2 = G::N2, CS = N1 + 1;
@@ -270,6 +299,13 @@ __global__ void __launch_bounds__(kThreads, (LOGH >= 19) ? 1 : 3) lg_col_inv(con
         double s = 0.0;
         for (int i = 0; i < kWarps; ++i) s += red[i];
         a.part[item * gridDim.x + blockIdx.x] = s;
+      }
+      if (a.has_tail) {
+        __shared__ int lastf;
+        if (last_cta(&a.tail.sc->done_inv, gridDim.x, &lastf)) {
+          lg_pro_tail(a.part, gridDim.x, a.tail, red);
+          if (threadIdx.x == 0) a.tail.sc->done_inv = 0;
+        }
       }
     }
   } else {
@@ -374,7 +410,7 @@ __device__ __forceinline__ void row_pair_step(const RowArgs& a, size_t item, int
 template <int LOGH>
 __global__ void __launch_bounds__(kThreads) lg_row_cta(const double2* __restrict__ T2, const double2* __restrict__ TWH,
                                                        const double2* __restrict__ TWA, RowArgs a) {
-  pdl_wait();
+  pdl_wait(2);
   if (a.gate && *a.gate) return;
   using G = Geo<LOGH>;
   constexpr int N1 = G::N1, N2 = G::N2;
@@ -490,7 +526,7 @@ template <int LOGH>
 __global__ void __launch_bounds__(kThreads) lg_row_warp(const double2* __restrict__ T2,
                                                         const double2* __restrict__ TWH,
                                                         const double2* __restrict__ TWA, RowArgs a) {
-  pdl_wait();
+  pdl_wait(3);
   if (a.gate && *a.gate) return;
   using Gm = Geo<LOGH>;
   constexpr int N1 = Gm::N1, N2 = Gm::N2;
@@ -710,6 +746,33 @@ cudaError_t large_correlate(const Plan& p, const double2* spec, size_t spec_stri
     ca.gate = gate;
     col_inv(p, Y, ca, ni, s);
   }
+  return cudaGetLastError();
+}
+
+// One Lanczos half-step correlation (one series): x = r * (*nrm.inv) (normalization of the
+// previous half-step's vector fused into the column FFT, written to nrm.basis / nrm.cur),
+// y = correlation - coef * prev into out, and the decision tail (lg_pro_tail) in the last
+// CTA of the inverse column pass.
+cudaError_t large_correlate_lanczos(const Plan& p, const double2* spec, const double* r, int n_in, const LgNorm& nrm,
+                                    double* out, int n_out, int ld_out, const double* prev, const double* coef,
+                                    double* part, const LgProTail& tail, cudaStream_t s) {
+  int N1, N2;
+  large_geom(p, &N1, &N2);
+  double2* Y = p.d_lbuf;
+  ColFwdArgs cf{};
+  cf.in[0] = ColFwdIn{r, 0, n_in, Y, vec16(r, 0), nrm};
+  col_fwd(p, cf, 1, 1, s);
+  RowArgs ra{1, Y, nullptr, spec, 0, nullptr, nullptr};
+  rows(p, ra, 1, false, s);
+  ColInvArgs ca{};
+  ca.mode = 0;
+  ca.n_out = n_out; ca.ld_out = ld_out; ca.out_stride = 0; ca.out = out;
+  ca.prev = prev; ca.prev_stride = 0;
+  ca.coef = coef;
+  ca.part = part;
+  ca.has_tail = 1;
+  ca.tail = tail;
+  col_inv(p, Y, ca, 1, s);
   return cudaGetLastError();
 }
 

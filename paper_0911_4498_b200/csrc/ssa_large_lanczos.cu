@@ -4,25 +4,33 @@
 // PAPER.md:402-411).
 //
 // The whole Lanczos loop is ONE CUDA graph launch: a WHILE conditional node whose body is
-// one step (half-steps A and B) of grid-wide kernels, with IF conditional nodes around the
-// work that only some steps need; every decision (reorthogonalize or not, a DGKS second
-// pass, a breakdown restart, the convergence test, the stop) is taken on the device, so
-// ssa_decompose only enqueues (no host synchronization, include/ssa.h conventions):
-//   correlation  three-pass four-step FFT (ssa_large_fft.cu) with the recurrence term
-//                fused in the epilogue: r = X^T u_j - beta_j v_{j-1} (or X v_j - alpha_j u_j),
-//                plus per-CTA partial sums of squares;  x and the previous vector are the
-//                plan's "current vector" buffers, so every launch has fixed arguments;
-//   lg_pro       one CTA: |r|, the PRO omega recurrences (or FRO: always), the decision;
-//                without reorthogonalization it also takes the Lanczos coefficient;
-//   IF reorth    dots (h = B^T r, per-chunk partials, the last CTA sums them in a fixed
-//                order), update (r -= B h, rows in reverse so the rows the dots read last
-//                hit L2), finish (norm, DGKS decision); IF again: a second pass;
-//   IF restart   breakdown (coefficient < 1e-12 running max): a fresh seeded vector
-//                orthogonalized twice against the basis, coefficient 0 (R11);
-//   normalize    the basis row and the current-vector buffer;
-//   lg_check     after half-step A, on the device-side schedule: the residual test of
-//                tgk.cuh on B_m, the next test step, the stop flag;
-//   IF not stop  half-step B; lg_loop sets the WHILE condition.
+// one step (half-steps A and B) of grid-wide kernels; every decision (reorthogonalize or
+// not, a DGKS second pass, a breakdown restart, the convergence test, the stop) is taken
+// on the device, so ssa_decompose only enqueues (no host synchronization, include/ssa.h
+// conventions).  A half-step:
+//   correlation  three-pass four-step FFT (ssa_large_fft.cu).  The column FFT reads the
+//                previous half-step's unnormalized vector r, scales it by 1/coefficient
+//                and stores it to its basis row and "current vector" buffer (the
+//                normalization of Alg. 1 lines 5 / 7); the epilogue subtracts the
+//                recurrence term, r = X^T u_j - beta_j v_{j-1} (or X v_j - alpha_j u_j),
+//                with per-CTA partial sums of squares, and its last CTA takes |r| and the
+//                reorthogonalization decision: the PRO omega recurrences or FRO
+//                (lg_pro_tail, lg_scalars.cuh); without reorthogonalization it also takes
+//                the Lanczos coefficient.  Every launch has fixed arguments;
+//   reorth       gated on the decision (a gated-off kernel returns at once; cheaper than
+//                an IF node when the pass runs on most half-steps): dots (h = B^T r,
+//                per-chunk partials summed in a fixed two-level order by the last CTAs),
+//                update (r -= B h, rows in reverse so the rows the dots read last hit L2;
+//                its last CTA takes the norm, the DGKS decision and the coefficient);
+//   IF fix-up    rare: the DGKS second pass and / or a breakdown restart (coefficient
+//                < 1e-12 running max: a fresh seeded vector orthogonalized twice against
+//                the basis, coefficient 0, R11), its handle set by whichever
+//                tail took the decision.
+// After half-step A the convergence test lg_check (tgk.cuh residuals of B_m on the
+// device-side schedule, the halt flag) runs on a parallel branch of the graph, concurrent
+// with half-step B, which therefore runs once more than needed on the last step (its
+// results unused); lg_loop (after both) advances j unless halted and sets the WHILE
+// condition.
 // Every kernel is launched with programmatic dependent launch (launch_pdl / pdl_wait) where
 // the graph allows it.  After the loop the bidiagonal SVD reuses bidiag_svd_tgk_kernel and
 // the Ritz vectors come from lg_ritz (grid-wide, one pass over each basis) with sign
@@ -31,47 +39,24 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <vector>
 
 #include "device_common.cuh"
 #include "tgk.cuh"
+#include "lg_scalars.cuh"
 
 namespace ssa {
 
+cudaError_t trace_attach_fft(unsigned long long* p);
+cudaError_t large_correlate_lanczos(const Plan& p, const double2* spec, const double* r, int n_in, const LgNorm& nrm,
+                                    double* out, int n_out, int ld_out, const double* prev, const double* coef,
+                                    double* part, const LgProTail& tail, cudaStream_t s);
 cudaError_t large_spectrum(const Plan& p, const double* series, double2* spec, int items, cudaStream_t s);
 cudaError_t launch_bidiag_svd(const Plan& p, const DecomposeArgs& a, cudaStream_t s);
 void large_geom(const Plan& p, int* N1, int* N2);
 
 constexpr int kLgChunk = 2048;  // elements per CTA of the start / restart vector
-constexpr double kLgEps = 2.220446049250313e-16;
-
-// device scalars of the long-series run (one struct, plan memory)
-struct LgScalars {
-  double nr;        // |r| before reorthogonalization (correlation partials)
-  double nrm;       // current |r|
-  double runmax;    // running max of alpha, beta
-  double res;       // last convergence estimate
-  double prev_res;  // previous estimate (test schedule)
-  double acur;      // alpha_j (coefficient of half-step B)
-  double bcur;      // beta_j  (coefficient of half-step A)
-  double nr_rs;     // restart vector norm before orthogonalization
-  int j;            // current step (1-based)
-  int m;            // B_m: steps so far (set by lg_check)
-  int halt;         // loop ends after half-step A of this step
-  int do_ro;        // this half-step reorthogonalizes
-  int again;        // DGKS second pass needed
-  int force;        // PRO follow-up: bit 0 the next v half-step, bit 1 the next u half-step
-  int restart;      // breakdown: restart vector pending
-  int stop;         // space exhausted: zero vector, stop at the next test
-  int breakdown;    // first breakdown step
-  int restarts;     // restarts so far
-  int extra;        // DGKS second passes
-  int conv;         // converged
-  int next_check, prev_m;
-  int rows_u, rows_v, rsteps;
-  unsigned int done_ctas;  // last-CTA counter of lg_dots
-  unsigned long long seed, series;  // start / restart vectors of this call's series
-};
 
 __device__ __forceinline__ double lg_rng(uint64_t seed, uint64_t series, uint64_t i) {
   // the same counter-based generator as the batched kernel (R6)
@@ -83,11 +68,19 @@ __device__ __forceinline__ double lg_rng(uint64_t seed, uint64_t series, uint64_
   return 2.0 * ((double)(x >> 11) * 0x1.0p-53) - 1.0;
 }
 
+// Device-side gates of the kernels of a half-step (no IF node around them): 0 the
+// reorthogonalization pass (do_ro), 1 the DGKS second pass (again), 2 the breakdown
+// restart (restart).  A gated-off launch returns at once.
+__device__ __forceinline__ bool lg_open(const LgScalars* sc, int gate) {
+  return gate == 0 ? sc->do_ro != 0 : gate == 1 ? sc->again != 0 : sc->restart != 0;
+}
+
 // Start vector (Alg. 1 line 1): r = seeded uniform(-1, 1), partial sums of squares; with
-// sc != null it is a breakdown restart: salt (restarts << 40) as the batched kernel.
+// sc != null it is a breakdown restart (gate 2): salt (restarts << 40) as the batched kernel.
 __global__ void __launch_bounds__(kThreads) lg_start(double* r, int n, int ld, uint64_t seed, uint64_t series,
                                                      double* part, const LgScalars* sc) {
-  pdl_wait();
+  pdl_wait(10);
+  if (sc && !lg_open(sc, 2)) return;
   __shared__ double red[kWarps];
   const uint64_t salt = sc ? ((uint64_t)sc->restarts << 40) : 0;
   if (sc) {
@@ -119,18 +112,21 @@ constexpr int kRoChunk = 512;
 constexpr int kRoE = kRoChunk / kThreads;  // 2
 constexpr int kRoG = 8;                    // rows per group (warp_sum8)
 
-__device__ __forceinline__ int lg_nb(const LgScalars* sc, int side) { return side == 0 ? sc->j - 1 : sc->j; }
+// dots: part[row][cta] = <basis[row][chunk], r[chunk]>, then a two-level fixed-order sum
+// (deterministic): the last CTA of each group of kDotGroup CTAs sums its group's partials
+// of every row (one thread per row, all kDotGroup loads in flight) into gpart[row][group];
+// the last group to finish sums the groups into h[row].  Rows are read with L2
+// evict_last so lg_update (rows in reverse) finds the last ones.
+constexpr int kDotGroup = 32;
 
-// dots: part[row][cta] = <basis[row][chunk], r[chunk]>, then the last CTA to finish sums the
-// partials of every row in a fixed order into h[row] (deterministic).  Rows are read with
-// L2 evict_last so lg_update (rows in reverse) finds the last ones.
 __global__ void __launch_bounds__(kThreads) lg_dots(const double* __restrict__ basis, int ld, int side,
-                                                    const double* __restrict__ r, double* part, int nchunk,
-                                                    double* h, LgScalars* sc) {
-  pdl_wait();
+                                                    const double* __restrict__ r, double* part, double* gpart,
+                                                    int nchunk, double* h, LgScalars* sc, int gate) {
+  pdl_wait(6);
+  if (!lg_open(sc, gate)) return;
   const int nb = lg_nb(sc, side);
   extern __shared__ double red[];  // [nb][kWarps]
-  __shared__ int last;
+  __shared__ int lastf;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int c0 = blockIdx.x * kRoChunk + threadIdx.x;
   const bool full = (blockIdx.x + 1) * kRoChunk <= ld;
@@ -138,7 +134,7 @@ __global__ void __launch_bounds__(kThreads) lg_dots(const double* __restrict__ b
 #pragma unroll
   for (int e = 0; e < kRoE; ++e) v[e] = (c0 + e * kThreads < ld) ? r[c0 + e * kThreads] : 0.0;
   const uint64_t pol = policy_evict_last();
-  for (int row0 = 0; row0 < nb; row0 += kRoG) {
+  auto group = [&](int row0, auto guarded) {
     double b[kRoG][kRoE];
 #pragma unroll
     for (int q = 0; q < kRoG; ++q)
@@ -146,9 +142,10 @@ __global__ void __launch_bounds__(kThreads) lg_dots(const double* __restrict__ b
       for (int e = 0; e < kRoE; ++e) {
         const int t = c0 + e * kThreads;
         double x = 0.0;
-        if (row0 + q < nb && (full || t < ld)) {
+        if (!decltype(guarded)::value || (row0 + q < nb && (full || t < ld))) {
           const double* ad = basis + (size_t)(row0 + q) * ld + t;
-          asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(x) : "l"(ad), "l"(pol));
+          // not volatile: the compiler may issue all kRoG x kRoE loads before the FMAs
+          asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(x) : "l"(ad), "l"(pol));
         }
         b[q][e] = x;
       }
@@ -163,7 +160,11 @@ __global__ void __launch_bounds__(kThreads) lg_dots(const double* __restrict__ b
     const double tot = warp_sum8(d, lane);
     const int q = (lane >> 2) & 7;
     if ((lane & 3) == 0 && row0 + q < nb) red[(row0 + q) * kWarps + w] = tot;
-  }
+  };
+  int row0 = 0;
+  if (full)  // whole groups of a whole chunk: no guards, all 16 loads in flight
+    for (; row0 + kRoG <= nb; row0 += kRoG) group(row0, std::false_type());
+  for (; row0 < nb; row0 += kRoG) group(row0, std::true_type());
   __syncthreads();
   for (int row = threadIdx.x; row < nb; row += kThreads) {
     double s = 0.0;
@@ -171,30 +172,54 @@ __global__ void __launch_bounds__(kThreads) lg_dots(const double* __restrict__ b
     for (int i = 0; i < kWarps; ++i) s += red[row * kWarps + i];
     part[(size_t)row * nchunk + blockIdx.x] = s;
   }
-  // last CTA: h[row] = sum over CTAs in index order (threadfence / counter pattern)
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) last = (atomicAdd(&sc->done_ctas, 1u) == gridDim.x - 1);
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  for (int row = w; row < nb; row += kWarps) {
+  // level 1: the last CTA of this group sums the group's partials, one thread per row
+  const int g = blockIdx.x / kDotGroup, ng = (nchunk + kDotGroup - 1) / kDotGroup;
+  const int g0 = g * kDotGroup, gn = min(kDotGroup, nchunk - g0);
+  if (!last_cta(&sc->grp_done[g], (unsigned)gn, &lastf)) return;
+  for (int row = threadIdx.x; row < nb; row += kThreads) {
+    const double* pr = part + (size_t)row * nchunk + g0;
     double s = 0.0;
-    for (int i = lane; i < nchunk; i += 32) s += __ldcg(part + (size_t)row * nchunk + i);
-    s = warp_sum(s);
-    if (lane == 0) h[row] = s;
+    for (int i0 = 0; i0 < gn; i0 += 16) {  // 16 loads in flight, summed in index order
+      double x[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) x[i] = (i0 + i < gn) ? __ldcg(pr + i0 + i) : 0.0;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) s += x[i];
+    }
+    gpart[(size_t)row * kLgMaxGroups + g] = s;
   }
-  if (threadIdx.x == 0) sc->done_ctas = 0;
+  if (threadIdx.x == 0) sc->grp_done[g] = 0;
+  // level 2: the last group sums the groups in index order
+  if (!last_cta(&sc->done_grp, (unsigned)ng, &lastf)) return;
+  for (int row = threadIdx.x; row < nb; row += kThreads) {
+    const double* pr = gpart + (size_t)row * kLgMaxGroups;
+    double s = 0.0;
+    for (int i0 = 0; i0 < ng; i0 += 16) {
+      double x[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) x[i] = (i0 + i < ng) ? __ldcg(pr + i0 + i) : 0.0;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) s += x[i];
+    }
+    h[row] = s;
+  }
+  if (threadIdx.x == 0) sc->done_grp = 0;
 }
 
 // update: r -= sum_row h[row] basis[row] (rows in reverse: the rows lg_dots read last
 // are still in L2), partial sums of squares; groups of kRoG rows, all loads in flight.
+// The last CTA then finishes the pass: |r| from the partials; pass 0 decides the DGKS
+// second pass (|r| < |r_before| / sqrt 2, or always for mode 2) and sets its IF handle;
+// otherwise (or after pass 1) it takes the Lanczos coefficient (lg_take_coef).
 __global__ void __launch_bounds__(kThreads) lg_update(const double* __restrict__ basis, int ld, int side,
                                                       const double* __restrict__ h, double* r, double* part,
-                                                      const LgScalars* sc) {
-  pdl_wait();
+                                                      LgScalars* sc, int pass, int gate, int mode, double* ab,
+                                                      int w, cudaGraphConditionalHandle h_fix) {
+  pdl_wait(7);
+  if (!lg_open(sc, gate)) return;
   const int nb = lg_nb(sc, side);
   __shared__ double red[kWarps];
+  __shared__ int lastf;
   extern __shared__ double hs[];  // nb coefficients
   for (int i = threadIdx.x; i < nb; i += blockDim.x) hs[i] = h[i];
   __syncthreads();
@@ -240,143 +265,30 @@ __global__ void __launch_bounds__(kThreads) lg_update(const double* __restrict__
     for (int i = 0; i < kWarps; ++i) t += red[i];
     part[blockIdx.x] = t;
   }
-}
-
-// fixed-order sum of n partials by one CTA (thread-strided, shuffle tree, warps in order)
-__device__ double cta_sum(const double* __restrict__ a, int n, double* red) {
-  double s = 0.0;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) s += a[i];
-  s = warp_sum(s);
-  __syncthreads();
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
-  __syncthreads();
-  double t = 0.0;
-  for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += red[i];
-  return t;
-}
-
-// The Lanczos coefficient of a half-step: |r| (or 0 at breakdown -> restart pending), into
-// ab (alpha_j: side 0, beta_{j+1}: side 1) and the current-coefficient slot.
-__device__ void lg_take_coef(LgScalars* sc, int side, double nn, double* ab, int w) {
-  const int j = sc->j;
-  double c = nn;
-  if (!(nn > 1e-12 * sc->runmax) || nn == 0.0) {
-    if (!sc->breakdown) sc->breakdown = j;
-    sc->restart = 1;
-    c = 0.0;
-  } else {
-    sc->runmax = fmax(sc->runmax, nn);
-  }
-  sc->nrm = nn;
-  if (side == 0) { ab[j] = c; sc->acur = c; }
-  else { ab[w + j + 1] = c; sc->bcur = c; }
-}
-
-// One CTA after the correlation of a half-step: |r| from the correlation partials, then
-// the reorthogonalization decision -- FRO (mode 1 / 2): whenever the basis is not empty;
-// PRO (mode 3): the omega recurrences of ssa_lanczos.cu (Larsen 1998 update_nu /
-// update_mu) over om[side][1..nb], against eta, plus the forced follow-up half-step.
-// Without reorthogonalization the coefficient is taken here.  Sets the IF handle of the
-// reorthogonalization body.
-__global__ void __launch_bounds__(kThreads) lg_pro(const double* __restrict__ cpart, int ncol, int side, LgScalars* sc,
-                                                   double* ab, int w, double* om, int mode, double eta,
-                                                   cudaGraphConditionalHandle h_ro) {
-  pdl_wait();
-  __shared__ double red[kWarps];
-  const double nr = sqrt(cta_sum(cpart, ncol, red));
-  const int j = sc->j, nb = lg_nb(sc, side);
-  double* mu = om;              // u side, 1-based
-  double* nu = om + (w + 1);    // v side
-  const double* alpha = ab;
-  const double* beta = ab + w;
-  int do_ro = (nb > 0) && !sc->stop;
-  if (mode == 3 && do_ro) {
-    const double anorm = sc->runmax;
-    double mx = 0.0;
-    if (side == 0) {
-      const double bj = sc->bcur, rj = hypot(nr, bj);
-      for (int i = 1 + threadIdx.x; i <= nb; i += blockDim.x) {
-        double t = fma(alpha[i], mu[i], fma(beta[i + 1], mu[i + 1], -bj * nu[i]));
-        const double d = kLgEps * (hypot(alpha[i], beta[i + 1]) + rj) + kLgEps * anorm;
-        t = (t + copysign(d, t)) / nr;
-        nu[i] = t;
-        mx = fmax(mx, fabs(t));
-      }
-    } else {
-      const double aj = sc->acur, rj = hypot(aj, nr);
-      for (int i = 1 + threadIdx.x; i <= nb; i += blockDim.x) {
-        double t = fma(alpha[i], nu[i], fma(beta[i], nu[i - 1], -aj * mu[i]));
-        const double d = kLgEps * (hypot(alpha[i], beta[i]) + rj) + kLgEps * anorm;
-        t = (t + copysign(d, t)) / nr;
-        mu[i] = t;
-        mx = fmax(mx, fabs(t));
-      }
-    }
-    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-    __syncthreads();
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
-    __syncthreads();
-    mx = 0.0;
-    for (int i = 0; i < kWarps; ++i) mx = fmax(mx, red[i]);
-    const int bit = 1 << side;
-    const bool forced = (sc->force & bit) != 0;
-    do_ro = (mx > eta) || forced || !(nr > 0.0);
-    __syncthreads();
-    if (do_ro) {
-      double* o = side == 0 ? nu : mu;
-      for (int i = 1 + threadIdx.x; i <= nb; i += blockDim.x) o[i] = kLgEps;
-    }
-    if (threadIdx.x == 0) sc->force = (do_ro && !forced) ? (sc->force | bit) : (sc->force & ~bit);
-  }
+  if (pass < 0) return;  // restart passes: lg_restart_norm finishes them
+  if (!last_cta(&sc->done_upd, gridDim.x, &lastf)) return;
+  const double nn = sqrt(cta_sum(part, gridDim.x, red));
   if (threadIdx.x != 0) return;
-  if (side == 0) nu[j] = 1.0;
-  else mu[j + 1] = 1.0;
-  sc->nr = nr;
-  sc->again = 0;
-  sc->restart = 0;
-  sc->do_ro = do_ro;
-  if (do_ro) {
-    sc->rsteps += 1;
-    if (side == 0) sc->rows_v += 2 * nb;
-    else sc->rows_u += 2 * nb;
-  } else {
-    lg_take_coef(sc, side, sc->stop ? 0.0 : nr, ab, w);
-    if (sc->stop) sc->restart = 0;
-  }
-  cudaGraphSetConditional(h_ro, do_ro ? 1u : 0u);
-}
-
-// After a reorthogonalization pass (one CTA): |r| from the update partials; pass 0 decides
-// the DGKS second pass (|r| < |r_before| / sqrt 2, or always for mode 2) and sets its IF
-// handle; otherwise (or after pass 1) the coefficient.
-__global__ void __launch_bounds__(kThreads) lg_finish(const double* __restrict__ part, int nch, int side, LgScalars* sc,
-                                                      int pass, int mode, double* ab, int w,
-                                                      cudaGraphConditionalHandle h_again) {
-  pdl_wait();
-  __shared__ double red[kWarps];
-  const double nn = sqrt(cta_sum(part, nch, red));
-  if (threadIdx.x != 0) return;
+  sc->done_upd = 0;
   int again = 0;
   if (pass == 0) {
     again = (mode == 2 || nn < 0.70710678118654752 * sc->nr) ? 1 : 0;
     if (again) {
       sc->extra += 1;
-      const int nb = lg_nb(sc, side);
       if (side == 0) sc->rows_v += 2 * nb;
       else sc->rows_u += 2 * nb;
     }
   }
   sc->again = again;
-  if (!again) lg_take_coef(sc, side, nn, ab, w);
-  if (pass == 0) cudaGraphSetConditional(h_again, again ? 1u : 0u);
-}
-
-// After the coefficient of a half-step: sets the IF handle of the breakdown restart.
-__global__ void lg_restart_gate(LgScalars* sc, cudaGraphConditionalHandle h_rs) {
-  if (threadIdx.x != 0) return;
-  const int rs = sc->restart;
-  if (rs) sc->restarts += 1;
-  cudaGraphSetConditional(h_rs, rs ? 1u : 0u);
+  if (pass == 0) {
+    // the fix-up IF node of this half-step: a DGKS second pass or a breakdown restart
+    if (!again) lg_take_coef(sc, side, nn, ab, w);
+    if (!again && sc->restart) sc->restarts += 1;
+    cudaGraphSetConditional(h_fix, (again || sc->restart) ? 1u : 0u);
+  } else {
+    lg_take_coef(sc, side, nn, ab, w);  // inside the fix-up body: its restart kernels follow
+    if (sc->restart) sc->restarts += 1;
+  }
 }
 
 // Restart vector after its two orthogonalization passes: q = |r| / |r_0|; a vector that
@@ -385,7 +297,8 @@ __global__ void lg_restart_gate(LgScalars* sc, cudaGraphConditionalHandle h_rs) 
 __global__ void __launch_bounds__(kThreads) lg_restart_norm(const double* __restrict__ part, int nch,
                                                             const double* __restrict__ spart, int nst, LgScalars* sc,
                                                             int side, double* om, int w) {
-  pdl_wait();
+  pdl_wait(11);
+  if (!lg_open(sc, 2)) return;
   __shared__ double red[kWarps];
   const double nn = sqrt(cta_sum(part, nch, red));
   const double n0 = sqrt(cta_sum(spart, nst, red));
@@ -396,49 +309,24 @@ __global__ void __launch_bounds__(kThreads) lg_restart_norm(const double* __rest
   if (threadIdx.x != 0) return;
   const bool ok = nn > 1e-8 * n0;
   sc->nr_rs = ok ? nn : 0.0;
+  sc->inv_next = ok ? 1.0 / nn : 0.0;
   if (!ok) sc->stop = 1;
-}
-
-// v = r / coef into the basis row (side 0: V row j-1, coefficient alpha_j; side 1: U row j,
-// beta_{j+1}) and the current-vector buffer; after a restart the scale is 1 / |r|.
-// fixed_row >= 0: the start vector u_1 (row 0, beta_1).
-__global__ void __launch_bounds__(kThreads) lg_normalize(const double* __restrict__ r, int n, int ld, int side,
-                                                         int fixed_row, const LgScalars* sc, const double* ab, int w,
-                                                         double* basis, double* cur) {
-  pdl_wait();
-  int row;
-  double c;
-  if (fixed_row >= 0) {
-    row = fixed_row;
-    c = ab[w + 1];
-  } else {
-    const int j = sc->j;
-    row = side == 0 ? j - 1 : j;
-    c = side == 0 ? ab[j] : ab[w + j + 1];
-    if (sc->restart) c = sc->nr_rs;
-  }
-  const double inv = (c > 0.0) ? 1.0 / c : 0.0;
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t < ld) {
-    const double v = (t < n) ? r[t] * inv : 0.0;
-    basis[(size_t)row * ld + t] = v;
-    cur[t] = v;
-  }
 }
 
 // beta_1 = |p_0| from the start vector's partials (Alg. 1 line 2)
 __global__ void __launch_bounds__(kThreads) lg_beta1(const double* __restrict__ part, int n, LgScalars* sc, double* ab,
                                                      int w) {
-  pdl_wait();
+  pdl_wait(16);
   __shared__ double red[kWarps];
   const double b1 = sqrt(cta_sum(part, n, red));
   if (threadIdx.x != 0) return;
   ab[w + 1] = b1;
   sc->bcur = b1;
+  sc->inv_next = 1.0 / b1;  // u_1 = p_0 / beta_1, applied by the first column FFT
 }
 
 __global__ void lg_init(LgScalars* sc, double* om, int w, int first_check, uint64_t seed, uint64_t series) {
-  pdl_wait();
+  pdl_wait(17);
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < 2 * (w + 1)) om[i] = (i == 1) ? 1.0 : 0.0;  // mu_1 = 1 (u_1)
   if (i == 0) {
@@ -454,14 +342,14 @@ __global__ void lg_init(LgScalars* sc, double* om, int w, int first_check, uint6
 
 // convergence test on B_m, m = j - 1 (tgk.cuh), on the device-side schedule (R7):
 // first at 2k, then every check_every steps stretched up to 2 check_every when the residual
-// decays geometrically; always at m_max and after the space was exhausted.  Sets halt and
-// the IF handle of half-step B.
+// decays geometrically; always at m_max and after the space was exhausted.  Sets halt (read
+// by lg_loop).  It runs concurrently with half-step B of the same step (a graph fork): B
+// does not wait for the test, and its results are simply unused when the loop halts.
 size_t lg_check_smem(int m_max) { return (size_t)(3 * (2 * m_max + 1) + 4 * kMaxK) * 8 + 64; }
 
 __global__ void __launch_bounds__(kThreads) lg_check(const double* __restrict__ ab, int w, int k, int m_max,
-                                                     int ce, double tol, double* scratch, LgScalars* sc,
-                                                     cudaGraphConditionalHandle h_b) {
-  pdl_wait();
+                                                     int ce, double tol, double* scratch, LgScalars* sc) {
+  pdl_wait(13);
   const int m = sc->j - 1;
   const bool due = m >= k && (m >= sc->next_check || m >= m_max || sc->stop);
   if (due) {
@@ -502,36 +390,42 @@ __global__ void __launch_bounds__(kThreads) lg_check(const double* __restrict__ 
   sc->m = m;
   const int halt = (due && (sc->conv || sc->stop)) || m >= m_max;
   sc->halt = halt;
-  cudaGraphSetConditional(h_b, halt ? 0u : 1u);
 }
 
 // end of a step: j advances unless the loop stops; the WHILE condition
 __global__ void lg_loop(LgScalars* sc, cudaGraphConditionalHandle h_while) {
+  trace_point(14);
   if (threadIdx.x != 0) return;
   const int go = !sc->halt;
   if (go) sc->j += 1;
   cudaGraphSetConditional(h_while, go ? 1u : 0u);
 }
 
-// Ritz vectors: out[i][t] = sum_row coef[row][i] basis[row][t], one element per thread
-// (U_k = U_{m+1} P_k, V_k = V_m Q_k, Eq. (1)), triples in blocks of
-// kRitzK (blockIdx.y).  The coefficient rows are staged through a fixed shared-memory tile
-// of kRitzRows rows (zero-padded to kRitzK per row, read as broadcast 16-byte loads), so
-// the kernel's shared memory does not depend on the step count m.
+// Ritz vectors: out[i][t] = sum_row coef[row][i] basis[row][t] (U_k = U_{m+1} P_k,
+// V_k = V_m Q_k, Eq. (1)), triples in blocks of kRitzK (blockIdx.y).  A
+// dense contraction (2 kRitzK flops per basis element read): each thread owns kRitzE
+// elements, so each coefficient pair read from shared memory (a broadcast 16-byte load)
+// feeds 2 kRitzE FMAs, and the basis loads of the next kRitzU rows are in flight while
+// the current ones are used.  The coefficient rows are staged through a fixed shared
+// tile of kRitzRows rows (zero-padded to kRitzK), so shared memory does not depend on m.
 constexpr int kRitzRows = 128;
 constexpr int kRitzK = 32;
+constexpr int kRitzE = 2;                     // elements per thread
+constexpr int kRitzSpan = kThreads * kRitzE;  // elements per CTA
 
 __global__ void __launch_bounds__(kThreads) lg_ritz(const double* __restrict__ basis, int ld, int add_rows,
                                                     const int* __restrict__ state, const double* __restrict__ coef,
                                                     int k, int n, double* out, double* amax, int* aidx) {
-  pdl_wait();
+  pdl_wait(15);
   const int rows = state[0] + add_rows;  // U_{m+1} (add 1) or V_m (add 0); m from the device
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int tb = blockIdx.x * kRitzSpan + threadIdx.x;
   const int i0 = blockIdx.y * kRitzK, ki = min(kRitzK, k - i0);
   __shared__ __align__(16) double cs[kRitzRows * kRitzK];
-  double acc[kRitzK];
+  double acc[kRitzE][kRitzK];
 #pragma unroll
-  for (int i = 0; i < kRitzK; ++i) acc[i] = 0.0;
+  for (int e = 0; e < kRitzE; ++e)
+#pragma unroll
+    for (int i = 0; i < kRitzK; ++i) acc[e][i] = 0.0;
   for (int r0 = 0; r0 < rows; r0 += kRitzRows) {
     const int nr = min(kRitzRows, rows - r0);
     __syncthreads();
@@ -540,23 +434,35 @@ __global__ void __launch_bounds__(kThreads) lg_ritz(const double* __restrict__ b
       cs[e] = (i < ki) ? __ldg(coef + (size_t)(r0 + r) * k + i0 + i) : 0.0;
     }
     __syncthreads();
-    if (t < n) {
-      for (int row = 0; row < nr; ++row) {
-        const double x = __ldcs(basis + (size_t)(r0 + row) * ld + t);
-        const double2* cr = reinterpret_cast<const double2*>(cs + (size_t)row * kRitzK);
+    const double* bp = basis + (size_t)r0 * ld;
+#pragma unroll 4
+    for (int row = 0; row < nr; ++row) {
+      double x[kRitzE];
 #pragma unroll
-        for (int i = 0; i < kRitzK / 2; ++i) {
-          const double2 c = cr[i];
-          acc[2 * i] = fma(c.x, x, acc[2 * i]);
-          acc[2 * i + 1] = fma(c.y, x, acc[2 * i + 1]);
+      for (int e = 0; e < kRitzE; ++e) {
+        const int t = tb + e * kThreads;
+        x[e] = (t < n) ? __ldcs(bp + (size_t)row * ld + t) : 0.0;
+      }
+      const double2* cr = reinterpret_cast<const double2*>(cs + (size_t)row * kRitzK);
+#pragma unroll
+      for (int i = 0; i < kRitzK / 2; ++i) {
+        const double2 c = cr[i];
+#pragma unroll
+        for (int e = 0; e < kRitzE; ++e) {
+          acc[e][2 * i] = fma(c.x, x[e], acc[e][2 * i]);
+          acc[e][2 * i + 1] = fma(c.y, x[e], acc[e][2 * i + 1]);
         }
       }
     }
   }
-  if (t < n) {
 #pragma unroll
-    for (int i = 0; i < kRitzK; ++i)
-      if (i < ki) out[(size_t)(i0 + i) * n + t] = acc[i];
+  for (int e = 0; e < kRitzE; ++e) {
+    const int t = tb + e * kThreads;
+    if (t < n) {
+#pragma unroll
+      for (int i = 0; i < kRitzK; ++i)
+        if (i < ki) out[(size_t)(i0 + i) * n + t] = acc[e][i];
+    }
   }
   if (amax) {
     // per-CTA argmax |out_i| (lowest index on ties) for sign canonicalization
@@ -566,8 +472,14 @@ __global__ void __launch_bounds__(kThreads) lg_ritz(const double* __restrict__ b
 #pragma unroll
     for (int i = 0; i < kRitzK; ++i) {
       if (i >= ki) break;
-      double v = (t < n) ? fabs(acc[i]) : -1.0;
-      int ix = t;
+      double v = -1.0;
+      int ix = 0x7fffffff;
+#pragma unroll
+      for (int e = 0; e < kRitzE; ++e) {  // increasing t: ties keep the lower index
+        const int t = tb + e * kThreads;
+        const double a = (t < n) ? fabs(acc[e][i]) : -1.0;
+        if (a > v) { v = a; ix = t; }
+      }
       for (int o = 16; o > 0; o >>= 1) {
         double v2 = __shfl_xor_sync(0xffffffffu, v, o);
         int i2 = __shfl_xor_sync(0xffffffffu, ix, o);
@@ -590,23 +502,30 @@ __global__ void __launch_bounds__(kThreads) lg_ritz(const double* __restrict__ b
   }
 }
 
+// sign of each Ritz pair from the largest-|.| entry of u_i (lowest index on ties): one warp
+// per triple over the per-CTA candidates of lg_ritz
 __global__ void lg_sign(const double* __restrict__ amax, const int* __restrict__ aidx, int nblk, int k,
                         const double* __restrict__ U, int L, double* sgn) {
-  pdl_wait();
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  pdl_wait(18);
+  const int i = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
   if (i >= k) return;
   double v = -1.0;
   int ix = 0x7fffffff;
-  for (int b = 0; b < nblk; ++b) {
+  for (int b = lane; b < nblk; b += 32) {
     const double v2 = amax[(size_t)b * k + i];
     const int i2 = aidx[(size_t)b * k + i];
     if (v2 > v || (v2 == v && i2 < ix)) { v = v2; ix = i2; }
   }
-  sgn[i] = (ix < L && U[(size_t)i * L + ix] < 0.0) ? -1.0 : 1.0;
+  for (int o = 16; o > 0; o >>= 1) {
+    const double v2 = __shfl_xor_sync(0xffffffffu, v, o);
+    const int i2 = __shfl_xor_sync(0xffffffffu, ix, o);
+    if (v2 > v || (v2 == v && i2 < ix)) { v = v2; ix = i2; }
+  }
+  if (lane == 0) sgn[i] = (ix < L && U[(size_t)i * L + ix] < 0.0) ? -1.0 : 1.0;
 }
 
 __global__ void lg_flip(double* X, int n, int k, const double* __restrict__ sgn) {
-  pdl_wait();
+  pdl_wait(19);
   const size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (size_t)n * k) return;
   const int i = (int)(idx / n);
@@ -614,7 +533,7 @@ __global__ void lg_flip(double* X, int n, int k, const double* __restrict__ sgn)
 }
 
 __global__ void lg_finite(const double* __restrict__ f, int N, int* state) {
-  pdl_wait();
+  pdl_wait(20);
   int bad = 0;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) bad |= !isfinite(f[i]);
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(state + 5, 1);
@@ -629,7 +548,7 @@ cudaError_t large_lanczos_set_attributes(int m_max) {
 }
 
 __global__ void lg_state(const LgScalars* sc, int* state) {
-  pdl_wait();
+  pdl_wait(21);
   if (threadIdx.x != 0) return;
   state[0] = sc->m;
   state[1] = sc->conv;
@@ -692,15 +611,19 @@ static cudaError_t build_lanczos_graph(Plan& p) {
   const size_t nchmax = (size_t)(std::max(ldL, ldK) + kRoChunk - 1) / kRoChunk;
   double* cpart = part + nchmax * (p.m_max + 2);
   double* spart = cpart + 1024;
+  double* gpart = spart + 1024;
   double* h = p.d_lgh;
   double* r = p.d_lgr;
   const int mode = p.opt.reorth;
   const double eta = p.opt.reorth_eta;
   const size_t dots_smem = (size_t)(p.m_max + 2) * kWarps * 8, upd_smem = (size_t)(p.m_max + 2) * 8;
   const int ce = p.opt.check_every > 0 ? p.opt.check_every : 4;
-  cudaStream_t cs[4] = {};
+  const int exp_bits = getenv("SSA_LG_EXP") ? atoi(getenv("SSA_LG_EXP")) : 0;  // graph-shape experiments
+  cudaStream_t cs[5] = {};
+  cudaEvent_t ev[2] = {};
   cudaError_t e = cudaSuccess;
-  for (int i = 0; i < 4 && e == cudaSuccess; ++i) e = cudaStreamCreateWithFlags(&cs[i], cudaStreamNonBlocking);
+  for (int i = 0; i < 5 && e == cudaSuccess; ++i) e = cudaStreamCreateWithFlags(&cs[i], cudaStreamNonBlocking);
+  for (int i = 0; i < 2 && e == cudaSuccess; ++i) e = cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming);
   cudaGraph_t g0 = nullptr;
   if (e == cudaSuccess) e = cudaGraphCreate(&g0, 0);
   cudaGraphConditionalHandle hw;
@@ -713,69 +636,85 @@ static cudaError_t build_lanczos_graph(Plan& p) {
   cudaGraphNode_t wnode;
   if (e == cudaSuccess) e = cudaGraphAddNode(&wnode, g0, nullptr, 0, &wp);
 
-  // reorthogonalization pass against the side's basis (CGS: dots, then update)
-  auto ro_pass = [&](cudaStream_t s, int side) {
+  // reorthogonalization pass against the side's basis (CGS: dots, then update; the last
+  // CTA of the update finishes the pass, pass < 0: restart passes, no finish), gated on
+  // the device (lg_open)
+  auto ro_pass = [&](cudaStream_t s, int side, int pass, int gate, cudaGraphConditionalHandle hfx) {
     const double* basis = side == 0 ? p.d_V : p.d_U;
     const int ld = side == 0 ? ldK : ldL;
     const int nch = (ld + kRoChunk - 1) / kRoChunk;
-    launch_pdl(lg_dots, dim3(nch), dim3(kThreads), dots_smem, s, basis, ld, side, r, part, nch, h, sc);
-    launch_pdl(lg_update, dim3(nch), dim3(kThreads), upd_smem, s, basis, ld, side, h, r, part, sc);
+    if (exp_bits & 1) {  // experiment: the dots pass without a programmatic dependency
+      lg_dots<<<nch, kThreads, dots_smem, s>>>(basis, ld, side, (const double*)r, part, gpart, nch, h, sc, gate);
+    } else {
+      launch_pdl(lg_dots, dim3(nch), dim3(kThreads), dots_smem, s, basis, ld, side, (const double*)r, part, gpart, nch,
+                 h, sc, gate);
+    }
+    launch_pdl(lg_update, dim3(nch), dim3(kThreads), upd_smem, s, basis, ld, side, (const double*)h, r, part, sc, pass,
+               gate, mode, ab, w, hfx);
     return nch;
   };
-  // one half-step on stream s (nested bodies on s1, s2)
+  // one half-step on stream s (the fix-up body on s1): the column FFT first normalizes
+  // the previous half-step's vector (r * inv_next -> basis row j - 1 and the current
+  // vector of that side); the correlation's last CTA takes the reorthogonalization
+  // decision (lg_pro_tail); the reorthogonalization pass runs gated on it; one IF node
+  // holds the rare fix-ups (DGKS second pass, breakdown restart), its handle set by
+  // whichever tail took the decision.
   auto half = [&](cudaStream_t s, int side, cudaStream_t s1, cudaStream_t s2) -> cudaError_t {
     const bool A = side == 0;
-    double* cur = A ? p.d_vcur : p.d_ucur;
-    double* basis = A ? p.d_V : p.d_U;
     const int n = A ? K : L, ld = A ? ldK : ldL, nch = (ld + kRoChunk - 1) / kRoChunk;
-    cudaError_t err = large_correlate(p, p.d_spec, 0, A ? p.d_ucur : p.d_vcur, 0, A ? L : K, r, 0, n, ld,
-                                      A ? p.d_vcur : p.d_ucur, 0,
-                                      A ? &sc->bcur : &sc->acur, cpart, 1, s, nullptr);
+    cudaGraphConditionalHandle hfx;
+    cudaError_t err = cond_handle(s, &hfx);
     if (err != cudaSuccess) return err;
-    cudaGraphConditionalHandle hro, hrs;
-    if ((err = cond_handle(s, &hro)) != cudaSuccess) return err;
-    launch_pdl(lg_pro, dim3(1), dim3(kThreads), 0, s, cpart, ncol, side, sc, ab, w, p.d_lgom, mode, eta, hro);
-    err = cond_if(s, hro, s1, [&](cudaStream_t sb) -> cudaError_t {
-      ro_pass(sb, side);
-      cudaGraphConditionalHandle hag;
-      cudaError_t e2 = cond_handle(sb, &hag);
-      if (e2 != cudaSuccess) return e2;
-      launch_pdl(lg_finish, dim3(1), dim3(kThreads), 0, sb, part, nch, side, sc, 0, mode, ab, w, hag);
-      return cond_if(sb, hag, s2, [&](cudaStream_t sc2) -> cudaError_t {
-        ro_pass(sc2, side);
-        launch_pdl(lg_finish, dim3(1), dim3(kThreads), 0, sc2, part, nch, side, sc, 1, mode, ab, w, hag);
+    // input: the other side's vector (u_j for A, v_j for B), normalized on the fly
+    LgNorm nrm{&sc->inv_next, &sc->j, A ? p.d_U : p.d_V, A ? p.d_ucur : p.d_vcur, A ? ldL : ldK};
+    LgProTail tail{sc, side, ab, w, p.d_lgom, mode, eta, hfx, 0, 0};
+    cudaGraphConditionalHandle hro = 0;
+    if (exp_bits & 2) {
+      if ((err = cond_handle(s, &hro)) != cudaSuccess) return err;
+      tail.has_ro = 1;
+      tail.h_ro = hro;
+    }
+    err = large_correlate_lanczos(p, p.d_spec, r, A ? L : K, nrm, r, n, ld, A ? p.d_vcur : p.d_ucur,
+                                  A ? &sc->bcur : &sc->acur, cpart, tail, s);
+    if (err != cudaSuccess) return err;
+    if (exp_bits & 2) {
+      err = cond_if(s, hro, s2, [&](cudaStream_t sb) -> cudaError_t {
+        ro_pass(sb, side, 0, 0, hfx);
         return cudaGetLastError();
       });
-    });
-    if (err != cudaSuccess) return err;
-    if ((err = cond_handle(s, &hrs)) != cudaSuccess) return err;
-    lg_restart_gate<<<1, 32, 0, s>>>(sc, hrs);
-    err = cond_if(s, hrs, s1, [&](cudaStream_t sb) -> cudaError_t {
+      if (err != cudaSuccess) return err;
+    } else {
+      ro_pass(s, side, 0, 0, hfx);
+    }
+    return cond_if(s, hfx, s1, [&](cudaStream_t sb) -> cudaError_t {
+      ro_pass(sb, side, 1, 1, hfx);  // DGKS second pass (gate: again)
       const int nst = (ld + kLgChunk - 1) / kLgChunk;
       launch_pdl(lg_start, dim3(nst), dim3(kThreads), 0, sb, r, n, ld, (uint64_t)0, (uint64_t)0, spart,
                  (const LgScalars*)sc);
-      ro_pass(sb, side);
-      ro_pass(sb, side);
-      launch_pdl(lg_restart_norm, dim3(1), dim3(kThreads), 0, sb, part, nch, spart, nst, sc, side, p.d_lgom, w);
+      ro_pass(sb, side, -1, 2, hfx);  // restart vector, orthogonalized twice (gate: restart)
+      ro_pass(sb, side, -1, 2, hfx);
+      launch_pdl(lg_restart_norm, dim3(1), dim3(kThreads), 0, sb, (const double*)part, nch, (const double*)spart, nst,
+                 sc, side, p.d_lgom, w);
       return cudaGetLastError();
     });
-    if (err != cudaSuccess) return err;
-    launch_pdl(lg_normalize, dim3((ld + kThreads - 1) / kThreads), dim3(kThreads), 0, s, r, n, ld, side, -1,
-               (const LgScalars*)sc, (const double*)ab, w, basis, cur);
-    return cudaGetLastError();
   };
 
   cudaGraph_t body = wp.conditional.phGraph_out[0];
   if (e == cudaSuccess) e = cudaStreamBeginCaptureToGraph(cs[0], body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed);
   if (e == cudaSuccess) {
     cudaError_t eb = half(cs[0], 0, cs[1], cs[2]);
-    cudaGraphConditionalHandle hb;
-    if (eb == cudaSuccess) eb = cond_handle(cs[0], &hb);
+    // fork: the convergence test on B_m (one CTA, cs[4]) runs beside half-step B (the rest
+    // of the GPU); join before lg_loop
+    if (eb == cudaSuccess) eb = cudaEventRecord(ev[0], cs[0]);
+    if (eb == cudaSuccess) eb = cudaStreamWaitEvent(cs[4], ev[0], 0);
     if (eb == cudaSuccess) {
-      launch_pdl(lg_check, dim3(1), dim3(kThreads), lg_check_smem(p.m_max), cs[0], (const double*)ab, w, k, p.m_max,
-                 ce, p.opt.tol, p.d_tgk, sc, hb);
-      eb = cond_if(cs[0], hb, cs[1], [&](cudaStream_t sb) { return half(sb, 1, cs[2], cs[3]); });
+      lg_check<<<1, kThreads, lg_check_smem(p.m_max), cs[4]>>>((const double*)ab, w, k, p.m_max, ce, p.opt.tol,
+                                                              p.d_tgk, sc);
+      eb = cudaGetLastError();
     }
+    if (eb == cudaSuccess) eb = cudaEventRecord(ev[1], cs[4]);
+    if (eb == cudaSuccess) eb = half(cs[0], 1, cs[1], cs[2]);
+    if (eb == cudaSuccess) eb = cudaStreamWaitEvent(cs[0], ev[1], 0);
     if (eb == cudaSuccess) {
       lg_loop<<<1, 32, 0, cs[0]>>>(sc, hw);
       eb = cudaGetLastError();
@@ -787,8 +726,10 @@ static cudaError_t build_lanczos_graph(Plan& p) {
   if (e == cudaSuccess) e = cudaGraphInstantiate(&p.lg_exec, g0, 0);
   if (e == cudaSuccess) p.lg_graph = g0;
   else if (g0) cudaGraphDestroy(g0);
-  for (int i = 0; i < 4; ++i)
+  for (int i = 0; i < 5; ++i)
     if (cs[i]) cudaStreamDestroy(cs[i]);
+  for (int i = 0; i < 2; ++i)
+    if (ev[i]) cudaEventDestroy(ev[i]);
   return e;
 }
 
@@ -809,6 +750,53 @@ cudaError_t large_graph_build(Plan& p) {
   if (getenv("SSA_DEBUG")) fprintf(stderr, "[ssa] long-series loop graph: %s, PDL %s\n", cudaGetErrorString(e),
                                    p.lg_pdl ? "on" : "off");
   return e;
+}
+
+// SSA_TRACE diagnostics (trace_point in device_common.cuh): a device buffer of kTraceMax
+// records, and a report on stderr of the time from each traced kernel's start to the next
+// traced start, summed per kernel id (this synchronizes the stream: diagnostics only).
+static unsigned long long* trace_buffer() {
+  static unsigned long long* buf = nullptr;
+  if (!getenv("SSA_TRACE")) return nullptr;
+  if (!buf && cudaMalloc(&buf, (size_t)(2 * kTraceMax + 1) * 8) != cudaSuccess) buf = nullptr;
+  return buf;
+}
+
+static void trace_report(unsigned long long* trace, cudaStream_t s) {
+  static const char* names[32] = {"?", "lg_col_fwd", "lg_row_cta", "lg_row_warp", "lg_col_inv", "-", "lg_dots",
+                                  "lg_update", "-", "-", "lg_start", "lg_restart_norm",
+                                  "-", "lg_check", "lg_loop", "lg_ritz", "lg_beta1", "lg_init", "lg_sign",
+                                  "lg_flip", "lg_finite", "lg_state"};
+  cudaStreamSynchronize(s);
+  unsigned long long n = 0;
+  cudaMemcpy(&n, trace, 8, cudaMemcpyDeviceToHost);
+  n = std::min<unsigned long long>(n, kTraceMax);
+  std::vector<unsigned long long> rec(2 * n);
+  cudaMemcpy(rec.data(), trace + 1, 2 * n * 8, cudaMemcpyDeviceToHost);
+  trace_attach(nullptr);
+  trace_attach_fft(nullptr);
+  std::vector<std::pair<unsigned long long, int>> ev(n);
+  for (size_t i = 0; i < n; ++i) ev[i] = {rec[2 * i], (int)rec[2 * i + 1]};
+  std::sort(ev.begin(), ev.end());
+  double tot[32] = {0};
+  int cnt[32] = {0};
+  for (size_t i = 0; i + 1 < n; ++i) {
+    const int id = ev[i].second & 31;
+    tot[id] += 1e-3 * (double)(ev[i + 1].first - ev[i].first);
+    cnt[id] += 1;
+  }
+  const double span = n > 1 ? 1e-3 * (double)(ev[n - 1].first - ev[0].first) : 0.0;
+  if (getenv("SSA_TRACE_SEQ")) {  // the raw sequence of a window of records
+    const size_t a0 = std::min<size_t>(n, (size_t)atoi(getenv("SSA_TRACE_SEQ")));
+    for (size_t i = a0; i + 1 < n && i < a0 + 40; ++i)
+      fprintf(stderr, "[ssa seq] %5zu %-16s %8.2f us\n", i, names[ev[i].second & 31],
+              1e-3 * (double)(ev[i + 1].first - ev[i].first));
+  }
+  fprintf(stderr, "[ssa trace] %llu kernels, %.1f us from first to last start\n", n, span);
+  for (int id = 0; id < 32; ++id)
+    if (cnt[id])
+      fprintf(stderr, "[ssa trace] %-16s %6d x %8.2f us = %9.1f us (%4.1f%%)\n", names[id], cnt[id], tot[id] / cnt[id],
+              tot[id], 100.0 * tot[id] / span);
 }
 
 // One long series b of the call: decompose into sigma/U/V (+info).  Everything is enqueued
@@ -832,6 +820,11 @@ cudaError_t large_decompose_one(Plan& p, const DecomposeArgs& a0, int b, cudaStr
   double* r = p.d_lgr;
   cudaError_t e;
   if ((e = large_graph_build(p))) return e;
+  unsigned long long* trace = nullptr;
+  if ((trace = trace_buffer()) != nullptr) {
+    if ((e = cudaMemsetAsync(trace, 0, 8, s))) return e;
+    if ((e = trace_attach(trace)) || (e = trace_attach_fft(trace))) return e;
+  }
   if ((e = cudaMemsetAsync(p.d_state, 0, kStateInts * sizeof(int), s))) return e;
   launch_pdl(lg_finite, dim3(64), dim3(kThreads), 0, s, a.series + (size_t)b * N, N, p.d_state);
   if ((e = large_spectrum(p, a.series + (size_t)b * N, p.d_spec, 1, s))) return e;
@@ -844,8 +837,6 @@ cudaError_t large_decompose_one(Plan& p, const DecomposeArgs& a0, int b, cudaStr
   // Alg. 1 lines 1-2: beta_1 = |p0|, u_1 = p0 / beta_1 (row 0 of U and the current u)
   launch_pdl(lg_start, dim3(nchL), dim3(kThreads), 0, s, r, L, ldL, a.seed, series, spart, (const LgScalars*)nullptr);
   launch_pdl(lg_beta1, dim3(1), dim3(kThreads), 0, s, (const double*)spart, nchL, sc, p.d_ab, w);
-  launch_pdl(lg_normalize, dim3((ldL + kThreads - 1) / kThreads), dim3(kThreads), 0, s, (const double*)r, L, ldL, 1, 0,
-             (const LgScalars*)sc, (const double*)p.d_ab, w, U, p.d_ucur);
   if ((e = cudaGraphLaunch(p.lg_exec, s))) return e;
   launch_pdl(lg_state, dim3(1), dim3(32), 0, s, (const LgScalars*)sc, p.d_state);
   // ---- bidiagonal SVD (reuses the batched kernel with one series) ----
@@ -857,7 +848,7 @@ cudaError_t large_decompose_one(Plan& p, const DecomposeArgs& a0, int b, cudaStr
   const double* cQ = p.d_coef + (size_t)mstride * k;
   double* Uo = a.Uout + (size_t)b * k * L;
   double* Vo = a.Vout + (size_t)b * k * K;
-  const int gU = (L + kThreads - 1) / kThreads, gV = (K + kThreads - 1) / kThreads;
+  const int gU = (L + kRitzSpan - 1) / kRitzSpan, gV = (K + kRitzSpan - 1) / kRitzSpan;
   double* amax = p.d_lgpart;
   int* aidx = reinterpret_cast<int*>(p.d_lgpart + (size_t)gU * k);
   // the Ritz kernel reads the step count m from the state word the SVD kernel used
@@ -866,11 +857,12 @@ cudaError_t large_decompose_one(Plan& p, const DecomposeArgs& a0, int b, cudaStr
              Uo, amax, aidx);
   launch_pdl(lg_ritz, dim3(gV, kb), dim3(kThreads), 0, s, (const double*)V, ldK, 0, (const int*)p.d_state, cQ, k, K,
              Vo, (double*)nullptr, (int*)nullptr);
-  launch_pdl(lg_sign, dim3((k + 31) / 32), dim3(32), 0, s, (const double*)amax, (const int*)aidx, gU, k, (const double*)Uo, L, h);
+  launch_pdl(lg_sign, dim3((k + 7) / 8), dim3(256), 0, s, (const double*)amax, (const int*)aidx, gU, k, (const double*)Uo, L, h);
   launch_pdl(lg_flip, dim3((int)(((size_t)L * k + kThreads - 1) / kThreads)), dim3(kThreads), 0, s, Uo, L, k,
              (const double*)h);
   launch_pdl(lg_flip, dim3((int)(((size_t)K * k + kThreads - 1) / kThreads)), dim3(kThreads), 0, s, Vo, K, k,
              (const double*)h);
+  if (trace) trace_report(trace, s);
   return cudaGetLastError();
 }
 

@@ -58,6 +58,7 @@ __global__ void __launch_bounds__(kSvdWarps * 32) bidiag_svd_kernel(const Decomp
       }
       continue;
     }
+    if (st[7]) continue;  // the Lanczos kernel already did the final SVD (thick restart)
     long long t0 = clock64();
     int nL = 0, nR = 0, it = 0;
     double fres = 0.0;
@@ -296,7 +297,8 @@ __global__ void __launch_bounds__(kThreads, 2) ritz_kernel(const DecomposeArgs a
     const double* cP = a.coef + (size_t)bl * 2 * mstride * k;
     for (int side = 0; side < 2; ++side) {
       const bool isU = side == 0;
-      const int n = isU ? L : K, ld = isU ? a.ldL : a.ldK, rows = isU ? m + 1 : m;
+      // U rows: m + 1 (B_m of Alg. 1), or st[11] after a thick restart (lanczos_trl.cuh)
+      const int n = isU ? L : K, ld = isU ? a.ldL : a.ldK, rows = isU ? (st[11] > 0 ? st[11] : m + 1) : m;
       const double* basis = isU ? a.U + (size_t)bl * (a.m_max + 1) * a.ldL : a.V + (size_t)bl * (a.m_max + 1) * a.ldK;
       const double* coef = cP + (isU ? 0 : (size_t)mstride * k);
       double* out = (isU ? a.Uout : a.Vout) + (size_t)b * k * n;

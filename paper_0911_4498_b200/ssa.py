@@ -40,7 +40,8 @@ class SsaError(RuntimeError):
 class Options(ctypes.Structure):
     _fields_ = [("tol", ctypes.c_double), ("max_steps", ctypes.c_int32), ("check_every", ctypes.c_int32),
                 ("seed", ctypes.c_uint64), ("reorth", ctypes.c_int32), ("reserved", ctypes.c_int32),
-                ("reorth_eta", ctypes.c_double), ("series_base", ctypes.c_int64)]
+                ("reorth_eta", ctypes.c_double), ("series_base", ctypes.c_int64), ("restart_dim", ctypes.c_int32),
+                ("restart_keep", ctypes.c_int32)]
 
 
 class SeriesInfo(ctypes.Structure):
@@ -151,7 +152,7 @@ class Plan:
     def __init__(self, N: int, L: int, k: int, batch: int, *, tol: float = 1e-12, max_steps: int = 0,
                  check_every: int = 4, seed: int = 42, reorth: int = 3, reorth_eta: float = 0.0,
                  series_base: int = 0, device: int | None = None, profile: bool = False, svd: str = "tgk",
-                 force_long: bool = False):
+                 force_long: bool = False, restart_dim: int = 0, restart_keep: int = 0):
         import torch
         lib = load_library()
         if not torch.cuda.is_available():
@@ -163,6 +164,7 @@ class Plan:
         if reorth_eta > 0.0:
             opt.reorth_eta = reorth_eta
         opt.series_base = int(series_base)
+        opt.restart_dim, opt.restart_keep = int(restart_dim), int(restart_keep)
         opt.reserved = (1 if profile else 0) | (2 if svd == "qr" else 0) | (4 if force_long else 0)
         h = ctypes.c_void_p()
         _check(lib.ssa_plan_create(N, L, k, batch, ctypes.byref(opt), self.device, ctypes.byref(h)))

@@ -6,6 +6,8 @@
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/graph_overhead tools/graph_overhead.cu
 #include <cuda_runtime.h>
 #include <stdio.h>
+#include <cooperative_groups.h>
+namespace cg = cooperative_groups;
 
 #define CK(x)                                                                      \
   do {                                                                             \
@@ -28,6 +30,12 @@ __global__ void k_loop(cudaGraphConditionalHandle h, int* it, int n) {
     int v = ++*it;
     cudaGraphSetConditional(h, v < n ? 1u : 0u);
   }
+}
+
+__global__ void k_gridsync(int n, int* c) {
+  cg::grid_group g = cg::this_grid();
+  for (int i = 0; i < n; ++i) g.sync();
+  if (c && threadIdx.x == 0 && blockIdx.x == 0) *c = n;
 }
 
 static bool g_pdl = true;
@@ -138,6 +146,22 @@ int main() {
              c[1], c[2], 1e3 * ms / iters, 1e3 * ms / iters / (nker + c[1]));
       CK(cudaGraphExecDestroy(ex));
     }
+  }
+  // grid-wide barrier of a cooperative persistent kernel (the alternative to a graph)
+  int sms = 0;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+  for (int per = 1; per <= 4; per *= 2) {
+    int n = 2000;
+    void* args[] = {&n, &it};
+    float ms = 0;
+    for (int w = 0; w < 2; ++w) {
+      CK(cudaEventRecord(a, s));
+      CK(cudaLaunchCooperativeKernel((void*)k_gridsync, dim3(sms * per), dim3(256), args, 0, s));
+      CK(cudaEventRecord(b, s));
+      CK(cudaEventSynchronize(b));
+    }
+    CK(cudaEventElapsedTime(&ms, a, b));
+    printf("grid.sync %d CTAs x 256: %.2f us per barrier\n", sms * per, 1e3 * ms / n);
   }
   return 0;
 }
