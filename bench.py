@@ -53,6 +53,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--batch", type=int, default=CFG["batch"], help="global batch, sharded over the GPUs (4096)")
     ap.add_argument("--no-fro", action="store_true", help="skip the FRO comparison line")
+    ap.add_argument("--no-trl", action="store_true", help="skip the thick-restart line")
     ap.add_argument("--no-overshoot", action="store_true", help="skip the test-schedule overshoot probe")
     ap.add_argument("--no-weak", action="store_true", help="skip the weak-scaling line (N > 1)")
     ap.add_argument("--no-e2e", action="store_true")
@@ -556,7 +557,7 @@ def run_reference(args, rank):
 
 
 # ------------------------------------------------------------------------ our arm
-def run_cfg2(P, ctx, host, b0, reorth, steps, warmup, flush, clk=None):
+def run_cfg2(P, ctx, host, b0, reorth, steps, warmup, flush, clk=None, **plan_kw):
     """Time `steps` decompose + reconstruct steps of this rank's shard (host rows, global
     index b0 of row 0) with the given reorthogonalization; returns a dict of results."""
     import torch
@@ -564,7 +565,7 @@ def run_cfg2(P, ctx, host, b0, reorth, steps, warmup, flush, clk=None):
     K = N - L + 1
     B = host.shape[0]
     series = torch.from_numpy(host).cuda()
-    plan = P.Plan(N, L, k, B, reorth=reorth, series_base=b0)
+    plan = P.Plan(N, L, k, B, reorth=reorth, series_base=b0, **plan_kw)
     sigma = torch.empty((B, k), dtype=torch.float64, device="cuda")
     U = torch.empty((B, k, L), dtype=torch.float64, device="cuda")
     V = torch.empty((B, k, K), dtype=torch.float64, device="cuda")
@@ -735,6 +736,32 @@ def main():
                                     "unit": "GB/s", "frac": algf / (lanf * 1e-3) / 1e9 / peak}}
         rf["plan"].close()
         del rf
+        torch.cuda.empty_cache()
+
+    # thick restart: Krylov dimension d = 40, keep
+    # p = 20 (the numpy model's trl:40:20, tools/model_reorth.py), FRO inside a cycle
+    if not args.no_trl:
+        d_trl, p_trl = 40, 20
+        rt = run_cfg2(P, ctx, host, b0, 1, 2, 1, flush, restart_dim=d_trl, restart_keep=p_trl)
+        inft = rt["inf"]
+        mt = inft["steps"].astype(np.int64)
+        thick = inft["reserved"].astype(np.int64)
+        # CGS rows from the info counters + each restart's in-place rotation of both bases
+        # (read d + 1 rows, write p (+1) rows per side)
+        rot_b = float((thick * 8 * ((d_trl + 1 + p_trl) * L + (d_trl + 2 + p_trl) * K)).sum())
+        algt = lanczos_alg_bytes(mt, inft["rows_u"], inft["rows_v"], N, L) + rot_b
+        lant = rt["phase_ms"]["lanczos"]
+        line["trl"] = {"value": triples / (rt["ms"] * 1e-3), "ms_per_step": rt["ms"], "restart_dim": d_trl,
+                       "restart_keep": p_trl, "lanczos_steps_mean": float(mt.mean()),
+                       "thick_restarts_mean": float(thick.mean()), "converged_fraction": float(inft["converged"].mean()),
+                       "max_residual": float(inft["max_residual"].max()),
+                       "lanczos_bytes_per_series": algt / B,
+                       "basis_bytes_per_series": 8 * (d_trl + 1) * (L + K),
+                       "basis_bytes_per_series_unrestarted": 8 * (max(256, 8 * k) + 1) * (L + K),
+                       "roofline": {"kernel": "lanczos_trl_kernel", "achieved": algt / (lant * 1e-3) / 1e9,
+                                    "peak": peak, "unit": "GB/s", "frac": algt / (lant * 1e-3) / 1e9 / peak}}
+        rt["plan"].close()
+        del rt
         torch.cuda.empty_cache()
 
     # overshoot of the convergence-test schedule: the first 256 series
