@@ -271,6 +271,8 @@ __global__ void __launch_bounds__(kThreads, 2) lanczos_trl_kernel(const Decompos
         const double om0 = sg[ord[0]];
         const double rel = (om0 > 0.0) ? mr / om0 : 0.0;
         const bool conv = rel <= 0.5 * a.tol;
+        // every warp has read sg / ord / W before the next correlation overwrites region A
+        if (!(conv || last || full)) __syncthreads();
         if (conv || last) {
           // final: sigma and the Ritz coefficients P_k (nu rows), Q_k (nc rows) for ritz_kernel
           double* cP = a.coef + (size_t)bl * 2 * (a.m_max + 2) * k;
