@@ -26,12 +26,21 @@ __device__ __forceinline__ int rr_player(int pos, int round, int n2) {
 
 // One-sided (Hestenes) Jacobi SVD of T_c = T[0:nu][0:nc] (row-major, ldT) into W (column c
 // of the rotated matrix at W + c ldw, ldw >= nu) and Qm (column c at Qm + c nc): T_c Q = W,
-// sigma_c = |W_c|, P_c = W_c / sigma_c.  Round-robin pairs (one warp per pair), sweeps
-// until none rotates (|w_p . w_q| <= 1e-15 |w_p| |w_q|, the oracle's criterion).
-// ord[i] = column of the i-th largest sigma (ties by column index).
+// sigma_c = |W_c|, P_c = W_c / sigma_c.  Round-robin pairs, one half-warp (16 lanes) per
+// pair, so the 16 half-warps of the CTA rotate 16 pairs at once; sweeps until none
+// rotates (|w_p . w_q| <= 1e-15 |w_p| |w_q|, the oracle's criterion).  ord[i] = column of
+// the i-th largest sigma (ties by column index).
+__device__ __forceinline__ double half_sum(double v) {  // sum over the 16 lanes of a half-warp
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
 __device__ void trl_jacobi(const double* T, int ldT, int nu, int nc, double* W, int ldw, double* Qm, double* sig,
                            int* ord, int* redi) {
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
+  const int hw = 2 * w + (lane >> 4), hl = lane & 15;  // half-warp index, lane in it
+  constexpr int kHalfWarps = 2 * kWarps;
   for (int idx = tid; idx < nc * ldw; idx += blockDim.x) {
     const int c = idx / ldw, r = idx - c * ldw;
     W[idx] = (r < nu) ? T[r * ldT + c] : 0.0;
@@ -42,38 +51,40 @@ __device__ void trl_jacobi(const double* T, int ldT, int nu, int nc, double* W, 
   for (int sweep = 0; sweep < 60 && n2 >= 2; ++sweep) {
     int rot = 0;
     for (int round = 0; round < n2 - 1; ++round) {
-      for (int pi = w; pi < n2 / 2; pi += kWarps) {
+      for (int pb = 0; pb < n2 / 2; pb += kHalfWarps) {  // warp-uniform trip count
+        const int pi = pb + hw;
         int p = rr_player(pi, round, n2), q = rr_player(n2 - 1 - pi, round, n2);
-        if (p >= nc || q >= nc) continue;
+        const bool act = pi < n2 / 2 && p < nc && q < nc;  // both halves run the shuffles
         if (p > q) {
           const int t = p;
           p = q;
           q = t;
         }
-        double* wp = W + (size_t)p * ldw;
-        double* wq = W + (size_t)q * ldw;
+        double* wp = W + (size_t)(act ? p : 0) * ldw;
+        double* wq = W + (size_t)(act ? q : 0) * ldw;
         double a = 0.0, b = 0.0, c = 0.0;
-        for (int r = lane; r < nu; r += 32) {
-          const double x = wp[r], y = wq[r];
-          a = fma(x, x, a);
-          b = fma(y, y, b);
-          c = fma(x, y, c);
-        }
-        a = warp_sum(a);
-        b = warp_sum(b);
-        c = warp_sum(c);
-        if (c != 0.0 && fabs(c) > 1e-15 * sqrt(a * b)) {
+        if (act)
+          for (int r = hl; r < nu; r += 16) {
+            const double x = wp[r], y = wq[r];
+            a = fma(x, x, a);
+            b = fma(y, y, b);
+            c = fma(x, y, c);
+          }
+        a = half_sum(a);
+        b = half_sum(b);
+        c = half_sum(c);
+        if (act && c != 0.0 && fabs(c) > 1e-15 * sqrt(a * b)) {
           const double zeta = (b - a) / (2.0 * c);
           const double t = copysign(1.0, zeta) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
           const double cs = 1.0 / sqrt(fma(t, t, 1.0)), sn = cs * t;
-          for (int r = lane; r < nu; r += 32) {
+          for (int r = hl; r < nu; r += 16) {
             const double x = wp[r], y = wq[r];
             wp[r] = cs * x - sn * y;
             wq[r] = fma(sn, x, cs * y);
           }
           double* qp = Qm + (size_t)p * nc;
           double* qq = Qm + (size_t)q * nc;
-          for (int r = lane; r < nc; r += 32) {
+          for (int r = hl; r < nc; r += 16) {
             const double x = qp[r], y = qq[r];
             qp[r] = cs * x - sn * y;
             qq[r] = fma(sn, x, cs * y);
