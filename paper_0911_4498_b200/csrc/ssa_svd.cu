@@ -252,35 +252,31 @@ size_t tgk_svd_smem_bytes(int m_max) {
   return (size_t)(3 * (2 * m_max + 1) + 2 * kMaxK + kMaxK + 2 * kMaxK) * 8 + kClInts * 4 + 16;
 }
 
-// Ritz rings: kRitzStages chunks of at most 32 E = 64 columns (512 B) per warp in flight
-constexpr int kRitzStages = 8;
-constexpr int kRitzChunk = 64;
+// Ritz assembly U_k = U_{m+1} P_k, V_k = V_m Q_k (Eq. (1)): a dense
+// contraction of the basis (rows) with the coefficient block (16 triples at a time) that
+// reads every basis element once.  Each CTA takes one series at a time from the work
+// queue; for each side and 16-triple block, each thread owns kRitzE elements of a
+// kRitzE x 256-element column window, keeps their 16 partial outputs in registers and
+// streams the rows with plain coalesced loads, kRitzU rows (kRitzE kRitzU loads) in
+// flight; the coefficient rows are read from shared memory as broadcast 16-byte loads.
+constexpr int kRitzE = 2;   // elements per thread per window
+constexpr int kRitzU = 8;   // rows per unrolled group
 
-// shared memory: rings, then the 16-wide coefficient block of the current side
-// ((m_max + 1) rows x 16), then the sign scratch
 size_t ritz_smem_bytes(int ldL, int ldK, int k, int m_max) {
-  (void)k;
-  size_t s = (size_t)kWarps * kRitzStages * kRitzChunk * 8;
-  s += (size_t)(m_max + 2) * 16 * 8;
+  (void)ldL; (void)ldK; (void)k;
+  size_t s = (size_t)(m_max + 2) * 16 * 8;
   s += (size_t)kWarps * kMaxK * (8 + 4) + kMaxK * 8;
-  s += (size_t)kWarps * kRitzStages * 8;
   return align16(s) + 16;
 }
 
 __global__ void __launch_bounds__(kThreads, 2) ritz_kernel(const DecomposeArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
-  double* rings = reinterpret_cast<double*>(smem_raw);
-  double* scoef = rings + (size_t)kWarps * kRitzStages * kRitzChunk;  // [(m_max+2)][16]
+  double* scoef = reinterpret_cast<double*>(smem_raw);                 // [(m_max+2)][16]
   double* mxv = scoef + (size_t)(a.m_max + 2) * 16;                    // [kWarps][kMaxK]
   double* sgn = mxv + kWarps * kMaxK;                                  // [kMaxK]
   int* mxi = reinterpret_cast<int*>(sgn + kMaxK);                      // [kWarps][kMaxK]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(mxi + kWarps * kMaxK);
   __shared__ int sb;
-  WarpRing rg;
-  ring_init<kRitzStages>(rg, rings + (size_t)w * kRitzStages * kRitzChunk, bars + w * kRitzStages);
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  __syncthreads();
   const int L = a.L, K = a.K, k = a.k;
   const int mstride = a.m_max + 2;
   unsigned long long t0 = clock64();
@@ -302,55 +298,66 @@ __global__ void __launch_bounds__(kThreads, 2) ritz_kernel(const DecomposeArgs a
       const double* basis = isU ? a.U + (size_t)bl * (a.m_max + 1) * a.ldL : a.V + (size_t)bl * (a.m_max + 1) * a.ldK;
       const double* coef = cP + (isU ? 0 : (size_t)mstride * k);
       double* out = (isU ? a.Uout : a.Vout) + (size_t)b * k * n;
-      const int slab = ld / kWarps;
-      const double* bw = basis + (size_t)w * slab;
-      constexpr int E = kRitzChunk / 32;
       for (int i0 = 0; i0 < k; i0 += 16) {
         const int ki = (k - i0) < 16 ? (k - i0) : 16;
-        // this block's coefficients (zero-filled to 16 columns) into shared memory: the
-        // inner loop then reads them as 8 broadcast 16-byte loads per row
         __syncthreads();
         for (int idx = tid; idx < rows * 16; idx += blockDim.x) {
           const int r = idx >> 4, i = idx & 15;
           scoef[idx] = (i < ki) ? __ldg(coef + (size_t)r * k + i0 + i) : 0.0;
         }
         __syncthreads();
-        for (int e0 = 0; e0 < slab; e0 += 32 * E) {
-          double acc[E][16];
+        for (int c0 = 0; c0 < n; c0 += kRitzE * kThreads) {
+          double acc[kRitzE][16];
 #pragma unroll
-          for (int t = 0; t < E; ++t)
+          for (int e = 0; e < kRitzE; ++e)
 #pragma unroll
-            for (int i = 0; i < 16; ++i) acc[t][i] = 0.0;
-          fence_proxy_async_smem();
-          __syncwarp();
-          // stream only this 32E-column chunk of each row: each basis byte is read once
-          // per block of 16 triples
-          const int cw = (slab - e0) < 32 * E ? (slab - e0) : 32 * E;
-          stream_rows<kRitzStages>(bw + e0, ld, rows, false, cw, rg, [&](int row, const double* ch) {
-            const double2* cr = reinterpret_cast<const double2*>(scoef + (size_t)row * 16);
-            double cf[16];
+            for (int i = 0; i < 16; ++i) acc[e][i] = 0.0;
+          const bool whole = c0 + kRitzE * kThreads <= n;
+          int r0 = 0;
+          for (; r0 + kRitzU <= rows; r0 += kRitzU) {
+            double x[kRitzU][kRitzE];
 #pragma unroll
-            for (int i = 0; i < 8; ++i) {
-              const double2 c2 = cr[i];
-              cf[2 * i] = c2.x;
-              cf[2 * i + 1] = c2.y;
+            for (int q = 0; q < kRitzU; ++q)
+#pragma unroll
+              for (int e = 0; e < kRitzE; ++e) {
+                const int col = c0 + tid + e * kThreads;
+                x[q][e] = (whole || col < n) ? __ldcs(basis + (size_t)(r0 + q) * ld + col) : 0.0;
+              }
+#pragma unroll
+            for (int q = 0; q < kRitzU; ++q) {
+              const double2* cr = reinterpret_cast<const double2*>(scoef + (size_t)(r0 + q) * 16);
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                const double2 c2 = cr[i];
+#pragma unroll
+                for (int e = 0; e < kRitzE; ++e) {
+                  acc[e][2 * i] = fma(c2.x, x[q][e], acc[e][2 * i]);
+                  acc[e][2 * i + 1] = fma(c2.y, x[q][e], acc[e][2 * i + 1]);
+                }
+              }
             }
+          }
+          for (; r0 < rows; ++r0) {
+            const double2* cr = reinterpret_cast<const double2*>(scoef + (size_t)r0 * 16);
 #pragma unroll
-            for (int t = 0; t < E; ++t) {
-              int e = t * 32 + lane;
-              double x = (e < cw) ? ch[e] : 0.0;
+            for (int e = 0; e < kRitzE; ++e) {
+              const int col = c0 + tid + e * kThreads;
+              const double x = (col < n) ? __ldcs(basis + (size_t)r0 * ld + col) : 0.0;
 #pragma unroll
-              for (int i = 0; i < 16; ++i) acc[t][i] = fma(cf[i], x, acc[t][i]);
+              for (int i = 0; i < 8; ++i) {
+                const double2 c2 = cr[i];
+                acc[e][2 * i] = fma(c2.x, x, acc[e][2 * i]);
+                acc[e][2 * i + 1] = fma(c2.y, x, acc[e][2 * i + 1]);
+              }
             }
-          });
+          }
 #pragma unroll
-          for (int t = 0; t < E; ++t) {
-            int e = e0 + t * 32 + lane;
-            int g = w * slab + e;
-            if (e < slab && g < n) {
+          for (int e = 0; e < kRitzE; ++e) {
+            const int col = c0 + tid + e * kThreads;
+            if (col < n) {
 #pragma unroll
               for (int i = 0; i < 16; ++i)
-                if (i < ki) out[(size_t)(i0 + i) * n + g] = acc[t][i];
+                if (i < ki) out[(size_t)(i0 + i) * n + col] = acc[e][i];
             }
           }
         }
