@@ -170,11 +170,9 @@ __device__ __forceinline__ void correlate_reg4096(double2* buf, const double2* t
 #pragma unroll
   for (int q = 0; q < 16; ++q) a[q] = buf[swz4096(16 * b3 + q)];
   dft16<false, false>(a);
-  // a[k] = Z_{t + 256 k}; publish the slots the partner reads (k >= 8; thread 0 also reads
-  // its own slot 0 for the self pair p = 0): own block, no hazard
+  // a[k] = Z_{t + 256 k}; publish them for the partner (own block: no hazard)
 #pragma unroll
-  for (int k = 8; k < 16; ++k) buf[swz4096(16 * b3 + k)] = a[k];
-  if (t == 0) buf[swz4096(16 * b3)] = a[0];
+  for (int k = 0; k < 16; ++k) buf[swz4096(16 * b3 + k)] = a[k];
   __syncthreads();
   // ---- pair step: p = t + 256 k, q = H - p (mod H) lives at thread tp = (256 - t) & 255,
   // slot kp = 15 - k (t = 0: (16 - k) & 15).  Every thread owns the pairs of its k < 8 (and
