@@ -143,6 +143,15 @@ ssa_status ssa_spectrum(ssa_plan_t plan, const double* d_series, double* d_spec,
 ssa_status ssa_matvec(ssa_plan_t plan, const double* d_spec, const double* d_x, double* d_y,
                       int transpose, void* stream);
 
+/* The same products for nvec vectors per series in one call, every vector of series b
+ * against the one stored spectrum of b (the products of a series share its spectrum, read
+ * from HBM once per call instead of once per product):
+ *   transpose = 0 : d_y[b][i] = X_b d_x[b][i]    d_x: [batch][nvec][K]  d_y: [batch][nvec][L]
+ *   transpose = 1 : d_y[b][i] = X_b^T d_x[b][i]  d_x: [batch][nvec][L]  d_y: [batch][nvec][K]
+ * nvec >= 1 and batch * nvec < 2^31, else SSA_ERR_INVALID_ARGUMENT.  Enqueue only. */
+ssa_status ssa_matvec_multi(ssa_plan_t plan, const double* d_spec, const double* d_x, double* d_y,
+                            int32_t nvec, int transpose, void* stream);
+
 /* Rank-1 Hankelization (diagonal averaging of sigma u v^T) of nterms terms per series via
  * linear convolution (sec 5, Eqs. hankelization1/conv, Alg. 4 with the
  * weights read as division by the antidiagonal counts c_t = min(t, L, K, N-t+1),

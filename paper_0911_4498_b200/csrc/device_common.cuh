@@ -42,6 +42,21 @@ __device__ __forceinline__ void trace_point(int id) {
     }
   }
 }
+// the same record from thread 0 of whichever CTA calls it (tail phases of a grid)
+__device__ __forceinline__ void trace_point_any(int id) {
+  if (threadIdx.x == 0) {
+    unsigned long long* tr = g_trace;
+    if (tr != nullptr) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      const unsigned long long i = atomicAdd(tr, 1ull);
+      if (i < (unsigned long long)kTraceMax) {
+        tr[1 + 2 * i] = t;
+        tr[2 + 2 * i] = (unsigned long long)id;
+      }
+    }
+  }
+}
 __device__ __forceinline__ void pdl_wait(int id) {
   pdl_wait();
   trace_point(id);

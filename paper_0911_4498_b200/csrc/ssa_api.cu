@@ -459,6 +459,31 @@ extern "C" ssa_status ssa_matvec(ssa_plan_t plan, const double* d_spec, const do
   return SSA_OK;
 }
 
+extern "C" ssa_status ssa_matvec_multi(ssa_plan_t plan, const double* d_spec, const double* d_x, double* d_y,
+                                       int32_t nvec, int transpose, void* stream) {
+  if (!plan || !d_spec || !d_x || !d_y) return fail(SSA_ERR_INVALID_ARGUMENT, "NULL argument");
+  if (((uintptr_t)d_spec) & 15) return fail(SSA_ERR_INVALID_ARGUMENT, "d_spec must be 16-byte aligned");
+  if (transpose != 0 && transpose != 1) return fail(SSA_ERR_INVALID_ARGUMENT, "transpose must be 0 or 1");
+  Plan& p = plan->p;
+  if (nvec < 1 || p.batch * (int64_t)nvec > INT32_MAX)
+    return fail(SSA_ERR_INVALID_ARGUMENT, "nvec must be >= 1 and batch * nvec < 2^31");
+  CK(cudaSetDevice(p.device), "cudaSetDevice");
+  const int n_in = transpose ? (int)p.L : (int)p.K, n_out = transpose ? (int)p.K : (int)p.L;
+  if (p.large) {
+    // one four-step pass per series: its nvec vectors against its one spectrum
+    for (int64_t b = 0; b < p.batch; ++b)
+      CK(ssa::large_correlate(p, reinterpret_cast<const double2*>(d_spec) + (size_t)b * (p.H + 1), 0,
+                              d_x + (size_t)b * nvec * n_in, (size_t)n_in, n_in, d_y + (size_t)b * nvec * n_out,
+                              (size_t)n_out, n_out, n_out, nullptr, 0, nullptr, nullptr, nvec, S(stream)),
+         "large matvec");
+  } else {
+    CK(ssa::launch_matvec(p, reinterpret_cast<const double2*>(d_spec), d_x, d_y, transpose, S(stream), nvec),
+       "matvec launch");
+  }
+  p.launches += 1;
+  return SSA_OK;
+}
+
 extern "C" ssa_status ssa_hankelize(ssa_plan_t plan, const double* d_sigma, const double* d_U, const double* d_V,
                                     int32_t nterms, double* d_out, void* stream) {
   if (!plan || !d_sigma || !d_U || !d_V || !d_out) return fail(SSA_ERR_INVALID_ARGUMENT, "NULL argument");

@@ -61,8 +61,8 @@ __global__ void __launch_bounds__(kThreads) spectrum_kernel(const double* __rest
 #undef SSA_SPEC
 }
 
-__global__ void __launch_bounds__(kThreads) matvec_kernel(const double2* __restrict__ spec, size_t spec_stride, int H,
-                                                          int n_in, int n_out, const double2* __restrict__ T,
+__global__ void __launch_bounds__(kThreads) matvec_kernel(const double2* __restrict__ spec, size_t spec_stride, int nvec,
+                                                          int H, int n_in, int n_out, const double2* __restrict__ T,
                                                           const double* __restrict__ x, double* __restrict__ y) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double2* buf = reinterpret_cast<double2*>(smem_raw);
@@ -72,7 +72,7 @@ __global__ void __launch_bounds__(kThreads) matvec_kernel(const double2* __restr
   const double* xb = x + (size_t)b * n_in;
   double* yb = y + (size_t)b * n_out;
   correlate_cta(
-      buf, sh, tw, spec + (size_t)b * spec_stride, n_in, n_out, [&](int i) { return __ldg(xb + i); },
+      buf, sh, tw, spec + (size_t)(b / nvec) * spec_stride, n_in, n_out, [&](int i) { return __ldg(xb + i); },
       [&](int t, double v) { yb[t] = v; });
 }
 
@@ -83,7 +83,7 @@ __device__ __forceinline__ void cp_async8(double* dst, const double* src) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
 }
 __global__ void __launch_bounds__(kThreads, 2) matvec4096_kernel(const double2* __restrict__ spec, size_t spec_stride,
-                                                                 int n_in, int n_out,
+                                                                 int nvec, int n_in, int n_out,
                                                                  const double2* __restrict__ T,
                                                                  const double* __restrict__ x, double* __restrict__ y,
                                                                  int nitems) {
@@ -96,7 +96,7 @@ __global__ void __launch_bounds__(kThreads, 2) matvec4096_kernel(const double2* 
     if (item < nitems) {
       const double* src = x + (size_t)item * n_in;
       for (int i = threadIdx.x; i < n_in; i += kThreads) cp_async8(stage + i, src + i);
-      const double2* sp = spec + (size_t)item * spec_stride;
+      const double2* sp = spec + (size_t)(item / nvec) * spec_stride;
       for (int i = threadIdx.x; i < 513; i += kThreads) asm volatile("prefetch.global.L2 [%0];" ::"l"(sp + 8 * i));
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
@@ -109,7 +109,7 @@ __global__ void __launch_bounds__(kThreads, 2) matvec4096_kernel(const double2* 
     __syncthreads();
     double* yb = y + (size_t)item * n_out;
     correlate_reg4096(
-        buf, t2, tw, stage, spec + (size_t)item * spec_stride, n_in, n_out, [&]() { fetch(item + gridDim.x); },
+        buf, t2, tw, stage, spec + (size_t)(item / nvec) * spec_stride, n_in, n_out, [&]() { fetch(item + gridDim.x); },
         [&](int t, double v) { yb[t] = v; });
   }
 }
@@ -338,23 +338,24 @@ cudaError_t launch_spectrum(const Plan& p, const double* series, double2* spec, 
 }
 
 cudaError_t launch_matvec_strided(const Plan& p, const double2* spec, size_t spec_stride, const double* x, double* y,
-                                  int transpose, cudaStream_t s) {
+                                  int transpose, cudaStream_t s, int nvec) {
   int n_in = transpose ? (int)p.L : (int)p.K;
   int n_out = transpose ? (int)p.K : (int)p.L;
+  const int64_t items = p.batch * nvec;
   if (p.H == 4096 && n_in <= 4097 && !getenv("SSA_MATVEC_SMEM")) {
-    const int grid = (int)std::min<int64_t>(p.batch, 2 * (int64_t)p.sms);
-    matvec4096_kernel<<<grid, kThreads, reg4096_smem(), s>>>(spec, spec_stride, n_in, n_out, p.d_twl, x, y,
-                                                              (int)p.batch);
+    const int grid = (int)std::min<int64_t>(items, 2 * (int64_t)p.sms);
+    matvec4096_kernel<<<grid, kThreads, reg4096_smem(), s>>>(spec, spec_stride, nvec, n_in, n_out, p.d_twl, x, y,
+                                                              (int)items);
     return cudaGetLastError();
   }
-  matvec_kernel<<<(unsigned)p.batch, kThreads, fft_smem((int)p.H), s>>>(spec, spec_stride, (int)p.H, n_in, n_out,
-                                                                        p.d_twl, x, y);
+  matvec_kernel<<<(unsigned)items, kThreads, fft_smem((int)p.H), s>>>(spec, spec_stride, nvec, (int)p.H, n_in, n_out,
+                                                                      p.d_twl, x, y);
   return cudaGetLastError();
 }
 
 cudaError_t launch_matvec(const Plan& p, const double2* spec, const double* x, double* y, int transpose,
-                          cudaStream_t s) {
-  return launch_matvec_strided(p, spec, (size_t)p.H + 1, x, y, transpose, s);
+                          cudaStream_t s, int nvec) {
+  return launch_matvec_strided(p, spec, (size_t)p.H + 1, x, y, transpose, s, nvec);
 }
 
 cudaError_t launch_group_hankelize(const Plan& p, const double* sigma, const double* U, const double* V,

@@ -147,11 +147,12 @@ inline cudaError_t raise_smem_limit(F* func, size_t bytes) {
 
 // launchers; return cudaGetLastError() after enqueue
 cudaError_t launch_spectrum(const Plan& p, const double* series, double2* spec, int nseries, cudaStream_t s);
+// nvec products per series: item b uses the spectrum of series b / nvec (x, y: [batch][nvec][n])
 cudaError_t launch_matvec(const Plan& p, const double2* spec, const double* x, double* y, int transpose,
-                          cudaStream_t s);
-// spec_stride (double2 elements) between the items' spectra; 0: one spectrum for all
+                          cudaStream_t s, int nvec = 1);
+// spec_stride (double2 elements) between the series' spectra; 0: one spectrum for all
 cudaError_t launch_matvec_strided(const Plan& p, const double2* spec, size_t spec_stride, const double* x, double* y,
-                                  int transpose, cudaStream_t s);
+                                  int transpose, cudaStream_t s, int nvec = 1);
 // heterogeneity matrix helpers (ssa_hmatrix.cu)
 cudaError_t launch_hm_windows(const double* f, int64_t nwin, int64_t B, double* win, cudaStream_t s);
 cudaError_t launch_hm_gather(const double* U, int64_t nwin, int k, int64_t L, const int32_t* d_idx, int nI, double* x,

@@ -166,6 +166,7 @@ __global__ void __launch_bounds__(kThreads) lg_dots(const double* __restrict__ b
     for (; row0 + kRoG <= nb; row0 += kRoG) group(row0, std::false_type());
   for (; row0 < nb; row0 += kRoG) group(row0, std::true_type());
   __syncthreads();
+  if (blockIdx.x == 0) trace_point_any(22);
   for (int row = threadIdx.x; row < nb; row += kThreads) {
     double s = 0.0;
 #pragma unroll
@@ -176,6 +177,7 @@ __global__ void __launch_bounds__(kThreads) lg_dots(const double* __restrict__ b
   const int g = blockIdx.x / kDotGroup, ng = (nchunk + kDotGroup - 1) / kDotGroup;
   const int g0 = g * kDotGroup, gn = min(kDotGroup, nchunk - g0);
   if (!last_cta(&sc->grp_done[g], (unsigned)gn, &lastf)) return;
+  if (g == 0) trace_point_any(23);
   for (int row = threadIdx.x; row < nb; row += kThreads) {
     const double* pr = part + (size_t)row * nchunk + g0;
     double s = 0.0;
@@ -191,6 +193,7 @@ __global__ void __launch_bounds__(kThreads) lg_dots(const double* __restrict__ b
   if (threadIdx.x == 0) sc->grp_done[g] = 0;
   // level 2: the last group sums the groups in index order
   if (!last_cta(&sc->done_grp, (unsigned)ng, &lastf)) return;
+  trace_point_any(24);
   for (int row = threadIdx.x; row < nb; row += kThreads) {
     const double* pr = gpart + (size_t)row * kLgMaxGroups;
     double s = 0.0;
@@ -265,8 +268,10 @@ __global__ void __launch_bounds__(kThreads) lg_update(const double* __restrict__
     for (int i = 0; i < kWarps; ++i) t += red[i];
     part[blockIdx.x] = t;
   }
+  if (blockIdx.x == 0) trace_point_any(25);
   if (pass < 0) return;  // restart passes: lg_restart_norm finishes them
   if (!last_cta(&sc->done_upd, gridDim.x, &lastf)) return;
+  trace_point_any(26);
   const double nn = sqrt(cta_sum(part, gridDim.x, red));
   if (threadIdx.x != 0) return;
   sc->done_upd = 0;
@@ -766,7 +771,8 @@ static void trace_report(unsigned long long* trace, cudaStream_t s) {
   static const char* names[32] = {"?", "lg_col_fwd", "lg_row_cta", "lg_row_warp", "lg_col_inv", "-", "lg_dots",
                                   "lg_update", "-", "-", "lg_start", "lg_restart_norm",
                                   "-", "lg_check", "lg_loop", "lg_ritz", "lg_beta1", "lg_init", "lg_sign",
-                                  "lg_flip", "lg_finite", "lg_state"};
+                                  "lg_flip", "lg_finite", "lg_state", "dots_streamed", "dots_tail1", "dots_tail2",
+                                  "upd_streamed", "upd_tail"};
   cudaStreamSynchronize(s);
   unsigned long long n = 0;
   cudaMemcpy(&n, trace, 8, cudaMemcpyDeviceToHost);

@@ -25,7 +25,7 @@ STATUS = {0: "SSA_OK", 1: "SSA_ERR_INVALID_ARGUMENT", 2: "SSA_ERR_NOT_CONVERGED"
 
 # every symbol include/ssa.h declares
 EXPORTS = ["ssa_options_default", "ssa_plan_create", "ssa_plan_destroy", "ssa_plan_fft_size",
-           "ssa_plan_max_steps", "ssa_spectrum", "ssa_matvec", "ssa_hankelize", "ssa_decompose",
+           "ssa_plan_max_steps", "ssa_spectrum", "ssa_matvec", "ssa_matvec_multi", "ssa_hankelize", "ssa_decompose",
            "ssa_reconstruct", "ssa_reconstruct_grouped", "ssa_hmatrix", "ssa_hmatrix_plan_create", "ssa_hmatrix_exec",
            "ssa_hmatrix_plan_destroy", "ssa_bootstrap", "ssa_run_host", "ssa_status_string", "ssa_last_error",
            "ssa_plan_launch_count", "ssa_plan_phase_ms", "ssa_plan_profile", "ssa_plan_bidiagonals"]
@@ -87,6 +87,7 @@ def load_library():
     lib.ssa_plan_bidiagonals.restype = ctypes.c_int
     lib.ssa_spectrum.argtypes = [vp, dp, dp, vp]
     lib.ssa_matvec.argtypes = [vp, dp, dp, dp, ctypes.c_int, vp]
+    lib.ssa_matvec_multi.argtypes = [vp, dp, dp, dp, ctypes.c_int32, ctypes.c_int, vp]
     lib.ssa_hankelize.argtypes = [vp, dp, dp, dp, i32, dp, vp]
     lib.ssa_decompose.argtypes = [vp, dp, dp, dp, dp, dp, vp]
     lib.ssa_reconstruct.argtypes = [vp, dp, dp, dp, dp, vp]
@@ -103,7 +104,7 @@ def load_library():
     lib.ssa_status_string.restype = ctypes.c_char_p
     lib.ssa_last_error.argtypes = []
     lib.ssa_last_error.restype = ctypes.c_char_p
-    for name in ("ssa_options_default", "ssa_plan_create", "ssa_spectrum", "ssa_matvec", "ssa_hankelize",
+    for name in ("ssa_options_default", "ssa_plan_create", "ssa_spectrum", "ssa_matvec", "ssa_matvec_multi", "ssa_hankelize",
                  "ssa_decompose", "ssa_reconstruct", "ssa_run_host"):
         getattr(lib, name).restype = ctypes.c_int
     _lib = lib
@@ -232,6 +233,21 @@ class Plan:
         _dev_f64(out, (self.batch, n_out), "out")
         _check(load_library().ssa_matvec(self._h, spec.data_ptr(), x.data_ptr(), out.data_ptr(),
                                          1 if transpose else 0, _stream(stream, self.device)))
+        return out
+
+    def matvec_multi(self, spec, x, transpose: bool = False, out=None, stream=None):
+        """nvec products per series against its spectrum: x [batch][nvec][K] (X x) or
+        [batch][nvec][L] (X^T x) -> [batch][nvec][L or K]."""
+        n_in, n_out = (self.L, self.K) if transpose else (self.K, self.L)
+        if x.dim() != 3:
+            raise ValueError("x must be [batch][nvec][n]")
+        nvec = x.shape[1]
+        _dev_f64(spec, (self.batch, self.M // 2 + 1, 2), "spec")
+        _dev_f64(x, (self.batch, nvec, n_in), "x")
+        out = self._t(self.batch, nvec, n_out) if out is None else out
+        _dev_f64(out, (self.batch, nvec, n_out), "out")
+        _check(load_library().ssa_matvec_multi(self._h, spec.data_ptr(), x.data_ptr(), out.data_ptr(), nvec,
+                                               1 if transpose else 0, _stream(stream, self.device)))
         return out
 
     def hankelize(self, sigma, U, V, out=None, stream=None):

@@ -14,6 +14,29 @@ if "cfg4" in which:
     y = plan.matvec(spec, v)
     torch.cuda.synchronize()
     print("cfg4 ok")
+if "cfg4m" in which:   # ssa_matvec_multi: 2048 series x 32 vectors (one bench chunk)
+    N, L, B, nv = 8192, 4096, 2048, 32
+    K = N - L + 1
+    g = torch.Generator(device="cuda").manual_seed(4)
+    F = torch.randn(B, N, dtype=torch.float64, device="cuda", generator=g)
+    v = torch.randn(B, nv, K, dtype=torch.float64, device="cuda", generator=g)
+    plan = P.Plan(N, L, 0, B)
+    spec = plan.spectrum(F)
+    y = plan.matvec_multi(spec, v)
+    y = plan.matvec_multi(spec, v, out=y)
+    torch.cuda.synchronize()
+    print("cfg4m ok")
+if "cfg3mv" in which:  # one long-series product (N = 2^20): the four-step kernels of the Lanczos loop
+    N, L = 1 << 20, 1 << 19
+    g = torch.Generator(device="cuda").manual_seed(3)
+    F = torch.randn(1, N, dtype=torch.float64, device="cuda", generator=g)
+    v = torch.randn(1, N - L + 1, dtype=torch.float64, device="cuda", generator=g)
+    plan = P.Plan(N, L, 0, 1)
+    spec = plan.spectrum(F)
+    for _ in range(3):
+        y = plan.matvec(spec, v)
+    torch.cuda.synchronize()
+    print("cfg3mv ok")
 if "cfg5" in which:
     N, L, Bc, T = 262144, 131072, 2, 50
     K = N - L + 1
