@@ -31,7 +31,23 @@ namespace ssa {
 
 cudaError_t trace_attach_fft(unsigned long long* p) { return trace_attach(p); }
 
-constexpr int kColW = 8;  // columns per CTA in the column passes (one warp each)
+constexpr int kColW = 8;  // columns per CTA in the column passes
+
+// Threads of a column-pass CTA: 256 (one warp per column) for the batched sizes; 512 (two
+// warps per column, 8 rows per thread) for H >= 2^19, where one item's 128 CTAs are all the
+// parallelism there is and the per-warp FFT chain sets the time (cfg3: one series, N = 2^20).
+template <int LOGH>
+__host__ __device__ constexpr int col_threads() { return LOGH >= 19 ? 512 : 256; }
+
+// barrier of the threads of one column: a warp, or a named barrier over its two warps
+template <int CT>
+struct ColSync {
+  int id;
+  __device__ __forceinline__ void operator()() const {
+    if constexpr (CT / kColW == 32) __syncwarp();
+    else asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(CT / kColW) : "memory");
+  }
+};
 
 struct WarpSync {
   __device__ __forceinline__ void operator()() const { __syncwarp(); }
@@ -112,17 +128,18 @@ struct ColFwdArgs {
 };
 
 template <int LOGH>
-__global__ void __launch_bounds__(kThreads) lg_col_fwd(ColFwdArgs args, const double2* __restrict__ T1,
+__global__ void __launch_bounds__(col_threads<LOGH>()) lg_col_fwd(ColFwdArgs args, const double2* __restrict__ T1,
                                                        const double2* __restrict__ TWH) {
-  pdl_wait(1);
-  if (args.gate && *args.gate) return;
   using G = Geo<LOGH>;
   constexpr int N1 = G::N1, N2 = G::N2, CS = N1 + 1;  // odd column stride (16-byte units)
-  constexpr int NE = (N1 * kColW + kThreads - 1) / kThreads;
+  constexpr int CT = col_threads<LOGH>(), RS = CT / kColW;  // threads, row step of a thread
+  constexpr int NE = (N1 * kColW + CT - 1) / CT;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double2* buf = reinterpret_cast<double2*>(smem_raw);
   const double2* th = TWH;
-  const TwSmem tw1 = load_tw2(T1, buf + kColW * CS, 2 * N1);
+  const TwSmem tw1 = load_tw2(T1, buf + kColW * CS, 2 * N1);  // constant: before the wait
+  pdl_wait(1);
+  if (args.gate && *args.gate) return;
   const ColFwdIn a = blockIdx.z ? args.in[1] : args.in[0];
   const int n2_0 = blockIdx.x * kColW;
   const double* xi = a.x + (size_t)blockIdx.y * a.xs;
@@ -136,8 +153,8 @@ __global__ void __launch_bounds__(kThreads) lg_col_fwd(ColFwdArgs args, const do
   double2 v[NE];
 #pragma unroll
   for (int j = 0; j < NE; ++j) {
-    const bool ok = threadIdx.x + j * kThreads < N1 * kColW;
-    const int i0 = i00 + j * (2 * N2 * (kThreads / kColW));
+    const bool ok = threadIdx.x + j * CT < N1 * kColW;
+    const int i0 = i00 + j * (2 * N2 * (RS));
     if (rvec && ok && i0 + 1 < a.n_in) {
       v[j] = __ldg(reinterpret_cast<const double2*>(xi + i0));
     } else {
@@ -153,8 +170,8 @@ __global__ void __launch_bounds__(kThreads) lg_col_fwd(ColFwdArgs args, const do
     double* brow = a.nrm.basis + (size_t)(*a.nrm.jrow - 1) * a.nrm.ld;
 #pragma unroll
     for (int j = 0; j < NE; ++j) {
-      const bool ok = threadIdx.x + j * kThreads < N1 * kColW;
-      const int i0 = i00 + j * (2 * N2 * (kThreads / kColW));
+      const bool ok = threadIdx.x + j * CT < N1 * kColW;
+      const int i0 = i00 + j * (2 * N2 * (RS));
       v[j].x *= inv;
       v[j].y *= inv;
       if (rvec && ok && i0 + 1 < a.n_in) {
@@ -167,28 +184,30 @@ __global__ void __launch_bounds__(kThreads) lg_col_fwd(ColFwdArgs args, const do
     }
     if (blockIdx.x == 0 && threadIdx.x < a.nrm.ld - a.n_in) brow[a.n_in + threadIdx.x] = 0.0;
   }
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // column of the FFT phase: warps [c * RS / 32, (c + 1) * RS / 32), thread ct of RS
+  const int fc = threadIdx.x / RS, ct = threadIdx.x % RS;
+  const ColSync<CT> csync{1 + fc};
   if constexpr (G::L1 >= 8) {
     // the thread holds rows r0 + 32 j of its column: the butterflies of the outermost
     // radix-8 pass, done in registers before the first shared-memory store
     __syncthreads();  // twiddle tables
-    dif_pass0_store<G::L1, kThreads / kColW>(v, r0, buf + cc * CS, tw1);
+    dif_pass0_store<G::L1, RS>(v, r0, buf + cc * CS, tw1);
     __syncthreads();
-    fft_run_inner_t<G::L1, false>(buf + w * CS, tw1, lane, 32, WarpSync());
+    fft_run_inner_t<G::L1, false>(buf + fc * CS, tw1, ct, RS, csync);
   } else {
 #pragma unroll
     for (int j = 0; j < NE; ++j)
-      if (threadIdx.x + j * kThreads < N1 * kColW) buf[cc * CS + fsw(r0 + (kThreads / kColW) * j)] = v[j];
+      if (threadIdx.x + j * CT < N1 * kColW) buf[cc * CS + fsw(r0 + (RS) * j)] = v[j];
     __syncthreads();
-    fft_run_t<G::L1, false>(buf + w * CS, tw1, lane, 32, WarpSync());
+    fft_run_t<G::L1, false>(buf + fc * CS, tw1, ct, RS, csync);
   }
   __syncthreads();
   // element j: column c = t & 7, k1 = (t >> 3) + (256 / 8) j; twiddle W_H^{n2 k1}
   const int c = threadIdx.x & (kColW - 1), k0 = threadIdx.x >> 3;
   const int n2 = n2_0 + c;
-  const int nval = (N1 * kColW - threadIdx.x + kThreads - 1) / kThreads;
-  twiddle_seq<LOGH, NE>(th, (long long)n2 * k0, (long long)n2 * (kThreads / kColW), nval, [&](int j, double2 w) {
-    const int k1 = k0 + (kThreads / kColW) * j;
+  const int nval = (N1 * kColW - threadIdx.x + CT - 1) / CT;
+  twiddle_seq<LOGH, NE>(th, (long long)n2 * k0, (long long)n2 * (RS), nval, [&](int j, double2 w) {
+    const int k1 = k0 + (RS) * j;
     const double2 z = buf[c * CS + fsw(rev_t<G::L1>(k1))];
     Yi[(size_t)n2 + (size_t)N2 * k1] = cmul(z, w);
   });
@@ -203,7 +222,8 @@ struct ColInvArgs {
   int n_out, ld_out;           // correlation output length and padded row length
   size_t out_stride;           // item stride of out
   double* out;
-  const double* prev;          // correlation: previous vector (may be null)
+  const double* prev;          // correlation: previous vector (may be null; read before the grid
+                               // dependency wait: no kernel of this correlation may write it)
   size_t prev_stride;
   const double* coef;          // correlation: per-item coefficient (device scalar), null -> 0
   double* part;                // correlation: partial sums of squares [items][gridDim.x]
@@ -215,45 +235,61 @@ struct ColInvArgs {
 };
 
 template <int LOGH>
-__global__ void __launch_bounds__(kThreads, (LOGH >= 19) ? 1 : 3) lg_col_inv(const double2* __restrict__ Y, const double2* __restrict__ T1,
+__global__ void __launch_bounds__(col_threads<LOGH>(), (LOGH >= 19) ? 1 : 3) lg_col_inv(const double2* __restrict__ Y, const double2* __restrict__ T1,
                                                        ColInvArgs a) {
-  pdl_wait(4);
-  if (a.gate && *a.gate) return;
   using G = Geo<LOGH>;
   constexpr int N1 = G::N1, N2 = G::N2, CS = N1 + 1;
-  constexpr int NE = (N1 * kColW + kThreads - 1) / kThreads;
+  constexpr int CT = col_threads<LOGH>(), RS = CT / kColW;  // threads, row step of a thread
+  constexpr int NE = (N1 * kColW + CT - 1) / CT;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double2* buf = reinterpret_cast<double2*>(smem_raw);
-  __shared__ double red[kWarps];
-  const TwSmem tw1 = load_tw2(T1, buf + kColW * CS, 2 * N1);
+  __shared__ double red[CT / 32];
   const int n2_0 = blockIdx.x * kColW;
   const size_t item = blockIdx.y;
   const double2* Yi = Y + item * G::H;
-  // thread t: column c = t & 7, rows n1 = (t >> 3) + 32 j (as in lg_col_fwd)
+  // thread t: column c = t & 7, rows n1 = (t >> 3) + RS j (as in lg_col_fwd)
   const int cc = threadIdx.x & (kColW - 1), r0 = threadIdx.x >> 3;
-  constexpr int RS = kThreads / kColW;  // row step between a thread's elements
+  // inputs that the preceding kernels of this correlation do not write, before the grid
+  // dependency wait: the tables and (correlation) the previous Lanczos vector of the
+  // recurrence term, written by an earlier half-step
+  const TwSmem tw1 = load_tw2(T1, buf + kColW * CS, 2 * N1);
+  double2 pr[NE];
+  if (a.mode == 0) {
+    const double* pv = a.prev ? a.prev + item * a.prev_stride : nullptr;
+#pragma unroll
+    for (int j = 0; j < NE; ++j) {
+      const int t = 2 * (n2_0 + cc + N2 * (r0 + RS * j));
+      const bool ok = threadIdx.x + j * CT < N1 * kColW;
+      pr[j].x = (pv && ok && t < a.n_out) ? __ldg(pv + t) : 0.0;
+      pr[j].y = (pv && ok && t + 1 < a.n_out) ? __ldg(pv + t + 1) : 0.0;
+    }
+  }
+  pdl_wait(4);
+  if (a.gate && *a.gate) return;
   double2 v[NE];
 #pragma unroll
   for (int j = 0; j < NE; ++j)
-    if (threadIdx.x + j * kThreads < N1 * kColW) v[j] = Yi[n2_0 + cc + N2 * (r0 + RS * j)];
+    if (threadIdx.x + j * CT < N1 * kColW) v[j] = Yi[n2_0 + cc + N2 * (r0 + RS * j)];
 #pragma unroll
   for (int j = 0; j < NE; ++j)
-    if (threadIdx.x + j * kThreads < N1 * kColW) buf[cc * CS + fsw(rev_t<G::L1>(r0 + RS * j))] = v[j];
+    if (threadIdx.x + j * CT < N1 * kColW) buf[cc * CS + fsw(rev_t<G::L1>(r0 + RS * j))] = v[j];
   __syncthreads();
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int fc = threadIdx.x / RS, ct = threadIdx.x % RS;  // column of the FFT phase (as lg_col_fwd)
+  const ColSync<CT> csync{1 + fc};
   // z[j] = H x packed point at row r0 + 32 j of this thread's column
   double2 z[NE];
   if constexpr (G::L1 >= 8) {
     // outermost inverse pass in registers: its outputs are exactly this thread's rows
-    fft_run_inner_t<G::L1, true>(buf + w * CS, tw1, lane, 32, WarpSync());
+    fft_run_inner_t<G::L1, true>(buf + fc * CS, tw1, ct, RS, csync);
     __syncthreads();
-    dif_pass0_inverse_load<G::L1, kThreads / kColW>(z, r0, buf + cc * CS, tw1);
+    dif_pass0_inverse_load<G::L1, RS>(z, r0, buf + cc * CS, tw1);
   } else {
-    fft_run_t<G::L1, true>(buf + w * CS, tw1, lane, 32, WarpSync());
+    fft_run_t<G::L1, true>(buf + fc * CS, tw1, ct, RS, csync);
     __syncthreads();
 #pragma unroll
     for (int j = 0; j < NE; ++j)
-      if (threadIdx.x + j * kThreads < N1 * kColW) z[j] = buf[cc * CS + fsw(r0 + RS * j)];
+      if (threadIdx.x + j * CT < N1 * kColW) z[j] = buf[cc * CS + fsw(r0 + RS * j)];
   }
   constexpr double invH = 1.0 / (double)G::H;
   double ss = 0.0;
@@ -264,19 +300,10 @@ __global__ void __launch_bounds__(kThreads, (LOGH >= 19) ? 1 : 3) lg_col_inv(con
   // real outputs t = 2n (z.x) and 2n + 1 (z.y)
   const int n2 = n2_0 + cc;
   if (a.mode == 0) {
-    const double* pv = a.prev ? a.prev + item * a.prev_stride : nullptr;
     double* o = a.out + item * a.out_stride;
-    double2 pr[NE];
-#pragma unroll
-    for (int j = 0; j < NE; ++j) {  // previous-vector loads first, all in flight
-      const int t = 2 * (n2 + N2 * (r0 + RS * j));
-      const bool ok = threadIdx.x + j * kThreads < N1 * kColW;
-      pr[j].x = (pv && ok && t < a.n_out) ? __ldg(pv + t) : 0.0;
-      pr[j].y = (pv && ok && t + 1 < a.n_out) ? __ldg(pv + t + 1) : 0.0;
-    }
 #pragma unroll
     for (int j = 0; j < NE; ++j) {
-      if (threadIdx.x + j * kThreads < N1 * kColW) {
+      if (threadIdx.x + j * CT < N1 * kColW) {
         const int n1 = r0 + RS * j;
         const int t = 2 * (n2 + N2 * n1);
         if (t < a.ld_out) {
@@ -297,7 +324,7 @@ __global__ void __launch_bounds__(kThreads, (LOGH >= 19) ? 1 : 3) lg_col_inv(con
       __syncthreads();
       if (threadIdx.x == 0) {
         double s = 0.0;
-        for (int i = 0; i < kWarps; ++i) s += red[i];
+        for (int i = 0; i < CT / 32; ++i) s += red[i];
         a.part[item * gridDim.x + blockIdx.x] = s;
       }
       if (a.has_tail) {
@@ -314,7 +341,7 @@ __global__ void __launch_bounds__(kThreads, (LOGH >= 19) ? 1 : 3) lg_col_inv(con
     const double scale = sg * invH;
 #pragma unroll
     for (int j = 0; j < NE; ++j) {
-      if (threadIdx.x + j * kThreads < N1 * kColW) {
+      if (threadIdx.x + j * CT < N1 * kColW) {
         const int n1 = r0 + RS * j;
         const int t = 2 * (n2 + N2 * n1);
         if (t < a.N) {
@@ -350,10 +377,33 @@ __device__ __forceinline__ int partner_k2(int A, int k2, int N2) {
 
 // The pair step for pairs k2 = k0, k0 + ks, ... of rows (rA, rB[, cA, cB]) already
 // transformed (digit-reversed).  WA = W_M^A; W_M^p = WA W_{2 N2}^{k2} (tw2).
-template <int LOGH>
+// Spectrum values of the pairs a thread takes in the pair step (k2 = k0 + ks i, i < NI),
+// loaded ahead (mode 1; the stored spectrum does not depend on the preceding kernels, so
+// the loads can be issued before the grid dependency wait and overlap its latency).
+template <int LOGH, int NI>
+struct RowSpecPre {
+  double2 Fp[NI], Fq[NI];
+  __device__ __forceinline__ void load(const RowArgs& a, size_t item, int A, bool two, int k0, int ks) {
+    using G = Geo<LOGH>;
+    constexpr int N1 = G::N1, N2 = G::N2, H = G::H;
+    const int npairs = two ? N2 : ((A == 0) ? N2 / 2 + 1 : N2 / 2);
+    const double2* F = a.spec + item * a.spec_stride;
+#pragma unroll
+    for (int i = 0; i < NI; ++i) {
+      const int k2 = k0 + ks * i;
+      const long long p = (long long)A + (long long)N1 * k2;
+      const long long q = (p == 0) ? H : H - p;
+      if (k2 < npairs) { Fp[i] = __ldg(F + p); Fq[i] = __ldg(F + q); }
+    }
+  }
+};
+
+// pre: NI > 0 -> the thread's pairs are k2 = k0 + ks i, i < NI (unrolled), mode 1 reads the
+// spectrum from pre; NI = 0 -> runtime loop, spectrum loads in place.
+template <int LOGH, int NI = 0>
 __device__ __forceinline__ void row_pair_step(const RowArgs& a, size_t item, int A, bool two, double2 WA,
                                               const TwSmem& tw2, double2* rA, double2* rB, double2* cA, double2* cB,
-                                              int k0, int ks) {
+                                              int k0, int ks, const RowSpecPre<LOGH, (NI > 0 ? NI : 1)>* pre = nullptr) {
   using G = Geo<LOGH>;
   constexpr int N1 = G::N1, N2 = G::N2, H = G::H;
   const int npairs = two ? N2 : ((A == 0) ? N2 / 2 + 1 : N2 / 2);
@@ -361,13 +411,19 @@ __device__ __forceinline__ void row_pair_step(const RowArgs& a, size_t item, int
   double2* rowBc = two ? cB : cA;
   const double2* F = (a.mode == 1) ? a.spec + item * a.spec_stride : nullptr;
   double2* Fo = (a.mode == 0) ? a.spec_out + item * (size_t)(H + 1) : nullptr;
-  for (int k2 = k0; k2 < npairs; k2 += ks) {
+#pragma unroll
+  for (int i = 0; i < (NI > 0 ? NI : 1 << 30); ++i) {
+    const int k2 = k0 + ks * i;
+    if (k2 >= npairs) break;
     const int k2q = partner_k2(A, k2, N2);
     const int pr = fsw(rev_t<G::L2>(k2)), qr = fsw(rev_t<G::L2>(k2q));
     const long long p = (long long)A + (long long)N1 * k2;
     const long long q = (p == 0) ? H : H - p;
     double2 Fp, Fq;
-    if (a.mode == 1) { Fp = __ldg(F + p); Fq = __ldg(F + q); }
+    if (a.mode == 1) {
+      if constexpr (NI > 0) { Fp = pre->Fp[i]; Fq = pre->Fq[i]; }
+      else { Fp = __ldg(F + p); Fq = __ldg(F + q); }
+    }
     const double2 W = cmul(WA, tw2(k2));  // exp(-2 pi i p / M), p = A + N1 k2
     auto split = [&](double2 Zp, double2 Zq, double2& Xp, double2& Xq) {
       double2 E = make_double2(0.5 * (Zp.x + Zq.x), 0.5 * (Zp.y - Zq.y));
@@ -410,8 +466,6 @@ __device__ __forceinline__ void row_pair_step(const RowArgs& a, size_t item, int
 template <int LOGH>
 __global__ void __launch_bounds__(kThreads) lg_row_cta(const double2* __restrict__ T2, const double2* __restrict__ TWH,
                                                        const double2* __restrict__ TWA, RowArgs a) {
-  pdl_wait(2);
-  if (a.gate && *a.gate) return;
   using G = Geo<LOGH>;
   constexpr int N1 = G::N1, N2 = G::N2;
   constexpr int NE = (N2 + kThreads - 1) / kThreads;
@@ -421,10 +475,17 @@ __global__ void __launch_bounds__(kThreads) lg_row_cta(const double2* __restrict
   double2* cA = bB + N2;                                // mode 2: row A of Yb
   double2* cB = cA + N2;                                // mode 2: row B of Yb
   const double2* th = TWH;
-  const TwSmem tw2 = load_tw2(T2, cB + N2, 2 * N2);
   const int A = blockIdx.x, B = (N1 - A) & (N1 - 1);
   const bool two = (A != B);
   const size_t item = blockIdx.y;
+  // constant inputs first (tables, the stored spectrum of the pair step), then the wait
+  // for the preceding kernel's output
+  const TwSmem tw2 = load_tw2(T2, cB + N2, 2 * N2);
+  const double2 WA = __ldg(TWA + A);
+  RowSpecPre<LOGH, NE> pre;
+  if (a.mode == 1) pre.load(a, item, A, two, threadIdx.x, kThreads);
+  pdl_wait(2);
+  if (a.gate && *a.gate) return;
   double2* Ya = a.Ya + item * G::H;
   double2* Yb = (a.mode == 2) ? a.Yb + item * G::H : nullptr;
   if constexpr (G::L2 >= 10) {
@@ -452,7 +513,7 @@ __global__ void __launch_bounds__(kThreads) lg_row_cta(const double2* __restrict
         fft_run_inner_t<G::L2, false>(row, tw2, t, 128, sync);
       }
       __syncthreads();
-      row_pair_step<LOGH>(a, item, A, two, __ldg(TWA + A), tw2, bA, bB, cA, cB, threadIdx.x, blockDim.x);
+      row_pair_step<LOGH, NE>(a, item, A, two, WA, tw2, bA, bB, cA, cB, threadIdx.x, kThreads, &pre);
       if (a.mode == 0) return;
       __syncthreads();
       if (active) {
@@ -496,8 +557,7 @@ __global__ void __launch_bounds__(kThreads) lg_row_cta(const double2* __restrict
     fft_run_t<G::L2, false>(cA, tw2, threadIdx.x, blockDim.x, CtaSync());
     if (two) fft_run_t<G::L2, false>(cB, tw2, threadIdx.x, blockDim.x, CtaSync());
   }
-  const double2 WA = __ldg(TWA + A);
-  row_pair_step<LOGH>(a, item, A, two, WA, tw2, bA, bB, cA, cB, threadIdx.x, blockDim.x);
+  row_pair_step<LOGH, NE>(a, item, A, two, WA, tw2, bA, bB, cA, cB, threadIdx.x, kThreads, &pre);
   if (a.mode == 0) return;
   __syncthreads();
   double2* oA = (a.mode == 2) ? cA : bA;
@@ -680,7 +740,7 @@ static void col_fwd(const Plan& p, const ColFwdArgs& ca, int nz, int items, cuda
   const int logH = ilog2(p.H);
   const int N2 = 1 << (logH - logH / 2);
   const dim3 grid(N2 / kColW, items, nz);
-#define SSA_LG_CF(LG) launch_pdl(lg_col_fwd<LG>, dim3(grid), dim3(kThreads), col_smem(LG), s, ca, p.d_tw1, p.d_tw4)
+#define SSA_LG_CF(LG) launch_pdl(lg_col_fwd<LG>, dim3(grid), dim3(col_threads<LG>()), col_smem(LG), s, ca, p.d_tw1, p.d_tw4)
   SSA_LG_DISPATCH(logH, SSA_LG_CF)
 #undef SSA_LG_CF
 }
@@ -688,7 +748,7 @@ static void col_inv(const Plan& p, const double2* Y, const ColInvArgs& ca, int i
   const int logH = ilog2(p.H);
   const int N2 = 1 << (logH - logH / 2);
   const dim3 grid(N2 / kColW, items);
-#define SSA_LG_CI(LG) launch_pdl(lg_col_inv<LG>, dim3(grid), dim3(kThreads), col_smem(LG), s, Y, p.d_tw1, ca)
+#define SSA_LG_CI(LG) launch_pdl(lg_col_inv<LG>, dim3(grid), dim3(col_threads<LG>()), col_smem(LG), s, Y, p.d_tw1, ca)
   SSA_LG_DISPATCH(logH, SSA_LG_CI)
 #undef SSA_LG_CI
 }
