@@ -407,99 +407,114 @@ __global__ void lg_loop(LgScalars* sc, cudaGraphConditionalHandle h_while) {
 }
 
 // Ritz vectors: out[i][t] = sum_row coef[row][i] basis[row][t] (U_k = U_{m+1} P_k,
-// V_k = V_m Q_k, Eq. (1)), triples in blocks of kRitzK (blockIdx.y).  A
-// dense contraction (2 kRitzK flops per basis element read): each thread owns kRitzE
-// elements, so each coefficient pair read from shared memory (a broadcast 16-byte load)
-// feeds 2 kRitzE FMAs, and the basis loads of the next kRitzU rows are in flight while
-// the current ones are used.  The coefficient rows are staged through a fixed shared
-// tile of kRitzRows rows (zero-padded to kRitzK), so shared memory does not depend on m.
+// V_k = V_m Q_k, Eq. (1)), triples in blocks of 32 (blockIdx.y).  A dense
+// contraction of arithmetic intensity 2 * 32 / 8 = 8 flop per basis byte (above the fp64
+// ridge), so it runs on the fp64 tensor cores: mma.sync m8n8k4 f64 (DMMA), M = triples,
+// N = elements, K = basis rows.  Each warp owns 8 kRmNt consecutive elements and all 32
+// triples (4 x kRmNt accumulator tiles); per k-step of 4 rows a lane loads its kRmNt basis
+// values (row 4 ks + (lane & 3), element 8 j + (lane >> 2): 64-byte row segments) and reads
+// its four A fragments from a shared tile of the coefficients stored in fragment order
+// ([k-step][M tile][lane]: conflict-free), staged kRitzRows rows at a time (shared memory
+// independent of m).
 constexpr int kRitzRows = 128;
 constexpr int kRitzK = 32;
-constexpr int kRitzE = 2;                     // elements per thread
-constexpr int kRitzSpan = kThreads * kRitzE;  // elements per CTA
+constexpr int kRmNt = 4;                     // 8-element N tiles per warp
+constexpr int kRitzSpan = kWarps * 8 * kRmNt;  // elements per CTA (256)
 
-__global__ void __launch_bounds__(kThreads) lg_ritz(const double* __restrict__ basis, int ld, int add_rows,
-                                                    const int* __restrict__ state, const double* __restrict__ coef,
-                                                    int k, int n, double* out, double* amax, int* aidx) {
+__device__ __forceinline__ void dmma_m8n8k4(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(kThreads, 2) lg_ritz(const double* __restrict__ basis, int ld, int add_rows,
+                                                       const int* __restrict__ state, const double* __restrict__ coef,
+                                                       int k, int n, double* out, double* amax, int* aidx) {
   pdl_wait(15);
   const int rows = state[0] + add_rows;  // U_{m+1} (add 1) or V_m (add 0); m from the device
-  const int tb = blockIdx.x * kRitzSpan + threadIdx.x;
   const int i0 = blockIdx.y * kRitzK, ki = min(kRitzK, k - i0);
-  __shared__ __align__(16) double cs[kRitzRows * kRitzK];
-  double acc[kRitzE][kRitzK];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
+  const int tw0 = blockIdx.x * kRitzSpan + w * 8 * kRmNt;  // the warp's first element
+  __shared__ __align__(16) double cf[kRitzRows / 4][4][32];  // [k-step][M tile][lane]
+  double acc[4][kRmNt][2];
 #pragma unroll
-  for (int e = 0; e < kRitzE; ++e)
+  for (int mt = 0; mt < 4; ++mt)
 #pragma unroll
-    for (int i = 0; i < kRitzK; ++i) acc[e][i] = 0.0;
+    for (int j = 0; j < kRmNt; ++j) acc[mt][j][0] = acc[mt][j][1] = 0.0;
   for (int r0 = 0; r0 < rows; r0 += kRitzRows) {
-    const int nr = min(kRitzRows, rows - r0);
+    const int nr = min(kRitzRows, rows - r0), nks = (nr + 3) >> 2;
     __syncthreads();
-    for (int e = threadIdx.x; e < nr * kRitzK; e += blockDim.x) {
-      const int r = e / kRitzK, i = e - r * kRitzK;
-      cs[e] = (i < ki) ? __ldg(coef + (size_t)(r0 + r) * k + i0 + i) : 0.0;
+    for (int e = threadIdx.x; e < nks * 128; e += kThreads) {
+      const int ks = e >> 7, mt = (e >> 5) & 3, l = e & 31;
+      const int r = 4 * ks + (l & 3), i = 8 * mt + (l >> 2);
+      cf[ks][mt][l] = (r < nr && i < ki) ? __ldg(coef + (size_t)(r0 + r) * k + i0 + i) : 0.0;
     }
     __syncthreads();
-    const double* bp = basis + (size_t)r0 * ld;
 #pragma unroll 4
-    for (int row = 0; row < nr; ++row) {
-      double x[kRitzE];
+    for (int ks = 0; ks < nks; ++ks) {
+      const int r = r0 + 4 * ks + q;
+      const double* bp = basis + (size_t)r * ld + tw0 + g;
+      double b[kRmNt];
 #pragma unroll
-      for (int e = 0; e < kRitzE; ++e) {
-        const int t = tb + e * kThreads;
-        x[e] = (t < n) ? __ldcs(bp + (size_t)row * ld + t) : 0.0;
-      }
-      const double2* cr = reinterpret_cast<const double2*>(cs + (size_t)row * kRitzK);
+      for (int j = 0; j < kRmNt; ++j) b[j] = (r < rows && tw0 + 8 * j + g < n) ? __ldcs(bp + 8 * j) : 0.0;
+      double a[4];
 #pragma unroll
-      for (int i = 0; i < kRitzK / 2; ++i) {
-        const double2 c = cr[i];
+      for (int mt = 0; mt < 4; ++mt) a[mt] = cf[ks][mt][lane];
 #pragma unroll
-        for (int e = 0; e < kRitzE; ++e) {
-          acc[e][2 * i] = fma(c.x, x[e], acc[e][2 * i]);
-          acc[e][2 * i + 1] = fma(c.y, x[e], acc[e][2 * i + 1]);
-        }
-      }
+      for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+        for (int j = 0; j < kRmNt; ++j) dmma_m8n8k4(acc[mt][j][0], acc[mt][j][1], a[mt], b[j]);
     }
   }
+  // D fragment: triple 8 mt + g, elements tw0 + 8 j + 2 q + {0, 1}
 #pragma unroll
-  for (int e = 0; e < kRitzE; ++e) {
-    const int t = tb + e * kThreads;
-    if (t < n) {
+  for (int mt = 0; mt < 4; ++mt) {
+    const int i = 8 * mt + g;
+    if (i < ki) {
+      double* o = out + (size_t)(i0 + i) * n;
 #pragma unroll
-      for (int i = 0; i < kRitzK; ++i)
-        if (i < ki) out[(size_t)(i0 + i) * n + t] = acc[e][i];
+      for (int j = 0; j < kRmNt; ++j) {
+        const int t = tw0 + 8 * j + 2 * q;
+        if (t + 1 < n && ((reinterpret_cast<uintptr_t>(o + t) & 15) == 0)) {
+          *reinterpret_cast<double2*>(o + t) = make_double2(acc[mt][j][0], acc[mt][j][1]);
+        } else {
+          if (t < n) o[t] = acc[mt][j][0];
+          if (t + 1 < n) o[t + 1] = acc[mt][j][1];
+        }
+      }
     }
   }
   if (amax) {
     // per-CTA argmax |out_i| (lowest index on ties) for sign canonicalization
     __shared__ double sv[kWarps][kRitzK];
     __shared__ int si[kWarps][kRitzK];
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
 #pragma unroll
-    for (int i = 0; i < kRitzK; ++i) {
-      if (i >= ki) break;
+    for (int mt = 0; mt < 4; ++mt) {
       double v = -1.0;
       int ix = 0x7fffffff;
 #pragma unroll
-      for (int e = 0; e < kRitzE; ++e) {  // increasing t: ties keep the lower index
-        const int t = tb + e * kThreads;
-        const double a = (t < n) ? fabs(acc[e][i]) : -1.0;
-        if (a > v) { v = a; ix = t; }
-      }
-      for (int o = 16; o > 0; o >>= 1) {
-        double v2 = __shfl_xor_sync(0xffffffffu, v, o);
-        int i2 = __shfl_xor_sync(0xffffffffu, ix, o);
+      for (int j = 0; j < kRmNt; ++j)  // increasing t: ties keep the lower index
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          const int t = tw0 + 8 * j + 2 * q + c;
+          const double av = (t < n) ? fabs(acc[mt][j][c]) : -1.0;
+          if (av > v) { v = av; ix = t; }
+        }
+      for (int o = 1; o < 4; o <<= 1) {  // the four lanes of triple 8 mt + g
+        const double v2 = __shfl_xor_sync(0xffffffffu, v, o);
+        const int i2 = __shfl_xor_sync(0xffffffffu, ix, o);
         if (v2 > v || (v2 == v && i2 < ix)) { v = v2; ix = i2; }
       }
-      if (lane == 0) { sv[w][i] = v; si[w][i] = ix; }
+      if (q == 0) { sv[w][8 * mt + g] = v; si[w][8 * mt + g] = ix; }
     }
     __syncthreads();
     if (threadIdx.x < ki) {
       double v = -1.0;
       int ix = 0x7fffffff;
-      for (int q = 0; q < kWarps; ++q)
-        if (sv[q][threadIdx.x] > v || (sv[q][threadIdx.x] == v && si[q][threadIdx.x] < ix)) {
-          v = sv[q][threadIdx.x];
-          ix = si[q][threadIdx.x];
+      for (int qq = 0; qq < kWarps; ++qq)
+        if (sv[qq][threadIdx.x] > v || (sv[qq][threadIdx.x] == v && si[qq][threadIdx.x] < ix)) {
+          v = sv[qq][threadIdx.x];
+          ix = si[qq][threadIdx.x];
         }
       amax[(size_t)blockIdx.x * k + i0 + threadIdx.x] = v;
       aidx[(size_t)blockIdx.x * k + i0 + threadIdx.x] = ix;
