@@ -172,7 +172,13 @@ ssa_status ssa_hankelize(ssa_plan_t plan, const double* d_sigma, const double* d
  * Each u_i is sign-canonicalized (largest-|.| entry positive, lowest index on ties; v_i
  * flipped with it).  Per-series failures (non-finite input -> INVALID_ARGUMENT, not
  * converged -> NOT_CONVERGED with the best triples written) are reported in d_info after
- * the stream synchronizes; the return value covers validation and launch only. */
+ * the stream synchronizes; the return value covers validation and launch only.
+ * Two execution paths, both enqueue-only: the batched path (one CTA per series, every
+ * series of the batch in flight) when the series' kernel fits one CTA's shared memory
+ * (M <= 16384, and for M = 16384 only while the per-series basis fits), otherwise the
+ * long-series path, which decomposes the series of the batch ONE AFTER ANOTHER, each with
+ * the whole GPU (four-step FFT products, grid-wide reorthogonalization; the Lanczos loop of
+ * each series is one CUDA graph launch with device-side decisions). */
 ssa_status ssa_decompose(ssa_plan_t plan, const double* d_series, double* d_sigma, double* d_U,
                          double* d_V, ssa_series_info* d_info, void* stream);
 

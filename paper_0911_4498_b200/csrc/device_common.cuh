@@ -119,6 +119,24 @@ __device__ __forceinline__ double warp_sum8(double* v, int lane) {
   return v[0];
 }
 
+// Streaming (evict-first) fp64 load without `volatile`, so the compiler may hoist a group
+// of them ahead of the arithmetic that consumes them.
+__device__ __forceinline__ double ldg_stream(const double* p) {
+  double x;
+  asm("ld.global.cs.f64 %0, [%1];" : "=d"(x) : "l"(p));
+  return x;
+}
+
+// fp64 tensor-core MMA (DMMA), D = A B + D with A 8x4 (row), B 4x8 (col), D 8x8: lane l
+// holds A[l >> 2][l & 3], B[l & 3][l >> 2] and D[l >> 2][2 (l & 3) + {0, 1}] (the layout is
+// checked on the device by tools/dmma_check.cu and by the Ritz parity tests).
+__device__ __forceinline__ void dmma_m8n8k4(double& d0, double& d1, double a, double b) {
+  // not volatile: the loads feeding later MMAs may be scheduled ahead of this one
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
 // Deterministic CTA sum: fixed shuffle tree, then warps summed in index order.
 __device__ __forceinline__ double block_sum(double v, double* red) {
   v = warp_sum(v);

@@ -419,13 +419,8 @@ __global__ void lg_loop(LgScalars* sc, cudaGraphConditionalHandle h_while) {
 constexpr int kRitzRows = 128;
 constexpr int kRitzK = 32;
 constexpr int kRmNt = 4;                     // 8-element N tiles per warp
+constexpr int kRmU = 4;                      // k-steps per load group (16 loads in flight)
 constexpr int kRitzSpan = kWarps * 8 * kRmNt;  // elements per CTA (256)
-
-__device__ __forceinline__ void dmma_m8n8k4(double& d0, double& d1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0, %1}, {%2}, {%3}, {%0, %1};"
-               : "+d"(d0), "+d"(d1)
-               : "d"(a), "d"(b));
-}
 
 __global__ void __launch_bounds__(kThreads, 2) lg_ritz(const double* __restrict__ basis, int ld, int add_rows,
                                                        const int* __restrict__ state, const double* __restrict__ coef,
@@ -450,20 +445,28 @@ __global__ void __launch_bounds__(kThreads, 2) lg_ritz(const double* __restrict_
       cf[ks][mt][l] = (r < nr && i < ki) ? __ldg(coef + (size_t)(r0 + r) * k + i0 + i) : 0.0;
     }
     __syncthreads();
-#pragma unroll 4
-    for (int ks = 0; ks < nks; ++ks) {
-      const int r = r0 + 4 * ks + q;
-      const double* bp = basis + (size_t)r * ld + tw0 + g;
-      double b[kRmNt];
+    // kRmU k-steps per group: all kRmU kRmNt basis loads issued, then the MMAs
+    for (int ks0 = 0; ks0 < nks; ks0 += kRmU) {
+      double b[kRmU][kRmNt];
 #pragma unroll
-      for (int j = 0; j < kRmNt; ++j) b[j] = (r < rows && tw0 + 8 * j + g < n) ? __ldcs(bp + 8 * j) : 0.0;
-      double a[4];
+      for (int u = 0; u < kRmU; ++u) {
+        const int r = r0 + 4 * (ks0 + u) + q;
+        const double* bp = basis + (size_t)r * ld + tw0 + g;
 #pragma unroll
-      for (int mt = 0; mt < 4; ++mt) a[mt] = cf[ks][mt][lane];
+        for (int j = 0; j < kRmNt; ++j)
+          b[u][j] = (ks0 + u < nks && r < rows && tw0 + 8 * j + g < n) ? ldg_stream(bp + 8 * j) : 0.0;
+      }
 #pragma unroll
-      for (int mt = 0; mt < 4; ++mt)
+      for (int u = 0; u < kRmU; ++u) {
+        const int ks = ks0 + u < nks ? ks0 + u : nks - 1;  // beyond nks: zero B, any A
+        double a[4];
 #pragma unroll
-        for (int j = 0; j < kRmNt; ++j) dmma_m8n8k4(acc[mt][j][0], acc[mt][j][1], a[mt], b[j]);
+        for (int mt = 0; mt < 4; ++mt) a[mt] = cf[ks][mt][lane];
+#pragma unroll
+        for (int mt = 0; mt < 4; ++mt)
+#pragma unroll
+          for (int j = 0; j < kRmNt; ++j) dmma_m8n8k4(acc[mt][j][0], acc[mt][j][1], a[mt], b[u][j]);
+      }
     }
   }
   // D fragment: triple 8 mt + g, elements tw0 + 8 j + 2 q + {0, 1}

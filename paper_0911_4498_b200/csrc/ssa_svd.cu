@@ -254,17 +254,19 @@ size_t tgk_svd_smem_bytes(int m_max) {
 
 // Ritz assembly U_k = U_{m+1} P_k, V_k = V_m Q_k (Eq. (1)): a dense
 // contraction of the basis (rows) with the coefficient block (16 triples at a time) that
-// reads every basis element once.  Each CTA takes one series at a time from the work
-// queue; for each side and 16-triple block, each thread owns kRitzE elements of a
-// kRitzE x 256-element column window, keeps their 16 partial outputs in registers and
-// streams the rows with plain coalesced loads, kRitzU rows (kRitzE kRitzU loads) in
-// flight; the coefficient rows are read from shared memory as broadcast 16-byte loads.
-constexpr int kRitzE = 2;   // elements per thread per window
-constexpr int kRitzU = 8;   // rows per unrolled group
+// reads every basis element once, on the fp64 tensor cores (mma.sync m8n8k4 f64: M =
+// triples (two 8-row tiles), N = elements, K = basis rows).  Each CTA takes one series at
+// a time from the work queue; for each side and 16-triple block, each warp owns 8 kRzNt
+// consecutive elements of a 64 kRzNt-element window; per k-step of 4 rows a lane loads
+// kRzNt basis values (row 4 ks + (lane & 3), elements 8 j + (lane >> 2)) and reads its two
+// A fragments from the coefficient block, staged in fragment order ([k-step][tile][lane]).
+constexpr int kRzNt = 8;                    // 8-element N tiles per warp
+constexpr int kRzSpan = kWarps * 8 * kRzNt;  // elements per CTA window (512)
+constexpr int kRzU = 2;                      // k-steps per load group (16 loads in flight)
 
 size_t ritz_smem_bytes(int ldL, int ldK, int k, int m_max) {
   (void)ldL; (void)ldK; (void)k;
-  size_t s = (size_t)(m_max + 2) * 16 * 8;
+  size_t s = (size_t)((m_max + 2 + 3) / 4) * 64 * 8;
   s += (size_t)kWarps * kMaxK * (8 + 4) + kMaxK * 8;
   return align16(s) + 16;
 }
@@ -272,8 +274,8 @@ size_t ritz_smem_bytes(int ldL, int ldK, int k, int m_max) {
 __global__ void __launch_bounds__(kThreads, 2) ritz_kernel(const DecomposeArgs a) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int tid = threadIdx.x, w = tid >> 5, lane = tid & 31;
-  double* scoef = reinterpret_cast<double*>(smem_raw);                 // [(m_max+2)][16]
-  double* mxv = scoef + (size_t)(a.m_max + 2) * 16;                    // [kWarps][kMaxK]
+  double* scoef = reinterpret_cast<double*>(smem_raw);                 // [k-steps][2][32]
+  double* mxv = scoef + (size_t)((a.m_max + 2 + 3) / 4) * 64;           // [kWarps][kMaxK]
   double* sgn = mxv + kWarps * kMaxK;                                  // [kMaxK]
   int* mxi = reinterpret_cast<int*>(sgn + kMaxK);                      // [kWarps][kMaxK]
   __shared__ int sb;
@@ -298,108 +300,121 @@ __global__ void __launch_bounds__(kThreads, 2) ritz_kernel(const DecomposeArgs a
       const double* basis = isU ? a.U + (size_t)bl * (a.m_max + 1) * a.ldL : a.V + (size_t)bl * (a.m_max + 1) * a.ldK;
       const double* coef = cP + (isU ? 0 : (size_t)mstride * k);
       double* out = (isU ? a.Uout : a.Vout) + (size_t)b * k * n;
+      const int nks = (rows + 3) >> 2, g = lane >> 2, q = lane & 3;
       for (int i0 = 0; i0 < k; i0 += 16) {
         const int ki = (k - i0) < 16 ? (k - i0) : 16;
         __syncthreads();
-        for (int idx = tid; idx < rows * 16; idx += blockDim.x) {
-          const int r = idx >> 4, i = idx & 15;
-          scoef[idx] = (i < ki) ? __ldg(coef + (size_t)r * k + i0 + i) : 0.0;
+        for (int idx = tid; idx < nks * 64; idx += blockDim.x) {
+          const int ks = idx >> 6, mt = (idx >> 5) & 1, l = idx & 31;
+          const int r = 4 * ks + (l & 3), i = 8 * mt + (l >> 2);
+          scoef[idx] = (r < rows && i < ki) ? __ldg(coef + (size_t)r * k + i0 + i) : 0.0;
         }
         __syncthreads();
-        for (int c0 = 0; c0 < n; c0 += kRitzE * kThreads) {
-          double acc[kRitzE][16];
+        // U side: running argmax |u_i| of this lane's triples 8 mt + g over its elements, in
+        // increasing element order (sign canonicalization, R12)
+        double bmax[2] = {-1.0, -1.0};
+        int bidx[2] = {0x7fffffff, 0x7fffffff};
+        for (int c0 = 0; c0 < n; c0 += kRzSpan) {
+          const int tw0 = c0 + w * 8 * kRzNt;  // the warp's first element
+          if (tw0 >= n) continue;               // no barrier below: idle warps may leave
+          double acc[2][kRzNt][2];
 #pragma unroll
-          for (int e = 0; e < kRitzE; ++e)
+          for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-            for (int i = 0; i < 16; ++i) acc[e][i] = 0.0;
-          const bool whole = c0 + kRitzE * kThreads <= n;
-          int r0 = 0;
-          for (; r0 + kRitzU <= rows; r0 += kRitzU) {
-            double x[kRitzU][kRitzE];
+            for (int jn = 0; jn < kRzNt; ++jn) acc[mt][jn][0] = acc[mt][jn][1] = 0.0;
+          const double* bq = basis + (size_t)q * ld + tw0 + g;
+          // kRzU k-steps per group: all kRzU kRzNt basis loads issued, then the MMAs
+          for (int ks0 = 0; ks0 < nks; ks0 += kRzU) {
+            double bv[kRzU][kRzNt];
 #pragma unroll
-            for (int q = 0; q < kRitzU; ++q)
+            for (int u = 0; u < kRzU; ++u) {
+              const int r = 4 * (ks0 + u) + q;
+              const double* bp = bq + (size_t)(4 * (ks0 + u)) * ld;
 #pragma unroll
-              for (int e = 0; e < kRitzE; ++e) {
-                const int col = c0 + tid + e * kThreads;
-                x[q][e] = (whole || col < n) ? __ldcs(basis + (size_t)(r0 + q) * ld + col) : 0.0;
+              for (int jn = 0; jn < kRzNt; ++jn)
+                bv[u][jn] = (r < rows && tw0 + 8 * jn + g < n) ? ldg_stream(bp + 8 * jn) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < kRzU; ++u) {
+              const int ks = ks0 + u < nks ? ks0 + u : nks - 1;  // beyond nks: zero B, any A
+              const double a0 = scoef[ks * 64 + lane], a1 = scoef[ks * 64 + 32 + lane];
+#pragma unroll
+              for (int jn = 0; jn < kRzNt; ++jn) {
+                dmma_m8n8k4(acc[0][jn][0], acc[0][jn][1], a0, bv[u][jn]);
+                dmma_m8n8k4(acc[1][jn][0], acc[1][jn][1], a1, bv[u][jn]);
               }
+            }
+          }
+          if (isU) {
 #pragma unroll
-            for (int q = 0; q < kRitzU; ++q) {
-              const double2* cr = reinterpret_cast<const double2*>(scoef + (size_t)(r0 + q) * 16);
+            for (int mt = 0; mt < 2; ++mt)
 #pragma unroll
-              for (int i = 0; i < 8; ++i) {
-                const double2 c2 = cr[i];
+              for (int jn = 0; jn < kRzNt; ++jn)
 #pragma unroll
-                for (int e = 0; e < kRitzE; ++e) {
-                  acc[e][2 * i] = fma(c2.x, x[q][e], acc[e][2 * i]);
-                  acc[e][2 * i + 1] = fma(c2.y, x[q][e], acc[e][2 * i + 1]);
+                for (int c = 0; c < 2; ++c) {
+                  const int t = tw0 + 8 * jn + 2 * q + c;
+                  const double av = fabs(acc[mt][jn][c]);
+                  if (t < n && av > bmax[mt]) { bmax[mt] = av; bidx[mt] = t; }
+                }
+          }
+          // D fragment: triple i0 + 8 mt + g, elements tw0 + 8 jn + 2 q + {0, 1}
+#pragma unroll
+          for (int mt = 0; mt < 2; ++mt) {
+            const int i = 8 * mt + g;
+            if (i < ki) {
+              double* o = out + (size_t)(i0 + i) * n;
+              const double sg = isU ? 1.0 : sgn[i0 + i];  // V side: sign of u_i known
+#pragma unroll
+              for (int jn = 0; jn < kRzNt; ++jn) {
+                const int t = tw0 + 8 * jn + 2 * q;
+                const double y0 = sg * acc[mt][jn][0], y1 = sg * acc[mt][jn][1];
+                if (t + 1 < n && ((reinterpret_cast<uintptr_t>(o + t) & 15) == 0)) {
+                  *reinterpret_cast<double2*>(o + t) = make_double2(y0, y1);
+                } else {
+                  if (t < n) o[t] = y0;
+                  if (t + 1 < n) o[t + 1] = y1;
                 }
               }
             }
           }
-          for (; r0 < rows; ++r0) {
-            const double2* cr = reinterpret_cast<const double2*>(scoef + (size_t)r0 * 16);
+        }
+        if (isU) {  // the four lanes of a triple, then one entry per warp
 #pragma unroll
-            for (int e = 0; e < kRitzE; ++e) {
-              const int col = c0 + tid + e * kThreads;
-              const double x = (col < n) ? __ldcs(basis + (size_t)r0 * ld + col) : 0.0;
-#pragma unroll
-              for (int i = 0; i < 8; ++i) {
-                const double2 c2 = cr[i];
-                acc[e][2 * i] = fma(c2.x, x, acc[e][2 * i]);
-                acc[e][2 * i + 1] = fma(c2.y, x, acc[e][2 * i + 1]);
-              }
+          for (int mt = 0; mt < 2; ++mt) {
+            double v = bmax[mt];
+            int ix = bidx[mt];
+            for (int o = 1; o < 4; o <<= 1) {
+              const double v2 = __shfl_xor_sync(0xffffffffu, v, o);
+              const int i2 = __shfl_xor_sync(0xffffffffu, ix, o);
+              if (v2 > v || (v2 == v && i2 < ix)) { v = v2; ix = i2; }
             }
-          }
-#pragma unroll
-          for (int e = 0; e < kRitzE; ++e) {
-            const int col = c0 + tid + e * kThreads;
-            if (col < n) {
-#pragma unroll
-              for (int i = 0; i < 16; ++i)
-                if (i < ki) out[(size_t)(i0 + i) * n + col] = acc[e][i];
-            }
+            if (q == 0 && 8 * mt + g < ki) { mxv[w * kMaxK + i0 + 8 * mt + g] = v; mxi[w * kMaxK + i0 + 8 * mt + g] = ix; }
           }
         }
       }
-    }
-    // sign canonicalization (R12): largest-|.| entry of each u_i (lowest index
-    // on ties), found from the just-written outputs (L2-resident)
-    __syncthreads();
-    for (int i = 0; i < k; ++i) {
-      const double* uo = a.Uout + ((size_t)b * k + i) * L;
-      double v = -1.0;
-      int ix = 0;
-      for (int t = tid; t < L; t += blockDim.x) {
-        double x = fabs(uo[t]);
-        if (x > v) { v = x; ix = t; }
+      if (isU) {
+        // sign canonicalization (R12): largest-|.| entry of each u_i (lowest
+        // index on ties) from the per-warp candidates of the U contraction; the V side
+        // that follows stores v_i with the sign applied
+        __syncthreads();
+        if (tid < k) {
+          double v = -1.0;
+          int ix = 0;
+          for (int qq = 0; qq < kWarps; ++qq) {
+            double v2 = mxv[qq * kMaxK + tid];
+            int i2 = mxi[qq * kMaxK + tid];
+            if (v2 > v || (v2 == v && i2 < ix)) { v = v2; ix = i2; }
+          }
+          const double* uo = a.Uout + ((size_t)b * k + tid) * L;
+          sgn[tid] = (uo[ix] < 0.0) ? -1.0 : 1.0;
+        }
+        __syncthreads();
       }
-      for (int o = 16; o > 0; o >>= 1) {
-        double v2 = __shfl_xor_sync(0xffffffffu, v, o);
-        int i2 = __shfl_xor_sync(0xffffffffu, ix, o);
-        if (v2 > v || (v2 == v && i2 < ix)) { v = v2; ix = i2; }
-      }
-      if (lane == 0) { mxv[w * kMaxK + i] = v; mxi[w * kMaxK + i] = ix; }
     }
-    __syncthreads();
-    if (tid < k) {
-      double v = -1.0;
-      int ix = 0;
-      for (int q = 0; q < kWarps; ++q) {
-        double v2 = mxv[q * kMaxK + tid];
-        int i2 = mxi[q * kMaxK + tid];
-        if (v2 > v || (v2 == v && i2 < ix)) { v = v2; ix = i2; }
-      }
-      const double* uo = a.Uout + ((size_t)b * k + tid) * L;
-      sgn[tid] = (uo[ix] < 0.0) ? -1.0 : 1.0;
-    }
-    __syncthreads();
-    for (int i = 0; i < k; ++i) {
+    for (int i = 0; i < k; ++i) {  // flip the u_i of negative sign (L2-resident rows)
       if (sgn[i] < 0.0) {
         double* uo = a.Uout + ((size_t)b * k + i) * L;
-        double* vo = a.Vout + ((size_t)b * k + i) * K;
         for (int t = tid; t < L; t += blockDim.x) uo[t] = -uo[t];
-        for (int t = tid; t < K; t += blockDim.x) vo[t] = -vo[t];
       }
     }
   }
