@@ -157,7 +157,7 @@ def threaded_product(f, L, x, transpose, pool, nblk):
 @pytest.mark.slow
 def test_cfg3_own_plan_residuals_and_closed_form(P):
     """BASELINE configs[2] exactly as bench.py runs it (one series N = 2^20, L = 2^19, k = 32,
-    the cfg3 seed).  The oracle cannot form X (2.2 TB), so:
+    the cfg3 seed, "full reorthogonalization": reorth = 1).  The oracle cannot form X (2.2 TB), so:
     (i) true residuals |X v_i - s_i u_i|, |X^T u_i - s_i v_i| <= 10 tol s_1 = 1e-11 s_1 with
         the oracle's direct O(LK) product (row / column blocks over the host cores) for
         triples 0, 1 (the leading pair), 18 (the last signal triple: the trend) and 31;
@@ -168,7 +168,7 @@ def test_cfg3_own_plan_residuals_and_closed_form(P):
     N, L, k = c["N"], c["L"], c["k"]
     K = N - L + 1
     f = ssa_inputs.cfg3_series()
-    s, U, V, _, info, _ = decompose(P, f[None], L, k)
+    s, U, V, _, info, _ = decompose(P, f[None], L, k, reorth=1)
     inf = info[0]
     assert inf["status"] == 0 and inf["converged"] == 1, inf
     s, U, V = s[0], U[0], V[0]
