@@ -232,6 +232,13 @@ struct ColInvArgs {
   const int* gate;             // device flag: nonzero -> the launch does nothing
   int has_tail;                // long-series Lanczos (one item): the last CTA runs lg_pro_tail
   LgProTail tail;
+  // fused first CGS pass (long-series Lanczos, FRO): partial dots of this CTA's outputs with
+  // every basis row of the tail's side into dpart[row][cta]; the last CTA sums them into dh
+  // (null: the separate lg_dots kernel does it)
+  const double* dbasis;
+  int dld;
+  double* dpart;
+  double* dh;
 };
 
 template <int LOGH>
@@ -301,19 +308,23 @@ __global__ void __launch_bounds__(col_threads<LOGH>(), (LOGH >= 19) ? 1 : 3) lg_
   const int n2 = n2_0 + cc;
   if (a.mode == 0) {
     double* o = a.out + item * a.out_stride;
+    double2 yv[NE];  // this thread's outputs (kept for the fused dots)
 #pragma unroll
     for (int j = 0; j < NE; ++j) {
+      yv[j] = make_double2(0.0, 0.0);
       if (threadIdx.x + j * CT < N1 * kColW) {
         const int n1 = r0 + RS * j;
         const int t = 2 * (n2 + N2 * n1);
         if (t < a.ld_out) {
           const double y = (t < a.n_out) ? fma(-cf, pr[j].x, z[j].x * invH) : 0.0;
           o[t] = y;
+          yv[j].x = y;
           ss = fma(y, y, ss);
         }
         if (t + 1 < a.ld_out) {
           const double y = (t + 1 < a.n_out) ? fma(-cf, pr[j].y, z[j].y * invH) : 0.0;
           o[t + 1] = y;
+          yv[j].y = y;
           ss = fma(y, y, ss);
         }
       }
@@ -321,16 +332,63 @@ __global__ void __launch_bounds__(col_threads<LOGH>(), (LOGH >= 19) ? 1 : 3) lg_
     if (a.part) {
       ss = warp_sum(ss);
       if (lane == 0) red[w] = ss;
-      __syncthreads();
+      __syncthreads();  // also: every thread is done with buf (reused below)
       if (threadIdx.x == 0) {
         double s = 0.0;
         for (int i = 0; i < CT / 32; ++i) s += red[i];
         a.part[item * gridDim.x + blockIdx.x] = s;
       }
+      int nbd = 0;
+      if (a.dbasis) {
+        // fused first CGS pass: <basis row b, r> over this CTA's outputs (16-byte pairs
+        // t, t + 1 of 8 columns: 128-byte row segments), two rows' loads in flight; per-warp
+        // sums into buf [row][warp], then one fixed-order sum per row -> dpart[row][cta]
+        nbd = lg_nb(a.tail.sc, a.tail.side);
+        double* wred = reinterpret_cast<double*>(buf);
+        for (int b0 = 0; b0 < nbd; b0 += 2) {
+          double2 x[2][NE];
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const double* brow = a.dbasis + (size_t)(b0 + q) * a.dld;
+#pragma unroll
+            for (int j = 0; j < NE; ++j) {
+              const int t = 2 * (n2 + N2 * (r0 + RS * j));
+              x[q][j] = (b0 + q < nbd && threadIdx.x + j * CT < N1 * kColW && t < a.ld_out)
+                            ? __ldcs(reinterpret_cast<const double2*>(brow + t))
+                            : make_double2(0.0, 0.0);
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            double d = 0.0;
+#pragma unroll
+            for (int j = 0; j < NE; ++j) d = fma(x[q][j].x, yv[j].x, fma(x[q][j].y, yv[j].y, d));
+            d = warp_sum(d);
+            if (lane == 0 && b0 + q < nbd) wred[(b0 + q) * (CT / 32) + w] = d;
+          }
+        }
+        __syncthreads();
+        for (int row = threadIdx.x; row < nbd; row += CT) {
+          double sd = 0.0;
+          for (int i = 0; i < CT / 32; ++i) sd += wred[row * (CT / 32) + i];
+          a.dpart[(size_t)row * gridDim.x + blockIdx.x] = sd;
+        }
+      }
       if (a.has_tail) {
         __shared__ int lastf;
         if (last_cta(&a.tail.sc->done_inv, gridDim.x, &lastf)) {
           lg_pro_tail(a.part, gridDim.x, a.tail, red);
+          if (a.dbasis) {
+            // h[row] = sum over the CTAs in index order: one warp per row, lane l takes
+            // partials l, l + 32, ... in order, then the fixed shuffle tree
+            for (int row = w; row < nbd; row += CT / 32) {
+              const double* pr0 = a.dpart + (size_t)row * gridDim.x;
+              double sd = 0.0;
+              for (int i = lane; i < (int)gridDim.x; i += 32) sd += __ldcg(pr0 + i);
+              sd = warp_sum(sd);
+              if (lane == 0) a.dh[row] = sd;
+            }
+          }
           if (threadIdx.x == 0) a.tail.sc->done_inv = 0;
         }
       }
@@ -727,6 +785,15 @@ cudaError_t large_set_attributes(int N1, int N2) {
 }
 
 // ---- host-side drivers ----------------------------------------------------------------
+// Basis rows the fused first CGS pass of lg_col_inv can hold per-warp sums for (its column
+// buffer, reused after the inverse FFT): 0 if the transform's column kernel is too small.
+int large_fused_dots_rows(long long H) {
+  int logH = 0;
+  while ((1ll << logH) < H) ++logH;
+  const int l1 = logH / 2, ct = logH >= 19 ? 512 : 256;
+  return (int)((size_t)kColW * ((1 << l1) + 1) * 16 / ((size_t)(ct / 32) * 8));
+}
+
 void large_geom(const Plan& p, int* N1, int* N2) {
   const int l = ilog2(p.H);
   *N1 = 1 << (l / 2);
@@ -815,7 +882,8 @@ cudaError_t large_correlate(const Plan& p, const double2* spec, size_t spec_stri
 // CTA of the inverse column pass.
 cudaError_t large_correlate_lanczos(const Plan& p, const double2* spec, const double* r, int n_in, const LgNorm& nrm,
                                     double* out, int n_out, int ld_out, const double* prev, const double* coef,
-                                    double* part, const LgProTail& tail, cudaStream_t s) {
+                                    double* part, const LgProTail& tail, cudaStream_t s, const double* dbasis,
+                                    int dld, double* dpart, double* dh) {
   int N1, N2;
   large_geom(p, &N1, &N2);
   double2* Y = p.d_lbuf;
@@ -832,6 +900,10 @@ cudaError_t large_correlate_lanczos(const Plan& p, const double2* spec, const do
   ca.part = part;
   ca.has_tail = 1;
   ca.tail = tail;
+  ca.dbasis = dbasis;
+  ca.dld = dld;
+  ca.dpart = dpart;
+  ca.dh = dh;
   col_inv(p, Y, ca, 1, s);
   return cudaGetLastError();
 }

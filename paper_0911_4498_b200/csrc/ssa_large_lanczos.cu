@@ -51,7 +51,10 @@ namespace ssa {
 cudaError_t trace_attach_fft(unsigned long long* p);
 cudaError_t large_correlate_lanczos(const Plan& p, const double2* spec, const double* r, int n_in, const LgNorm& nrm,
                                     double* out, int n_out, int ld_out, const double* prev, const double* coef,
-                                    double* part, const LgProTail& tail, cudaStream_t s);
+                                    double* part, const LgProTail& tail, cudaStream_t s,
+                                    const double* dbasis = nullptr, int dld = 0, double* dpart = nullptr,
+                                    double* dh = nullptr);
+int large_fused_dots_rows(long long H);
 cudaError_t large_spectrum(const Plan& p, const double* series, double2* spec, int items, cudaStream_t s);
 cudaError_t launch_bidiag_svd(const Plan& p, const DecomposeArgs& a, cudaStream_t s);
 void large_geom(const Plan& p, int* N1, int* N2);
@@ -642,6 +645,10 @@ static cudaError_t build_lanczos_graph(Plan& p) {
   const size_t dots_smem = (size_t)(p.m_max + 2) * kWarps * 8, upd_smem = (size_t)(p.m_max + 2) * 8;
   const int ce = p.opt.check_every > 0 ? p.opt.check_every : 4;
   const int exp_bits = getenv("SSA_LG_EXP") ? atoi(getenv("SSA_LG_EXP")) : 0;  // graph-shape experiments
+  // fused first-pass dots (FRO / CGS2 only: PRO skips passes), when the column kernel's
+  // buffer holds the per-warp sums of every basis row (m_max + 1 rows)
+  const bool fuse_dots = (mode == 1 || mode == 2) && !getenv("SSA_LG_NOFUSE") &&
+                         p.m_max + 2 <= large_fused_dots_rows((long long)p.H);
   cudaStream_t cs[5] = {};
   cudaEvent_t ev[2] = {};
   cudaError_t e = cudaSuccess;
@@ -697,8 +704,13 @@ static cudaError_t build_lanczos_graph(Plan& p) {
       tail.has_ro = 1;
       tail.h_ro = hro;
     }
+    // FRO / CGS2 (every half-step reorthogonalizes): the first CGS pass's dots are fused
+    // into the correlation's last kernel (lg_col_inv: each CTA's outputs against every
+    // basis row, no grid-wide wait on r), so only the update kernel follows
+    const bool fuse = fuse_dots && !(exp_bits & 2);
     err = large_correlate_lanczos(p, p.d_spec, r, A ? L : K, nrm, r, n, ld, A ? p.d_vcur : p.d_ucur,
-                                  A ? &sc->bcur : &sc->acur, cpart, tail, s);
+                                  A ? &sc->bcur : &sc->acur, cpart, tail, s, fuse ? (A ? p.d_V : p.d_U) : nullptr,
+                                  ld, part, h);
     if (err != cudaSuccess) return err;
     if (exp_bits & 2) {
       err = cond_if(s, hro, s2, [&](cudaStream_t sb) -> cudaError_t {
@@ -706,6 +718,9 @@ static cudaError_t build_lanczos_graph(Plan& p) {
         return cudaGetLastError();
       });
       if (err != cudaSuccess) return err;
+    } else if (fuse) {
+      launch_pdl(lg_update, dim3(nch), dim3(kThreads), upd_smem, s, (A ? (const double*)p.d_V : (const double*)p.d_U),
+                 ld, side, (const double*)h, r, part, sc, 0, 0, mode, ab, w, hfx);
     } else {
       ro_pass(s, side, 0, 0, hfx);
     }

@@ -116,12 +116,14 @@ def test_exact_degenerate_pairs(P, k, force_long):
         assert np.linalg.norm(G[0].sum(axis=0) - f) <= 1e-10 * np.linalg.norm(f)
 
 
-def test_long_path_k32_vs_oracle(P):
+@pytest.mark.parametrize("reorth", [3, 1, 2])
+def test_long_path_k32_vs_oracle(P, reorth):
     """The long-series kernels (four-step FFT, grid-wide reorthogonalization, lg_ritz) at
-    cfg3's k = 32, forced onto N = 4096 so the full Jacobi oracle can check every triple."""
+    cfg3's k = 32, forced onto N = 4096 so the full Jacobi oracle can check every triple;
+    PRO, FRO and CGS2 (the last two run the first CGS pass's dots fused into lg_col_inv)."""
     N, L, k = 4096, 2048, 32
     f = ssa_inputs.cfg3_like_series(N)
-    s, U, V, G, info, _ = decompose(P, f[None], L, k, force_long=True)
+    s, U, V, G, info, _ = decompose(P, f[None], L, k, force_long=True, reorth=reorth)
     assert info[0]["status"] == 0, info[0]
     s_ref, U_ref, V_ref, _ = oracle.svd(f, L, k + 1)
     G_ref = np.stack([oracle.hankelize_rank1(s_ref[i], U_ref[i], V_ref[i]) for i in range(k)])
