@@ -345,6 +345,8 @@ __global__ void __launch_bounds__(col_threads<LOGH>(), (LOGH >= 19) ? 1 : 3) lg_
         // sums into buf [row][warp], then one fixed-order sum per row -> dpart[row][cta]
         nbd = lg_nb(a.tail.sc, a.tail.side);
         double* wred = reinterpret_cast<double*>(buf);
+        // streaming (evict-first) loads: measured faster here than lg_dots' evict_last
+        // (cfg3 59.9 vs 61.1 ms), although lg_update then finds fewer rows in L2
         for (int b0 = 0; b0 < nbd; b0 += 2) {
           double2 x[2][NE];
 #pragma unroll

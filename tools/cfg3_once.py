@@ -3,7 +3,7 @@ import sys, torch
 sys.path.insert(0, '.')
 import paper_0911_4498_b200 as P, ssa_inputs
 f = ssa_inputs.cfg3_series()
-plan = P.Plan(1 << 20, 1 << 19, 32, 1)
+plan = P.Plan(1 << 20, 1 << 19, 32, 1, reorth=int(sys.argv[1]) if len(sys.argv) > 1 else 1)
 x = torch.from_numpy(f[None].copy()).cuda()
 s, U, V, info = plan.decompose(x)
 torch.cuda.synchronize()
