@@ -75,7 +75,18 @@ __device__ __forceinline__ int lg_nb(const LgScalars* sc, int side) { return sid
 // fixed-order sum of n partials by one CTA (thread-strided, shuffle tree, warps in order)
 __device__ inline double cta_sum(const double* a, int n, double* red) {
   double s = 0.0;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) s += __ldcg(a + i);
+  // loads four at a time in flight, added in index order (same sum as one at a time)
+  const int step = blockDim.x;
+  int i = threadIdx.x;
+  for (; i + 3 * step < n; i += 4 * step) {
+    const double x0 = __ldcg(a + i), x1 = __ldcg(a + i + step), x2 = __ldcg(a + i + 2 * step),
+                 x3 = __ldcg(a + i + 3 * step);
+    s += x0;
+    s += x1;
+    s += x2;
+    s += x3;
+  }
+  for (; i < n; i += step) s += __ldcg(a + i);
   s = warp_sum(s);
   __syncthreads();
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
