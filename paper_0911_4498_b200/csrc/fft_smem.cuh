@@ -170,6 +170,31 @@ __device__ __forceinline__ void dft8(double2* a) {
   a[3] = cadd(e3, t3); a[7] = csub(e3, t3);
 }
 
+// dft8 with a[4..7] == 0 (the zero-padded half of a real-FFT input): the first radix-2
+// stage of each dft4 is the identity, 16 additions fewer.
+template <bool INV>
+__device__ __forceinline__ void dft8_lowhalf(double2* a) {
+  const double r = 0.70710678118654752440084436210485;  // 1/sqrt(2)
+  const double2 ea = a[0], eb = a[2], oa = a[1], ob = a[3];
+  const double2 eb_i = mul_mi<INV>(eb), ob_i = mul_mi<INV>(ob);
+  const double2 e0 = cadd(ea, eb), e1 = cadd(ea, eb_i), e2 = csub(ea, eb), e3 = csub(ea, eb_i);
+  const double2 o0 = cadd(oa, ob), o1 = cadd(oa, ob_i), o2 = csub(oa, ob), o3 = csub(oa, ob_i);
+  double2 t1, t2, t3;
+  if (!INV) {
+    t1 = make_double2(r * (o1.x + o1.y), r * (o1.y - o1.x));    // * (1 - i)/sqrt2
+    t2 = make_double2(o2.y, -o2.x);                               // * -i
+    t3 = make_double2(r * (o3.y - o3.x), -r * (o3.x + o3.y));   // * (-1 - i)/sqrt2
+  } else {
+    t1 = make_double2(r * (o1.x - o1.y), r * (o1.y + o1.x));    // * (1 + i)/sqrt2
+    t2 = make_double2(-o2.y, o2.x);                               // * i
+    t3 = make_double2(-r * (o3.x + o3.y), r * (o3.x - o3.y));   // * (-1 + i)/sqrt2
+  }
+  a[0] = cadd(e0, o0); a[4] = csub(e0, o0);
+  a[1] = cadd(e1, t1); a[5] = csub(e1, t1);
+  a[2] = cadd(e2, t2); a[6] = csub(e2, t2);
+  a[3] = cadd(e3, t3); a[7] = csub(e3, t3);
+}
+
 template <int R, bool INV>
 __device__ __forceinline__ void dftR(double2* a) {
   if constexpr (R == 8) dft8<INV>(a);
@@ -287,8 +312,11 @@ __device__ __forceinline__ void fft_run_inner_t(double2* buf, const TW& T, int t
 // n1 = base + STRIDE b (b < NB = Q / STRIDE) with inputs e = b + NB q.  Forward: the pass
 // outputs y[n1 + Q k] are stored to buf (swizzled); the rest of the transform is
 // fft_run_inner_t.
+// lowhalf: inputs q >= 4 (the upper half of the block) are zero (zero padding of a real
+// input), so the butterfly skips their additions.
 template <int LOGH, int STRIDE, class TW>
-__device__ __forceinline__ void dif_pass0_store(const double2* v, int base, double2* buf, const TW& tw) {
+__device__ __forceinline__ void dif_pass0_store(const double2* v, int base, double2* buf, const TW& tw,
+                                                bool lowhalf = false) {
   constexpr int Q = 1 << (LOGH - 3), NB = Q / STRIDE;
   static_assert(NB >= 1, "pass 0 needs 8 values per butterfly");
 #pragma unroll
@@ -297,7 +325,8 @@ __device__ __forceinline__ void dif_pass0_store(const double2* v, int base, doub
     double2 a[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) a[q] = v[b + NB * q];
-    dftR<8, false>(a);
+    if (lowhalf) dft8_lowhalf<false>(a);
+    else dftR<8, false>(a);
     double2 w[8];
     w[1] = tw.pass_w(LOGH, LOGH, n1);
     w[2] = cmul(w[1], w[1]); w[3] = cmul(w[2], w[1]);

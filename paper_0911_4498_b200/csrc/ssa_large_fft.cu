@@ -191,7 +191,9 @@ __global__ void __launch_bounds__(col_threads<LOGH>()) lg_col_fwd(ColFwdArgs arg
     // the thread holds rows r0 + 32 j of its column: the butterflies of the outermost
     // radix-8 pass, done in registers before the first shared-memory store
     __syncthreads();  // twiddle tables
-    dif_pass0_store<G::L1, RS>(v, r0, buf + cc * CS, tw1);
+    // the upper half of every column is zero padding when 2 (n2 + H/2) >= n_in (all
+    // columns for n_in <= H: the u / v / Lanczos vectors are at most half of M)
+    dif_pass0_store<G::L1, RS>(v, r0, buf + cc * CS, tw1, 2 * (n2_0 + cc) + G::H >= a.n_in);
     __syncthreads();
     fft_run_inner_t<G::L1, false>(buf + fc * CS, tw1, ct, RS, csync);
   } else {
