@@ -383,14 +383,26 @@ __global__ void __launch_bounds__(col_threads<LOGH>(), (LOGH >= 19) ? 1 : 3) lg_
         if (last_cta(&a.tail.sc->done_inv, gridDim.x, &lastf)) {
           lg_pro_tail(a.part, gridDim.x, a.tail, red);
           if (a.dbasis) {
-            // h[row] = sum over the CTAs in index order: one warp per row, lane l takes
-            // partials l, l + 32, ... in order, then the fixed shuffle tree
-            for (int row = w; row < nbd; row += CT / 32) {
-              const double* pr0 = a.dpart + (size_t)row * gridDim.x;
+            // h[row] = sum of the CTAs' partials in a fixed order: four threads per row,
+            // thread s of the four adds partials s, s + 4, ... (all loads in flight), then
+            // a fixed two-level shuffle tree; 128 rows per pass of the CTA
+            const int sub = threadIdx.x & 3;
+            for (int row0 = 0; row0 < nbd; row0 += CT / 4) {
+              const int row = row0 + (threadIdx.x >> 2);
               double sd = 0.0;
-              for (int i = lane; i < (int)gridDim.x; i += 32) sd += __ldcg(pr0 + i);
-              sd = warp_sum(sd);
-              if (lane == 0) a.dh[row] = sd;
+              if (row < nbd) {
+                const double* pr0 = a.dpart + (size_t)row * gridDim.x;
+                for (int i = sub; i < (int)gridDim.x; i += 16) {
+                  double x[4];
+#pragma unroll
+                  for (int u = 0; u < 4; ++u) x[u] = (i + 4 * u < (int)gridDim.x) ? __ldcg(pr0 + i + 4 * u) : 0.0;
+#pragma unroll
+                  for (int u = 0; u < 4; ++u) sd += x[u];
+                }
+              }
+              sd += __shfl_xor_sync(0xffffffffu, sd, 1);
+              sd += __shfl_xor_sync(0xffffffffu, sd, 2);
+              if (sub == 0 && row < nbd) a.dh[row] = sd;
             }
           }
           if (threadIdx.x == 0) a.tail.sc->done_inv = 0;
