@@ -116,7 +116,7 @@ static std::vector<double2> make_twiddles2(int64_t M) {
 
 static void free_plan(Plan& p) {
   void* ptrs[] = {p.d_tw, p.d_twl, p.d_spec, p.d_U, p.d_V, p.d_ab, p.d_state, p.d_tgk, p.d_rot, p.d_vecs, p.d_coef,
-                  p.d_info, p.d_counters, p.d_hscratch, p.d_prof, p.d_tgkw, p.d_tw1, p.d_tw2, p.d_tw4, p.d_twp, p.d_lbuf,
+                  p.d_info, p.d_counters, p.d_hscratch, p.d_prof, p.d_tgkw, p.d_tw1, p.d_tw2, p.d_tw4, p.d_twp, p.d_rcpc, p.d_lbuf,
                   p.d_lgsc, p.d_lgpart, p.d_lgh, p.d_lgr, p.d_series, p.d_sigma, p.d_Uout, p.d_Vout,
                   p.d_recon, p.d_elem, p.d_bs, p.d_lgom, p.d_ucur, p.d_vcur};
   if (p.lg_exec) cudaGraphExecDestroy(p.lg_exec);
@@ -380,6 +380,17 @@ extern "C" ssa_status ssa_plan_create(int64_t N, int64_t L, int32_t k, int64_t b
     }
     if (e == cudaSuccess) e = ssa::large_set_attributes(N1, N2);
     if (e != cudaSuccess) { st = cuda_fail(e, "large FFT setup"); goto bad; }
+    {
+      // 1/c_t of the Hankelization weights: every count is in [1, min(L, K)]
+      const int64_t mn = std::min<int64_t>(L, N - L + 1);
+      std::vector<double> rc((size_t)mn);
+      for (int64_t c = 1; c <= mn; ++c) rc[(size_t)c - 1] = 1.0 / (double)c;
+      if ((st = alloc((void**)&p.d_rcpc, rc.size() * 8, "hankelization weights")) != SSA_OK) goto bad;
+      if ((e = cudaMemcpy(p.d_rcpc, rc.data(), rc.size() * 8, cudaMemcpyHostToDevice))) {
+        st = cuda_fail(e, "large FFT setup");
+        goto bad;
+      }
+    }
     // work buffers: ~512 MB, at least 2 items (hankelization needs a pair)
     p.lbuf_items = (int)std::max<int64_t>(2, std::min<int64_t>(256, ((int64_t)512 << 20) / (H * 16)));
     if ((st = alloc((void**)&p.d_lbuf, (size_t)p.lbuf_items * H * 16, "large FFT buffers")) != SSA_OK) goto bad;

@@ -81,6 +81,7 @@ struct Plan {
   double2* d_tw2 = nullptr;      // two-level table for the N2-point sub-FFTs (M = 2 N2)
   double2* d_tw4 = nullptr;      // four-step twiddles: two-level W_H table (large_twh_entries)
   double2* d_twp = nullptr;      // pair-step row factors W_M^A, A <= N1/2
+  double* d_rcpc = nullptr;      // 1/c for the antidiagonal counts c = 1..min(L, K) (hankelization)
   int hank_per = 64;             // terms per four-step hankelization batch
   cudaStream_t lg_aux = nullptr; // second stream: alternate hankelization batches overlap
   cudaEvent_t lg_ev[2] = {};     // fork / join events of lg_aux

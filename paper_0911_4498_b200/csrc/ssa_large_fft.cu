@@ -25,6 +25,7 @@
 #include <algorithm>
 
 #include "device_common.cuh"
+#include "fft_reg.cuh"
 #include "lg_scalars.cuh"
 
 namespace ssa {
@@ -100,16 +101,6 @@ __device__ __forceinline__ void twiddle_seq(const double2* __restrict__ th, long
       }
     }
   }
-}
-
-// 1/c for an integer count c >= 1, to within an ulp: float reciprocal, two Newton steps
-// in fp64 (no fp64 division and its slow-path branch in the hot epilogue).
-__device__ __forceinline__ double rcp_count(int c) {
-  const double cd = (double)c;
-  double r = (double)__frcp_rn((float)c);
-  r = fma(r, fma(-cd, r, 1.0), r);
-  r = fma(r, fma(-cd, r, 1.0), r);
-  return r;
 }
 
 // ---- pass 1: forward column FFTs on packed real input x (len n_in) -------------------
@@ -231,6 +222,7 @@ struct ColInvArgs {
   double* part;                // correlation: partial sums of squares [items][gridDim.x]
   const double* sigma;         // hankelization: per-item sigma
   int N, L, K;                 // hankelization: weights
+  const double* rcpc;          // hankelization: 1/c for c = 1..min(L, K) (plan table)
   const int* gate;             // device flag: nonzero -> the launch does nothing
   int has_tail;                // long-series Lanczos (one item): the last CTA runs lg_pro_tail
   LgProTail tail;
@@ -420,12 +412,127 @@ __global__ void __launch_bounds__(col_threads<LOGH>(), (LOGH >= 19) ? 1 : 3) lg_
         const int t = 2 * (n2 + N2 * n1);
         if (t < a.N) {
           const int c0 = min(min(t + 1, mn), a.N - t);
-          o[t] = z[j].x * scale * rcp_count(c0);
+          o[t] = z[j].x * scale * __ldg(a.rcpc + c0 - 1);
           if (t + 1 < a.N) {
             const int c1 = min(min(t + 2, mn), a.N - t - 1);
-            o[t + 1] = z[j].y * scale * rcp_count(c1);
+            o[t + 1] = z[j].y * scale * __ldg(a.rcpc + c1 - 1);
           }
         }
+      }
+    }
+  }
+}
+
+// ---- register radix-16 x 16 column passes for N1 = 256 (H = 2^16, 2^17: cfg5) --------
+// The hankelization's column FFTs with one shared-memory exchange instead of three radix-8 /
+// radix-4 passes (the column kernels above are bound by shared-memory wavefronts): a
+// 256-point column is 16 x 16; thread (c, q) of the CTA's 16 columns first holds rows
+// q + 16 j of column c (a 16-point DFT in registers, dft16, then the internal twiddles
+// W_256^{q k}), one transposing exchange through shared memory, then frequencies / rows
+// q + 16 j (the second 16-point DFT).  Same layouts and results as lg_col_fwd / lg_col_inv
+// (mode 1): Y[n2 + N2 k1] natural order, the DFT split of PAPER.md:473-509.
+constexpr int kColW16 = 16;   // columns per CTA
+constexpr int kCS16 = 257;    // column stride in shared memory (16-byte units, odd)
+static size_t col16_smem() { return ((size_t)kColW16 * kCS16 + tw2_entries(512)) * 16; }
+
+template <int LOGH>
+__global__ void __launch_bounds__(kThreads, 2) lg_col16_fwd(ColFwdArgs args, const double2* __restrict__ T1,
+                                                            const double2* __restrict__ TWH) {
+  using G = Geo<LOGH>;
+  static_assert(G::N1 == 256, "radix-16 x 16 columns");
+  constexpr int N2 = G::N2;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double2* buf = reinterpret_cast<double2*>(smem_raw);
+  const TwSmem tw1 = load_tw2(T1, buf + kColW16 * kCS16, 512);  // W_512^t
+  pdl_wait(1);
+  if (args.gate && *args.gate) return;
+  const ColFwdIn a = blockIdx.z ? args.in[1] : args.in[0];
+  const int c = threadIdx.x & 15, q = threadIdx.x >> 4;
+  const int n2 = blockIdx.x * kColW16 + c;
+  const double* xi = a.x + (size_t)blockIdx.y * a.xs;
+  double2* Yi = a.Y + (size_t)blockIdx.y * G::H;
+  const bool rvec = a.vec && ((reinterpret_cast<uintptr_t>(xi) & 15) == 0);
+  // rows n1 = q + 16 j >= 128 (j >= 8) are zero padding when 2 (n2 + H/2) >= n_in
+  const bool half = 2 * n2 + G::H >= a.n_in;
+  double2 v[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const int i0 = 2 * (n2 + N2 * (q + 16 * j));
+    if (j >= 8 && half) {
+      v[j] = make_double2(0.0, 0.0);
+    } else if (rvec && i0 + 1 < a.n_in) {
+      v[j] = __ldg(reinterpret_cast<const double2*>(xi + i0));
+    } else {
+      v[j].x = (i0 < a.n_in) ? __ldg(xi + i0) : 0.0;
+      v[j].y = (i0 + 1 < a.n_in) ? __ldg(xi + i0 + 1) : 0.0;
+    }
+  }
+  __syncthreads();  // twiddle table
+  if (half) dft16<false, true>(v);
+  else dft16<false, false>(v);
+  twiddle16<false>(v, tw1(2 * q));  // v[k] *= W_256^{q k}
+  double2* col = buf + c * kCS16;
+#pragma unroll
+  for (int k = 0; k < 16; ++k) col[q * 16 + k] = v[k];
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = col[i * 16 + q];
+  dft16<false, false>(v);  // v[j] = column spectrum at k1 = q + 16 j
+  twiddle_seq<LOGH, 16>(TWH, (long long)n2 * q, (long long)n2 * 16, 16, [&](int j, double2 w) {
+    Yi[(size_t)n2 + (size_t)N2 * (q + 16 * j)] = cmul(v[j], w);
+  });
+}
+
+// Inverse columns + hankelization epilogue (lg_col_inv mode 1): g_t = sigma y_t / c_t.
+template <int LOGH>
+__global__ void __launch_bounds__(kThreads, 2) lg_col16_hank(const double2* __restrict__ Y,
+                                                             const double2* __restrict__ T1, ColInvArgs a) {
+  using G = Geo<LOGH>;
+  static_assert(G::N1 == 256, "radix-16 x 16 columns");
+  constexpr int N2 = G::N2;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double2* buf = reinterpret_cast<double2*>(smem_raw);
+  const TwSmem tw1 = load_tw2(T1, buf + kColW16 * kCS16, 512);
+  pdl_wait(4);
+  if (a.gate && *a.gate) return;
+  const size_t item = blockIdx.y;
+  const double2* Yi = Y + item * G::H;
+  const int c = threadIdx.x & 15, q = threadIdx.x >> 4;
+  const int n2 = blockIdx.x * kColW16 + c;
+  double2 v[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) v[j] = Yi[(size_t)n2 + (size_t)N2 * (q + 16 * j)];  // k1 = q + 16 j
+  __syncthreads();  // twiddle table
+  dft16<true, false>(v);
+  twiddle16<true>(v, tw1(2 * q));  // v[n] *= W_256^{-q n}
+  double2* col = buf + c * kCS16;
+#pragma unroll
+  for (int n = 0; n < 16; ++n) col[q * 16 + n] = v[n];
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = col[i * 16 + q];
+  dft16<true, false>(v);  // v[j] = H x packed point n2 + N2 (q + 16 j)
+  const double scale = a.sigma[item] * (1.0 / (double)G::H);
+  const int mn = a.L < a.K ? a.L : a.K;
+  double* o = a.out + item * a.out_stride;
+  const bool ovec = (reinterpret_cast<uintptr_t>(o) & 15) == 0;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const int t = 2 * (n2 + N2 * (q + 16 * j));
+    if (t < a.N) {
+      const int c0 = min(min(t + 1, mn), a.N - t);
+      const double g0 = v[j].x * scale * __ldg(a.rcpc + c0 - 1);
+      if (t + 1 < a.N) {
+        const int c1 = min(min(t + 2, mn), a.N - t - 1);
+        const double g1 = v[j].y * scale * __ldg(a.rcpc + c1 - 1);
+        if (ovec) {
+          *reinterpret_cast<double2*>(o + t) = make_double2(g0, g1);
+        } else {
+          o[t] = g0;
+          o[t + 1] = g1;
+        }
+      } else {
+        o[t] = g0;
       }
     }
   }
@@ -797,6 +904,12 @@ cudaError_t large_set_attributes(int N1, int N2) {
   } while (0)
   SSA_LG_DISPATCH(logH, SSA_LG_ATTR)
 #undef SSA_LG_ATTR
+  if (logH == 16 || logH == 17) {
+    if ((e = raise_smem_limit(lg_col16_fwd<16>, col16_smem()))) return e;
+    if ((e = raise_smem_limit(lg_col16_hank<16>, col16_smem()))) return e;
+    if ((e = raise_smem_limit(lg_col16_fwd<17>, col16_smem()))) return e;
+    if ((e = raise_smem_limit(lg_col16_hank<17>, col16_smem()))) return e;
+  }
   return e;
 }
 
@@ -953,14 +1066,28 @@ cudaError_t large_hankelize(Plan& p, const double* sigma, const double* U, const
     ColFwdArgs cf{};
     cf.in[0] = ColFwdIn{U + t0 * p.L, (size_t)p.L, (int)p.L, Ya, vec16(U, p.L)};
     cf.in[1] = ColFwdIn{V + t0 * p.K, (size_t)p.K, (int)p.K, Yb, vec16(V, p.K)};
-    col_fwd(p, cf, 2, ni, st);
+    const int logH = ilog2(p.H);
+    const bool r16 = (logH == 16 || logH == 17) && !getenv("SSA_HANK_R8");
+    if (r16) {
+      const dim3 grid((unsigned)(p.H >> 8) / kColW16, ni, 2);
+      if (logH == 16) launch_pdl(lg_col16_fwd<16>, grid, dim3(kThreads), col16_smem(), st, cf, p.d_tw1, p.d_tw4);
+      else launch_pdl(lg_col16_fwd<17>, grid, dim3(kThreads), col16_smem(), st, cf, p.d_tw1, p.d_tw4);
+    } else {
+      col_fwd(p, cf, 2, ni, st);
+    }
     RowArgs ra{2, Ya, Yb, nullptr, 0, nullptr, nullptr};
     rows(p, ra, ni, true, st);
     ColInvArgs ca{};
     ca.mode = 1;
     ca.out_stride = (size_t)p.N; ca.out = out + t0 * p.N;
-    ca.sigma = sigma + t0; ca.N = (int)p.N; ca.L = (int)p.L; ca.K = (int)p.K;
-    col_inv(p, Yb, ca, ni, st);
+    ca.sigma = sigma + t0; ca.N = (int)p.N; ca.L = (int)p.L; ca.K = (int)p.K; ca.rcpc = p.d_rcpc;
+    if (r16) {
+      const dim3 grid((unsigned)(p.H >> 8) / kColW16, ni);
+      if (logH == 16) launch_pdl(lg_col16_hank<16>, grid, dim3(kThreads), col16_smem(), st, (const double2*)Yb, p.d_tw1, ca);
+      else launch_pdl(lg_col16_hank<17>, grid, dim3(kThreads), col16_smem(), st, (const double2*)Yb, p.d_tw1, ca);
+    } else {
+      col_inv(p, Yb, ca, ni, st);
+    }
   }
   if (two) {
     if ((err = cudaEventRecord(p.lg_ev[1], p.lg_aux))) return err;

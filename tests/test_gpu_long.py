@@ -105,6 +105,23 @@ def test_cfg5_shape_sampled_terms(P):
         assert nrel(g[0, i], ref) <= 1e-10
 
 
+@pytest.mark.parametrize("N,L", [(100003, 37001), (100003, 70001), (131072, 65536), (150001, 100000)])
+def test_long_hankelize_radix16_columns(P, N, L):
+    """H = 2^16 and 2^17 (N1 = 256): the register radix-16 x 16 column kernels
+    (lg_col16_fwd / lg_col16_hank).  Ragged N (odd item stride: the scalar store path),
+    L < K and L > K (inputs longer than H / 2 packed points: the non-padded columns), the
+    H = 2^17 with L > K; two terms per problem, three problems, every term against
+    the oracle's direct averaging (Alg. 4)."""
+    K = N - L + 1
+    B, T = 3, 2
+    rng = np.random.default_rng(N + L)
+    s = rng.uniform(0.5, 2, (B, T)); U = rng.standard_normal((B, T, L)); V = rng.standard_normal((B, T, K))
+    plan = P.Plan(N, L, 0, B)
+    g = plan.hankelize(cuda(s), cuda(U), cuda(V)).cpu().numpy()
+    for b, i in ((0, 0), (1, 1), (2, 1)):
+        assert nrel(g[b, i], oracle.hankelize_rank1(s[b, i], U[b, i], V[b, i])) <= 1e-12
+
+
 @pytest.mark.parametrize("N,L,k", [(1024, 512, 10), (600, 250, 8), (4096, 2048, 16), (700, 520, 6)])
 def test_long_decompose_vs_oracle(P, N, L, k):
     """The long-series Lanczos path forced onto sizes the Jacobi oracle can do."""
