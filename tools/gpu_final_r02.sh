@@ -21,6 +21,11 @@ timeout 900 /usr/local/cuda/bin/ncu --set full --clock-control none --import-sou
 python tools/ncu_summary.py /tmp/prof_micro.ncu-rep $O/ncu_r02_micro_summary.json --batch 1 \
   --note "tools/micro_once.py cfg4m cfg5 cfg3mv: matvec4096_kernel (ssa_matvec_multi, 2048 series x 32 vectors), cfg5 four-step kernels (64-term batch), cfg3-size four-step correlation (one item); ncu --set full --clock-control none" > /dev/null 2>&1
 python tools/ncu_stalls.py /tmp/prof_micro.ncu-rep > $O/ncu_r02_micro_stalls.txt 2>&1
+timeout 600 /usr/local/cuda/bin/ncu --set full --clock-control none --import-source on -k regex:"lg_col16|lg_row_warp" -c 6 \
+  -o /tmp/prof_cfg5 python tools/micro_once.py cfg5 > $O/ncu_cfg5.log 2>&1
+python tools/ncu_summary.py /tmp/prof_cfg5.ncu-rep $O/ncu_r02_cfg5_summary.json --batch 1 \
+  --note "tools/micro_once.py cfg5: the four-step Hankelization kernels of one 64-term batch at N = 2^18 (lg_col16_fwd: u and v columns, lg_row_warp: row pairs + product, lg_col16_hank: inverse columns + sigma/c epilogue); ncu --set full --clock-control none" > /dev/null 2>&1
+python tools/ncu_stalls.py /tmp/prof_cfg5.ncu-rep > $O/ncu_r02_cfg5_stalls.txt 2>&1
 timeout 600 /usr/local/cuda/bin/ncu --set full --clock-control none -k regex:"lg_ritz" -c 2 -o /tmp/prof_lgritz python tools/cfg3_once.py > $O/ncu_lgritz.log 2>&1
 python tools/ncu_stalls.py /tmp/prof_lgritz.ncu-rep > $O/ncu_r02_lgritz_stalls.txt 2>&1
 SSA_TRACE=1 timeout 300 python tools/cfg3_once.py > $O/cfg3_trace.log 2>&1
