@@ -461,10 +461,10 @@ __global__ void __launch_bounds__(kThreads, 2) lg_col16_fwd(ColFwdArgs args, con
     if (j >= 8 && half) {
       v[j] = make_double2(0.0, 0.0);
     } else if (rvec && i0 + 1 < a.n_in) {
-      v[j] = __ldg(reinterpret_cast<const double2*>(xi + i0));
+      v[j] = __ldcs(reinterpret_cast<const double2*>(xi + i0));
     } else {
-      v[j].x = (i0 < a.n_in) ? __ldg(xi + i0) : 0.0;
-      v[j].y = (i0 + 1 < a.n_in) ? __ldg(xi + i0 + 1) : 0.0;
+      v[j].x = (i0 < a.n_in) ? __ldcs(xi + i0) : 0.0;
+      v[j].y = (i0 + 1 < a.n_in) ? __ldcs(xi + i0 + 1) : 0.0;
     }
   }
   __syncthreads();  // twiddle table
@@ -501,7 +501,7 @@ __global__ void __launch_bounds__(kThreads, 2) lg_col16_hank(const double2* __re
   const int n2 = blockIdx.x * kColW16 + c;
   double2 v[16];
 #pragma unroll
-  for (int j = 0; j < 16; ++j) v[j] = Yi[(size_t)n2 + (size_t)N2 * (q + 16 * j)];  // k1 = q + 16 j
+  for (int j = 0; j < 16; ++j) v[j] = __ldcs(Yi + (size_t)n2 + (size_t)N2 * (q + 16 * j));  // k1 = q + 16 j
   __syncthreads();  // twiddle table
   dft16<true, false>(v);
   twiddle16<true>(v, tw1(2 * q));  // v[n] *= W_256^{-q n}
@@ -526,13 +526,13 @@ __global__ void __launch_bounds__(kThreads, 2) lg_col16_hank(const double2* __re
         const int c1 = min(min(t + 2, mn), a.N - t - 1);
         const double g1 = v[j].y * scale * __ldg(a.rcpc + c1 - 1);
         if (ovec) {
-          *reinterpret_cast<double2*>(o + t) = make_double2(g0, g1);
+          __stcs(reinterpret_cast<double2*>(o + t), make_double2(g0, g1));
         } else {
-          o[t] = g0;
-          o[t + 1] = g1;
+          __stcs(o + t, g0);
+          __stcs(o + t + 1, g1);
         }
       } else {
-        o[t] = g0;
+        __stcs(o + t, g0);
       }
     }
   }
@@ -793,10 +793,11 @@ __global__ void __launch_bounds__(kThreads) lg_row_warp(const double2* __restric
   double2 v[NE];
   if (mine) {
     const double2* src = ((j >> 1) ? Yb : Ya) + (size_t)((j & 1) ? B : A) * N2;
+    const bool dead = (a.mode == 2) && !(j >> 1);  // product mode: Ya is not read again
 #pragma unroll
     for (int e = 0; e < NE; ++e) {
       const int i = lane + 32 * e;
-      if (i < N2) v[e] = src[i];
+      if (i < N2) v[e] = dead ? __ldcs(src + i) : src[i];
     }
   }
   __syncthreads();  // tables
@@ -1044,6 +1045,9 @@ cudaError_t large_hankelize(Plan& p, const double* sigma, const double* U, const
   // the next batch's work.  SSA_HANK_PER overrides the batch size (tuning).
   const int cap = std::max(1, p.lbuf_items / 4);
   int per = std::max(1, std::min(cap, p.hank_per));
+  // H <= 2^17: keep the two buffers of the batches in flight on both streams (2 x per x 32 H
+  // bytes) near half of the 126 MB L2 (cfg5: 16 terms per batch measured best, 8-16 within 1 %)
+  if (p.H <= (1 << 17)) per = std::max(1, std::min(per, std::max(8, (int)((64u << 20) / (32u * (unsigned)p.H)))));
   if (const char* e = getenv("SSA_HANK_PER")) per = std::max(1, std::min(cap, atoi(e)));
   const bool two = nterm_total > (size_t)per && p.lbuf_items >= 4;
   cudaError_t err;
