@@ -426,29 +426,29 @@ __global__ void __launch_bounds__(col_threads<LOGH>(), (LOGH >= 19) ? 1 : 3) lg_
 // ---- register radix-16 x 16 column passes for N1 = 256 (H = 2^16, 2^17: cfg5) --------
 // The hankelization's column FFTs with one shared-memory exchange instead of three radix-8 /
 // radix-4 passes (the column kernels above are bound by shared-memory wavefronts): a
-// 256-point column is 16 x 16; thread (c, q) of the CTA's 16 columns first holds rows
+// 256-point column is 16 x 16; thread (c, q) of the CTA's CW columns first holds rows
 // q + 16 j of column c (a 16-point DFT in registers, dft16, then the internal twiddles
 // W_256^{q k}), one transposing exchange through shared memory, then frequencies / rows
 // q + 16 j (the second 16-point DFT).  Same layouts and results as lg_col_fwd / lg_col_inv
 // (mode 1): Y[n2 + N2 k1] natural order, the DFT split of PAPER.md:473-509.
-constexpr int kColW16 = 16;   // columns per CTA
+// CW columns per CTA (16 x CW threads): 16 (256 threads, 2 CTAs/SM) or 8 (128 threads, 4 CTAs/SM)
 constexpr int kCS16 = 257;    // column stride in shared memory (16-byte units, odd)
-static size_t col16_smem() { return ((size_t)kColW16 * kCS16 + tw2_entries(512)) * 16; }
+static size_t col16_smem(int cw) { return ((size_t)cw * kCS16 + tw2_entries(512)) * 16; }
 
-template <int LOGH>
-__global__ void __launch_bounds__(kThreads, 2) lg_col16_fwd(ColFwdArgs args, const double2* __restrict__ T1,
+template <int LOGH, int CW>
+__global__ void __launch_bounds__(16 * CW, 512 / (16 * CW)) lg_col16_fwd(ColFwdArgs args, const double2* __restrict__ T1,
                                                             const double2* __restrict__ TWH) {
   using G = Geo<LOGH>;
   static_assert(G::N1 == 256, "radix-16 x 16 columns");
   constexpr int N2 = G::N2;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double2* buf = reinterpret_cast<double2*>(smem_raw);
-  const TwSmem tw1 = load_tw2(T1, buf + kColW16 * kCS16, 512);  // W_512^t
+  const TwSmem tw1 = load_tw2(T1, buf + CW * kCS16, 512);  // W_512^t
   pdl_wait(1);
   if (args.gate && *args.gate) return;
   const ColFwdIn a = blockIdx.z ? args.in[1] : args.in[0];
-  const int c = threadIdx.x & 15, q = threadIdx.x >> 4;
-  const int n2 = blockIdx.x * kColW16 + c;
+  const int c = threadIdx.x & (CW - 1), q = threadIdx.x / CW;
+  const int n2 = blockIdx.x * CW + c;
   const double* xi = a.x + (size_t)blockIdx.y * a.xs;
   double2* Yi = a.Y + (size_t)blockIdx.y * G::H;
   const bool rvec = a.vec && ((reinterpret_cast<uintptr_t>(xi) & 15) == 0);
@@ -484,21 +484,21 @@ __global__ void __launch_bounds__(kThreads, 2) lg_col16_fwd(ColFwdArgs args, con
 }
 
 // Inverse columns + hankelization epilogue (lg_col_inv mode 1): g_t = sigma y_t / c_t.
-template <int LOGH>
-__global__ void __launch_bounds__(kThreads, 2) lg_col16_hank(const double2* __restrict__ Y,
+template <int LOGH, int CW>
+__global__ void __launch_bounds__(16 * CW, 512 / (16 * CW)) lg_col16_hank(const double2* __restrict__ Y,
                                                              const double2* __restrict__ T1, ColInvArgs a) {
   using G = Geo<LOGH>;
   static_assert(G::N1 == 256, "radix-16 x 16 columns");
   constexpr int N2 = G::N2;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double2* buf = reinterpret_cast<double2*>(smem_raw);
-  const TwSmem tw1 = load_tw2(T1, buf + kColW16 * kCS16, 512);
+  const TwSmem tw1 = load_tw2(T1, buf + CW * kCS16, 512);
   pdl_wait(4);
   if (a.gate && *a.gate) return;
   const size_t item = blockIdx.y;
   const double2* Yi = Y + item * G::H;
-  const int c = threadIdx.x & 15, q = threadIdx.x >> 4;
-  const int n2 = blockIdx.x * kColW16 + c;
+  const int c = threadIdx.x & (CW - 1), q = threadIdx.x / CW;
+  const int n2 = blockIdx.x * CW + c;
   double2 v[16];
 #pragma unroll
   for (int j = 0; j < 16; ++j) v[j] = __ldcs(Yi + (size_t)n2 + (size_t)N2 * (q + 16 * j));  // k1 = q + 16 j
@@ -906,10 +906,14 @@ cudaError_t large_set_attributes(int N1, int N2) {
   SSA_LG_DISPATCH(logH, SSA_LG_ATTR)
 #undef SSA_LG_ATTR
   if (logH == 16 || logH == 17) {
-    if ((e = raise_smem_limit(lg_col16_fwd<16>, col16_smem()))) return e;
-    if ((e = raise_smem_limit(lg_col16_hank<16>, col16_smem()))) return e;
-    if ((e = raise_smem_limit(lg_col16_fwd<17>, col16_smem()))) return e;
-    if ((e = raise_smem_limit(lg_col16_hank<17>, col16_smem()))) return e;
+    if ((e = raise_smem_limit(lg_col16_fwd<16, 16>, col16_smem(16)))) return e;
+    if ((e = raise_smem_limit(lg_col16_hank<16, 16>, col16_smem(16)))) return e;
+    if ((e = raise_smem_limit(lg_col16_fwd<17, 16>, col16_smem(16)))) return e;
+    if ((e = raise_smem_limit(lg_col16_hank<17, 16>, col16_smem(16)))) return e;
+    if ((e = raise_smem_limit(lg_col16_fwd<16, 8>, col16_smem(8)))) return e;
+    if ((e = raise_smem_limit(lg_col16_hank<16, 8>, col16_smem(8)))) return e;
+    if ((e = raise_smem_limit(lg_col16_fwd<17, 8>, col16_smem(8)))) return e;
+    if ((e = raise_smem_limit(lg_col16_hank<17, 8>, col16_smem(8)))) return e;
   }
   return e;
 }
@@ -1072,10 +1076,15 @@ cudaError_t large_hankelize(Plan& p, const double* sigma, const double* U, const
     cf.in[1] = ColFwdIn{V + t0 * p.K, (size_t)p.K, (int)p.K, Yb, vec16(V, p.K)};
     const int logH = ilog2(p.H);
     const bool r16 = (logH == 16 || logH == 17) && !getenv("SSA_HANK_R8");
+    const bool cw8 = getenv("SSA_COL16_CW16") == nullptr;  // 8 columns per CTA (128 threads, 4 CTAs/SM) measured 0.7 % faster than 16
     if (r16) {
-      const dim3 grid((unsigned)(p.H >> 8) / kColW16, ni, 2);
-      if (logH == 16) launch_pdl(lg_col16_fwd<16>, grid, dim3(kThreads), col16_smem(), st, cf, p.d_tw1, p.d_tw4);
-      else launch_pdl(lg_col16_fwd<17>, grid, dim3(kThreads), col16_smem(), st, cf, p.d_tw1, p.d_tw4);
+      const int cw = cw8 ? 8 : 16;
+      const dim3 grid((unsigned)(p.H >> 8) / cw, ni, 2);
+      const dim3 blk(16 * cw);
+      if (logH == 16 && !cw8) launch_pdl(lg_col16_fwd<16, 16>, grid, blk, col16_smem(16), st, cf, p.d_tw1, p.d_tw4);
+      else if (logH == 16) launch_pdl(lg_col16_fwd<16, 8>, grid, blk, col16_smem(8), st, cf, p.d_tw1, p.d_tw4);
+      else if (!cw8) launch_pdl(lg_col16_fwd<17, 16>, grid, blk, col16_smem(16), st, cf, p.d_tw1, p.d_tw4);
+      else launch_pdl(lg_col16_fwd<17, 8>, grid, blk, col16_smem(8), st, cf, p.d_tw1, p.d_tw4);
     } else {
       col_fwd(p, cf, 2, ni, st);
     }
@@ -1086,9 +1095,13 @@ cudaError_t large_hankelize(Plan& p, const double* sigma, const double* U, const
     ca.out_stride = (size_t)p.N; ca.out = out + t0 * p.N;
     ca.sigma = sigma + t0; ca.N = (int)p.N; ca.L = (int)p.L; ca.K = (int)p.K; ca.rcpc = p.d_rcpc;
     if (r16) {
-      const dim3 grid((unsigned)(p.H >> 8) / kColW16, ni);
-      if (logH == 16) launch_pdl(lg_col16_hank<16>, grid, dim3(kThreads), col16_smem(), st, (const double2*)Yb, p.d_tw1, ca);
-      else launch_pdl(lg_col16_hank<17>, grid, dim3(kThreads), col16_smem(), st, (const double2*)Yb, p.d_tw1, ca);
+      const int cw = cw8 ? 8 : 16;
+      const dim3 grid((unsigned)(p.H >> 8) / cw, ni);
+      const dim3 blk(16 * cw);
+      if (logH == 16 && !cw8) launch_pdl(lg_col16_hank<16, 16>, grid, blk, col16_smem(16), st, (const double2*)Yb, p.d_tw1, ca);
+      else if (logH == 16) launch_pdl(lg_col16_hank<16, 8>, grid, blk, col16_smem(8), st, (const double2*)Yb, p.d_tw1, ca);
+      else if (!cw8) launch_pdl(lg_col16_hank<17, 16>, grid, blk, col16_smem(16), st, (const double2*)Yb, p.d_tw1, ca);
+      else launch_pdl(lg_col16_hank<17, 8>, grid, blk, col16_smem(8), st, (const double2*)Yb, p.d_tw1, ca);
     } else {
       col_inv(p, Yb, ca, ni, st);
     }
